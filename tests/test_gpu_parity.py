@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle (-m gpu).
+
+Tolerance (BASELINE.json north_star, R21): per-column max-norm
+relative error <= 1e-9 on Hessian entries (primary); entrywise <= 1e-9 for
+entries >= 1e-4 * max|H| (secondary: both sides carry absolute rounding
+errors ~1e-14 * cond * max|H|, which swamp smaller entries).  Intermediates (g, J-based quantities, Z, Y_x, Psi) use
+1e-11 relative to the block's max.  Integer outputs (orderings, sizes) are
+compared exactly.
+"""
+import numpy as np
+import pytest
+
+import gridgen
+from oracle import powerflow as pf
+from oracle import reduction as red
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+rh = pytest.importorskip("paper_2201_00241_b200")
+
+TOL_H = 1e-9
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def col_rel_err(A, B):
+    den = np.maximum(np.max(np.abs(B), axis=0), 1e-300)
+    return float(np.max(np.max(np.abs(A - B), axis=0) / den))
+
+
+def entry_rel_err(A, B, floor=1e-4):
+    m = np.abs(B) >= floor * np.max(np.abs(B))
+    return float(np.max(np.abs(A - B)[m] / np.abs(B)[m]))
+
+
+def setup(grid):
+    ctx = rh.RedHess(0)
+    ctx.load_grid(grid)
+    x, p = ctx.state_vectors(grid)
+    xd, pd = _dev(x), _dev(p)
+    ctx.set_state(xd, pd)
+    return ctx, x, p
+
+
+CASES = [("case9", dict(tap_line=True)), ("case118", dict(tap_line=True)), ("case1354pegase", {}),
+         ("case2869pegase", {})]
+
+
+@pytest.fixture(scope="module", params=CASES, ids=[c[0] for c in CASES])
+def solved_case(request):
+    name, kw = request.param
+    g = pf.backout_loads(gridgen.make_grid(name, **kw))
+    L = pf.Layout(g)
+    x, p = pf.state_vectors(g, L)
+    grad, lam = red.reduced_gradient(g, x, p, L)
+    ops = red.operators(g, x, p, lam, L)
+    return name, g, L, x, p, grad, lam, ops
+
+
+def test_residual_objective(solved_case):
+    name, g, L, x, p, *_ = solved_case
+    g2 = gridgen.make_grid(name)        # unsolved point: g != 0
+    ctx, x2, p2 = setup(g2)
+    gd, fd = ctx.residual()
+    want = pf.residual(g2, x2, p2)
+    assert np.max(np.abs(_np(gd) - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+    fw = pf.objective(g2, x2, p2)
+    assert abs(_np(fd)[0] - fw) <= 1e-12 * abs(fw)
+
+
+def test_reduced_gradient(solved_case):
+    name, g, L, x, p, grad, lam, ops = solved_case
+    ctx, *_ = setup(g)
+    gd, ld = ctx.reduced_gradient()
+    assert np.max(np.abs(_np(ld) - lam)) <= 1e-10 * np.max(np.abs(lam))
+    assert np.max(np.abs(_np(gd) - grad)) <= 1e-10 * np.max(np.abs(grad))
+
+
+def test_hvp_stages_random_W(solved_case):
+    name, g, L, x, p, grad, lam, ops = solved_case
+    ctx, *_ = setup(g)
+    ctx.reduced_gradient()
+    for N in (1, 3, 37):
+        W = gridgen.random_W(L.n_p, N, seed=N)
+        trace = {}
+        HWo = red.hvp_batch(ops, W, trace)
+        HW, Z, Yx, Psi = (_np(t) for t in ctx.hvp_stages(_dev(W)))
+        assert col_rel_err(Z, trace["Z"]) <= 1e-10, "Z"
+        assert col_rel_err(Yx, trace["Yx"]) <= 1e-10, "Yx"
+        assert col_rel_err(Psi, trace["Psi"]) <= 1e-10, "Psi"
+        assert col_rel_err(HW, HWo) <= TOL_H, "HW"
+        HW2 = _np(ctx.hvp(_dev(W)))       # fused kernel == staged kernels bitwise
+        assert np.array_equal(HW2, HW)
+
+
+def test_full_hessian_parity(solved_case):
+    name, g, L, x, p, grad, lam, ops = solved_case
+    ctx, *_ = setup(g)
+    ctx.reduced_gradient()
+    N = {"case9": 5, "case118": 64, "case1354pegase": 256, "case2869pegase": 512}[name]
+    H = _np(ctx.full_hessian(N))
+    Ho = red.full_hessian(ops, N)
+    assert col_rel_err(H, Ho) <= TOL_H
+    assert entry_rel_err(H, Ho) <= TOL_H
+    # batch invariance: bitwise identical across N (fixed per-column arithmetic order)
+    for N2 in (1, 7, L.n_p):
+        assert np.array_equal(_np(ctx.full_hessian(N2)), H), N2
+    # transposed shard layout
+    j0, j1 = L.n_p // 3, L.n_p // 3 + min(50, L.n_p - L.n_p // 3)
+    Ht = _np(ctx.hessian_columns(j0, j1, 16, transposed=True))
+    assert np.array_equal(Ht.T, H[:, j0:j1])
+
+
+def test_set_multipliers_any_lambda(solved_case):
+    name, g, L, x, p, *_ = solved_case
+    if name not in ("case9", "case118"):
+        pytest.skip("small cases only")
+    ctx, *_ = setup(g)
+    lam = np.random.default_rng(9).standard_normal(L.n_x)
+    ctx.set_multipliers(_dev(lam))
+    H = _np(ctx.full_hessian(32))
+    Ho = red.full_hessian(red.operators(g, x, p, lam, L), 32)
+    assert col_rel_err(H, Ho) <= TOL_H
+
+
+def test_end_to_end_host_call(solved_case):
+    name, g, L, x, p, grad, lam, ops = solved_case
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g)
+    gh, H = ctx.reduced_hessian_host(x, p, 64)
+    assert np.max(np.abs(gh - grad)) <= 1e-10 * np.max(np.abs(grad))
+    assert col_rel_err(H, red.full_hessian(ops, 64)) <= TOL_H
+
+
+@pytest.mark.parametrize("name", ["case1354pegase", "case2869pegase", "case9241pegase"])
+def test_lossless_closed_form_gpu(name):
+    # no oracle needed: H_PgPg = 2 c2_ref 11^T + diag(2 c2), v rows/cols == 0
+    g = gridgen.make_grid(name, lossless=True)
+    ctx, x, p = setup(g)
+    ctx.reduced_gradient()
+    N = gridgen.CONFIG_N.get(name, 256)
+    H = _np(ctx.full_hessian(N))
+    xb, xk, pb, pk = ctx.orderings()
+    c2 = np.zeros(g.n_bus)
+    c2[g.gen_bus] = g.c2
+    ref = int(np.flatnonzero(g.bus_type == gridgen.REF)[0])
+    pgm = pk == rh.KIND_PG
+    Hc = np.zeros_like(H)
+    Hc[np.ix_(pgm, pgm)] = 2 * c2[ref] + np.diag(2 * c2[pb[pgm]])
+    assert np.max(np.abs(H - Hc)) <= 1e-10 * np.max(np.abs(Hc))
+
+
+def test_case9241_sampled_columns_vs_oracle():
+    """Full size of the north-star config, in the launch configuration the bench
+    uses (N = 1024): sampled columns checked against the oracle one by one."""
+    g = pf.backout_loads(gridgen.make_grid("case9241pegase"))
+    L = pf.Layout(g)
+    x, p = pf.state_vectors(g, L)
+    grad, lam = red.reduced_gradient(g, x, p, L)
+    ops = red.operators(g, x, p, lam, L)
+    ctx, *_ = setup(g)
+    gd, _ = ctx.reduced_gradient()
+    assert np.max(np.abs(_np(gd) - grad)) <= 1e-10 * np.max(np.abs(grad))
+    H = _np(ctx.full_hessian(1024))
+    cols = sorted(set(np.random.default_rng(0).choice(L.n_p, 24, replace=False).tolist() + [0, L.n_p - 1]))
+    W = np.zeros((L.n_p, len(cols)))
+    W[cols, np.arange(len(cols))] = 1.0
+    Ho = red.hvp_batch(ops, W)
+    assert col_rel_err(H[:, cols], Ho) <= TOL_H
+    # symmetry diagnostic (R18): raw columns, symmetric to rounding
+    assert np.max(np.abs(H - H.T)) <= 1e-9 * np.max(np.abs(H))
+
+
+def test_call_order_errors():
+    g = gridgen.make_grid("case9")
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g)
+    W = _dev(np.ones((ctx.n_p, 2)))
+    with pytest.raises(rh.RHError) as ei:
+        ctx.hvp(W)
+    assert ei.value.code == rh.RH_E_ORDER
+    x, p = ctx.state_vectors(g)
+    ctx.set_state(_dev(x), _dev(p))
+    with pytest.raises(rh.RHError) as ei:
+        ctx.hvp(W)
+    assert ei.value.code == rh.RH_E_ORDER
+    ctx.reduced_gradient()
+    ctx.hvp(W)
+    assert ctx.launch_count() > 0
+
+
+def test_singular_pivot_reported():
+    # v = 0 at every PQ bus makes every Q-row of J vanish -> zero pivots
+    g = gridgen.make_grid("case118")
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g)
+    x, p = ctx.state_vectors(g)
+    xb, xk, pb, pk = ctx.orderings()
+    x[xk == rh.KIND_V] = 0.0
+    x[xk == rh.KIND_THETA] = 0.0
+    with pytest.raises(rh.RHError) as ei:
+        ctx.set_state(_dev(x), _dev(p))
+    assert ei.value.code in (rh.RH_E_SINGULAR,)
