@@ -97,6 +97,9 @@ typedef struct rh_info {
   int32_t levels_fwd;   /* dependency levels of the L and U^T sweeps                  */
   int32_t levels_bwd;   /* dependency levels of the U and L^T sweeps                  */
   int32_t max_level_rows;
+  int32_t n_blocks;     /* elimination-tree blocks (segments of whole subtrees)        */
+  int32_t sep_rows;     /* rows of the separator segment above the blocks              */
+  int32_t seg_levels;   /* max dependency levels inside one segment (any sweep)        */
   int64_t workspace_bytes; /* current device workspace                                 */
 } rh_info;
 
@@ -129,6 +132,11 @@ int rh_orderings(const rh_ctx *ctx, int32_t *x_bus, int32_t *x_kind,
  * row in the forward / backward sweeps).  Any pointer may be NULL. */
 int rh_symbolic(const rh_ctx *ctx, int32_t *perm, int32_t *lu_rowptr, int32_t *lu_colidx,
                 int32_t *level_fwd, int32_t *level_bwd);
+
+/* Segment of every permuted row (host output [n_x]): 0..n_blocks-1 = block
+ * (a union of whole elimination subtrees, processed in shared memory by one
+ * CTA per column chunk), n_blocks = separator. */
+int rh_segments(const rh_ctx *ctx, int32_t *segment_of_row);
 
 /* Set the operating point: x [n_x], p [n_p] DEVICE arrays.  Runs the state
  * kernels (line trig, bus injections, g, P_ref), assembles J and G_p
@@ -189,10 +197,11 @@ int rh_reduced_hessian_host(rh_ctx *ctx, const double *x, const double *p, int32
  * (bench accounting of "gpu_launches"). */
 int64_t rh_launch_count(const rh_ctx *ctx);
 
-/* Device-time breakdown of the most recent rh_hvp-class call when stage
- * timing is enabled (rh_set_timing(ctx, 1)); ms_out[6] receives
- * {L+SpMul, U, FoR, U^T, L^T+SpMulAdd, total}; if the HVP ran as one fused
- * kernel, only total (index 5) is set and the rest are 0. */
+/* Device-time breakdown of the most recent HVP batch when stage timing is
+ * enabled (rh_set_timing(ctx, 1); adds one host sync per batch): ms_out[9]
+ * receives the eight kernels of one Alg. 2 batch {blocks L (+SpMul),
+ * separator L+U, blocks U, tensor projection, blocks U^T, separator U^T+L^T,
+ * blocks L^T, SpMulAdd} and their total. */
 int rh_set_timing(rh_ctx *ctx, int enable);
 int rh_stage_times(const rh_ctx *ctx, float *ms_out);
 

@@ -25,7 +25,7 @@ KIND_THETA, KIND_V, KIND_PG = 0, 1, 2
 
 # every symbol declared in include/redhess.h (checked by tests/test_abi.py)
 EXPORTS = ["rh_create", "rh_destroy", "rh_last_error", "rh_load_grid", "rh_get_info", "rh_orderings",
-           "rh_symbolic", "rh_set_state", "rh_residual", "rh_reduced_gradient", "rh_set_multipliers",
+           "rh_symbolic", "rh_segments", "rh_set_state", "rh_residual", "rh_reduced_gradient", "rh_set_multipliers",
            "rh_hvp", "rh_hvp_stages", "rh_hessian_columns", "rh_full_hessian", "rh_reduced_hessian_host",
            "rh_launch_count", "rh_set_timing", "rh_stage_times"]
 
@@ -50,7 +50,8 @@ class rh_info(ctypes.Structure):
     _fields_ = [("n_bus", ctypes.c_int32), ("n_line", ctypes.c_int32), ("n_x", ctypes.c_int32),
                 ("n_p", ctypes.c_int32), ("nnz_J", ctypes.c_int32), ("nnz_Gp", ctypes.c_int32),
                 ("nnz_LU", ctypes.c_int32), ("levels_fwd", ctypes.c_int32), ("levels_bwd", ctypes.c_int32),
-                ("max_level_rows", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
+                ("max_level_rows", ctypes.c_int32), ("n_blocks", ctypes.c_int32), ("sep_rows", ctypes.c_int32),
+                ("seg_levels", ctypes.c_int32), ("workspace_bytes", ctypes.c_int64)]
 
 
 def _load():
@@ -67,6 +68,7 @@ def _load():
         "rh_get_info": ([vp, ctypes.POINTER(rh_info)], ctypes.c_int),
         "rh_orderings": ([vp, vp, vp, vp, vp], ctypes.c_int),
         "rh_symbolic": ([vp, vp, vp, vp, vp, vp], ctypes.c_int),
+        "rh_segments": ([vp, vp], ctypes.c_int),
         "rh_set_state": ([vp, vp, vp, vp], ctypes.c_int),
         "rh_residual": ([vp, vp, vp, vp], ctypes.c_int),
         "rh_reduced_gradient": ([vp, vp, vp, vp], ctypes.c_int),
@@ -88,11 +90,15 @@ def _load():
     return lib
 
 
-_lib = _load()
+_LIB = None
 
 
 def lib():
-    return _lib
+    """The loaded libredhess.so (raises ImportError if it is missing: no CPU fallback)."""
+    global _LIB
+    if _LIB is None:
+        _LIB = _load()
+    return _LIB
 
 
 def _ptr(a):
@@ -126,7 +132,7 @@ class RedHess:
 
     def __init__(self, device: int = 0):
         h = ctypes.c_void_p()
-        rc = _lib.rh_create(int(device), ctypes.byref(h))
+        rc = lib().rh_create(int(device), ctypes.byref(h))
         if rc != RH_OK:
             raise RHError(rc, f"rh_create(device={device}) failed")
         self._h = h
@@ -136,7 +142,7 @@ class RedHess:
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.rh_destroy(self._h)
+            lib().rh_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -147,7 +153,7 @@ class RedHess:
 
     def _rc(self, rc):
         if rc != RH_OK:
-            raise RHError(rc, _lib.rh_last_error(self._h).decode())
+            raise RHError(rc, lib().rh_last_error(self._h).decode())
 
     # ------------------------------------------------------------------ grid
     def load_grid(self, grid):
@@ -165,19 +171,19 @@ class RedHess:
                     n_gen=keep["gen_bus"].shape[0], theta_ref=float(grid.theta_ref),
                     **{k: v.ctypes.data for k, v in keep.items()})
         nx, npp = ctypes.c_int32(), ctypes.c_int32()
-        self._rc(_lib.rh_load_grid(self._h, ctypes.byref(g), ctypes.byref(nx), ctypes.byref(npp)))
+        self._rc(lib().rh_load_grid(self._h, ctypes.byref(g), ctypes.byref(nx), ctypes.byref(npp)))
         self.n_x, self.n_p = nx.value, npp.value
         return self.n_x, self.n_p
 
     def get_info(self):
         info = rh_info()
-        self._rc(_lib.rh_get_info(self._h, ctypes.byref(info)))
+        self._rc(lib().rh_get_info(self._h, ctypes.byref(info)))
         return {k: getattr(info, k) for k, _ in rh_info._fields_}
 
     def orderings(self):
         xb, xk = np.zeros(self.n_x, np.int32), np.zeros(self.n_x, np.int32)
         pb, pk = np.zeros(self.n_p, np.int32), np.zeros(self.n_p, np.int32)
-        self._rc(_lib.rh_orderings(self._h, _ptr(xb), _ptr(xk), _ptr(pb), _ptr(pk)))
+        self._rc(lib().rh_orderings(self._h, _ptr(xb), _ptr(xk), _ptr(pb), _ptr(pk)))
         return xb, xk, pb, pk
 
     def symbolic(self):
@@ -187,8 +193,10 @@ class RedHess:
         ci = np.zeros(info["nnz_LU"], np.int32)
         lf = np.zeros(self.n_x, np.int32)
         lb = np.zeros(self.n_x, np.int32)
-        self._rc(_lib.rh_symbolic(self._h, _ptr(perm), _ptr(rp), _ptr(ci), _ptr(lf), _ptr(lb)))
-        return dict(perm=perm, rowptr=rp, colidx=ci, level_fwd=lf, level_bwd=lb)
+        self._rc(lib().rh_symbolic(self._h, _ptr(perm), _ptr(rp), _ptr(ci), _ptr(lf), _ptr(lb)))
+        seg = np.zeros(self.n_x, np.int32)
+        self._rc(lib().rh_segments(self._h, _ptr(seg)))
+        return dict(perm=perm, rowptr=rp, colidx=ci, level_fwd=lf, level_bwd=lb, segment=seg)
 
     def state_vectors(self, grid):
         """x, p (numpy) from the grid's bus-level theta, v, Pg in this library's orderings."""
@@ -204,25 +212,25 @@ class RedHess:
     def set_state(self, x, p, stream=None):
         _check_dev(x, self.n_x, "x")
         _check_dev(p, self.n_p, "p")
-        self._rc(_lib.rh_set_state(self._h, _ptr(x), _ptr(p), _stream(stream)))
+        self._rc(lib().rh_set_state(self._h, _ptr(x), _ptr(p), _stream(stream)))
 
     def residual(self, g=None, f=None, stream=None):
         import torch
         g = torch.empty(self.n_x, dtype=torch.float64, device="cuda") if g is None else g
         f = torch.empty(1, dtype=torch.float64, device="cuda") if f is None else f
-        self._rc(_lib.rh_residual(self._h, _ptr(g), _ptr(f), _stream(stream)))
+        self._rc(lib().rh_residual(self._h, _ptr(g), _ptr(f), _stream(stream)))
         return g, f
 
     def reduced_gradient(self, grad=None, lam=None, stream=None):
         import torch
         grad = torch.empty(self.n_p, dtype=torch.float64, device="cuda") if grad is None else grad
         lam = torch.empty(self.n_x, dtype=torch.float64, device="cuda") if lam is None else lam
-        self._rc(_lib.rh_reduced_gradient(self._h, _ptr(grad), _ptr(lam), _stream(stream)))
+        self._rc(lib().rh_reduced_gradient(self._h, _ptr(grad), _ptr(lam), _stream(stream)))
         return grad, lam
 
     def set_multipliers(self, lam, stream=None):
         _check_dev(lam, self.n_x, "lambda")
-        self._rc(_lib.rh_set_multipliers(self._h, _ptr(lam), _stream(stream)))
+        self._rc(lib().rh_set_multipliers(self._h, _ptr(lam), _stream(stream)))
 
     def hvp(self, W, HW=None, stream=None):
         """W: [n_p][N] float64 CUDA tensor (batch index fastest) -> HW [n_p][N]."""
@@ -230,7 +238,7 @@ class RedHess:
         _check_dev(W, name="W")
         N = W.shape[1]
         HW = torch.empty((self.n_p, N), dtype=torch.float64, device=W.device) if HW is None else HW
-        self._rc(_lib.rh_hvp(self._h, _ptr(W), W.stride(0), _ptr(HW), HW.stride(0), N, _stream(stream)))
+        self._rc(lib().rh_hvp(self._h, _ptr(W), W.stride(0), _ptr(HW), HW.stride(0), N, _stream(stream)))
         return HW
 
     def hvp_stages(self, W, stream=None):
@@ -239,7 +247,7 @@ class RedHess:
         N = W.shape[1]
         HW = torch.empty((self.n_p, N), dtype=torch.float64, device=W.device)
         Z, Yx, Psi = (torch.empty((self.n_x, N), dtype=torch.float64, device=W.device) for _ in range(3))
-        self._rc(_lib.rh_hvp_stages(self._h, _ptr(W), W.stride(0), _ptr(HW), HW.stride(0), N, _ptr(Z), _ptr(Yx),
+        self._rc(lib().rh_hvp_stages(self._h, _ptr(W), W.stride(0), _ptr(HW), HW.stride(0), N, _ptr(Z), _ptr(Yx),
                                     _ptr(Psi), Z.stride(0), _stream(stream)))
         return HW, Z, Yx, Psi
 
@@ -248,7 +256,7 @@ class RedHess:
         if H is None:
             shape = (j1 - j0, self.n_p) if transposed else (self.n_p, j1 - j0)
             H = torch.empty(shape, dtype=torch.float64, device="cuda")
-        self._rc(_lib.rh_hessian_columns(self._h, j0, j1, N, _ptr(H), H.stride(0), int(bool(transposed)),
+        self._rc(lib().rh_hessian_columns(self._h, j0, j1, N, _ptr(H), H.stride(0), int(bool(transposed)),
                                          _stream(stream)))
         return H
 
@@ -256,7 +264,7 @@ class RedHess:
         import torch
         H = torch.empty((self.n_p, self.n_p), dtype=torch.float64, device="cuda") if H is None else H
         _check_dev(H, self.n_p * self.n_p, "H")
-        self._rc(_lib.rh_full_hessian(self._h, N, _ptr(H), _stream(stream)))
+        self._rc(lib().rh_full_hessian(self._h, N, _ptr(H), _stream(stream)))
         return H
 
     # ------------------------------------------------------------------ compute (host buffers)
@@ -266,19 +274,19 @@ class RedHess:
             H = np.empty((self.n_p, self.n_p))
         if grad is None:
             grad = np.empty(self.n_p)
-        self._rc(_lib.rh_reduced_hessian_host(self._h, _ptr(x), _ptr(p), N, _ptr(grad), _ptr(H)))
+        self._rc(lib().rh_reduced_hessian_host(self._h, _ptr(x), _ptr(p), N, _ptr(grad), _ptr(H)))
         return grad, H
 
     # ------------------------------------------------------------------ accounting
     def launch_count(self):
-        return int(_lib.rh_launch_count(self._h))
+        return int(lib().rh_launch_count(self._h))
 
     def set_timing(self, enable=True):
-        self._rc(_lib.rh_set_timing(self._h, int(bool(enable))))
+        self._rc(lib().rh_set_timing(self._h, int(bool(enable))))
 
     def stage_times(self):
-        out = np.zeros(6, np.float32)
-        self._rc(_lib.rh_stage_times(self._h, _ptr(out)))
+        out = np.zeros(9, np.float32)
+        self._rc(lib().rh_stage_times(self._h, _ptr(out)))
         return out
 
 

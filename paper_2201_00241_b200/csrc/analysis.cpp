@@ -15,15 +15,21 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <set>
 #include <sstream>
+#include <stdexcept>
+#include <unordered_map>
 
 #include "../../include/redhess.h"
 
 namespace rh {
 
 namespace {
+
+constexpr int kSchedWarps = 16;  // warps of the block sweep kernel (512 threads)
 
 template <class T>
 void sort_unique(std::vector<T> &v) {
@@ -65,9 +71,426 @@ std::vector<int32_t> minimum_degree(std::vector<std::vector<int32_t>> adj) {
   return order;
 }
 
+
+// Subtree-to-warp schedule of one block's sweep.  Lanes
+// own columns, so a warp needs no synchronization between rows it computes
+// itself; only a dependency computed by ANOTHER warp needs a CTA barrier.
+// The block's forest is split into <= ~nw "pieces" (whole subtrees) of
+// balanced cost, packed onto warps (LPT); the few removed roots ("top" rows)
+// are scheduled greedily: a top row joins the warp that owns its dependencies
+// in the current super-level, or opens a new super-level when they span
+// several warps.  Forward: pieces first, then top rows; backward: the reverse.
+// Returns the rows in schedule order; bounds[sl * nw + w] .. bounds[sl * nw + w + 1]
+// are warp w's rows in super-level sl (positions relative to the block start).
+std::vector<int32_t> warp_schedule(const Analysis &A, const std::vector<int32_t> &rows, int s, bool fwd,
+                                   const std::vector<std::vector<int32_t>> &Ls,
+                                   const std::vector<std::vector<int32_t>> &Lrow, int nw,
+                                   std::vector<int32_t> &bounds) {
+  const int n = (int)rows.size();
+  std::unordered_map<int, int> li;
+  li.reserve(n * 2);
+  for (int i = 0; i < n; ++i) li[rows[i]] = i;
+  std::vector<int> par(n, -1);
+  std::vector<std::vector<int>> kids(n);
+  std::vector<double> cost(n), sc(n);
+  for (int i = 0; i < n; ++i) {
+    const int r = rows[i];
+    if (!Ls[r].empty()) {
+      auto it = li.find(Ls[r][0]);
+      if (it != li.end()) par[i] = it->second;
+    }
+    cost[i] = 8.0 + (double)(fwd ? Lrow[r].size() : Ls[r].size());
+  }
+  for (int i = 0; i < n; ++i)
+    if (par[i] >= 0) kids[par[i]].push_back(i);
+  // subtree costs (children have smaller global index: process ascending)
+  std::vector<int> ordi(n);
+  std::iota(ordi.begin(), ordi.end(), 0);
+  std::sort(ordi.begin(), ordi.end(), [&](int a, int b) { return rows[a] < rows[b]; });
+  for (int i : ordi) {
+    sc[i] = cost[i];
+    for (int k : kids[i]) sc[i] += sc[k];
+  }
+  double total = 0;
+  std::vector<int> pieces;
+  for (int i = 0; i < n; ++i)
+    if (par[i] < 0) {
+      pieces.push_back(i);
+      total += sc[i];
+    }
+  const double target = total / nw;
+  std::vector<char> is_top(n, 0);
+  for (int it = 0; it < 4 * nw; ++it) {
+    int best = -1;
+    for (int k = 0; k < (int)pieces.size(); ++k)
+      if (best < 0 || sc[pieces[k]] > sc[pieces[best]]) best = k;
+    if (best < 0 || sc[pieces[best]] <= 1.25 * target || kids[pieces[best]].empty()) break;
+    const int p = pieces[best];
+    pieces.erase(pieces.begin() + best);
+    is_top[p] = 1;
+    for (int k : kids[p]) pieces.push_back(k);
+  }
+  // LPT packing of pieces onto warps
+  std::sort(pieces.begin(), pieces.end(), [&](int a, int b) { return sc[a] > sc[b]; });
+  std::vector<double> load(nw, 0.0);
+  std::vector<std::vector<int>> wrows(nw);
+  std::vector<int> owner(n, -1);
+  for (int p : pieces) {
+    const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    load[w] += sc[p];
+    // rows of the piece in topological order of this direction
+    std::vector<int> st{p}, sub;
+    while (!st.empty()) {
+      const int x = st.back();
+      st.pop_back();
+      sub.push_back(x);
+      for (int k : kids[x]) st.push_back(k);
+    }
+    std::sort(sub.begin(), sub.end(), [&](int a, int b) { return fwd ? rows[a] < rows[b] : rows[a] > rows[b]; });
+    for (int x : sub) wrows[w].push_back(x);
+  }
+  // top rows: topological order of this direction
+  std::vector<int> tops;
+  for (int i = 0; i < n; ++i)
+    if (is_top[i]) tops.push_back(i);
+  std::sort(tops.begin(), tops.end(), [&](int a, int b) { return fwd ? rows[a] < rows[b] : rows[a] > rows[b]; });
+  std::vector<std::vector<std::vector<int>>> SL;
+  auto emit_pieces = [&]() {
+    SL.push_back(wrows);
+  };
+  auto greedy_tops = [&]() {
+    std::vector<int> w_of(n, -1);  // warp of a top row in the CURRENT super-level
+    std::vector<std::vector<int>> cur(nw);
+    std::vector<double> cl(nw, 0.0);
+    std::vector<int> members;
+    for (int i : tops) {
+      std::set<int> ws;
+      for (int k : (fwd ? Lrow[rows[i]] : Ls[rows[i]])) {
+        auto itk = li.find(k);
+        if (itk != li.end() && w_of[itk->second] >= 0) ws.insert(w_of[itk->second]);
+      }
+      if (ws.size() >= 2) {  // dependencies on several warps: barrier, new super-level
+        SL.push_back(cur);
+        cur.assign(nw, {});
+        cl.assign(nw, 0.0);
+        for (int m : members) w_of[m] = -1;
+        members.clear();
+        ws.clear();
+      }
+      const int w = ws.empty() ? (int)(std::min_element(cl.begin(), cl.end()) - cl.begin()) : *ws.begin();
+      cur[w].push_back(i);
+      cl[w] += cost[i];
+      w_of[i] = w;
+      members.push_back(i);
+    }
+    if (!members.empty()) SL.push_back(cur);
+  };
+  if (fwd) {
+    emit_pieces();
+    greedy_tops();
+  } else {
+    greedy_tops();
+    emit_pieces();
+  }
+  std::vector<int32_t> out;
+  bounds.clear();
+  for (auto &sl : SL)
+    for (int w = 0; w < nw; ++w) {
+      bounds.push_back((int)out.size());
+      for (int i : sl[w]) out.push_back(rows[i]);
+    }
+  bounds.push_back((int)out.size());
+  if ((int)out.size() != n) throw std::runtime_error("warp_schedule lost rows");
+  if (getenv("RH_DEBUG_SCHED") && s < 3) {
+    fprintf(stderr, "block %d %s rows %d total cost %.0f target %.0f pieces %zu tops %zu SLs %zu\n", s,
+            fwd ? "fwd" : "bwd", n, total, target, pieces.size(), tops.size(), SL.size());
+    for (size_t k = 0; k < SL.size(); ++k) {
+      double mx = 0;
+      int mr = 0;
+      for (int w = 0; w < nw; ++w) {
+        double c = 0;
+        for (int i : SL[k][w]) c += cost[i];
+        mx = std::max(mx, c);
+        mr = std::max(mr, (int)SL[k][w].size());
+      }
+      fprintf(stderr, "   SL %zu: max warp cost %.0f, max warp rows %d\n", k, mx, mr);
+    }
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// Elimination-tree segments (blocks of whole subtrees + the separator), the
+// per-segment level schedules of the four sweeps, and the refactorization
+// schedule (DESIGN.md "Sweeps" and "Refactorization").
+// ---------------------------------------------------------------------------
+template <class FPos>
+void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
+                    const std::vector<std::vector<int32_t>> &Lrow, FPos fpos, int rmax) {
+  const int nx = A.n_x;
+  A.rmax = rmax;
+  std::vector<int32_t> parent(nx, -1), size(nx, 1);
+  for (int k = 0; k < nx; ++k)
+    if (!Ls[k].empty()) parent[k] = Ls[k][0];
+  for (int k = 0; k < nx; ++k)
+    if (parent[k] >= 0) size[parent[k]] += size[k];
+  // maximal subtrees of <= rmax rows
+  std::vector<int32_t> roots;
+  for (int k = 0; k < nx; ++k)
+    if (size[k] <= rmax && (parent[k] < 0 || size[parent[k]] > rmax)) roots.push_back(k);
+  // first-fit decreasing bin packing of the subtrees into blocks of <= rmax rows
+  std::vector<int32_t> rord(roots);
+  std::stable_sort(rord.begin(), rord.end(), [&](int a, int b) { return size[a] > size[b]; });
+  std::vector<int32_t> bin_fill;
+  std::vector<int32_t> root_bin(nx, -1);
+  for (int r : rord) {
+    int b = -1;
+    for (size_t q = 0; q < bin_fill.size(); ++q)
+      if (bin_fill[q] + size[r] <= rmax) {
+        b = (int)q;
+        break;
+      }
+    if (b < 0) {
+      b = (int)bin_fill.size();
+      bin_fill.push_back(0);
+    }
+    bin_fill[b] += size[r];
+    root_bin[r] = b;
+  }
+  const int nb = (int)bin_fill.size();
+  A.nblk = nb;
+  A.seg_of.assign(nx, nb);
+  for (int k = nx - 1; k >= 0; --k) {
+    if (root_bin[k] >= 0)
+      A.seg_of[k] = root_bin[k];
+    else if (parent[k] >= 0 && A.seg_of[parent[k]] < nb)
+      A.seg_of[k] = A.seg_of[parent[k]];
+  }
+  const int nseg = nb + 1;
+  A.seg_row_off.assign(nseg + 1, 0);
+  for (int k = 0; k < nx; ++k) A.seg_row_off[A.seg_of[k] + 1]++;
+  for (int s = 0; s < nseg; ++s) A.seg_row_off[s + 1] += A.seg_row_off[s];
+  A.row_global.assign(nx, 0);
+  A.loc_of.assign(nx, 0);
+  {
+    std::vector<int32_t> fill(A.seg_row_off.begin(), A.seg_row_off.end() - 1);
+    for (int k = 0; k < nx; ++k) {
+      const int s = A.seg_of[k];
+      A.loc_of[k] = fill[s] - A.seg_row_off[s];
+      A.row_global[fill[s]++] = k;
+    }
+  }
+  A.max_seg_rows = 0;
+  for (int s = 0; s < nb; ++s) A.max_seg_rows = std::max(A.max_seg_rows, A.seg_row_off[s + 1] - A.seg_row_off[s]);
+  A.sep_rows = A.seg_row_off[nseg] - A.seg_row_off[nb];
+
+  auto build = [&](SegSweep &S, bool fwd) {
+    // local levels: deps within the same segment only
+    std::vector<int32_t> lv(nx, 0);
+    if (fwd) {
+      for (int i = 0; i < nx; ++i) {
+        int l = 0;
+        for (int k : Lrow[i])
+          if (A.seg_of[k] == A.seg_of[i]) l = std::max(l, lv[k] + 1);
+        lv[i] = l;
+      }
+    } else {
+      for (int i = nx - 1; i >= 0; --i) {
+        int l = 0;
+        for (int k : Ls[i])
+          if (A.seg_of[k] == A.seg_of[i]) l = std::max(l, lv[k] + 1);
+        lv[i] = l;
+      }
+    }
+    S.seg_lvl.assign(nseg + 1, 0);
+    S.lvl_ptr.clear();
+    S.order.clear();
+    S.rptr.assign(1, 0);
+    S.rext.clear();
+    S.dep.clear();
+    S.src_a.clear();
+    S.src_b.clear();
+    S.dsrc.clear();
+    S.ext_off.assign(nseg + 1, 0);
+    S.ext_rows.clear();
+    S.max_levels = 0;
+    for (int s = 0; s < nseg; ++s) {
+      S.seg_lvl[s] = (int)S.lvl_ptr.size();
+      std::vector<int32_t> rows(A.row_global.begin() + A.seg_row_off[s],
+                                A.row_global.begin() + A.seg_row_off[s + 1]);
+      const int nr_s = (int)rows.size();
+      std::vector<int32_t> ext;  // blocks only: separator rows this segment depends on
+      if (s < nb) {
+        for (int r : rows)
+          for (int k : (fwd ? Lrow[r] : Ls[r]))
+            if (A.seg_of[k] != s) ext.push_back(k);
+        sort_unique(ext);
+      }
+      S.ext_off[s] = (int)S.ext_rows.size();
+      S.ext_rows.insert(S.ext_rows.end(), ext.begin(), ext.end());
+      auto ext_local = [&](int k) -> int {
+        auto it = std::lower_bound(ext.begin(), ext.end(), k);
+        return nr_s + (int)(it - ext.begin());
+      };
+      std::stable_sort(rows.begin(), rows.end(), [&](int a, int b) { return lv[a] < lv[b]; });
+      int nl = 0;
+      for (int r : rows) nl = std::max(nl, lv[r] + 1);
+      S.max_levels = std::max(S.max_levels, nl);
+      const int qbase = (int)S.order.size();
+      if (s < nb) {
+        // blocks: subtree-to-warp schedule ("super-levels" x warps), see warp_schedule
+        std::vector<int32_t> bounds;
+        rows = warp_schedule(A, rows, s, fwd, Ls, Lrow, kSchedWarps, bounds);
+        for (int b : bounds) S.lvl_ptr.push_back(qbase + b);
+        S.max_levels = std::max(S.max_levels, (int)(bounds.size() - 1) / kSchedWarps);
+      } else {
+        std::vector<int32_t> cnt(nl + 1, 0);
+        for (int r : rows) cnt[lv[r] + 1]++;
+        for (int l = 0; l < nl; ++l) cnt[l + 1] += cnt[l];
+        for (int l = 0; l <= nl; ++l) S.lvl_ptr.push_back(qbase + cnt[l]);
+      }
+      if (fwd) {  // level order of every segment for the refactorization (R_A)
+        A.fact_seg_lvl.push_back((int)A.fact_lvl_ptr.size());
+        std::vector<int32_t> lrows(rows);
+        std::stable_sort(lrows.begin(), lrows.end(), [&](int a, int b) { return lv[a] < lv[b]; });
+        std::vector<int32_t> cnt(nl + 1, 0);
+        for (int r : lrows) cnt[lv[r] + 1]++;
+        for (int l = 0; l < nl; ++l) cnt[l + 1] += cnt[l];
+        const int fb = (int)A.fact_order.size();
+        for (int l = 0; l <= nl; ++l) A.fact_lvl_ptr.push_back(fb + cnt[l]);
+        for (int r : lrows) A.fact_order.push_back(A.loc_of[r]);
+      }
+      for (int r : rows) {
+        S.order.push_back(A.loc_of[r]);
+        const std::vector<int32_t> &deps = fwd ? Lrow[r] : Ls[r];
+        for (int pass = 0; pass < 2; ++pass) {   // external entries first, then local
+          for (int k : deps) {
+            const bool local = A.seg_of[k] == s || s < nb;   // blocks: staged ext rows are local
+            if (local != (pass == 1)) continue;
+            S.dep.push_back(A.seg_of[k] == s ? A.loc_of[k] : (s < nb ? ext_local(k) : k));
+            S.src_a.push_back(fpos(r, k));   // fwd: L[r,k]  bwd: U[r,k]
+            S.src_b.push_back(fpos(k, r));   // fwd: U[k,r]  bwd: L[k,r]
+          }
+          if (pass == 0) S.rext.push_back((int)S.dep.size());
+        }
+        S.rptr.push_back((int)S.dep.size());
+        S.dsrc.push_back(A.F_diag[r]);
+      }
+    }
+    S.seg_lvl[nseg] = (int)S.lvl_ptr.size();
+    S.ext_off[nseg] = (int)S.ext_rows.size();
+    if (fwd) A.fact_seg_lvl.push_back((int)A.fact_lvl_ptr.size());
+  };
+  A.fact_seg_lvl.clear();
+  A.fact_lvl_ptr.clear();
+  A.fact_order.clear();
+  build(A.fwd, true);
+  build(A.bwd, false);
+  A.blk_gp_ptr.assign(nb + 1, 0);
+  A.blk_gp_loc.clear();
+  for (int s = 0; s < nb; ++s) {
+    for (int q = A.seg_row_off[s]; q < A.seg_row_off[s + 1]; ++q) {
+      const int r = A.row_global[q];
+      if (A.gp_rptr[r + 1] > A.gp_rptr[r]) A.blk_gp_loc.push_back(q - A.seg_row_off[s]);
+    }
+    A.blk_gp_ptr[s + 1] = (int)A.blk_gp_loc.size();
+  }
+
+  // ---------------- refactorization schedule ----------------
+  // R_A: block rows staged in shared memory (local order), up-looking per row.
+  A.blk_fo_off.assign(nb + 1, 0);
+  A.fo.clear();
+  A.max_blk_fnnz = 0;
+  std::vector<int32_t> fo_of(nx, -1);
+  for (int s = 0; s < nb; ++s) {
+    A.blk_fo_off[s] = (int)A.fo.size();
+    int off = 0;
+    for (int q = A.seg_row_off[s]; q < A.seg_row_off[s + 1]; ++q) {
+      const int r = A.row_global[q];
+      fo_of[r] = off;
+      A.fo.push_back(off);
+      off += A.F_rowptr[r + 1] - A.F_rowptr[r];
+    }
+    A.fo.push_back(off);
+    A.max_blk_fnnz = std::max(A.max_blk_fnnz, off);
+  }
+  A.blk_fo_off[nb] = (int)A.fo.size();
+  A.ks_ptr.assign(nx + 1, 0);
+  A.ks_pos.clear();
+  A.ks_k.clear();
+  A.ks_kf.clear();
+  A.ks_ulen.clear();
+  A.ks_tgt.clear();
+  A.tgt.clear();
+  for (int i = 0; i < nx; ++i) {
+    const int si = A.seg_of[i];
+    const int rb = A.F_rowptr[i];
+    for (int k : Lrow[i]) {
+      const int sk = A.seg_of[k];
+      if (si == nb && sk == nb) continue;  // separator x separator: R_B2 (right-looking)
+      A.ks_pos.push_back(fpos(i, k) - rb);
+      if (si < nb) {  // R_A: k in the same block
+        A.ks_k.push_back(A.loc_of[k]);
+        A.ks_kf.push_back(fo_of[k] + (A.F_diag[k] - A.F_rowptr[k]));
+      } else {        // R_B1: k in a block, row i in the separator
+        A.ks_k.push_back(k);
+        A.ks_kf.push_back(A.F_diag[k]);
+      }
+      const int ub = A.F_diag[k] + 1, ue = A.F_rowptr[k + 1];
+      A.ks_ulen.push_back(ue - ub);
+      A.ks_tgt.push_back((int)A.tgt.size());
+      for (int u = ub; u < ue; ++u) A.tgt.push_back(fpos(i, A.F_col[u]) - rb);
+    }
+    A.ks_ptr[i + 1] = (int)A.ks_pos.size();
+  }
+  // R_B2: separator x separator entries, right-looking in separator order
+  const int sb0 = A.seg_row_off[nb];
+  const int ns = A.sep_rows;
+  std::vector<std::vector<std::pair<int, int>>> srow(ns);  // (global col, slot)
+  A.sb_src.clear();
+  for (int a = 0; a < ns; ++a) {
+    const int i = A.row_global[sb0 + a];
+    for (int e = A.F_rowptr[i]; e < A.F_rowptr[i + 1]; ++e) {
+      const int j = A.F_col[e];
+      if (A.seg_of[j] == nb) {
+        srow[a].push_back({j, (int)A.sb_src.size()});
+        A.sb_src.push_back(e);
+      }
+    }
+  }
+  auto slot = [&](int a, int j) -> int {
+    auto &v = srow[a];
+    auto it = std::lower_bound(v.begin(), v.end(), std::make_pair(j, -1));
+    return (it != v.end() && it->first == j) ? it->second : -1;
+  };
+  A.sb_diag.assign(ns, -1);
+  A.sb_lptr.assign(ns + 1, 0);
+  A.sb_uptr.assign(ns + 1, 0);
+  A.sb_lslot.clear();
+  A.sb_trip.clear();
+  for (int a = 0; a < ns; ++a) {
+    const int k = A.row_global[sb0 + a];
+    A.sb_diag[a] = slot(a, k);
+    std::vector<int> lrows;  // separator rows i > k with F[i,k] != 0 (= U pattern of row k, symmetric)
+    for (int i : Ls[k])
+      if (A.seg_of[i] == nb) lrows.push_back(i);
+    for (int i : lrows) A.sb_lslot.push_back(slot(A.loc_of[i], k));
+    for (int i : lrows) {
+      const int li = slot(A.loc_of[i], k);
+      for (int j : Ls[k]) {  // U columns of row k (all separator)
+        A.sb_trip.push_back(li);
+        A.sb_trip.push_back(slot(a, j));
+        A.sb_trip.push_back(slot(A.loc_of[i], j));
+      }
+    }
+    A.sb_lptr[a + 1] = (int)A.sb_lslot.size();
+    A.sb_uptr[a + 1] = (int)(A.sb_trip.size() / 3);
+  }
+}
+
 }  // namespace
 
-std::string analyze(const ::rh_grid &g, Analysis &A) {
+std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
   std::ostringstream err;
   const int n = g.n_bus, m = g.n_line, ng = g.n_gen;
   if (n < 2) return "grid needs at least 2 buses";
@@ -483,6 +906,7 @@ std::string analyze(const ::rh_grid &g, Analysis &A) {
   A.near_ref.push_back(A.ref);
   for (int s = A.bl_ptr[A.ref]; s < A.bl_ptr[A.ref + 1]; ++s) A.near_ref.push_back(A.bl_other[s]);
   sort_unique(A.near_ref);
+  build_segments(A, Ls, Lrow, fpos, rmax);
   return "";
 }
 

@@ -25,6 +25,30 @@ struct Sweep {
   int nlev() const { return (int)lev_ptr.size() - 1; }
 };
 
+// Segment decomposition of the elimination tree:
+// segments 0..nblk-1 are BLOCKS (unions of whole subtrees of <= Rmax rows);
+// segment nblk is the SEPARATOR (the rows above the blocks).  A block row
+// depends (forward: L, U^T) only on rows of its own block; backward (U, L^T)
+// on its block and the separator.  A separator row depends forward on blocks
+// and the separator, backward only on the separator.
+struct SegSweep {
+  std::vector<int32_t> lvl_ptr;   // per segment s: lvl_ptr[seg_lvl[s] .. seg_lvl[s+1]-1] = level bounds (into q)
+  std::vector<int32_t> seg_lvl;   // [nseg + 1]
+  std::vector<int32_t> order;     // [n_x] q -> local row index within the segment
+  std::vector<int32_t> rptr;      // [n_x + 1] q -> entry range: [rptr[q], rext[q]) external, [rext[q], rptr[q+1]) local
+  std::vector<int32_t> rext;      // [n_x]
+  std::vector<int32_t> dep;       // [nnz] local: index in the same segment; external: global permuted row
+  std::vector<int32_t> src_a;     // [nnz] F position, first sweep (fwd: L[i,k];  bwd: U[i,k])
+  std::vector<int32_t> src_b;     // [nnz] F position, second sweep (fwd: U[k,i]; bwd: L[k,i])
+  std::vector<int32_t> dsrc;      // [n_x] F position of the pivot of row (q)
+  // blocks: the separator rows a block's sweep depends on are staged next to the
+  // block's own rows (local indices nr .. nr + n_ext - 1), so block sweeps have
+  // no external entries; the separator keeps external (global-row) entries.
+  std::vector<int32_t> ext_off;   // [nseg + 1]
+  std::vector<int32_t> ext_rows;  // global permuted rows
+  int max_levels = 0;
+};
+
 struct Analysis {
   // ---------------- grid copy ----------------
   int n_bus = 0, n_line = 0, n_gen = 0, ref = -1;
@@ -64,8 +88,8 @@ struct Analysis {
   // G_p CSC (by p column): positions into gp value array and permuted rows
   std::vector<int32_t> gpc_ptr, gpc_pos, gpc_row;
 
-  // refactorization schedule: rows in forward level order
-  std::vector<int32_t> fact_order;
+  // refactorization schedule: per segment, rows in forward local level order (local indices)
+  std::vector<int32_t> fact_seg_lvl, fact_lvl_ptr, fact_order;
 
   // the four sweeps
   Sweep sL, sU, sUt, sLt;
@@ -75,9 +99,38 @@ struct Analysis {
   // outputs: >= 0 permuted row of -Y_x ; <= -2 row -(d+2) of Y_p ; -1 none
   std::vector<int32_t> yth_dst, yv_dst;     // per bus
   std::vector<int32_t> near_ref;            // buses b in {ref} u A(ref) (unique)
+
+  // ---------------- etree segments ----------------
+  int rmax = 0;                             // max rows per block
+  int nblk = 0;                             // number of blocks; segment nblk = separator
+  std::vector<int32_t> seg_row_off;         // [nblk + 2]
+  std::vector<int32_t> row_global;          // [n_x] local -> permuted global row, per segment (ascending)
+  std::vector<int32_t> seg_of, loc_of;      // [n_x] segment / local index of every permuted row
+  int max_seg_rows = 0, sep_rows = 0;
+  SegSweep fwd, bwd;                        // fwd: L and U^T ; bwd: U and L^T
+  std::vector<int32_t> blk_gp_ptr, blk_gp_loc;  // per block: local rows carrying G_p entries
+
+  // ---------------- refactorization schedule ----------------
+  // R_A (per block, shared memory): F rows of the block staged at fo (block-local offsets)
+  std::vector<int32_t> blk_fo_off;          // [nblk + 1] offset into fo (rows of the block, local order)
+  std::vector<int32_t> fo;                  // [n_block_rows + nblk] smem offsets of each block row (+ end)
+  int max_blk_fnnz = 0;
+  // per row (ks range by permuted global row): k-steps of the up-looking elimination
+  std::vector<int32_t> ks_ptr;              // [n_x + 1]
+  std::vector<int32_t> ks_pos;              // offset of column k inside row i
+  std::vector<int32_t> ks_k;                // k: block-local index (R_A) or global row (R_B1)
+  std::vector<int32_t> ks_kf;               // R_A: smem offset of row k's pivot; R_B1: F position of the pivot
+  std::vector<int32_t> ks_ulen;             // number of U entries of row k
+  std::vector<int32_t> ks_tgt;              // start in tgt
+  std::vector<int32_t> tgt;                 // offsets inside row i of the U columns of row k
+  // R_B2 (separator, right-looking, shared memory)
+  std::vector<int32_t> sb_src;              // [nslots] F positions of separator-column entries of separator rows
+  std::vector<int32_t> sb_diag;             // [sep_rows] slot of the pivot of separator row (local)
+  std::vector<int32_t> sb_lptr, sb_lslot;   // per step: slots (i, k) of column k, i > k
+  std::vector<int32_t> sb_uptr, sb_trip;    // per step: triples (l_slot, u_slot, target) packed 3 x int32
 };
 
 // Returns "" on success, else an error message (grid rejected).
-std::string analyze(const ::rh_grid &g, Analysis &A);
+std::string analyze(const ::rh_grid &g, Analysis &A, int rmax = 512);
 
 }  // namespace rh

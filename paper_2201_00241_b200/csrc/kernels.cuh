@@ -1,12 +1,10 @@
-// Device kernels of the batched adjoint-adjoint reduced Hessian (sm_100a, fp64).
+// Device-side parameter blocks of the batched adjoint-adjoint reduced Hessian
+// (sm_100a, fp64).  See redhess.cu for the kernels and DESIGN.md for the design.
 //
-// Layout of the batched blocks: the n_x x N blocks Z
-// and Psi live in library scratch, tiled by columns: tile t holds columns
-// [t*T, t*T+T) of all n_x (permuted) rows, element (row r, col c) at
-// X[(t * n_x + r) * T + c].  One CTA owns one column tile for the whole HVP,
-// so the entire Alg. 2 pipeline runs without any
-// inter-CTA synchronization: columns are independent ("slice by slice, in an
-// embarrassingly parallel fashion").
+// Batched blocks in HBM: Z and Psi are [n_x][ld]
+// row-major in the PERMUTED row numbering of the factorization, batch index
+// fastest (SoA across the batch), ld = N rounded up to a multiple of 32.
+// W and HW are the caller's [n_p][ldw] / [n_p][ldhw] blocks.
 #pragma once
 
 #include <cstdint>
@@ -15,50 +13,65 @@ namespace rh {
 
 constexpr int kThreads = 256;
 
-struct DSweep {
-  int nlev;
-  const int *__restrict__ lev_ptr;   // [nlev+1]
-  const int *__restrict__ rows;      // [n] level order
-  const int *__restrict__ rptr;      // [n+1]
-  const int *__restrict__ col;       // [nnz]
-  const double *__restrict__ val;    // [nnz]
-  const double *__restrict__ dinv;   // [n] (null: unit diagonal)
+// One dependency pattern (forward: L / U^T, backward: U / L^T) split into
+// elimination-tree segments (blocks + separator), each with its own levels.
+struct DSeg {
+  const int *__restrict__ seg_lvl;   // [nseg + 1] into lvl_ptr
+  const int *__restrict__ lvl_ptr;   // level bounds into q
+  const int *__restrict__ order;     // [n_x] q -> local row
+  const int *__restrict__ rptr;      // [n_x + 1]
+  const int *__restrict__ rext;      // [n_x]: [rptr, rext) external entries, [rext, rptr+1) local
+  const int *__restrict__ dep;       // local row index (local entries) / global permuted row (external)
+  const int *__restrict__ ext_off;   // [nseg + 1] blocks: staged separator rows
+  const int *__restrict__ ext_rows;
 };
 
-enum : int {
-  PH_L = 1,        // SpMul (B = G_p W) fused into the forward L sweep: L Z' = -P B
-  PH_U = 2,        // backward U sweep: Z' = U^{-1} Z'
-  PH_FOR = 4,      // BatchTensorProjection by forward-over-reverse (bus-centric)
-  PH_UT = 8,       // forward U^T sweep on -Y_x
-  PH_LT = 16,      // backward L^T sweep -> Psi'
-  PH_MULADD = 32,  // SpMulAdd HW = Y_p + G_p^T Psi
-  PH_ALL = 63
-};
-
-struct HvpParams {
-  int n_x, n_p, n_bus, N;
-  const double *W;  // [n_p][ldw] or null with ident_j0 >= 0 (Cartesian block e_{j0..})
+struct SegParams {
+  int n_x, n_p, n_bus, N, ld;
+  int nblk;                          // segment nblk = separator
+  const int *seg_row_off, *row_global;
+  DSeg fwd, bwd;
+  const double *vL, *vUt, *vU, *vLt;   // values per sweep (entry order of fwd / bwd)
+  const double *dinv_fwd, *dinv_bwd;   // 1 / u_ii in fwd / bwd q order
+  int ns, sep_off;                     // separator rows, first separator slot in row_global
+  const double *Sinv, *SinvT;          // dense [ns][ns] inverse of the separator block L_ss U_ss (+ transpose)
+  double *Tsep;                        // [ns][ld] separator right-hand sides
+  const int *blk_gp_ptr, *blk_gp_loc;  // per block: local rows with G_p entries
+  const double *W;                   // [n_p][ldw]; null with ident_j0 >= 0 (Cartesian block)
   long long ldw;
+  int ident_j0;
   double *HW;
   long long ldhw;
-  int ident_j0;
-  int transposed;   // HW element (row i, col k) at k*ldhw + i instead of i*ldhw + k
-  double *X1, *X2;  // tiled scratch
-  DSweep L, U, Ut, Lt;
-  const int *gp_rptr, *gp_col;
+  int transposed;
+  double *Z, *P;                     // [n_x][ld] work blocks (Z, then -Y_x -> Psi)
+  const int *gp_rptr, *gp_col;       // G_p CSR over permuted rows
   const double *gp_val;
-  const int *gpc_ptr, *gpc_row;
+  const int *gpc_ptr, *gpc_row;      // G_p CSC (p columns), rows permuted
   const double *gpc_val;
-  const int *bl_ptr, *bl_line, *bl_end;
-  const int *o_dth_src, *o_dv_src;   // per incident slot: delta sources of the other end
+  // forward-over-reverse tape
+  const int *bl_ptr, *bl_line, *bl_end, *o_dth_src, *o_dv_src;
   const int *dth_src, *dv_src, *yth_dst, *yv_dst, *pg_p;
-  const double4 *coef;               // per line (K, a_i, a_j, m)
-  const double *dcoef;               // per bus 2 (G_ii mu_P - B_ii mu_Q)
-  const double *refg_th, *refg_v;    // grad P_ref over bus theta / v
-  const double *c2b;                 // per-bus c2
+  const double4 *coef;
+  const double *dcoef, *refg_th, *refg_v, *c2b;
   const int *near_ref;
   int n_near_ref;
-  double f2ref;                      // f''(Pg_ref) = 2 c2_ref
+  double f2ref;
+  int debug;                         // experiment bits (0 in production)
+  long long *dbg;
+};
+
+struct FactParams {
+  int nblk, ns;
+  const int *seg_row_off, *row_global;
+  const int *fwd_seg_lvl, *fwd_lvl_ptr, *fwd_order;
+  const int *blk_fo_off, *fo;
+  const int *F_rowptr, *F_diag;
+  double *F_val;
+  const int *ks_ptr, *ks_pos, *ks_k, *ks_kf, *ks_ulen, *ks_tgt, *tgt;
+  const int *sb_src, *sb_diag, *sb_lptr, *sb_lslot, *sb_uptr, *sb_trip;
+  double *dinv, *rowmax;             // per permuted row
+  int *status;
+  double pivtol;
 };
 
 }  // namespace rh

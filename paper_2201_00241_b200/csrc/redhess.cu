@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -190,71 +191,118 @@ __global__ void k_objective(int n_bus, int ref, const int *has_gen, const double
   }
 }
 
+
 // ============================================================================
 // numeric refactorization on the fixed pattern (
-// PAPER.md:764-767).  Up-looking Doolittle, one warp per row, rows taken in
-// forward-level (topological) order from a ticket counter; a row waits on
-// per-row completion flags of the rows it depends on (no grid barrier; the
-// ticket order makes the wait deadlock-free).  Static diagonal pivots (R15).
+// PAPER.md:764-767), static diagonal pivots (R15), three phases over the
+// elimination-tree segments:
+//   R_A  one CTA per block: the block's F rows staged in shared memory,
+//        up-looking Doolittle row by row in local level order (warp per row);
+//   R_B1 one warp per separator row: the updates from block columns;
+//   R_B2 one CTA: right-looking elimination of the separator x separator
+//        submatrix in shared memory (one barrier pair per pivot).
+// Every entry receives its updates in a fixed order: deterministic.
 // ============================================================================
 
-__global__ void __launch_bounds__(kThreads) k_refactor(int nx, const int *__restrict__ order,
-                                                       const int *__restrict__ rowptr,
-                                                       const int *__restrict__ colidx,
-                                                       const int *__restrict__ diag, double *val, int *flags,
-                                                       int epoch, int *ticket, int *status, double pivtol) {
-  const int lane = threadIdx.x & 31;
-  for (;;) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(ticket, 1);
-    t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= nx) return;
-    const int i = order[t];
-    const int rb = rowptr[i], re = rowptr[i + 1], dpos = diag[i];
-    double amax = 0.0;
-    for (int e = rb + lane; e < re; e += 32) amax = fmax(amax, fabs(val[e]));
-    amax = warp_max(amax);
-    for (int e = rb + lane; e < dpos; e += 32) {
-      const int k = colidx[e];
-      while (ld_acquire(flags + k) != epoch) {
+__global__ void __launch_bounds__(kThreads) k_fact_blocks(FactParams f) {
+  extern __shared__ double sm[];
+  const int s = blockIdx.x;
+  const int r0 = f.seg_row_off[s], nr = f.seg_row_off[s + 1] - r0;
+  const int fb = f.blk_fo_off[s];
+  double *SF = sm;                                   // [fo end]
+  double *sdinv = sm + f.fo[fb + nr];                // [nr]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int a = warp; a < nr; a += nw) {
+    const int i = f.row_global[r0 + a];
+    const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off, rb = f.F_rowptr[i];
+    for (int t = lane; t < len; t += 32) SF[off + t] = f.F_val[rb + t];
+  }
+  __syncthreads();
+  const int l0 = f.fwd_seg_lvl[s], l1 = f.fwd_seg_lvl[s + 1] - 1;
+  for (int l = l0; l < l1; ++l) {
+    const int q0 = f.fwd_lvl_ptr[l], q1 = f.fwd_lvl_ptr[l + 1];
+    for (int q = q0 + warp; q < q1; q += nw) {
+      const int a = f.fwd_order[q];
+      const int i = f.row_global[r0 + a];
+      const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off;
+      double amax = 0.0;
+      for (int t = lane; t < len; t += 32) amax = fmax(amax, fabs(SF[off + t]));
+      amax = warp_max(amax);
+      for (int ks = f.ks_ptr[i]; ks < f.ks_ptr[i + 1]; ++ks) {
+        const int pos = f.ks_pos[ks];
+        const double lik = SF[off + pos] * sdinv[f.ks_k[ks]];
+        __syncwarp();
+        if (lane == 0) SF[off + pos] = lik;
+        const int kf = f.ks_kf[ks] + 1, ulen = f.ks_ulen[ks], t0 = f.ks_tgt[ks];
+        for (int t = lane; t < ulen; t += 32) SF[off + f.tgt[t0 + t]] -= lik * SF[kf + t];
+        __syncwarp();
       }
-    }
-    __syncwarp();
-    __threadfence();  // invalidate stale L1 lines before reading other rows
-    for (int e = rb; e < dpos; ++e) {
-      const int k = colidx[e];
-      const int dk = diag[k];
-      const double lik = val[e] / val[dk];
-      __syncwarp();
-      if (lane == 0) val[e] = lik;
-      const int ub = dk + 1, ue = rowptr[k + 1];
-      for (int u = ub + lane; u < ue; u += 32) {
-        const int j = colidx[u];
-        // binary search j in row i (j > k, present by construction of the fill)
-        int lo = e + 1, hi = re - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (colidx[mid] < j)
-            lo = mid + 1;
-          else
-            hi = mid;
-        }
-        val[lo] -= lik * val[u];
+      const double piv = SF[off + (f.F_diag[i] - f.F_rowptr[i])];
+      if (lane == 0) {
+        const double di = 1.0 / piv;
+        sdinv[a] = di;
+        f.dinv[i] = di;
+        if (!(fabs(piv) > f.pivtol * amax)) atomicMax(f.status, i + 1);
       }
       __syncwarp();
     }
-    if (lane == 0) {
-      const double piv = val[dpos];
-      if (!(fabs(piv) > pivtol * amax)) atomicMax(status, i + 1);
-    }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(flags + i, epoch);
+    __syncthreads();
+  }
+  for (int a = warp; a < nr; a += nw) {
+    const int i = f.row_global[r0 + a];
+    const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off, rb = f.F_rowptr[i];
+    for (int t = lane; t < len; t += 32) f.F_val[rb + t] = SF[off + t];
   }
 }
 
-// copy factor values into the four sweep value arrays + inverted pivots,
-// and G_p values into CSC order
+__global__ void __launch_bounds__(kThreads) k_fact_sep_rows(FactParams f) {
+  const int lane = threadIdx.x & 31;
+  const int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (a >= f.ns) return;
+  const int i = f.row_global[f.seg_row_off[f.nblk] + a];
+  const int rb = f.F_rowptr[i], re = f.F_rowptr[i + 1];
+  double *w = f.F_val + rb;
+  double amax = 0.0;
+  for (int e = rb + lane; e < re; e += 32) amax = fmax(amax, fabs(f.F_val[e]));
+  amax = warp_max(amax);
+  if (lane == 0) f.rowmax[i] = amax;
+  for (int ks = f.ks_ptr[i]; ks < f.ks_ptr[i + 1]; ++ks) {
+    const int pos = f.ks_pos[ks];
+    const double lik = w[pos] * f.dinv[f.ks_k[ks]];
+    __syncwarp();
+    if (lane == 0) w[pos] = lik;
+    const double *uk = f.F_val + f.ks_kf[ks] + 1;
+    const int ulen = f.ks_ulen[ks], t0 = f.ks_tgt[ks];
+    for (int t = lane; t < ulen; t += 32) w[f.tgt[t0 + t]] -= lik * uk[t];
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_fact_sep(FactParams f, int nslots) {
+  extern __shared__ double S[];
+  for (int t = threadIdx.x; t < nslots; t += blockDim.x) S[t] = f.F_val[f.sb_src[t]];
+  __syncthreads();
+  const int sb0 = f.seg_row_off[f.nblk];
+  for (int a = 0; a < f.ns; ++a) {
+    const double piv = S[f.sb_diag[a]];
+    const double di = 1.0 / piv;
+    if (threadIdx.x == 0) {
+      const int k = f.row_global[sb0 + a];
+      f.dinv[k] = di;
+      if (!(fabs(piv) > f.pivtol * f.rowmax[k])) atomicMax(f.status, k + 1);
+    }
+    for (int t = f.sb_lptr[a] + threadIdx.x; t < f.sb_lptr[a + 1]; t += blockDim.x) S[f.sb_lslot[t]] *= di;
+    __syncthreads();
+    for (int t = f.sb_uptr[a] + threadIdx.x; t < f.sb_uptr[a + 1]; t += blockDim.x) {
+      const int *tr = f.sb_trip + 3 * t;
+      S[tr[2]] -= S[tr[0]] * S[tr[1]];
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < nslots; t += blockDim.x) f.F_val[f.sb_src[t]] = S[t];
+}
+
+// copy factor values into the sweep value arrays (entry order of the sweeps)
 __global__ void k_gather_vals(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n) dst[e] = F[src[e]];
@@ -265,194 +313,482 @@ __global__ void k_gather_inv(int n, const int *__restrict__ src, const double *_
 }
 
 // ============================================================================
-// batched sweeps: one CTA walks all levels of its
-// column tile with CTA barriers only.  Each row slot is T threads (one per
-// column of the tile); rows of one level are independent.
+// batched triangular sweeps over elimination-tree segments (SURVEY.md
+// 8(a)-6, 8(a)-8).  One CTA = (segment, chunk of C columns).  The segment's
+// rows x C columns live in shared memory for the whole sweep; dependencies
+// outside the segment (separator rows for a block's backward sweep, block
+// rows for the separator's forward sweep) are read from HBM/L2.  Each level
+// of the segment is one CTA barrier; each row is C lanes (one per column),
+// so the coefficient and index loads are warp-uniform broadcasts and the
+// shared-memory gathers are contiguous.
 // ============================================================================
 
-template <int T, bool DIAG>
-__device__ __forceinline__ void sweep_inplace(const DSweep &S, double *__restrict__ X) {
-  const int c = threadIdx.x % T;
-  const int slot = threadIdx.x / T;
-  constexpr int nslots = kThreads / T;
-  for (int lv = 0; lv < S.nlev; ++lv) {
-    const int beg = S.lev_ptr[lv], end = S.lev_ptr[lv + 1];
-    for (int q = beg + slot; q < end; q += nslots) {
-      const int r = S.rows[q];
-      const int e0 = S.rptr[q], e1 = S.rptr[q + 1];
-      double acc = X[r * T + c];
-      for (int e = e0; e < e1; ++e) acc -= S.val[e] * X[S.col[e] * T + c];
-      if (DIAG) acc *= S.dinv[q];
-      X[r * T + c] = acc;
-    }
-    __syncthreads();
-  }
-}
-
-__device__ __forceinline__ double load_W(const HvpParams &h, int row, int col) {
+__device__ __forceinline__ double load_W(const SegParams &h, int row, int col) {
   if (col >= h.N) return 0.0;
   if (h.ident_j0 >= 0) return row == h.ident_j0 + col ? 1.0 : 0.0;
   return h.W[(long long)row * h.ldw + col];
 }
 
-__device__ __forceinline__ long long hw_index(const HvpParams &h, int row, int col) {
+__device__ __forceinline__ long long hw_index(const SegParams &h, int row, int col) {
   return h.transposed ? (long long)col * h.ldhw + row : (long long)row * h.ldhw + col;
 }
 
-// forward L sweep with the SpMul fused into the right-hand side:
-// row r of -B = -(G_p W)[r] is formed on the fly
-template <int T>
-__device__ __forceinline__ void sweep_L_spmul(const HvpParams &h, double *__restrict__ X, int col0) {
-  const int c = threadIdx.x % T;
-  const int slot = threadIdx.x / T;
-  constexpr int nslots = kThreads / T;
-  const int col = col0 + c;
-  const DSweep &S = h.L;
-  for (int lv = 0; lv < S.nlev; ++lv) {
-    const int beg = S.lev_ptr[lv], end = S.lev_ptr[lv + 1];
-    for (int q = beg + slot; q < end; q += nslots) {
-      const int r = S.rows[q];
-      double acc = 0.0;
-      const int g0 = h.gp_rptr[r], g1 = h.gp_rptr[r + 1];
-      for (int e = g0; e < g1; ++e) acc -= h.gp_val[e] * load_W(h, h.gp_col[e], col);
-      const int e0 = S.rptr[q], e1 = S.rptr[q + 1];
-      for (int e = e0; e < e1; ++e) acc -= S.val[e] * X[S.col[e] * T + c];
-      X[r * T + c] = acc;
+// ----------------------------------------------------------------------------
+// Block segments.  One CTA = (block, 32 columns), 512 threads: one warp per
+// row, one lane per column.  The block's X tile (rows x 32 columns) AND its
+// sweep structure (levels, rows, entries, coefficients) are staged in shared
+// memory, so a row's dependency chain is shared-memory only; the coefficient
+// and index reads are warp-uniform broadcasts and the X gathers are 256 B
+// contiguous (conflict-free).  External entries (separator rows of Z / P in
+// the backward sweeps) are read from L2/HBM.
+// ----------------------------------------------------------------------------
+constexpr int kSegThreads = 512;
+constexpr int kSegC = 32;   // columns of the single-RHS (lambda) path
+
+struct SegStage {  // shared-memory carve-up of one block sweep
+  double *X, *dinv;
+  double2 *ent;     // per entry: (coefficient, local dependency index as a bit-cast integer)
+  int *order, *rptr, *lvl;
+  int nq, ne, nlev;
+};
+
+// Stage a block's sweep structure (levels, rows, entries, pivots) in shared
+// memory behind an X tile of `nrx` rows x C columns.
+__device__ __forceinline__ SegStage stage_seg(const DSeg &S, const double *__restrict__ val,
+                                              const double *__restrict__ dinv, int seg, int nrx, int C, double *sm) {
+  SegStage t;
+  const int l0 = S.seg_lvl[seg], l1 = S.seg_lvl[seg + 1];
+  t.nlev = l1 - l0 - 1;
+  const int qb = S.lvl_ptr[l0];
+  t.nq = S.lvl_ptr[l1 - 1] - qb;
+  const int eb = S.rptr[qb];
+  t.ne = S.rptr[qb + t.nq] - eb;
+  t.X = sm;
+  t.ent = reinterpret_cast<double2 *>(t.X + (size_t)nrx * C);
+  t.dinv = reinterpret_cast<double *>(t.ent + t.ne);
+  t.order = reinterpret_cast<int *>(t.dinv + t.nq);
+  t.rptr = t.order + t.nq;
+  t.lvl = t.rptr + t.nq + 1;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < t.ne; i += blockDim.x)
+    t.ent[i] = make_double2(val[eb + i], __longlong_as_double((long long)S.dep[eb + i]));
+  for (int i = threadIdx.x; i < t.nq; i += blockDim.x) {
+    t.order[i] = S.order[qb + i];
+    t.dinv[i] = dinv ? dinv[qb + i] : 1.0;
+  }
+  for (int i = threadIdx.x; i <= t.nq; i += blockDim.x) t.rptr[i] = S.rptr[qb + i] - eb;
+  for (int i = threadIdx.x; i <= t.nlev; i += blockDim.x) t.lvl[i] = S.lvl_ptr[l0 + i] - qb;
+  return t;
+}
+
+// bytes of shared memory stage_seg needs for a block
+__host__ __device__ inline size_t seg_smem_bytes(int nrx, int nq, int ne, int nlev, int C) {
+  return (size_t)nrx * C * 8 + (size_t)ne * 16 + (size_t)nq * 8 + (size_t)nq * 4 + (size_t)(nq + 1) * 4 +
+         (size_t)(nlev + 1) * 4 + 16;
+}
+
+template <int CPL>
+__device__ __forceinline__ void ldx(const double *p, double (&x)[CPL]) {
+  if constexpr (CPL == 1) {
+    x[0] = p[0];
+  } else {
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2) {
+      const double2 v = *reinterpret_cast<const double2 *>(p + i);
+      x[i] = v.x;
+      x[i + 1] = v.y;
+    }
+  }
+}
+template <int CPL>
+__device__ __forceinline__ void stx(double *p, const double (&x)[CPL]) {
+  if constexpr (CPL == 1) {
+    p[0] = x[0];
+  } else {
+#pragma unroll
+    for (int i = 0; i < CPL; i += 2) *reinterpret_cast<double2 *>(p + i) = make_double2(x[i], x[i + 1]);
+  }
+}
+
+// One sweep over a block, level by level, one warp per row, CPL columns per
+// lane (32 * CPL columns per CTA).  All dependencies are in shared memory
+// (the block's rows and the staged separator rows it depends on).
+template <int CPL>
+__device__ __forceinline__ void seg_sweep(const SegStage &t, bool use_dinv, long long *rowclk = nullptr) {
+  constexpr int C = 32 * CPL;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double *Xl = t.X + lane * CPL;
+  // t.lvl holds super-level x warp boundaries: warp w of super-level s owns
+  // rows [lvl[s*nw + w], lvl[s*nw + w + 1]) in dependency order (no sync needed
+  // inside a warp: every lane only touches its own columns)
+  const int nsl = t.nlev / nw;
+  for (int sl = 0; sl < nsl; ++sl) {
+    const int q1 = t.lvl[sl * nw + warp + 1];
+    for (int q = t.lvl[sl * nw + warp]; q < q1; ++q) {
+      if (rowclk && lane == 0 && q < 1000) {
+        long long tt;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(tt));
+        rowclk[2 * q] = tt;
+        rowclk[2 * q + 1] = (t.rptr[q + 1] - t.rptr[q]) + 1000 * sl + 100000 * warp;
+      }
+      const int a = t.order[q];
+      int e = t.rptr[q];
+      const int e1 = t.rptr[q + 1];
+      double s0[CPL], s1[CPL];
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) s0[i] = s1[i] = 0.0;
+      for (; e + 4 <= e1; e += 4) {
+        const double2 p0 = t.ent[e], p1 = t.ent[e + 1], p2 = t.ent[e + 2], p3 = t.ent[e + 3];
+        double x0[CPL], x1[CPL], x2[CPL], x3[CPL];
+        ldx<CPL>(Xl + (int)__double_as_longlong(p0.y) * C, x0);
+        ldx<CPL>(Xl + (int)__double_as_longlong(p1.y) * C, x1);
+        ldx<CPL>(Xl + (int)__double_as_longlong(p2.y) * C, x2);
+        ldx<CPL>(Xl + (int)__double_as_longlong(p3.y) * C, x3);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+          s0[i] = fma(p0.x, x0[i], s0[i]);
+          s1[i] = fma(p1.x, x1[i], s1[i]);
+          s0[i] = fma(p2.x, x2[i], s0[i]);
+          s1[i] = fma(p3.x, x3[i], s1[i]);
+        }
+      }
+      for (; e < e1; ++e) {
+        const double2 p0 = t.ent[e];
+        double x0[CPL];
+        ldx<CPL>(Xl + (int)__double_as_longlong(p0.y) * C, x0);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) s0[i] = fma(p0.x, x0[i], s0[i]);
+      }
+      double xa[CPL];
+      ldx<CPL>(Xl + a * C, xa);
+      const double d = t.dinv[q];
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        xa[i] -= s0[i] + s1[i];
+        if (use_dinv) xa[i] *= d;
+      }
+      stx<CPL>(const_cast<double *>(Xl) + a * C, xa);
     }
     __syncthreads();
   }
 }
 
-template <int T>
-__device__ __forceinline__ double delta_src(const HvpParams &h, const double *__restrict__ X1, int src, int c,
-                                            int col) {
-  if (src >= 0) return X1[src * T + c];
+enum : int {
+  MODE_L = 0,     // blocks:    rhs = -G_p W (SpMul fused), L sweep            -> Z
+  MODE_LU = 1,    // separator: rhs = -G_p W - L_sb Z_b, then S^-1             -> Z
+  MODE_U = 2,     // blocks:    U sweep                                        -> Z
+  MODE_UT = 3,    // blocks:    U^T sweep on -Y_x                              -> P
+  MODE_UTLT = 4,  // separator: -Y_x - U_bs^T P_b, then S^-T                   -> P
+  MODE_LT = 5     // blocks:    L^T sweep                                      -> P = Psi
+};
+
+__device__ __forceinline__ double rhs_gpw(const SegParams &h, int row, int col) {
+  double v = 0.0;
+  for (int e = h.gp_rptr[row]; e < h.gp_rptr[row + 1]; ++e) v -= h.gp_val[e] * load_W(h, h.gp_col[e], col);
+  return v;
+}
+
+// Block kernel: one CTA = (block, 32 * CPL columns), 512 threads.
+template <int CPL>
+__global__ void __launch_bounds__(kSegThreads) k_seg(SegParams h, int mode) {
+  constexpr int C = 32 * CPL;
+  extern __shared__ double sm[];
+  const int seg = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int col0 = blockIdx.y * C;
+  const int r0 = h.seg_row_off[seg], nr = h.seg_row_off[seg + 1] - r0;
+  double *G = mode <= MODE_U ? h.Z : h.P;
+  const bool fwd = mode == MODE_L || mode == MODE_UT;
+  const DSeg &S = fwd ? h.fwd : h.bwd;
+  const double *val = mode == MODE_L ? h.vL : mode == MODE_U ? h.vU : mode == MODE_UT ? h.vUt : h.vLt;
+  const double *dinv = mode == MODE_U ? h.dinv_bwd : mode == MODE_UT ? h.dinv_fwd : nullptr;
+  const int x0 = S.ext_off[seg], nxr = S.ext_off[seg + 1] - x0;
+  long long tk[4] = {0, 0, 0, 0};
+  const bool instr = (h.debug & 8) && h.dbg && threadIdx.x == 0;
+  if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[0]));
+  const SegStage t = stage_seg(S, val, dinv, seg, nr + nxr, C, sm);
+  constexpr int CH = C / 2;  // 16-byte chunks per row
+  if (mode == MODE_L) {
+    for (int i = threadIdx.x; i < nr * C; i += blockDim.x) t.X[i] = 0.0;
+    __syncthreads();
+    // -G_p W only on the rows that have G_p entries (rows adjacent to generator buses)
+    for (int k = h.blk_gp_ptr[seg] + warp; k < h.blk_gp_ptr[seg + 1]; k += nw) {
+      const int a = h.blk_gp_loc[k];
+      const int row = h.row_global[r0 + a];
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) t.X[a * C + lane * CPL + i] = rhs_gpw(h, row, col0 + lane * CPL + i);
+    }
+  } else {
+    // asynchronous 16 B copies global -> shared (LDGSTS)
+    for (int i = threadIdx.x; i < nr * CH; i += blockDim.x) {
+      const int a = i / CH, ch = i % CH;
+      const double *src = G + (long long)h.row_global[r0 + a] * h.ld + col0 + 2 * ch;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(t.X + a * C + 2 * ch);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    }
+  }
+  // separator rows this block depends on (backward sweeps), staged after the block's rows
+  for (int i = threadIdx.x; i < nxr * CH; i += blockDim.x) {
+    const int k = i / CH, ch = i % CH;
+    const double *src = G + (long long)S.ext_rows[x0 + k] * h.ld + col0 + 2 * ch;
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(t.X + (nr + k) * C + 2 * ch);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[1]));
+  seg_sweep<CPL>(t, dinv != nullptr,
+                 ((h.debug & 64) && h.dbg && blockIdx.x == 0 && blockIdx.y == 0) ? h.dbg + 6 * 60000 : nullptr);
+  if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[2]));
+  for (int i = threadIdx.x; i < nr * CH; i += blockDim.x) {
+    const int a = i / CH, ch = i % CH;
+    *reinterpret_cast<double2 *>(G + (long long)h.row_global[r0 + a] * h.ld + col0 + 2 * ch) =
+        *reinterpret_cast<const double2 *>(t.X + a * C + 2 * ch);
+  }
+  if (instr) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[3]));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    long long *d = h.dbg + 6 * (mode * 65536 / 6 / 6 * 0 + blockIdx.y * gridDim.x + blockIdx.x);
+    d[0] = tk[0]; d[1] = tk[1]; d[2] = tk[2]; d[3] = tk[3]; d[4] = smid; d[5] = t.nlev / (blockDim.x >> 5);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Separator segment: (1) k_sep_gather forms the
+// right-hand side of the separator rows, rhs - (block columns) x (block rows),
+// fully parallel (warp per separator row, lane per column); (2) k_sep_gemm
+// applies the dense inverse S^-1 (S = L_ss U_ss, inverted once per state by
+// k_sep_inverse): the separator's ~100-level dependency chain becomes one
+// [ns x ns] x [ns x N] fp64 GEMM, written straight into the separator rows.
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) {
+  const int lane = threadIdx.x & 31;
+  const int qoff = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const int col = blockIdx.y * 32 + lane;
+  const int seg = h.nblk;
+  const int qb = h.fwd.lvl_ptr[h.fwd.seg_lvl[seg]], qe = h.fwd.lvl_ptr[h.fwd.seg_lvl[seg + 1] - 1];
+  const int q = qb + qoff;
+  if (q >= qe) return;
+  double *G = mode == MODE_LU ? h.Z : h.P;
+  const double *val = mode == MODE_LU ? h.vL : h.vUt;
+  const int a = h.fwd.order[q];
+  const int row = h.row_global[h.sep_off + a];
+  const double v0 = mode == MODE_LU ? rhs_gpw(h, row, col) : G[(long long)row * h.ld + col];
+  int e = h.fwd.rptr[q];
+  const int ex = h.fwd.rext[q];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (; e + 4 <= ex; e += 4) {
+    const int d0 = h.fwd.dep[e], d1 = h.fwd.dep[e + 1], d2 = h.fwd.dep[e + 2], d3 = h.fwd.dep[e + 3];
+    const double x0 = G[(long long)d0 * h.ld + col], x1 = G[(long long)d1 * h.ld + col];
+    const double x2 = G[(long long)d2 * h.ld + col], x3 = G[(long long)d3 * h.ld + col];
+    s0 = fma(val[e], x0, s0);
+    s1 = fma(val[e + 1], x1, s1);
+    s2 = fma(val[e + 2], x2, s2);
+    s3 = fma(val[e + 3], x3, s3);
+  }
+  for (; e < ex; ++e) s0 = fma(val[e], G[(long long)h.fwd.dep[e] * h.ld + col], s0);
+  h.Tsep[(long long)a * h.ld + col] = v0 - ((s0 + s1) + (s2 + s3));
+}
+
+// C[m][n] = sum_k M[m][k] T[k][n] for the separator rows m (written to
+// G[row_global[sep_off + m]][n]); 64x64 output tile per CTA, 4x4 per thread,
+// k in tiles of 16 staged in shared memory.  Fixed k order: deterministic.
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+__global__ void __launch_bounds__(256) k_sep_gemm(SegParams h, int mode) {
+  __shared__ double As[GBK][GBM + 1];
+  __shared__ double Bs[GBK][GBN];
+  const int ns = h.ns;
+  const double *M = mode == MODE_LU ? h.Sinv : h.SinvT;
+  double *G = mode == MODE_LU ? h.Z : h.P;
+  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  for (int k0 = 0; k0 < ns; k0 += GBK) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int idx = threadIdx.x + r * 256;  // 1024 = 64 x 16
+      const int mm = idx / GBK, kk = idx % GBK;
+      const int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < ns && gk < ns) ? M[(long long)gm * ns + gk] : 0.0;
+      const int kb = idx / GBN, nn = idx % GBN;
+      const int gk2 = k0 + kb;
+      Bs[kb][nn] = (gk2 < ns && n0 + nn < h.ld) ? h.Tsep[(long long)gk2 * h.ld + n0 + nn] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= ns) continue;
+    double *out = G + (long long)h.row_global[h.sep_off + gm] * h.ld + n0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (n0 + tx + 16 * j < h.ld) out[tx + 16 * j] = acc[i][j];
+  }
+}
+
+// Dense inverse of the separator block S = L_ss U_ss, column by column: one
+// warp per column j solves L_ss U_ss x = e_j by forward then backward
+// substitution over the separator's local entries in level order.  Writes
+// S^-1 (row-major) and its transpose.  Once per state.
+__global__ void __launch_bounds__(kThreads) k_sep_inverse(SegParams h, double *Sinv, double *SinvT) {
+  extern __shared__ double sx[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kThreads / 32;
+  const int j = blockIdx.x * nw + warp;  // column
+  if (j >= h.ns) return;
+  const int ns = h.ns, seg = h.nblk;
+  double *x = sx + warp * ns;
+  for (int r = lane; r < ns; r += 32) x[r] = r == j ? 1.0 : 0.0;
+  __syncwarp();
+  for (int which = 0; which < 2; ++which) {
+    const DSeg &S = which == 0 ? h.fwd : h.bwd;
+    const double *val = which == 0 ? h.vL : h.vU;
+    const int l0 = S.seg_lvl[seg], l1 = S.seg_lvl[seg + 1] - 1;
+    for (int l = l0; l < l1; ++l) {
+      for (int q = S.lvl_ptr[l] + lane; q < S.lvl_ptr[l + 1]; q += 32) {
+        const int a = S.order[q];
+        double v = x[a];
+        for (int e = S.rext[q]; e < S.rptr[q + 1]; ++e) v -= val[e] * x[S.dep[e]];
+        if (which == 1) v *= h.dinv_bwd[q];
+        x[a] = v;
+      }
+      __syncwarp();
+    }
+  }
+  for (int r = lane; r < ns; r += 32) {
+    Sinv[(long long)r * ns + j] = x[r];
+    SinvT[(long long)j * ns + r] = x[r];
+  }
+}
+
+// ============================================================================
+// BatchTensorProjection (PAPER.md:550-566, 602; Eq. so_model PAPER.md:497-513)
+// by hand-written forward-over-reverse on the line graph with a hoisted tape:
+// per line (K, a_i, a_j, m) is column independent (k_coefs, once per state and
+// lambda); per column it is 8 FMAs per line end.  Bus-centric gather ("edges
+// then nodes") without atomics.  Thread = (bus, column).
+// ============================================================================
+
+__device__ __forceinline__ double delta_src(const SegParams &h, int src, int col) {
+  if (src >= 0) return h.Z[(long long)src * h.ld + col];
   if (src == -1) return 0.0;
   return load_W(h, -(src + 2), col);
 }
 
-// BatchTensorProjection (PAPER.md:550-566, 602; Eq. so_model PAPER.md:497-513)
-// by hand-written forward-over-reverse on the line graph, hoisted tape:
-// per line (K, a_i, a_j, m) is column independent (computed once per state
-// and lambda by k_coefs); per column it is 8 FMAs per line end.  Bus-centric
-// gather ("edges then nodes") without atomics.
-template <int T>
-__device__ __forceinline__ void tensor_projection(const HvpParams &h, const double *__restrict__ X1,
-                                                  double *__restrict__ X2, int col0, double *s_ref) {
-  const int c = threadIdx.x % T;
-  const int slot = threadIdx.x / T;
-  constexpr int nslots = kThreads / T;
-  const int col = col0 + c;
-  // s = grad P_ref . delta per column (REF objective rank-1 term, R22)
-  if (slot == 0) {
-    double s = 0.0;
+// one warp per bus, one lane per column (32 columns per CTA column chunk):
+// every index / coefficient load is warp-uniform, every Z load is 256 B.
+__global__ void __launch_bounds__(kThreads) k_for(SegParams h) {
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  const int col = blockIdx.y * 32 + lane;
+  if (b >= h.n_bus) return;
+  const double dth_b = delta_src(h, h.dth_src[b], col);
+  const double dv_b = delta_src(h, h.dv_src[b], col);
+  double yth = 0.0;
+  double yv = h.dcoef[b] * dv_b;
+  const int s0 = h.bl_ptr[b], s1 = h.bl_ptr[b + 1];
+#pragma unroll 2
+  for (int s = s0; s < s1; ++s) {
+    const double4 k = h.coef[h.bl_line[s]];
+    const double dth_o = delta_src(h, h.o_dth_src[s], col);
+    const double dv_o = delta_src(h, h.o_dv_src[s], col);
+    if (h.bl_end[s] == 0) {  // b is the from-end i
+      const double D = dth_b - dth_o;
+      yth += k.x * D + k.y * dv_b + k.z * dv_o;
+      yv += k.y * D + k.w * dv_o;
+    } else {                 // b is the to-end j
+      const double D = dth_o - dth_b;
+      yth -= k.x * D + k.y * dv_o + k.z * dv_b;
+      yv += k.z * D + k.w * dv_o;
+    }
+  }
+  // REF objective rank-1 term f''(Pg_ref) (grad P_ref . delta) grad P_ref (R22):
+  // only the buses of {ref} u A(ref) carry a nonzero grad P_ref entry
+  const double rt = h.refg_th[b], rv = h.refg_v[b];
+  if (rt != 0.0 || rv != 0.0) {
+    double sref = 0.0;
     for (int q = 0; q < h.n_near_ref; ++q) {
-      const int b = h.near_ref[q];
-      s += h.refg_th[b] * delta_src<T>(h, X1, h.dth_src[b], c, col) +
-           h.refg_v[b] * delta_src<T>(h, X1, h.dv_src[b], c, col);
+      const int o = h.near_ref[q];
+      sref += h.refg_th[o] * delta_src(h, h.dth_src[o], col) + h.refg_v[o] * delta_src(h, h.dv_src[o], col);
     }
-    s_ref[c] = h.f2ref * s;
+    sref *= h.f2ref;
+    yth += sref * rt;
+    yv += sref * rv;
   }
-  __syncthreads();
-  const double sr = s_ref[c];
-  for (int b = slot; b < h.n_bus; b += nslots) {
-    const double dth_b = delta_src<T>(h, X1, h.dth_src[b], c, col);
-    const double dv_b = delta_src<T>(h, X1, h.dv_src[b], c, col);
-    double yth = sr * h.refg_th[b];
-    double yv = h.dcoef[b] * dv_b + sr * h.refg_v[b];
-    const int s0 = h.bl_ptr[b], s1 = h.bl_ptr[b + 1];
-    for (int s = s0; s < s1; ++s) {
-      const double4 k = h.coef[h.bl_line[s]];
-      const double dth_o = delta_src<T>(h, X1, h.o_dth_src[s], c, col);
-      const double dv_o = delta_src<T>(h, X1, h.o_dv_src[s], c, col);
-      if (h.bl_end[s] == 0) {  // b is the from-end i
-        const double D = dth_b - dth_o;
-        yth += k.x * D + k.y * dv_b + k.z * dv_o;
-        yv += k.y * D + k.w * dv_o;
-      } else {                 // b is the to-end j
-        const double D = dth_o - dth_b;
-        yth -= k.x * D + k.y * dv_o + k.z * dv_b;
-        yv += k.z * D + k.w * dv_o;
-      }
-    }
-    const int dt = h.yth_dst[b];
-    if (dt >= 0) X2[dt * T + c] = -yth;
-    const int dv = h.yv_dst[b];
-    if (dv >= 0) {
-      X2[dv * T + c] = -yv;
-    } else if (col < h.N) {
-      h.HW[hw_index(h, -(dv + 2), col)] = yv;
-    }
-    const int pg = h.pg_p[b];
-    if (pg >= 0 && col < h.N) h.HW[hw_index(h, pg, col)] = 2.0 * h.c2b[b] * load_W(h, pg, col);
+  const int dt = h.yth_dst[b];
+  if (dt >= 0) h.P[(long long)dt * h.ld + col] = -yth;
+  const int dv = h.yv_dst[b];
+  if (dv >= 0) {
+    h.P[(long long)dv * h.ld + col] = -yv;
+  } else if (col < h.N) {
+    h.HW[hw_index(h, -(dv + 2), col)] = yv;
   }
-  __syncthreads();
+  const int pg = h.pg_p[b];
+  if (pg >= 0 && col < h.N) h.HW[hw_index(h, pg, col)] = 2.0 * h.c2b[b] * load_W(h, pg, col);
 }
 
-// SpMulAdd HW = Y_p + G_p^T Psi, by p column (CSC of G_p)
-template <int T>
-__device__ __forceinline__ void spmuladd(const HvpParams &h, const double *__restrict__ X2, int col0) {
-  const int c = threadIdx.x % T;
-  const int slot = threadIdx.x / T;
-  constexpr int nslots = kThreads / T;
-  const int col = col0 + c;
-  if (col >= h.N) return;
-  for (int cp = slot; cp < h.n_p; cp += nslots) {
-    const long long idx = hw_index(h, cp, col);
-    double acc = h.HW[idx];
-    for (int q = h.gpc_ptr[cp]; q < h.gpc_ptr[cp + 1]; ++q) acc += h.gpc_val[q] * X2[h.gpc_row[q] * T + c];
-    h.HW[idx] = acc;
-  }
+// SpMulAdd HW = Y_p + G_p^T Psi, thread = (p row, column)
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
+  const int c = threadIdx.x % C;
+  const int cp = blockIdx.x * (kThreads / C) + threadIdx.x / C;
+  const int col = blockIdx.y * C + c;
+  if (cp >= h.n_p || col >= h.N) return;
+  const long long idx = hw_index(h, cp, col);
+  double acc = h.HW[idx];
+  for (int q = h.gpc_ptr[cp]; q < h.gpc_ptr[cp + 1]; ++q) acc += h.gpc_val[q] * h.P[(long long)h.gpc_row[q] * h.ld + col];
+  h.HW[idx] = acc;
 }
 
-// The fused HVP: one CTA per column tile runs Alg. 2 end to end
-// -- no stage boundaries, no host syncs (cf. the two
-// explicit synchronizations of PAPER.md:798-805).  PHASES selects a subset
-// for the staged (per-stage timing / parity) mode.
-template <int T>
-__global__ void __launch_bounds__(kThreads) k_hvp(HvpParams h, int phases) {
-  __shared__ double s_ref[T];
-  const int tile = blockIdx.x;
-  const int col0 = tile * T;
-  double *X1 = h.X1 + (long long)tile * h.n_x * T;
-  double *X2 = h.X2 + (long long)tile * h.n_x * T;
-  if (phases & PH_L) sweep_L_spmul<T>(h, X1, col0);
-  if (phases & PH_U) sweep_inplace<T, true>(h.U, X1);
-  if (phases & PH_FOR) tensor_projection<T>(h, X1, X2, col0, s_ref);
-  if (phases & PH_UT) sweep_inplace<T, true>(h.Ut, X2);
-  if (phases & PH_LT) sweep_inplace<T, false>(h.Lt, X2);
-  if (phases & PH_MULADD) spmuladd<T>(h, X2, col0);
+// natural-order copy of a permuted block: out[k][col] = sgn * X[pinv[k]][col]
+__global__ void k_unpermute(int n_x, int N, int ld, const int *pinv, const double *X, double sgn, double *out,
+                            long long ldo) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)n_x * N) return;
+  const int k = (int)(idx / N), col = (int)(idx % N);
+  out[(long long)k * ldo + col] = sgn * X[(long long)pinv[k] * ld + col];
 }
 
 // ============================================================================
 // first-order adjoint + reduced gradient, single column
 // ============================================================================
 
-// rhs of J^T lambda = -grad_x f:  X'[pinv[k]] = -mu_ref * dP_ref/dx_k
 __global__ void k_grad_rhs(int n_x, const int *x_bus, const int *x_kind, const int *pinv, const double *refg_th,
                            const double *refg_v, const double *scal, double *X) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n_x) return;
   const int b = x_bus[k];
   const double g = x_kind[k] == RH_KIND_THETA ? refg_th[b] : refg_v[b];
-  X[pinv[k]] = -scal[2] * g;
+  X[(long long)pinv[k] * 32] = -scal[2] * g;
 }
-
-__global__ void __launch_bounds__(kThreads) k_solve_T1(DSweep Ut, DSweep Lt, double *X) {
-  sweep_inplace<1, true>(Ut, X);
-  sweep_inplace<1, false>(Lt, X);
-}
-
 __global__ void k_grad_out(int n_x, int n_p, const int *pinv, const int *p_bus, const int *p_kind,
                            const double *c2b, const double *c1b, const double *p, const double *refg_v,
                            const double *scal, const int *gpc_ptr, const int *gpc_row, const double *gpc_val,
                            const double *X, double *lam, double *grad) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n_x) lam[k] = X[pinv[k]];
+  if (k < n_x) lam[k] = X[(long long)pinv[k] * 32];
   if (k < n_p) {
     const int b = p_bus[k];
     double acc = p_kind[k] == RH_KIND_PG ? 2.0 * c2b[b] * p[k] + c1b[b] : scal[2] * refg_v[b];
-    for (int q = gpc_ptr[k]; q < gpc_ptr[k + 1]; ++q) acc += gpc_val[q] * X[gpc_row[q]];
+    for (int q = gpc_ptr[k]; q < gpc_ptr[k + 1]; ++q) acc += gpc_val[q] * X[(long long)gpc_row[q] * 32];
     grad[k] = acc;
   }
 }
@@ -488,16 +824,6 @@ __global__ void k_coefs(int m, int n_bus, const int *lf, const int *lt, const do
   if (l < n_bus) dcoef[l] = 2.0 * (G_ii[l] * muP[l] - B_ii[l] * muQ[l]);
 }
 
-// natural-order copy of a tiled block: out[k][col] = sgn * X[tile][pinv[k]][c]
-__global__ void k_untile(int n_x, int N, int T, const int *pinv, const double *X, double sgn, double *out,
-                         long long ld) {
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)n_x * N) return;
-  const int k = (int)(idx / N), col = (int)(idx % N);
-  const int tile = col / T, c = col % T;
-  out[(long long)k * ld + col] = sgn * X[((long long)tile * n_x + pinv[k]) * T + c];
-}
-
 // ============================================================================
 // context
 // ============================================================================
@@ -521,12 +847,8 @@ T *dalloc(size_t n, std::vector<void *> &pool) {
   return p;
 }
 
-struct DevSweepStore {
-  DSweep d{};
-  int *src = nullptr, *diag_src = nullptr;
-  int nnz = 0, n = 0;
-  double *dinv_mut = nullptr, *val_mut = nullptr;
-};
+constexpr int C_FOR = 16;   // columns per CTA, tensor projection / SpMulAdd
+constexpr int kSmemMax = 220 * 1024;
 
 }  // namespace
 
@@ -538,42 +860,53 @@ struct rh_ctx {
   Analysis A;
   std::vector<void *> pool;   // grid-lifetime device buffers
   long long launches = 0;
-  int epoch = 0;
   bool timing = false;
-  float stage_ms[6] = {0, 0, 0, 0, 0, 0};
+  float stage_ms[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
 
   // device grid + analysis
   int *bus_type, *lf, *lt, *bl_ptr, *bl_line, *bl_other, *bl_end, *has_gen;
   double *G_ii, *B_ii, *Pd, *Qd, *G_ft, *B_ft, *G_tf, *B_tf, *c2b, *c1b, *c0b;
   int *x_bus, *x_kind, *p_bus, *p_kind, *th_x, *v_x, *pinv;
-  int *F_rowptr, *F_col, *F_diag, *fact_order;
+  int *F_rowptr, *F_diag;
   double *F_val;
-  int *flags, *ticket, *status;
+  int *status;
   int *diag_pos, *slot_pos, *gp_rptr, *gp_col, *gp_self_pos, *gp_pg_pos, *gp_slot_pos;
   double *gp_val;
   int *gpc_ptr, *gpc_pos, *gpc_row;
   double *gpc_val;
-  DevSweepStore sL, sU, sUt, sLt;
   int *dth_src, *dv_src, *yth_dst, *yv_dst, *o_dth_src, *o_dv_src, *pg_p, *near_ref;
+  // segments
+  int *seg_row_off, *row_global;
+  DSeg dfwd, dbwd;
+  int *fwd_src_a, *fwd_src_b, *bwd_src_a, *bwd_src_b, *fwd_dsrc, *bwd_dsrc;
+  double *vL, *vUt, *vU, *vLt, *dinv_fwd, *dinv_bwd;
+  int nnz_fwd = 0, nnz_bwd = 0;
+  // refactorization schedule
+  int *blk_fo_off, *fo, *ks_ptr, *ks_pos, *ks_k, *ks_kf, *ks_ulen, *ks_tgt, *tgt;
+  int *sb_src, *sb_diag, *sb_lptr, *sb_lslot, *sb_uptr, *sb_trip;
+  double *dinv_rows, *rowmax;
+  double *Sinv = nullptr, *SinvT = nullptr;
+  size_t smem_fact_blk = 0, smem_fact_sep = 0, smem_seg_blk = 0, smem_seg_blk1 = 0;
+  int cpl = 2;   // columns per lane of the HVP block kernels (32 * cpl columns per CTA)
   // state
   double *x, *p, *th, *v, *pgb, *P, *Q, *g, *refg_th, *refg_v, *scal;
   double2 *cs;
   double *lam, *muP, *muQ, *dcoef, *X1col;
   double4 *coef;
   // workspace
-  double *X1 = nullptr, *X2 = nullptr;
-  size_t ws_elems = 0;
-  double *Wtmp = nullptr;
-  size_t wtmp_elems = 0;
+  double *Zb = nullptr, *Pb = nullptr, *Tsep = nullptr;
+  size_t ws_elems = 0, tsep_elems = 0;
+  int *blk_gp_ptr, *blk_gp_loc;
+  int *fact_seg_lvl, *fact_lvl_ptr, *fact_order;
 
   void free_all() {
     for (void *q : pool) cudaFree(q);
     pool.clear();
-    if (X1) cudaFree(X1);
-    if (X2) cudaFree(X2);
-    if (Wtmp) cudaFree(Wtmp);
-    X1 = X2 = Wtmp = nullptr;
-    ws_elems = wtmp_elems = 0;
+    if (Zb) cudaFree(Zb);
+    if (Pb) cudaFree(Pb);
+    if (Tsep) cudaFree(Tsep);
+    Zb = Pb = Tsep = nullptr;
+    ws_elems = tsep_elems = 0;
   }
 };
 
@@ -599,6 +932,20 @@ int fail(rh_ctx *c, int code, const std::string &msg) {
 
 inline int nblk(long long n, int t = kThreads) { return (int)((n + t - 1) / t); }
 
+size_t seg_smem_max(const Analysis &A, int C) {
+  size_t m = 0;
+  for (const SegSweep *S : {&A.fwd, &A.bwd}) {
+    for (int s = 0; s < A.nblk; ++s) {
+      const int l0 = S->seg_lvl[s], l1 = S->seg_lvl[s + 1];
+      const int qb = S->lvl_ptr[l0], qe = S->lvl_ptr[l1 - 1];
+      const int ne = S->rptr[qe] - S->rptr[qb];
+      const int nrx = A.seg_row_off[s + 1] - A.seg_row_off[s] + S->ext_off[s + 1] - S->ext_off[s];
+      m = std::max(m, seg_smem_bytes(nrx, qe - qb, ne, l1 - l0 - 1, C));
+    }
+  }
+  return m;
+}
+
 int upload(rh_ctx *c) {
   const Analysis &A = c->A;
   auto &P = c->pool;
@@ -611,13 +958,45 @@ int upload(rh_ctx *c) {
   UP(G_tf, A.G_tf); UP(B_tf, A.B_tf); UP(c2b, A.c2b); UP(c1b, A.c1b); UP(c0b, A.c0b);
   UP(x_bus, A.x_bus); UP(x_kind, A.x_kind); UP(p_bus, A.p_bus); UP(p_kind, A.p_kind);
   UP(th_x, A.th_x); UP(v_x, A.v_x); UP(pinv, A.pinv);
-  UP(F_rowptr, A.F_rowptr); UP(F_col, A.F_col); UP(F_diag, A.F_diag); UP(fact_order, A.fact_order);
+  UP(F_rowptr, A.F_rowptr); UP(F_diag, A.F_diag);
   UP(diag_pos, A.diag_pos); UP(slot_pos, A.slot_pos); UP(gp_rptr, A.gp_rptr); UP(gp_col, A.gp_col);
   UP(gp_self_pos, A.gp_self_pos); UP(gp_pg_pos, A.gp_pg_pos); UP(gp_slot_pos, A.gp_slot_pos);
   UP(gpc_ptr, A.gpc_ptr); UP(gpc_pos, A.gpc_pos); UP(gpc_row, A.gpc_row);
   UP(dth_src, A.dth_src); UP(dv_src, A.dv_src); UP(yth_dst, A.yth_dst); UP(yv_dst, A.yv_dst);
   UP(pg_p, A.pg_p); UP(near_ref, A.near_ref);
+  UP(seg_row_off, A.seg_row_off); UP(row_global, A.row_global);
+  UP(fact_seg_lvl, A.fact_seg_lvl); UP(fact_lvl_ptr, A.fact_lvl_ptr); UP(fact_order, A.fact_order);
+  UP(blk_gp_ptr, A.blk_gp_ptr); UP(blk_gp_loc, A.blk_gp_loc);
+  UP(fwd_src_a, A.fwd.src_a); UP(fwd_src_b, A.fwd.src_b); UP(bwd_src_a, A.bwd.src_a); UP(bwd_src_b, A.bwd.src_b);
+  UP(fwd_dsrc, A.fwd.dsrc); UP(bwd_dsrc, A.bwd.dsrc);
+  UP(blk_fo_off, A.blk_fo_off); UP(fo, A.fo); UP(ks_ptr, A.ks_ptr); UP(ks_pos, A.ks_pos); UP(ks_k, A.ks_k);
+  UP(ks_kf, A.ks_kf); UP(ks_ulen, A.ks_ulen); UP(ks_tgt, A.ks_tgt); UP(tgt, A.tgt);
+  UP(sb_src, A.sb_src); UP(sb_diag, A.sb_diag); UP(sb_lptr, A.sb_lptr); UP(sb_lslot, A.sb_lslot);
+  UP(sb_uptr, A.sb_uptr); UP(sb_trip, A.sb_trip);
 #undef UP
+  auto mkseg = [&](DSeg &D, const SegSweep &S) {
+    int *a, *b, *o, *r, *x, *d, *eo, *er;
+    chk(eo = dalloc_copy(S.ext_off, P));
+    chk(er = dalloc_copy(S.ext_rows, P));
+    D.ext_off = eo;
+    D.ext_rows = er;
+    chk(a = dalloc_copy(S.seg_lvl, P));
+    chk(b = dalloc_copy(S.lvl_ptr, P));
+    chk(o = dalloc_copy(S.order, P));
+    chk(r = dalloc_copy(S.rptr, P));
+    chk(x = dalloc_copy(S.rext, P));
+    chk(d = dalloc_copy(S.dep, P));
+    D.seg_lvl = a;
+    D.lvl_ptr = b;
+    D.order = o;
+    D.rptr = r;
+    D.rext = x;
+    D.dep = d;
+  };
+  mkseg(c->dfwd, A.fwd);
+  mkseg(c->dbwd, A.bwd);
+  c->nnz_fwd = (int)A.fwd.dep.size();
+  c->nnz_bwd = (int)A.bwd.dep.size();
   std::vector<int32_t> odth(2 * A.n_line), odv(2 * A.n_line);
   for (int s = 0; s < 2 * A.n_line; ++s) {
     odth[s] = A.dth_src[A.bl_other[s]];
@@ -626,41 +1005,18 @@ int upload(rh_ctx *c) {
   chk(c->o_dth_src = dalloc_copy(odth, P));
   chk(c->o_dv_src = dalloc_copy(odv, P));
   const int nx = A.n_x, np_ = A.n_p, nb = A.n_bus, m = A.n_line;
-  const size_t nF = A.F_col.size();
-  chk(c->F_val = dalloc<double>(nF, P));
-  chk(c->flags = dalloc<int>(nx, P));
-  chk(c->ticket = dalloc<int>(1, P));
+  chk(c->F_val = dalloc<double>(A.F_col.size(), P));
   chk(c->status = dalloc<int>(1, P));
   chk(c->gp_val = dalloc<double>(A.gp_col.size(), P));
   chk(c->gpc_val = dalloc<double>(A.gp_col.size(), P));
-  auto mk = [&](DevSweepStore &S, const Sweep &H) {
-    S.n = nx;
-    S.nnz = (int)H.col.size();
-    S.d.nlev = H.nlev();
-    int *lp, *rw, *rp, *cl;
-    chk(lp = dalloc_copy(H.lev_ptr, P));
-    chk(rw = dalloc_copy(H.rows, P));
-    chk(rp = dalloc_copy(H.rptr, P));
-    chk(cl = dalloc_copy(H.col, P));
-    chk(S.src = dalloc_copy(H.src, P));
-    chk(S.diag_src = dalloc_copy(H.diag_src, P));
-    chk(S.val_mut = dalloc<double>(H.col.size(), P));
-    S.d.lev_ptr = lp;
-    S.d.rows = rw;
-    S.d.rptr = rp;
-    S.d.col = cl;
-    S.d.val = S.val_mut;
-    if (H.diag_src.empty() || H.diag_src[0] < 0) {
-      S.d.dinv = nullptr;
-    } else {
-      chk(S.dinv_mut = dalloc<double>(nx, P));
-      S.d.dinv = S.dinv_mut;
-    }
-  };
-  mk(c->sL, A.sL);
-  mk(c->sU, A.sU);
-  mk(c->sUt, A.sUt);
-  mk(c->sLt, A.sLt);
+  chk(c->vL = dalloc<double>(c->nnz_fwd, P));
+  chk(c->vUt = dalloc<double>(c->nnz_fwd, P));
+  chk(c->vU = dalloc<double>(c->nnz_bwd, P));
+  chk(c->vLt = dalloc<double>(c->nnz_bwd, P));
+  chk(c->dinv_fwd = dalloc<double>(nx, P));
+  chk(c->dinv_bwd = dalloc<double>(nx, P));
+  chk(c->dinv_rows = dalloc<double>(nx, P));
+  chk(c->rowmax = dalloc<double>(nx, P));
   chk(c->x = dalloc<double>(nx, P));
   chk(c->p = dalloc<double>(np_, P));
   chk(c->th = dalloc<double>(nb, P));
@@ -677,35 +1033,53 @@ int upload(rh_ctx *c) {
   chk(c->muP = dalloc<double>(nb, P));
   chk(c->muQ = dalloc<double>(nb, P));
   chk(c->dcoef = dalloc<double>(nb, P));
-  chk(c->X1col = dalloc<double>(nx, P));
+  chk(c->X1col = dalloc<double>((size_t)nx * kSegC, P));
   chk(c->coef = dalloc<double4>(m, P));
+  const size_t ns2 = (size_t)A.sep_rows * A.sep_rows;
+  chk(c->Sinv = dalloc<double>(ns2, P));
+  chk(c->SinvT = dalloc<double>(ns2, P));
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
-  cudaError_t e = cudaMemset(c->flags, 0, sizeof(int) * nx);
+  // shared-memory footprints
+  c->smem_fact_blk = (size_t)(A.max_blk_fnnz + A.rmax) * sizeof(double);
+  c->smem_fact_sep = std::max<size_t>(1, A.sb_src.size()) * sizeof(double);
+  c->smem_seg_blk = seg_smem_max(A, 32 * c->cpl);
+  c->smem_seg_blk1 = seg_smem_max(A, kSegC);
+  cudaFuncSetAttribute(k_fact_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  cudaFuncSetAttribute(k_fact_sep, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  cudaFuncSetAttribute(k_seg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  cudaFuncSetAttribute(k_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  cudaFuncSetAttribute(k_seg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  cudaFuncSetAttribute(k_sep_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(c, RH_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
-  c->epoch = 0;
   return RH_OK;
 }
 
-int pick_T(int N) {
-  // columns per CTA: keep >= ~148 CTAs when N allows (148 SMs), T in {1..32}
-  if (N >= 148 * 16) return 16;
-  if (N >= 148 * 8) return 8;
-  if (N >= 148 * 4) return 4;
-  if (N >= 148 * 2) return 2;
-  return 1;
+int ensure_tsep(rh_ctx *c, int ld) {
+  const size_t need = (size_t)ld * (size_t)std::max(1, c->A.sep_rows);
+  if (need <= c->tsep_elems) return RH_OK;
+  if (c->Tsep) cudaFree(c->Tsep);
+  c->Tsep = nullptr;
+  c->tsep_elems = 0;
+  if (cudaMalloc(&c->Tsep, need * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, RH_E_NOMEM, "workspace allocation failed");
+  }
+  c->tsep_elems = need;
+  return RH_OK;
 }
 
-int ensure_ws(rh_ctx *c, int N, int T) {
-  const size_t ntiles = (size_t)((N + T - 1) / T);
-  const size_t need = ntiles * T * (size_t)c->A.n_x;
+int ensure_ws(rh_ctx *c, int ld) {
+  const size_t need = (size_t)ld * (size_t)c->A.n_x;
+  if (int rc = ensure_tsep(c, ld)) return rc;
   if (need <= c->ws_elems) return RH_OK;
-  if (c->X1) cudaFree(c->X1);
-  if (c->X2) cudaFree(c->X2);
-  c->X1 = c->X2 = nullptr;
+  if (c->Zb) cudaFree(c->Zb);
+  if (c->Pb) cudaFree(c->Pb);
+  c->Zb = c->Pb = nullptr;
   c->ws_elems = 0;
-  if (cudaMalloc(&c->X1, need * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&c->X2, need * sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&c->Zb, need * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&c->Pb, need * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return fail(c, RH_E_NOMEM, "workspace allocation failed");
   }
@@ -713,18 +1087,25 @@ int ensure_ws(rh_ctx *c, int N, int T) {
   return RH_OK;
 }
 
-HvpParams make_params(rh_ctx *c) {
-  HvpParams h{};
+SegParams make_params(rh_ctx *c) {
+  SegParams h{};
   const Analysis &A = c->A;
   h.n_x = A.n_x;
   h.n_p = A.n_p;
   h.n_bus = A.n_bus;
-  h.X1 = c->X1;
-  h.X2 = c->X2;
-  h.L = c->sL.d;
-  h.U = c->sU.d;
-  h.Ut = c->sUt.d;
-  h.Lt = c->sLt.d;
+  h.nblk = A.nblk;
+  h.seg_row_off = c->seg_row_off;
+  h.row_global = c->row_global;
+  h.fwd = c->dfwd;
+  h.bwd = c->dbwd;
+  h.vL = c->vL;
+  h.vUt = c->vUt;
+  h.vU = c->vU;
+  h.vLt = c->vLt;
+  h.dinv_fwd = c->dinv_fwd;
+  h.dinv_bwd = c->dinv_bwd;
+  h.Z = c->Zb;
+  h.P = c->Pb;
   h.gp_rptr = c->gp_rptr;
   h.gp_col = c->gp_col;
   h.gp_val = c->gp_val;
@@ -749,18 +1130,20 @@ HvpParams make_params(rh_ctx *c) {
   h.near_ref = c->near_ref;
   h.n_near_ref = (int)A.near_ref.size();
   h.f2ref = 2.0 * A.c2b[A.ref];
-  return h;
-}
-
-void launch_hvp(int T, const HvpParams &h, int phases, int ntiles, cudaStream_t st) {
-  switch (T) {
-    case 1: k_hvp<1><<<ntiles, kThreads, 0, st>>>(h, phases); break;
-    case 2: k_hvp<2><<<ntiles, kThreads, 0, st>>>(h, phases); break;
-    case 4: k_hvp<4><<<ntiles, kThreads, 0, st>>>(h, phases); break;
-    case 8: k_hvp<8><<<ntiles, kThreads, 0, st>>>(h, phases); break;
-    case 16: k_hvp<16><<<ntiles, kThreads, 0, st>>>(h, phases); break;
-    default: k_hvp<32><<<ntiles, kThreads, 0, st>>>(h, phases); break;
+  h.ns = A.sep_rows;
+  h.sep_off = A.seg_row_off[A.nblk];
+  h.Sinv = c->Sinv;
+  h.Tsep = c->Tsep;
+  h.blk_gp_ptr = c->blk_gp_ptr;
+  h.blk_gp_loc = c->blk_gp_loc;
+  if (const char *env = getenv("RH_DEBUG")) h.debug = atoi(env);  // timing experiments only
+  if (h.debug & 8) {
+    static long long *dbg = nullptr;
+    if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 6 * 65536);
+    h.dbg = dbg;
   }
+  h.SinvT = c->SinvT;
+  return h;
 }
 
 int check_ready(rh_ctx *c, bool need_mult) {
@@ -787,64 +1170,119 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
   return RH_OK;
 }
 
-// one Alg. 2 batch; W == nullptr with ident_j0 >= 0 for a Cartesian block
+void launch_seg(int cpl, dim3 g, size_t smem, cudaStream_t st, const SegParams &h, int mode) {
+  if (cpl >= 4)
+    k_seg<4><<<g, kSegThreads, smem, st>>>(h, mode);
+  else if (cpl >= 2)
+    k_seg<2><<<g, kSegThreads, smem, st>>>(h, mode);
+  else
+    k_seg<1><<<g, kSegThreads, smem, st>>>(h, mode);
+}
+
+// one Alg. 2 batch: eight stream-ordered kernels, no host
+// synchronization (cf. the two explicit syncs of PAPER.md:798-805).
+// W == nullptr with ident_j0 >= 0 selects the Cartesian block e_{j0..j0+N-1}.
 int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW, long long ldhw,
              int transposed, int N, cudaStream_t st, double *Zo = nullptr, double *Yxo = nullptr,
              double *Psio = nullptr, long long ldz = 0) {
   if (N <= 0) return RH_OK;
-  const int T = pick_T(N);
-  int rc = ensure_ws(c, N, T);
+  const Analysis &A = c->A;
+  const int C = 32 * c->cpl;
+  const int ld = (N + C - 1) / C * C;
+  int rc = ensure_ws(c, ld);
   if (rc) return rc;
-  HvpParams h = make_params(c);
+  SegParams h = make_params(c);
   h.N = N;
+  h.ld = ld;
   h.W = W;
   h.ldw = ldw;
   h.ident_j0 = ident_j0;
   h.HW = HW;
   h.ldhw = ldhw;
   h.transposed = transposed;
-  const int ntiles = (N + T - 1) / T;
-  const bool staged = c->timing || Zo || Yxo || Psio;
-  if (!staged) {
-    launch_hvp(T, h, PH_ALL, ntiles, st);
-    RH_LAUNCHED(c);
-    return RH_OK;
-  }
-  const int ph[5] = {PH_L, PH_U, PH_FOR, PH_UT | PH_LT, PH_MULADD};
-  cudaEvent_t ev[6];
+  const int nb = A.nblk;
+  const bool has_sep = A.sep_rows > 0;
+  const dim3 gA(nb, ld / C), gSg(nblk(A.sep_rows, kThreads / 32), ld / 32),
+      gSm((ld + GBN - 1) / GBN, (A.sep_rows + GBM - 1) / GBM);
+  const dim3 gF(nblk(A.n_bus, kThreads / 32), ld / 32), gM(nblk(A.n_p, kThreads / C_FOR), ld / C_FOR);
+  const int nx = A.n_x;
+  const long long tot = (long long)nx * N;
+  cudaEvent_t ev[9];
   if (c->timing)
     for (auto &e : ev) cudaEventCreate(&e);
-  const int nx = c->A.n_x;
-  const long long tot = (long long)nx * N;
-  for (int s = 0; s < 5; ++s) {
-    if (c->timing) cudaEventRecord(ev[s], st);
-    if (s == 3 && Yxo) {  // Y_x before the transposed solve: X2 holds -Y_x
-      k_untile<<<nblk(tot), kThreads, 0, st>>>(nx, N, T, c->pinv, c->X2, -1.0, Yxo, ldz);
-      RH_LAUNCHED(c);
-    }
-    launch_hvp(T, h, ph[s], ntiles, st);
+  auto mark = [&](int i) {
+    if (c->timing) cudaEventRecord(ev[i], st);
+  };
+  mark(0);
+  launch_seg(c->cpl, gA, c->smem_seg_blk, st, h, MODE_L);
+  RH_LAUNCHED(c);
+  mark(1);
+  if (has_sep) {
+    k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_LU);
     RH_LAUNCHED(c);
-    if (s == 1 && Zo) {
-      k_untile<<<nblk(tot), kThreads, 0, st>>>(nx, N, T, c->pinv, c->X1, 1.0, Zo, ldz);
-      RH_LAUNCHED(c);
+    k_sep_gemm<<<gSm, 256, 0, st>>>(h, MODE_LU);
+    RH_LAUNCHED(c);
+  }
+  mark(2);
+  launch_seg(c->cpl, (h.debug & 32) ? dim3(h.debug >> 8, 1) : gA, c->smem_seg_blk, st, h, MODE_U);
+  RH_LAUNCHED(c);
+  if ((h.debug & 8) && h.dbg) {  // timing experiment: dump per-CTA timestamps of this launch
+    std::vector<long long> hb((size_t)6 * ((h.debug & 32) ? (h.debug >> 8) : gA.x * gA.y));
+    cudaMemcpyAsync(hb.data(), h.dbg, hb.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE *fp = fopen("gpurun_out/kseg_timing.bin", "wb")) {
+      fwrite(hb.data(), 8, hb.size(), fp);
+      fclose(fp);
     }
-    if (s == 3 && Psio) {
-      k_untile<<<nblk(tot), kThreads, 0, st>>>(nx, N, T, c->pinv, c->X2, 1.0, Psio, ldz);
-      RH_LAUNCHED(c);
+    if (h.debug & 64) {
+      std::vector<long long> rc(2000);
+      cudaMemcpy(rc.data(), h.dbg + 6 * 60000, 2000 * 8, cudaMemcpyDeviceToHost);
+      if (FILE *fp = fopen("gpurun_out/kseg_rows.bin", "wb")) {
+        fwrite(rc.data(), 8, rc.size(), fp);
+        fclose(fp);
+      }
     }
   }
+  if (Zo) {
+    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, c->Zb, 1.0, Zo, ldz);
+    RH_LAUNCHED(c);
+  }
+  mark(3);
+  k_for<<<gF, kThreads, 0, st>>>(h);
+  RH_LAUNCHED(c);
+  if (Yxo) {
+    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, c->Pb, -1.0, Yxo, ldz);
+    RH_LAUNCHED(c);
+  }
+  mark(4);
+  launch_seg(c->cpl, gA, c->smem_seg_blk, st, h, MODE_UT);
+  RH_LAUNCHED(c);
+  mark(5);
+  if (has_sep) {
+    k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_UTLT);
+    RH_LAUNCHED(c);
+    k_sep_gemm<<<gSm, 256, 0, st>>>(h, MODE_UTLT);
+    RH_LAUNCHED(c);
+  }
+  mark(6);
+  launch_seg(c->cpl, gA, c->smem_seg_blk, st, h, MODE_LT);
+  RH_LAUNCHED(c);
+  if (Psio) {
+    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, c->Pb, 1.0, Psio, ldz);
+    RH_LAUNCHED(c);
+  }
+  mark(7);
+  k_muladd<C_FOR><<<gM, kThreads, 0, st>>>(h);
+  RH_LAUNCHED(c);
+  mark(8);
   if (c->timing) {
-    cudaEventRecord(ev[5], st);
-    cudaEventSynchronize(ev[5]);
-    float t[5];
-    for (int s = 0; s < 5; ++s) cudaEventElapsedTime(&t[s], ev[s], ev[s + 1]);
-    // {L+SpMul, U, FoR, U^T+L^T (reported in slot 3, slot 4 = MulAdd), total}
-    c->stage_ms[0] = t[0];
-    c->stage_ms[1] = t[1];
-    c->stage_ms[2] = t[2];
-    c->stage_ms[3] = t[3];
-    c->stage_ms[4] = t[4];
-    c->stage_ms[5] = t[0] + t[1] + t[2] + t[3] + t[4];
+    cudaEventSynchronize(ev[8]);
+    float tot_ms = 0.f;
+    for (int s = 0; s < 8; ++s) {
+      cudaEventElapsedTime(&c->stage_ms[s], ev[s], ev[s + 1]);
+      tot_ms += c->stage_ms[s];
+    }
+    c->stage_ms[8] = tot_ms;
     for (auto &e : ev) cudaEventDestroy(e);
   }
   return RH_OK;
@@ -899,8 +1337,25 @@ int rh_load_grid(rh_ctx *c, const rh_grid *g, int32_t *n_x, int32_t *n_p) {
     c->free_all();
   }
   c->loaded = c->has_state = c->has_mult = false;
-  std::string msg = analyze(*g, c->A);
-  if (!msg.empty()) return fail(c, RH_E_GRID, msg);
+  // block size: the largest whose shared-memory stages fit
+  std::string msg;
+  bool fits = false;
+  c->cpl = 2;
+  if (const char *env = getenv("RH_CPL")) c->cpl = atoi(env) >= 4 ? 4 : atoi(env) >= 2 ? 2 : 1;  // tuning override
+  std::vector<int> cands = {256, 128, 512, 64};
+  if (const char *env = getenv("RH_RMAX")) cands.insert(cands.begin(), atoi(env));  // tuning override
+  for (int rmax : cands) {
+    msg = analyze(*g, c->A, rmax);
+    if (!msg.empty()) return fail(c, RH_E_GRID, msg);
+    const Analysis &A = c->A;
+    const size_t lim = (size_t)kSmemMax;
+    fits = A.sb_src.size() * sizeof(double) <= lim &&
+           (size_t)8 * A.sep_rows * sizeof(double) <= lim && seg_smem_max(A, 32 * c->cpl) <= lim &&
+           seg_smem_max(A, kSegC) <= lim &&
+           (size_t)(A.max_blk_fnnz + A.rmax) * sizeof(double) <= lim;
+    if (fits) break;
+  }
+  if (!fits) return fail(c, RH_E_GRID, "grid too large for the shared-memory segment kernels");
   if (!c->host_only) {
     int rc = upload(c);
     if (rc) return rc;
@@ -926,6 +1381,9 @@ int rh_get_info(const rh_ctx *c, rh_info *info) {
   info->levels_fwd = A.nlev_fwd;
   info->levels_bwd = A.nlev_bwd;
   info->max_level_rows = A.max_level_rows;
+  info->n_blocks = A.nblk;
+  info->sep_rows = A.sep_rows;
+  info->seg_levels = std::max(A.fwd.max_levels, A.bwd.max_levels);
   info->workspace_bytes = (int64_t)c->ws_elems * 2 * (int64_t)sizeof(double);
   return RH_OK;
 }
@@ -954,6 +1412,13 @@ int rh_symbolic(const rh_ctx *c, int32_t *perm, int32_t *lu_rowptr, int32_t *lu_
   return RH_OK;
 }
 
+int rh_segments(const rh_ctx *c, int32_t *segment_of_row) {
+  if (!c) return RH_E_ARG;
+  if (!c->loaded) return RH_E_ORDER;
+  if (segment_of_row) std::copy(c->A.seg_of.begin(), c->A.seg_of.end(), segment_of_row);
+  return RH_OK;
+}
+
 int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   if (!c || !x || !p) return fail(c, RH_E_ARG, "null argument");
   if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
@@ -969,7 +1434,6 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   RH_CUDA(c, cudaMemsetAsync(c->gp_val, 0, sizeof(double) * A.gp_col.size(), st));
   RH_CUDA(c, cudaMemsetAsync(c->refg_th, 0, sizeof(double) * nb, st));
   RH_CUDA(c, cudaMemsetAsync(c->refg_v, 0, sizeof(double) * nb, st));
-  RH_CUDA(c, cudaMemsetAsync(c->ticket, 0, sizeof(int), st));
   RH_CUDA(c, cudaMemsetAsync(c->status, 0, sizeof(int), st));
   k_bus_state<<<nblk(nx + np_ + 1), kThreads, 0, st>>>(nx, np_, c->x_bus, c->x_kind, c->p_bus, c->p_kind, c->x,
                                                       c->p, c->th, c->v, c->pgb, A.ref, A.theta_ref);
@@ -1015,27 +1479,71 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   k_objective<<<1, kThreads, 0, st>>>(nb, A.ref, c->has_gen, c->c2b, c->c1b, c->c0b, c->pgb, c->P, c->Pd,
                                       c->scal);
   RH_LAUNCHED(c);
-  // numeric refactorization
-  c->epoch += 1;
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device);
-  const int fblocks = std::min(nsm * 4, std::max(1, nblk((long long)nx * 32)));
-  k_refactor<<<fblocks, kThreads, 0, st>>>(nx, c->fact_order, c->F_rowptr, c->F_col, c->F_diag, c->F_val,
-                                           c->flags, c->epoch, c->ticket, c->status, 1e-14);
+  // numeric refactorization: blocks, separator rows (block updates), separator
+  FactParams f{};
+  f.nblk = A.nblk;
+  f.ns = A.sep_rows;
+  f.seg_row_off = c->seg_row_off;
+  f.row_global = c->row_global;
+  f.fwd_seg_lvl = c->fact_seg_lvl;
+  f.fwd_lvl_ptr = c->fact_lvl_ptr;
+  f.fwd_order = c->fact_order;
+  f.blk_fo_off = c->blk_fo_off;
+  f.fo = c->fo;
+  f.F_rowptr = c->F_rowptr;
+  f.F_diag = c->F_diag;
+  f.F_val = c->F_val;
+  f.ks_ptr = c->ks_ptr;
+  f.ks_pos = c->ks_pos;
+  f.ks_k = c->ks_k;
+  f.ks_kf = c->ks_kf;
+  f.ks_ulen = c->ks_ulen;
+  f.ks_tgt = c->ks_tgt;
+  f.tgt = c->tgt;
+  f.sb_src = c->sb_src;
+  f.sb_diag = c->sb_diag;
+  f.sb_lptr = c->sb_lptr;
+  f.sb_lslot = c->sb_lslot;
+  f.sb_uptr = c->sb_uptr;
+  f.sb_trip = c->sb_trip;
+  f.dinv = c->dinv_rows;
+  f.rowmax = c->rowmax;
+  f.status = c->status;
+  f.pivtol = 1e-14;
+  k_fact_blocks<<<A.nblk, kThreads, c->smem_fact_blk, st>>>(f);
   RH_LAUNCHED(c);
-  for (DevSweepStore *S : {&c->sL, &c->sU, &c->sUt, &c->sLt}) {
-    if (S->nnz > 0) {
-      k_gather_vals<<<nblk(S->nnz), kThreads, 0, st>>>(S->nnz, S->src, c->F_val, S->val_mut);
-      RH_LAUNCHED(c);
-    }
-    if (S->dinv_mut) {
-      k_gather_inv<<<nblk(S->n), kThreads, 0, st>>>(S->n, S->diag_src, c->F_val, S->dinv_mut);
-      RH_LAUNCHED(c);
-    }
+  if (A.sep_rows > 0) {
+    k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, 0, st>>>(f);
+    RH_LAUNCHED(c);
+    k_fact_sep<<<1, 1024, c->smem_fact_sep, st>>>(f, (int)A.sb_src.size());
+    RH_LAUNCHED(c);
+  }
+  struct G {
+    int n;
+    const int *src;
+    double *dst;
+    bool inv;
+  } gs[] = {{c->nnz_fwd, c->fwd_src_a, c->vL, false}, {c->nnz_fwd, c->fwd_src_b, c->vUt, false},
+            {c->nnz_bwd, c->bwd_src_a, c->vU, false},  {c->nnz_bwd, c->bwd_src_b, c->vLt, false},
+            {nx, c->fwd_dsrc, c->dinv_fwd, true},      {nx, c->bwd_dsrc, c->dinv_bwd, true}};
+  for (const G &q : gs) {
+    if (q.n <= 0) continue;
+    if (q.inv)
+      k_gather_inv<<<nblk(q.n), kThreads, 0, st>>>(q.n, q.src, c->F_val, q.dst);
+    else
+      k_gather_vals<<<nblk(q.n), kThreads, 0, st>>>(q.n, q.src, c->F_val, q.dst);
+    RH_LAUNCHED(c);
   }
   const int ngp = (int)A.gp_col.size();
   if (ngp > 0) {
     k_gather_vals<<<nblk(ngp), kThreads, 0, st>>>(ngp, c->gpc_pos, c->gp_val, c->gpc_val);
+    RH_LAUNCHED(c);
+  }
+  if (A.sep_rows > 0) {
+    SegParams h = make_params(c);
+    const int nw = kThreads / 32;
+    k_sep_inverse<<<(A.sep_rows + nw - 1) / nw, kThreads, (size_t)nw * A.sep_rows * sizeof(double), st>>>(
+        h, c->Sinv, c->SinvT);
     RH_LAUNCHED(c);
   }
   int status = 0;
@@ -1068,7 +1576,22 @@ int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *str
   k_grad_rhs<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->x_bus, c->x_kind, c->pinv, c->refg_th, c->refg_v,
                                                 c->scal, c->X1col);
   RH_LAUNCHED(c);
-  k_solve_T1<<<1, kThreads, 0, st>>>(c->sUt.d, c->sLt.d, c->X1col);
+  // J^T lambda = -grad_x f: U^T then L^T sweeps, one column
+  if (int rc2 = ensure_tsep(c, kSegC)) return rc2;
+  SegParams h = make_params(c);
+  if (const char *env = getenv("RH_DEBUG")) h.debug = atoi(env);
+  h.N = 1;
+  h.ld = kSegC;   // column 0 carries the right-hand side, columns 1..31 stay zero
+  h.P = c->X1col;
+  k_seg<1><<<dim3(A.nblk, 1), kSegThreads, c->smem_seg_blk1, st>>>(h, MODE_UT);
+  RH_LAUNCHED(c);
+  if (A.sep_rows > 0) {
+    k_sep_gather<<<dim3(nblk(A.sep_rows, kThreads / 32), 1), kThreads, 0, st>>>(h, MODE_UTLT);
+    RH_LAUNCHED(c);
+    k_sep_gemm<<<dim3(1, (A.sep_rows + GBM - 1) / GBM), 256, 0, st>>>(h, MODE_UTLT);
+    RH_LAUNCHED(c);
+  }
+  k_seg<1><<<dim3(A.nblk, 1), kSegThreads, c->smem_seg_blk1, st>>>(h, MODE_LT);
   RH_LAUNCHED(c);
   k_grad_out<<<nblk(std::max(A.n_x, A.n_p)), kThreads, 0, st>>>(
       A.n_x, A.n_p, c->pinv, c->p_bus, c->p_kind, c->c2b, c->c1b, c->p, c->refg_v, c->scal, c->gpc_ptr, c->gpc_row,
@@ -1181,7 +1704,7 @@ int rh_set_timing(rh_ctx *c, int enable) {
 
 int rh_stage_times(const rh_ctx *c, float *ms_out) {
   if (!c || !ms_out) return RH_E_ARG;
-  for (int i = 0; i < 6; ++i) ms_out[i] = c->stage_ms[i];
+  for (int i = 0; i < 9; ++i) ms_out[i] = c->stage_ms[i];
   return RH_OK;
 }
 

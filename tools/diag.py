@@ -45,7 +45,8 @@ def main(cases, parity=True):
         H = ctx.full_hessian(N)
         torch.cuda.synchronize()
         Hn = H.cpu().numpy()
-        line = f"{name}: n_x={info['n_x']} n_p={info['n_p']} nnzLU={info['nnz_LU']} lev={info['levels_fwd']} "
+        line = (f"{name}: n_x={info['n_x']} n_p={info['n_p']} nnzLU={info['nnz_LU']} lev={info['levels_fwd']} "
+                f"blocks={info['n_blocks']} sep={info['sep_rows']} seglev={info['seg_levels']} ")
         if parity and info["n_x"] < 10000:
             L = pf.Layout(g)
             xo, po = pf.state_vectors(g, L)
@@ -76,8 +77,8 @@ def main(cases, parity=True):
         st = ctx.stage_times()
         ctx.set_timing(False)
         print(f"   set_state {t_state[0]:.3f} ms, grad {t_grad[0]:.3f} ms, full H (N={N}) {t_full[0]:.3f} ms, "
-              f"hvp(N={N}) {t_hvp[0]:.3f} ms -> {N / t_hvp[0] * 1e3:.3e} HVP/s; stages L/U/FoR/UtLt/MulAdd "
-              f"{['%.3f' % v for v in st[:5]]}", flush=True)
+              f"hvp(N={N}) {t_hvp[0]:.3f} ms -> {N / t_hvp[0] * 1e3:.3e} HVP/s; stages A_L/B_LU/A_U/FoR/A_Ut/B_UtLt/A_Lt/MulAdd "
+              f"{['%.3f' % v for v in st[:8]]}", flush=True)
 
 
 if __name__ == "__main__":
