@@ -373,6 +373,13 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
           }
           if (pass == 0) S.rext.push_back((int)S.dep.size());
         }
+        if (s < nb) {  // blocks: pad every row to a multiple of 4 entries (coefficient 0, own row)
+          while ((S.dep.size() - S.rptr.back()) % 4 != 0) {
+            S.dep.push_back(A.loc_of[r]);
+            S.src_a.push_back(-1);
+            S.src_b.push_back(-1);
+          }
+        }
         S.rptr.push_back((int)S.dep.size());
         S.dsrc.push_back(A.F_diag[r]);
       }

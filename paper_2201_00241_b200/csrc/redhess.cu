@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(1024) k_fact_sep(FactParams f, int nslots) {
 // copy factor values into the sweep value arrays (entry order of the sweeps)
 __global__ void k_gather_vals(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n) dst[e] = F[src[e]];
+  if (e < n) dst[e] = src[e] >= 0 ? F[src[e]] : 0.0;   // src < 0: padding entry
 }
 __global__ void k_gather_inv(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -346,14 +346,16 @@ constexpr int kSegThreads = 512;
 constexpr int kSegC = 32;   // columns of the single-RHS (lambda) path
 
 struct SegStage {  // shared-memory carve-up of one block sweep
-  double *X, *dinv;
-  double2 *ent;     // per entry: (coefficient, local dependency index as a bit-cast integer)
-  int *order, *rptr, *lvl;
+  double *X;
+  double2 *ent;     // per entry: (coefficient, byte offset of the dependency row in X, bit-cast)
+  int4 *meta;       // per row q: (byte offset of the row in X, first entry, number of 4-entry groups, -)
+  double *dinv;
+  int *lvl;
   int nq, ne, nlev;
 };
 
-// Stage a block's sweep structure (levels, rows, entries, pivots) in shared
-// memory behind an X tile of `nrx` rows x C columns.
+// Stage a block's sweep structure in shared memory behind an X tile of `nrx`
+// rows x C columns.  Rows are padded to multiples of 4 entries on the host.
 __device__ __forceinline__ SegStage stage_seg(const DSeg &S, const double *__restrict__ val,
                                               const double *__restrict__ dinv, int seg, int nrx, int C, double *sm) {
   SegStage t;
@@ -363,28 +365,27 @@ __device__ __forceinline__ SegStage stage_seg(const DSeg &S, const double *__res
   t.nq = S.lvl_ptr[l1 - 1] - qb;
   const int eb = S.rptr[qb];
   t.ne = S.rptr[qb + t.nq] - eb;
+  const long long rowb = (long long)C * 8;
   t.X = sm;
   t.ent = reinterpret_cast<double2 *>(t.X + (size_t)nrx * C);
-  t.dinv = reinterpret_cast<double *>(t.ent + t.ne);
-  t.order = reinterpret_cast<int *>(t.dinv + t.nq);
-  t.rptr = t.order + t.nq;
-  t.lvl = t.rptr + t.nq + 1;
+  t.meta = reinterpret_cast<int4 *>(t.ent + t.ne);
+  t.dinv = reinterpret_cast<double *>(t.meta + t.nq);
+  t.lvl = reinterpret_cast<int *>(t.dinv + t.nq);
 #pragma unroll 4
   for (int i = threadIdx.x; i < t.ne; i += blockDim.x)
-    t.ent[i] = make_double2(val[eb + i], __longlong_as_double((long long)S.dep[eb + i]));
+    t.ent[i] = make_double2(val[eb + i], __longlong_as_double((long long)S.dep[eb + i] * rowb));
   for (int i = threadIdx.x; i < t.nq; i += blockDim.x) {
-    t.order[i] = S.order[qb + i];
+    const int e0 = S.rptr[qb + i] - eb, e1 = S.rptr[qb + i + 1] - eb;
+    t.meta[i] = make_int4((int)(S.order[qb + i] * rowb), e0, (e1 - e0) >> 2, 0);
     t.dinv[i] = dinv ? dinv[qb + i] : 1.0;
   }
-  for (int i = threadIdx.x; i <= t.nq; i += blockDim.x) t.rptr[i] = S.rptr[qb + i] - eb;
   for (int i = threadIdx.x; i <= t.nlev; i += blockDim.x) t.lvl[i] = S.lvl_ptr[l0 + i] - qb;
   return t;
 }
 
 // bytes of shared memory stage_seg needs for a block
 __host__ __device__ inline size_t seg_smem_bytes(int nrx, int nq, int ne, int nlev, int C) {
-  return (size_t)nrx * C * 8 + (size_t)ne * 16 + (size_t)nq * 8 + (size_t)nq * 4 + (size_t)(nq + 1) * 4 +
-         (size_t)(nlev + 1) * 4 + 16;
+  return (size_t)nrx * C * 8 + (size_t)ne * 16 + (size_t)nq * 16 + (size_t)nq * 8 + (size_t)(nlev + 1) * 4 + 16;
 }
 
 template <int CPL>
@@ -410,40 +411,32 @@ __device__ __forceinline__ void stx(double *p, const double (&x)[CPL]) {
   }
 }
 
-// One sweep over a block, level by level, one warp per row, CPL columns per
-// lane (32 * CPL columns per CTA).  All dependencies are in shared memory
-// (the block's rows and the staged separator rows it depends on).
+// One sweep over a block: super-level by super-level (CTA barrier between),
+// each warp walking its rows in dependency order with no synchronization (its
+// lanes own their columns).  Per row: 4-entry groups of (coefficient, X row
+// offset) broadcasts and conflict-free X gathers, two FMA chains, next row's
+// metadata prefetched.
 template <int CPL>
-__device__ __forceinline__ void seg_sweep(const SegStage &t, bool use_dinv, long long *rowclk = nullptr) {
-  constexpr int C = 32 * CPL;
+__device__ __forceinline__ void seg_sweep(const SegStage &t, bool use_dinv) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const double *Xl = t.X + lane * CPL;
-  // t.lvl holds super-level x warp boundaries: warp w of super-level s owns
-  // rows [lvl[s*nw + w], lvl[s*nw + w + 1]) in dependency order (no sync needed
-  // inside a warp: every lane only touches its own columns)
+  const char *Xb = reinterpret_cast<const char *>(t.X) + lane * CPL * 8;
   const int nsl = t.nlev / nw;
   for (int sl = 0; sl < nsl; ++sl) {
-    const int q1 = t.lvl[sl * nw + warp + 1];
-    for (int q = t.lvl[sl * nw + warp]; q < q1; ++q) {
-      if (rowclk && lane == 0 && q < 1000) {
-        long long tt;
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(tt));
-        rowclk[2 * q] = tt;
-        rowclk[2 * q + 1] = (t.rptr[q + 1] - t.rptr[q]) + 1000 * sl + 100000 * warp;
-      }
-      const int a = t.order[q];
-      int e = t.rptr[q];
-      const int e1 = t.rptr[q + 1];
+    const int q0 = t.lvl[sl * nw + warp], q1 = t.lvl[sl * nw + warp + 1];
+    int4 m = q0 < q1 ? t.meta[q0] : make_int4(0, 0, 0, 0);
+    for (int q = q0; q < q1; ++q) {
+      const int4 mn = q + 1 < q1 ? t.meta[q + 1] : m;
       double s0[CPL], s1[CPL];
 #pragma unroll
       for (int i = 0; i < CPL; ++i) s0[i] = s1[i] = 0.0;
-      for (; e + 4 <= e1; e += 4) {
-        const double2 p0 = t.ent[e], p1 = t.ent[e + 1], p2 = t.ent[e + 2], p3 = t.ent[e + 3];
+      const double2 *ep = t.ent + m.y;
+      for (int g = 0; g < m.z; ++g, ep += 4) {
+        const double2 p0 = ep[0], p1 = ep[1], p2 = ep[2], p3 = ep[3];
         double x0[CPL], x1[CPL], x2[CPL], x3[CPL];
-        ldx<CPL>(Xl + (int)__double_as_longlong(p0.y) * C, x0);
-        ldx<CPL>(Xl + (int)__double_as_longlong(p1.y) * C, x1);
-        ldx<CPL>(Xl + (int)__double_as_longlong(p2.y) * C, x2);
-        ldx<CPL>(Xl + (int)__double_as_longlong(p3.y) * C, x3);
+        ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p0.y)), x0);
+        ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p1.y)), x1);
+        ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p2.y)), x2);
+        ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p3.y)), x3);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
           s0[i] = fma(p0.x, x0[i], s0[i]);
@@ -452,22 +445,17 @@ __device__ __forceinline__ void seg_sweep(const SegStage &t, bool use_dinv, long
           s1[i] = fma(p3.x, x3[i], s1[i]);
         }
       }
-      for (; e < e1; ++e) {
-        const double2 p0 = t.ent[e];
-        double x0[CPL];
-        ldx<CPL>(Xl + (int)__double_as_longlong(p0.y) * C, x0);
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) s0[i] = fma(p0.x, x0[i], s0[i]);
-      }
+      double *xr = reinterpret_cast<double *>(const_cast<char *>(Xb) + m.x);
       double xa[CPL];
-      ldx<CPL>(Xl + a * C, xa);
+      ldx<CPL>(xr, xa);
       const double d = t.dinv[q];
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
         xa[i] -= s0[i] + s1[i];
         if (use_dinv) xa[i] *= d;
       }
-      stx<CPL>(const_cast<double *>(Xl) + a * C, xa);
+      stx<CPL>(xr, xa);
+      m = mn;
     }
     __syncthreads();
   }
@@ -490,7 +478,7 @@ __device__ __forceinline__ double rhs_gpw(const SegParams &h, int row, int col) 
 
 // Block kernel: one CTA = (block, 32 * CPL columns), 512 threads.
 template <int CPL>
-__global__ void __launch_bounds__(kSegThreads) k_seg(SegParams h, int mode) {
+__global__ void __launch_bounds__(kSegThreads, 1) k_seg(SegParams h, int mode) {
   constexpr int C = 32 * CPL;
   extern __shared__ double sm[];
   const int seg = blockIdx.x;
@@ -522,7 +510,7 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(SegParams h, int mode) {
     // asynchronous 16 B copies global -> shared (LDGSTS)
     for (int i = threadIdx.x; i < nr * CH; i += blockDim.x) {
       const int a = i / CH, ch = i % CH;
-      const double *src = G + (long long)h.row_global[r0 + a] * h.ld + col0 + 2 * ch;
+      const double *src = G + (long long)(r0 + a) * h.ld + col0 + 2 * ch;
       const unsigned dst = (unsigned)__cvta_generic_to_shared(t.X + a * C + 2 * ch);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     }
@@ -537,12 +525,11 @@ __global__ void __launch_bounds__(kSegThreads) k_seg(SegParams h, int mode) {
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[1]));
-  seg_sweep<CPL>(t, dinv != nullptr,
-                 ((h.debug & 64) && h.dbg && blockIdx.x == 0 && blockIdx.y == 0) ? h.dbg + 6 * 60000 : nullptr);
+  seg_sweep<CPL>(t, dinv != nullptr);
   if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[2]));
   for (int i = threadIdx.x; i < nr * CH; i += blockDim.x) {
     const int a = i / CH, ch = i % CH;
-    *reinterpret_cast<double2 *>(G + (long long)h.row_global[r0 + a] * h.ld + col0 + 2 * ch) =
+    *reinterpret_cast<double2 *>(G + (long long)(r0 + a) * h.ld + col0 + 2 * ch) =
         *reinterpret_cast<const double2 *>(t.X + a * C + 2 * ch);
   }
   if (instr) {
@@ -574,7 +561,7 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
   const double *val = mode == MODE_LU ? h.vL : h.vUt;
   const int a = h.fwd.order[q];
   const int row = h.row_global[h.sep_off + a];
-  const double v0 = mode == MODE_LU ? rhs_gpw(h, row, col) : G[(long long)row * h.ld + col];
+  const double v0 = mode == MODE_LU ? rhs_gpw(h, row, col) : G[(long long)(h.sep_off + a) * h.ld + col];
   int e = h.fwd.rptr[q];
   const int ex = h.fwd.rext[q];
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -591,57 +578,88 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
   h.Tsep[(long long)a * h.ld + col] = v0 - ((s0 + s1) + (s2 + s3));
 }
 
-// C[m][n] = sum_k M[m][k] T[k][n] for the separator rows m (written to
-// G[row_global[sep_off + m]][n]); 64x64 output tile per CTA, 4x4 per thread,
-// k in tiles of 16 staged in shared memory.  Fixed k order: deterministic.
-constexpr int GBM = 64, GBN = 64, GBK = 16;
-__global__ void __launch_bounds__(256) k_sep_gemm(SegParams h, int mode) {
-  __shared__ double As[GBK][GBM + 1];
-  __shared__ double Bs[GBK][GBN];
-  const int ns = h.ns;
+// C[m][n] = sum_k M[m][k] T[k][n] written to the separator slab of Z / P
+// (rows sep_off + m, contiguous in segment order).  64 x 64 output tile per
+// CTA, 128 threads, 8 x 4 outputs per thread, k in tiles of 16 staged in
+// shared memory with the next tile prefetched into registers.  Fixed k order:
+// deterministic.
+constexpr int GBM = 64, GBN = 64, GBK = 16, GTHREADS = 128;
+__global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
+  __shared__ __align__(16) double As[GBK][GBM + 2];   // +2: conflict-free transposed stores
+  __shared__ __align__(16) double Bs[GBK][GBN];
+  const int ns = h.ns, ld = h.ld;
   const double *M = mode == MODE_LU ? h.Sinv : h.SinvT;
   double *G = mode == MODE_LU ? h.Z : h.P;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  double acc[4][4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;  // 16 x 8 threads: n = tx*4.., m = ty*8..
+  double acc[8][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  for (int k0 = 0; k0 < ns; k0 += GBK) {
+  double ra[8], rb[8];
+  auto load = [&](int k0) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int idx = threadIdx.x + r * 256;  // 1024 = 64 x 16
+    for (int r = 0; r < 8; ++r) {
+      const int idx = tid + r * GTHREADS;          // 1024 = 64 (m) x 16 (k)
       const int mm = idx / GBK, kk = idx % GBK;
       const int gm = m0 + mm, gk = k0 + kk;
-      As[kk][mm] = (gm < ns && gk < ns) ? M[(long long)gm * ns + gk] : 0.0;
-      const int kb = idx / GBN, nn = idx % GBN;
+      ra[r] = (gm < ns && gk < ns) ? __ldg(M + (long long)gm * ns + gk) : 0.0;
+      const int kb = idx / GBN, nn = idx % GBN;    // 1024 = 16 (k) x 64 (n)
       const int gk2 = k0 + kb;
-      Bs[kb][nn] = (gk2 < ns && n0 + nn < h.ld) ? h.Tsep[(long long)gk2 * h.ld + n0 + nn] : 0.0;
+      rb[r] = (gk2 < ns && n0 + nn < ld) ? h.Tsep[(long long)gk2 * ld + n0 + nn] : 0.0;
     }
+  };
+  auto store = [&]() {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int idx = tid + r * GTHREADS;
+      As[idx % GBK][idx / GBK] = ra[r];
+      Bs[idx / GBN][idx % GBN] = rb[r];
+    }
+  };
+  load(0);
+  for (int k0 = 0; k0 < ns; k0 += GBK) {
+    store();
     __syncthreads();
+    if (k0 + GBK < ns) load(k0 + GBK);
 #pragma unroll
     for (int kk = 0; kk < GBK; ++kk) {
-      double a[4], b[4];
+      double a[8], bv[4];
+      const double2 *ap = reinterpret_cast<const double2 *>(&As[kk][ty * 8]);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+      for (int i = 0; i < 4; ++i) {
+        const double2 v = ap[i];
+        a[2 * i] = v.x;
+        a[2 * i + 1] = v.y;
+      }
+      const double2 *bp = reinterpret_cast<const double2 *>(&Bs[kk][tx * 4]);
+      const double2 b0 = bp[0], b1 = bp[1];
+      bv[0] = b0.x;
+      bv[1] = b0.y;
+      bv[2] = b1.x;
+      bv[3] = b1.y;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gm = m0 + ty * 4 + i;
+  for (int i = 0; i < 8; ++i) {
+    const int gm = m0 + ty * 8 + i;
     if (gm >= ns) continue;
-    double *out = G + (long long)h.row_global[h.sep_off + gm] * h.ld + n0;
+    double *out = G + (long long)(h.sep_off + gm) * ld + n0 + tx * 4;
+    if (n0 + tx * 4 + 3 < ld) {
+      reinterpret_cast<double2 *>(out)[0] = make_double2(acc[i][0], acc[i][1]);
+      reinterpret_cast<double2 *>(out)[1] = make_double2(acc[i][2], acc[i][3]);
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (n0 + tx + 16 * j < h.ld) out[tx + 16 * j] = acc[i][j];
+      for (int j = 0; j < 4; ++j)
+        if (n0 + tx * 4 + j < ld) out[j] = acc[i][j];
+    }
   }
 }
 
@@ -693,72 +711,113 @@ __device__ __forceinline__ double delta_src(const SegParams &h, int src, int col
   return load_W(h, -(src + 2), col);
 }
 
-// one warp per bus, one lane per column (32 columns per CTA column chunk):
-// every index / coefficient load is warp-uniform, every Z load is 256 B.
+// One warp per bus, one lane per column, FCH column chunks per warp processed
+// together (index / coefficient loads amortized, FCH independent gathers in
+// flight per incident line).
+constexpr int FCH = 4;
 __global__ void __launch_bounds__(kThreads) k_for(SegParams h) {
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  const int col = blockIdx.y * 32 + lane;
   if (b >= h.n_bus) return;
-  const double dth_b = delta_src(h, h.dth_src[b], col);
-  const double dv_b = delta_src(h, h.dv_src[b], col);
-  double yth = 0.0;
-  double yv = h.dcoef[b] * dv_b;
+  const int nch = h.ld / 32;
+  const int ch0 = blockIdx.y * FCH;
+  int col[FCH];
+#pragma unroll
+  for (int u = 0; u < FCH; ++u) col[u] = (ch0 + u < nch ? ch0 + u : nch - 1) * 32 + lane;
+  const int dths = h.dth_src[b], dvs = h.dv_src[b];
+  const double dc = h.dcoef[b];
+  double dth_b[FCH], dv_b[FCH], yth[FCH], yv[FCH];
+#pragma unroll
+  for (int u = 0; u < FCH; ++u) {
+    dth_b[u] = delta_src(h, dths, col[u]);
+    dv_b[u] = delta_src(h, dvs, col[u]);
+    yth[u] = 0.0;
+    yv[u] = dc * dv_b[u];
+  }
   const int s0 = h.bl_ptr[b], s1 = h.bl_ptr[b + 1];
-#pragma unroll 2
   for (int s = s0; s < s1; ++s) {
     const double4 k = h.coef[h.bl_line[s]];
-    const double dth_o = delta_src(h, h.o_dth_src[s], col);
-    const double dv_o = delta_src(h, h.o_dv_src[s], col);
-    if (h.bl_end[s] == 0) {  // b is the from-end i
-      const double D = dth_b - dth_o;
-      yth += k.x * D + k.y * dv_b + k.z * dv_o;
-      yv += k.y * D + k.w * dv_o;
-    } else {                 // b is the to-end j
-      const double D = dth_o - dth_b;
-      yth -= k.x * D + k.y * dv_o + k.z * dv_b;
-      yv += k.z * D + k.w * dv_o;
+    const int os = h.o_dth_src[s], ov = h.o_dv_src[s];
+    const bool from = h.bl_end[s] == 0;
+    double dth_o[FCH], dv_o[FCH];
+#pragma unroll
+    for (int u = 0; u < FCH; ++u) {
+      dth_o[u] = delta_src(h, os, col[u]);
+      dv_o[u] = delta_src(h, ov, col[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < FCH; ++u) {
+      if (from) {  // b is the from-end i
+        const double D = dth_b[u] - dth_o[u];
+        yth[u] += k.x * D + k.y * dv_b[u] + k.z * dv_o[u];
+        yv[u] += k.y * D + k.w * dv_o[u];
+      } else {     // b is the to-end j
+        const double D = dth_o[u] - dth_b[u];
+        yth[u] -= k.x * D + k.y * dv_o[u] + k.z * dv_b[u];
+        yv[u] += k.z * D + k.w * dv_o[u];
+      }
     }
   }
   // REF objective rank-1 term f''(Pg_ref) (grad P_ref . delta) grad P_ref (R22):
   // only the buses of {ref} u A(ref) carry a nonzero grad P_ref entry
   const double rt = h.refg_th[b], rv = h.refg_v[b];
   if (rt != 0.0 || rv != 0.0) {
-    double sref = 0.0;
-    for (int q = 0; q < h.n_near_ref; ++q) {
-      const int o = h.near_ref[q];
-      sref += h.refg_th[o] * delta_src(h, h.dth_src[o], col) + h.refg_v[o] * delta_src(h, h.dv_src[o], col);
+#pragma unroll
+    for (int u = 0; u < FCH; ++u) {
+      double sref = 0.0;
+      for (int q = 0; q < h.n_near_ref; ++q) {
+        const int o = h.near_ref[q];
+        sref += h.refg_th[o] * delta_src(h, h.dth_src[o], col[u]) + h.refg_v[o] * delta_src(h, h.dv_src[o], col[u]);
+      }
+      sref *= h.f2ref;
+      yth[u] += sref * rt;
+      yv[u] += sref * rv;
     }
-    sref *= h.f2ref;
-    yth += sref * rt;
-    yv += sref * rv;
   }
-  const int dt = h.yth_dst[b];
-  if (dt >= 0) h.P[(long long)dt * h.ld + col] = -yth;
-  const int dv = h.yv_dst[b];
-  if (dv >= 0) {
-    h.P[(long long)dv * h.ld + col] = -yv;
-  } else if (col < h.N) {
-    h.HW[hw_index(h, -(dv + 2), col)] = yv;
+  const int dt = h.yth_dst[b], dv = h.yv_dst[b], pg = h.pg_p[b];
+  const double c2x2 = 2.0 * h.c2b[b];
+#pragma unroll
+  for (int u = 0; u < FCH; ++u) {
+    if (ch0 + u >= nch) break;
+    const int c = col[u];
+    if (dt >= 0) h.P[(long long)dt * h.ld + c] = -yth[u];
+    if (dv >= 0) {
+      h.P[(long long)dv * h.ld + c] = -yv[u];
+    } else if (c < h.N) {
+      h.HW[hw_index(h, -(dv + 2), c)] = yv[u];
+    }
+    if (pg >= 0 && c < h.N) h.HW[hw_index(h, pg, c)] = c2x2 * load_W(h, pg, c);
   }
-  const int pg = h.pg_p[b];
-  if (pg >= 0 && col < h.N) h.HW[hw_index(h, pg, col)] = 2.0 * h.c2b[b] * load_W(h, pg, col);
 }
 
-// SpMulAdd HW = Y_p + G_p^T Psi, thread = (p row, column)
-template <int C>
+// SpMulAdd HW = Y_p + G_p^T Psi: one warp per p row, lanes over
+// columns, FCH chunks per warp
 __global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
-  const int c = threadIdx.x % C;
-  const int cp = blockIdx.x * (kThreads / C) + threadIdx.x / C;
-  const int col = blockIdx.y * C + c;
-  if (cp >= h.n_p || col >= h.N) return;
-  const long long idx = hw_index(h, cp, col);
-  double acc = h.HW[idx];
-  for (int q = h.gpc_ptr[cp]; q < h.gpc_ptr[cp + 1]; ++q) acc += h.gpc_val[q] * h.P[(long long)h.gpc_row[q] * h.ld + col];
-  h.HW[idx] = acc;
+  const int lane = threadIdx.x & 31;
+  const int cp = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (cp >= h.n_p) return;
+  const int q0 = h.gpc_ptr[cp], q1 = h.gpc_ptr[cp + 1];
+  const int ch0 = blockIdx.y * FCH;
+  double acc[FCH];
+  int col[FCH];
+#pragma unroll
+  for (int u = 0; u < FCH; ++u) {
+    col[u] = (ch0 + u) * 32 + lane;
+    acc[u] = col[u] < h.N ? h.HW[hw_index(h, cp, col[u])] : 0.0;
+  }
+  for (int q = q0; q < q1; ++q) {
+    const double g = h.gpc_val[q];
+    const double *pr = h.P + (long long)h.gpc_row[q] * h.ld;
+#pragma unroll
+    for (int u = 0; u < FCH; ++u)
+      if (col[u] < h.ld) acc[u] = fma(g, pr[col[u]], acc[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < FCH; ++u)
+    if (col[u] < h.N) h.HW[hw_index(h, cp, col[u])] = acc[u];
 }
 
-// natural-order copy of a permuted block: out[k][col] = sgn * X[pinv[k]][col]
+// natural-order copy of an internal block: out[k][col] = sgn * X[zmap[k]][col]
 __global__ void k_unpermute(int n_x, int N, int ld, const int *pinv, const double *X, double sgn, double *out,
                             long long ldo) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -847,7 +906,6 @@ T *dalloc(size_t n, std::vector<void *> &pool) {
   return p;
 }
 
-constexpr int C_FOR = 16;   // columns per CTA, tensor projection / SpMulAdd
 constexpr int kSmemMax = 220 * 1024;
 
 }  // namespace
@@ -957,12 +1015,22 @@ int upload(rh_ctx *c) {
   UP(G_ii, A.G_ii); UP(B_ii, A.B_ii); UP(Pd, A.Pd); UP(Qd, A.Qd); UP(G_ft, A.G_ft); UP(B_ft, A.B_ft);
   UP(G_tf, A.G_tf); UP(B_tf, A.B_tf); UP(c2b, A.c2b); UP(c1b, A.c1b); UP(c0b, A.c0b);
   UP(x_bus, A.x_bus); UP(x_kind, A.x_kind); UP(p_bus, A.p_bus); UP(p_kind, A.p_kind);
-  UP(th_x, A.th_x); UP(v_x, A.v_x); UP(pinv, A.pinv);
+  // Z and P rows are stored in SEGMENT order (blocks, then the separator, each
+  // contiguous): zrow[factor row] = segment position; zmap[natural x] = Z row.
+  std::vector<int32_t> zrow(A.n_x), zmap(A.n_x);
+  for (int q = 0; q < A.n_x; ++q) zrow[A.row_global[q]] = q;
+  for (int k = 0; k < A.n_x; ++k) zmap[k] = zrow[A.pinv[k]];
+  auto zr = [&](std::vector<int32_t> v) {  // >= 0 entries are factor rows -> Z rows
+    for (auto &x : v)
+      if (x >= 0) x = zrow[x];
+    return v;
+  };
+  UP(th_x, A.th_x); UP(v_x, A.v_x); UP(pinv, zmap);
   UP(F_rowptr, A.F_rowptr); UP(F_diag, A.F_diag);
   UP(diag_pos, A.diag_pos); UP(slot_pos, A.slot_pos); UP(gp_rptr, A.gp_rptr); UP(gp_col, A.gp_col);
   UP(gp_self_pos, A.gp_self_pos); UP(gp_pg_pos, A.gp_pg_pos); UP(gp_slot_pos, A.gp_slot_pos);
-  UP(gpc_ptr, A.gpc_ptr); UP(gpc_pos, A.gpc_pos); UP(gpc_row, A.gpc_row);
-  UP(dth_src, A.dth_src); UP(dv_src, A.dv_src); UP(yth_dst, A.yth_dst); UP(yv_dst, A.yv_dst);
+  UP(gpc_ptr, A.gpc_ptr); UP(gpc_pos, A.gpc_pos); UP(gpc_row, zr(A.gpc_row));
+  UP(dth_src, zr(A.dth_src)); UP(dv_src, zr(A.dv_src)); UP(yth_dst, zr(A.yth_dst)); UP(yv_dst, zr(A.yv_dst));
   UP(pg_p, A.pg_p); UP(near_ref, A.near_ref);
   UP(seg_row_off, A.seg_row_off); UP(row_global, A.row_global);
   UP(fact_seg_lvl, A.fact_seg_lvl); UP(fact_lvl_ptr, A.fact_lvl_ptr); UP(fact_order, A.fact_order);
@@ -974,7 +1042,14 @@ int upload(rh_ctx *c) {
   UP(sb_src, A.sb_src); UP(sb_diag, A.sb_diag); UP(sb_lptr, A.sb_lptr); UP(sb_lslot, A.sb_lslot);
   UP(sb_uptr, A.sb_uptr); UP(sb_trip, A.sb_trip);
 #undef UP
-  auto mkseg = [&](DSeg &D, const SegSweep &S) {
+  auto mkseg = [&](DSeg &D, const SegSweep &S0) {
+    SegSweep S = S0;
+    for (auto &x : S.ext_rows) x = zrow[x];
+    {  // separator external entries: factor rows -> Z rows
+      const int qb = S.lvl_ptr[S.seg_lvl[A.nblk]], qe = S.lvl_ptr[S.seg_lvl[A.nblk + 1] - 1];
+      for (int q = qb; q < qe; ++q)
+        for (int e = S.rptr[q]; e < S.rext[q]; ++e) S.dep[e] = zrow[S.dep[e]];
+    }
     int *a, *b, *o, *r, *x, *d, *eo, *er;
     chk(eo = dalloc_copy(S.ext_off, P));
     chk(er = dalloc_copy(S.ext_rows, P));
@@ -998,9 +1073,10 @@ int upload(rh_ctx *c) {
   c->nnz_fwd = (int)A.fwd.dep.size();
   c->nnz_bwd = (int)A.bwd.dep.size();
   std::vector<int32_t> odth(2 * A.n_line), odv(2 * A.n_line);
+  const std::vector<int32_t> zdth = zr(A.dth_src), zdv = zr(A.dv_src);
   for (int s = 0; s < 2 * A.n_line; ++s) {
-    odth[s] = A.dth_src[A.bl_other[s]];
-    odv[s] = A.dv_src[A.bl_other[s]];
+    odth[s] = zdth[A.bl_other[s]];
+    odv[s] = zdv[A.bl_other[s]];
   }
   chk(c->o_dth_src = dalloc_copy(odth, P));
   chk(c->o_dv_src = dalloc_copy(odv, P));
@@ -1204,7 +1280,8 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   const bool has_sep = A.sep_rows > 0;
   const dim3 gA(nb, ld / C), gSg(nblk(A.sep_rows, kThreads / 32), ld / 32),
       gSm((ld + GBN - 1) / GBN, (A.sep_rows + GBM - 1) / GBM);
-  const dim3 gF(nblk(A.n_bus, kThreads / 32), ld / 32), gM(nblk(A.n_p, kThreads / C_FOR), ld / C_FOR);
+  const int nch32 = ld / 32, fch = (nch32 + FCH - 1) / FCH;
+  const dim3 gF(nblk(A.n_bus, kThreads / 32), fch), gM(nblk(A.n_p, kThreads / 32), fch);
   const int nx = A.n_x;
   const long long tot = (long long)nx * N;
   cudaEvent_t ev[9];
@@ -1220,7 +1297,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   if (has_sep) {
     k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_LU);
     RH_LAUNCHED(c);
-    k_sep_gemm<<<gSm, 256, 0, st>>>(h, MODE_LU);
+    k_sep_gemm<<<gSm, GTHREADS, 0, st>>>(h, MODE_LU);
     RH_LAUNCHED(c);
   }
   mark(2);
@@ -1233,14 +1310,6 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     if (FILE *fp = fopen("gpurun_out/kseg_timing.bin", "wb")) {
       fwrite(hb.data(), 8, hb.size(), fp);
       fclose(fp);
-    }
-    if (h.debug & 64) {
-      std::vector<long long> rc(2000);
-      cudaMemcpy(rc.data(), h.dbg + 6 * 60000, 2000 * 8, cudaMemcpyDeviceToHost);
-      if (FILE *fp = fopen("gpurun_out/kseg_rows.bin", "wb")) {
-        fwrite(rc.data(), 8, rc.size(), fp);
-        fclose(fp);
-      }
     }
   }
   if (Zo) {
@@ -1261,7 +1330,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   if (has_sep) {
     k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
-    k_sep_gemm<<<gSm, 256, 0, st>>>(h, MODE_UTLT);
+    k_sep_gemm<<<gSm, GTHREADS, 0, st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
   }
   mark(6);
@@ -1272,7 +1341,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     RH_LAUNCHED(c);
   }
   mark(7);
-  k_muladd<C_FOR><<<gM, kThreads, 0, st>>>(h);
+  k_muladd<<<gM, kThreads, 0, st>>>(h);
   RH_LAUNCHED(c);
   mark(8);
   if (c->timing) {
@@ -1588,7 +1657,7 @@ int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *str
   if (A.sep_rows > 0) {
     k_sep_gather<<<dim3(nblk(A.sep_rows, kThreads / 32), 1), kThreads, 0, st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
-    k_sep_gemm<<<dim3(1, (A.sep_rows + GBM - 1) / GBM), 256, 0, st>>>(h, MODE_UTLT);
+    k_sep_gemm<<<dim3(1, (A.sep_rows + GBM - 1) / GBM), GTHREADS, 0, st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
   }
   k_seg<1><<<dim3(A.nblk, 1), kSegThreads, c->smem_seg_blk1, st>>>(h, MODE_LT);
