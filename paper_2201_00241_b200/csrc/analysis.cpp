@@ -465,34 +465,10 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
       }
     }
   }
-  auto slot = [&](int a, int j) -> int {
-    auto &v = srow[a];
-    auto it = std::lower_bound(v.begin(), v.end(), std::make_pair(j, -1));
-    return (it != v.end() && it->first == j) ? it->second : -1;
-  };
-  A.sb_diag.assign(ns, -1);
-  A.sb_lptr.assign(ns + 1, 0);
-  A.sb_uptr.assign(ns + 1, 0);
-  A.sb_lslot.clear();
-  A.sb_trip.clear();
-  for (int a = 0; a < ns; ++a) {
-    const int k = A.row_global[sb0 + a];
-    A.sb_diag[a] = slot(a, k);
-    std::vector<int> lrows;  // separator rows i > k with F[i,k] != 0 (= U pattern of row k, symmetric)
-    for (int i : Ls[k])
-      if (A.seg_of[i] == nb) lrows.push_back(i);
-    for (int i : lrows) A.sb_lslot.push_back(slot(A.loc_of[i], k));
-    for (int i : lrows) {
-      const int li = slot(A.loc_of[i], k);
-      for (int j : Ls[k]) {  // U columns of row k (all separator)
-        A.sb_trip.push_back(li);
-        A.sb_trip.push_back(slot(a, j));
-        A.sb_trip.push_back(slot(A.loc_of[i], j));
-      }
-    }
-    A.sb_lptr[a + 1] = (int)A.sb_lslot.size();
-    A.sb_uptr[a + 1] = (int)(A.sb_trip.size() / 3);
-  }
+  // dense position (row-major, ns x ns) of every separator x separator entry
+  A.sb_dense.assign(A.sb_src.size(), 0);
+  for (int a = 0; a < ns; ++a)
+    for (auto &pr : srow[a]) A.sb_dense[pr.second] = a * ns + A.loc_of[pr.first];
 }
 
 }  // namespace

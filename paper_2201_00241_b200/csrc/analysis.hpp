@@ -123,11 +123,9 @@ struct Analysis {
   std::vector<int32_t> ks_ulen;             // number of U entries of row k
   std::vector<int32_t> ks_tgt;              // start in tgt
   std::vector<int32_t> tgt;                 // offsets inside row i of the U columns of row k
-  // R_B2 (separator, right-looking, shared memory)
+  // separator block S (Schur complement after R_B1), densified for its inversion
   std::vector<int32_t> sb_src;              // [nslots] F positions of separator-column entries of separator rows
-  std::vector<int32_t> sb_diag;             // [sep_rows] slot of the pivot of separator row (local)
-  std::vector<int32_t> sb_lptr, sb_lslot;   // per step: slots (i, k) of column k, i > k
-  std::vector<int32_t> sb_uptr, sb_trip;    // per step: triples (l_slot, u_slot, target) packed 3 x int32
+  std::vector<int32_t> sb_dense;            // [nslots] row-major position in the dense ns x ns block
 };
 
 // Returns "" on success, else an error message (grid rejected).

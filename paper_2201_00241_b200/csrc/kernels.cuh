@@ -68,7 +68,6 @@ struct FactParams {
   const int *F_rowptr, *F_diag;
   double *F_val;
   const int *ks_ptr, *ks_pos, *ks_k, *ks_kf, *ks_ulen, *ks_tgt, *tgt;
-  const int *sb_src, *sb_diag, *sb_lptr, *sb_lslot, *sb_uptr, *sb_trip;
   double *dinv, *rowmax;             // per permuted row
   int *status;
   double pivtol;

@@ -278,28 +278,182 @@ __global__ void __launch_bounds__(kThreads) k_fact_sep_rows(FactParams f) {
   }
 }
 
-__global__ void __launch_bounds__(1024) k_fact_sep(FactParams f, int nslots) {
-  extern __shared__ double S[];
-  for (int t = threadIdx.x; t < nslots; t += blockDim.x) S[t] = f.F_val[f.sb_src[t]];
-  __syncthreads();
-  const int sb0 = f.seg_row_off[f.nblk];
-  for (int a = 0; a < f.ns; ++a) {
-    const double piv = S[f.sb_diag[a]];
-    const double di = 1.0 / piv;
-    if (threadIdx.x == 0) {
-      const int k = f.row_global[sb0 + a];
-      f.dinv[k] = di;
-      if (!(fabs(piv) > f.pivtol * f.rowmax[k])) atomicMax(f.status, k + 1);
+// ----------------------------------------------------------------------------
+// Separator block: after R_B1 the separator rows' separator-column entries hold
+// the Schur complement S = A_ss - L_sb U_bs.  It is densified and inverted in
+// place by blocked Gauss-Jordan elimination with static (diagonal) pivots, the
+// same pivots the up-looking factorization would use (R15): the
+// separator's ~100-level triangular chains then become one dense product per
+// batch (k_sep_gemm).  Panel width GJB; per panel three launches.
+// ----------------------------------------------------------------------------
+constexpr int GJB = 32;
+
+__global__ void k_sep_dense(int nslots, const int *__restrict__ src, const int *__restrict__ dpos,
+                            const double *__restrict__ F, double *S) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nslots) S[dpos[t]] = F[src[t]];
+}
+
+// Gauss-Jordan inverse of the b x b (b <= 32) diagonal block of panel K by one
+// warp: lane j holds column j of D in registers; pivot rows and columns move by
+// shuffles.  Static pivots, checked against the separator row's original max.
+__device__ __forceinline__ void gj_invert_diag(const double *S, int ns, int K, int b, double (&d)[GJB], const double *rowmax,
+                                               const int *sep_rows, int *status, double pivtol, bool check) {
+  const int j = threadIdx.x & 31;
+#pragma unroll
+  for (int i = 0; i < GJB; ++i) d[i] = (i < b && j < b) ? S[(long long)(K + i) * ns + K + j] : (i == j ? 1.0 : 0.0);
+#pragma unroll
+  for (int k = 0; k < GJB; ++k) {
+    const double piv = __shfl_sync(0xffffffffu, d[k], k);
+    const double inv = 1.0 / piv;
+    if (check && j == 0 && k < b) {
+      const int row = sep_rows[K + k];
+      if (!(fabs(piv) > pivtol * rowmax[row])) atomicMax(status, row + 1);
     }
-    for (int t = f.sb_lptr[a] + threadIdx.x; t < f.sb_lptr[a + 1]; t += blockDim.x) S[f.sb_lslot[t]] *= di;
-    __syncthreads();
-    for (int t = f.sb_uptr[a] + threadIdx.x; t < f.sb_uptr[a + 1]; t += blockDim.x) {
-      const int *tr = f.sb_trip + 3 * t;
-      S[tr[2]] -= S[tr[0]] * S[tr[1]];
+    const double rk = j == k ? inv : d[k] * inv;  // new pivot row, column j
+#pragma unroll
+    for (int i = 0; i < GJB; ++i) {
+      if (i == k) continue;
+      const double f = __shfl_sync(0xffffffffu, d[i], k);  // D[i][k]
+      d[i] = j == k ? -f * inv : fma(-f, rk, d[i]);
     }
-    __syncthreads();
+    d[k] = rk;
   }
-  for (int t = threadIdx.x; t < nslots; t += blockDim.x) f.F_val[f.sb_src[t]] = S[t];
+}
+
+// E -= C * (Dinv * Rp) for every element outside the panel rows / columns.
+// Every CTA inverts the diagonal block itself (warp 0, registers); CTA (0,0)
+// publishes Dinv for k_gj_panel.  64 x 64 tile, 4 x 4 outputs per thread.
+__global__ void __launch_bounds__(256) k_gj_update(double *S, int ns, int K, double *Dinv_out, const double *rowmax,
+                                                   const int *sep_rows, int *status, double pivtol) {
+  __shared__ double Ds[GJB][GJB + 1];
+  __shared__ double Cs[GJB][64 + 1];    // C^T: Cs[k][r] = S[i0 + r][K + k]
+  __shared__ double Ps[GJB][64 + 1];    // panel rows: Ps[k][c] = S[K + k][j0 + c], then R = Dinv * Ps
+  const int b = min(GJB, ns - K);
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    double d[GJB];
+    const bool lead = blockIdx.x == 0 && blockIdx.y == 0;
+    gj_invert_diag(S, ns, K, b, d, rowmax, sep_rows, status, pivtol, lead);
+#pragma unroll
+    for (int i = 0; i < GJB; ++i) {
+      Ds[i][tid] = d[i];
+      if (lead) Dinv_out[i * GJB + tid] = d[i];
+    }
+  }
+  for (int t = tid; t < 64 * GJB; t += 256) {
+    const int r = t / GJB, k = t % GJB;  // coalesced over k within a row
+    const int gi = i0 + r;
+    Cs[k][r] = (gi < ns && k < b) ? S[(long long)gi * ns + K + k] : 0.0;
+    const int k2 = t / 64, c = t % 64;   // coalesced over c
+    const int gj = j0 + c;
+    Ps[k2][c] = (k2 < b && gj < ns) ? S[(long long)(K + k2) * ns + gj] : 0.0;
+  }
+  __syncthreads();
+  double rr[GJB * 64 / 256];
+#pragma unroll
+  for (int u = 0; u < GJB * 64 / 256; ++u) {
+    const int t = tid + u * 256;
+    const int k = t / 64, c = t % 64;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int m = 0; m < GJB; ++m) acc = fma(Ds[k][m], Ps[m][c], acc);
+    rr[u] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < GJB * 64 / 256; ++u) {
+    const int t = tid + u * 256;
+    Ps[t / 64][t % 64] = rr[u];
+  }
+  __syncthreads();
+  const int tx = tid % 16, ty = tid / 16;
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < GJB; ++k) {
+    double cv[4], rv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cv[u] = Cs[k][ty + 16 * u];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) rv[v] = Ps[k][tx + 16 * v];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = fma(cv[u], rv[v], acc[u][v]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int gi = i0 + ty + 16 * u;
+    if (gi >= ns || (gi >= K && gi < K + b)) continue;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int gj = j0 + tx + 16 * v;
+      if (gj >= ns || (gj >= K && gj < K + b)) continue;
+      S[(long long)gi * ns + gj] -= acc[u][v];
+    }
+  }
+}
+
+// panel rows S[K, t] = Dinv * S[K, t] and panel columns S[t, K] = -S[t, K] * Dinv
+// for a 32-wide tile of t (outside the panel); the diagonal block becomes Dinv.
+__global__ void __launch_bounds__(256) k_gj_panel(double *S, int ns, int K, const double *__restrict__ Dinv) {
+  __shared__ double Ds[GJB][GJB + 1];
+  __shared__ double T[GJB][GJB + 1];
+  const int b = min(GJB, ns - K);
+  const int t0 = blockIdx.x * GJB;
+  const int tid = threadIdx.x;
+  for (int t = tid; t < GJB * GJB; t += 256) Ds[t / GJB][t % GJB] = Dinv[t];
+  if (t0 >= K && t0 < K + b) {  // the diagonal block
+    __syncthreads();
+    for (int t = tid; t < GJB * GJB; t += 256) {
+      const int r = t / GJB, c = t % GJB;
+      if (r < b && c < b) S[(long long)(K + r) * ns + K + c] = Ds[r][c];
+    }
+    return;
+  }
+  // panel rows: T[k][c] = S[K + k][t0 + c]
+  for (int t = tid; t < GJB * GJB; t += 256) {
+    const int k = t / GJB, c = t % GJB;
+    T[k][c] = (k < b && t0 + c < ns) ? S[(long long)(K + k) * ns + t0 + c] : 0.0;
+  }
+  __syncthreads();
+  for (int t = tid; t < GJB * GJB; t += 256) {
+    const int k = t / GJB, c = t % GJB;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int m = 0; m < GJB; ++m) acc = fma(Ds[k][m], T[m][c], acc);
+    if (k < b && t0 + c < ns) S[(long long)(K + k) * ns + t0 + c] = acc;
+  }
+  __syncthreads();
+  // panel columns: T[r][k] = S[t0 + r][K + k]
+  for (int t = tid; t < GJB * GJB; t += 256) {
+    const int r = t / GJB, k = t % GJB;
+    T[r][k] = (k < b && t0 + r < ns) ? S[(long long)(t0 + r) * ns + K + k] : 0.0;
+  }
+  __syncthreads();
+  for (int t = tid; t < GJB * GJB; t += 256) {
+    const int r = t / GJB, k = t % GJB;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int m = 0; m < GJB; ++m) acc = fma(T[r][m], Ds[m][k], acc);
+    if (k < b && t0 + r < ns) S[(long long)(t0 + r) * ns + K + k] = -acc;
+  }
+}
+
+__global__ void k_transpose(const double *__restrict__ A, double *AT, int n) {
+  __shared__ double tile[32][33];
+  const int x = blockIdx.x * 32 + threadIdx.x, y0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y)
+    if (x < n && y0 + r < n) tile[r][threadIdx.x] = A[(long long)(y0 + r) * n + x];
+  __syncthreads();
+  const int xo = blockIdx.y * 32 + threadIdx.x, yo0 = blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y)
+    if (xo < n && yo0 + r < n) AT[(long long)(yo0 + r) * n + xo] = tile[threadIdx.x][r];
 }
 
 // copy factor values into the sweep value arrays (entry order of the sweeps)
@@ -663,39 +817,6 @@ __global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
   }
 }
 
-// Dense inverse of the separator block S = L_ss U_ss, column by column: one
-// warp per column j solves L_ss U_ss x = e_j by forward then backward
-// substitution over the separator's local entries in level order.  Writes
-// S^-1 (row-major) and its transpose.  Once per state.
-__global__ void __launch_bounds__(kThreads) k_sep_inverse(SegParams h, double *Sinv, double *SinvT) {
-  extern __shared__ double sx[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kThreads / 32;
-  const int j = blockIdx.x * nw + warp;  // column
-  if (j >= h.ns) return;
-  const int ns = h.ns, seg = h.nblk;
-  double *x = sx + warp * ns;
-  for (int r = lane; r < ns; r += 32) x[r] = r == j ? 1.0 : 0.0;
-  __syncwarp();
-  for (int which = 0; which < 2; ++which) {
-    const DSeg &S = which == 0 ? h.fwd : h.bwd;
-    const double *val = which == 0 ? h.vL : h.vU;
-    const int l0 = S.seg_lvl[seg], l1 = S.seg_lvl[seg + 1] - 1;
-    for (int l = l0; l < l1; ++l) {
-      for (int q = S.lvl_ptr[l] + lane; q < S.lvl_ptr[l + 1]; q += 32) {
-        const int a = S.order[q];
-        double v = x[a];
-        for (int e = S.rext[q]; e < S.rptr[q + 1]; ++e) v -= val[e] * x[S.dep[e]];
-        if (which == 1) v *= h.dinv_bwd[q];
-        x[a] = v;
-      }
-      __syncwarp();
-    }
-  }
-  for (int r = lane; r < ns; r += 32) {
-    Sinv[(long long)r * ns + j] = x[r];
-    SinvT[(long long)j * ns + r] = x[r];
-  }
-}
 
 // ============================================================================
 // BatchTensorProjection (Eq. so_model)
@@ -941,7 +1062,8 @@ struct rh_ctx {
   int nnz_fwd = 0, nnz_bwd = 0;
   // refactorization schedule
   int *blk_fo_off, *fo, *ks_ptr, *ks_pos, *ks_k, *ks_kf, *ks_ulen, *ks_tgt, *tgt;
-  int *sb_src, *sb_diag, *sb_lptr, *sb_lslot, *sb_uptr, *sb_trip;
+  int *sb_src, *sb_dense;
+  double *gj_dinv;
   double *dinv_rows, *rowmax;
   double *Sinv = nullptr, *SinvT = nullptr;
   size_t smem_fact_blk = 0, smem_fact_sep = 0, smem_seg_blk = 0, smem_seg_blk1 = 0;
@@ -1039,8 +1161,7 @@ int upload(rh_ctx *c) {
   UP(fwd_dsrc, A.fwd.dsrc); UP(bwd_dsrc, A.bwd.dsrc);
   UP(blk_fo_off, A.blk_fo_off); UP(fo, A.fo); UP(ks_ptr, A.ks_ptr); UP(ks_pos, A.ks_pos); UP(ks_k, A.ks_k);
   UP(ks_kf, A.ks_kf); UP(ks_ulen, A.ks_ulen); UP(ks_tgt, A.ks_tgt); UP(tgt, A.tgt);
-  UP(sb_src, A.sb_src); UP(sb_diag, A.sb_diag); UP(sb_lptr, A.sb_lptr); UP(sb_lslot, A.sb_lslot);
-  UP(sb_uptr, A.sb_uptr); UP(sb_trip, A.sb_trip);
+  UP(sb_src, A.sb_src); UP(sb_dense, A.sb_dense);
 #undef UP
   auto mkseg = [&](DSeg &D, const SegSweep &S0) {
     SegSweep S = S0;
@@ -1114,18 +1235,16 @@ int upload(rh_ctx *c) {
   const size_t ns2 = (size_t)A.sep_rows * A.sep_rows;
   chk(c->Sinv = dalloc<double>(ns2, P));
   chk(c->SinvT = dalloc<double>(ns2, P));
+  chk(c->gj_dinv = dalloc<double>(GJB * GJB, P));
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
   // shared-memory footprints
   c->smem_fact_blk = (size_t)(A.max_blk_fnnz + A.rmax) * sizeof(double);
-  c->smem_fact_sep = std::max<size_t>(1, A.sb_src.size()) * sizeof(double);
   c->smem_seg_blk = seg_smem_max(A, 32 * c->cpl);
   c->smem_seg_blk1 = seg_smem_max(A, kSegC);
   cudaFuncSetAttribute(k_fact_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  cudaFuncSetAttribute(k_fact_sep, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaFuncSetAttribute(k_seg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaFuncSetAttribute(k_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaFuncSetAttribute(k_seg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  cudaFuncSetAttribute(k_sep_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(c, RH_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
@@ -1418,7 +1537,7 @@ int rh_load_grid(rh_ctx *c, const rh_grid *g, int32_t *n_x, int32_t *n_p) {
     if (!msg.empty()) return fail(c, RH_E_GRID, msg);
     const Analysis &A = c->A;
     const size_t lim = (size_t)kSmemMax;
-    fits = A.sb_src.size() * sizeof(double) <= lim &&
+    fits =
            (size_t)8 * A.sep_rows * sizeof(double) <= lim && seg_smem_max(A, 32 * c->cpl) <= lim &&
            seg_smem_max(A, kSegC) <= lim &&
            (size_t)(A.max_blk_fnnz + A.rmax) * sizeof(double) <= lim;
@@ -1569,12 +1688,6 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   f.ks_ulen = c->ks_ulen;
   f.ks_tgt = c->ks_tgt;
   f.tgt = c->tgt;
-  f.sb_src = c->sb_src;
-  f.sb_diag = c->sb_diag;
-  f.sb_lptr = c->sb_lptr;
-  f.sb_lslot = c->sb_lslot;
-  f.sb_uptr = c->sb_uptr;
-  f.sb_trip = c->sb_trip;
   f.dinv = c->dinv_rows;
   f.rowmax = c->rowmax;
   f.status = c->status;
@@ -1584,7 +1697,21 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   if (A.sep_rows > 0) {
     k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, 0, st>>>(f);
     RH_LAUNCHED(c);
-    k_fact_sep<<<1, 1024, c->smem_fact_sep, st>>>(f, (int)A.sb_src.size());
+    // dense Schur complement of the separator, inverted by blocked Gauss-Jordan
+    const int ns = A.sep_rows;
+    RH_CUDA(c, cudaMemsetAsync(c->Sinv, 0, sizeof(double) * (size_t)ns * ns, st));
+    const int nsl = (int)A.sb_src.size();
+    k_sep_dense<<<nblk(nsl), kThreads, 0, st>>>(nsl, c->sb_src, c->sb_dense, c->F_val, c->Sinv);
+    RH_LAUNCHED(c);
+    const int nt = (ns + 63) / 64;
+    for (int K = 0; K < ns; K += GJB) {
+      k_gj_update<<<dim3(nt, nt), 256, 0, st>>>(c->Sinv, ns, K, c->gj_dinv, c->rowmax,
+                                                 c->row_global + A.seg_row_off[A.nblk], c->status, 1e-14);
+      RH_LAUNCHED(c);
+      k_gj_panel<<<(ns + GJB - 1) / GJB, 256, 0, st>>>(c->Sinv, ns, K, c->gj_dinv);
+      RH_LAUNCHED(c);
+    }
+    k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
     RH_LAUNCHED(c);
   }
   struct G {
@@ -1606,13 +1733,6 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   const int ngp = (int)A.gp_col.size();
   if (ngp > 0) {
     k_gather_vals<<<nblk(ngp), kThreads, 0, st>>>(ngp, c->gpc_pos, c->gp_val, c->gpc_val);
-    RH_LAUNCHED(c);
-  }
-  if (A.sep_rows > 0) {
-    SegParams h = make_params(c);
-    const int nw = kThreads / 32;
-    k_sep_inverse<<<(A.sep_rows + nw - 1) / nw, kThreads, (size_t)nw * A.sep_rows * sizeof(double), st>>>(
-        h, c->Sinv, c->SinvT);
     RH_LAUNCHED(c);
   }
   int status = 0;
