@@ -14,6 +14,7 @@
 #include "analysis.hpp"
 
 #include <algorithm>
+#include <cstdint>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -422,33 +423,40 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
     A.max_blk_fnnz = std::max(A.max_blk_fnnz, off);
   }
   A.blk_fo_off[nb] = (int)A.fo.size();
+  // k-steps in SEGMENT order (q = position in row_global): a block's k-steps and
+  // target offsets are contiguous, so R_A stages them in shared memory
   A.ks_ptr.assign(nx + 1, 0);
-  A.ks_pos.clear();
+  A.ks4.clear();
   A.ks_k.clear();
-  A.ks_kf.clear();
-  A.ks_ulen.clear();
-  A.ks_tgt.clear();
-  A.tgt.clear();
-  for (int i = 0; i < nx; ++i) {
+  A.tgt16.clear();
+  A.max_blk_ks = A.max_blk_tgt = 0;
+  for (int q = 0; q < nx; ++q) {
+    const int i = A.row_global[q];
     const int si = A.seg_of[i];
     const int rb = A.F_rowptr[i];
     for (int k : Lrow[i]) {
       const int sk = A.seg_of[k];
-      if (si == nb && sk == nb) continue;  // separator x separator: R_B2 (right-looking)
-      A.ks_pos.push_back(fpos(i, k) - rb);
-      if (si < nb) {  // R_A: k in the same block
-        A.ks_k.push_back(A.loc_of[k]);
-        A.ks_kf.push_back(fo_of[k] + (A.F_diag[k] - A.F_rowptr[k]));
-      } else {        // R_B1: k in a block, row i in the separator
-        A.ks_k.push_back(k);
-        A.ks_kf.push_back(A.F_diag[k]);
-      }
+      if (si == nb && sk == nb) continue;  // separator x separator: dense Gauss-Jordan
       const int ub = A.F_diag[k] + 1, ue = A.F_rowptr[k + 1];
-      A.ks_ulen.push_back(ue - ub);
-      A.ks_tgt.push_back((int)A.tgt.size());
-      for (int u = ub; u < ue; ++u) A.tgt.push_back(fpos(i, A.F_col[u]) - rb);
+      const int kf = si < nb ? fo_of[k] + (A.F_diag[k] - A.F_rowptr[k]) : A.F_diag[k];
+      A.ks4.push_back(fpos(i, k) - rb);
+      A.ks4.push_back(kf);
+      A.ks4.push_back(ue - ub);
+      A.ks4.push_back((int)A.tgt16.size());
+      A.ks_k.push_back(si < nb ? A.loc_of[k] : k);
+      for (int u = ub; u < ue; ++u) A.tgt16.push_back((uint16_t)(fpos(i, A.F_col[u]) - rb));
     }
-    A.ks_ptr[i + 1] = (int)A.ks_pos.size();
+    A.ks_ptr[q + 1] = (int)A.ks_k.size();
+  }
+  for (int s = 0; s < nb; ++s) {
+    const int q0 = A.seg_row_off[s], q1 = A.seg_row_off[s + 1];
+    const int k0 = A.ks_ptr[q0], k1 = A.ks_ptr[q1];
+    A.max_blk_ks = std::max(A.max_blk_ks, k1 - k0);
+    if (k1 > k0) {
+      const int t0 = A.ks4[4 * k0 + 3];
+      const int t1 = A.ks4[4 * (k1 - 1) + 3] + A.ks4[4 * (k1 - 1) + 2];
+      A.max_blk_tgt = std::max(A.max_blk_tgt, t1 - t0);
+    }
   }
   // R_B2: separator x separator entries, right-looking in separator order
   const int sb0 = A.seg_row_off[nb];

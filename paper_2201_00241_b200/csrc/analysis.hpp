@@ -115,14 +115,13 @@ struct Analysis {
   std::vector<int32_t> blk_fo_off;          // [nblk + 1] offset into fo (rows of the block, local order)
   std::vector<int32_t> fo;                  // [n_block_rows + nblk] smem offsets of each block row (+ end)
   int max_blk_fnnz = 0;
-  // per row (ks range by permuted global row): k-steps of the up-looking elimination
+  // k-steps of the up-looking elimination, by SEGMENT position q (row_global order)
   std::vector<int32_t> ks_ptr;              // [n_x + 1]
-  std::vector<int32_t> ks_pos;              // offset of column k inside row i
+  std::vector<int32_t> ks4;                 // per k-step: (offset of column k in row i, pivot of row k
+                                            //  (R_A: smem offset / R_B1: F position), U length of row k, tgt start)
   std::vector<int32_t> ks_k;                // k: block-local index (R_A) or global row (R_B1)
-  std::vector<int32_t> ks_kf;               // R_A: smem offset of row k's pivot; R_B1: F position of the pivot
-  std::vector<int32_t> ks_ulen;             // number of U entries of row k
-  std::vector<int32_t> ks_tgt;              // start in tgt
-  std::vector<int32_t> tgt;                 // offsets inside row i of the U columns of row k
+  std::vector<uint16_t> tgt16;              // offsets inside row i of the U columns of row k
+  int max_blk_ks = 0, max_blk_tgt = 0;
   // separator block S (Schur complement after R_B1), densified for its inversion
   std::vector<int32_t> sb_src;              // [nslots] F positions of separator-column entries of separator rows
   std::vector<int32_t> sb_dense;            // [nslots] row-major position in the dense ns x ns block

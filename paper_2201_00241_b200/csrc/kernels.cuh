@@ -12,6 +12,7 @@
 namespace rh {
 
 constexpr int kThreads = 256;
+constexpr int kSegThreads = 512;   // block kernels: 16 warps (must match the host schedule's kSchedWarps)
 
 // One dependency pattern (forward: L / U^T, backward: U / L^T) split into
 // elimination-tree segments (blocks + separator), each with its own levels.
@@ -67,7 +68,8 @@ struct FactParams {
   const int *blk_fo_off, *fo;
   const int *F_rowptr, *F_diag;
   double *F_val;
-  const int *ks_ptr, *ks_pos, *ks_k, *ks_kf, *ks_ulen, *ks_tgt, *tgt;
+  const int *ks_ptr, *ks4, *ks_k;
+  const unsigned short *tgt16;
   double *dinv, *rowmax;             // per permuted row
   int *status;
   double pivtol;

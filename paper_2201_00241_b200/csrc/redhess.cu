@@ -204,40 +204,65 @@ __global__ void k_objective(int n_bus, int ref, const int *has_gen, const double
 // Every entry receives its updates in a fixed order: deterministic.
 // ============================================================================
 
-__global__ void __launch_bounds__(kThreads) k_fact_blocks(FactParams f) {
+// R_A: one CTA (16 warps) per block.  The block's F rows, its k-step records
+// and target offsets are staged in shared memory; rows follow the block's
+// forward subtree-to-warp schedule (the same one as the L / U^T sweeps: row i
+// depends on Lrow(i), its descendants), so a warp eliminates its subtrees
+// without CTA barriers (warp lanes split every row update; __syncwarp orders
+// the rows of one warp).
+__global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   extern __shared__ double sm[];
   const int s = blockIdx.x;
   const int r0 = f.seg_row_off[s], nr = f.seg_row_off[s + 1] - r0;
   const int fb = f.blk_fo_off[s];
+  const int kb = f.ks_ptr[r0], nks = f.ks_ptr[r0 + nr] - kb;
+  const int tb = nks > 0 ? f.ks4[4 * kb + 3] : 0;
+  const int ntg = nks > 0 ? f.ks4[4 * (kb + nks - 1) + 3] + f.ks4[4 * (kb + nks - 1) + 2] - tb : 0;
   double *SF = sm;                                   // [fo end]
-  double *sdinv = sm + f.fo[fb + nr];                // [nr]
+  double *sdinv = SF + f.fo[fb + nr];                // [nr]
+  const int d_end = (f.fo[fb + nr] + nr + 1) & ~1;   // 16-byte boundary for the int4 records
+  int4 *sks = reinterpret_cast<int4 *>(SF + d_end);
+  int *skk = reinterpret_cast<int *>(sks + nks);
+  unsigned short *stg = reinterpret_cast<unsigned short *>(skk + nks);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int a = warp; a < nr; a += nw) {
     const int i = f.row_global[r0 + a];
     const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off, rb = f.F_rowptr[i];
     for (int t = lane; t < len; t += 32) SF[off + t] = f.F_val[rb + t];
   }
+  const int4 *gks = reinterpret_cast<const int4 *>(f.ks4);
+  for (int t = threadIdx.x; t < nks; t += blockDim.x) {
+    int4 v = gks[kb + t];
+    v.w -= tb;
+    sks[t] = v;
+    skk[t] = f.ks_k[kb + t];
+  }
+  for (int t = threadIdx.x; t < ntg; t += blockDim.x) stg[t] = f.tgt16[tb + t];
   __syncthreads();
   const int l0 = f.fwd_seg_lvl[s], l1 = f.fwd_seg_lvl[s + 1] - 1;
-  for (int l = l0; l < l1; ++l) {
-    const int q0 = f.fwd_lvl_ptr[l], q1 = f.fwd_lvl_ptr[l + 1];
-    for (int q = q0 + warp; q < q1; q += nw) {
+  const int nsl = (l1 - l0) / nw;
+  for (int sl = 0; sl < nsl; ++sl) {
+    const int q1 = f.fwd_lvl_ptr[l0 + sl * nw + warp + 1];
+    for (int q = f.fwd_lvl_ptr[l0 + sl * nw + warp]; q < q1; ++q) {
       const int a = f.fwd_order[q];
       const int i = f.row_global[r0 + a];
       const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off;
+      double *w = SF + off;
       double amax = 0.0;
-      for (int t = lane; t < len; t += 32) amax = fmax(amax, fabs(SF[off + t]));
+      for (int t = lane; t < len; t += 32) amax = fmax(amax, fabs(w[t]));
       amax = warp_max(amax);
-      for (int ks = f.ks_ptr[i]; ks < f.ks_ptr[i + 1]; ++ks) {
-        const int pos = f.ks_pos[ks];
-        const double lik = SF[off + pos] * sdinv[f.ks_k[ks]];
+      const int k1 = f.ks_ptr[r0 + a + 1] - kb;
+      for (int ks = f.ks_ptr[r0 + a] - kb; ks < k1; ++ks) {
+        const int4 m = sks[ks];
+        const double lik = w[m.x] * sdinv[skk[ks]];
         __syncwarp();
-        if (lane == 0) SF[off + pos] = lik;
-        const int kf = f.ks_kf[ks] + 1, ulen = f.ks_ulen[ks], t0 = f.ks_tgt[ks];
-        for (int t = lane; t < ulen; t += 32) SF[off + f.tgt[t0 + t]] -= lik * SF[kf + t];
+        if (lane == 0) w[m.x] = lik;
+        const double *uk = SF + m.y + 1;
+        const unsigned short *tg = stg + m.w;
+        for (int t = lane; t < m.z; t += 32) w[tg[t]] -= lik * uk[t];
         __syncwarp();
       }
-      const double piv = SF[off + (f.F_diag[i] - f.F_rowptr[i])];
+      const double piv = w[f.F_diag[i] - f.F_rowptr[i]];
       if (lane == 0) {
         const double di = 1.0 / piv;
         sdinv[a] = di;
@@ -255,25 +280,30 @@ __global__ void __launch_bounds__(kThreads) k_fact_blocks(FactParams f) {
   }
 }
 
+// R_B1: one warp per separator row: the updates from block columns (rows of
+// blocks are final).  Afterwards the separator x separator entries hold the
+// Schur complement.
 __global__ void __launch_bounds__(kThreads) k_fact_sep_rows(FactParams f) {
   const int lane = threadIdx.x & 31;
   const int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= f.ns) return;
-  const int i = f.row_global[f.seg_row_off[f.nblk] + a];
+  const int q = f.seg_row_off[f.nblk] + a;
+  const int i = f.row_global[q];
   const int rb = f.F_rowptr[i], re = f.F_rowptr[i + 1];
   double *w = f.F_val + rb;
   double amax = 0.0;
   for (int e = rb + lane; e < re; e += 32) amax = fmax(amax, fabs(f.F_val[e]));
   amax = warp_max(amax);
   if (lane == 0) f.rowmax[i] = amax;
-  for (int ks = f.ks_ptr[i]; ks < f.ks_ptr[i + 1]; ++ks) {
-    const int pos = f.ks_pos[ks];
-    const double lik = w[pos] * f.dinv[f.ks_k[ks]];
+  const int4 *gks = reinterpret_cast<const int4 *>(f.ks4);
+  for (int ks = f.ks_ptr[q]; ks < f.ks_ptr[q + 1]; ++ks) {
+    const int4 m = gks[ks];
+    const double lik = w[m.x] * f.dinv[f.ks_k[ks]];
     __syncwarp();
-    if (lane == 0) w[pos] = lik;
-    const double *uk = f.F_val + f.ks_kf[ks] + 1;
-    const int ulen = f.ks_ulen[ks], t0 = f.ks_tgt[ks];
-    for (int t = lane; t < ulen; t += 32) w[f.tgt[t0 + t]] -= lik * uk[t];
+    if (lane == 0) w[m.x] = lik;
+    const double *uk = f.F_val + m.y + 1;
+    const unsigned short *tg = f.tgt16 + m.w;
+    for (int t = lane; t < m.z; t += 32) w[tg[t]] -= lik * uk[t];
     __syncwarp();
   }
 }
@@ -295,53 +325,55 @@ __global__ void k_sep_dense(int nslots, const int *__restrict__ src, const int *
 }
 
 // Gauss-Jordan inverse of the b x b (b <= 32) diagonal block of panel K by one
-// warp: lane j holds column j of D in registers; pivot rows and columns move by
-// shuffles.  Static pivots, checked against the separator row's original max.
-__device__ __forceinline__ void gj_invert_diag(const double *S, int ns, int K, int b, double (&d)[GJB], const double *rowmax,
-                                               const int *sep_rows, int *status, double pivtol, bool check) {
+// warp: D in shared memory, lane j updates column j, __syncwarp between
+// pivots.  Static pivots, checked against the separator row's original max.
+__device__ __forceinline__ void gj_diag_warp(const double *S, int ns, int K, double *Dinv, const double *rowmax,
+                                             const int *sep_rows, int *status, double pivtol) {
+  __shared__ double D[GJB][GJB + 1];
   const int j = threadIdx.x & 31;
-#pragma unroll
-  for (int i = 0; i < GJB; ++i) d[i] = (i < b && j < b) ? S[(long long)(K + i) * ns + K + j] : (i == j ? 1.0 : 0.0);
-#pragma unroll
+  const int b = min(GJB, ns - K);
+  for (int i = 0; i < GJB; ++i) D[i][j] = (i < b && j < b) ? S[(long long)(K + i) * ns + K + j] : (i == j ? 1.0 : 0.0);
+  __syncwarp();
   for (int k = 0; k < GJB; ++k) {
-    const double piv = __shfl_sync(0xffffffffu, d[k], k);
+    const double piv = D[k][k];
     const double inv = 1.0 / piv;
-    if (check && j == 0 && k < b) {
+    if (j == 0 && k < b) {
       const int row = sep_rows[K + k];
       if (!(fabs(piv) > pivtol * rowmax[row])) atomicMax(status, row + 1);
     }
-    const double rk = j == k ? inv : d[k] * inv;  // new pivot row, column j
+    const double rk = j == k ? inv : D[k][j] * inv;  // new pivot row, column j
+    double fk[GJB], dj[GJB];
 #pragma unroll
-    for (int i = 0; i < GJB; ++i) {
-      if (i == k) continue;
-      const double f = __shfl_sync(0xffffffffu, d[i], k);  // D[i][k]
-      d[i] = j == k ? -f * inv : fma(-f, rk, d[i]);
+    for (int i = 0; i < GJB; ++i) {  // all loads first (independent), then the updates
+      fk[i] = D[i][k];
+      dj[i] = D[i][j];
     }
-    d[k] = rk;
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < GJB; ++i)
+      if (i != k) D[i][j] = j == k ? -fk[i] * inv : fma(-fk[i], rk, dj[i]);
+    D[k][j] = rk;
+    __syncwarp();
   }
+  for (int i = 0; i < GJB; ++i) Dinv[i * GJB + j] = D[i][j];
+}
+
+__global__ void __launch_bounds__(32) k_gj_diag(const double *S, int ns, int K, double *Dinv, const double *rowmax,
+                                                const int *sep_rows, int *status, double pivtol) {
+  gj_diag_warp(S, ns, K, Dinv, rowmax, sep_rows, status, pivtol);
 }
 
 // E -= C * (Dinv * Rp) for every element outside the panel rows / columns.
 // Every CTA inverts the diagonal block itself (warp 0, registers); CTA (0,0)
 // publishes Dinv for k_gj_panel.  64 x 64 tile, 4 x 4 outputs per thread.
-__global__ void __launch_bounds__(256) k_gj_update(double *S, int ns, int K, double *Dinv_out, const double *rowmax,
-                                                   const int *sep_rows, int *status, double pivtol) {
+__global__ void __launch_bounds__(256) k_gj_update(double *S, int ns, int K, const double *__restrict__ Dinv) {
   __shared__ double Ds[GJB][GJB + 1];
   __shared__ double Cs[GJB][64 + 1];    // C^T: Cs[k][r] = S[i0 + r][K + k]
   __shared__ double Ps[GJB][64 + 1];    // panel rows: Ps[k][c] = S[K + k][j0 + c], then R = Dinv * Ps
   const int b = min(GJB, ns - K);
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
   const int tid = threadIdx.x;
-  if (tid < 32) {
-    double d[GJB];
-    const bool lead = blockIdx.x == 0 && blockIdx.y == 0;
-    gj_invert_diag(S, ns, K, b, d, rowmax, sep_rows, status, pivtol, lead);
-#pragma unroll
-    for (int i = 0; i < GJB; ++i) {
-      Ds[i][tid] = d[i];
-      if (lead) Dinv_out[i * GJB + tid] = d[i];
-    }
-  }
+  for (int t = tid; t < GJB * GJB; t += 256) Ds[t / GJB][t % GJB] = Dinv[t];
   for (int t = tid; t < 64 * GJB; t += 256) {
     const int r = t / GJB, k = t % GJB;  // coalesced over k within a row
     const int gi = i0 + r;
@@ -401,12 +433,18 @@ __global__ void __launch_bounds__(256) k_gj_update(double *S, int ns, int K, dou
 
 // panel rows S[K, t] = Dinv * S[K, t] and panel columns S[t, K] = -S[t, K] * Dinv
 // for a 32-wide tile of t (outside the panel); the diagonal block becomes Dinv.
-__global__ void __launch_bounds__(256) k_gj_panel(double *S, int ns, int K, const double *__restrict__ Dinv) {
+__global__ void __launch_bounds__(256) k_gj_panel(double *S, int ns, int K, const double *__restrict__ Dinv,
+                                                  double *Dnext, const double *rowmax, const int *sep_rows,
+                                                  int *status, double pivtol) {
   __shared__ double Ds[GJB][GJB + 1];
   __shared__ double T[GJB][GJB + 1];
   const int b = min(GJB, ns - K);
-  const int t0 = blockIdx.x * GJB;
   const int tid = threadIdx.x;
+  if (blockIdx.x == gridDim.x - 1) {  // the next panel's diagonal block: final after this panel's update
+    if (tid < 32 && K + GJB < ns) gj_diag_warp(S, ns, K + GJB, Dnext, rowmax, sep_rows, status, pivtol);
+    return;
+  }
+  const int t0 = blockIdx.x * GJB;
   for (int t = tid; t < GJB * GJB; t += 256) Ds[t / GJB][t % GJB] = Dinv[t];
   if (t0 >= K && t0 < K + b) {  // the diagonal block
     __syncthreads();
@@ -496,7 +534,6 @@ __device__ __forceinline__ long long hw_index(const SegParams &h, int row, int c
 // contiguous (conflict-free).  External entries (separator rows of Z / P in
 // the backward sweeps) are read from L2/HBM.
 // ----------------------------------------------------------------------------
-constexpr int kSegThreads = 512;
 constexpr int kSegC = 32;   // columns of the single-RHS (lambda) path
 
 struct SegStage {  // shared-memory carve-up of one block sweep
@@ -1061,7 +1098,8 @@ struct rh_ctx {
   double *vL, *vUt, *vU, *vLt, *dinv_fwd, *dinv_bwd;
   int nnz_fwd = 0, nnz_bwd = 0;
   // refactorization schedule
-  int *blk_fo_off, *fo, *ks_ptr, *ks_pos, *ks_k, *ks_kf, *ks_ulen, *ks_tgt, *tgt;
+  int *blk_fo_off, *fo, *ks_ptr, *ks4, *ks_k;
+  unsigned short *tgt16;
   int *sb_src, *sb_dense;
   double *gj_dinv;
   double *dinv_rows, *rowmax;
@@ -1112,6 +1150,10 @@ int fail(rh_ctx *c, int code, const std::string &msg) {
 
 inline int nblk(long long n, int t = kThreads) { return (int)((n + t - 1) / t); }
 
+size_t fact_smem_bytes(const Analysis &A) {
+  return (size_t)(A.max_blk_fnnz + A.rmax + 2) * 8 + (size_t)A.max_blk_ks * 20 + (size_t)A.max_blk_tgt * 2 + 64;
+}
+
 size_t seg_smem_max(const Analysis &A, int C) {
   size_t m = 0;
   for (const SegSweep *S : {&A.fwd, &A.bwd}) {
@@ -1159,8 +1201,8 @@ int upload(rh_ctx *c) {
   UP(blk_gp_ptr, A.blk_gp_ptr); UP(blk_gp_loc, A.blk_gp_loc);
   UP(fwd_src_a, A.fwd.src_a); UP(fwd_src_b, A.fwd.src_b); UP(bwd_src_a, A.bwd.src_a); UP(bwd_src_b, A.bwd.src_b);
   UP(fwd_dsrc, A.fwd.dsrc); UP(bwd_dsrc, A.bwd.dsrc);
-  UP(blk_fo_off, A.blk_fo_off); UP(fo, A.fo); UP(ks_ptr, A.ks_ptr); UP(ks_pos, A.ks_pos); UP(ks_k, A.ks_k);
-  UP(ks_kf, A.ks_kf); UP(ks_ulen, A.ks_ulen); UP(ks_tgt, A.ks_tgt); UP(tgt, A.tgt);
+  UP(blk_fo_off, A.blk_fo_off); UP(fo, A.fo); UP(ks_ptr, A.ks_ptr); UP(ks4, A.ks4); UP(ks_k, A.ks_k);
+  chk(c->tgt16 = reinterpret_cast<unsigned short *>(dalloc_copy(A.tgt16, P)));
   UP(sb_src, A.sb_src); UP(sb_dense, A.sb_dense);
 #undef UP
   auto mkseg = [&](DSeg &D, const SegSweep &S0) {
@@ -1235,10 +1277,10 @@ int upload(rh_ctx *c) {
   const size_t ns2 = (size_t)A.sep_rows * A.sep_rows;
   chk(c->Sinv = dalloc<double>(ns2, P));
   chk(c->SinvT = dalloc<double>(ns2, P));
-  chk(c->gj_dinv = dalloc<double>(GJB * GJB, P));
+  chk(c->gj_dinv = dalloc<double>(2 * GJB * GJB, P));
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
   // shared-memory footprints
-  c->smem_fact_blk = (size_t)(A.max_blk_fnnz + A.rmax) * sizeof(double);
+  c->smem_fact_blk = fact_smem_bytes(A);
   c->smem_seg_blk = seg_smem_max(A, 32 * c->cpl);
   c->smem_seg_blk1 = seg_smem_max(A, kSegC);
   cudaFuncSetAttribute(k_fact_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
@@ -1540,7 +1582,7 @@ int rh_load_grid(rh_ctx *c, const rh_grid *g, int32_t *n_x, int32_t *n_p) {
     fits =
            (size_t)8 * A.sep_rows * sizeof(double) <= lim && seg_smem_max(A, 32 * c->cpl) <= lim &&
            seg_smem_max(A, kSegC) <= lim &&
-           (size_t)(A.max_blk_fnnz + A.rmax) * sizeof(double) <= lim;
+           fact_smem_bytes(A) <= lim;
     if (fits) break;
   }
   if (!fits) return fail(c, RH_E_GRID, "grid too large for the shared-memory segment kernels");
@@ -1673,26 +1715,23 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   f.ns = A.sep_rows;
   f.seg_row_off = c->seg_row_off;
   f.row_global = c->row_global;
-  f.fwd_seg_lvl = c->fact_seg_lvl;
-  f.fwd_lvl_ptr = c->fact_lvl_ptr;
-  f.fwd_order = c->fact_order;
+  f.fwd_seg_lvl = c->dfwd.seg_lvl;   // blocks: forward subtree-to-warp schedule
+  f.fwd_lvl_ptr = c->dfwd.lvl_ptr;
+  f.fwd_order = c->dfwd.order;
   f.blk_fo_off = c->blk_fo_off;
   f.fo = c->fo;
   f.F_rowptr = c->F_rowptr;
   f.F_diag = c->F_diag;
   f.F_val = c->F_val;
   f.ks_ptr = c->ks_ptr;
-  f.ks_pos = c->ks_pos;
   f.ks_k = c->ks_k;
-  f.ks_kf = c->ks_kf;
-  f.ks_ulen = c->ks_ulen;
-  f.ks_tgt = c->ks_tgt;
-  f.tgt = c->tgt;
+  f.ks4 = c->ks4;
+  f.tgt16 = c->tgt16;
   f.dinv = c->dinv_rows;
   f.rowmax = c->rowmax;
   f.status = c->status;
   f.pivtol = 1e-14;
-  k_fact_blocks<<<A.nblk, kThreads, c->smem_fact_blk, st>>>(f);
+  k_fact_blocks<<<A.nblk, kSegThreads, c->smem_fact_blk, st>>>(f);
   RH_LAUNCHED(c);
   if (A.sep_rows > 0) {
     k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, 0, st>>>(f);
@@ -1704,11 +1743,15 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
     k_sep_dense<<<nblk(nsl), kThreads, 0, st>>>(nsl, c->sb_src, c->sb_dense, c->F_val, c->Sinv);
     RH_LAUNCHED(c);
     const int nt = (ns + 63) / 64;
-    for (int K = 0; K < ns; K += GJB) {
-      k_gj_update<<<dim3(nt, nt), 256, 0, st>>>(c->Sinv, ns, K, c->gj_dinv, c->rowmax,
-                                                 c->row_global + A.seg_row_off[A.nblk], c->status, 1e-14);
+    const int *sep_rows = c->row_global + A.seg_row_off[A.nblk];
+    k_gj_diag<<<1, 32, 0, st>>>(c->Sinv, ns, 0, c->gj_dinv, c->rowmax, sep_rows, c->status, 1e-14);
+    RH_LAUNCHED(c);
+    for (int K = 0, ping = 0; K < ns; K += GJB, ping ^= 1) {
+      double *dcur = c->gj_dinv + ping * GJB * GJB, *dnext = c->gj_dinv + (ping ^ 1) * GJB * GJB;
+      k_gj_update<<<dim3(nt, nt), 256, 0, st>>>(c->Sinv, ns, K, dcur);
       RH_LAUNCHED(c);
-      k_gj_panel<<<(ns + GJB - 1) / GJB, 256, 0, st>>>(c->Sinv, ns, K, c->gj_dinv);
+      k_gj_panel<<<(ns + GJB - 1) / GJB + 1, 256, 0, st>>>(c->Sinv, ns, K, dcur, dnext, c->rowmax, sep_rows,
+                                                            c->status, 1e-14);
       RH_LAUNCHED(c);
     }
     k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
