@@ -334,7 +334,11 @@ def main():
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_val = n_p / t_e2e.item()
 
-    # ---- roofline of the dominant kernel (k_hvp, the fused HVP)
+    # ---- roofline of the dominant kernel: k_seg, the shared-memory block sweeps
+    # (4 of the 8 kernels of an Alg. 2 batch).  Algorithmic HBM bytes of one
+    # k_seg launch: read + write of every block row of Z (or P) for the batch,
+    # 2 * (n_x - ns) * N * 8 B.  Per-stage device times
+    # come from CUDA events the library records around each kernel of a batch.
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -342,14 +346,25 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    m2_bytes_per_hvp = (6 * n_x + 5 * n_p) * 8            # SURVEY.md 8(d) model M2
+    ctx.set_timing(True)
+    stage = np.zeros(9)
+    for _ in range(5):
+        ctx.hvp(W, HW)
+        stage += ctx.stage_times()
+    ctx.set_timing(False)
+    stage /= 5
+    seg_ms = stage[[0, 2, 4, 6]]                      # A_L, A_U, A_Ut, A_Lt
+    ns = info["sep_rows"]
+    seg_bytes = 2.0 * (n_x - ns) * N * 8
+    achieved = seg_bytes / (seg_ms.mean() * 1e-3) / 1e9 if seg_ms.mean() > 0 else None
+    m2_bytes_per_hvp = (6 * n_x + 5 * n_p) * 8            # SURVEY.md 8(d) model M2, whole path
     cols_local = j1 - j0
-    achieved = m2_bytes_per_hvp * cols_local / (ms_hess * 1e-3) / 1e9 if ms_hess > 0 else None
+    path_gbs = m2_bytes_per_hvp * cols_local / (ms_hess * 1e-3) / 1e9 if ms_hess > 0 else None
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         key = f"{case}:N={N}"
-        if key in prof:
+        if key in prof and prof[key].get("kernel", "").startswith("k_seg"):
             traffic = prof[key].get("dram_bytes_per_launch")
     except Exception:
         pass
@@ -371,17 +386,24 @@ def main():
                        "n_line": info["n_line"], "n_x": n_x, "n_p": n_p, "N": N,
                        "batches_per_rank": -(-max(cols_local, 1) // N), "parallelism": f"columns{world}",
                        "l2": "flushed (256 MB write) between timed steps" if flush is not None else "not flushed",
-                       "nnz_LU": info["nnz_LU"], "levels": info["levels_fwd"],
+                       "nnz_LU": info["nnz_LU"], "levels": info["levels_fwd"], "blocks": info["n_blocks"],
+                       "separator_rows": info["sep_rows"],
                        "residual_inf": resid_inf},
             "full_hessian_ms": ms_step, "hessian_batches_ms": ms_hess, "state_refactor_grad_ms": ms_pre,
             "batched_hvps_per_s": hvps, "batched_hvp_ms": t_hvp.item(),
             "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": t_e2e.item() * 1e3},
-            "roofline": {"bound": "hbm", "kernel": "k_hvp (fused Alg. 2 per column tile)",
+            "roofline": {"bound": "hbm", "kernel": "k_seg (block triangular sweeps, 4 of 8 kernels per batch)",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "algorithmic_bytes_per_hvp": m2_bytes_per_hvp, "model": "M2 (6 n_x + 5 n_p) * 8 B"},
+                         "algorithmic_bytes_per_launch": seg_bytes,
+                         "model": "2 (n_x - n_sep) N 8 B per k_seg launch",
+                         "launch_ms": float(seg_ms.mean()),
+                         "stage_ms": {k: float(v) for k, v in zip(
+                             ["A_L", "B_LU", "A_U", "FoR", "A_Ut", "B_UtLt", "A_Lt", "MulAdd", "total"], stage)},
+                         "path_m2_gbs": path_gbs, "path_m2_frac": (path_gbs / peak) if path_gbs else None,
+                         "path_model": "M2 (6 n_x + 5 n_p) * 8 B per HVP (SURVEY.md 8(d))"},
             "cpu_baseline": cpu,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         }

@@ -169,7 +169,7 @@ __global__ void k_assemble(AsmParams a) {
 __global__ void k_objective(int n_bus, int ref, const int *has_gen, const double *c2b, const double *c1b,
                             const double *c0b, const double *pgb, const double *P, const double *Pd,
                             double *scal) {
-  __shared__ double red[kThreads];
+  __shared__ double red[1024];
   const double pg_ref = P[ref] + Pd[ref];
   double acc = 0.0;
   for (int b = threadIdx.x; b < n_bus; b += blockDim.x) {
@@ -325,37 +325,37 @@ __global__ void k_sep_dense(int nslots, const int *__restrict__ src, const int *
 }
 
 // Gauss-Jordan inverse of the b x b (b <= 32) diagonal block of panel K by one
-// warp: D in shared memory, lane j updates column j, __syncwarp between
-// pivots.  Static pivots, checked against the separator row's original max.
+// warp: lane j holds column j of D in registers (compile-time row index), the
+// pivot column moves by shuffles; the pivot loop stays rolled (small code).
+// Static pivots, checked against the separator row's original max.
 __device__ __forceinline__ void gj_diag_warp(const double *S, int ns, int K, double *Dinv, const double *rowmax,
                                              const int *sep_rows, int *status, double pivtol) {
-  __shared__ double D[GJB][GJB + 1];
   const int j = threadIdx.x & 31;
   const int b = min(GJB, ns - K);
-  for (int i = 0; i < GJB; ++i) D[i][j] = (i < b && j < b) ? S[(long long)(K + i) * ns + K + j] : (i == j ? 1.0 : 0.0);
-  __syncwarp();
-  for (int k = 0; k < GJB; ++k) {
-    const double piv = D[k][k];
-    const double inv = 1.0 / piv;
-    if (j == 0 && k < b) {
-      const int row = sep_rows[K + k];
-      if (!(fabs(piv) > pivtol * rowmax[row])) atomicMax(status, row + 1);
-    }
-    const double rk = j == k ? inv : D[k][j] * inv;  // new pivot row, column j
-    double fk[GJB], dj[GJB];
+  double d[GJB];
 #pragma unroll
-    for (int i = 0; i < GJB; ++i) {  // all loads first (independent), then the updates
-      fk[i] = D[i][k];
-      dj[i] = D[i][j];
-    }
-    __syncwarp();
+  for (int i = 0; i < GJB; ++i) d[i] = (i < b && j < b) ? S[(long long)(K + i) * ns + K + j] : (i == j ? 1.0 : 0.0);
+  const double rm = j < b ? rowmax[sep_rows[K + j]] : 0.0;   // pivot threshold of row K + j
+  bool bad = false;
+#pragma unroll 1
+  for (int k = 0; k < GJB; ++k) {
+    double dk = 0.0;  // D[k][j]
 #pragma unroll
     for (int i = 0; i < GJB; ++i)
-      if (i != k) D[i][j] = j == k ? -fk[i] * inv : fma(-fk[i], rk, dj[i]);
-    D[k][j] = rk;
-    __syncwarp();
+      if (i == k) dk = d[i];
+    const double piv = __shfl_sync(0xffffffffu, dk, k);
+    const double inv = 1.0 / piv;
+    if (j == k && k < b && !(fabs(piv) > pivtol * rm)) bad = true;
+    const double rk = j == k ? inv : dk * inv;  // new pivot row, column j
+#pragma unroll
+    for (int i = 0; i < GJB; ++i) {
+      const double f = __shfl_sync(0xffffffffu, d[i], k);  // D[i][k]
+      d[i] = i == k ? rk : (j == k ? -f * inv : fma(-f, rk, d[i]));
+    }
   }
-  for (int i = 0; i < GJB; ++i) Dinv[i * GJB + j] = D[i][j];
+  if (bad) atomicMax(status, sep_rows[K + j] + 1);
+#pragma unroll
+  for (int i = 0; i < GJB; ++i) Dinv[i * GJB + j] = d[i];
 }
 
 __global__ void __launch_bounds__(32) k_gj_diag(const double *S, int ns, int K, double *Dinv, const double *rowmax,
@@ -872,8 +872,8 @@ __device__ __forceinline__ double delta_src(const SegParams &h, int src, int col
 // One warp per bus, one lane per column, FCH column chunks per warp processed
 // together (index / coefficient loads amortized, FCH independent gathers in
 // flight per incident line).
-constexpr int FCH = 4;
-__global__ void __launch_bounds__(kThreads) k_for(SegParams h) {
+constexpr int FCH = 2;
+__global__ void __launch_bounds__(kThreads, 4) k_for(SegParams h) {
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   if (b >= h.n_bus) return;
@@ -950,7 +950,7 @@ __global__ void __launch_bounds__(kThreads) k_for(SegParams h) {
 
 // SpMulAdd HW = Y_p + G_p^T Psi: one warp per p row, lanes over
 // columns, FCH chunks per warp
-__global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
+__global__ void __launch_bounds__(kThreads, 4) k_muladd(SegParams h) {
   const int lane = threadIdx.x & 31;
   const int cp = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
   if (cp >= h.n_p) return;
@@ -1114,6 +1114,8 @@ struct rh_ctx {
   // workspace
   double *Zb = nullptr, *Pb = nullptr, *Tsep = nullptr;
   size_t ws_elems = 0, tsep_elems = 0;
+  double *e2e_buf = nullptr;     // rh_reduced_hessian_host staging (x, p, grad, H)
+  cudaStream_t e2e_st = nullptr;
   int *blk_gp_ptr, *blk_gp_loc;
   int *fact_seg_lvl, *fact_lvl_ptr, *fact_order;
 
@@ -1123,7 +1125,10 @@ struct rh_ctx {
     if (Zb) cudaFree(Zb);
     if (Pb) cudaFree(Pb);
     if (Tsep) cudaFree(Tsep);
-    Zb = Pb = Tsep = nullptr;
+    if (e2e_buf) cudaFree(e2e_buf);
+    if (e2e_st) cudaStreamDestroy(e2e_st);
+    Zb = Pb = Tsep = e2e_buf = nullptr;
+    e2e_st = nullptr;
     ws_elems = tsep_elems = 0;
   }
 };
@@ -1706,8 +1711,8 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   a.refg_v = c->refg_v;
   k_assemble<<<nblk(nb, 128), 128, 0, st>>>(a);
   RH_LAUNCHED(c);
-  k_objective<<<1, kThreads, 0, st>>>(nb, A.ref, c->has_gen, c->c2b, c->c1b, c->c0b, c->pgb, c->P, c->Pd,
-                                      c->scal);
+  k_objective<<<1, 1024, 0, st>>>(nb, A.ref, c->has_gen, c->c2b, c->c1b, c->c0b, c->pgb, c->P, c->Pd,
+                                  c->scal);
   RH_LAUNCHED(c);
   // numeric refactorization: blocks, separator rows (block updates), separator
   FactParams f{};
@@ -1892,38 +1897,26 @@ int rh_reduced_hessian_host(rh_ctx *c, const double *x, const double *p, int32_t
   RH_CUDA(c, cudaSetDevice(c->device));
   const Analysis &A = c->A;
   const size_t nx = A.n_x, np_ = A.n_p;
-  double *dx = nullptr, *dp = nullptr, *dg = nullptr, *dH = nullptr;
-  cudaStream_t st = nullptr;
-  RH_CUDA(c, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  int rc = RH_OK;
-  do {
-    if (cudaMallocAsync(&dx, nx * 8, st) || cudaMallocAsync(&dp, np_ * 8, st) ||
-        cudaMallocAsync(&dg, np_ * 8, st) || cudaMallocAsync(&dH, np_ * np_ * 8, st)) {
-      rc = fail(c, RH_E_NOMEM, "allocation failed");
-      break;
+  // context-owned staging buffers and stream (allocated once per grid)
+  if (!c->e2e_st) RH_CUDA(c, cudaStreamCreateWithFlags(&c->e2e_st, cudaStreamNonBlocking));
+  if (!c->e2e_buf) {
+    if (cudaMalloc(&c->e2e_buf, (nx + 2 * np_ + np_ * np_) * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, RH_E_NOMEM, "allocation failed");
     }
-    if (cudaMemcpyAsync(dx, x, nx * 8, cudaMemcpyHostToDevice, st) ||
-        cudaMemcpyAsync(dp, p, np_ * 8, cudaMemcpyHostToDevice, st)) {
-      rc = fail(c, RH_E_CUDA, "H2D copy failed");
-      break;
-    }
-    if ((rc = rh_set_state(c, dx, dp, st))) break;
-    if ((rc = rh_reduced_gradient(c, dg, nullptr, st))) break;
-    if ((rc = rh_full_hessian(c, N, dH, st))) break;
-    if ((grad_p && cudaMemcpyAsync(grad_p, dg, np_ * 8, cudaMemcpyDeviceToHost, st)) ||
-        cudaMemcpyAsync(H, dH, np_ * np_ * 8, cudaMemcpyDeviceToHost, st)) {
-      rc = fail(c, RH_E_CUDA, "D2H copy failed");
-      break;
-    }
-    if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(c, RH_E_CUDA, "stream sync failed");
-  } while (0);
-  cudaFreeAsync(dx, st);
-  cudaFreeAsync(dp, st);
-  cudaFreeAsync(dg, st);
-  cudaFreeAsync(dH, st);
-  cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
-  return rc;
+  }
+  cudaStream_t st = c->e2e_st;
+  double *dx = c->e2e_buf, *dp = dx + nx, *dg = dp + np_, *dH = dg + np_;
+  RH_CUDA(c, cudaMemcpyAsync(dx, x, nx * 8, cudaMemcpyHostToDevice, st));
+  RH_CUDA(c, cudaMemcpyAsync(dp, p, np_ * 8, cudaMemcpyHostToDevice, st));
+  int rc = rh_set_state(c, dx, dp, st);
+  if (!rc) rc = rh_reduced_gradient(c, dg, nullptr, st);
+  if (!rc) rc = rh_full_hessian(c, N, dH, st);
+  if (rc) return rc;
+  if (grad_p) RH_CUDA(c, cudaMemcpyAsync(grad_p, dg, np_ * 8, cudaMemcpyDeviceToHost, st));
+  RH_CUDA(c, cudaMemcpyAsync(H, dH, np_ * np_ * 8, cudaMemcpyDeviceToHost, st));
+  RH_CUDA(c, cudaStreamSynchronize(st));
+  return RH_OK;
 }
 
 int64_t rh_launch_count(const rh_ctx *c) { return c ? c->launches : 0; }
