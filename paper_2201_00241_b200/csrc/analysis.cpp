@@ -31,6 +31,7 @@ namespace rh {
 namespace {
 
 constexpr int kSchedWarps = 16;  // warps of the block sweep kernel (512 threads)
+constexpr int kMaxTops = 32;      // cap on a block's densely inverted top rows
 
 template <class T>
 void sort_unique(std::vector<T> &v) {
@@ -73,20 +74,16 @@ std::vector<int32_t> minimum_degree(std::vector<std::vector<int32_t>> adj) {
 }
 
 
-// Subtree-to-warp schedule of one block's sweep.  Lanes
-// own columns, so a warp needs no synchronization between rows it computes
-// itself; only a dependency computed by ANOTHER warp needs a CTA barrier.
-// The block's forest is split into <= ~nw "pieces" (whole subtrees) of
-// balanced cost, packed onto warps (LPT); the few removed roots ("top" rows)
-// are scheduled greedily: a top row joins the warp that owns its dependencies
-// in the current super-level, or opens a new super-level when they span
-// several warps.  Forward: pieces first, then top rows; backward: the reverse.
-// Returns the rows in schedule order; bounds[sl * nw + w] .. bounds[sl * nw + w + 1]
-// are warp w's rows in super-level sl (positions relative to the block start).
-std::vector<int32_t> warp_schedule(const Analysis &A, const std::vector<int32_t> &rows, int s, bool fwd,
-                                   const std::vector<std::vector<int32_t>> &Ls,
-                                   const std::vector<std::vector<int32_t>> &Lrow, int nw,
-                                   std::vector<int32_t> &bounds) {
+// Subtree-to-warp split of one block.  Lanes own
+// columns, so a warp needs no synchronization between rows it computes
+// itself.  The block's forest is cut into <= ~nw "pieces" (whole subtrees) of
+// balanced cost packed onto warps (LPT); the removed roots ("tops", <= max_tops,
+// a near-dense chain at the top of the block) are not chained row by row:
+// their diagonal block is inverted once per state (k_tops_inverse) and applied
+// as a dense product, so every sweep of a block needs only 2-3 CTA barriers.
+// The same split serves both directions and the refactorization.
+BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<std::vector<int32_t>> &Ls,
+                       const std::vector<std::vector<int32_t>> &Lrow, int nw, int max_tops) {
   const int n = (int)rows.size();
   std::unordered_map<int, int> li;
   li.reserve(n * 2);
@@ -100,15 +97,14 @@ std::vector<int32_t> warp_schedule(const Analysis &A, const std::vector<int32_t>
       auto it = li.find(Ls[r][0]);
       if (it != li.end()) par[i] = it->second;
     }
-    cost[i] = 8.0 + (double)(fwd ? Lrow[r].size() : Ls[r].size());
+    cost[i] = 8.0 + (double)(Lrow[r].size() + Ls[r].size());
   }
   for (int i = 0; i < n; ++i)
     if (par[i] >= 0) kids[par[i]].push_back(i);
-  // subtree costs (children have smaller global index: process ascending)
   std::vector<int> ordi(n);
   std::iota(ordi.begin(), ordi.end(), 0);
-  std::sort(ordi.begin(), ordi.end(), [&](int a, int b) { return rows[a] < rows[b]; });
-  for (int i : ordi) {
+  std::sort(ordi.begin(), ordi.end(), [&](int x, int y) { return rows[x] < rows[y]; });
+  for (int i : ordi) {  // children have smaller global index
     sc[i] = cost[i];
     for (int k : kids[i]) sc[i] += sc[k];
   }
@@ -121,7 +117,8 @@ std::vector<int32_t> warp_schedule(const Analysis &A, const std::vector<int32_t>
     }
   const double target = total / nw;
   std::vector<char> is_top(n, 0);
-  for (int it = 0; it < 4 * nw; ++it) {
+  int ntop = 0;
+  while (ntop < max_tops) {
     int best = -1;
     for (int k = 0; k < (int)pieces.size(); ++k)
       if (best < 0 || sc[pieces[k]] > sc[pieces[best]]) best = k;
@@ -129,95 +126,29 @@ std::vector<int32_t> warp_schedule(const Analysis &A, const std::vector<int32_t>
     const int p = pieces[best];
     pieces.erase(pieces.begin() + best);
     is_top[p] = 1;
+    ++ntop;
     for (int k : kids[p]) pieces.push_back(k);
   }
-  // LPT packing of pieces onto warps
-  std::sort(pieces.begin(), pieces.end(), [&](int a, int b) { return sc[a] > sc[b]; });
+  std::sort(pieces.begin(), pieces.end(), [&](int x, int y) { return sc[x] > sc[y]; });
   std::vector<double> load(nw, 0.0);
-  std::vector<std::vector<int>> wrows(nw);
-  std::vector<int> owner(n, -1);
+  BlockSplit B;
+  B.warp_rows.assign(nw, {});
   for (int p : pieces) {
     const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
     load[w] += sc[p];
-    // rows of the piece in topological order of this direction
-    std::vector<int> st{p}, sub;
+    std::vector<int> st{p};
     while (!st.empty()) {
       const int x = st.back();
       st.pop_back();
-      sub.push_back(x);
+      B.warp_rows[w].push_back(rows[x]);
       for (int k : kids[x]) st.push_back(k);
     }
-    std::sort(sub.begin(), sub.end(), [&](int a, int b) { return fwd ? rows[a] < rows[b] : rows[a] > rows[b]; });
-    for (int x : sub) wrows[w].push_back(x);
   }
-  // top rows: topological order of this direction
-  std::vector<int> tops;
+  for (auto &v : B.warp_rows) std::sort(v.begin(), v.end());  // ascending = forward topological
   for (int i = 0; i < n; ++i)
-    if (is_top[i]) tops.push_back(i);
-  std::sort(tops.begin(), tops.end(), [&](int a, int b) { return fwd ? rows[a] < rows[b] : rows[a] > rows[b]; });
-  std::vector<std::vector<std::vector<int>>> SL;
-  auto emit_pieces = [&]() {
-    SL.push_back(wrows);
-  };
-  auto greedy_tops = [&]() {
-    std::vector<int> w_of(n, -1);  // warp of a top row in the CURRENT super-level
-    std::vector<std::vector<int>> cur(nw);
-    std::vector<double> cl(nw, 0.0);
-    std::vector<int> members;
-    for (int i : tops) {
-      std::set<int> ws;
-      for (int k : (fwd ? Lrow[rows[i]] : Ls[rows[i]])) {
-        auto itk = li.find(k);
-        if (itk != li.end() && w_of[itk->second] >= 0) ws.insert(w_of[itk->second]);
-      }
-      if (ws.size() >= 2) {  // dependencies on several warps: barrier, new super-level
-        SL.push_back(cur);
-        cur.assign(nw, {});
-        cl.assign(nw, 0.0);
-        for (int m : members) w_of[m] = -1;
-        members.clear();
-        ws.clear();
-      }
-      const int w = ws.empty() ? (int)(std::min_element(cl.begin(), cl.end()) - cl.begin()) : *ws.begin();
-      cur[w].push_back(i);
-      cl[w] += cost[i];
-      w_of[i] = w;
-      members.push_back(i);
-    }
-    if (!members.empty()) SL.push_back(cur);
-  };
-  if (fwd) {
-    emit_pieces();
-    greedy_tops();
-  } else {
-    greedy_tops();
-    emit_pieces();
-  }
-  std::vector<int32_t> out;
-  bounds.clear();
-  for (auto &sl : SL)
-    for (int w = 0; w < nw; ++w) {
-      bounds.push_back((int)out.size());
-      for (int i : sl[w]) out.push_back(rows[i]);
-    }
-  bounds.push_back((int)out.size());
-  if ((int)out.size() != n) throw std::runtime_error("warp_schedule lost rows");
-  if (getenv("RH_DEBUG_SCHED") && s < 3) {
-    fprintf(stderr, "block %d %s rows %d total cost %.0f target %.0f pieces %zu tops %zu SLs %zu\n", s,
-            fwd ? "fwd" : "bwd", n, total, target, pieces.size(), tops.size(), SL.size());
-    for (size_t k = 0; k < SL.size(); ++k) {
-      double mx = 0;
-      int mr = 0;
-      for (int w = 0; w < nw; ++w) {
-        double c = 0;
-        for (int i : SL[k][w]) c += cost[i];
-        mx = std::max(mx, c);
-        mr = std::max(mr, (int)SL[k][w].size());
-      }
-      fprintf(stderr, "   SL %zu: max warp cost %.0f, max warp rows %d\n", k, mx, mr);
-    }
-  }
-  return out;
+    if (is_top[i]) B.tops.push_back(rows[i]);
+  std::sort(B.tops.begin(), B.tops.end());
+  return B;
 }
 
 // ---------------------------------------------------------------------------
@@ -338,12 +269,40 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
       for (int r : rows) nl = std::max(nl, lv[r] + 1);
       S.max_levels = std::max(S.max_levels, nl);
       const int qbase = (int)S.order.size();
+      std::vector<char> top_row;  // blocks: membership in the block's tops, by local index
       if (s < nb) {
-        // blocks: subtree-to-warp schedule ("super-levels" x warps), see warp_schedule
-        std::vector<int32_t> bounds;
-        rows = warp_schedule(A, rows, s, fwd, Ls, Lrow, kSchedWarps, bounds);
-        for (int b : bounds) S.lvl_ptr.push_back(qbase + b);
-        S.max_levels = std::max(S.max_levels, (int)(bounds.size() - 1) / kSchedWarps);
+        // blocks: [warp pieces] + [tops] (forward) or [tops] + [warp pieces] (backward);
+        // lvl entries: nw + 1 piece bounds, then the tops' [begin, end)
+        const BlockSplit &B = A.split[s];
+        std::vector<int32_t> ord;
+        std::vector<int32_t> pb(kSchedWarps + 1, 0), tb(2, 0);
+        auto add_pieces = [&]() {
+          for (int w = 0; w < kSchedWarps; ++w) {
+            pb[w] = (int)ord.size();
+            if (fwd)
+              ord.insert(ord.end(), B.warp_rows[w].begin(), B.warp_rows[w].end());
+            else
+              ord.insert(ord.end(), B.warp_rows[w].rbegin(), B.warp_rows[w].rend());
+          }
+          pb[kSchedWarps] = (int)ord.size();
+        };
+        auto add_tops = [&]() {
+          tb[0] = (int)ord.size();
+          ord.insert(ord.end(), B.tops.begin(), B.tops.end());   // dense phase: any order
+          tb[1] = (int)ord.size();
+        };
+        if (fwd) {
+          add_pieces();
+          add_tops();
+        } else {
+          add_tops();
+          add_pieces();
+        }
+        rows = ord;
+        for (int b : pb) S.lvl_ptr.push_back(qbase + b);
+        for (int b : tb) S.lvl_ptr.push_back(qbase + b);
+        top_row.assign(nr_s, 0);
+        for (int r : B.tops) top_row[A.loc_of[r]] = 1;
       } else {
         std::vector<int32_t> cnt(nl + 1, 0);
         for (int r : rows) cnt[lv[r] + 1]++;
@@ -361,24 +320,47 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
         for (int l = 0; l <= nl; ++l) A.fact_lvl_ptr.push_back(fb + cnt[l]);
         for (int r : lrows) A.fact_order.push_back(A.loc_of[r]);
       }
+      auto pad4 = [&](int r) {  // blocks: pad to a multiple of 4 entries (coefficient 0, own row)
+        while ((S.dep.size() - S.rptr.back()) % 4 != 0) {
+          S.dep.push_back(A.loc_of[r]);
+          S.src_a.push_back(-1);
+          S.src_b.push_back(-1);
+        }
+      };
       for (int r : rows) {
         S.order.push_back(A.loc_of[r]);
         const std::vector<int32_t> &deps = fwd ? Lrow[r] : Ls[r];
-        for (int pass = 0; pass < 2; ++pass) {   // external entries first, then local
+        const bool is_top = s < nb && top_row[A.loc_of[r]];
+        if (s < nb) {
+          // blocks: local (and staged separator) entries; a top row keeps only its entries
+          // outside the tops, then gets one dense entry per top row (values: k_tops_inverse)
           for (int k : deps) {
-            const bool local = A.seg_of[k] == s || s < nb;   // blocks: staged ext rows are local
-            if (local != (pass == 1)) continue;
-            S.dep.push_back(A.seg_of[k] == s ? A.loc_of[k] : (s < nb ? ext_local(k) : k));
+            if (is_top && A.seg_of[k] == s && top_row[A.loc_of[k]]) continue;
+            S.dep.push_back(A.seg_of[k] == s ? A.loc_of[k] : ext_local(k));
             S.src_a.push_back(fpos(r, k));   // fwd: L[r,k]  bwd: U[r,k]
             S.src_b.push_back(fpos(k, r));   // fwd: U[k,r]  bwd: L[k,r]
           }
-          if (pass == 0) S.rext.push_back((int)S.dep.size());
-        }
-        if (s < nb) {  // blocks: pad every row to a multiple of 4 entries (coefficient 0, own row)
-          while ((S.dep.size() - S.rptr.back()) % 4 != 0) {
-            S.dep.push_back(A.loc_of[r]);
-            S.src_a.push_back(-1);
-            S.src_b.push_back(-1);
+          pad4(r);
+          S.rext.push_back((int)S.dep.size());   // blocks: start of the dense (tops) entries
+          if (is_top) {
+            (fwd ? A.top_fwd_base : A.top_bwd_base).push_back((int)S.dep.size());
+            for (int j : A.split[s].tops) {
+              S.dep.push_back(A.loc_of[j]);
+              S.src_a.push_back(-1);
+              S.src_b.push_back(-1);
+            }
+            pad4(r);
+          }
+        } else {
+          for (int pass = 0; pass < 2; ++pass) {   // separator: external entries first, then local
+            for (int k : deps) {
+              const bool local = A.seg_of[k] == s;
+              if (local != (pass == 1)) continue;
+              S.dep.push_back(local ? A.loc_of[k] : k);
+              S.src_a.push_back(fpos(r, k));
+              S.src_b.push_back(fpos(k, r));
+            }
+            if (pass == 0) S.rext.push_back((int)S.dep.size());
           }
         }
         S.rptr.push_back((int)S.dep.size());
@@ -392,8 +374,61 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
   A.fact_seg_lvl.clear();
   A.fact_lvl_ptr.clear();
   A.fact_order.clear();
+  // subtree-to-warp split of every block (shared by both directions and R_A)
+  A.split.assign(nb, BlockSplit());
+  int tops_cap = kMaxTops;
+  if (const char *env = getenv("RH_TOPS")) tops_cap = std::max(0, std::min(kMaxTops, atoi(env)));  // tuning override
+  for (int s = 0; s < nb; ++s) {
+    std::vector<int32_t> rows(A.row_global.begin() + A.seg_row_off[s], A.row_global.begin() + A.seg_row_off[s + 1]);
+    A.split[s] = split_block(rows, Ls, Lrow, kSchedWarps, tops_cap);
+  }
+  A.top_fwd_base.clear();
+  A.top_bwd_base.clear();
   build(A.fwd, true);
   build(A.bwd, false);
+  if (getenv("RH_DEBUG_SCHED")) {  // tuning aid: per-block chain lengths (rows, 4-entry groups)
+    for (const SegSweep *S : {&A.fwd, &A.bwd}) {
+      long long worst = 0, sum = 0;
+      for (int s = 0; s < nb; ++s) {
+        const int *lv = S->lvl_ptr.data() + S->seg_lvl[s];
+        int mr = 0, mg = 0;
+        for (int w = 0; w < kSchedWarps; ++w) {
+          int g = 0;
+          for (int q = lv[w]; q < lv[w + 1]; ++q) g += (S->rext[q] - S->rptr[q]) / 4;
+          mr = std::max(mr, lv[w + 1] - lv[w]);
+          mg = std::max(mg, g);
+        }
+        const int nt = lv[kSchedWarps + 2] - lv[kSchedWarps + 1];
+        int tg = 0;
+        for (int q = lv[kSchedWarps + 1]; q < lv[kSchedWarps + 2]; ++q) tg = std::max(tg, (S->rext[q] - S->rptr[q]) / 4);
+        const long long est = 60LL * mr + 40LL * mg + (nt ? 1000 + 40LL * tg + 40LL * ((nt + 3) / 4) * ((nt + 15) / 16) : 0);
+        // shared-memory wavefronts at 64 columns: per row meta + ldx(4) + stx(4) + dinv; per group 4 ent + 16 X
+        const int qa = A.seg_row_off[s], qz = A.seg_row_off[s + 1];
+        const long long wf = 10LL * (qz - qa) + 20LL * (S->rptr[qz] - S->rptr[qa]) / 4;
+        worst = std::max(worst, est);
+        sum += est;
+        if (s < 4 || getenv("RH_DEBUG_SCHED")[0] == '2')
+          fprintf(stderr, "%s blk %d rows %d: warp max rows %d groups %d | tops %d outer-groups %d | est %lld cyc | smem wavefronts %lld (entries %d)\n",
+                  S == &A.fwd ? "fwd" : "bwd", s, qz - qa, mr, mg, nt, tg, est, wf, S->rptr[qz] - S->rptr[qa]);
+      }
+      fprintf(stderr, "%s: est worst %lld mean %lld cycles\n", S == &A.fwd ? "fwd" : "bwd", worst, sum / std::max(nb, 1));
+    }
+  }
+  // tops of every block for k_tops_inverse: rows and F positions of T x T
+  A.top_ptr.assign(nb + 1, 0);
+  A.top_rows.clear();
+  A.top_fpos.clear();
+  A.top_fpos_ptr.assign(nb + 1, 0);
+  A.max_tops = 0;
+  for (int s = 0; s < nb; ++s) {
+    const auto &T = A.split[s].tops;
+    A.top_rows.insert(A.top_rows.end(), T.begin(), T.end());
+    A.top_ptr[s + 1] = (int)A.top_rows.size();
+    for (int x : T)
+      for (int y : T) A.top_fpos.push_back(fpos(x, y));
+    A.top_fpos_ptr[s + 1] = (int)A.top_fpos.size();
+    A.max_tops = std::max(A.max_tops, (int)T.size());
+  }
   A.blk_gp_ptr.assign(nb + 1, 0);
   A.blk_gp_loc.clear();
   for (int s = 0; s < nb; ++s) {

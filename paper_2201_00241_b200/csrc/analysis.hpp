@@ -49,6 +49,11 @@ struct SegSweep {
   int max_levels = 0;
 };
 
+struct BlockSplit {
+  std::vector<std::vector<int32_t>> warp_rows;  // per warp: piece rows (global, ascending)
+  std::vector<int32_t> tops;                    // top rows (global, ascending)
+};
+
 struct Analysis {
   // ---------------- grid copy ----------------
   int n_bus = 0, n_line = 0, n_gen = 0, ref = -1;
@@ -109,6 +114,11 @@ struct Analysis {
   int max_seg_rows = 0, sep_rows = 0;
   SegSweep fwd, bwd;                        // fwd: L and U^T ; bwd: U and L^T
   std::vector<int32_t> blk_gp_ptr, blk_gp_loc;  // per block: local rows carrying G_p entries
+  std::vector<BlockSplit> split;            // per block
+  // tops of every block (densely inverted per state): rows, F positions of T x T,
+  // and the first dense entry of every top row in the fwd / bwd entry arrays
+  std::vector<int32_t> top_ptr, top_rows, top_fpos_ptr, top_fpos, top_fwd_base, top_bwd_base;
+  int max_tops = 0;
 
   // ---------------- refactorization schedule ----------------
   // R_A (per block, shared memory): F rows of the block staged at fo (block-local offsets)

@@ -239,40 +239,41 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   }
   for (int t = threadIdx.x; t < ntg; t += blockDim.x) stg[t] = f.tgt16[tb + t];
   __syncthreads();
-  const int l0 = f.fwd_seg_lvl[s], l1 = f.fwd_seg_lvl[s + 1] - 1;
-  const int nsl = (l1 - l0) / nw;
-  for (int sl = 0; sl < nsl; ++sl) {
-    const int q1 = f.fwd_lvl_ptr[l0 + sl * nw + warp + 1];
-    for (int q = f.fwd_lvl_ptr[l0 + sl * nw + warp]; q < q1; ++q) {
-      const int a = f.fwd_order[q];
-      const int i = f.row_global[r0 + a];
-      const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off;
-      double *w = SF + off;
-      double amax = 0.0;
-      for (int t = lane; t < len; t += 32) amax = fmax(amax, fabs(w[t]));
-      amax = warp_max(amax);
-      const int k1 = f.ks_ptr[r0 + a + 1] - kb;
-      for (int ks = f.ks_ptr[r0 + a] - kb; ks < k1; ++ks) {
-        const int4 m = sks[ks];
-        const double lik = w[m.x] * sdinv[skk[ks]];
-        __syncwarp();
-        if (lane == 0) w[m.x] = lik;
-        const double *uk = SF + m.y + 1;
-        const unsigned short *tg = stg + m.w;
-        for (int t = lane; t < m.z; t += 32) w[tg[t]] -= lik * uk[t];
-        __syncwarp();
-      }
-      const double piv = w[f.F_diag[i] - f.F_rowptr[i]];
-      if (lane == 0) {
-        const double di = 1.0 / piv;
-        sdinv[a] = di;
-        f.dinv[i] = di;
-        if (!(fabs(piv) > f.pivtol * amax)) atomicMax(f.status, i + 1);
-      }
+  // forward split of the block: lvl[0..nw] = each warp's piece rows, lvl[nw+1..nw+2] = tops
+  const int *lv = f.fwd_lvl_ptr + f.fwd_seg_lvl[s];
+  auto eliminate = [&](int q) {
+    const int a = f.fwd_order[q];
+    const int i = f.row_global[r0 + a];
+    const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off;
+    double *w = SF + off;
+    double amax = 0.0;
+    for (int t = lane; t < len; t += 32) amax = fmax(amax, fabs(w[t]));
+    amax = warp_max(amax);
+    const int k1 = f.ks_ptr[r0 + a + 1] - kb;
+    for (int ks = f.ks_ptr[r0 + a] - kb; ks < k1; ++ks) {
+      const int4 m = sks[ks];
+      const double lik = w[m.x] * sdinv[skk[ks]];
+      __syncwarp();
+      if (lane == 0) w[m.x] = lik;
+      const double *uk = SF + m.y + 1;
+      const unsigned short *tg = stg + m.w;
+      for (int t = lane; t < m.z; t += 32) w[tg[t]] -= lik * uk[t];
       __syncwarp();
     }
-    __syncthreads();
-  }
+    const double piv = w[f.F_diag[i] - f.F_rowptr[i]];
+    if (lane == 0) {
+      const double di = 1.0 / piv;
+      sdinv[a] = di;
+      f.dinv[i] = di;
+      if (!(fabs(piv) > f.pivtol * amax)) atomicMax(f.status, i + 1);
+    }
+    __syncwarp();
+  };
+  for (int q = lv[warp]; q < lv[warp + 1]; ++q) eliminate(q);
+  __syncthreads();
+  if (warp == 0)
+    for (int q = lv[nw + 1]; q < lv[nw + 2]; ++q) eliminate(q);   // tops: ascending, one warp
+  __syncthreads();
   for (int a = warp; a < nr; a += nw) {
     const int i = f.row_global[r0 + a];
     const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off, rb = f.F_rowptr[i];
@@ -494,6 +495,59 @@ __global__ void k_transpose(const double *__restrict__ A, double *AT, int n) {
     if (xo < n && yo0 + r < n) AT[(long long)(yo0 + r) * n + xo] = tile[threadIdx.x][r];
 }
 
+// Dense inverses of every block's top diagonal block T x T (once per state):
+// M_L = (L_TT)^-1 (unit lower) and M_U = (U_TT)^-1, written into the sweeps'
+// dense entries: L rows get M_L, U^T rows M_U^T, U rows M_U, L^T rows M_L^T.
+// One CTA per block, one thread per column (forward / backward substitution).
+constexpr int kMaxTops = 64;
+__global__ void __launch_bounds__(kMaxTops) k_tops_inverse(const int *top_ptr, const int *top_fpos_ptr,
+                                                           const int *top_fpos, const int *fwd_base,
+                                                           const int *bwd_base, const double *F, double *vL,
+                                                           double *vUt, double *vU, double *vLt) {
+  extern __shared__ double tops_sm[];
+  double(*T)[kMaxTops + 1] = reinterpret_cast<double(*)[kMaxTops + 1]>(tops_sm);  // L_TT below, U_TT on/above
+  double(*ML)[kMaxTops + 1] = T + kMaxTops;
+  double(*MU)[kMaxTops + 1] = ML + kMaxTops;
+  const int s = blockIdx.x;
+  const int t0 = top_ptr[s], nt = top_ptr[s + 1] - t0;
+  if (nt == 0) return;
+  const int *fp = top_fpos + top_fpos_ptr[s];
+  for (int x = threadIdx.x; x < nt * nt; x += blockDim.x) {
+    const int pos = fp[x];
+    T[x / nt][x % nt] = pos >= 0 ? F[pos] : 0.0;
+  }
+  __syncthreads();
+  const int b = threadIdx.x;
+  if (b < nt) {
+    // column b of M_L: unit lower, rows a >= b
+    for (int a = 0; a < nt; ++a) {
+      double v = a == b ? 1.0 : 0.0;
+      if (a > b)
+        for (int k = b; k < a; ++k) v -= T[a][k] * ML[k][b];
+      ML[a][b] = a < b ? 0.0 : v;
+    }
+    // column b of M_U: upper, rows a <= b, backward
+    for (int a = nt - 1; a >= 0; --a) {
+      double v = 0.0;
+      if (a <= b) {
+        v = a == b ? 1.0 : 0.0;
+        for (int k = a + 1; k <= b; ++k) v -= T[a][k] * MU[k][b];
+        v /= T[a][a];
+      }
+      MU[a][b] = v;
+    }
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < nt * nt; x += blockDim.x) {
+    const int a = x / nt, c = x % nt;
+    const int fb = fwd_base[t0 + a], bb = bwd_base[t0 + a];
+    vL[fb + c] = ML[a][c];
+    vUt[fb + c] = MU[c][a];
+    vU[bb + c] = MU[a][c];
+    vLt[bb + c] = ML[c][a];
+  }
+}
+
 // copy factor values into the sweep value arrays (entry order of the sweeps)
 __global__ void k_gather_vals(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -543,17 +597,20 @@ struct SegStage {  // shared-memory carve-up of one block sweep
   double *dinv;
   int *lvl;
   int nq, ne, nlev;
+  long long *prof;  // timing experiment (RH_DEBUG & 8): per-warp piece and top-phase cycles, else null
 };
 
 // Stage a block's sweep structure in shared memory behind an X tile of `nrx`
 // rows x C columns.  Rows are padded to multiples of 4 entries on the host.
 __device__ __forceinline__ SegStage stage_seg(const DSeg &S, const double *__restrict__ val,
-                                              const double *__restrict__ dinv, int seg, int nrx, int C, double *sm) {
+                                              const double *__restrict__ dinv, int seg, int qb, int nq, int nrx,
+                                              int C, double *sm) {
+  // a block's rows occupy q in [qb, qb + nq) = its segment rows (any lvl layout)
   SegStage t;
+  t.prof = nullptr;
   const int l0 = S.seg_lvl[seg], l1 = S.seg_lvl[seg + 1];
   t.nlev = l1 - l0 - 1;
-  const int qb = S.lvl_ptr[l0];
-  t.nq = S.lvl_ptr[l1 - 1] - qb;
+  t.nq = nq;
   const int eb = S.rptr[qb];
   t.ne = S.rptr[qb + t.nq] - eb;
   const long long rowb = (long long)C * 8;
@@ -566,8 +623,8 @@ __device__ __forceinline__ SegStage stage_seg(const DSeg &S, const double *__res
   for (int i = threadIdx.x; i < t.ne; i += blockDim.x)
     t.ent[i] = make_double2(val[eb + i], __longlong_as_double((long long)S.dep[eb + i] * rowb));
   for (int i = threadIdx.x; i < t.nq; i += blockDim.x) {
-    const int e0 = S.rptr[qb + i] - eb, e1 = S.rptr[qb + i + 1] - eb;
-    t.meta[i] = make_int4((int)(S.order[qb + i] * rowb), e0, (e1 - e0) >> 2, 0);
+    const int e0 = S.rptr[qb + i] - eb, ex = S.rext[qb + i] - eb, e1 = S.rptr[qb + i + 1] - eb;
+    t.meta[i] = make_int4((int)(S.order[qb + i] * rowb), e0, (ex - e0) >> 2, (e1 - ex) >> 2);
     t.dinv[i] = dinv ? dinv[qb + i] : 1.0;
   }
   for (int i = threadIdx.x; i <= t.nlev; i += blockDim.x) t.lvl[i] = S.lvl_ptr[l0 + i] - qb;
@@ -602,53 +659,125 @@ __device__ __forceinline__ void stx(double *p, const double (&x)[CPL]) {
   }
 }
 
-// One sweep over a block: super-level by super-level (CTA barrier between),
-// each warp walking its rows in dependency order with no synchronization (its
-// lanes own their columns).  Per row: 4-entry groups of (coefficient, X row
-// offset) broadcasts and conflict-free X gathers, two FMA chains, next row's
-// metadata prefetched.
+// Sum over `ng` 4-entry groups starting at ep: val * X[row] for this lane's columns.
 template <int CPL>
-__device__ __forceinline__ void seg_sweep(const SegStage &t, bool use_dinv) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const char *Xb = reinterpret_cast<const char *>(t.X) + lane * CPL * 8;
-  const int nsl = t.nlev / nw;
-  for (int sl = 0; sl < nsl; ++sl) {
-    const int q0 = t.lvl[sl * nw + warp], q1 = t.lvl[sl * nw + warp + 1];
-    int4 m = q0 < q1 ? t.meta[q0] : make_int4(0, 0, 0, 0);
-    for (int q = q0; q < q1; ++q) {
-      const int4 mn = q + 1 < q1 ? t.meta[q + 1] : m;
-      double s0[CPL], s1[CPL];
+__device__ __forceinline__ void group_sum(const double2 *ep, int ng, const char *Xb, double (&acc)[CPL]) {
+  double s1[CPL];
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) s0[i] = s1[i] = 0.0;
-      const double2 *ep = t.ent + m.y;
-      for (int g = 0; g < m.z; ++g, ep += 4) {
-        const double2 p0 = ep[0], p1 = ep[1], p2 = ep[2], p3 = ep[3];
-        double x0[CPL], x1[CPL], x2[CPL], x3[CPL];
-        ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p0.y)), x0);
-        ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p1.y)), x1);
-        ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p2.y)), x2);
-        ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p3.y)), x3);
+  for (int i = 0; i < CPL; ++i) s1[i] = 0.0;
+  for (int g = 0; g < ng; ++g, ep += 4) {
+    const double2 p0 = ep[0], p1 = ep[1], p2 = ep[2], p3 = ep[3];
+    double x0[CPL], x1[CPL], x2[CPL], x3[CPL];
+    ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p0.y)), x0);
+    ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p1.y)), x1);
+    ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p2.y)), x2);
+    ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p3.y)), x3);
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-          s0[i] = fma(p0.x, x0[i], s0[i]);
-          s1[i] = fma(p1.x, x1[i], s1[i]);
-          s0[i] = fma(p2.x, x2[i], s0[i]);
-          s1[i] = fma(p3.x, x3[i], s1[i]);
-        }
-      }
-      double *xr = reinterpret_cast<double *>(const_cast<char *>(Xb) + m.x);
-      double xa[CPL];
-      ldx<CPL>(xr, xa);
-      const double d = t.dinv[q];
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) {
-        xa[i] -= s0[i] + s1[i];
-        if (use_dinv) xa[i] *= d;
-      }
-      stx<CPL>(xr, xa);
-      m = mn;
+    for (int i = 0; i < CPL; ++i) {
+      acc[i] = fma(p0.x, x0[i], acc[i]);
+      s1[i] = fma(p1.x, x1[i], s1[i]);
+      acc[i] = fma(p2.x, x2[i], acc[i]);
+      s1[i] = fma(p3.x, x3[i], s1[i]);
     }
-    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) acc[i] += s1[i];
+}
+
+// One sweep over a block.  lvl[0..nw] bound each warp's
+// piece rows (whole subtrees, dependency order, no synchronization: lanes own
+// their columns); lvl[nw+1..nw+2] bound the block's top rows, solved densely:
+// t = X - (entries outside the tops), then X_T = M t with M the inverse of the
+// tops' diagonal block (k_tops_inverse).  Forward: pieces, then tops;
+// backward: tops, then pieces.  3-4 CTA barriers per sweep.
+constexpr int kMaxTopRowsPerWarp = 4;   // 64 tops / 16 warps
+template <int CPL>
+__device__ __forceinline__ void seg_pieces(const SegStage &t, bool use_dinv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const char *Xb = reinterpret_cast<const char *>(t.X) + lane * CPL * 8;
+  const int q0 = t.lvl[warp], q1 = t.lvl[warp + 1];
+  const long long c0 = t.prof ? clock64() : 0;
+  int4 m = q0 < q1 ? t.meta[q0] : make_int4(0, 0, 0, 0);
+  for (int q = q0; q < q1; ++q) {
+    const int4 mn = q + 1 < q1 ? t.meta[q + 1] : m;
+    double acc[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
+    group_sum<CPL>(t.ent + m.y, m.z, Xb, acc);
+    double *xr = reinterpret_cast<double *>(const_cast<char *>(Xb) + m.x);
+    double xa[CPL];
+    ldx<CPL>(xr, xa);
+    const double d = t.dinv[q];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      xa[i] -= acc[i];
+      if (use_dinv) xa[i] *= d;
+    }
+    stx<CPL>(xr, xa);
+    m = mn;
+  }
+  if (t.prof && lane == 0) t.prof[warp] = clock64() - c0;
+  __syncthreads();
+}
+
+template <int CPL>
+__device__ __forceinline__ void seg_tops(const SegStage &t, int nw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const char *Xb = reinterpret_cast<const char *>(t.X) + lane * CPL * 8;
+  const int q0 = t.lvl[nw + 1], q1 = t.lvl[nw + 2];
+  if (q0 >= q1) return;
+  const long long c0 = t.prof ? clock64() : 0;
+  // gather: t_r = X_r - sum over entries outside the tops (in place)
+  for (int q = q0 + warp; q < q1; q += nw) {
+    const int4 m = t.meta[q];
+    double acc[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
+    group_sum<CPL>(t.ent + m.y, m.z, Xb, acc);
+    double *xr = reinterpret_cast<double *>(const_cast<char *>(Xb) + m.x);
+    double xa[CPL];
+    ldx<CPL>(xr, xa);
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) xa[i] -= acc[i];
+    stx<CPL>(xr, xa);
+  }
+  __syncthreads();
+  const long long c1 = t.prof ? clock64() : 0;
+  // dense: X_T = M t_T (results held in registers until every warp has read t)
+  double out[kMaxTopRowsPerWarp][CPL];
+#pragma unroll
+  for (int u = 0; u < kMaxTopRowsPerWarp; ++u) {
+    const int q = q0 + warp + u * nw;
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) out[u][i] = 0.0;
+    if (q < q1) {
+      const int4 m = t.meta[q];
+      group_sum<CPL>(t.ent + m.y + 4 * m.z, m.w, Xb, out[u]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kMaxTopRowsPerWarp; ++u) {
+    const int q = q0 + warp + u * nw;
+    if (q < q1) stx<CPL>(reinterpret_cast<double *>(const_cast<char *>(Xb) + t.meta[q].x), out[u]);
+  }
+  __syncthreads();
+  if (t.prof && threadIdx.x == 0) {
+    t.prof[16] = c1 - c0;
+    t.prof[17] = clock64() - c1;
+    t.prof[18] = q1 - q0;
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void seg_sweep(const SegStage &t, bool use_dinv, bool fwd) {
+  const int nw = blockDim.x >> 5;
+  if (fwd) {
+    seg_pieces<CPL>(t, use_dinv);
+    seg_tops<CPL>(t, nw);
+  } else {
+    seg_tops<CPL>(t, nw);
+    seg_pieces<CPL>(t, use_dinv);
   }
 }
 
@@ -685,7 +814,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg(SegParams h, int mode) {
   long long tk[4] = {0, 0, 0, 0};
   const bool instr = (h.debug & 8) && h.dbg && threadIdx.x == 0;
   if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[0]));
-  const SegStage t = stage_seg(S, val, dinv, seg, nr + nxr, C, sm);
+  SegStage t = stage_seg(S, val, dinv, seg, r0, nr, nr + nxr, C, sm);
+  t.prof = ((h.debug & 8) && h.dbg) ? h.dbg + 6 * 65536 + 20 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
   constexpr int CH = C / 2;  // 16-byte chunks per row
   if (mode == MODE_L) {
     for (int i = threadIdx.x; i < nr * C; i += blockDim.x) t.X[i] = 0.0;
@@ -716,7 +846,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_seg(SegParams h, int mode) {
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[1]));
-  seg_sweep<CPL>(t, dinv != nullptr);
+  seg_sweep<CPL>(t, dinv != nullptr, fwd);
   if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[2]));
   for (int i = threadIdx.x; i < nr * CH; i += blockDim.x) {
     const int a = i / CH, ch = i % CH;
@@ -1118,6 +1248,7 @@ struct rh_ctx {
   cudaStream_t e2e_st = nullptr;
   int *blk_gp_ptr, *blk_gp_loc;
   int *fact_seg_lvl, *fact_lvl_ptr, *fact_order;
+  int *top_ptr, *top_fpos_ptr, *top_fpos, *top_fwd_base, *top_bwd_base;
 
   void free_all() {
     for (void *q : pool) cudaFree(q);
@@ -1164,7 +1295,7 @@ size_t seg_smem_max(const Analysis &A, int C) {
   for (const SegSweep *S : {&A.fwd, &A.bwd}) {
     for (int s = 0; s < A.nblk; ++s) {
       const int l0 = S->seg_lvl[s], l1 = S->seg_lvl[s + 1];
-      const int qb = S->lvl_ptr[l0], qe = S->lvl_ptr[l1 - 1];
+      const int qb = A.seg_row_off[s], qe = A.seg_row_off[s + 1];
       const int ne = S->rptr[qe] - S->rptr[qb];
       const int nrx = A.seg_row_off[s + 1] - A.seg_row_off[s] + S->ext_off[s + 1] - S->ext_off[s];
       m = std::max(m, seg_smem_bytes(nrx, qe - qb, ne, l1 - l0 - 1, C));
@@ -1203,6 +1334,8 @@ int upload(rh_ctx *c) {
   UP(pg_p, A.pg_p); UP(near_ref, A.near_ref);
   UP(seg_row_off, A.seg_row_off); UP(row_global, A.row_global);
   UP(fact_seg_lvl, A.fact_seg_lvl); UP(fact_lvl_ptr, A.fact_lvl_ptr); UP(fact_order, A.fact_order);
+  UP(top_ptr, A.top_ptr); UP(top_fpos_ptr, A.top_fpos_ptr); UP(top_fpos, A.top_fpos);
+  UP(top_fwd_base, A.top_fwd_base); UP(top_bwd_base, A.top_bwd_base);
   UP(blk_gp_ptr, A.blk_gp_ptr); UP(blk_gp_loc, A.blk_gp_loc);
   UP(fwd_src_a, A.fwd.src_a); UP(fwd_src_b, A.fwd.src_b); UP(bwd_src_a, A.bwd.src_a); UP(bwd_src_b, A.bwd.src_b);
   UP(fwd_dsrc, A.fwd.dsrc); UP(bwd_dsrc, A.bwd.dsrc);
@@ -1290,6 +1423,7 @@ int upload(rh_ctx *c) {
   c->smem_seg_blk1 = seg_smem_max(A, kSegC);
   cudaFuncSetAttribute(k_fact_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaFuncSetAttribute(k_seg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  cudaFuncSetAttribute(k_tops_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaFuncSetAttribute(k_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaFuncSetAttribute(k_seg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
   cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
@@ -1381,7 +1515,7 @@ SegParams make_params(rh_ctx *c) {
   if (const char *env = getenv("RH_DEBUG")) h.debug = atoi(env);  // timing experiments only
   if (h.debug & 8) {
     static long long *dbg = nullptr;
-    if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 6 * 65536);
+    if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 26 * 65536);
     h.dbg = dbg;
   }
   h.SinvT = c->SinvT;
@@ -1475,6 +1609,12 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     cudaStreamSynchronize(st);
     if (FILE *fp = fopen("gpurun_out/kseg_timing.bin", "wb")) {
       fwrite(hb.data(), 8, hb.size(), fp);
+      fclose(fp);
+    }
+    std::vector<long long> hp((size_t)20 * (hb.size() / 6));
+    cudaMemcpy(hp.data(), h.dbg + 6 * 65536, hp.size() * 8, cudaMemcpyDeviceToHost);
+    if (FILE *fp = fopen("gpurun_out/kseg_phases.bin", "wb")) {
+      fwrite(hp.data(), 8, hp.size(), fp);
       fclose(fp);
     }
   }
@@ -1781,6 +1921,11 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   const int ngp = (int)A.gp_col.size();
   if (ngp > 0) {
     k_gather_vals<<<nblk(ngp), kThreads, 0, st>>>(ngp, c->gpc_pos, c->gp_val, c->gpc_val);
+    RH_LAUNCHED(c);
+  }
+  if (A.max_tops > 0) {
+    k_tops_inverse<<<A.nblk, kMaxTops, 3 * kMaxTops * (kMaxTops + 1) * sizeof(double), st>>>(c->top_ptr, c->top_fpos_ptr, c->top_fpos, c->top_fwd_base,
+                                                c->top_bwd_base, c->F_val, c->vL, c->vUt, c->vU, c->vLt);
     RH_LAUNCHED(c);
   }
   int status = 0;
