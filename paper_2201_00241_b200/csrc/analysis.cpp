@@ -14,6 +14,7 @@
 #include "analysis.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cstdint>
 #include <cmath>
 #include <cstdio>
@@ -82,51 +83,65 @@ std::vector<int32_t> minimum_degree(std::vector<std::vector<int32_t>> adj) {
 // their diagonal block is inverted once per state (k_tops_inverse) and applied
 // as a dense product, so every sweep of a block needs only 2-3 CTA barriers.
 // The same split serves both directions and the refactorization.
-BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<std::vector<int32_t>> &Ls,
-                       const std::vector<std::vector<int32_t>> &Lrow, int nw, int max_tops) {
-  const int n = (int)rows.size();
+//
+// Nodes are bus UNITS (the 1 or 2 rows of a bus, see UnitSweep): a unit's rows
+// always land in the same piece (or both in the tops), so the bus-unit sweeps
+// can process them together.  A unit's parent is the unit holding the
+// elimination-tree parent of its highest row.
+BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<int32_t> &unit_lo,
+                       const std::vector<std::vector<int32_t>> &Ls, const std::vector<std::vector<int32_t>> &Lrow,
+                       int nw, int max_tops) {
+  const int n = (int)rows.size();   // ascending permuted rows
+  std::vector<int> uofr(n), ubeg;   // unit of each local row, first local row of each unit
+  for (int i = 0; i < n; ++i) {
+    if (i == 0 || unit_lo[rows[i]] != unit_lo[rows[i - 1]]) ubeg.push_back(i);
+    uofr[i] = (int)ubeg.size() - 1;
+  }
+  const int nu = (int)ubeg.size();
+  ubeg.push_back(n);
   std::unordered_map<int, int> li;
   li.reserve(n * 2);
   for (int i = 0; i < n; ++i) li[rows[i]] = i;
-  std::vector<int> par(n, -1);
-  std::vector<std::vector<int>> kids(n);
-  std::vector<double> cost(n), sc(n);
-  for (int i = 0; i < n; ++i) {
-    const int r = rows[i];
-    if (!Ls[r].empty()) {
-      auto it = li.find(Ls[r][0]);
-      if (it != li.end()) par[i] = it->second;
+  std::vector<int> par(nu, -1);
+  std::vector<std::vector<int>> kids(nu);
+  std::vector<double> cost(nu, 0.0), sc(nu);
+  std::vector<int> usize(nu);
+  for (int u = 0; u < nu; ++u) {
+    usize[u] = ubeg[u + 1] - ubeg[u];
+    const int hi = rows[ubeg[u + 1] - 1];
+    if (!Ls[hi].empty()) {
+      auto it = li.find(Ls[hi][0]);
+      if (it != li.end()) par[u] = uofr[it->second];
     }
-    cost[i] = 8.0 + (double)(Lrow[r].size() + Ls[r].size());
+    for (int i = ubeg[u]; i < ubeg[u + 1]; ++i) cost[u] += 8.0 + (double)(Lrow[rows[i]].size() + Ls[rows[i]].size());
   }
-  for (int i = 0; i < n; ++i)
-    if (par[i] >= 0) kids[par[i]].push_back(i);
-  std::vector<int> ordi(n);
-  std::iota(ordi.begin(), ordi.end(), 0);
-  std::sort(ordi.begin(), ordi.end(), [&](int x, int y) { return rows[x] < rows[y]; });
-  for (int i : ordi) {  // children have smaller global index
-    sc[i] = cost[i];
-    for (int k : kids[i]) sc[i] += sc[k];
+  for (int u = 0; u < nu; ++u)
+    if (par[u] >= 0) kids[par[u]].push_back(u);
+  for (int u = 0; u < nu; ++u) {  // children precede parents (ascending rows)
+    sc[u] = cost[u];
+    for (int k : kids[u]) sc[u] += sc[k];
   }
   double total = 0;
   std::vector<int> pieces;
-  for (int i = 0; i < n; ++i)
-    if (par[i] < 0) {
-      pieces.push_back(i);
-      total += sc[i];
+  for (int u = 0; u < nu; ++u)
+    if (par[u] < 0) {
+      pieces.push_back(u);
+      total += sc[u];
     }
   const double target = total / nw;
-  std::vector<char> is_top(n, 0);
-  int ntop = 0;
-  while (ntop < max_tops) {
+  std::vector<char> is_top(nu, 0);
+  int ntop = 0, ntop_units = 0;
+  while (true) {
     int best = -1;
     for (int k = 0; k < (int)pieces.size(); ++k)
       if (best < 0 || sc[pieces[k]] > sc[pieces[best]]) best = k;
     if (best < 0 || sc[pieces[best]] <= 1.25 * target || kids[pieces[best]].empty()) break;
     const int p = pieces[best];
+    if (ntop + usize[p] > max_tops || ntop_units >= UnitSweep::kMaxTopUnits) break;
     pieces.erase(pieces.begin() + best);
     is_top[p] = 1;
-    ++ntop;
+    ntop += usize[p];
+    ++ntop_units;
     for (int k : kids[p]) pieces.push_back(k);
   }
   std::sort(pieces.begin(), pieces.end(), [&](int x, int y) { return sc[x] > sc[y]; });
@@ -140,15 +155,228 @@ BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<std::
     while (!st.empty()) {
       const int x = st.back();
       st.pop_back();
-      B.warp_rows[w].push_back(rows[x]);
+      for (int i = ubeg[x]; i < ubeg[x + 1]; ++i) B.warp_rows[w].push_back(rows[i]);
       for (int k : kids[x]) st.push_back(k);
     }
   }
   for (auto &v : B.warp_rows) std::sort(v.begin(), v.end());  // ascending = forward topological
-  for (int i = 0; i < n; ++i)
-    if (is_top[i]) B.tops.push_back(rows[i]);
+  for (int u = 0; u < nu; ++u)
+    if (is_top[u])
+      for (int i = ubeg[u]; i < ubeg[u + 1]; ++i) B.tops.push_back(rows[i]);
   std::sort(B.tops.begin(), B.tops.end());
   return B;
+}
+
+// ---------------------------------------------------------------------------
+// Bus-unit schedule of the block sweeps of one pattern direction (UnitSweep;
+// DESIGN.md "Block sweeps").  fwd: rows ascending, deps = L row (sweeps L and
+// U^T); bwd: rows descending, deps = U row (sweeps U and L^T).  Sweep a takes
+// the coefficient (i, k) from F(i, k), sweep b from F(k, i).
+// ---------------------------------------------------------------------------
+template <class FPos>
+void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> &Ls,
+                 const std::vector<std::vector<int32_t>> &Lrow, FPos fpos) {
+  UnitSweep &U = fwd ? A.ufwd : A.ubwd;
+  const SegSweep &S = fwd ? A.fwd : A.bwd;
+  const int nb = A.nblk;
+  U = UnitSweep();
+  U.unit_off.assign(1, 0);
+  U.tmeta_off.assign(1, 0);
+  U.rec_off.assign(1, 0);
+  U.doff_off.assign(1, 0);
+  U.top_pos_off.assign(1, 0);
+  auto deps = [&](int i) -> const std::vector<int32_t> & { return fwd ? Lrow[i] : Ls[i]; };
+  auto coef = [&](bool b, int i, int k) -> int {   // src code of the coefficient (row i, dep k)
+    const auto &d = deps(i);
+    if (!std::binary_search(d.begin(), d.end(), k)) return -1;
+    return b ? fpos(k, i) : fpos(i, k);
+  };
+  for (int s = 0; s < nb; ++s) {
+    const int r0 = A.seg_row_off[s], nr = A.seg_row_off[s + 1] - r0;
+    const int x0 = S.ext_off[s], nxr = S.ext_off[s + 1] - x0;
+    U.max_rows = std::max(U.max_rows, nr + nxr);
+    std::unordered_map<int, int> ext_pos;   // separator row -> tile row
+    for (int k = 0; k < nxr; ++k) ext_pos[S.ext_rows[x0 + k]] = nr + k;
+    auto tile_row = [&](int k) { return A.seg_of[k] == s ? A.loc_of[k] : ext_pos.at(k); };
+    const BlockSplit &B = A.usplit[s];
+    std::vector<char> top(nr, 0);
+    for (int r : B.tops) top[A.loc_of[r]] = 1;
+    // units in schedule order: pieces (warp by warp, sweep order), then tops
+    std::vector<std::vector<int>> units;   // rows in sweep order (first, second)
+    std::vector<int> lvl;
+    auto add_units = [&](std::vector<int32_t> rows) {
+      if (!fwd) std::reverse(rows.begin(), rows.end());
+      for (size_t i = 0; i < rows.size(); ++i) {
+        const int r = rows[i];
+        if (i + 1 < rows.size() && A.unit_lo[rows[i + 1]] == A.unit_lo[r]) {
+          units.push_back({r, rows[i + 1]});
+          ++i;
+        } else {
+          units.push_back({r});
+        }
+      }
+    };
+    for (int w = 0; w < UnitSweep::kWarps; ++w) {
+      lvl.push_back((int)units.size());
+      add_units(B.warp_rows[w]);
+    }
+    lvl.push_back((int)units.size());
+    const int tu0 = (int)units.size();
+    add_units(B.tops);
+    const int tu1 = (int)units.size();
+    lvl.push_back(tu0);
+    lvl.push_back(tu1);
+    while ((int)lvl.size() < UnitSweep::kLvl) lvl.push_back(0);
+    U.lvl.insert(U.lvl.end(), lvl.begin(), lvl.end());
+    const int rec0 = (int)U.src_a.size() / 2, off0 = (int)U.doff.size();
+    // dependency units: (first tile row, number of values)
+    auto dep_units = [&](const std::vector<int> &u, bool tops_only, bool skip_tops) {
+      std::vector<std::pair<int, int>> du;   // (first dependency row (permuted), values)
+      std::set<int> seen;
+      for (int i : u)
+        for (int k : deps(i)) {
+          if (std::find(u.begin(), u.end(), k) != u.end()) continue;
+          const bool kt = A.seg_of[k] == s && top[A.loc_of[k]];
+          if ((tops_only && !kt) || (skip_tops && kt)) continue;
+          int lo = A.unit_lo[k], nv = (lo + 1 < A.n_x && A.unit_lo[lo + 1] == lo) ? 2 : 1;
+          if (A.seg_of[k] != s) {   // staged separator rows: two values only if both are staged
+            if (nv == 2 && !(ext_pos.count(lo) && ext_pos.count(lo + 1))) {
+              lo = k;
+              nv = 1;
+            }
+          }
+          if (seen.insert(lo).second) du.push_back({lo, nv});
+        }
+      std::stable_sort(du.begin(), du.end(), [&](const std::pair<int, int> &a, const std::pair<int, int> &b) {
+        return tile_row(a.first) < tile_row(b.first);
+      });
+      return du;
+    };
+    // emit one dependency list; returns the int4 meta; `hdr`: piece unit header
+    // records.  Every dependency is a pair of tile rows (o0, o1) (byte offsets;
+    // a one-value dependency repeats its row with a zero second coefficient);
+    // lists are padded to chunks of 4 with zero dependencies on the unit's row.
+    auto emit = [&](const std::vector<int> &u, const std::vector<std::pair<int, int>> &du, bool hdr,
+                    std::vector<int> *pos_rows, std::vector<int32_t> *pos_out) {
+      const bool two = u.size() == 2;
+      const int cbeg = (int)U.src_a.size() / 2 - rec0, obeg = (int)U.doff.size() - off0;
+      auto rec = [&](int a0, int a1, int b0, int b1) {
+        U.src_a.push_back(a0);
+        U.src_a.push_back(a1);
+        U.src_b.push_back(b0);
+        U.src_b.push_back(b1);
+      };
+      if (hdr) {
+        // (dinv_f, dinv_s): sweep a = fwd L (unit) / bwd U; sweep b = fwd U^T / bwd L^T (unit)
+        auto inv = [&](int i) { return -2 - A.F_diag[i]; };
+        const int f = u[0], sr = two ? u[1] : -1;
+        rec(fwd ? -1 : inv(f), (!fwd && two) ? inv(sr) : -1, fwd ? inv(f) : -1, (fwd && two) ? inv(sr) : -1);
+        if (two) rec(coef(false, sr, f), -1, coef(true, sr, f), -1);
+      }
+      const int nd = (int)du.size(), nchunk = (nd + 3) / 4;
+      const int rowb = UnitSweep::kCols * 8;
+      for (int di = 0; di < 4 * nchunk; ++di) {
+        if (di >= nd) {   // padding: zero coefficients on the unit's own (finite) row
+          U.doff.push_back(A.loc_of[u[0]] * rowb);
+          U.doff.push_back(A.loc_of[u[0]] * rowb);
+          rec(-1, -1, -1, -1);
+          if (two) rec(-1, -1, -1, -1);
+          continue;
+        }
+        const int k0 = du[di].first, nv = du[di].second, k1 = nv == 2 ? k0 + 1 : -1;
+        U.doff.push_back(tile_row(k0) * rowb);
+        U.doff.push_back(tile_row(nv == 2 ? k1 : k0) * rowb);
+        const size_t at = U.src_a.size();
+        auto cf = [&](bool b, int i, int k) { return k < 0 ? -1 : coef(b, i, k); };
+        rec(cf(false, u[0], k0), cf(false, u[0], k1), cf(true, u[0], k0), cf(true, u[0], k1));
+        if (two) rec(cf(false, u[1], k0), cf(false, u[1], k1), cf(true, u[1], k0), cf(true, u[1], k1));
+        if (pos_rows) {   // dense tops list: record where M(row, dep) lives
+          const std::vector<int> &T = *pos_rows;
+          auto ti = [&](int r) { return (int)(std::lower_bound(T.begin(), T.end(), r) - T.begin()); };
+          const int nt = (int)T.size();
+          for (int ri = 0; ri < (int)u.size(); ++ri)
+            for (int v = 0; v < nv; ++v) (*pos_out)[ti(u[ri]) * nt + ti(k0 + v)] = (int)(at + 2 * ri + v);
+        }
+      }
+      return std::array<int, 4>{A.loc_of[u[0]] | ((two ? A.loc_of[u[1]] : 0) << 16), cbeg, obeg,
+                                nchunk | ((two ? 1 : 0) << 16)};
+    };
+    const int nt = (int)B.tops.size();
+    std::vector<int32_t> tpos((size_t)nt * nt, -1);
+    std::vector<int> tops_sorted(B.tops.begin(), B.tops.end());
+    for (int ui = 0; ui < (int)units.size(); ++ui) {
+      const auto &u = units[ui];
+      const bool is_top = ui >= tu0;
+      const auto m = emit(u, dep_units(u, false, is_top), !is_top, nullptr, nullptr);
+      U.meta.insert(U.meta.end(), m.begin(), m.end());
+    }
+    for (int ui = tu0; ui < tu1; ++ui) {   // dense lists of the tops: every top unit
+      const auto &u = units[ui];
+      std::vector<std::pair<int, int>> du;
+      for (int vi = tu0; vi < tu1; ++vi) {
+        const auto &v = units[vi];
+        const int lo = std::min(v.front(), v.back());
+        du.push_back({lo, (int)v.size()});
+      }
+      const auto m = emit(u, du, false, &tops_sorted, &tpos);
+      U.tmeta.insert(U.tmeta.end(), m.begin(), m.end());
+    }
+    // double positions were recorded relative to the global record array
+    U.top_pos.insert(U.top_pos.end(), tpos.begin(), tpos.end());
+    U.top_pos_off.push_back((int)U.top_pos.size());
+    U.unit_off.push_back((int)(U.meta.size() / 4));
+    U.tmeta_off.push_back((int)(U.tmeta.size() / 4));
+    U.rec_off.push_back((int)U.src_a.size() / 2);
+    U.doff_off.push_back((int)U.doff.size());
+    const int nrec = (int)U.src_a.size() / 2 - rec0, noff = (int)U.doff.size() - off0;
+    U.max_units = std::max(U.max_units, (int)units.size());
+    U.max_tunits = std::max(U.max_tunits, tu1 - tu0);
+    U.max_rec = std::max(U.max_rec, nrec);
+    U.max_doff = std::max(U.max_doff, noff);
+    // scheduling weight ~ shared-memory wavefronts of one 32-column tile
+    U.cost.push_back(std::max(1, 3 * nrec + noff / 8 + 6 * nr + 4 * nxr));
+  }
+  if (getenv("RH_DEBUG_SCHED")) {
+    long long tot = 0;
+    for (int c : U.cost) tot += c;
+    for (int s = 0; s < nb && s < 6; ++s) {   // per-warp chain: units and records
+      const int *lv = U.lvl.data() + s * UnitSweep::kLvl;
+      const int ub = U.unit_off[s];
+      int mu = 0, mr = 0, sr = 0;
+      for (int w = 0; w < UnitSweep::kWarps; ++w) {
+        int r = 0;
+        for (int u = lv[w]; u < lv[w + 1]; ++u) {
+          const int *m = U.meta.data() + 4 * (ub + u);
+          r += (m[3] & 0xffff) * 4 * ((m[3] >> 16) ? 2 : 1);
+        }
+        mu = std::max(mu, lv[w + 1] - lv[w]);
+        mr = std::max(mr, r);
+        sr += r;
+      }
+      fprintf(stderr, "  %s blk %d: units %d, warp max units %d, warp max records %d (mean %d), tops units %d\n",
+              fwd ? "fwd" : "bwd", s, U.unit_off[s + 1] - ub, mu, mr, sr / UnitSweep::kWarps,
+              lv[UnitSweep::kWarps + 2] - lv[UnitSweep::kWarps + 1]);
+    }
+    fprintf(stderr, "units %s: blocks %d max rows %d units %d tops-units %d rec %d doff %d; records %zu, cost sum %lld\n",
+            fwd ? "fwd" : "bwd", nb, U.max_rows, U.max_units, U.max_tunits, U.max_rec, U.max_doff,
+            U.src_a.size() / 2, tot);
+    // shared-memory wavefronts of one 32-column tile (X loads 2, broadcast loads 1), mean over blocks
+    long long wf_piece = 0, wf_tops = 0, deps = 0, real = 0;
+    for (size_t u = 0; u < U.meta.size() / 4; ++u) {
+      const int *m = U.meta.data() + 4 * u;
+      const int nchk = m[3] & 0xffff, two = m[3] >> 16;
+      wf_piece += nchk * (16 + (two ? 8 : 4) + 2) + (two ? 2 : 1) + 4 * (two ? 2 : 1) + 1;
+      deps += 4 * nchk;
+    }
+    for (size_t u = 0; u < U.tmeta.size() / 4; ++u) {
+      const int *m = U.tmeta.data() + 4 * u;
+      const int nchk = m[3] & 0xffff, two = m[3] >> 16;
+      wf_tops += nchk * (16 + (two ? 8 : 4) + 2) + 2 * (two ? 2 : 1);
+    }
+    for (size_t i = 0; i < U.doff.size(); i += 2) real += U.doff[i] != U.doff[i + 1] || true;
+    fprintf(stderr, "  smem wavefronts per tile: units+gather %lld, tops dense %lld; dep slots %lld\n",
+            wf_piece / std::max(nb, 1), wf_tops / std::max(nb, 1), deps / std::max(nb, 1));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -199,6 +427,11 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
       A.seg_of[k] = A.seg_of[parent[k]];
   }
   const int nseg = nb + 1;
+  // bus units: consecutive permuted rows of one bus in one segment (theta_b, v_b)
+  A.unit_lo.assign(nx, 0);
+  for (int k = 0; k < nx; ++k)
+    A.unit_lo[k] = (k > 0 && A.x_bus[A.perm[k]] == A.x_bus[A.perm[k - 1]] && A.seg_of[k] == A.seg_of[k - 1])
+                       ? A.unit_lo[k - 1] : k;
   A.seg_row_off.assign(nseg + 1, 0);
   for (int k = 0; k < nx; ++k) A.seg_row_off[A.seg_of[k] + 1]++;
   for (int s = 0; s < nseg; ++s) A.seg_row_off[s + 1] += A.seg_row_off[s];
@@ -380,7 +613,12 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
   if (const char *env = getenv("RH_TOPS")) tops_cap = std::max(0, std::min(kMaxTops, atoi(env)));  // tuning override
   for (int s = 0; s < nb; ++s) {
     std::vector<int32_t> rows(A.row_global.begin() + A.seg_row_off[s], A.row_global.begin() + A.seg_row_off[s + 1]);
-    A.split[s] = split_block(rows, Ls, Lrow, kSchedWarps, tops_cap);
+    A.split[s] = split_block(rows, A.unit_lo, Ls, Lrow, kSchedWarps, tops_cap);
+  }
+  A.usplit.assign(nb, BlockSplit());
+  for (int s = 0; s < nb; ++s) {
+    std::vector<int32_t> rows(A.row_global.begin() + A.seg_row_off[s], A.row_global.begin() + A.seg_row_off[s + 1]);
+    A.usplit[s] = split_block(rows, A.unit_lo, Ls, Lrow, UnitSweep::kWarps, tops_cap);
   }
   A.top_fwd_base.clear();
   A.top_bwd_base.clear();
@@ -414,6 +652,8 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
       fprintf(stderr, "%s: est worst %lld mean %lld cycles\n", S == &A.fwd ? "fwd" : "bwd", worst, sum / std::max(nb, 1));
     }
   }
+  build_units(A, true, Ls, Lrow, fpos);
+  build_units(A, false, Ls, Lrow, fpos);
   // tops of every block for k_tops_inverse: rows and F positions of T x T
   A.top_ptr.assign(nb + 1, 0);
   A.top_rows.clear();
@@ -421,7 +661,7 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
   A.top_fpos_ptr.assign(nb + 1, 0);
   A.max_tops = 0;
   for (int s = 0; s < nb; ++s) {
-    const auto &T = A.split[s].tops;
+    const auto &T = A.usplit[s].tops;
     A.top_rows.insert(A.top_rows.end(), T.begin(), T.end());
     A.top_ptr[s + 1] = (int)A.top_rows.size();
     for (int x : T)

@@ -54,6 +54,42 @@ struct BlockSplit {
   std::vector<int32_t> tops;                    // top rows (global, ascending)
 };
 
+// Bus-unit schedule of the block sweeps.  The
+// (theta_b, v_b) rows of a PQ bus are consecutive in the ordering and have the
+// same L / U pattern outside their 2 x 2 diagonal block, so a sweep processes
+// a bus ("unit", 1 or 2 rows) at once: every dependency value loaded from
+// shared memory feeds both rows (half the shared-memory traffic per FMA).
+// Per block, units are listed warp piece by warp piece (sweep order), then the
+// tops.  Tile rows: the block's rows (local index), then its staged separator
+// rows (backward sweeps).
+struct UnitSweep {
+  static constexpr int kWarps = 8;   // warps of the unit sweep kernel (k_blk: 2 CTAs per SM)
+  static constexpr int kLvl = 12;    // per block: kWarps + 1 piece bounds, 2 tops bounds, 1 pad
+  static constexpr int kCols = 32;   // columns of a sweep tile (one per lane)
+  static constexpr int kMaxTopUnits = 16;   // one tops unit per warp
+  std::vector<int32_t> unit_off;     // [nblk + 1] units of each block
+  std::vector<int32_t> lvl;          // [nblk * kLvl], block-relative unit indices
+  // per unit (int4): row_f | row_s << 16 (tile rows, sweep order), first record
+  // (double2, block-relative), first dependency offset pair (int, block-
+  // relative, multiple of 8), nchunks | two_rows << 16.  A dependency is a
+  // pair of tile-row byte offsets (o0, o1) and one (one-row unit) or two
+  // (two-row unit) double2 coefficient records (c_f0, c_f1), (c_s0, c_s1);
+  // lists are padded to chunks of 4 dependencies.
+  std::vector<int32_t> meta;
+  std::vector<int32_t> tmeta;        // tops units only (same format): the dense list
+  std::vector<int32_t> tmeta_off;    // [nblk + 1] into tmeta (units)
+  std::vector<int32_t> rec_off;      // [nblk + 1] double2 records
+  // per record double: F position (>= 0), -1 zero, <= -2: 1 / F[-s - 2];
+  // a: first sweep of the pattern (fwd L, bwd U), b: second (fwd U^T, bwd L^T)
+  std::vector<int32_t> src_a, src_b;
+  std::vector<int32_t> doff_off;     // [nblk + 1]
+  std::vector<int32_t> doff;         // (o0, o1) byte offsets of a dependency's tile rows
+  std::vector<int32_t> top_pos;      // per block nt x nt: double index of M(a, c) (tops ascending)
+  std::vector<int32_t> top_pos_off;  // [nblk + 1]
+  std::vector<int32_t> cost;         // [nblk] per-tile cost estimate (scheduling weight)
+  int max_units = 0, max_tunits = 0, max_rec = 0, max_doff = 0, max_rows = 0;
+};
+
 struct Analysis {
   // ---------------- grid copy ----------------
   int n_bus = 0, n_line = 0, n_gen = 0, ref = -1;
@@ -114,7 +150,10 @@ struct Analysis {
   int max_seg_rows = 0, sep_rows = 0;
   SegSweep fwd, bwd;                        // fwd: L and U^T ; bwd: U and L^T
   std::vector<int32_t> blk_gp_ptr, blk_gp_loc;  // per block: local rows carrying G_p entries
-  std::vector<BlockSplit> split;            // per block
+  std::vector<BlockSplit> split;            // per block (16 warps: refactorization R_A)
+  std::vector<BlockSplit> usplit;           // per block (UnitSweep::kWarps: unit sweeps, tops)
+  std::vector<int32_t> unit_lo;             // [n_x] lowest permuted row of the row's bus unit
+  UnitSweep ufwd, ubwd;                     // bus-unit block sweeps (fwd: L, U^T; bwd: U, L^T)
   // tops of every block (densely inverted per state): rows, F positions of T x T,
   // and the first dense entry of every top row in the fwd / bwd entry arrays
   std::vector<int32_t> top_ptr, top_rows, top_fpos_ptr, top_fpos, top_fwd_base, top_bwd_base;

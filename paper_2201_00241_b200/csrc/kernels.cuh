@@ -27,13 +27,28 @@ struct DSeg {
   const int *__restrict__ ext_rows;
 };
 
+// Bus-unit schedule of one pattern direction (analysis.hpp UnitSweep).
+struct DUnit {
+  const int4 *__restrict__ meta;     // per unit
+  const int4 *__restrict__ tmeta;    // per tops unit: dense list
+  const int *__restrict__ unit_off, *__restrict__ tmeta_off, *__restrict__ lvl, *__restrict__ rec_off;
+  const int *__restrict__ doff_off, *__restrict__ doff;
+  const int *__restrict__ blk_order;  // blocks by decreasing cost (tile tickets are block-major in this order)
+  const int *__restrict__ ext_off, *__restrict__ ext_rows;   // staged separator rows (Z rows)
+};
+
 struct SegParams {
   int n_x, n_p, n_bus, N, ld;
   int nblk;                          // segment nblk = separator
+  DUnit uf, ub;                      // bus-unit block sweeps: fwd (L, U^T), bwd (U, L^T)
+  const double2 *uL, *uUt, *uU, *uLt;  // their record values (per state)
+  int maxrx;                         // max tile rows (block rows + staged separator rows)
+  int smem_stride;                   // bytes per buffer (two buffers: current tile, prefetched tile)
+  int smem_x_off, smem_meta_off, smem_tmeta_off, smem_rec_off, smem_doff_off, smem_lvl_off;  // bytes
+  int *blk_ctr;                      // [2 per mode] tile ticket counter, CTAs done (self-resetting)
   const int *seg_row_off, *row_global;
   DSeg fwd, bwd;
-  const double *vL, *vUt, *vU, *vLt;   // values per sweep (entry order of fwd / bwd)
-  const double *dinv_fwd, *dinv_bwd;   // 1 / u_ii in fwd / bwd q order
+  const double *vL, *vUt;             // separator rows' L / U^T values (fwd entry order)
   int ns, sep_off;                     // separator rows, first separator slot in row_global
   const double *Sinv, *SinvT;          // dense [ns][ns] inverse of the separator block L_ss U_ss (+ transpose)
   double *Tsep;                        // [ns][ld] separator right-hand sides

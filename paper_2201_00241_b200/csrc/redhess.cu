@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <numeric>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -501,8 +502,8 @@ __global__ void k_transpose(const double *__restrict__ A, double *AT, int n) {
 // One CTA per block, one thread per column (forward / backward substitution).
 constexpr int kMaxTops = 64;
 __global__ void __launch_bounds__(kMaxTops) k_tops_inverse(const int *top_ptr, const int *top_fpos_ptr,
-                                                           const int *top_fpos, const int *fwd_base,
-                                                           const int *bwd_base, const double *F, double *vL,
+                                                           const int *top_fpos, const int *fwd_pos,
+                                                           const int *bwd_pos, const double *F, double *vL,
                                                            double *vUt, double *vU, double *vLt) {
   extern __shared__ double tops_sm[];
   double(*T)[kMaxTops + 1] = reinterpret_cast<double(*)[kMaxTops + 1]>(tops_sm);  // L_TT below, U_TT on/above
@@ -538,13 +539,19 @@ __global__ void __launch_bounds__(kMaxTops) k_tops_inverse(const int *top_ptr, c
     }
   }
   __syncthreads();
+  // dense tops records of the bus-unit sweeps: (a, c) -> double index
+  const int *fp_ = fwd_pos + top_fpos_ptr[s], *bp_ = bwd_pos + top_fpos_ptr[s];
   for (int x = threadIdx.x; x < nt * nt; x += blockDim.x) {
     const int a = x / nt, c = x % nt;
-    const int fb = fwd_base[t0 + a], bb = bwd_base[t0 + a];
-    vL[fb + c] = ML[a][c];
-    vUt[fb + c] = MU[c][a];
-    vU[bb + c] = MU[a][c];
-    vLt[bb + c] = ML[c][a];
+    const int fb = fp_[x], bb = bp_[x];
+    if (fb >= 0) {
+      vL[fb] = ML[a][c];
+      vUt[fb] = MU[c][a];
+    }
+    if (bb >= 0) {
+      vU[bb] = MU[a][c];
+      vLt[bb] = ML[c][a];
+    }
   }
 }
 
@@ -553,9 +560,12 @@ __global__ void k_gather_vals(int n, const int *__restrict__ src, const double *
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n) dst[e] = src[e] >= 0 ? F[src[e]] : 0.0;   // src < 0: padding entry
 }
-__global__ void k_gather_inv(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
+// unit-sweep record values: src >= 0: F[src]; -1: 0; <= -2: 1 / F[-src - 2]
+__global__ void k_gather_code(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n) dst[e] = 1.0 / F[src[e]];
+  if (e >= n) return;
+  const int c = src[e];
+  dst[e] = c >= 0 ? F[c] : c == -1 ? 0.0 : 1.0 / F[-c - 2];
 }
 
 // ============================================================================
@@ -579,207 +589,7 @@ __device__ __forceinline__ long long hw_index(const SegParams &h, int row, int c
   return h.transposed ? (long long)col * h.ldhw + row : (long long)row * h.ldhw + col;
 }
 
-// ----------------------------------------------------------------------------
-// Block segments.  One CTA = (block, 32 columns), 512 threads: one warp per
-// row, one lane per column.  The block's X tile (rows x 32 columns) AND its
-// sweep structure (levels, rows, entries, coefficients) are staged in shared
-// memory, so a row's dependency chain is shared-memory only; the coefficient
-// and index reads are warp-uniform broadcasts and the X gathers are 256 B
-// contiguous (conflict-free).  External entries (separator rows of Z / P in
-// the backward sweeps) are read from L2/HBM.
-// ----------------------------------------------------------------------------
 constexpr int kSegC = 32;   // columns of the single-RHS (lambda) path
-
-struct SegStage {  // shared-memory carve-up of one block sweep
-  double *X;
-  double2 *ent;     // per entry: (coefficient, byte offset of the dependency row in X, bit-cast)
-  int4 *meta;       // per row q: (byte offset of the row in X, first entry, number of 4-entry groups, -)
-  double *dinv;
-  int *lvl;
-  int nq, ne, nlev;
-  long long *prof;  // timing experiment (RH_DEBUG & 8): per-warp piece and top-phase cycles, else null
-};
-
-// Stage a block's sweep structure in shared memory behind an X tile of `nrx`
-// rows x C columns.  Rows are padded to multiples of 4 entries on the host.
-__device__ __forceinline__ SegStage stage_seg(const DSeg &S, const double *__restrict__ val,
-                                              const double *__restrict__ dinv, int seg, int qb, int nq, int nrx,
-                                              int C, double *sm) {
-  // a block's rows occupy q in [qb, qb + nq) = its segment rows (any lvl layout)
-  SegStage t;
-  t.prof = nullptr;
-  const int l0 = S.seg_lvl[seg], l1 = S.seg_lvl[seg + 1];
-  t.nlev = l1 - l0 - 1;
-  t.nq = nq;
-  const int eb = S.rptr[qb];
-  t.ne = S.rptr[qb + t.nq] - eb;
-  const long long rowb = (long long)C * 8;
-  t.X = sm;
-  t.ent = reinterpret_cast<double2 *>(t.X + (size_t)nrx * C);
-  t.meta = reinterpret_cast<int4 *>(t.ent + t.ne);
-  t.dinv = reinterpret_cast<double *>(t.meta + t.nq);
-  t.lvl = reinterpret_cast<int *>(t.dinv + t.nq);
-#pragma unroll 4
-  for (int i = threadIdx.x; i < t.ne; i += blockDim.x)
-    t.ent[i] = make_double2(val[eb + i], __longlong_as_double((long long)S.dep[eb + i] * rowb));
-  for (int i = threadIdx.x; i < t.nq; i += blockDim.x) {
-    const int e0 = S.rptr[qb + i] - eb, ex = S.rext[qb + i] - eb, e1 = S.rptr[qb + i + 1] - eb;
-    t.meta[i] = make_int4((int)(S.order[qb + i] * rowb), e0, (ex - e0) >> 2, (e1 - ex) >> 2);
-    t.dinv[i] = dinv ? dinv[qb + i] : 1.0;
-  }
-  for (int i = threadIdx.x; i <= t.nlev; i += blockDim.x) t.lvl[i] = S.lvl_ptr[l0 + i] - qb;
-  return t;
-}
-
-// bytes of shared memory stage_seg needs for a block
-__host__ __device__ inline size_t seg_smem_bytes(int nrx, int nq, int ne, int nlev, int C) {
-  return (size_t)nrx * C * 8 + (size_t)ne * 16 + (size_t)nq * 16 + (size_t)nq * 8 + (size_t)(nlev + 1) * 4 + 16;
-}
-
-template <int CPL>
-__device__ __forceinline__ void ldx(const double *p, double (&x)[CPL]) {
-  if constexpr (CPL == 1) {
-    x[0] = p[0];
-  } else {
-#pragma unroll
-    for (int i = 0; i < CPL; i += 2) {
-      const double2 v = *reinterpret_cast<const double2 *>(p + i);
-      x[i] = v.x;
-      x[i + 1] = v.y;
-    }
-  }
-}
-template <int CPL>
-__device__ __forceinline__ void stx(double *p, const double (&x)[CPL]) {
-  if constexpr (CPL == 1) {
-    p[0] = x[0];
-  } else {
-#pragma unroll
-    for (int i = 0; i < CPL; i += 2) *reinterpret_cast<double2 *>(p + i) = make_double2(x[i], x[i + 1]);
-  }
-}
-
-// Sum over `ng` 4-entry groups starting at ep: val * X[row] for this lane's columns.
-template <int CPL>
-__device__ __forceinline__ void group_sum(const double2 *ep, int ng, const char *Xb, double (&acc)[CPL]) {
-  double s1[CPL];
-#pragma unroll
-  for (int i = 0; i < CPL; ++i) s1[i] = 0.0;
-  for (int g = 0; g < ng; ++g, ep += 4) {
-    const double2 p0 = ep[0], p1 = ep[1], p2 = ep[2], p3 = ep[3];
-    double x0[CPL], x1[CPL], x2[CPL], x3[CPL];
-    ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p0.y)), x0);
-    ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p1.y)), x1);
-    ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p2.y)), x2);
-    ldx<CPL>(reinterpret_cast<const double *>(Xb + __double_as_longlong(p3.y)), x3);
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) {
-      acc[i] = fma(p0.x, x0[i], acc[i]);
-      s1[i] = fma(p1.x, x1[i], s1[i]);
-      acc[i] = fma(p2.x, x2[i], acc[i]);
-      s1[i] = fma(p3.x, x3[i], s1[i]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < CPL; ++i) acc[i] += s1[i];
-}
-
-// One sweep over a block.  lvl[0..nw] bound each warp's
-// piece rows (whole subtrees, dependency order, no synchronization: lanes own
-// their columns); lvl[nw+1..nw+2] bound the block's top rows, solved densely:
-// t = X - (entries outside the tops), then X_T = M t with M the inverse of the
-// tops' diagonal block (k_tops_inverse).  Forward: pieces, then tops;
-// backward: tops, then pieces.  3-4 CTA barriers per sweep.
-constexpr int kMaxTopRowsPerWarp = 4;   // 64 tops / 16 warps
-template <int CPL>
-__device__ __forceinline__ void seg_pieces(const SegStage &t, bool use_dinv) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const char *Xb = reinterpret_cast<const char *>(t.X) + lane * CPL * 8;
-  const int q0 = t.lvl[warp], q1 = t.lvl[warp + 1];
-  const long long c0 = t.prof ? clock64() : 0;
-  int4 m = q0 < q1 ? t.meta[q0] : make_int4(0, 0, 0, 0);
-  for (int q = q0; q < q1; ++q) {
-    const int4 mn = q + 1 < q1 ? t.meta[q + 1] : m;
-    double acc[CPL];
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
-    group_sum<CPL>(t.ent + m.y, m.z, Xb, acc);
-    double *xr = reinterpret_cast<double *>(const_cast<char *>(Xb) + m.x);
-    double xa[CPL];
-    ldx<CPL>(xr, xa);
-    const double d = t.dinv[q];
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) {
-      xa[i] -= acc[i];
-      if (use_dinv) xa[i] *= d;
-    }
-    stx<CPL>(xr, xa);
-    m = mn;
-  }
-  if (t.prof && lane == 0) t.prof[warp] = clock64() - c0;
-  __syncthreads();
-}
-
-template <int CPL>
-__device__ __forceinline__ void seg_tops(const SegStage &t, int nw) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const char *Xb = reinterpret_cast<const char *>(t.X) + lane * CPL * 8;
-  const int q0 = t.lvl[nw + 1], q1 = t.lvl[nw + 2];
-  if (q0 >= q1) return;
-  const long long c0 = t.prof ? clock64() : 0;
-  // gather: t_r = X_r - sum over entries outside the tops (in place)
-  for (int q = q0 + warp; q < q1; q += nw) {
-    const int4 m = t.meta[q];
-    double acc[CPL];
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
-    group_sum<CPL>(t.ent + m.y, m.z, Xb, acc);
-    double *xr = reinterpret_cast<double *>(const_cast<char *>(Xb) + m.x);
-    double xa[CPL];
-    ldx<CPL>(xr, xa);
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) xa[i] -= acc[i];
-    stx<CPL>(xr, xa);
-  }
-  __syncthreads();
-  const long long c1 = t.prof ? clock64() : 0;
-  // dense: X_T = M t_T (results held in registers until every warp has read t)
-  double out[kMaxTopRowsPerWarp][CPL];
-#pragma unroll
-  for (int u = 0; u < kMaxTopRowsPerWarp; ++u) {
-    const int q = q0 + warp + u * nw;
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) out[u][i] = 0.0;
-    if (q < q1) {
-      const int4 m = t.meta[q];
-      group_sum<CPL>(t.ent + m.y + 4 * m.z, m.w, Xb, out[u]);
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int u = 0; u < kMaxTopRowsPerWarp; ++u) {
-    const int q = q0 + warp + u * nw;
-    if (q < q1) stx<CPL>(reinterpret_cast<double *>(const_cast<char *>(Xb) + t.meta[q].x), out[u]);
-  }
-  __syncthreads();
-  if (t.prof && threadIdx.x == 0) {
-    t.prof[16] = c1 - c0;
-    t.prof[17] = clock64() - c1;
-    t.prof[18] = q1 - q0;
-  }
-}
-
-template <int CPL>
-__device__ __forceinline__ void seg_sweep(const SegStage &t, bool use_dinv, bool fwd) {
-  const int nw = blockDim.x >> 5;
-  if (fwd) {
-    seg_pieces<CPL>(t, use_dinv);
-    seg_tops<CPL>(t, nw);
-  } else {
-    seg_tops<CPL>(t, nw);
-    seg_pieces<CPL>(t, use_dinv);
-  }
-}
 
 enum : int {
   MODE_L = 0,     // blocks:    rhs = -G_p W (SpMul fused), L sweep            -> Z
@@ -796,69 +606,305 @@ __device__ __forceinline__ double rhs_gpw(const SegParams &h, int row, int col) 
   return v;
 }
 
-// Block kernel: one CTA = (block, 32 * CPL columns), 512 threads.
-template <int CPL>
-__global__ void __launch_bounds__(kSegThreads, 1) k_seg(SegParams h, int mode) {
-  constexpr int C = 32 * CPL;
-  extern __shared__ double sm[];
-  const int seg = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int col0 = blockIdx.y * C;
-  const int r0 = h.seg_row_off[seg], nr = h.seg_row_off[seg + 1] - r0;
-  double *G = mode <= MODE_U ? h.Z : h.P;
-  const bool fwd = mode == MODE_L || mode == MODE_UT;
-  const DSeg &S = fwd ? h.fwd : h.bwd;
-  const double *val = mode == MODE_L ? h.vL : mode == MODE_U ? h.vU : mode == MODE_UT ? h.vUt : h.vLt;
-  const double *dinv = mode == MODE_U ? h.dinv_bwd : mode == MODE_UT ? h.dinv_fwd : nullptr;
-  const int x0 = S.ext_off[seg], nxr = S.ext_off[seg + 1] - x0;
-  long long tk[4] = {0, 0, 0, 0};
-  const bool instr = (h.debug & 8) && h.dbg && threadIdx.x == 0;
-  if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[0]));
-  SegStage t = stage_seg(S, val, dinv, seg, r0, nr, nr + nxr, C, sm);
-  t.prof = ((h.debug & 8) && h.dbg) ? h.dbg + 6 * 65536 + 20 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
-  constexpr int CH = C / 2;  // 16-byte chunks per row
-  if (mode == MODE_L) {
-    for (int i = threadIdx.x; i < nr * C; i += blockDim.x) t.X[i] = 0.0;
-    __syncthreads();
-    // -G_p W only on the rows that have G_p entries (rows adjacent to generator buses)
-    for (int k = h.blk_gp_ptr[seg] + warp; k < h.blk_gp_ptr[seg + 1]; k += nw) {
-      const int a = h.blk_gp_loc[k];
-      const int row = h.row_global[r0 + a];
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) t.X[a * C + lane * CPL + i] = rhs_gpw(h, row, col0 + lane * CPL + i);
+// ----------------------------------------------------------------------------
+// Block sweeps by bus units.
+// Persistent: one CTA per SM walks a contiguous range of (block, 32-column
+// chunk) tiles, balanced by the host's per-block cost.  The next tile's rows
+// stream into the second X buffer (cp.async) while the current tile is swept,
+// so the HBM traffic overlaps the shared-memory-bound sweep.  Lanes own
+// columns; a warp walks its pieces' units without synchronization; a unit is
+// the 1 or 2 rows of one bus, so every dependency value read from shared
+// memory feeds both rows (half the shared-memory wavefronts per FMA of a
+// row-by-row sweep).  The tops (a dense chain at the top of the block) are
+// applied as a dense product with their inverse (k_tops_inverse).
+// ----------------------------------------------------------------------------
+constexpr int kBC = UnitSweep::kCols;   // columns per tile: one per lane
+constexpr int kRowB = kBC * 8;           // bytes per tile row
+
+struct UStage {
+  const int4 *meta, *tmeta;
+  const double2 *rec;
+  const int4 *doff;
+  const int *lvl;
+};
+
+__device__ __forceinline__ double lds(const char *p) { return *reinterpret_cast<const double *>(p); }
+
+// sf = sum c_f x, ss = sum c_s x over a dependency list of `nch` chunks of 4
+// dependencies (tile-row byte offsets o0, o1; records (c_f0, c_f1) [, (c_s0,
+// c_s1)]).  Branch-free, two-deep FMA chains, fixed order (deterministic).
+template <bool TWO>
+__device__ __forceinline__ void dep_sums(const double2 *__restrict__ rc, const int4 *__restrict__ of, int nch,
+                                         const char *Xb, double &sf, double &ss) {
+  double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (int c = 0; c < nch; ++c, of += 2, rc += TWO ? 8 : 4) {
+    const int4 a = of[0], b = of[1];
+    const double x00 = lds(Xb + a.x), x01 = lds(Xb + a.y), x10 = lds(Xb + a.z), x11 = lds(Xb + a.w);
+    const double x20 = lds(Xb + b.x), x21 = lds(Xb + b.y), x30 = lds(Xb + b.z), x31 = lds(Xb + b.w);
+    if (TWO) {
+      const double2 p0 = rc[0], q0 = rc[1], p1 = rc[2], q1 = rc[3], p2 = rc[4], q2 = rc[5], p3 = rc[6], q3 = rc[7];
+      f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1); s0 = fma(q0.x, x00, s0); s1 = fma(q0.y, x01, s1);
+      f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3); s2 = fma(q1.x, x10, s2); s3 = fma(q1.y, x11, s3);
+      f0 = fma(p2.x, x20, f0); f1 = fma(p2.y, x21, f1); s0 = fma(q2.x, x20, s0); s1 = fma(q2.y, x21, s1);
+      f2 = fma(p3.x, x30, f2); f3 = fma(p3.y, x31, f3); s2 = fma(q3.x, x30, s2); s3 = fma(q3.y, x31, s3);
+    } else {
+      const double2 p0 = rc[0], p1 = rc[1], p2 = rc[2], p3 = rc[3];
+      f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1);
+      f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3);
+      f0 = fma(p2.x, x20, f0); f1 = fma(p2.y, x21, f1);
+      f2 = fma(p3.x, x30, f2); f3 = fma(p3.y, x31, f3);
     }
+  }
+  sf = (f0 + f1) + (f2 + f3);
+  ss = (s0 + s1) + (s2 + s3);
+}
+
+// one piece unit: x_f = (x_f - sum) d_f ; x_s = (x_s - sum - c_sf x_f) d_s
+template <bool DINV>
+__device__ __forceinline__ void unit_solve(const UStage &t, const int4 m, char *Xb) {
+  const int rf = (m.x & 0xffff) * kRowB, rs = (m.x >> 16) * kRowB;
+  const int nch = m.w & 0xffff;
+  const double2 *rc = t.rec + m.y;
+  const int4 *of = t.doff + (m.z >> 2);
+  double sf, ss;
+  const double2 hd = rc[0];
+  if (m.w >> 16) {
+    const double csf = rc[1].x;
+    dep_sums<true>(rc + 2, of, nch, Xb, sf, ss);
+    double xf = lds(Xb + rf) - sf;
+    if (DINV) xf *= hd.x;
+    double xs = fma(-csf, xf, lds(Xb + rs) - ss);
+    if (DINV) xs *= hd.y;
+    *reinterpret_cast<double *>(Xb + rf) = xf;
+    *reinterpret_cast<double *>(Xb + rs) = xs;
   } else {
-    // asynchronous 16 B copies global -> shared (LDGSTS)
-    for (int i = threadIdx.x; i < nr * CH; i += blockDim.x) {
-      const int a = i / CH, ch = i % CH;
-      const double *src = G + (long long)(r0 + a) * h.ld + col0 + 2 * ch;
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(t.X + a * C + 2 * ch);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    dep_sums<false>(rc + 1, of, nch, Xb, sf, ss);
+    double xf = lds(Xb + rf) - sf;
+    if (DINV) xf *= hd.x;
+    *reinterpret_cast<double *>(Xb + rf) = xf;
+  }
+}
+
+template <bool DINV>
+__device__ __forceinline__ void unit_pieces(const UStage &t, char *Xb, int warp) {
+  const int q0 = t.lvl[warp], q1 = t.lvl[warp + 1];
+  int4 m = q0 < q1 ? t.meta[q0] : make_int4(0, 0, 0, 0);
+  for (int u = q0; u < q1; ++u) {
+    const int4 mn = u + 1 < q1 ? t.meta[u + 1] : m;
+    unit_solve<DINV>(t, m, Xb);
+    m = mn;
+  }
+}
+
+// tops: t_T = X_T - (dependencies outside the tops), then X_T = M t_T with M
+// the inverse of the tops' diagonal block (<= kMaxTopUnits units, two per warp).
+constexpr int kBlkThreads = UnitSweep::kWarps * 32;
+constexpr int kTopsLvl = UnitSweep::kWarps + 1;   // lvl[kWarps + 1], lvl[kWarps + 2]: tops units
+static_assert(UnitSweep::kMaxTopUnits <= 2 * UnitSweep::kWarps, "two tops units per warp at most");
+__device__ __forceinline__ void unit_tops(const UStage &t, char *Xb, int warp) {
+  const int u0 = t.lvl[kTopsLvl], u1 = t.lvl[kTopsLvl + 1];
+  if (u0 >= u1) return;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int u = u0 + warp + k * UnitSweep::kWarps;
+    if (u < u1) {
+      const int4 m = t.meta[u];
+      const int rf = (m.x & 0xffff) * kRowB, rs = (m.x >> 16) * kRowB;
+      double sf, ss;
+      if (m.w >> 16) {
+        dep_sums<true>(t.rec + m.y, t.doff + (m.z >> 2), m.w & 0xffff, Xb, sf, ss);
+        *reinterpret_cast<double *>(Xb + rf) = lds(Xb + rf) - sf;
+        *reinterpret_cast<double *>(Xb + rs) = lds(Xb + rs) - ss;
+      } else {
+        dep_sums<false>(t.rec + m.y, t.doff + (m.z >> 2), m.w & 0xffff, Xb, sf, ss);
+        *reinterpret_cast<double *>(Xb + rf) = lds(Xb + rf) - sf;
+      }
     }
   }
-  // separator rows this block depends on (backward sweeps), staged after the block's rows
-  for (int i = threadIdx.x; i < nxr * CH; i += blockDim.x) {
-    const int k = i / CH, ch = i % CH;
-    const double *src = G + (long long)S.ext_rows[x0 + k] * h.ld + col0 + 2 * ch;
-    const unsigned dst = (unsigned)__cvta_generic_to_shared(t.X + (nr + k) * C + 2 * ch);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[1]));
-  seg_sweep<CPL>(t, dinv != nullptr, fwd);
-  if (instr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[2]));
-  for (int i = threadIdx.x; i < nr * CH; i += blockDim.x) {
-    const int a = i / CH, ch = i % CH;
-    *reinterpret_cast<double2 *>(G + (long long)(r0 + a) * h.ld + col0 + 2 * ch) =
-        *reinterpret_cast<const double2 *>(t.X + a * C + 2 * ch);
+  double of_[2], os_[2];
+  int4 mm[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int u = u0 + warp + k * UnitSweep::kWarps;
+    of_[k] = os_[k] = 0.0;
+    mm[k] = make_int4(0, 0, 0, 0);
+    if (u < u1) {
+      mm[k] = t.meta[u];
+      const int4 d = t.tmeta[u - u0];
+      if (d.w >> 16)
+        dep_sums<true>(t.rec + d.y, t.doff + (d.z >> 2), d.w & 0xffff, Xb, of_[k], os_[k]);
+      else
+        dep_sums<false>(t.rec + d.y, t.doff + (d.z >> 2), d.w & 0xffff, Xb, of_[k], os_[k]);
+    }
   }
-  if (instr) {
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk[3]));
-    unsigned smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    long long *d = h.dbg + 6 * (mode * 65536 / 6 / 6 * 0 + blockIdx.y * gridDim.x + blockIdx.x);
-    d[0] = tk[0]; d[1] = tk[1]; d[2] = tk[2]; d[3] = tk[3]; d[4] = smid; d[5] = t.nlev / (blockDim.x >> 5);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (u0 + warp + k * UnitSweep::kWarps < u1) {
+      *reinterpret_cast<double *>(Xb + (mm[k].x & 0xffff) * kRowB) = of_[k];
+      if (mm[k].w >> 16) *reinterpret_cast<double *>(Xb + (mm[k].x >> 16) * kRowB) = os_[k];
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+// right-hand side -G_p W of a block's rows (SpMul fused into the L sweep,
+// PAPER.md:600): warp per G_p row, the row's entries fetched by the lanes at
+// once, lane = column
+__device__ __forceinline__ void tile_rhs_gpw(const SegParams &h, int s, int col0, double *X, int lane, int warp,
+                                             int nw) {
+  const int r0 = h.seg_row_off[s];
+  const int col = col0 + lane;
+  for (int k = h.blk_gp_ptr[s] + warp; k < h.blk_gp_ptr[s + 1]; k += nw) {
+    const int a = h.blk_gp_loc[k];
+    const int row = h.row_global[r0 + a];
+    const int e0 = h.gp_rptr[row], ne = h.gp_rptr[row + 1] - e0;
+    double acc = 0.0;
+    for (int b = 0; b < ne; b += 32) {
+      const int my = b + lane < ne ? h.gp_col[e0 + b + lane] : 0;
+      const double mv = b + lane < ne ? h.gp_val[e0 + b + lane] : 0.0;
+      const int n = min(32, ne - b);
+      for (int j = 0; j < n; ++j) {
+        const int pc = __shfl_sync(0xffffffffu, my, j);
+        const double gv = __shfl_sync(0xffffffffu, mv, j);
+        acc = fma(gv, load_W(h, pc, col), acc);
+      }
+    }
+    X[a * kBC + lane] = -acc;
+  }
+}
+
+// TMA bulk copies (cp.async.bulk) and their mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+// Block sweeps (see above): 2 CTAs of 8 warps per SM, each sweeping one
+// (block, 32-column) tile at a time taken from a global ticket counter
+// (blocks in decreasing cost order); the tile and the block's unit schedule
+// arrive by TMA bulk copies on one mbarrier, the result leaves by bulk stores.
+// While one CTA waits on copies, barriers or a dependency chain, the other
+// CTA's sweep uses the SM.
+__global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ int s_tk;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool fwd = mode == MODE_L || mode == MODE_UT;
+  const DUnit &U = fwd ? h.uf : h.ub;
+  const double2 *vals = mode == MODE_L ? h.uL : mode == MODE_U ? h.uU : mode == MODE_UT ? h.uUt : h.uLt;
+  const bool dinv = mode == MODE_U || mode == MODE_UT;
+  double *G = mode <= MODE_U ? h.Z : h.P;
+  int *ctr = h.blk_ctr + 2 * mode;
+  const int nch = h.ld / kBC;
+  const int ntiles = h.nblk * nch;
+  double *X = reinterpret_cast<double *>(smraw + h.smem_x_off);
+  UStage st;
+  st.meta = reinterpret_cast<const int4 *>(smraw + h.smem_meta_off);
+  st.tmeta = reinterpret_cast<const int4 *>(smraw + h.smem_tmeta_off);
+  st.rec = reinterpret_cast<const double2 *>(smraw + h.smem_rec_off);
+  st.doff = reinterpret_cast<const int4 *>(smraw + h.smem_doff_off);
+  st.lvl = reinterpret_cast<const int *>(smraw + h.smem_lvl_off);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned parity = 0;
+  char *Xb = reinterpret_cast<char *>(X) + lane * 8;
+  for (;;) {
+    if (tid == 0) s_tk = atomicAdd(ctr, 1);
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // my previous stores have read X
+    __syncthreads();
+    const int tk = s_tk;
+    if (tk >= ntiles) break;
+    // timing experiment (RH_DEBUG & 8, MODE_U): per ticket [8 warps' pieces | units << 48, wait, tops, t0, t1]
+    long long *prof = ((h.debug & 8) && h.dbg && mode == MODE_U && tk < 8192) ? h.dbg + (long long)tk * 12 : nullptr;
+    const long long c_a = prof ? clock64() : 0;
+    const int s = U.blk_order[tk / nch], col0 = (tk % nch) * kBC;
+    const int r0 = h.seg_row_off[s], nr = h.seg_row_off[s + 1] - r0;
+    const int x0 = U.ext_off[s], nxr = mode == MODE_L ? 0 : U.ext_off[s + 1] - x0;
+    const int ub = U.unit_off[s], nu = U.unit_off[s + 1] - ub;
+    const int tb = U.tmeta_off[s], ntu = U.tmeta_off[s + 1] - tb;
+    const int rb = U.rec_off[s], nrec = U.rec_off[s + 1] - rb;
+    const int ob = U.doff_off[s], nof = U.doff_off[s + 1] - ob;
+    const int nxrows = mode == MODE_L ? 0 : nr + nxr;
+    if (tid == 0) {
+      const unsigned tx = 16u * (nu + ntu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + (unsigned)kRowB * nxrows;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx)
+                   : "memory");
+      bulk_g2s(smraw + h.smem_meta_off, U.meta + ub, 16u * nu, &mbar);
+      if (ntu) bulk_g2s(smraw + h.smem_tmeta_off, U.tmeta + tb, 16u * ntu, &mbar);
+      bulk_g2s(smraw + h.smem_rec_off, vals + rb, 16u * nrec, &mbar);
+      if (nof) bulk_g2s(smraw + h.smem_doff_off, U.doff + ob, 4u * nof, &mbar);
+      bulk_g2s(smraw + h.smem_lvl_off, U.lvl + s * UnitSweep::kLvl, 4u * UnitSweep::kLvl, &mbar);
+    }
+    for (int a = tid; a < nxrows; a += blockDim.x) {
+      const long long grow = a < nr ? r0 + a : U.ext_rows[x0 + a - nr];
+      bulk_g2s(X + a * kBC, G + grow * h.ld + col0, kRowB, &mbar);
+    }
+    if (mode == MODE_L) {   // right-hand side -G_p W (SpMul fused)
+      for (int i = tid; i < nr * (kBC / 2); i += blockDim.x) reinterpret_cast<double2 *>(X)[i] = make_double2(0.0, 0.0);
+      __syncthreads();
+      tile_rhs_gpw(h, s, col0, X, lane, warp, UnitSweep::kWarps);
+    }
+    {  // wait for the copies of this tile
+      unsigned done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(smem_u32(&mbar)), "r"(parity)
+                     : "memory");
+      parity ^= 1;
+    }
+    __syncthreads();
+    const long long c_b = prof ? clock64() : 0;
+    if (fwd) {
+      if (dinv) unit_pieces<true>(st, Xb, warp); else unit_pieces<false>(st, Xb, warp);
+      __syncthreads();
+      unit_tops(st, Xb, warp);
+    } else {
+      unit_tops(st, Xb, warp);
+      const long long c_c = prof ? clock64() : 0;
+      if (dinv) unit_pieces<true>(st, Xb, warp); else unit_pieces<false>(st, Xb, warp);
+      if (prof && lane == 0) {
+        prof[warp] = (clock64() - c_c) | ((long long)(st.lvl[warp + 1] - st.lvl[warp]) << 48);
+        if (warp == 0) {
+          prof[8] = c_b - c_a;
+          prof[9] = c_c - c_b;
+          prof[10] = c_a;
+        }
+      }
+      __syncthreads();
+      if (prof && tid == 0) prof[11] = clock64();
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // sweep writes -> bulk store reads
+    __syncthreads();
+    for (int a = tid; a < nr; a += blockDim.x) bulk_s2g(G + (long long)(r0 + a) * h.ld + col0, X + a * kBC, kRowB);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  // the last CTA out resets the ticket counter for the next launch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -1194,7 +1240,8 @@ T *dalloc(size_t n, std::vector<void *> &pool) {
   return p;
 }
 
-constexpr int kSmemMax = 220 * 1024;
+constexpr int kSmemMax = 227 * 1024;   // sm_100 opt-in maximum of dynamic shared memory per block
+constexpr int kSmemSM = 228 * 1024;    // shared memory per SM
 
 }  // namespace
 
@@ -1225,7 +1272,7 @@ struct rh_ctx {
   int *seg_row_off, *row_global;
   DSeg dfwd, dbwd;
   int *fwd_src_a, *fwd_src_b, *bwd_src_a, *bwd_src_b, *fwd_dsrc, *bwd_dsrc;
-  double *vL, *vUt, *vU, *vLt, *dinv_fwd, *dinv_bwd;
+  double *vL, *vUt;   // separator rows' L / U^T entries (k_sep_gather)
   int nnz_fwd = 0, nnz_bwd = 0;
   // refactorization schedule
   int *blk_fo_off, *fo, *ks_ptr, *ks4, *ks_k;
@@ -1234,8 +1281,7 @@ struct rh_ctx {
   double *gj_dinv;
   double *dinv_rows, *rowmax;
   double *Sinv = nullptr, *SinvT = nullptr;
-  size_t smem_fact_blk = 0, smem_fact_sep = 0, smem_seg_blk = 0, smem_seg_blk1 = 0;
-  int cpl = 2;   // columns per lane of the HVP block kernels (32 * cpl columns per CTA)
+  size_t smem_fact_blk = 0, smem_fact_sep = 0;
   // state
   double *x, *p, *th, *v, *pgb, *P, *Q, *g, *refg_th, *refg_v, *scal;
   double2 *cs;
@@ -1249,6 +1295,16 @@ struct rh_ctx {
   int *blk_gp_ptr, *blk_gp_loc;
   int *fact_seg_lvl, *fact_lvl_ptr, *fact_order;
   int *top_ptr, *top_fpos_ptr, *top_fpos, *top_fwd_base, *top_bwd_base;
+  // bus-unit block sweeps
+  DUnit duf{}, dub{};
+  double2 *uL = nullptr, *uUt = nullptr, *uU = nullptr, *uLt = nullptr;
+  int nrec_f = 0, nrec_b = 0;
+  int *uf_src_a, *uf_src_b, *ub_src_a, *ub_src_b, *uf_top_pos, *ub_top_pos;
+  int maxrx = 0, nsm = 148;
+  int smem_x_off = 0, smem_meta_off = 0, smem_tmeta_off = 0, smem_rec_off = 0, smem_doff_off = 0, smem_lvl_off = 0;
+  int smem_stride = 0;
+  int *blk_ctr = nullptr;
+  size_t smem_blk = 0;
 
   void free_all() {
     for (void *q : pool) cudaFree(q);
@@ -1290,18 +1346,33 @@ size_t fact_smem_bytes(const Analysis &A) {
   return (size_t)(A.max_blk_fnnz + A.rmax + 2) * 8 + (size_t)A.max_blk_ks * 20 + (size_t)A.max_blk_tgt * 2 + 64;
 }
 
-size_t seg_smem_max(const Analysis &A, int C) {
-  size_t m = 0;
-  for (const SegSweep *S : {&A.fwd, &A.bwd}) {
-    for (int s = 0; s < A.nblk; ++s) {
-      const int l0 = S->seg_lvl[s], l1 = S->seg_lvl[s + 1];
-      const int qb = A.seg_row_off[s], qe = A.seg_row_off[s + 1];
-      const int ne = S->rptr[qe] - S->rptr[qb];
-      const int nrx = A.seg_row_off[s + 1] - A.seg_row_off[s] + S->ext_off[s + 1] - S->ext_off[s];
-      m = std::max(m, seg_smem_bytes(nrx, qe - qb, ne, l1 - l0 - 1, C));
-    }
-  }
-  return m;
+size_t blk_smem_layout(const Analysis &A, int *off7);
+bool blk_smem_fits(const Analysis &A, size_t lim) {
+  int o[7];
+  return 2 * (blk_smem_layout(A, o) + 1024) <= lim;   // two CTAs per SM, + static shared memory
+}
+
+
+// shared-memory carve-up of k_blk (2 CTAs per SM): the X tile, then one
+// block's unit schedule.  Returns the total bytes.
+size_t blk_smem_layout(const Analysis &A, int *off7) {
+  auto al = [](size_t x) { return (x + 127) & ~(size_t)127; };
+  const int maxrx = std::max(A.ufwd.max_rows, A.ubwd.max_rows);
+  size_t off = 0;
+  off7[0] = (int)off;
+  off += al((size_t)maxrx * kBC * 8);
+  off7[1] = (int)off;
+  off += al((size_t)std::max(A.ufwd.max_units, A.ubwd.max_units) * 16);
+  off7[2] = (int)off;
+  off += al((size_t)std::max(A.ufwd.max_tunits, A.ubwd.max_tunits) * 16);
+  off7[3] = (int)off;
+  off += al((size_t)std::max(A.ufwd.max_rec, A.ubwd.max_rec) * 16);
+  off7[4] = (int)off;
+  off += al((size_t)std::max(A.ufwd.max_doff, A.ubwd.max_doff) * 4);
+  off7[5] = (int)off;
+  off += al(UnitSweep::kLvl * 4);
+  off7[6] = (int)off;
+  return off;
 }
 
 int upload(rh_ctx *c) {
@@ -1371,6 +1442,51 @@ int upload(rh_ctx *c) {
   };
   mkseg(c->dfwd, A.fwd);
   mkseg(c->dbwd, A.bwd);
+  auto mkunit = [&](DUnit &D, const UnitSweep &U, const DSeg &S) {
+    D.meta = reinterpret_cast<const int4 *>(dalloc_copy(U.meta, P));
+    D.tmeta = reinterpret_cast<const int4 *>(dalloc_copy(U.tmeta, P));
+    chk(D.meta);
+    chk(D.tmeta);
+    chk(D.unit_off = dalloc_copy(U.unit_off, P));
+    chk(D.tmeta_off = dalloc_copy(U.tmeta_off, P));
+    chk(D.lvl = dalloc_copy(U.lvl, P));
+    chk(D.rec_off = dalloc_copy(U.rec_off, P));
+    chk(D.doff_off = dalloc_copy(U.doff_off, P));
+    chk(D.doff = dalloc_copy(U.doff, P));
+    std::vector<int32_t> ord(A.nblk);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return U.cost[x] > U.cost[y]; });
+    chk(D.blk_order = dalloc_copy(ord, P));
+    D.ext_off = S.ext_off;
+    D.ext_rows = S.ext_rows;
+  };
+  mkunit(c->duf, A.ufwd, c->dfwd);
+  mkunit(c->dub, A.ubwd, c->dbwd);
+  c->nrec_f = (int)A.ufwd.src_a.size() / 2;
+  c->nrec_b = (int)A.ubwd.src_a.size() / 2;
+  chk(c->uf_src_a = dalloc_copy(A.ufwd.src_a, P));
+  chk(c->uf_src_b = dalloc_copy(A.ufwd.src_b, P));
+  chk(c->ub_src_a = dalloc_copy(A.ubwd.src_a, P));
+  chk(c->ub_src_b = dalloc_copy(A.ubwd.src_b, P));
+  chk(c->uf_top_pos = dalloc_copy(A.ufwd.top_pos, P));
+  chk(c->ub_top_pos = dalloc_copy(A.ubwd.top_pos, P));
+  chk(c->blk_ctr = dalloc<int>(16, P));
+  chk(c->uL = dalloc<double2>(c->nrec_f, P));
+  chk(c->uUt = dalloc<double2>(c->nrec_f, P));
+  chk(c->uU = dalloc<double2>(c->nrec_b, P));
+  chk(c->uLt = dalloc<double2>(c->nrec_b, P));
+  {
+    int o[7];
+    c->maxrx = std::max(A.ufwd.max_rows, A.ubwd.max_rows);
+    c->smem_blk = blk_smem_layout(A, o);
+    c->smem_stride = o[6];
+    c->smem_x_off = o[0];
+    c->smem_meta_off = o[1];
+    c->smem_tmeta_off = o[2];
+    c->smem_rec_off = o[3];
+    c->smem_doff_off = o[4];
+    c->smem_lvl_off = o[5];
+  }
   c->nnz_fwd = (int)A.fwd.dep.size();
   c->nnz_bwd = (int)A.bwd.dep.size();
   std::vector<int32_t> odth(2 * A.n_line), odv(2 * A.n_line);
@@ -1388,10 +1504,6 @@ int upload(rh_ctx *c) {
   chk(c->gpc_val = dalloc<double>(A.gp_col.size(), P));
   chk(c->vL = dalloc<double>(c->nnz_fwd, P));
   chk(c->vUt = dalloc<double>(c->nnz_fwd, P));
-  chk(c->vU = dalloc<double>(c->nnz_bwd, P));
-  chk(c->vLt = dalloc<double>(c->nnz_bwd, P));
-  chk(c->dinv_fwd = dalloc<double>(nx, P));
-  chk(c->dinv_bwd = dalloc<double>(nx, P));
   chk(c->dinv_rows = dalloc<double>(nx, P));
   chk(c->rowmax = dalloc<double>(nx, P));
   chk(c->x = dalloc<double>(nx, P));
@@ -1419,14 +1531,22 @@ int upload(rh_ctx *c) {
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
   // shared-memory footprints
   c->smem_fact_blk = fact_smem_bytes(A);
-  c->smem_seg_blk = seg_smem_max(A, 32 * c->cpl);
-  c->smem_seg_blk1 = seg_smem_max(A, kSegC);
-  cudaFuncSetAttribute(k_fact_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  cudaFuncSetAttribute(k_seg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  cudaFuncSetAttribute(k_tops_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  cudaFuncSetAttribute(k_seg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
-  cudaFuncSetAttribute(k_seg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+  {  // opt-in dynamic shared memory: the device maximum minus each kernel's static shared memory
+    int optin = kSmemMax;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    auto allow = [&](const void *fn) {
+      cudaFuncAttributes fa;
+      if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+    };
+    allow((const void *)k_fact_blocks);
+    allow((const void *)k_tops_inverse);
+    allow((const void *)k_blk);
+    cudaGetLastError();
+  }
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
   cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 16 * sizeof(int));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(c, RH_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
   return RH_OK;
@@ -1476,10 +1596,6 @@ SegParams make_params(rh_ctx *c) {
   h.bwd = c->dbwd;
   h.vL = c->vL;
   h.vUt = c->vUt;
-  h.vU = c->vU;
-  h.vLt = c->vLt;
-  h.dinv_fwd = c->dinv_fwd;
-  h.dinv_bwd = c->dinv_bwd;
   h.Z = c->Zb;
   h.P = c->Pb;
   h.gp_rptr = c->gp_rptr;
@@ -1519,6 +1635,21 @@ SegParams make_params(rh_ctx *c) {
     h.dbg = dbg;
   }
   h.SinvT = c->SinvT;
+  h.uf = c->duf;
+  h.ub = c->dub;
+  h.uL = c->uL;
+  h.uUt = c->uUt;
+  h.uU = c->uU;
+  h.uLt = c->uLt;
+  h.maxrx = c->maxrx;
+  h.smem_stride = c->smem_stride;
+  h.blk_ctr = c->blk_ctr;
+  h.smem_x_off = c->smem_x_off;
+  h.smem_meta_off = c->smem_meta_off;
+  h.smem_tmeta_off = c->smem_tmeta_off;
+  h.smem_rec_off = c->smem_rec_off;
+  h.smem_doff_off = c->smem_doff_off;
+  h.smem_lvl_off = c->smem_lvl_off;
   return h;
 }
 
@@ -1546,14 +1677,6 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
   return RH_OK;
 }
 
-void launch_seg(int cpl, dim3 g, size_t smem, cudaStream_t st, const SegParams &h, int mode) {
-  if (cpl >= 4)
-    k_seg<4><<<g, kSegThreads, smem, st>>>(h, mode);
-  else if (cpl >= 2)
-    k_seg<2><<<g, kSegThreads, smem, st>>>(h, mode);
-  else
-    k_seg<1><<<g, kSegThreads, smem, st>>>(h, mode);
-}
 
 // one Alg. 2 batch: eight stream-ordered kernels, no host
 // synchronization (cf. the two explicit syncs of PAPER.md:798-805).
@@ -1563,8 +1686,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
              double *Psio = nullptr, long long ldz = 0) {
   if (N <= 0) return RH_OK;
   const Analysis &A = c->A;
-  const int C = 32 * c->cpl;
-  const int ld = (N + C - 1) / C * C;
+  const int ld = (N + kBC - 1) / kBC * kBC;
   int rc = ensure_ws(c, ld);
   if (rc) return rc;
   SegParams h = make_params(c);
@@ -1578,7 +1700,8 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   h.transposed = transposed;
   const int nb = A.nblk;
   const bool has_sep = A.sep_rows > 0;
-  const dim3 gA(nb, ld / C), gSg(nblk(A.sep_rows, kThreads / 32), ld / 32),
+  const int gA = (int)std::min<long long>(2LL * c->nsm, (long long)nb * (ld / kBC));
+  const dim3 gSg(nblk(A.sep_rows, kThreads / 32), ld / 32),
       gSm((ld + GBN - 1) / GBN, (A.sep_rows + GBM - 1) / GBM);
   const int nch32 = ld / 32, fch = (nch32 + FCH - 1) / FCH;
   const dim3 gF(nblk(A.n_bus, kThreads / 32), fch), gM(nblk(A.n_p, kThreads / 32), fch);
@@ -1591,7 +1714,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     if (c->timing) cudaEventRecord(ev[i], st);
   };
   mark(0);
-  launch_seg(c->cpl, gA, c->smem_seg_blk, st, h, MODE_L);
+  k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_L);
   RH_LAUNCHED(c);
   mark(1);
   if (has_sep) {
@@ -1601,20 +1724,14 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     RH_LAUNCHED(c);
   }
   mark(2);
-  launch_seg(c->cpl, (h.debug & 32) ? dim3(h.debug >> 8, 1) : gA, c->smem_seg_blk, st, h, MODE_U);
+  k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
   RH_LAUNCHED(c);
-  if ((h.debug & 8) && h.dbg) {  // timing experiment: dump per-CTA timestamps of this launch
-    std::vector<long long> hb((size_t)6 * ((h.debug & 32) ? (h.debug >> 8) : gA.x * gA.y));
+  if ((h.debug & 8) && h.dbg) {  // timing experiment: per-tile cycles of this launch (tools/kblk_prof.py)
+    std::vector<long long> hb((size_t)12 * std::min(8192, nb * (ld / kBC)));
     cudaMemcpyAsync(hb.data(), h.dbg, hb.size() * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    if (FILE *fp = fopen("gpurun_out/kseg_timing.bin", "wb")) {
+    if (FILE *fp = fopen("gpurun_out/kblk_prof.bin", "wb")) {
       fwrite(hb.data(), 8, hb.size(), fp);
-      fclose(fp);
-    }
-    std::vector<long long> hp((size_t)20 * (hb.size() / 6));
-    cudaMemcpy(hp.data(), h.dbg + 6 * 65536, hp.size() * 8, cudaMemcpyDeviceToHost);
-    if (FILE *fp = fopen("gpurun_out/kseg_phases.bin", "wb")) {
-      fwrite(hp.data(), 8, hp.size(), fp);
       fclose(fp);
     }
   }
@@ -1630,7 +1747,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     RH_LAUNCHED(c);
   }
   mark(4);
-  launch_seg(c->cpl, gA, c->smem_seg_blk, st, h, MODE_UT);
+  k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_UT);
   RH_LAUNCHED(c);
   mark(5);
   if (has_sep) {
@@ -1640,7 +1757,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     RH_LAUNCHED(c);
   }
   mark(6);
-  launch_seg(c->cpl, gA, c->smem_seg_blk, st, h, MODE_LT);
+  k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_LT);
   RH_LAUNCHED(c);
   if (Psio) {
     k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, c->Pb, 1.0, Psio, ldz);
@@ -1715,8 +1832,6 @@ int rh_load_grid(rh_ctx *c, const rh_grid *g, int32_t *n_x, int32_t *n_p) {
   // block size: the largest whose shared-memory stages fit
   std::string msg;
   bool fits = false;
-  c->cpl = 2;
-  if (const char *env = getenv("RH_CPL")) c->cpl = atoi(env) >= 4 ? 4 : atoi(env) >= 2 ? 2 : 1;  // tuning override
   std::vector<int> cands = {256, 128, 512, 64};
   if (const char *env = getenv("RH_RMAX")) cands.insert(cands.begin(), atoi(env));  // tuning override
   for (int rmax : cands) {
@@ -1725,9 +1840,9 @@ int rh_load_grid(rh_ctx *c, const rh_grid *g, int32_t *n_x, int32_t *n_p) {
     const Analysis &A = c->A;
     const size_t lim = (size_t)kSmemMax;
     fits =
-           (size_t)8 * A.sep_rows * sizeof(double) <= lim && seg_smem_max(A, 32 * c->cpl) <= lim &&
-           seg_smem_max(A, kSegC) <= lim &&
-           fact_smem_bytes(A) <= lim;
+           (size_t)8 * A.sep_rows * sizeof(double) <= lim &&
+           fact_smem_bytes(A) <= lim && blk_smem_fits(A, kSmemSM) &&
+           A.ufwd.max_tunits <= UnitSweep::kMaxTopUnits && A.ubwd.max_tunits <= UnitSweep::kMaxTopUnits;
     if (fits) break;
   }
   if (!fits) return fail(c, RH_E_GRID, "grid too large for the shared-memory segment kernels");
@@ -1902,30 +2017,37 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
     k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
     RH_LAUNCHED(c);
   }
-  struct G {
-    int n;
-    const int *src;
-    double *dst;
-    bool inv;
-  } gs[] = {{c->nnz_fwd, c->fwd_src_a, c->vL, false}, {c->nnz_fwd, c->fwd_src_b, c->vUt, false},
-            {c->nnz_bwd, c->bwd_src_a, c->vU, false},  {c->nnz_bwd, c->bwd_src_b, c->vLt, false},
-            {nx, c->fwd_dsrc, c->dinv_fwd, true},      {nx, c->bwd_dsrc, c->dinv_bwd, true}};
-  for (const G &q : gs) {
-    if (q.n <= 0) continue;
-    if (q.inv)
-      k_gather_inv<<<nblk(q.n), kThreads, 0, st>>>(q.n, q.src, c->F_val, q.dst);
-    else
-      k_gather_vals<<<nblk(q.n), kThreads, 0, st>>>(q.n, q.src, c->F_val, q.dst);
-    RH_LAUNCHED(c);
+  {  // separator rows' entries of the forward pattern (k_sep_gather): L and U^T values
+    const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
+    const int e0 = A.fwd.rptr[qb], ne = A.fwd.rptr[qe] - e0;
+    if (ne > 0) {
+      k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_a + e0, c->F_val, c->vL + e0);
+      RH_LAUNCHED(c);
+      k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_b + e0, c->F_val, c->vUt + e0);
+      RH_LAUNCHED(c);
+    }
   }
   const int ngp = (int)A.gp_col.size();
   if (ngp > 0) {
     k_gather_vals<<<nblk(ngp), kThreads, 0, st>>>(ngp, c->gpc_pos, c->gp_val, c->gpc_val);
     RH_LAUNCHED(c);
   }
+  struct GU {
+    int n;
+    const int *src;
+    double2 *dst;
+  } gu[] = {{c->nrec_f, c->uf_src_a, c->uL}, {c->nrec_f, c->uf_src_b, c->uUt},
+            {c->nrec_b, c->ub_src_a, c->uU}, {c->nrec_b, c->ub_src_b, c->uLt}};
+  for (const GU &q : gu) {
+    if (q.n <= 0) continue;
+    k_gather_code<<<nblk(2LL * q.n), kThreads, 0, st>>>(2 * q.n, q.src, c->F_val, reinterpret_cast<double *>(q.dst));
+    RH_LAUNCHED(c);
+  }
   if (A.max_tops > 0) {
-    k_tops_inverse<<<A.nblk, kMaxTops, 3 * kMaxTops * (kMaxTops + 1) * sizeof(double), st>>>(c->top_ptr, c->top_fpos_ptr, c->top_fpos, c->top_fwd_base,
-                                                c->top_bwd_base, c->F_val, c->vL, c->vUt, c->vU, c->vLt);
+    k_tops_inverse<<<A.nblk, kMaxTops, 3 * kMaxTops * (kMaxTops + 1) * sizeof(double), st>>>(
+        c->top_ptr, c->top_fpos_ptr, c->top_fpos, c->uf_top_pos, c->ub_top_pos, c->F_val,
+        reinterpret_cast<double *>(c->uL), reinterpret_cast<double *>(c->uUt), reinterpret_cast<double *>(c->uU),
+        reinterpret_cast<double *>(c->uLt));
     RH_LAUNCHED(c);
   }
   int status = 0;
@@ -1965,7 +2087,8 @@ int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *str
   h.N = 1;
   h.ld = kSegC;   // column 0 carries the right-hand side, columns 1..31 stay zero
   h.P = c->X1col;
-  k_seg<1><<<dim3(A.nblk, 1), kSegThreads, c->smem_seg_blk1, st>>>(h, MODE_UT);
+  const int g1 = std::min(2 * c->nsm, A.nblk);
+  k_blk<<<g1, kBlkThreads, c->smem_blk, st>>>(h, MODE_UT);
   RH_LAUNCHED(c);
   if (A.sep_rows > 0) {
     k_sep_gather<<<dim3(nblk(A.sep_rows, kThreads / 32), 1), kThreads, 0, st>>>(h, MODE_UTLT);
@@ -1973,7 +2096,7 @@ int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *str
     k_sep_gemm<<<dim3(1, (A.sep_rows + GBM - 1) / GBM), GTHREADS, 0, st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
   }
-  k_seg<1><<<dim3(A.nblk, 1), kSegThreads, c->smem_seg_blk1, st>>>(h, MODE_LT);
+  k_blk<<<g1, kBlkThreads, c->smem_blk, st>>>(h, MODE_LT);
   RH_LAUNCHED(c);
   k_grad_out<<<nblk(std::max(A.n_x, A.n_p)), kThreads, 0, st>>>(
       A.n_x, A.n_p, c->pinv, c->p_bus, c->p_kind, c->c2b, c->c1b, c->p, c->refg_v, c->scal, c->gpc_ptr, c->gpc_row,

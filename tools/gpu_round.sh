@@ -12,7 +12,7 @@ timeout 900 python bench.py "$@" > $OUT/bench.json 2> $OUT/bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline "$@" > $OUT/ncu_launch_bench.log 2>&1
 python tools/launch_summary.py $OUT/launches.csv > $OUT/launch_summary.txt 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_seg|k_for|k_sep_gemm|k_sep_gather|k_muladd' -s 10 -c 8 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_blk|k_for|k_sep_gemm|k_sep_gather|k_muladd" -s 10 -c 8 \
     -o $OUT/prof_hvp python tools/prof_hvp.py case9241pegase 1024 3 > $OUT/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_fact_blocks|k_gj_update|k_gj_panel' -c 4 \
     -o $OUT/prof_fact python tools/prof_hvp.py case9241pegase 64 1 > $OUT/ncu_full_fact.log 2>&1
