@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreads) k_fact_sep_rows(FactParams f) {
 // place by blocked Gauss-Jordan elimination with static (diagonal) pivots, the
 // same pivots the up-looking factorization would use (R15): the
 // separator's ~100-level triangular chains then become one dense product per
-// batch (k_sep_gemm).  Panel width GJB; per panel three launches.
+// batch (k_sep_gemm).  Panel width GJB; one persistent launch (k_sep_inverse).
 // ----------------------------------------------------------------------------
 constexpr int GJB = 32;
 
@@ -326,162 +326,191 @@ __global__ void k_sep_dense(int nslots, const int *__restrict__ src, const int *
   if (t < nslots) S[dpos[t]] = F[src[t]];
 }
 
-// Gauss-Jordan inverse of the b x b (b <= 32) diagonal block of panel K by one
-// warp: lane j holds column j of D in registers (compile-time row index), the
-// pivot column moves by shuffles; the pivot loop stays rolled (small code).
-// Static pivots, checked against the separator row's original max.
-__device__ __forceinline__ void gj_diag_warp(const double *S, int ns, int K, double *Dinv, const double *rowmax,
-                                             const int *sep_rows, int *status, double pivtol) {
-  const int j = threadIdx.x & 31;
-  const int b = min(GJB, ns - K);
-  double d[GJB];
-#pragma unroll
-  for (int i = 0; i < GJB; ++i) d[i] = (i < b && j < b) ? S[(long long)(K + i) * ns + K + j] : (i == j ? 1.0 : 0.0);
-  const double rm = j < b ? rowmax[sep_rows[K + j]] : 0.0;   // pivot threshold of row K + j
-  bool bad = false;
-#pragma unroll 1
-  for (int k = 0; k < GJB; ++k) {
-    double dk = 0.0;  // D[k][j]
-#pragma unroll
-    for (int i = 0; i < GJB; ++i)
-      if (i == k) dk = d[i];
-    const double piv = __shfl_sync(0xffffffffu, dk, k);
-    const double inv = 1.0 / piv;
-    if (j == k && k < b && !(fabs(piv) > pivtol * rm)) bad = true;
-    const double rk = j == k ? inv : dk * inv;  // new pivot row, column j
-#pragma unroll
-    for (int i = 0; i < GJB; ++i) {
-      const double f = __shfl_sync(0xffffffffu, d[i], k);  // D[i][k]
-      d[i] = i == k ? rk : (j == k ? -f * inv : fma(-f, rk, d[i]));
+// Grid-wide barrier of a cooperative launch (all CTAs co-resident): arrival
+// counter + generation word; the last arrival resets the counter and bumps the
+// generation.  `gen` is the generation this CTA waits to leave.
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(&bar[1], 1u);
+    } else {
+      while ((unsigned)ld_acquire(reinterpret_cast<const int *>(&bar[1])) == gen) {
+      }
     }
+    __threadfence();
   }
-  if (bad) atomicMax(status, sep_rows[K + j] + 1);
-#pragma unroll
-  for (int i = 0; i < GJB; ++i) Dinv[i * GJB + j] = d[i];
+  ++gen;
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(32) k_gj_diag(const double *S, int ns, int K, double *Dinv, const double *rowmax,
-                                                const int *sep_rows, int *status, double pivtol) {
-  gj_diag_warp(S, ns, K, Dinv, rowmax, sep_rows, status, pivtol);
-}
-
-// E -= C * (Dinv * Rp) for every element outside the panel rows / columns.
-// Every CTA inverts the diagonal block itself (warp 0, registers); CTA (0,0)
-// publishes Dinv for k_gj_panel.  64 x 64 tile, 4 x 4 outputs per thread.
-__global__ void __launch_bounds__(256) k_gj_update(double *S, int ns, int K, const double *__restrict__ Dinv) {
-  __shared__ double Ds[GJB][GJB + 1];
-  __shared__ double Cs[GJB][64 + 1];    // C^T: Cs[k][r] = S[i0 + r][K + k]
-  __shared__ double Ps[GJB][64 + 1];    // panel rows: Ps[k][c] = S[K + k][j0 + c], then R = Dinv * Ps
-  const int b = min(GJB, ns - K);
-  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+// Blocked Gauss-Jordan inverse of the dense separator block S in ONE
+// persistent cooperative launch (replaces 2 launches per panel).  Per panel K
+// (width GJB) every CTA inverts the panel's diagonal block D itself (warp 0,
+// registers; static pivots checked against the row's original max) while its
+// other warps stage C = S[tile rows, K], P = S[K, tile cols] and T = S[tile];
+// then, for its 64 x 64 output tiles, R = D^-1 P (D^-1 on panel columns, with
+// T := 0 there) and
+//   S'[panel rows] = R,   S'[other rows] = T - C R
+// which is the block GJ step [D B; C E] -> [D^-1, D^-1 B; -C D^-1, E - C D^-1 B].
+// S' is written to the other buffer (ping-pong), one grid barrier per panel.
+constexpr int GJT = 64;   // output tile
+constexpr size_t gj_smem_bytes() { return sizeof(double) * (GJB * (GJB + 1) + (2 * GJB + GJT) * (GJT + 1)); }
+__global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int ns, const double *rowmax,
+                                                     const int *sep_rows, int *status, double pivtol,
+                                                     unsigned *bar) {
+  extern __shared__ double gj_sm[];   // dynamic: gj_smem_bytes()
+  double(*Ds)[GJB + 1] = reinterpret_cast<double(*)[GJB + 1]>(gj_sm);
+  double(*Cs)[GJT + 1] = reinterpret_cast<double(*)[GJT + 1]>(gj_sm + GJB * (GJB + 1));   // C^T: Cs[m][r] = S[i0 + r][K + m]
+  double(*Rs)[GJT + 1] = Cs + GJB;                                                     // P, then R
+  double(*Ts)[GJT + 1] = Rs + GJB;
+  __shared__ unsigned s_gen;
   const int tid = threadIdx.x;
-  for (int t = tid; t < GJB * GJB; t += 256) Ds[t / GJB][t % GJB] = Dinv[t];
-  for (int t = tid; t < 64 * GJB; t += 256) {
-    const int r = t / GJB, k = t % GJB;  // coalesced over k within a row
-    const int gi = i0 + r;
-    Cs[k][r] = (gi < ns && k < b) ? S[(long long)gi * ns + K + k] : 0.0;
-    const int k2 = t / 64, c = t % 64;   // coalesced over c
-    const int gj = j0 + c;
-    Ps[k2][c] = (k2 < b && gj < ns) ? S[(long long)(K + k2) * ns + gj] : 0.0;
-  }
+  const int nt = (ns + GJT - 1) / GJT, ntiles = nt * nt;
+  if (tid == 0) s_gen = (unsigned)ld_acquire(reinterpret_cast<const int *>(&bar[1]));
   __syncthreads();
-  double rr[GJB * 64 / 256];
+  unsigned gen = s_gen;
+  double *Sin = Sa, *Sout = Sb;
+  __shared__ double prow[2][GJB];
+  const int warp = tid >> 5, lane = tid & 31;
+  // stage C^T, P and T (T := 0 on the panel columns) of one output tile; `t0`,
+  // `nthr`: the participating threads.  Batches of 16 loads in flight per thread.
+  auto load_tile = [&](const double *Sin, int K, int b, int i0, int j0, int t0, int nthr) {
+    constexpr int NB = 16;
+    for (int base = t0; base < GJT * GJB; base += NB * nthr) {
+      double va[NB], vb[NB];
 #pragma unroll
-  for (int u = 0; u < GJB * 64 / 256; ++u) {
-    const int t = tid + u * 256;
-    const int k = t / 64, c = t % 64;
-    double acc = 0.0;
+      for (int q = 0; q < NB; ++q) {
+        const int t = base + q * nthr;
+        const int r = t / GJB, m = t % GJB, m2 = t / GJT, c = t % GJT;
+        va[q] = (t < GJT * GJB && i0 + r < ns && m < b) ? __ldcg(Sin + (long long)(i0 + r) * ns + K + m) : 0.0;
+        vb[q] = (t < GJT * GJB && m2 < b && j0 + c < ns) ? __ldcg(Sin + (long long)(K + m2) * ns + j0 + c) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int t = base + q * nthr;
+        if (t < GJT * GJB) {
+          Cs[t % GJB][t / GJB] = va[q];
+          Rs[t / GJT][t % GJT] = vb[q];
+        }
+      }
+    }
+    for (int base = t0; base < GJT * GJT; base += NB * nthr) {
+      double vt[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int t = base + q * nthr, r = t / GJT, c = t % GJT;
+        const bool inJ = j0 + c >= K && j0 + c < K + b;
+        vt[q] = (t < GJT * GJT && i0 + r < ns && j0 + c < ns && !inJ) ? __ldcg(Sin + (long long)(i0 + r) * ns + j0 + c) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int t = base + q * nthr;
+        if (t < GJT * GJT) Ts[t / GJT][t % GJT] = vt[q];
+      }
+    }
+  };
+  for (int K = 0; K < ns; K += GJB) {
+    const int b = min(GJB, ns - K);
+    if (warp < 4) {
+      // D^-1 -> Ds (every CTA, redundantly) by 4 warps: thread = (rows 8w..8w+7, column lane);
+      // the pivot row goes through shared memory, the pivot column by shuffles
+      const int j = lane;
+      double v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int i = 8 * warp + r;
+        v[r] = (i < b && j < b) ? __ldcg(Sin + (long long)(K + i) * ns + K + j) : (i == j ? 1.0 : 0.0);
+      }
+      bool bad = false;
+#pragma unroll
+      for (int k = 0; k < GJB; ++k) {
+        const int wk = k >> 3, kk = k & 7;
+        if (warp == wk) prow[k & 1][j] = v[kk];
+        double f[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) f[r] = __shfl_sync(0xffffffffu, v[r], k);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        const double pk = prow[k & 1][k];
+        const double inv = 1.0 / pk;
+        const double rk = j == k ? inv : prow[k & 1][j] * inv;
+        if (warp == wk && j == k && k < b && !(fabs(pk) > pivtol * rowmax[sep_rows[K + k]])) bad = true;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int i = 8 * warp + r;
+          v[r] = i == k ? rk : (j == k ? -f[r] * inv : fma(-f[r], rk, v[r]));
+        }
+      }
+      if (bad && blockIdx.x == 0) atomicMax(status, sep_rows[K + j] + 1);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) Ds[8 * warp + r][j] = v[r];
+    } else if (blockIdx.x < ntiles) {
+      const int tile = blockIdx.x;
+      load_tile(Sin, K, b, (tile / nt) * GJT, (tile % nt) * GJT, tid - 128, 128);
+    }
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int i0 = (tile / nt) * GJT, j0 = (tile % nt) * GJT;
+      if (tile != (int)blockIdx.x) load_tile(Sin, K, b, i0, j0, tid, blockDim.x);
+      __syncthreads();   // Ds (first tile), Cs, Rs = P, Ts
+      double rr[GJB * GJT / 256];
+#pragma unroll
+      for (int u = 0; u < GJB * GJT / 256; ++u) {
+        const int t = tid + u * 256, m = t / GJT, c = t % GJT;
+        const int gj = j0 + c;
+        double acc = 0.0;
+        if (gj >= K && gj < K + b) {
+          acc = Ds[m][gj - K];
+        } else {
 #pragma unroll 8
-    for (int m = 0; m < GJB; ++m) acc = fma(Ds[k][m], Ps[m][c], acc);
-    rr[u] = acc;
-  }
-  __syncthreads();
+          for (int l = 0; l < GJB; ++l) acc = fma(Ds[m][l], Rs[l][c], acc);
+        }
+        rr[u] = acc;
+      }
+      __syncthreads();
 #pragma unroll
-  for (int u = 0; u < GJB * 64 / 256; ++u) {
-    const int t = tid + u * 256;
-    Ps[t / 64][t % 64] = rr[u];
-  }
-  __syncthreads();
-  const int tx = tid % 16, ty = tid / 16;
-  double acc[4][4];
+      for (int u = 0; u < GJB * GJT / 256; ++u) {
+        const int t = tid + u * 256;
+        Rs[t / GJT][t % GJT] = rr[u];
+      }
+      __syncthreads();
+      const int tx = tid % 16, ty = tid / 16;
+      double acc[4][4];
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+        for (int v = 0; v < 4; ++v) acc[u][v] = Ts[ty + 16 * u][tx + 16 * v];
 #pragma unroll 4
-  for (int k = 0; k < GJB; ++k) {
-    double cv[4], rv[4];
+      for (int m = 0; m < GJB; ++m) {
+        double cv[4], rv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) cv[u] = Cs[k][ty + 16 * u];
+        for (int u = 0; u < 4; ++u) cv[u] = Cs[m][ty + 16 * u];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) rv[v] = Ps[k][tx + 16 * v];
+        for (int v = 0; v < 4; ++v) rv[v] = Rs[m][tx + 16 * v];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = fma(cv[u], rv[v], acc[u][v]);
-  }
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(-cv[u], rv[v], acc[u][v]);
+      }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int gi = i0 + ty + 16 * u;
-    if (gi >= ns || (gi >= K && gi < K + b)) continue;
+      for (int u = 0; u < 4; ++u) {
+        const int gi = i0 + ty + 16 * u;
+        if (gi >= ns) continue;
+        const bool inI = gi >= K && gi < K + b;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int gj = j0 + tx + 16 * v;
-      if (gj >= ns || (gj >= K && gj < K + b)) continue;
-      S[(long long)gi * ns + gj] -= acc[u][v];
+        for (int v = 0; v < 4; ++v) {
+          const int gj = j0 + tx + 16 * v;
+          if (gj < ns) __stcg(Sout + (long long)gi * ns + gj, inI ? Rs[gi - K][tx + 16 * v] : acc[u][v]);
+        }
+      }
+      __syncthreads();
     }
-  }
-}
-
-// panel rows S[K, t] = Dinv * S[K, t] and panel columns S[t, K] = -S[t, K] * Dinv
-// for a 32-wide tile of t (outside the panel); the diagonal block becomes Dinv.
-__global__ void __launch_bounds__(256) k_gj_panel(double *S, int ns, int K, const double *__restrict__ Dinv,
-                                                  double *Dnext, const double *rowmax, const int *sep_rows,
-                                                  int *status, double pivtol) {
-  __shared__ double Ds[GJB][GJB + 1];
-  __shared__ double T[GJB][GJB + 1];
-  const int b = min(GJB, ns - K);
-  const int tid = threadIdx.x;
-  if (blockIdx.x == gridDim.x - 1) {  // the next panel's diagonal block: final after this panel's update
-    if (tid < 32 && K + GJB < ns) gj_diag_warp(S, ns, K + GJB, Dnext, rowmax, sep_rows, status, pivtol);
-    return;
-  }
-  const int t0 = blockIdx.x * GJB;
-  for (int t = tid; t < GJB * GJB; t += 256) Ds[t / GJB][t % GJB] = Dinv[t];
-  if (t0 >= K && t0 < K + b) {  // the diagonal block
-    __syncthreads();
-    for (int t = tid; t < GJB * GJB; t += 256) {
-      const int r = t / GJB, c = t % GJB;
-      if (r < b && c < b) S[(long long)(K + r) * ns + K + c] = Ds[r][c];
-    }
-    return;
-  }
-  // panel rows: T[k][c] = S[K + k][t0 + c]
-  for (int t = tid; t < GJB * GJB; t += 256) {
-    const int k = t / GJB, c = t % GJB;
-    T[k][c] = (k < b && t0 + c < ns) ? S[(long long)(K + k) * ns + t0 + c] : 0.0;
-  }
-  __syncthreads();
-  for (int t = tid; t < GJB * GJB; t += 256) {
-    const int k = t / GJB, c = t % GJB;
-    double acc = 0.0;
-#pragma unroll 8
-    for (int m = 0; m < GJB; ++m) acc = fma(Ds[k][m], T[m][c], acc);
-    if (k < b && t0 + c < ns) S[(long long)(K + k) * ns + t0 + c] = acc;
-  }
-  __syncthreads();
-  // panel columns: T[r][k] = S[t0 + r][K + k]
-  for (int t = tid; t < GJB * GJB; t += 256) {
-    const int r = t / GJB, k = t % GJB;
-    T[r][k] = (k < b && t0 + r < ns) ? S[(long long)(t0 + r) * ns + K + k] : 0.0;
-  }
-  __syncthreads();
-  for (int t = tid; t < GJB * GJB; t += 256) {
-    const int r = t / GJB, k = t % GJB;
-    double acc = 0.0;
-#pragma unroll 8
-    for (int m = 0; m < GJB; ++m) acc = fma(T[r][m], Ds[m][k], acc);
-    if (k < b && t0 + r < ns) S[(long long)(t0 + r) * ns + K + k] = -acc;
+    grid_barrier(bar, gen);
+    double *t = Sin;
+    Sin = Sout;
+    Sout = t;
   }
 }
 
@@ -1278,7 +1307,9 @@ struct rh_ctx {
   int *blk_fo_off, *fo, *ks_ptr, *ks4, *ks_k;
   unsigned short *tgt16;
   int *sb_src, *sb_dense;
-  double *gj_dinv;
+  double *Sbuf = nullptr;   // ping-pong partner of Sinv in k_sep_inverse
+  unsigned *grid_bar = nullptr;
+  int coop_blocks = 1;
   double *dinv_rows, *rowmax;
   double *Sinv = nullptr, *SinvT = nullptr;
   size_t smem_fact_blk = 0, smem_fact_sep = 0;
@@ -1527,7 +1558,8 @@ int upload(rh_ctx *c) {
   const size_t ns2 = (size_t)A.sep_rows * A.sep_rows;
   chk(c->Sinv = dalloc<double>(ns2, P));
   chk(c->SinvT = dalloc<double>(ns2, P));
-  chk(c->gj_dinv = dalloc<double>(2 * GJB * GJB, P));
+  chk(c->Sbuf = dalloc<double>(std::max<size_t>(ns2, 1), P));
+  chk(c->grid_bar = dalloc<unsigned>(2, P));
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
   // shared-memory footprints
   c->smem_fact_blk = fact_smem_bytes(A);
@@ -1542,11 +1574,18 @@ int upload(rh_ctx *c) {
     allow((const void *)k_fact_blocks);
     allow((const void *)k_tops_inverse);
     allow((const void *)k_blk);
+    allow((const void *)k_sep_inverse);
     cudaGetLastError();
   }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
   cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
   if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 16 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->grid_bar, 0, 2 * sizeof(unsigned));
+  {  // co-resident CTAs of k_sep_inverse (cooperative launch)
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sep_inverse, 256, gj_smem_bytes());
+    c->coop_blocks = std::max(1, per_sm) * c->nsm;
+  }
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(c, RH_E_CUDA, std::string("upload: ") + cudaGetErrorString(e));
   return RH_OK;
@@ -2002,18 +2041,21 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
     const int nsl = (int)A.sb_src.size();
     k_sep_dense<<<nblk(nsl), kThreads, 0, st>>>(nsl, c->sb_src, c->sb_dense, c->F_val, c->Sinv);
     RH_LAUNCHED(c);
-    const int nt = (ns + 63) / 64;
+    // blocked Gauss-Jordan, one cooperative launch; the result lands in Sinv
+    const int npanel = (ns + GJB - 1) / GJB;
+    double *Sa = (npanel & 1) ? c->Sbuf : c->Sinv, *Sb = (npanel & 1) ? c->Sinv : c->Sbuf;
+    if (Sa != c->Sinv) RH_CUDA(c, cudaMemcpyAsync(Sa, c->Sinv, sizeof(double) * (size_t)ns * ns, cudaMemcpyDeviceToDevice, st));
     const int *sep_rows = c->row_global + A.seg_row_off[A.nblk];
-    k_gj_diag<<<1, 32, 0, st>>>(c->Sinv, ns, 0, c->gj_dinv, c->rowmax, sep_rows, c->status, 1e-14);
+    int nsv = ns;
+    double pivtol = 1e-14;
+    const double *rowmax = c->rowmax;
+    int *status = c->status;
+    unsigned *bar = c->grid_bar;
+    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar};
+    const int ntl = ((ns + GJT - 1) / GJT) * ((ns + GJT - 1) / GJT);
+    const int grid = std::max(1, std::min(ntl, c->coop_blocks));
+    RH_CUDA(c, cudaLaunchCooperativeKernel((const void *)k_sep_inverse, dim3(grid), dim3(256), args, gj_smem_bytes(), st));
     RH_LAUNCHED(c);
-    for (int K = 0, ping = 0; K < ns; K += GJB, ping ^= 1) {
-      double *dcur = c->gj_dinv + ping * GJB * GJB, *dnext = c->gj_dinv + (ping ^ 1) * GJB * GJB;
-      k_gj_update<<<dim3(nt, nt), 256, 0, st>>>(c->Sinv, ns, K, dcur);
-      RH_LAUNCHED(c);
-      k_gj_panel<<<(ns + GJB - 1) / GJB + 1, 256, 0, st>>>(c->Sinv, ns, K, dcur, dnext, c->rowmax, sep_rows,
-                                                            c->status, 1e-14);
-      RH_LAUNCHED(c);
-    }
     k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
     RH_LAUNCHED(c);
   }
