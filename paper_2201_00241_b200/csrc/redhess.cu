@@ -361,7 +361,7 @@ constexpr int GJT = 64;   // output tile
 constexpr size_t gj_smem_bytes() { return sizeof(double) * (GJB * (GJB + 1) + (2 * GJB + GJT) * (GJT + 1)); }
 __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int ns, const double *rowmax,
                                                      const int *sep_rows, int *status, double pivtol,
-                                                     unsigned *bar) {
+                                                     unsigned *bar, long long *dbg) {
   extern __shared__ double gj_sm[];   // dynamic: gj_smem_bytes()
   double(*Ds)[GJB + 1] = reinterpret_cast<double(*)[GJB + 1]>(gj_sm);
   double(*Cs)[GJT + 1] = reinterpret_cast<double(*)[GJT + 1]>(gj_sm + GJB * (GJB + 1));   // C^T: Cs[m][r] = S[i0 + r][K + m]
@@ -413,8 +413,10 @@ __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int
       }
     }
   };
+  long long *prof = (dbg && tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) ? dbg + (blockIdx.x ? 512 : 0) : nullptr;
   for (int K = 0; K < ns; K += GJB) {
     const int b = min(GJB, ns - K);
+    if (prof) prof[(K / GJB) * 4] = clock64();   // timing experiment (RH_DEBUG & 16)
     if (warp < 4) {
       // D^-1 -> Ds (every CTA, redundantly) by 4 warps: thread = (rows 8w..8w+7, column lane);
       // the pivot row goes through shared memory, the pivot column by shuffles
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int
       const int i0 = (tile / nt) * GJT, j0 = (tile % nt) * GJT;
       if (tile != (int)blockIdx.x) load_tile(Sin, K, b, i0, j0, tid, blockDim.x);
       __syncthreads();   // Ds (first tile), Cs, Rs = P, Ts
+      if (prof && tile == (int)blockIdx.x) prof[(K / GJB) * 4 + 1] = clock64();
       double rr[GJB * GJT / 256];
 #pragma unroll
       for (int u = 0; u < GJB * GJT / 256; ++u) {
@@ -507,7 +510,9 @@ __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int
       }
       __syncthreads();
     }
+    if (prof) prof[(K / GJB) * 4 + 2] = clock64();
     grid_barrier(bar, gen);
+    if (prof) prof[(K / GJB) * 4 + 3] = clock64();
     double *t = Sin;
     Sin = Sout;
     Sout = t;
@@ -976,50 +981,60 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
 
 // C[m][n] = sum_k M[m][k] T[k][n] written to the separator slab of Z / P
 // (rows sep_off + m, contiguous in segment order).  64 x 64 output tile per
-// CTA, 128 threads, 8 x 4 outputs per thread, k in tiles of 16 staged in
-// shared memory with the next tile prefetched into registers.  Fixed k order:
-// deterministic.
-constexpr int GBM = 64, GBN = 64, GBK = 16, GTHREADS = 128;
+// CTA; in-CTA split-K: 4 groups of 128 threads each sweep a quarter of the k
+// tiles (8 x 4 outputs per thread, k tiles of 16 staged in shared memory with
+// the next tile prefetched into registers), then the partial tiles are added
+// in fixed group order (deterministic).
+constexpr int GBM = 64, GBN = 64, GBK = 8, GGRP = 4, GTHREADS = 128 * GGRP;
 __global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
-  __shared__ __align__(16) double As[GBK][GBM + 2];   // +2: conflict-free transposed stores
-  __shared__ __align__(16) double Bs[GBK][GBN];
+  // per group: As [GBK][GBM + 2] (+2: conflict-free transposed stores), Bs [GBK][GBN];
+  // afterwards the reduction tile Red [GBM][GBN] reuses the same space
+  constexpr int kAs = GBK * (GBM + 2), kBs = GBK * GBN, kBuf = GGRP * (kAs + kBs);
+  static_assert(kBuf >= GBM * GBN, "reduction tile fits");
+  __shared__ __align__(16) double gbuf[kBuf];
   const int ns = h.ns, ld = h.ld;
   const double *M = mode == MODE_LU ? h.Sinv : h.SinvT;
   double *G = mode == MODE_LU ? h.Z : h.P;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
-  const int tid = threadIdx.x;
+  const int grp = threadIdx.x >> 7, tid = threadIdx.x & 127;
+  double(*As)[GBM + 2] = reinterpret_cast<double(*)[GBM + 2]>(gbuf + grp * (kAs + kBs));
+  double(*Bs)[GBN] = reinterpret_cast<double(*)[GBN]>(gbuf + grp * (kAs + kBs) + kAs);
+  double(*Red)[GBN] = reinterpret_cast<double(*)[GBN]>(gbuf);
   const int tx = tid % 16, ty = tid / 16;  // 16 x 8 threads: n = tx*4.., m = ty*8..
+  const int nkt = (ns + GBK - 1) / GBK;
+  const int kt0 = nkt * grp / GGRP, kt1 = nkt * (grp + 1) / GGRP;   // this group's k tiles
   double acc[8][4];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  double ra[8], rb[8];
+  constexpr int NL = GBM * GBK / 128;   // loads per thread per array
+  double ra[NL], rb[NL];
   auto load = [&](int k0) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int idx = tid + r * GTHREADS;          // 1024 = 64 (m) x 16 (k)
+    for (int r = 0; r < NL; ++r) {
+      const int idx = tid + r * 128;                // 512 = 64 (m) x 8 (k)
       const int mm = idx / GBK, kk = idx % GBK;
       const int gm = m0 + mm, gk = k0 + kk;
       ra[r] = (gm < ns && gk < ns) ? __ldg(M + (long long)gm * ns + gk) : 0.0;
-      const int kb = idx / GBN, nn = idx % GBN;    // 1024 = 16 (k) x 64 (n)
+      const int kb = idx / GBN, nn = idx % GBN;    // 512 = 8 (k) x 64 (n)
       const int gk2 = k0 + kb;
       rb[r] = (gk2 < ns && n0 + nn < ld) ? h.Tsep[(long long)gk2 * ld + n0 + nn] : 0.0;
     }
   };
   auto store = [&]() {
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const int idx = tid + r * GTHREADS;
+    for (int r = 0; r < NL; ++r) {
+      const int idx = tid + r * 128;
       As[idx % GBK][idx / GBK] = ra[r];
       Bs[idx / GBN][idx % GBN] = rb[r];
     }
   };
-  load(0);
-  for (int k0 = 0; k0 < ns; k0 += GBK) {
+  if (kt0 < kt1) load(kt0 * GBK);
+  for (int kt = kt0; kt < kt1; ++kt) {
     store();
-    __syncthreads();
-    if (k0 + GBK < ns) load(k0 + GBK);
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+    if (kt + 1 < kt1) load((kt + 1) * GBK);
 #pragma unroll
     for (int kk = 0; kk < GBK; ++kk) {
       double a[8], bv[4];
@@ -1041,20 +1056,36 @@ __global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
     }
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+  }
+  // fixed-order reduction of the group partials: Red = p0; Red += p1; Red += p2; out = Red + p3
+  __syncthreads();
+  for (int g = 0; g < GGRP - 1; ++g) {
+    if (grp == g) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) Red[ty * 8 + i][tx * 4 + j] = g == 0 ? acc[i][j] : Red[ty * 8 + i][tx * 4 + j] + acc[i][j];
+    }
     __syncthreads();
   }
+  if (grp == GGRP - 1) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int gm = m0 + ty * 8 + i;
-    if (gm >= ns) continue;
-    double *out = G + (long long)(h.sep_off + gm) * ld + n0 + tx * 4;
-    if (n0 + tx * 4 + 3 < ld) {
-      reinterpret_cast<double2 *>(out)[0] = make_double2(acc[i][0], acc[i][1]);
-      reinterpret_cast<double2 *>(out)[1] = make_double2(acc[i][2], acc[i][3]);
-    } else {
+    for (int i = 0; i < 8; ++i) {
+      const int gm = m0 + ty * 8 + i;
+      if (gm >= ns) continue;
+      double o[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (n0 + tx * 4 + j < ld) out[j] = acc[i][j];
+      for (int j = 0; j < 4; ++j) o[j] = Red[ty * 8 + i][tx * 4 + j] + acc[i][j];
+      double *out = G + (long long)(h.sep_off + gm) * ld + n0 + tx * 4;
+      if (n0 + tx * 4 + 3 < ld) {
+        reinterpret_cast<double2 *>(out)[0] = make_double2(o[0], o[1]);
+        reinterpret_cast<double2 *>(out)[1] = make_double2(o[2], o[3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (n0 + tx * 4 + j < ld) out[j] = o[j];
+      }
     }
   }
 }
@@ -2051,11 +2082,27 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
     const double *rowmax = c->rowmax;
     int *status = c->status;
     unsigned *bar = c->grid_bar;
-    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar};
+    long long *gdbg = nullptr;
+    if (const char *env = getenv("RH_DEBUG"))   // timing experiment: per-panel stamps
+      if (atoi(env) & 16) {
+        static long long *buf = nullptr;
+        if (!buf) cudaMalloc(&buf, 1024 * sizeof(long long));
+        gdbg = buf;
+      }
+    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar, &gdbg};
     const int ntl = ((ns + GJT - 1) / GJT) * ((ns + GJT - 1) / GJT);
     const int grid = std::max(1, std::min(ntl, c->coop_blocks));
     RH_CUDA(c, cudaLaunchCooperativeKernel((const void *)k_sep_inverse, dim3(grid), dim3(256), args, gj_smem_bytes(), st));
     RH_LAUNCHED(c);
+    if (gdbg) {
+      std::vector<long long> hb(1024);
+      cudaMemcpyAsync(hb.data(), gdbg, 1024 * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      if (FILE *fp = fopen("gpurun_out/gj_prof.bin", "wb")) {
+        fwrite(hb.data(), 8, hb.size(), fp);
+        fclose(fp);
+      }
+    }
     k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
     RH_LAUNCHED(c);
   }
