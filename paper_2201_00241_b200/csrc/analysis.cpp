@@ -380,6 +380,129 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
 }
 
 // ---------------------------------------------------------------------------
+// Tiles of the staged tensor projection (ForGroups): every bus is an output of
+// the group of its theta row's segment (the REF bus, which has no theta row,
+// goes with its lowest neighbour); separator buses in chunks of kMaxOut.
+// ---------------------------------------------------------------------------
+void build_for_groups(Analysis &A) {
+  ForGroups &F = A.fg;
+  F = ForGroups();
+  const int n = A.n_bus, nb = A.nblk;
+  std::vector<int> gseg(n, -1);   // segment of each bus
+  for (int b = 0; b < n; ++b)
+    if (b != A.ref) gseg[b] = A.seg_of[A.pinv[A.th_x[b]]];
+  {
+    int lo = -1;
+    for (int s = A.bl_ptr[A.ref]; s < A.bl_ptr[A.ref + 1]; ++s)
+      if (lo < 0 || A.bl_other[s] < lo) lo = A.bl_other[s];
+    gseg[A.ref] = lo >= 0 ? gseg[lo] : nb;
+  }
+  std::vector<std::vector<int>> seg_bus(nb + 1);
+  for (int b = 0; b < n; ++b) seg_bus[gseg[b]].push_back(b);
+  auto theta_row = [&](int b) { return b == A.ref ? -1 : A.pinv[A.th_x[b]]; };
+  for (auto &v : seg_bus)
+    std::stable_sort(v.begin(), v.end(), [&](int x, int y) { return theta_row(x) < theta_row(y); });
+  // greedy: a segment's buses (theta-row order) while outputs + halo fit kMaxLoc
+  std::vector<std::vector<int>> groups;
+  {
+    std::vector<int> mark(n, -1);
+    int gid = 0;
+    for (int s = 0; s <= nb; ++s) {
+      std::vector<int> cur;
+      int nloc = 0;
+      auto close = [&]() {
+        if (!cur.empty()) groups.push_back(cur);
+        cur.clear();
+        nloc = 0;
+        ++gid;
+      };
+      for (int b : seg_bus[s]) {
+        int add = mark[b] == gid ? 0 : 1;
+        for (int q = A.bl_ptr[b]; q < A.bl_ptr[b + 1]; ++q) add += mark[A.bl_other[q]] == gid ? 0 : 1;
+        if (!cur.empty() && nloc + add + (int)A.near_ref.size() > ForGroups::kMaxLoc) close();
+        cur.push_back(b);
+        if (mark[b] != gid) ++nloc;
+        mark[b] = gid;
+        for (int q = A.bl_ptr[b]; q < A.bl_ptr[b + 1]; ++q)
+          if (mark[A.bl_other[q]] != gid) {
+            mark[A.bl_other[q]] = gid;
+            ++nloc;
+          }
+      }
+      close();
+    }
+  }
+  std::vector<char> near(n, 0);
+  for (int b : A.near_ref) near[b] = 1;
+  F.grp_off.assign(1, 0);
+  F.grp_obase.assign(1, 0);
+  F.grp_ref.assign(1, 0);
+  F.grp_sbase.assign(1, 0);
+  std::vector<int> lidx(n, -1);
+  for (const auto &out : groups) {
+    std::vector<int> locs(out);
+    for (int i = 0; i < (int)locs.size(); ++i) lidx[locs[i]] = i;
+    bool has_ref = false;
+    for (int b : out) {
+      has_ref = has_ref || near[b];
+      for (int s = A.bl_ptr[b]; s < A.bl_ptr[b + 1]; ++s) {
+        const int o = A.bl_other[s];
+        if (lidx[o] < 0) {
+          lidx[o] = (int)locs.size();
+          locs.push_back(o);
+        }
+      }
+    }
+    if (has_ref)
+      for (int o : A.near_ref)
+        if (lidx[o] < 0) {
+          lidx[o] = (int)locs.size();
+          locs.push_back(o);
+        }
+    int zrows = 0;
+    for (int b : locs) {
+      F.loc.push_back(A.dth_src[b]);
+      F.loc.push_back(A.dv_src[b]);
+      F.loc.push_back(b);
+      F.loc.push_back(0);
+      zrows += (A.dth_src[b] >= 0) + (A.dv_src[b] >= 0);
+    }
+    const int sbase = (int)F.slots.size() / 2;
+    for (int b : out) {
+      const int first = (int)F.slots.size() / 2 - sbase;
+      for (int s = A.bl_ptr[b]; s < A.bl_ptr[b + 1]; ++s) {
+        F.slots.push_back(A.bl_line[s]);
+        F.slots.push_back(lidx[A.bl_other[s]] * 2 + (A.bl_end[s] ? 1 : 0));
+      }
+      F.out_bus.push_back(b);
+      F.out_dst.push_back(A.yth_dst[b]);
+      F.out_dst.push_back(A.yv_dst[b]);
+      F.out_dst.push_back(first);
+      F.out_dst.push_back(A.bl_ptr[b + 1] - A.bl_ptr[b]);
+    }
+    while ((F.slots.size() / 2) % 4) {   // pad the group's slot range to a multiple of 4
+      F.slots.push_back(-1);
+      F.slots.push_back(0);
+    }
+    F.grp_sbase.push_back((int)F.slots.size() / 2);
+    F.max_slots = std::max(F.max_slots, F.grp_sbase.back() - sbase);
+    if (has_ref)
+      for (int o : A.near_ref) F.ref_loc.push_back(lidx[o]);
+    for (int b : locs) lidx[b] = -1;
+    F.grp_off.push_back(F.grp_off.back() + (int)locs.size());
+    F.grp_nout.push_back((int)out.size());
+    F.grp_obase.push_back(F.grp_obase.back() + (int)out.size());
+    F.grp_zrows.push_back(zrows);
+    F.grp_ref.push_back((int)F.ref_loc.size());
+    F.max_loc = std::max(F.max_loc, (int)locs.size());
+    F.max_nout = std::max(F.max_nout, (int)out.size());
+  }
+  if (getenv("RH_DEBUG_SCHED"))
+    fprintf(stderr, "for groups %zu: max locals %d, max outputs %d, locals %zu (buses %d)\n", F.grp_nout.size(),
+            F.max_loc, F.max_nout, F.loc.size() / 4, n);
+}
+
+// ---------------------------------------------------------------------------
 // Elimination-tree segments (blocks of whole subtrees + the separator), the
 // per-segment level schedules of the four sweeps, and the refactorization
 // schedule (DESIGN.md "Sweeps" and "Refactorization").
@@ -1173,6 +1296,7 @@ std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
   for (int s = A.bl_ptr[A.ref]; s < A.bl_ptr[A.ref + 1]; ++s) A.near_ref.push_back(A.bl_other[s]);
   sort_unique(A.near_ref);
   build_segments(A, Ls, Lrow, fpos, rmax);
+  build_for_groups(A);
   return "";
 }
 

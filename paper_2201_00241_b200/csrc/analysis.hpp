@@ -90,6 +90,29 @@ struct UnitSweep {
   int max_units = 0, max_tunits = 0, max_rec = 0, max_doff = 0, max_rows = 0;
 };
 
+// Tiles of the staged tensor projection (k_for):
+// output buses grouped by the segment of their theta row (blocks; the
+// separator in chunks), each group with its halo of neighbour buses, so one
+// CTA stages every delta row a group needs once in shared memory.
+struct ForGroups {
+  static constexpr int kMaxLoc = 160;   // locals (outputs + halo) per group: 2 CTAs of k_for per SM
+  std::vector<int32_t> grp_off;    // [ng + 1] locals of each group: its output buses first, then the halo
+  std::vector<int32_t> grp_nout;   // [ng]
+  std::vector<int32_t> grp_obase;  // [ng + 1] first output of each group in out_ptr
+  std::vector<int32_t> grp_zrows;  // [ng] staged Z rows of each group
+  // per local (int4): theta source, v source (permuted row >= 0, W row -(p + 2), -1 zero), bus, 0
+  std::vector<int32_t> loc;
+  std::vector<int32_t> grp_sbase;  // [ng + 1] first slot of each group (groups padded to 4 slots)
+  std::vector<int32_t> out_bus;    // [n_out] bus of every output
+  // [4 * n_out]: theta output row (permuted, -1 none), v output row (permuted >= 0, Y_p row -(p + 2)),
+  // first slot (group-local), slot count
+  std::vector<int32_t> out_dst;
+  std::vector<int32_t> slots;      // [2 * nslots]: line (-1 padding), other end's local index * 2 + (1 if the bus is the to-end)
+  std::vector<int32_t> grp_ref;    // [ng + 1] into ref_loc (groups with an output in {ref} u A(ref))
+  std::vector<int32_t> ref_loc;    // local indices of the {ref} u A(ref) buses
+  int max_loc = 0, max_nout = 0, max_slots = 0;
+};
+
 struct Analysis {
   // ---------------- grid copy ----------------
   int n_bus = 0, n_line = 0, n_gen = 0, ref = -1;
@@ -154,6 +177,7 @@ struct Analysis {
   std::vector<BlockSplit> usplit;           // per block (UnitSweep::kWarps: unit sweeps, tops)
   std::vector<int32_t> unit_lo;             // [n_x] lowest permuted row of the row's bus unit
   UnitSweep ufwd, ubwd;                     // bus-unit block sweeps (fwd: L, U^T; bwd: U, L^T)
+  ForGroups fg;                             // staged tensor projection tiles
   // tops of every block (densely inverted per state): rows, F positions of T x T,
   // and the first dense entry of every top row in the fwd / bwd entry arrays
   std::vector<int32_t> top_ptr, top_rows, top_fpos_ptr, top_fpos, top_fwd_base, top_bwd_base;

@@ -72,6 +72,14 @@ struct SegParams {
   const int *near_ref;
   int n_near_ref;
   double f2ref;
+  // staged tensor projection tiles (analysis.hpp ForGroups; sources / outputs in Z rows)
+  const int *fg_off, *fg_nout, *fg_obase, *fg_zrows, *fg_sbase, *fg_ref, *fg_ref_loc;
+  int fg_maxloc, fg_maxout, fg_maxslots;
+  const int4 *fg_loc, *fg_odst;        // per local: sources, bus; per output: theta row, v row, first slot, slots
+  const int *fg_soe;                   // per slot: other end's local * 2 + to-end
+  const double4 *fg_scoef, *fg_ometa;  // per state and lambda (k_for_tape): slot coefficients; dcoef, grad P_ref
+  const int *p_kind;                   // Pg diagonal of Y_p in k_muladd
+  const double *pdiag;                 // [n_p] 2 c2 (Pg parameters) else 0
   int debug;                         // experiment bits (0 in production)
   long long *dbg;
 };

@@ -1105,84 +1105,129 @@ __device__ __forceinline__ double delta_src(const SegParams &h, int src, int col
   return load_W(h, -(src + 2), col);
 }
 
-// One warp per bus, one lane per column, FCH column chunks per warp processed
-// together (index / coefficient loads amortized, FCH independent gathers in
-// flight per incident line).
-constexpr int FCH = 2;
-__global__ void __launch_bounds__(kThreads, 4) k_for(SegParams h) {
-  const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  if (b >= h.n_bus) return;
-  const int nch = h.ld / 32;
-  const int ch0 = blockIdx.y * FCH;
-  int col[FCH];
-#pragma unroll
-  for (int u = 0; u < FCH; ++u) col[u] = (ch0 + u < nch ? ch0 + u : nch - 1) * 32 + lane;
-  const int dths = h.dth_src[b], dvs = h.dv_src[b];
-  const double dc = h.dcoef[b];
-  double dth_b[FCH], dv_b[FCH], yth[FCH], yv[FCH];
-#pragma unroll
-  for (int u = 0; u < FCH; ++u) {
-    dth_b[u] = delta_src(h, dths, col[u]);
-    dv_b[u] = delta_src(h, dvs, col[u]);
-    yth[u] = 0.0;
-    yv[u] = dc * dv_b[u];
+// Staged tiles: one CTA = (bus group, 32 columns) (analysis.hpp ForGroups).
+// The delta rows (dtheta, dv) of the group's buses and of their neighbours are
+// staged once in shared memory (Z rows by TMA bulk copies on an mbarrier, v
+// parameters from W), so each line end's gather reads shared memory instead
+// of L2; warp per output bus, lane per column.
+__global__ void __launch_bounds__(256) k_for(SegParams h) {
+  extern __shared__ __align__(128) double fsm[];   // [maxloc][2][32] delta rows, then the tile's tape
+  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ double sref[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int g = blockIdx.x, col0 = blockIdx.y * 32, col = col0 + lane;
+  const int l0 = h.fg_off[g], nl = h.fg_off[g + 1] - l0, nout = h.fg_nout[g], ob = h.fg_obase[g];
+  const int sb = h.fg_sbase[g], nsl = h.fg_sbase[g + 1] - sb;
+  double4 *s_coef = reinterpret_cast<double4 *>(fsm + (size_t)h.fg_maxloc * 64);
+  double4 *s_meta = s_coef + h.fg_maxslots;
+  int4 *s_dst = reinterpret_cast<int4 *>(s_meta + h.fg_maxout);
+  int *s_oe = reinterpret_cast<int *>(s_dst + h.fg_maxout);
+  int2 *s_fill = reinterpret_cast<int2 *>(s_oe + h.fg_maxslots);   // [2 maxloc]
+  __shared__ int s_nfill;
+  if (tid == 0) {
+    s_nfill = 0;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    const unsigned tx = 256u * h.fg_zrows[g] + 36u * nsl + 48u * nout;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx) : "memory");
+    bulk_g2s(s_coef, h.fg_scoef + sb, 32u * nsl, &mbar);
+    bulk_g2s(s_oe, h.fg_soe + sb, 4u * nsl, &mbar);
+    bulk_g2s(s_meta, h.fg_ometa + ob, 32u * nout, &mbar);
+    bulk_g2s(s_dst, h.fg_odst + ob, 16u * nout, &mbar);
   }
-  const int s0 = h.bl_ptr[b], s1 = h.bl_ptr[b + 1];
-  for (int s = s0; s < s1; ++s) {
-    const double4 k = h.coef[h.bl_line[s]];
-    const int os = h.o_dth_src[s], ov = h.o_dv_src[s];
-    const bool from = h.bl_end[s] == 0;
-    double dth_o[FCH], dv_o[FCH];
+  __syncthreads();
+  // thread per local: bulk copies of its Z rows; rows without a Z source go to
+  // a list (zero, or a v parameter from W) that the warps then fill, lane =
+  // column, 4 rows in flight per warp
+  for (int l = tid; l < nl; l += blockDim.x) {
+    const int4 e = h.fg_loc[l0 + l];
+    if (e.x >= 0) bulk_g2s(fsm + l * 64, h.Z + (long long)e.x * h.ld + col0, 256, &mbar);
+    else s_fill[atomicAdd(&s_nfill, 1)] = make_int2(l * 64, -1);
+    if (e.y >= 0) bulk_g2s(fsm + l * 64 + 32, h.Z + (long long)e.y * h.ld + col0, 256, &mbar);
+    else s_fill[atomicAdd(&s_nfill, 1)] = make_int2(l * 64 + 32, e.y == -1 ? -1 : -(e.y + 2));
+  }
+  __syncthreads();
+  for (int f = 4 * warp; f < s_nfill; f += 4 * nw) {
+    double v[4];
 #pragma unroll
-    for (int u = 0; u < FCH; ++u) {
-      dth_o[u] = delta_src(h, os, col[u]);
-      dv_o[u] = delta_src(h, ov, col[u]);
+    for (int u = 0; u < 4; ++u) {
+      const int2 q = f + u < s_nfill ? s_fill[f + u] : make_int2(-1, -1);
+      v[u] = q.y >= 0 ? load_W(h, q.y, col) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < FCH; ++u) {
-      if (from) {  // b is the from-end i
-        const double D = dth_b[u] - dth_o[u];
-        yth[u] += k.x * D + k.y * dv_b[u] + k.z * dv_o[u];
-        yv[u] += k.y * D + k.w * dv_o[u];
-      } else {     // b is the to-end j
-        const double D = dth_o[u] - dth_b[u];
-        yth[u] -= k.x * D + k.y * dv_o[u] + k.z * dv_b[u];
-        yv[u] += k.z * D + k.w * dv_o[u];
+    for (int u = 0; u < 4; ++u)
+      if (f + u < s_nfill) fsm[s_fill[f + u].x + lane] = v[u];
+  }
+  {
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(smem_u32(&mbar))
+                   : "memory");
+  }
+  __syncthreads();
+  const int r0 = h.fg_ref[g], r1 = h.fg_ref[g + 1];
+  if (r0 < r1) {   // REF objective rank-1 term f''(Pg_ref) (grad P_ref . delta) (R22), once per tile
+    if (warp == 0) {
+      double sr = 0.0;
+      for (int q = r0; q < r1; ++q) {
+        const int l = h.fg_ref_loc[q], b = h.fg_loc[l0 + l].z;
+        sr += h.refg_th[b] * fsm[l * 64 + lane] + h.refg_v[b] * fsm[l * 64 + 32 + lane];
+      }
+      sref[lane] = sr * h.f2ref;
+    }
+    __syncthreads();
+  }
+  for (int i = warp; i < nout; i += nw) {   // warp per output bus, lane per column, all from shared memory
+    const int4 d = s_dst[i];
+    const double4 mt = s_meta[i];
+    const double dth_b = fsm[i * 64 + lane], dv_b = fsm[i * 64 + 32 + lane];
+    double yth = 0.0, yv = mt.x * dv_b;
+    for (int q = d.z; q < d.z + d.w; ++q) {
+      const double4 k = s_coef[q];
+      const int oe = s_oe[q], o = oe >> 1;
+      const double dth_o = fsm[o * 64 + lane], dv_o = fsm[o * 64 + 32 + lane];
+      if (!(oe & 1)) {   // b is the from-end i
+        const double D = dth_b - dth_o;
+        yth += k.x * D + k.y * dv_b + k.z * dv_o;
+        yv += k.y * D + k.w * dv_o;
+      } else {           // b is the to-end j
+        const double D = dth_o - dth_b;
+        yth -= k.x * D + k.y * dv_o + k.z * dv_b;
+        yv += k.z * D + k.w * dv_o;
       }
     }
-  }
-  // REF objective rank-1 term f''(Pg_ref) (grad P_ref . delta) grad P_ref (R22):
-  // only the buses of {ref} u A(ref) carry a nonzero grad P_ref entry
-  const double rt = h.refg_th[b], rv = h.refg_v[b];
-  if (rt != 0.0 || rv != 0.0) {
-#pragma unroll
-    for (int u = 0; u < FCH; ++u) {
-      double sref = 0.0;
-      for (int q = 0; q < h.n_near_ref; ++q) {
-        const int o = h.near_ref[q];
-        sref += h.refg_th[o] * delta_src(h, h.dth_src[o], col[u]) + h.refg_v[o] * delta_src(h, h.dv_src[o], col[u]);
-      }
-      sref *= h.f2ref;
-      yth[u] += sref * rt;
-      yv[u] += sref * rv;
+    if (mt.y != 0.0 || mt.z != 0.0) {
+      yth += sref[lane] * mt.y;
+      yv += sref[lane] * mt.z;
     }
-  }
-  const int dt = h.yth_dst[b], dv = h.yv_dst[b], pg = h.pg_p[b];
-  const double c2x2 = 2.0 * h.c2b[b];
-#pragma unroll
-  for (int u = 0; u < FCH; ++u) {
-    if (ch0 + u >= nch) break;
-    const int c = col[u];
-    if (dt >= 0) h.P[(long long)dt * h.ld + c] = -yth[u];
-    if (dv >= 0) {
-      h.P[(long long)dv * h.ld + c] = -yv[u];
-    } else if (c < h.N) {
-      h.HW[hw_index(h, -(dv + 2), c)] = yv[u];
+    if (d.x >= 0) h.P[(long long)d.x * h.ld + col] = -yth;
+    if (d.y >= 0) {
+      h.P[(long long)d.y * h.ld + col] = -yv;
+    } else if (d.y <= -2 && col < h.N) {
+      h.HW[hw_index(h, -(d.y + 2), col)] = yv;
     }
-    if (pg >= 0 && c < h.N) h.HW[hw_index(h, pg, c)] = c2x2 * load_W(h, pg, c);
   }
 }
+
+// The FoR tape in tile order (once per state and lambda, after k_coefs): the
+// line coefficients of every slot and (dcoef, grad P_ref) of every output.
+__global__ void k_for_tape(int nslots, int nout, const int2 *slots, const int *out_bus, const double4 *coef,
+                           const double *dcoef, const double *refg_th, const double *refg_v, double4 *scoef,
+                           double4 *ometa) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nslots) {
+    const int line = slots[t].x;
+    scoef[t] = line >= 0 ? coef[line] : make_double4(0.0, 0.0, 0.0, 0.0);
+  } else if (t - nslots < nout) {
+    const int o = t - nslots, b = out_bus[o];
+    ometa[o] = make_double4(dcoef[b], refg_th[b], refg_v[b], 0.0);
+  }
+}
+
+constexpr int FCH = 2;   // column chunks of 32 per warp in k_muladd
 
 // SpMulAdd HW = Y_p + G_p^T Psi: one warp per p row, lanes over
 // columns, FCH chunks per warp
@@ -1195,9 +1240,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_muladd(SegParams h) {
   double acc[FCH];
   int col[FCH];
 #pragma unroll
+  // Y_p: a Pg row is the cost diagonal 2 c2 w (from W); a v row was written by k_for
+  const double c2x2 = h.pdiag[cp];
+  const bool pg = c2x2 != 0.0 || h.p_kind[cp] == RH_KIND_PG;
   for (int u = 0; u < FCH; ++u) {
     col[u] = (ch0 + u) * 32 + lane;
-    acc[u] = col[u] < h.N ? h.HW[hw_index(h, cp, col[u])] : 0.0;
+    acc[u] = col[u] < h.N ? (pg ? c2x2 * load_W(h, cp, col[u]) : h.HW[hw_index(h, cp, col[u])]) : 0.0;
   }
   for (int q = q0; q < q1; ++q) {
     const double g = h.gpc_val[q];
@@ -1366,7 +1414,12 @@ struct rh_ctx {
   int smem_x_off = 0, smem_meta_off = 0, smem_tmeta_off = 0, smem_rec_off = 0, smem_doff_off = 0, smem_lvl_off = 0;
   int smem_stride = 0;
   int *blk_ctr = nullptr;
-  size_t smem_blk = 0;
+  size_t smem_blk = 0, smem_for = 0;
+  int *fg_off, *fg_nout, *fg_obase, *fg_zrows, *fg_sbase, *fg_ref, *fg_ref_loc, *fg_soe, *fg_out_bus;
+  int4 *fg_loc, *fg_odst;
+  int2 *fg_slots;
+  double4 *fg_scoef, *fg_ometa;
+  double *pdiag;   // [n_p] 2 c2 of a Pg parameter's generator, else 0 (grid data)
 
   void free_all() {
     for (void *q : pool) cudaFree(q);
@@ -1522,6 +1575,42 @@ int upload(rh_ctx *c) {
     D.ext_off = S.ext_off;
     D.ext_rows = S.ext_rows;
   };
+  {  // staged tensor projection tiles; delta sources and outputs -> Z rows
+    const ForGroups &F = A.fg;
+    std::vector<int32_t> loc = F.loc, dst = F.out_dst, soe(F.slots.size() / 2);
+    for (size_t i = 0; i < loc.size(); i += 4) {
+      if (loc[i] >= 0) loc[i] = zrow[loc[i]];
+      if (loc[i + 1] >= 0) loc[i + 1] = zrow[loc[i + 1]];
+    }
+    for (size_t i = 0; i < dst.size(); i += 4) {
+      if (dst[i] >= 0) dst[i] = zrow[dst[i]];
+      if (dst[i + 1] >= 0) dst[i + 1] = zrow[dst[i + 1]];
+    }
+    for (size_t q = 0; q < soe.size(); ++q) soe[q] = F.slots[2 * q + 1];
+    c->fg_loc = reinterpret_cast<int4 *>(dalloc_copy(loc, P));
+    c->fg_odst = reinterpret_cast<int4 *>(dalloc_copy(dst, P));
+    c->fg_slots = reinterpret_cast<int2 *>(dalloc_copy(F.slots, P));
+    chk(c->fg_loc);
+    chk(c->fg_odst);
+    chk(c->fg_slots);
+    chk(c->fg_soe = dalloc_copy(soe, P));
+    chk(c->fg_out_bus = dalloc_copy(F.out_bus, P));
+    chk(c->fg_off = dalloc_copy(F.grp_off, P));
+    chk(c->fg_nout = dalloc_copy(F.grp_nout, P));
+    chk(c->fg_obase = dalloc_copy(F.grp_obase, P));
+    chk(c->fg_zrows = dalloc_copy(F.grp_zrows, P));
+    chk(c->fg_sbase = dalloc_copy(F.grp_sbase, P));
+    chk(c->fg_ref = dalloc_copy(F.grp_ref, P));
+    chk(c->fg_ref_loc = dalloc_copy(F.ref_loc, P));
+    chk(c->fg_scoef = dalloc<double4>(soe.size(), P));
+    std::vector<double> pdiag(A.n_p, 0.0);
+    for (int q = 0; q < A.n_p; ++q)
+      if (A.p_kind[q] == RH_KIND_PG) pdiag[q] = 2.0 * A.c2b[A.p_bus[q]];
+    chk(c->pdiag = dalloc_copy(pdiag, P));
+    chk(c->fg_ometa = dalloc<double4>(F.out_bus.size(), P));
+    c->smem_for = (size_t)F.max_loc * 64 * sizeof(double) + (size_t)F.max_slots * 36 + (size_t)F.max_nout * 48 +
+                  (size_t)F.max_loc * 16;
+  }
   mkunit(c->duf, A.ufwd, c->dfwd);
   mkunit(c->dub, A.ubwd, c->dbwd);
   c->nrec_f = (int)A.ufwd.src_a.size() / 2;
@@ -1606,6 +1695,7 @@ int upload(rh_ctx *c) {
     allow((const void *)k_tops_inverse);
     allow((const void *)k_blk);
     allow((const void *)k_sep_inverse);
+    allow((const void *)k_for);
     cudaGetLastError();
   }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
@@ -1712,6 +1802,23 @@ SegParams make_params(rh_ctx *c) {
   h.uU = c->uU;
   h.uLt = c->uLt;
   h.maxrx = c->maxrx;
+  h.fg_off = c->fg_off;
+  h.fg_maxloc = A.fg.max_loc;
+  h.fg_maxout = A.fg.max_nout;
+  h.fg_maxslots = A.fg.max_slots;
+  h.fg_nout = c->fg_nout;
+  h.fg_obase = c->fg_obase;
+  h.fg_zrows = c->fg_zrows;
+  h.fg_sbase = c->fg_sbase;
+  h.fg_ref = c->fg_ref;
+  h.fg_ref_loc = c->fg_ref_loc;
+  h.fg_loc = c->fg_loc;
+  h.fg_odst = c->fg_odst;
+  h.fg_soe = c->fg_soe;
+  h.fg_scoef = c->fg_scoef;
+  h.fg_ometa = c->fg_ometa;
+  h.p_kind = c->p_kind;
+  h.pdiag = c->pdiag;
   h.smem_stride = c->smem_stride;
   h.blk_ctr = c->blk_ctr;
   h.smem_x_off = c->smem_x_off;
@@ -1742,6 +1849,10 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
   k_coefs<<<nblk(std::max(A.n_line, A.n_bus)), kThreads, 0, st>>>(
       A.n_line, A.n_bus, c->lf, c->lt, c->G_ft, c->B_ft, c->G_tf, c->B_tf, c->G_ii, c->B_ii, c->cs, c->v,
       c->muP, c->muQ, c->coef, c->dcoef);
+  RH_LAUNCHED(c);
+  const int nsl = (int)A.fg.slots.size() / 2, nout = (int)A.fg.out_bus.size();
+  k_for_tape<<<nblk(nsl + nout), kThreads, 0, st>>>(nsl, nout, c->fg_slots, c->fg_out_bus, c->coef, c->dcoef,
+                                                   c->refg_th, c->refg_v, c->fg_scoef, c->fg_ometa);
   RH_LAUNCHED(c);
   c->has_mult = true;
   return RH_OK;
@@ -1774,7 +1885,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   const dim3 gSg(nblk(A.sep_rows, kThreads / 32), ld / 32),
       gSm((ld + GBN - 1) / GBN, (A.sep_rows + GBM - 1) / GBM);
   const int nch32 = ld / 32, fch = (nch32 + FCH - 1) / FCH;
-  const dim3 gF(nblk(A.n_bus, kThreads / 32), fch), gM(nblk(A.n_p, kThreads / 32), fch);
+  const dim3 gF((int)A.fg.grp_nout.size(), ld / 32), gM(nblk(A.n_p, kThreads / 32), fch);
   const int nx = A.n_x;
   const long long tot = (long long)nx * N;
   cudaEvent_t ev[9];
@@ -1810,7 +1921,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     RH_LAUNCHED(c);
   }
   mark(3);
-  k_for<<<gF, kThreads, 0, st>>>(h);
+  k_for<<<gF, 256, c->smem_for, st>>>(h);
   RH_LAUNCHED(c);
   if (Yxo) {
     k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, c->Pb, -1.0, Yxo, ldz);
