@@ -1186,18 +1186,13 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     const double dth_b = fsm[i * 64 + lane], dv_b = fsm[i * 64 + 32 + lane];
     double yth = 0.0, yv = mt.x * dv_b;
     for (int q = d.z; q < d.z + d.w; ++q) {
+      // canonical slot coefficients (k_for_tape): D = dth_b - dth_o,
+      // yth += K D + c2 dv_b + c3 dv_o,  yv += c2 D + m dv_o
       const double4 k = s_coef[q];
-      const int oe = s_oe[q], o = oe >> 1;
-      const double dth_o = fsm[o * 64 + lane], dv_o = fsm[o * 64 + 32 + lane];
-      if (!(oe & 1)) {   // b is the from-end i
-        const double D = dth_b - dth_o;
-        yth += k.x * D + k.y * dv_b + k.z * dv_o;
-        yv += k.y * D + k.w * dv_o;
-      } else {           // b is the to-end j
-        const double D = dth_o - dth_b;
-        yth -= k.x * D + k.y * dv_o + k.z * dv_b;
-        yv += k.z * D + k.w * dv_o;
-      }
+      const int o = s_oe[q] >> 1;
+      const double D = dth_b - fsm[o * 64 + lane], dv_o = fsm[o * 64 + 32 + lane];
+      yth = fma(k.x, D, fma(k.y, dv_b, fma(k.z, dv_o, yth)));
+      yv = fma(k.y, D, fma(k.w, dv_o, yv));
     }
     if (mt.y != 0.0 || mt.z != 0.0) {
       yth += sref[lane] * mt.y;
@@ -1213,14 +1208,19 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
 }
 
 // The FoR tape in tile order (once per state and lambda, after k_coefs): the
-// line coefficients of every slot and (dcoef, grad P_ref) of every output.
+// line coefficients (K, a_i, a_j, m) of every slot in the orientation of the
+// slot's bus b: from-end (K, a_i, a_j, m), to-end (K, -a_j, -a_i, m), so that
+// with D = dth_b - dth_o both ends read yth += K D + c2 dv_b + c3 dv_o and
+// yv += c2 D + m dv_o; and (dcoef, grad P_ref) of every output.
 __global__ void k_for_tape(int nslots, int nout, const int2 *slots, const int *out_bus, const double4 *coef,
                            const double *dcoef, const double *refg_th, const double *refg_v, double4 *scoef,
                            double4 *ometa) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < nslots) {
-    const int line = slots[t].x;
-    scoef[t] = line >= 0 ? coef[line] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const int2 sl = slots[t];
+    double4 k = sl.x >= 0 ? coef[sl.x] : make_double4(0.0, 0.0, 0.0, 0.0);
+    if (sl.y & 1) k = make_double4(k.x, -k.z, -k.y, k.w);   // b is the to-end
+    scoef[t] = k;
   } else if (t - nslots < nout) {
     const int o = t - nslots, b = out_bus[o];
     ometa[o] = make_double4(dcoef[b], refg_th[b], refg_v[b], 0.0);
