@@ -334,9 +334,9 @@ def main():
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_val = n_p / t_e2e.item()
 
-    # ---- roofline of the dominant kernel: k_seg, the shared-memory block sweeps
+    # ---- roofline of the dominant kernel: k_blk, the bus-unit block sweeps
     # (4 of the 8 kernels of an Alg. 2 batch).  Algorithmic HBM bytes of one
-    # k_seg launch: read + write of every block row of Z (or P) for the batch,
+    # k_blk launch: read + write of every block row of Z (or P) for the batch,
     # 2 * (n_x - ns) * N * 8 B.  Per-stage device times
     # come from CUDA events the library records around each kernel of a batch.
     peaks = {}
@@ -364,7 +364,7 @@ def main():
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         key = f"{case}:N={N}"
-        if key in prof and prof[key].get("kernel", "").startswith("k_seg"):
+        if key in prof and prof[key].get("kernel", "").startswith("k_blk"):
             traffic = prof[key].get("dram_bytes_per_launch")
     except Exception:
         pass
@@ -394,11 +394,11 @@ def main():
             "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": t_e2e.item() * 1e3},
-            "roofline": {"bound": "hbm", "kernel": "k_seg (block triangular sweeps, 4 of 8 kernels per batch)",
+            "roofline": {"bound": "hbm", "kernel": "k_blk (bus-unit block triangular sweeps, 4 of 8 kernels per batch)",
                          "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": seg_bytes,
-                         "model": "2 (n_x - n_sep) N 8 B per k_seg launch",
+                         "model": "2 (n_x - n_sep) N 8 B per k_blk launch",
                          "launch_ms": float(seg_ms.mean()),
                          "stage_ms": {k: float(v) for k, v in zip(
                              ["A_L", "B_LU", "A_U", "FoR", "A_Ut", "B_UtLt", "A_Lt", "MulAdd", "total"], stage)},
