@@ -219,10 +219,10 @@ def main():
     resid_inf = float(g_res.abs().max().item())
     torch.cuda.synchronize()
 
-    cpad = (n_p + world - 1) // world
-    j0, j1 = min(n_p, rank * cpad), min(n_p, (rank + 1) * cpad)
-    Hloc = torch.zeros((cpad, n_p), dtype=torch.float64, device=dev)       # my columns, transposed layout
-    Hall = torch.zeros((cpad * world, n_p), dtype=torch.float64, device=dev)
+    from paper_2201_00241_b200.parallel import ShardedHessian, gather_columns
+    sh = ShardedHessian(ctx)                 # column shard of SURVEY.md 8(e), transposed slabs
+    j0, j1, cpad = sh.j0, sh.j1, sh.c
+    Hloc, Hall = sh.H_local, sh.H_all
     grad = torch.empty(n_p, dtype=torch.float64, device=dev)
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
@@ -235,12 +235,11 @@ def main():
         ctx.reduced_gradient(grad)
         if timed:
             ev[1].record(stream)
-        if j1 > j0:
-            ctx.hessian_columns(j0, j1, N, H=Hloc, transposed=True)
+        sh.local_columns(N)
         if timed:
             ev[2].record(stream)
         if world > 1:
-            dist.all_gather_into_tensor(Hall, Hloc)
+            gather_columns(Hloc, n_p, out=Hall)   # one NCCL all-gather
         if timed:
             ev[3].record(stream)
 
@@ -313,9 +312,7 @@ def main():
             p.copy_(p_h, non_blocking=True)
             ctx.set_state(x, p)
             ctx.reduced_gradient(grad)
-            if j1 > j0:
-                ctx.hessian_columns(j0, j1, N, H=Hloc, transposed=True)
-            dist.all_gather_into_tensor(Hall, Hloc)
+            sh.full(N)
             g_h.copy_(grad, non_blocking=True)
             H_h.copy_(Hall, non_blocking=True)
             torch.cuda.synchronize()
