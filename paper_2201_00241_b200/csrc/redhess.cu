@@ -211,6 +211,8 @@ __global__ void k_objective(int n_bus, int ref, const int *has_gen, const double
 // depends on Lrow(i), its descendants), so a warp eliminates its subtrees
 // without CTA barriers (warp lanes split every row update; __syncwarp orders
 // the rows of one warp).
+constexpr int kMaxTopsFact = 64;   // tops rows of a block (analysis kMaxTops <= this)
+constexpr int kMaxRowsFact = 1024; // rows of a block (Rmax <= this)
 __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   extern __shared__ double sm[];
   const int s = blockIdx.x;
@@ -226,10 +228,14 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   int *skk = reinterpret_cast<int *>(sks + nks);
   unsigned short *stg = reinterpret_cast<unsigned short *>(skk + nks);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int a = warp; a < nr; a += nw) {
+  // stage the block's F rows: thread per row, 8-byte cp.async copies all in flight
+  for (int a = threadIdx.x; a < nr; a += blockDim.x) {
     const int i = f.row_global[r0 + a];
     const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off, rb = f.F_rowptr[i];
-    for (int t = lane; t < len; t += 32) SF[off + t] = f.F_val[rb + t];
+    for (int t = 0; t < len; ++t) {
+      const unsigned d = (unsigned)__cvta_generic_to_shared(SF + off + t);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(f.F_val + rb + t) : "memory");
+    }
   }
   const int4 *gks = reinterpret_cast<const int4 *>(f.ks4);
   for (int t = threadIdx.x; t < nks; t += blockDim.x) {
@@ -239,6 +245,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     skk[t] = f.ks_k[kb + t];
   }
   for (int t = threadIdx.x; t < ntg; t += blockDim.x) stg[t] = f.tgt16[tb + t];
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   // forward split of the block: lvl[0..nw] = each warp's piece rows, lvl[nw+1..nw+2] = tops
   const int *lv = f.fwd_lvl_ptr + f.fwd_seg_lvl[s];
@@ -272,13 +279,91 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   };
   for (int q = lv[warp]; q < lv[warp + 1]; ++q) eliminate(q);
   __syncthreads();
-  if (warp == 0)
-    for (int q = lv[nw + 1]; q < lv[nw + 2]; ++q) eliminate(q);   // tops: ascending, one warp
+  // tops (rows q in [tq0, tq1), ascending): T1, warp per tops row, applies the
+  // k-steps from piece rows (final now; a piece row is never an ancestor of a
+  // tops row, so these steps commute with the tops' own); T2 is right-looking
+  // over the tops k ascending, one barrier per k: every warp takes the now
+  // final pivot of row k and applies the (i, k) steps of its tops rows i > k.
+  const int tq0 = lv[nw + 1], tq1 = lv[nw + 2], ntq = tq1 - tq0;
+  if (ntq > 0) {
+    __shared__ int s_cur[kMaxTopsFact];     // per tops row: next k-step with k in the tops
+    __shared__ double s_amax[kMaxTopsFact];
+    __shared__ int s_topq[kMaxTopsFact];    // block-local row of every tops row
+    __shared__ int4 s_trow[kMaxTopsFact];   // per tops row: F row (global), smem row offset, pivot offset, k-steps end
+    __shared__ unsigned char s_tflag[kMaxRowsFact];   // tops membership by block-local row
+    for (int a = threadIdx.x; a < nr; a += blockDim.x) s_tflag[a] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntq; t += blockDim.x) {
+      s_topq[t] = f.fwd_order[tq0 + t];
+      s_tflag[s_topq[t]] = 1;
+    }
+    __syncthreads();
+    auto is_top = [&](int kloc) { return s_tflag[kloc] != 0; };
+    auto kstep = [&](double *w, int ks, double dk) {
+      const int4 m = sks[ks];
+      const double lik = w[m.x] * dk;
+      __syncwarp();
+      if (lane == 0) w[m.x] = lik;
+      const double *uk = SF + m.y + 1;
+      const unsigned short *tg = stg + m.w;
+      for (int t = lane; t < m.z; t += 32) w[tg[t]] -= lik * uk[t];
+      __syncwarp();
+    };
+    for (int t = warp; t < ntq; t += nw) {   // T1
+      const int a = s_topq[t];
+      const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off;
+      double *w = SF + off;
+      double amax = 0.0;
+      for (int u = lane; u < len; u += 32) amax = fmax(amax, fabs(w[u]));
+      amax = warp_max(amax);
+      const int k1 = f.ks_ptr[r0 + a + 1] - kb;
+      int first_top = k1;
+      for (int ks = f.ks_ptr[r0 + a] - kb; ks < k1; ++ks) {
+        if (is_top(skk[ks])) {
+          first_top = min(first_top, ks);
+          continue;
+        }
+        kstep(w, ks, sdinv[skk[ks]]);
+      }
+      if (lane == 0) {
+        s_cur[t] = first_top;
+        s_amax[t] = amax;
+        const int i = f.row_global[r0 + a];
+        s_trow[t] = make_int4(i, off, off + (f.F_diag[i] - f.F_rowptr[i]), k1);
+      }
+    }
+    __syncthreads();
+    for (int tk = 0; tk < ntq; ++tk) {   // T2
+      const int ak = s_topq[tk];
+      const int4 rk = s_trow[tk];
+      const int ik = rk.x;
+      const double piv = SF[rk.z];
+      const double dk = 1.0 / piv;
+      if (tk % nw == warp && lane == 0) {
+        sdinv[ak] = dk;
+        f.dinv[ik] = dk;
+        if (!(fabs(piv) > f.pivtol * s_amax[tk])) atomicMax(f.status, ik + 1);
+      }
+      for (int t = tk + 1 + ((warp - (tk + 1) % nw + nw) % nw); t < ntq; t += nw) {
+        // t == tk + 1 + warp (mod nw): rows i > k spread over the warps
+        const int4 rt = s_trow[t];
+        const int k1 = rt.w;
+        int ks = s_cur[t];
+        if (ks < k1 && skk[ks] == ak) {
+          kstep(SF + rt.y, ks, dk);
+          for (++ks; ks < k1 && !is_top(skk[ks]); ++ks) {
+          }
+          if (lane == 0) s_cur[t] = ks;
+        }
+      }
+      __syncthreads();
+    }
+  }
   __syncthreads();
-  for (int a = warp; a < nr; a += nw) {
+  for (int a = threadIdx.x; a < nr; a += blockDim.x) {   // write back: thread per row
     const int i = f.row_global[r0 + a];
     const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off, rb = f.F_rowptr[i];
-    for (int t = lane; t < len; t += 32) f.F_val[rb + t] = SF[off + t];
+    for (int t = 0; t < len; ++t) f.F_val[rb + t] = SF[off + t];
   }
 }
 
@@ -531,60 +616,50 @@ __global__ void k_transpose(const double *__restrict__ A, double *AT, int n) {
 }
 
 // Dense inverses of every block's top diagonal block T x T (once per state):
-// M_L = (L_TT)^-1 (unit lower) and M_U = (U_TT)^-1, written into the sweeps'
-// dense entries: L rows get M_L, U^T rows M_U^T, U rows M_U, L^T rows M_L^T.
-// One CTA per block, one thread per column (forward / backward substitution).
-constexpr int kMaxTops = 64;
-__global__ void __launch_bounds__(kMaxTops) k_tops_inverse(const int *top_ptr, const int *top_fpos_ptr,
-                                                           const int *top_fpos, const int *fwd_pos,
-                                                           const int *bwd_pos, const double *F, double *vL,
-                                                           double *vUt, double *vU, double *vLt) {
-  extern __shared__ double tops_sm[];
-  double(*T)[kMaxTops + 1] = reinterpret_cast<double(*)[kMaxTops + 1]>(tops_sm);  // L_TT below, U_TT on/above
-  double(*ML)[kMaxTops + 1] = T + kMaxTops;
-  double(*MU)[kMaxTops + 1] = ML + kMaxTops;
+// M_L = (L_TT)^-1 (unit lower) and M_U = (U_TT)^-1, written into the unit
+// sweeps' dense tops records: L gets M_L, U^T M_U^T, U M_U, L^T M_L^T.
+// One CTA per block, thread per entry (a, b) of each inverse: column-oriented
+// (right-looking) substitution, one barrier per step:
+//   M_L: for k ascending, M[a][b] -= T[a][k] M[k][b] for a > k (M starts at I);
+//   M_U: for k descending, M[k][b] /= T[k][k], then M[a][b] -= T[a][k] M[k][b] for a < k.
+constexpr int kMaxTops = 32;
+__global__ void __launch_bounds__(kMaxTops * kMaxTops) k_tops_inverse(const int *top_ptr, const int *top_fpos_ptr,
+                                                                     const int *top_fpos, const int *fwd_pos,
+                                                                     const int *bwd_pos, const double *F, double *vL,
+                                                                     double *vUt, double *vU, double *vLt) {
+  __shared__ double T[kMaxTops][kMaxTops + 1];   // L_TT below the diagonal, U_TT on/above
+  __shared__ double ML[kMaxTops][kMaxTops + 1], MU[kMaxTops][kMaxTops + 1];
   const int s = blockIdx.x;
   const int t0 = top_ptr[s], nt = top_ptr[s + 1] - t0;
   if (nt == 0) return;
-  const int *fp = top_fpos + top_fpos_ptr[s];
-  for (int x = threadIdx.x; x < nt * nt; x += blockDim.x) {
-    const int pos = fp[x];
-    T[x / nt][x % nt] = pos >= 0 ? F[pos] : 0.0;
+  const int a = threadIdx.x / kMaxTops, b = threadIdx.x % kMaxTops;
+  const bool in = a < nt && b < nt;
+  if (in) {
+    const int pos = top_fpos[top_fpos_ptr[s] + a * nt + b];
+    T[a][b] = pos >= 0 ? F[pos] : 0.0;
+    ML[a][b] = MU[a][b] = a == b ? 1.0 : 0.0;
   }
   __syncthreads();
-  const int b = threadIdx.x;
-  if (b < nt) {
-    // column b of M_L: unit lower, rows a >= b
-    for (int a = 0; a < nt; ++a) {
-      double v = a == b ? 1.0 : 0.0;
-      if (a > b)
-        for (int k = b; k < a; ++k) v -= T[a][k] * ML[k][b];
-      ML[a][b] = a < b ? 0.0 : v;
-    }
-    // column b of M_U: upper, rows a <= b, backward
-    for (int a = nt - 1; a >= 0; --a) {
-      double v = 0.0;
-      if (a <= b) {
-        v = a == b ? 1.0 : 0.0;
-        for (int k = a + 1; k <= b; ++k) v -= T[a][k] * MU[k][b];
-        v /= T[a][a];
-      }
-      MU[a][b] = v;
-    }
+  for (int k = 0; k < nt; ++k) {   // M_L (unit lower); M_L[a][b] is final for a <= k
+    if (in && a > k) ML[a][b] -= T[a][k] * ML[k][b];
+    __syncthreads();
   }
-  __syncthreads();
-  // dense tops records of the bus-unit sweeps: (a, c) -> double index
-  const int *fp_ = fwd_pos + top_fpos_ptr[s], *bp_ = bwd_pos + top_fpos_ptr[s];
-  for (int x = threadIdx.x; x < nt * nt; x += blockDim.x) {
-    const int a = x / nt, c = x % nt;
-    const int fb = fp_[x], bb = bp_[x];
+  for (int k = nt - 1; k >= 0; --k) {   // M_U (upper): row k is final after its division
+    if (in && a == k) MU[k][b] /= T[k][k];
+    __syncthreads();
+    if (in && a < k) MU[a][b] -= T[a][k] * MU[k][b];
+    __syncthreads();
+  }
+  if (in) {
+    const int x = a * nt + b;
+    const int fb = fwd_pos[top_fpos_ptr[s] + x], bb = bwd_pos[top_fpos_ptr[s] + x];
     if (fb >= 0) {
-      vL[fb] = ML[a][c];
-      vUt[fb] = MU[c][a];
+      vL[fb] = ML[a][b];
+      vUt[fb] = MU[b][a];
     }
     if (bb >= 0) {
-      vU[bb] = MU[a][c];
-      vLt[bb] = ML[c][a];
+      vU[bb] = MU[a][b];
+      vLt[bb] = ML[b][a];
     }
   }
 }
@@ -1692,7 +1767,6 @@ int upload(rh_ctx *c) {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
     };
     allow((const void *)k_fact_blocks);
-    allow((const void *)k_tops_inverse);
     allow((const void *)k_blk);
     allow((const void *)k_sep_inverse);
     allow((const void *)k_for);
@@ -2022,7 +2096,7 @@ int rh_load_grid(rh_ctx *c, const rh_grid *g, int32_t *n_x, int32_t *n_p) {
     const size_t lim = (size_t)kSmemMax;
     fits =
            (size_t)8 * A.sep_rows * sizeof(double) <= lim &&
-           fact_smem_bytes(A) <= lim && blk_smem_fits(A, kSmemSM) &&
+           fact_smem_bytes(A) <= lim && blk_smem_fits(A, kSmemSM) && A.max_seg_rows <= kMaxRowsFact &&
            A.ufwd.max_tunits <= UnitSweep::kMaxTopUnits && A.ubwd.max_tunits <= UnitSweep::kMaxTopUnits;
     if (fits) break;
   }
@@ -2244,7 +2318,7 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
     RH_LAUNCHED(c);
   }
   if (A.max_tops > 0) {
-    k_tops_inverse<<<A.nblk, kMaxTops, 3 * kMaxTops * (kMaxTops + 1) * sizeof(double), st>>>(
+    k_tops_inverse<<<A.nblk, kMaxTops * kMaxTops, 0, st>>>(
         c->top_ptr, c->top_fpos_ptr, c->top_fpos, c->uf_top_pos, c->ub_top_pos, c->F_val,
         reinterpret_cast<double *>(c->uL), reinterpret_cast<double *>(c->uUt), reinterpret_cast<double *>(c->uU),
         reinterpret_cast<double *>(c->uLt));
