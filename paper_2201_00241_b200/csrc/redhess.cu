@@ -411,6 +411,17 @@ __global__ void k_sep_dense(int nslots, const int *__restrict__ src, const int *
   if (t < nslots) S[dpos[t]] = F[src[t]];
 }
 
+// 1/x to ~1 ulp: hardware approximation + two Newton steps (pivot reciprocals
+// on the Gauss-Jordan critical path; static pivots, R15)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Grid-wide barrier of a cooperative launch (all CTAs co-resident): arrival
 // counter + generation word; the last arrival resets the counter and bumps the
 // generation.  `gen` is the generation this CTA waits to leave.
@@ -443,8 +454,8 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
 // which is the block GJ step [D B; C E] -> [D^-1, D^-1 B; -C D^-1, E - C D^-1 B].
 // S' is written to the other buffer (ping-pong), one grid barrier per panel.
 constexpr int GJT = 64;   // output tile
-constexpr size_t gj_smem_bytes() { return sizeof(double) * (GJB * (GJB + 1) + (2 * GJB + GJT) * (GJT + 1)); }
-__global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int ns, const double *rowmax,
+constexpr size_t gj_smem_bytes() { return sizeof(double) * (GJB * (GJB + 1) + (3 * GJB + GJT) * (GJT + 1)); }
+__global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, int ns, const double *rowmax,
                                                      const int *sep_rows, int *status, double pivtol,
                                                      unsigned *bar, long long *dbg) {
   extern __shared__ double gj_sm[];   // dynamic: gj_smem_bytes()
@@ -452,6 +463,7 @@ __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int
   double(*Cs)[GJT + 1] = reinterpret_cast<double(*)[GJT + 1]>(gj_sm + GJB * (GJB + 1));   // C^T: Cs[m][r] = S[i0 + r][K + m]
   double(*Rs)[GJT + 1] = Cs + GJB;                                                     // P, then R
   double(*Ts)[GJT + 1] = Rs + GJB;
+  double(*R2)[GJT + 1] = Ts + GJT;   // R = D^-1 P
   __shared__ unsigned s_gen;
   const int tid = threadIdx.x;
   const int nt = (ns + GJT - 1) / GJT, ntiles = nt * nt;
@@ -522,7 +534,7 @@ __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int
         for (int r = 0; r < 8; ++r) f[r] = __shfl_sync(0xffffffffu, v[r], k);
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const double pk = prow[k & 1][k];
-        const double inv = 1.0 / pk;
+        const double inv = fast_rcp(pk);
         const double rk = j == k ? inv : prow[k & 1][j] * inv;
         if (warp == wk && j == k && k < b && !(fabs(pk) > pivtol * rowmax[sep_rows[K + k]])) bad = true;
 #pragma unroll
@@ -543,25 +555,28 @@ __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int
       if (tile != (int)blockIdx.x) load_tile(Sin, K, b, i0, j0, tid, blockDim.x);
       __syncthreads();   // Ds (first tile), Cs, Rs = P, Ts
       if (prof && tile == (int)blockIdx.x) prof[(K / GJB) * 4 + 1] = clock64();
-      double rr[GJB * GJT / 256];
+      {  // R = D^-1 P (D^-1 itself on panel columns): thread = 4 rows x 2 columns
+        const int cg = tid & 31, rg = tid >> 5;
 #pragma unroll
-      for (int u = 0; u < GJB * GJT / 256; ++u) {
-        const int t = tid + u * 256, m = t / GJT, c = t % GJT;
-        const int gj = j0 + c;
-        double acc = 0.0;
-        if (gj >= K && gj < K + b) {
-          acc = Ds[m][gj - K];
-        } else {
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = cg + 32 * h2, gj = j0 + c;
+          double acc[4];
+          if (gj >= K && gj < K + b) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[v] = Ds[rg + 8 * v][gj - K];
+          } else {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[v] = 0.0;
 #pragma unroll 8
-          for (int l = 0; l < GJB; ++l) acc = fma(Ds[m][l], Rs[l][c], acc);
-        }
-        rr[u] = acc;
-      }
-      __syncthreads();
+            for (int l = 0; l < GJB; ++l) {
+              const double r = Rs[l][c];
 #pragma unroll
-      for (int u = 0; u < GJB * GJT / 256; ++u) {
-        const int t = tid + u * 256;
-        Rs[t / GJT][t % GJT] = rr[u];
+              for (int v = 0; v < 4; ++v) acc[v] = fma(Ds[rg + 8 * v][l], r, acc[v]);
+            }
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) R2[rg + 8 * v][c] = acc[v];
+        }
       }
       __syncthreads();
       const int tx = tid % 16, ty = tid / 16;
@@ -576,7 +591,7 @@ __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int
 #pragma unroll
         for (int u = 0; u < 4; ++u) cv[u] = Cs[m][ty + 16 * u];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) rv[v] = Rs[m][tx + 16 * v];
+        for (int v = 0; v < 4; ++v) rv[v] = R2[m][tx + 16 * v];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -590,7 +605,7 @@ __global__ void __launch_bounds__(256) k_sep_inverse(double *Sa, double *Sb, int
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int gj = j0 + tx + 16 * v;
-          if (gj < ns) __stcg(Sout + (long long)gi * ns + gj, inI ? Rs[gi - K][tx + 16 * v] : acc[u][v]);
+          if (gj < ns) __stcg(Sout + (long long)gi * ns + gj, inI ? R2[gi - K][tx + 16 * v] : acc[u][v]);
         }
       }
       __syncthreads();
