@@ -1181,6 +1181,20 @@ __global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
 }
 
 
+// Single right-hand side (the first-order adjoint): separator rows of P =
+// S^-T t, warp per row, lanes over k (coalesced rows of S^-T), fixed order.
+__global__ void __launch_bounds__(kThreads) k_sep_gemv(SegParams h, int mode) {
+  const int lane = threadIdx.x & 31;
+  const int m = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (m >= h.ns) return;
+  const double *M = (mode == MODE_LU ? h.Sinv : h.SinvT) + (long long)m * h.ns;
+  double *G = mode == MODE_LU ? h.Z : h.P;
+  double acc = 0.0;
+  for (int k = lane; k < h.ns; k += 32) acc = fma(__ldg(M + k), h.Tsep[(long long)k * h.ld], acc);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) G[(long long)(h.sep_off + m) * h.ld] = acc;
+}
+
 // ============================================================================
 // BatchTensorProjection (Eq. so_model)
 // by hand-written forward-over-reverse on the line graph with a hoisted tape:
@@ -2382,7 +2396,7 @@ int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *str
   if (A.sep_rows > 0) {
     k_sep_gather<<<dim3(nblk(A.sep_rows, kThreads / 32), 1), kThreads, 0, st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
-    k_sep_gemm<<<dim3(1, (A.sep_rows + GBM - 1) / GBM), GTHREADS, 0, st>>>(h, MODE_UTLT);
+    k_sep_gemv<<<nblk(A.sep_rows, kThreads / 32), kThreads, 0, st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
   }
   k_blk<<<g1, kBlkThreads, c->smem_blk, st>>>(h, MODE_LT);
