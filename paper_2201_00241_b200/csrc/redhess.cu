@@ -1070,111 +1070,117 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
 }
 
 // C[m][n] = sum_k M[m][k] T[k][n] written to the separator slab of Z / P
-// (rows sep_off + m, contiguous in segment order).  64 x 64 output tile per
-// CTA; in-CTA split-K: 4 groups of 128 threads each sweep a quarter of the k
-// tiles (8 x 4 outputs per thread, k tiles of 16 staged in shared memory with
-// the next tile prefetched into registers), then the partial tiles are added
-// in fixed group order (deterministic).
-constexpr int GBM = 64, GBN = 64, GBK = 8, GGRP = 4, GTHREADS = 128 * GGRP;
+// (rows sep_off + m, contiguous in segment order): the one dense contraction
+// of the path, on the fp64 tensor cores (DMMA, mma.sync m8n8k4).  64 x 64
+// output tile per CTA, 8 warps of 32 x 16 (4 x 2 mma tiles), k in tiles of 16
+// staged in shared memory (double-buffered, next tile prefetched into
+// registers).  Fixed k order: deterministic.
+constexpr int GBM = 64, GBN = 64, GBK = 16, GGRP = 2, GTHREADS = 256 * GGRP;
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+// in-CTA split-K: GGRP groups of 8 warps take alternate k tiles (more DMMA
+// chains in flight per SM); the partial tiles are added in fixed group order
+constexpr size_t gemm_smem_bytes() {
+  return sizeof(double) * GGRP * 2 * (GBM * (GBK + 1) + GBK * (GBN + 1));
+}
 __global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
-  // per group: As [GBK][GBM + 2] (+2: conflict-free transposed stores), Bs [GBK][GBN];
-  // afterwards the reduction tile Red [GBM][GBN] reuses the same space
-  constexpr int kAs = GBK * (GBM + 2), kBs = GBK * GBN, kBuf = GGRP * (kAs + kBs);
-  static_assert(kBuf >= GBM * GBN, "reduction tile fits");
-  __shared__ __align__(16) double gbuf[kBuf];
+  extern __shared__ __align__(16) double gsm[];
+  const int grp = threadIdx.x >> 8;
+  typedef double ATile[GBM][GBK + 1];
+  typedef double BTile[GBK][GBN + 1];
+  ATile *As = reinterpret_cast<ATile *>(gsm + grp * 2 * (GBM * (GBK + 1) + GBK * (GBN + 1)));
+  BTile *Bs = reinterpret_cast<BTile *>(reinterpret_cast<double *>(As) + 2 * GBM * (GBK + 1));
   const int ns = h.ns, ld = h.ld;
   const double *M = mode == MODE_LU ? h.Sinv : h.SinvT;
   double *G = mode == MODE_LU ? h.Z : h.P;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
-  const int grp = threadIdx.x >> 7, tid = threadIdx.x & 127;
-  double(*As)[GBM + 2] = reinterpret_cast<double(*)[GBM + 2]>(gbuf + grp * (kAs + kBs));
-  double(*Bs)[GBN] = reinterpret_cast<double(*)[GBN]>(gbuf + grp * (kAs + kBs) + kAs);
-  double(*Red)[GBN] = reinterpret_cast<double(*)[GBN]>(gbuf);
-  const int tx = tid % 16, ty = tid / 16;  // 16 x 8 threads: n = tx*4.., m = ty*8..
-  const int nkt = (ns + GBK - 1) / GBK;
-  const int kt0 = nkt * grp / GGRP, kt1 = nkt * (grp + 1) / GGRP;   // this group's k tiles
-  double acc[8][4];
+  const int tid = threadIdx.x & 255, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;   // warp tile rows wm*32.., cols wn*16..
+  const int gid = lane >> 2, tig = lane & 3;
+  double acc[4][2][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  constexpr int NL = GBM * GBK / 128;   // loads per thread per array
-  double ra[NL], rb[NL];
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double ra[4], rb[4];
   auto load = [&](int k0) {
 #pragma unroll
-    for (int r = 0; r < NL; ++r) {
-      const int idx = tid + r * 128;                // 512 = 64 (m) x 8 (k)
+    for (int r = 0; r < 4; ++r) {
+      const int idx = tid + r * 256;            // 1024 = 64 (m) x 16 (k), k fastest
       const int mm = idx / GBK, kk = idx % GBK;
-      const int gm = m0 + mm, gk = k0 + kk;
-      ra[r] = (gm < ns && gk < ns) ? __ldg(M + (long long)gm * ns + gk) : 0.0;
-      const int kb = idx / GBN, nn = idx % GBN;    // 512 = 8 (k) x 64 (n)
-      const int gk2 = k0 + kb;
-      rb[r] = (gk2 < ns && n0 + nn < ld) ? h.Tsep[(long long)gk2 * ld + n0 + nn] : 0.0;
+      ra[r] = (m0 + mm < ns && k0 + kk < ns) ? __ldg(M + (long long)(m0 + mm) * ns + k0 + kk) : 0.0;
+      const int kb = idx / GBN, nn = idx % GBN;  // 1024 = 16 (k) x 64 (n), n fastest
+      rb[r] = (k0 + kb < ns && n0 + nn < ld) ? h.Tsep[(long long)(k0 + kb) * ld + n0 + nn] : 0.0;
     }
   };
-  auto store = [&]() {
+  auto store = [&](int buf) {
 #pragma unroll
-    for (int r = 0; r < NL; ++r) {
-      const int idx = tid + r * 128;
-      As[idx % GBK][idx / GBK] = ra[r];
-      Bs[idx / GBN][idx % GBN] = rb[r];
+    for (int r = 0; r < 4; ++r) {
+      const int idx = tid + r * 256;
+      As[buf][idx / GBK][idx % GBK] = ra[r];
+      Bs[buf][idx / GBN][idx % GBN] = rb[r];
     }
   };
-  if (kt0 < kt1) load(kt0 * GBK);
-  for (int kt = kt0; kt < kt1; ++kt) {
-    store();
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-    if (kt + 1 < kt1) load((kt + 1) * GBK);
-#pragma unroll
-    for (int kk = 0; kk < GBK; ++kk) {
-      double a[8], bv[4];
-      const double2 *ap = reinterpret_cast<const double2 *>(&As[kk][ty * 8]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double2 v = ap[i];
-        a[2 * i] = v.x;
-        a[2 * i + 1] = v.y;
-      }
-      const double2 *bp = reinterpret_cast<const double2 *>(&Bs[kk][tx * 4]);
-      const double2 b0 = bp[0], b1 = bp[1];
-      bv[0] = b0.x;
-      bv[1] = b0.y;
-      bv[2] = b1.x;
-      bv[3] = b1.y;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], bv[j], acc[i][j]);
-    }
-    asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+  auto gsync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + grp) : "memory"); };
+  const int kstep = GBK * GGRP;
+  int buf = 0;
+  if (grp * GBK < ns) {
+    load(grp * GBK);
+    store(0);
   }
-  // fixed-order reduction of the group partials: Red = p0; Red += p1; Red += p2; out = Red + p3
+  gsync();
+  for (int k0 = grp * GBK; k0 < ns; k0 += kstep, buf ^= 1) {
+    if (k0 + kstep < ns) load(k0 + kstep);
+    double a[GBK / 4][4], bv[GBK / 4][2];   // all fragments of the k tile, then 32 DMMA
+#pragma unroll
+    for (int q = 0; q < GBK / 4; ++q) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[q][i] = As[buf][wm * 32 + i * 8 + gid][4 * q + tig];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bv[q][j] = Bs[buf][4 * q + tig][wn * 16 + j * 8 + gid];
+    }
+#pragma unroll
+    for (int q = 0; q < GBK / 4; ++q)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[q][i], bv[q][j]);
+    if (k0 + kstep < ns) store(buf ^ 1);
+    gsync();
+  }
+  // fixed-order reduction: group 1 parks its partial tile, group 0 adds and stores
   __syncthreads();
-  for (int g = 0; g < GGRP - 1; ++g) {
-    if (grp == g) {
+  double(*Red)[GBN + 2] = reinterpret_cast<double(*)[GBN + 2]>(gsm);
+  if (grp == 1) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) Red[ty * 8 + i][tx * 4 + j] = g == 0 ? acc[i][j] : Red[ty * 8 + i][tx * 4 + j] + acc[i][j];
-    }
-    __syncthreads();
+      for (int j = 0; j < 2; ++j) {
+        const int r = wm * 32 + i * 8 + gid, c = wn * 16 + j * 8 + 2 * tig;
+        Red[r][c] = acc[i][j][0];
+        Red[r][c + 1] = acc[i][j][1];
+      }
   }
-  if (grp == GGRP - 1) {
+  __syncthreads();
+  if (grp == 0) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int gm = m0 + ty * 8 + i;
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + wm * 32 + i * 8 + gid;
       if (gm >= ns) continue;
-      double o[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) o[j] = Red[ty * 8 + i][tx * 4 + j] + acc[i][j];
-      double *out = G + (long long)(h.sep_off + gm) * ld + n0 + tx * 4;
-      if (n0 + tx * 4 + 3 < ld) {
-        reinterpret_cast<double2 *>(out)[0] = make_double2(o[0], o[1]);
-        reinterpret_cast<double2 *>(out)[1] = make_double2(o[2], o[3]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (n0 + tx * 4 + j < ld) out[j] = o[j];
+      for (int j = 0; j < 2; ++j) {
+        const int r = wm * 32 + i * 8 + gid, c = wn * 16 + j * 8 + 2 * tig;
+        const int gn = n0 + c;
+        const double o0 = acc[i][j][0] + Red[r][c], o1 = acc[i][j][1] + Red[r][c + 1];
+        double *out = G + (long long)(h.sep_off + gm) * ld + gn;
+        if (gn + 1 < ld) {
+          *reinterpret_cast<double2 *>(out) = make_double2(o0, o1);
+        } else if (gn < ld) {
+          out[0] = o0;
+        }
       }
     }
   }
@@ -1799,6 +1805,7 @@ int upload(rh_ctx *c) {
     allow((const void *)k_blk);
     allow((const void *)k_sep_inverse);
     allow((const void *)k_for);
+    allow((const void *)k_sep_gemm);
     cudaGetLastError();
   }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
@@ -2004,7 +2011,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   if (has_sep) {
     k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_LU);
     RH_LAUNCHED(c);
-    k_sep_gemm<<<gSm, GTHREADS, 0, st>>>(h, MODE_LU);
+    k_sep_gemm<<<gSm, GTHREADS, gemm_smem_bytes(), st>>>(h, MODE_LU);
     RH_LAUNCHED(c);
   }
   mark(2);
@@ -2037,7 +2044,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   if (has_sep) {
     k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
-    k_sep_gemm<<<gSm, GTHREADS, 0, st>>>(h, MODE_UTLT);
+    k_sep_gemm<<<gSm, GTHREADS, gemm_smem_bytes(), st>>>(h, MODE_UTLT);
     RH_LAUNCHED(c);
   }
   mark(6);
