@@ -273,7 +273,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         rec(fwd ? -1 : inv(f), (!fwd && two) ? inv(sr) : -1, fwd ? inv(f) : -1, (fwd && two) ? inv(sr) : -1);
         if (two) rec(coef(false, sr, f), -1, coef(true, sr, f), -1);
       }
-      const int nd = (int)du.size(), nchunk = (nd + 3) / 4;
+      const int nd = (int)du.size(), nchunk = std::max(1, (nd + 3) / 4);   // >= 1 chunk (straight-line chunk 0)
       const int rowb = UnitSweep::kCols * 8;
       for (int di = 0; di < 4 * nchunk; ++di) {
         if (di >= nd) {   // padding: zero coefficients on the unit's own (finite) row

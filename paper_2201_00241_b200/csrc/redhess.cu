@@ -758,27 +758,38 @@ __device__ __forceinline__ double lds(const char *p) { return *reinterpret_cast<
 // dependencies (tile-row byte offsets o0, o1; records (c_f0, c_f1) [, (c_s0,
 // c_s1)]).  Branch-free, two-deep FMA chains, fixed order (deterministic).
 template <bool TWO>
+__device__ __forceinline__ void dep_chunk(const double2 *__restrict__ rc, const int4 *__restrict__ of, const char *Xb,
+                                          double &f0, double &f1, double &f2, double &f3, double &s0, double &s1,
+                                          double &s2, double &s3) {
+  const int4 a = of[0], b = of[1];
+  const double x00 = lds(Xb + a.x), x01 = lds(Xb + a.y), x10 = lds(Xb + a.z), x11 = lds(Xb + a.w);
+  const double x20 = lds(Xb + b.x), x21 = lds(Xb + b.y), x30 = lds(Xb + b.z), x31 = lds(Xb + b.w);
+  if (TWO) {
+    const double2 p0 = rc[0], q0 = rc[1], p1 = rc[2], q1 = rc[3], p2 = rc[4], q2 = rc[5], p3 = rc[6], q3 = rc[7];
+    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1); s0 = fma(q0.x, x00, s0); s1 = fma(q0.y, x01, s1);
+    f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3); s2 = fma(q1.x, x10, s2); s3 = fma(q1.y, x11, s3);
+    f0 = fma(p2.x, x20, f0); f1 = fma(p2.y, x21, f1); s0 = fma(q2.x, x20, s0); s1 = fma(q2.y, x21, s1);
+    f2 = fma(p3.x, x30, f2); f3 = fma(p3.y, x31, f3); s2 = fma(q3.x, x30, s2); s3 = fma(q3.y, x31, s3);
+  } else {
+    const double2 p0 = rc[0], p1 = rc[1], p2 = rc[2], p3 = rc[3];
+    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1);
+    f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3);
+    f0 = fma(p2.x, x20, f0); f1 = fma(p2.y, x21, f1);
+    f2 = fma(p3.x, x30, f2); f3 = fma(p3.y, x31, f3);
+  }
+}
+
+// sf = sum c_f x, ss = sum c_s x over a dependency list of `nch` >= 1 chunks
+// of 4 dependencies (tile-row byte offsets o0, o1; records (c_f0, c_f1) [,
+// (c_s0, c_s1)]).  Chunk 0 straight-line, the rest rolled: most units have one.
+// Branch-free, two-deep FMA chains, fixed order (deterministic).
+template <bool TWO>
 __device__ __forceinline__ void dep_sums(const double2 *__restrict__ rc, const int4 *__restrict__ of, int nch,
                                          const char *Xb, double &sf, double &ss) {
   double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  for (int c = 0; c < nch; ++c, of += 2, rc += TWO ? 8 : 4) {
-    const int4 a = of[0], b = of[1];
-    const double x00 = lds(Xb + a.x), x01 = lds(Xb + a.y), x10 = lds(Xb + a.z), x11 = lds(Xb + a.w);
-    const double x20 = lds(Xb + b.x), x21 = lds(Xb + b.y), x30 = lds(Xb + b.z), x31 = lds(Xb + b.w);
-    if (TWO) {
-      const double2 p0 = rc[0], q0 = rc[1], p1 = rc[2], q1 = rc[3], p2 = rc[4], q2 = rc[5], p3 = rc[6], q3 = rc[7];
-      f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1); s0 = fma(q0.x, x00, s0); s1 = fma(q0.y, x01, s1);
-      f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3); s2 = fma(q1.x, x10, s2); s3 = fma(q1.y, x11, s3);
-      f0 = fma(p2.x, x20, f0); f1 = fma(p2.y, x21, f1); s0 = fma(q2.x, x20, s0); s1 = fma(q2.y, x21, s1);
-      f2 = fma(p3.x, x30, f2); f3 = fma(p3.y, x31, f3); s2 = fma(q3.x, x30, s2); s3 = fma(q3.y, x31, s3);
-    } else {
-      const double2 p0 = rc[0], p1 = rc[1], p2 = rc[2], p3 = rc[3];
-      f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1);
-      f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3);
-      f0 = fma(p2.x, x20, f0); f1 = fma(p2.y, x21, f1);
-      f2 = fma(p3.x, x30, f2); f3 = fma(p3.y, x31, f3);
-    }
-  }
+  dep_chunk<TWO>(rc, of, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
+#pragma unroll 1
+  for (int c = 1; c < nch; ++c) dep_chunk<TWO>(rc + c * (TWO ? 8 : 4), of + 2 * c, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
   sf = (f0 + f1) + (f2 + f3);
   ss = (s0 + s1) + (s2 + s3);
 }
@@ -813,6 +824,7 @@ template <bool DINV>
 __device__ __forceinline__ void unit_pieces(const UStage &t, char *Xb, int warp) {
   const int q0 = t.lvl[warp], q1 = t.lvl[warp + 1];
   int4 m = q0 < q1 ? t.meta[q0] : make_int4(0, 0, 0, 0);
+#pragma unroll 1
   for (int u = q0; u < q1; ++u) {
     const int4 mn = u + 1 < q1 ? t.meta[u + 1] : m;
     unit_solve<DINV>(t, m, Xb);
@@ -911,6 +923,9 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
                    smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(mbar))
                : "memory");
 }
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
                "r"(bytes)
@@ -967,7 +982,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     const int ob = U.doff_off[s], nof = U.doff_off[s + 1] - ob;
     const int nxrows = mode == MODE_L ? 0 : nr + nxr;
     if (tid == 0) {
-      const unsigned tx = 16u * (nu + ntu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + (unsigned)kRowB * nxrows;
+      const unsigned tx = 16u * (nu + ntu + nrec) + 4u * nof + 4u * UnitSweep::kLvl;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx)
                    : "memory");
       bulk_g2s(smraw + h.smem_meta_off, U.meta + ub, 16u * nu, &mbar);
@@ -976,15 +991,19 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
       if (nof) bulk_g2s(smraw + h.smem_doff_off, U.doff + ob, 4u * nof, &mbar);
       bulk_g2s(smraw + h.smem_lvl_off, U.lvl + s * UnitSweep::kLvl, 4u * UnitSweep::kLvl, &mbar);
     }
-    for (int a = tid; a < nxrows; a += blockDim.x) {
-      const long long grow = a < nr ? r0 + a : U.ext_rows[x0 + a - nr];
-      bulk_g2s(X + a * kBC, G + grow * h.ld + col0, kRowB, &mbar);
+    {  // X rows: 16-byte cp.async (LSU path; 256 B TMA bulk copies are rate-bound on the TMA unit)
+      const int c = tid & 15;
+      for (int a = tid >> 4; a < nxrows; a += blockDim.x >> 4) {
+        const long long grow = a < nr ? r0 + a : U.ext_rows[x0 + a - nr];
+        cp_async16(X + a * kBC + 2 * c, G + grow * h.ld + col0 + 2 * c);
+      }
     }
     if (mode == MODE_L) {   // right-hand side -G_p W (SpMul fused)
       for (int i = tid; i < nr * (kBC / 2); i += blockDim.x) reinterpret_cast<double2 *>(X)[i] = make_double2(0.0, 0.0);
       __syncthreads();
       tile_rhs_gpw(h, s, col0, X, lane, warp, UnitSweep::kWarps);
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     {  // wait for the copies of this tile
       unsigned done = 0;
       while (!done)
@@ -1991,7 +2010,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   h.transposed = transposed;
   const int nb = A.nblk;
   const bool has_sep = A.sep_rows > 0;
-  const int gA = (int)std::min<long long>(2LL * c->nsm, (long long)nb * (ld / kBC));
+  const int gA = (int)std::min<long long>(((h.debug & 64) ? 1LL : 2LL) * c->nsm, (long long)nb * (ld / kBC));   // debug 64: 1 CTA/SM (experiment)
   const dim3 gSg(nblk(A.sep_rows, kThreads / 32), ld / 32),
       gSm((ld + GBN - 1) / GBN, (A.sep_rows + GBM - 1) / GBM);
   const int nch32 = ld / 32, fch = (nch32 + FCH - 1) / FCH;
