@@ -184,7 +184,6 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
   U.tmeta_off.assign(1, 0);
   U.rec_off.assign(1, 0);
   U.doff_off.assign(1, 0);
-  U.top_pos_off.assign(1, 0);
   auto deps = [&](int i) -> const std::vector<int32_t> & { return fwd ? Lrow[i] : Ls[i]; };
   auto coef = [&](bool b, int i, int k) -> int {   // src code of the coefficient (row i, dep k)
     const auto &d = deps(i);
@@ -226,6 +225,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
     const int tu1 = (int)units.size();
     lvl.push_back(tu0);
     lvl.push_back(tu1);
+    lvl.push_back((int)B.tops.size());   // tops rows
     while ((int)lvl.size() < UnitSweep::kLvl) lvl.push_back(0);
     U.lvl.insert(U.lvl.end(), lvl.begin(), lvl.end());
     const int rec0 = (int)U.src_a.size() / 2, off0 = (int)U.doff.size();
@@ -285,7 +285,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         }
         const int k0 = du[di].first, nv = du[di].second, k1 = nv == 2 ? k0 + 1 : -1;
         U.doff.push_back(tile_row(k0) * rowb);
-        U.doff.push_back(tile_row(nv == 2 ? k1 : k0) * rowb);
+        U.doff.push_back(tile_row(nv == 2 ? k1 : k0) * rowb);   // one-value dependency: its row again, zero coefficient
         const size_t at = U.src_a.size();
         auto cf = [&](bool b, int i, int k) { return k < 0 ? -1 : coef(b, i, k); };
         rec(cf(false, u[0], k0), cf(false, u[0], k1), cf(true, u[0], k0), cf(true, u[0], k1));
@@ -301,29 +301,17 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
       return std::array<int, 4>{A.loc_of[u[0]] | ((two ? A.loc_of[u[1]] : 0) << 16), cbeg, obeg,
                                 nchunk | ((two ? 1 : 0) << 16)};
     };
-    const int nt = (int)B.tops.size();
-    std::vector<int32_t> tpos((size_t)nt * nt, -1);
-    std::vector<int> tops_sorted(B.tops.begin(), B.tops.end());
     for (int ui = 0; ui < (int)units.size(); ++ui) {
       const auto &u = units[ui];
       const bool is_top = ui >= tu0;
       const auto m = emit(u, dep_units(u, false, is_top), !is_top, nullptr, nullptr);
       U.meta.insert(U.meta.end(), m.begin(), m.end());
     }
-    for (int ui = tu0; ui < tu1; ++ui) {   // dense lists of the tops: every top unit
-      const auto &u = units[ui];
-      std::vector<std::pair<int, int>> du;
-      for (int vi = tu0; vi < tu1; ++vi) {
-        const auto &v = units[vi];
-        const int lo = std::min(v.front(), v.back());
-        du.push_back({lo, (int)v.size()});
-      }
-      const auto m = emit(u, du, false, &tops_sorted, &tpos);
-      U.tmeta.insert(U.tmeta.end(), m.begin(), m.end());
+    {  // tops (dense product on the fp64 tensor cores): tile rows of the block's tops, ascending
+      const std::vector<int32_t> &T = B.tops;
+      for (int a = 0; a < UnitSweep::kTopRows; ++a)
+        U.top_rows.push_back(T.empty() ? 0 : A.loc_of[T[a < (int)T.size() ? a : 0]]);
     }
-    // double positions were recorded relative to the global record array
-    U.top_pos.insert(U.top_pos.end(), tpos.begin(), tpos.end());
-    U.top_pos_off.push_back((int)U.top_pos.size());
     U.unit_off.push_back((int)(U.meta.size() / 4));
     U.tmeta_off.push_back((int)(U.tmeta.size() / 4));
     U.rec_off.push_back((int)U.src_a.size() / 2);
@@ -368,11 +356,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
       wf_piece += nchk * (16 + (two ? 8 : 4) + 2) + (two ? 2 : 1) + 4 * (two ? 2 : 1) + 1;
       deps += 4 * nchk;
     }
-    for (size_t u = 0; u < U.tmeta.size() / 4; ++u) {
-      const int *m = U.tmeta.data() + 4 * u;
-      const int nchk = m[3] & 0xffff, two = m[3] >> 16;
-      wf_tops += nchk * (16 + (two ? 8 : 4) + 2) + 2 * (two ? 2 : 1);
-    }
+    wf_tops = 16 * 2 * 8 * 4;   // DMMA: 16 output tiles x 8 k-steps x (A + B fragments)
     for (size_t i = 0; i < U.doff.size(); i += 2) real += U.doff[i] != U.doff[i + 1] || true;
     fprintf(stderr, "  smem wavefronts per tile: units+gather %lld, tops dense %lld; dep slots %lld\n",
             wf_piece / std::max(nb, 1), wf_tops / std::max(nb, 1), deps / std::max(nb, 1));

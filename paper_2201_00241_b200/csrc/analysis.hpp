@@ -76,16 +76,16 @@ struct UnitSweep {
   // (two-row unit) double2 coefficient records (c_f0, c_f1), (c_s0, c_s1);
   // lists are padded to chunks of 4 dependencies.
   std::vector<int32_t> meta;
-  std::vector<int32_t> tmeta;        // tops units only (same format): the dense list
+  std::vector<int32_t> tmeta;        // (unused: the tops' dense product runs on DMMA, see top_rows)
   std::vector<int32_t> tmeta_off;    // [nblk + 1] into tmeta (units)
+  static constexpr int kTopRows = 32;   // tops rows of a block (dense 32 x 32 product)
+  std::vector<int32_t> top_rows;     // [nblk * kTopRows] tile rows of the tops, ascending (padded with the first)
   std::vector<int32_t> rec_off;      // [nblk + 1] double2 records
   // per record double: F position (>= 0), -1 zero, <= -2: 1 / F[-s - 2];
   // a: first sweep of the pattern (fwd L, bwd U), b: second (fwd U^T, bwd L^T)
   std::vector<int32_t> src_a, src_b;
   std::vector<int32_t> doff_off;     // [nblk + 1]
   std::vector<int32_t> doff;         // (o0, o1) byte offsets of a dependency's tile rows
-  std::vector<int32_t> top_pos;      // per block nt x nt: double index of M(a, c) (tops ascending)
-  std::vector<int32_t> top_pos_off;  // [nblk + 1]
   std::vector<int32_t> cost;         // [nblk] per-tile cost estimate (scheduling weight)
   int max_units = 0, max_tunits = 0, max_rec = 0, max_doff = 0, max_rows = 0;
 };

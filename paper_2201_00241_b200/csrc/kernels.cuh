@@ -30,7 +30,7 @@ struct DSeg {
 // Bus-unit schedule of one pattern direction (analysis.hpp UnitSweep).
 struct DUnit {
   const int4 *__restrict__ meta;     // per unit
-  const int4 *__restrict__ tmeta;    // per tops unit: dense list
+  const int *__restrict__ top_rows;  // [nblk][32] tile rows of the tops (ascending, padded)
   const int *__restrict__ unit_off, *__restrict__ tmeta_off, *__restrict__ lvl, *__restrict__ rec_off;
   const int *__restrict__ doff_off, *__restrict__ doff;
   const int *__restrict__ blk_order;  // blocks by decreasing cost (tile tickets are block-major in this order)
@@ -42,9 +42,10 @@ struct SegParams {
   int nblk;                          // segment nblk = separator
   DUnit uf, ub;                      // bus-unit block sweeps: fwd (L, U^T), bwd (U, L^T)
   const double2 *uL, *uUt, *uU, *uLt;  // their record values (per state)
+  const double *tL, *tUt, *tU, *tLt;   // [nblk][32][36] dense tops inverses per sweep (k_tops_inverse)
   int maxrx;                         // max tile rows (block rows + staged separator rows)
   int smem_stride;                   // bytes per buffer (two buffers: current tile, prefetched tile)
-  int smem_x_off, smem_meta_off, smem_tmeta_off, smem_rec_off, smem_doff_off, smem_lvl_off;  // bytes
+  int smem_x_off, smem_meta_off, smem_tmeta_off, smem_rec_off, smem_doff_off, smem_lvl_off;  // bytes (tmeta: tops M + rows)
   int *blk_ctr;                      // [2 per mode] tile ticket counter, CTAs done (self-resetting)
   const int *seg_row_off, *row_global;
   DSeg fwd, bwd;

@@ -631,28 +631,28 @@ __global__ void k_transpose(const double *__restrict__ A, double *AT, int n) {
 }
 
 // Dense inverses of every block's top diagonal block T x T (once per state):
-// M_L = (L_TT)^-1 (unit lower) and M_U = (U_TT)^-1, written into the unit
-// sweeps' dense tops records: L gets M_L, U^T M_U^T, U M_U, L^T M_L^T.
-// One CTA per block, thread per entry (a, b) of each inverse: column-oriented
-// (right-looking) substitution, one barrier per step:
+// M_L = (L_TT)^-1 (unit lower) and M_U = (U_TT)^-1, written as dense 32 x 32
+// blocks (row stride kTopLd, zero beyond T) for the tops' DMMA product in
+// k_blk: L gets M_L, U^T M_U^T, U M_U, L^T M_L^T.  One CTA per block, thread per
+// entry (a, b) of each inverse: column-oriented (right-looking) substitution,
+// one barrier per step:
 //   M_L: for k ascending, M[a][b] -= T[a][k] M[k][b] for a > k (M starts at I);
 //   M_U: for k descending, M[k][b] /= T[k][k], then M[a][b] -= T[a][k] M[k][b] for a < k.
 constexpr int kMaxTops = 32;
+constexpr int kTopLd = 36;   // row stride (doubles) of a block's dense tops inverse: conflict-free DMMA A fragments
 __global__ void __launch_bounds__(kMaxTops * kMaxTops) k_tops_inverse(const int *top_ptr, const int *top_fpos_ptr,
-                                                                     const int *top_fpos, const int *fwd_pos,
-                                                                     const int *bwd_pos, const double *F, double *vL,
-                                                                     double *vUt, double *vU, double *vLt) {
+                                                                     const int *top_fpos, const double *F, double *dL,
+                                                                     double *dUt, double *dU, double *dLt) {
   __shared__ double T[kMaxTops][kMaxTops + 1];   // L_TT below the diagonal, U_TT on/above
   __shared__ double ML[kMaxTops][kMaxTops + 1], MU[kMaxTops][kMaxTops + 1];
   const int s = blockIdx.x;
   const int t0 = top_ptr[s], nt = top_ptr[s + 1] - t0;
-  if (nt == 0) return;
   const int a = threadIdx.x / kMaxTops, b = threadIdx.x % kMaxTops;
   const bool in = a < nt && b < nt;
+  ML[a][b] = MU[a][b] = a == b && a < nt ? 1.0 : 0.0;
   if (in) {
     const int pos = top_fpos[top_fpos_ptr[s] + a * nt + b];
     T[a][b] = pos >= 0 ? F[pos] : 0.0;
-    ML[a][b] = MU[a][b] = a == b ? 1.0 : 0.0;
   }
   __syncthreads();
   for (int k = 0; k < nt; ++k) {   // M_L (unit lower); M_L[a][b] is final for a <= k
@@ -665,18 +665,11 @@ __global__ void __launch_bounds__(kMaxTops * kMaxTops) k_tops_inverse(const int 
     if (in && a < k) MU[a][b] -= T[a][k] * MU[k][b];
     __syncthreads();
   }
-  if (in) {
-    const int x = a * nt + b;
-    const int fb = fwd_pos[top_fpos_ptr[s] + x], bb = bwd_pos[top_fpos_ptr[s] + x];
-    if (fb >= 0) {
-      vL[fb] = ML[a][b];
-      vUt[fb] = MU[b][a];
-    }
-    if (bb >= 0) {
-      vU[bb] = MU[a][b];
-      vLt[bb] = ML[b][a];
-    }
-  }
+  const size_t o = (size_t)s * 32 * kTopLd + a * kTopLd + b;
+  dL[o] = ML[a][b];
+  dUt[o] = MU[b][a];
+  dU[o] = MU[a][b];
+  dLt[o] = ML[b][a];
 }
 
 // copy factor values into the sweep value arrays (entry order of the sweeps)
@@ -746,7 +739,9 @@ constexpr int kBC = UnitSweep::kCols;   // columns per tile: one per lane
 constexpr int kRowB = kBC * 8;           // bytes per tile row
 
 struct UStage {
-  const int4 *meta, *tmeta;
+  const int4 *meta;
+  const double *topM;    // [32][kTopLd] dense tops inverse of this sweep
+  const int *toprow;     // [32] tile rows of the tops
   const double2 *rec;
   const int4 *doff;
   const int *lvl;
@@ -837,11 +832,16 @@ __device__ __forceinline__ void unit_pieces(const UStage &t, char *Xb, int warp)
 constexpr int kBlkThreads = UnitSweep::kWarps * 32;
 constexpr int kTopsLvl = UnitSweep::kWarps + 1;   // lvl[kWarps + 1], lvl[kWarps + 2]: tops units
 static_assert(UnitSweep::kMaxTopUnits <= 2 * UnitSweep::kWarps, "two tops units per warp at most");
-__device__ __forceinline__ void unit_tops(const UStage &t, char *Xb, int warp) {
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void unit_tops(const UStage &t, char *Xb, const double *X, int warp, int lane) {
   const int u0 = t.lvl[kTopsLvl], u1 = t.lvl[kTopsLvl + 1];
   if (u0 >= u1) return;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 2; ++k) {   // gather: t_T = X_T - (dependencies outside the tops)
     const int u = u0 + warp + k * UnitSweep::kWarps;
     if (u < u1) {
       const int4 m = t.meta[u];
@@ -858,29 +858,24 @@ __device__ __forceinline__ void unit_tops(const UStage &t, char *Xb, int warp) {
     }
   }
   __syncthreads();
-  double of_[2], os_[2];
-  int4 mm[2];
+  // X_T = M t_T: 32 x 32 (tops rows x tile columns) on the fp64 tensor cores;
+  // warp = one 8-row tile x two 8-column tiles, k in steps of 4 (8 DMMA each)
+  const int gid = lane >> 2, tig = lane & 3, mt = warp >> 1, nb = (warp & 1) * 2;
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int u = u0 + warp + k * UnitSweep::kWarps;
-    of_[k] = os_[k] = 0.0;
-    mm[k] = make_int4(0, 0, 0, 0);
-    if (u < u1) {
-      mm[k] = t.meta[u];
-      const int4 d = t.tmeta[u - u0];
-      if (d.w >> 16)
-        dep_sums<true>(t.rec + d.y, t.doff + (d.z >> 2), d.w & 0xffff, Xb, of_[k], os_[k]);
-      else
-        dep_sums<false>(t.rec + d.y, t.doff + (d.z >> 2), d.w & 0xffff, Xb, of_[k], os_[k]);
-    }
+  for (int k = 0; k < UnitSweep::kTopRows / 4; ++k) {
+    const double a = t.topM[(mt * 8 + gid) * kTopLd + k * 4 + tig];
+    const int br = t.toprow[k * 4 + tig] * kBC;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) dmma_8x8x4(c[j][0], c[j][1], a, X[br + (nb + j) * 8 + gid]);
   }
   __syncthreads();
+  const int nt = t.lvl[kTopsLvl + 2];   // tops rows
+  if (mt * 8 + gid < nt) {
+    double *xr = const_cast<double *>(X) + t.toprow[mt * 8 + gid] * kBC;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    if (u0 + warp + k * UnitSweep::kWarps < u1) {
-      *reinterpret_cast<double *>(Xb + (mm[k].x & 0xffff) * kRowB) = of_[k];
-      if (mm[k].w >> 16) *reinterpret_cast<double *>(Xb + (mm[k].x >> 16) * kRowB) = os_[k];
-    }
+    for (int j = 0; j < 2; ++j)
+      *reinterpret_cast<double2 *>(xr + (nb + j) * 8 + 2 * tig) = make_double2(c[j][0], c[j][1]);
   }
   __syncthreads();
 }
@@ -954,7 +949,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
   double *X = reinterpret_cast<double *>(smraw + h.smem_x_off);
   UStage st;
   st.meta = reinterpret_cast<const int4 *>(smraw + h.smem_meta_off);
-  st.tmeta = reinterpret_cast<const int4 *>(smraw + h.smem_tmeta_off);
+  st.topM = reinterpret_cast<const double *>(smraw + h.smem_tmeta_off);
+  st.toprow = reinterpret_cast<const int *>(smraw + h.smem_tmeta_off + 32 * kTopLd * 8);
   st.rec = reinterpret_cast<const double2 *>(smraw + h.smem_rec_off);
   st.doff = reinterpret_cast<const int4 *>(smraw + h.smem_doff_off);
   st.lvl = reinterpret_cast<const int *>(smraw + h.smem_lvl_off);
@@ -977,16 +973,17 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     const int r0 = h.seg_row_off[s], nr = h.seg_row_off[s + 1] - r0;
     const int x0 = U.ext_off[s], nxr = mode == MODE_L ? 0 : U.ext_off[s + 1] - x0;
     const int ub = U.unit_off[s], nu = U.unit_off[s + 1] - ub;
-    const int tb = U.tmeta_off[s], ntu = U.tmeta_off[s + 1] - tb;
     const int rb = U.rec_off[s], nrec = U.rec_off[s + 1] - rb;
     const int ob = U.doff_off[s], nof = U.doff_off[s + 1] - ob;
     const int nxrows = mode == MODE_L ? 0 : nr + nxr;
     if (tid == 0) {
-      const unsigned tx = 16u * (nu + ntu + nrec) + 4u * nof + 4u * UnitSweep::kLvl;
+      const double *dM = mode == MODE_L ? h.tL : mode == MODE_U ? h.tU : mode == MODE_UT ? h.tUt : h.tLt;
+      const unsigned tx = 16u * (nu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + 32u * kTopLd * 8 + 128u;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx)
                    : "memory");
       bulk_g2s(smraw + h.smem_meta_off, U.meta + ub, 16u * nu, &mbar);
-      if (ntu) bulk_g2s(smraw + h.smem_tmeta_off, U.tmeta + tb, 16u * ntu, &mbar);
+      bulk_g2s(smraw + h.smem_tmeta_off, dM + (size_t)s * 32 * kTopLd, 32u * kTopLd * 8, &mbar);
+      bulk_g2s(smraw + h.smem_tmeta_off + 32 * kTopLd * 8, U.top_rows + s * 32, 128u, &mbar);
       bulk_g2s(smraw + h.smem_rec_off, vals + rb, 16u * nrec, &mbar);
       if (nof) bulk_g2s(smraw + h.smem_doff_off, U.doff + ob, 4u * nof, &mbar);
       bulk_g2s(smraw + h.smem_lvl_off, U.lvl + s * UnitSweep::kLvl, 4u * UnitSweep::kLvl, &mbar);
@@ -1018,9 +1015,9 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     if (fwd) {
       if (dinv) unit_pieces<true>(st, Xb, warp); else unit_pieces<false>(st, Xb, warp);
       __syncthreads();
-      unit_tops(st, Xb, warp);
+      unit_tops(st, Xb, X, warp, lane);
     } else {
-      unit_tops(st, Xb, warp);
+      unit_tops(st, Xb, X, warp, lane);
       const long long c_c = prof ? clock64() : 0;
       if (dinv) unit_pieces<true>(st, Xb, warp); else unit_pieces<false>(st, Xb, warp);
       if (prof && lane == 0) {
@@ -1095,11 +1092,6 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
 // staged in shared memory (double-buffered, next tile prefetched into
 // registers).  Fixed k order: deterministic.
 constexpr int GBM = 64, GBN = 64, GBK = 16, GGRP = 2, GTHREADS = 256 * GGRP;
-__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 // in-CTA split-K: GGRP groups of 8 warps take alternate k tiles (more DMMA
 // chains in flight per SM); the partial tiles are added in fixed group order
 constexpr size_t gemm_smem_bytes() {
@@ -1538,7 +1530,8 @@ struct rh_ctx {
   DUnit duf{}, dub{};
   double2 *uL = nullptr, *uUt = nullptr, *uU = nullptr, *uLt = nullptr;
   int nrec_f = 0, nrec_b = 0;
-  int *uf_src_a, *uf_src_b, *ub_src_a, *ub_src_b, *uf_top_pos, *ub_top_pos;
+  int *uf_src_a, *uf_src_b, *ub_src_a, *ub_src_b;
+  double *tL = nullptr, *tUt = nullptr, *tU = nullptr, *tLt = nullptr;   // dense tops inverses
   int maxrx = 0, nsm = 148;
   int smem_x_off = 0, smem_meta_off = 0, smem_tmeta_off = 0, smem_rec_off = 0, smem_doff_off = 0, smem_lvl_off = 0;
   int smem_stride = 0;
@@ -1608,7 +1601,7 @@ size_t blk_smem_layout(const Analysis &A, int *off7) {
   off7[1] = (int)off;
   off += al((size_t)std::max(A.ufwd.max_units, A.ubwd.max_units) * 16);
   off7[2] = (int)off;
-  off += al((size_t)std::max(A.ufwd.max_tunits, A.ubwd.max_tunits) * 16);
+  off += al((size_t)32 * kTopLd * 8 + 128);   // dense tops inverse + tops rows
   off7[3] = (int)off;
   off += al((size_t)std::max(A.ufwd.max_rec, A.ubwd.max_rec) * 16);
   off7[4] = (int)off;
@@ -1688,9 +1681,8 @@ int upload(rh_ctx *c) {
   mkseg(c->dbwd, A.bwd);
   auto mkunit = [&](DUnit &D, const UnitSweep &U, const DSeg &S) {
     D.meta = reinterpret_cast<const int4 *>(dalloc_copy(U.meta, P));
-    D.tmeta = reinterpret_cast<const int4 *>(dalloc_copy(U.tmeta, P));
     chk(D.meta);
-    chk(D.tmeta);
+    chk(D.top_rows = dalloc_copy(U.top_rows, P));
     chk(D.unit_off = dalloc_copy(U.unit_off, P));
     chk(D.tmeta_off = dalloc_copy(U.tmeta_off, P));
     chk(D.lvl = dalloc_copy(U.lvl, P));
@@ -1748,8 +1740,7 @@ int upload(rh_ctx *c) {
   chk(c->uf_src_b = dalloc_copy(A.ufwd.src_b, P));
   chk(c->ub_src_a = dalloc_copy(A.ubwd.src_a, P));
   chk(c->ub_src_b = dalloc_copy(A.ubwd.src_b, P));
-  chk(c->uf_top_pos = dalloc_copy(A.ufwd.top_pos, P));
-  chk(c->ub_top_pos = dalloc_copy(A.ubwd.top_pos, P));
+  for (double **t : {&c->tL, &c->tUt, &c->tU, &c->tLt}) chk(*t = dalloc<double>((size_t)A.nblk * 32 * kTopLd, P));
   chk(c->blk_ctr = dalloc<int>(16, P));
   chk(c->uL = dalloc<double2>(c->nrec_f, P));
   chk(c->uUt = dalloc<double2>(c->nrec_f, P));
@@ -1930,6 +1921,10 @@ SegParams make_params(rh_ctx *c) {
   h.uUt = c->uUt;
   h.uU = c->uU;
   h.uLt = c->uLt;
+  h.tL = c->tL;
+  h.tUt = c->tUt;
+  h.tU = c->tU;
+  h.tLt = c->tLt;
   h.maxrx = c->maxrx;
   h.fg_off = c->fg_off;
   h.fg_maxloc = A.fg.max_loc;
@@ -2373,10 +2368,8 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
     RH_LAUNCHED(c);
   }
   if (A.max_tops > 0) {
-    k_tops_inverse<<<A.nblk, kMaxTops * kMaxTops, 0, st>>>(
-        c->top_ptr, c->top_fpos_ptr, c->top_fpos, c->uf_top_pos, c->ub_top_pos, c->F_val,
-        reinterpret_cast<double *>(c->uL), reinterpret_cast<double *>(c->uUt), reinterpret_cast<double *>(c->uU),
-        reinterpret_cast<double *>(c->uLt));
+    k_tops_inverse<<<A.nblk, kMaxTops * kMaxTops, 0, st>>>(c->top_ptr, c->top_fpos_ptr, c->top_fpos, c->F_val,
+                                                           c->tL, c->tUt, c->tU, c->tLt);
     RH_LAUNCHED(c);
   }
   int status = 0;
