@@ -785,6 +785,40 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
     }
     A.blk_gp_ptr[s + 1] = (int)A.blk_gp_loc.size();
   }
+  A.gpe_off.assign(1, 0);
+  A.gpe_row.clear();
+  A.gpe_col.clear();
+  A.gpe_src.clear();
+  A.gpe_split.clear();
+  A.max_gpe = 0;
+  for (int s = 0; s < nb; ++s) {
+    const int e0 = (int)A.gpe_src.size();
+    std::vector<int> row_start;   // block-relative entry index of every row's first entry
+    for (int q = A.seg_row_off[s]; q < A.seg_row_off[s + 1]; ++q) {
+      const int r = A.row_global[q];
+      if (A.gp_rptr[r + 1] == A.gp_rptr[r]) continue;
+      row_start.push_back((int)A.gpe_src.size() - e0);
+      for (int e = A.gp_rptr[r]; e < A.gp_rptr[r + 1]; ++e) {
+        A.gpe_row.push_back((q - A.seg_row_off[s]) * UnitSweep::kCols * 8);
+        A.gpe_col.push_back(A.gp_col[e]);
+        A.gpe_src.push_back(e);
+      }
+    }
+    const int ne = (int)A.gpe_src.size() - e0;
+    A.max_gpe = std::max(A.max_gpe, ne);
+    // 8 warp ranges, balanced by entries, split at row starts
+    std::vector<int> sp(UnitSweep::kWarps + 1, ne);
+    sp[0] = 0;
+    for (int w = 1; w < UnitSweep::kWarps; ++w) {
+      const int target = (int)((long long)ne * w / UnitSweep::kWarps);
+      auto it = std::lower_bound(row_start.begin(), row_start.end(), target);
+      sp[w] = it == row_start.end() ? ne : *it;
+      sp[w] = std::max(sp[w], sp[w - 1]);
+    }
+    for (int w = 0; w <= UnitSweep::kWarps; ++w) A.gpe_split.push_back(sp[w]);
+    while (A.gpe_split.size() % 12) A.gpe_split.push_back(0);
+    A.gpe_off.push_back((int)A.gpe_src.size());
+  }
 
   // ---------------- refactorization schedule ----------------
   // R_A: block rows staged in shared memory (local order), up-looking per row.

@@ -173,6 +173,12 @@ struct Analysis {
   int max_seg_rows = 0, sep_rows = 0;
   SegSweep fwd, bwd;                        // fwd: L and U^T ; bwd: U and L^T
   std::vector<int32_t> blk_gp_ptr, blk_gp_loc;  // per block: local rows carrying G_p entries
+  // per block, the G_p entries of its rows in tile order (row ascending, CSR order within a
+  // row): tile-row byte offset, p column, G_p value position; and 8 warp ranges split at rows
+  std::vector<int32_t> gpe_off;                 // [nblk + 1]
+  std::vector<int32_t> gpe_row, gpe_col, gpe_src;
+  std::vector<int32_t> gpe_split;               // [nblk * 12]: 9 block-relative bounds, pad
+  int max_gpe = 0;
   std::vector<BlockSplit> split;            // per block (16 warps: refactorization R_A)
   std::vector<BlockSplit> usplit;           // per block (UnitSweep::kWarps: unit sweeps, tops)
   std::vector<int32_t> unit_lo;             // [n_x] lowest permuted row of the row's bus unit

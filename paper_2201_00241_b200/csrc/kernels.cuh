@@ -43,6 +43,8 @@ struct SegParams {
   DUnit uf, ub;                      // bus-unit block sweeps: fwd (L, U^T), bwd (U, L^T)
   const double2 *uL, *uUt, *uU, *uLt;  // their record values (per state)
   const double *tL, *tUt, *tU, *tLt;   // [nblk][32][36] dense tops inverses per sweep (k_tops_inverse)
+  const int *gpe_off, *gpe_split;      // L sweep: per block G_p entry records and 8 warp ranges
+  const double2 *gpe_rec;
   int maxrx;                         // max tile rows (block rows + staged separator rows)
   int smem_stride;                   // bytes per buffer (two buffers: current tile, prefetched tile)
   int smem_x_off, smem_meta_off, smem_tmeta_off, smem_rec_off, smem_doff_off, smem_lvl_off;  // bytes (tmeta: tops M + rows)

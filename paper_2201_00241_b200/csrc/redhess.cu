@@ -672,6 +672,16 @@ __global__ void __launch_bounds__(kMaxTops * kMaxTops) k_tops_inverse(const int 
   dLt[o] = ML[b][a];
 }
 
+// G_p entry records of the L sweep's right-hand side (per state): value, then
+// the tile-row byte offset and the p column packed into the second double
+__global__ void k_gather_gpe(int n, const int *__restrict__ src, const int *__restrict__ row,
+                             const int *__restrict__ pcol, const double *__restrict__ gp_val, double2 *rec) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n)
+    rec[i] = make_double2(gp_val[src[i]],
+                          __longlong_as_double((long long)(unsigned)row[i] | ((long long)pcol[i] << 32)));
+}
+
 // copy factor values into the sweep value arrays (entry order of the sweeps)
 __global__ void k_gather_vals(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -886,29 +896,37 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
 }
 
 // right-hand side -G_p W of a block's rows (SpMul fused into the L sweep,
-// PAPER.md:600): warp per G_p row, the row's entries fetched by the lanes at
-// once, lane = column
-__device__ __forceinline__ void tile_rhs_gpw(const SegParams &h, int s, int col0, double *X, int lane, int warp,
-                                             int nw) {
-  const int r0 = h.seg_row_off[s];
-  const int col = col0 + lane;
-  for (int k = h.blk_gp_ptr[s] + warp; k < h.blk_gp_ptr[s + 1]; k += nw) {
-    const int a = h.blk_gp_loc[k];
-    const int row = h.row_global[r0 + a];
-    const int e0 = h.gp_rptr[row], ne = h.gp_rptr[row + 1] - e0;
-    double acc = 0.0;
-    for (int b = 0; b < ne; b += 32) {
-      const int my = b + lane < ne ? h.gp_col[e0 + b + lane] : 0;
-      const double mv = b + lane < ne ? h.gp_val[e0 + b + lane] : 0.0;
-      const int n = min(32, ne - b);
-      for (int j = 0; j < n; ++j) {
-        const int pc = __shfl_sync(0xffffffffu, my, j);
-        const double gv = __shfl_sync(0xffffffffu, mv, j);
-        acc = fma(gv, load_W(h, pc, col), acc);
-      }
+// PAPER.md:600) from the block's staged G_p entry records (value; tile-row
+// byte offset | p column << 32), row ascending: a warp takes a range of whole
+// rows and keeps a running sum, 8 W loads in flight (lane = column).  The
+// same per-row order as rhs_gpw (CSR order): bitwise identical.
+__device__ __forceinline__ void tile_rhs_entries(const SegParams &h, const double2 *er, int e0, int e1, int col,
+                                                 double *Xl) {
+  double acc = 0.0;
+  int cur = -1;
+  for (int e = e0; e < e1; e += 8) {
+    double w[8], v[8];
+    int ro[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double2 r = e + u < e1 ? er[e + u] : make_double2(0.0, 0.0);
+      const long long m = __double_as_longlong(r.y);
+      v[u] = r.x;
+      ro[u] = e + u < e1 ? (int)(m & 0xffffffffll) : -2;
+      w[u] = e + u < e1 ? load_W(h, (int)(m >> 32), col) : 0.0;
     }
-    X[a * kBC + lane] = -acc;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (ro[u] == -2) break;
+      if (ro[u] != cur) {
+        if (cur >= 0) Xl[cur / 8] = -acc;
+        acc = 0.0;
+        cur = ro[u];
+      }
+      acc = fma(v[u], w[u], acc);
+    }
   }
+  if (cur >= 0) Xl[cur / 8] = -acc;
 }
 
 // TMA bulk copies (cp.async.bulk) and their mbarrier
@@ -978,7 +996,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     const int nxrows = mode == MODE_L ? 0 : nr + nxr;
     if (tid == 0) {
       const double *dM = mode == MODE_L ? h.tL : mode == MODE_U ? h.tU : mode == MODE_UT ? h.tUt : h.tLt;
-      const unsigned tx = 16u * (nu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + 32u * kTopLd * 8 + 128u;
+      const unsigned tx = 16u * (nu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + 32u * kTopLd * 8 + 128u +
+                          (mode == MODE_L ? 16u * (h.gpe_off[s + 1] - h.gpe_off[s]) + 48u : 0u);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx)
                    : "memory");
       bulk_g2s(smraw + h.smem_meta_off, U.meta + ub, 16u * nu, &mbar);
@@ -987,6 +1006,11 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
       bulk_g2s(smraw + h.smem_rec_off, vals + rb, 16u * nrec, &mbar);
       if (nof) bulk_g2s(smraw + h.smem_doff_off, U.doff + ob, 4u * nof, &mbar);
       bulk_g2s(smraw + h.smem_lvl_off, U.lvl + s * UnitSweep::kLvl, 4u * UnitSweep::kLvl, &mbar);
+      if (mode == MODE_L) {   // G_p entry records + warp ranges, behind the block's rows
+        const int g0 = h.gpe_off[s], ng = h.gpe_off[s + 1] - g0;
+        if (ng) bulk_g2s(X + nr * kBC, h.gpe_rec + g0, 16u * ng, &mbar);
+        bulk_g2s(reinterpret_cast<double2 *>(X + nr * kBC) + ng, h.gpe_split + s * 12, 48u, &mbar);
+      }
     }
     {  // X rows: 16-byte cp.async (LSU path; 256 B TMA bulk copies are rate-bound on the TMA unit)
       const int c = tid & 15;
@@ -995,11 +1019,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
         cp_async16(X + a * kBC + 2 * c, G + grow * h.ld + col0 + 2 * c);
       }
     }
-    if (mode == MODE_L) {   // right-hand side -G_p W (SpMul fused)
+    if (mode == MODE_L)   // right-hand side -G_p W (SpMul fused): zero, then the G_p rows below
       for (int i = tid; i < nr * (kBC / 2); i += blockDim.x) reinterpret_cast<double2 *>(X)[i] = make_double2(0.0, 0.0);
-      __syncthreads();
-      tile_rhs_gpw(h, s, col0, X, lane, warp, UnitSweep::kWarps);
-    }
     asm volatile("cp.async.wait_all;" ::: "memory");
     {  // wait for the copies of this tile
       unsigned done = 0;
@@ -1011,6 +1032,12 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
       parity ^= 1;
     }
     __syncthreads();
+    if (mode == MODE_L) {   // G_p rows of the block from the staged entry records (behind the block rows)
+      const double2 *er = reinterpret_cast<const double2 *>(X + nr * kBC);
+      const int *sp = reinterpret_cast<const int *>(er + (h.gpe_off[s + 1] - h.gpe_off[s]));
+      tile_rhs_entries(h, er, sp[warp], sp[warp + 1], col0 + lane, X + lane);
+      __syncthreads();
+    }
     const long long c_b = prof ? clock64() : 0;
     if (fwd) {
       if (dinv) unit_pieces<true>(st, Xb, warp); else unit_pieces<false>(st, Xb, warp);
@@ -1542,6 +1569,8 @@ struct rh_ctx {
   int2 *fg_slots;
   double4 *fg_scoef, *fg_ometa;
   double *pdiag;   // [n_p] 2 c2 of a Pg parameter's generator, else 0 (grid data)
+  int *gpe_off, *gpe_row, *gpe_col, *gpe_src, *gpe_split;
+  double2 *gpe_rec;
 
   void free_all() {
     for (void *q : pool) cudaFree(q);
@@ -1592,9 +1621,18 @@ bool blk_smem_fits(const Analysis &A, size_t lim) {
 
 // shared-memory carve-up of k_blk (2 CTAs per SM): the X tile, then one
 // block's unit schedule.  Returns the total bytes.
+int blk_max_rows(const Analysis &A) {   // tile rows, incl. the L sweep's G_p entry records behind the block rows
+  int m = std::max(A.ufwd.max_rows, A.ubwd.max_rows);
+  for (int s = 0; s < A.nblk; ++s) {
+    const int nr = A.seg_row_off[s + 1] - A.seg_row_off[s], ne = A.gpe_off[s + 1] - A.gpe_off[s];
+    m = std::max(m, nr + (16 * ne + 48 + kRowB - 1) / kRowB);
+  }
+  return m;
+}
+
 size_t blk_smem_layout(const Analysis &A, int *off7) {
   auto al = [](size_t x) { return (x + 127) & ~(size_t)127; };
-  const int maxrx = std::max(A.ufwd.max_rows, A.ubwd.max_rows);
+  const int maxrx = blk_max_rows(A);
   size_t off = 0;
   off7[0] = (int)off;
   off += al((size_t)maxrx * kBC * 8);
@@ -1742,13 +1780,19 @@ int upload(rh_ctx *c) {
   chk(c->ub_src_b = dalloc_copy(A.ubwd.src_b, P));
   for (double **t : {&c->tL, &c->tUt, &c->tU, &c->tLt}) chk(*t = dalloc<double>((size_t)A.nblk * 32 * kTopLd, P));
   chk(c->blk_ctr = dalloc<int>(16, P));
+  chk(c->gpe_off = dalloc_copy(A.gpe_off, P));
+  chk(c->gpe_row = dalloc_copy(A.gpe_row, P));
+  chk(c->gpe_col = dalloc_copy(A.gpe_col, P));
+  chk(c->gpe_src = dalloc_copy(A.gpe_src, P));
+  chk(c->gpe_split = dalloc_copy(A.gpe_split, P));
+  chk(c->gpe_rec = dalloc<double2>(std::max<size_t>(1, A.gpe_src.size()), P));
   chk(c->uL = dalloc<double2>(c->nrec_f, P));
   chk(c->uUt = dalloc<double2>(c->nrec_f, P));
   chk(c->uU = dalloc<double2>(c->nrec_b, P));
   chk(c->uLt = dalloc<double2>(c->nrec_b, P));
   {
     int o[7];
-    c->maxrx = std::max(A.ufwd.max_rows, A.ubwd.max_rows);
+    c->maxrx = blk_max_rows(A);
     c->smem_blk = blk_smem_layout(A, o);
     c->smem_stride = o[6];
     c->smem_x_off = o[0];
@@ -1925,6 +1969,9 @@ SegParams make_params(rh_ctx *c) {
   h.tUt = c->tUt;
   h.tU = c->tU;
   h.tLt = c->tLt;
+  h.gpe_off = c->gpe_off;
+  h.gpe_split = c->gpe_split;
+  h.gpe_rec = c->gpe_rec;
   h.maxrx = c->maxrx;
   h.fg_off = c->fg_off;
   h.fg_maxloc = A.fg.max_loc;
@@ -2350,6 +2397,11 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
       k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_b + e0, c->F_val, c->vUt + e0);
       RH_LAUNCHED(c);
     }
+  }
+  if (!A.gpe_src.empty()) {
+    const int ne = (int)A.gpe_src.size();
+    k_gather_gpe<<<nblk(ne), kThreads, 0, st>>>(ne, c->gpe_src, c->gpe_row, c->gpe_col, c->gp_val, c->gpe_rec);
+    RH_LAUNCHED(c);
   }
   const int ngp = (int)A.gp_col.size();
   if (ngp > 0) {
