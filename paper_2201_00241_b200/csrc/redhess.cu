@@ -1546,8 +1546,15 @@ struct rh_ctx {
   double *lam, *muP, *muQ, *dcoef, *X1col;
   double4 *coef;
   // workspace
-  double *Zb = nullptr, *Pb = nullptr, *Tsep = nullptr;
-  size_t ws_elems = 0, tsep_elems = 0;
+  // batch workspaces: [0] on the caller's stream, [1] on an internal stream so
+  // that consecutive batches of a full Hessian overlap (rh_hessian_columns)
+  struct Workspace {
+    double *Z = nullptr, *P = nullptr, *Tsep = nullptr;
+    size_t elems = 0, tsep_elems = 0;
+    int *ctr = nullptr;   // k_blk ticket counters of this workspace
+  } ws[2];
+  cudaStream_t st1 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   double *e2e_buf = nullptr;     // rh_reduced_hessian_host staging (x, p, grad, H)
   cudaStream_t e2e_st = nullptr;
   int *blk_gp_ptr, *blk_gp_loc;
@@ -1575,14 +1582,20 @@ struct rh_ctx {
   void free_all() {
     for (void *q : pool) cudaFree(q);
     pool.clear();
-    if (Zb) cudaFree(Zb);
-    if (Pb) cudaFree(Pb);
-    if (Tsep) cudaFree(Tsep);
+    for (auto &w : ws) {
+      if (w.Z) cudaFree(w.Z);
+      if (w.P) cudaFree(w.P);
+      if (w.Tsep) cudaFree(w.Tsep);
+      w = Workspace();
+    }
     if (e2e_buf) cudaFree(e2e_buf);
     if (e2e_st) cudaStreamDestroy(e2e_st);
-    Zb = Pb = Tsep = e2e_buf = nullptr;
-    e2e_st = nullptr;
-    ws_elems = tsep_elems = 0;
+    if (st1) cudaStreamDestroy(st1);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    e2e_buf = nullptr;
+    e2e_st = st1 = nullptr;
+    ev_fork = ev_join = nullptr;
   }
 };
 
@@ -1779,7 +1792,9 @@ int upload(rh_ctx *c) {
   chk(c->ub_src_a = dalloc_copy(A.ubwd.src_a, P));
   chk(c->ub_src_b = dalloc_copy(A.ubwd.src_b, P));
   for (double **t : {&c->tL, &c->tUt, &c->tU, &c->tLt}) chk(*t = dalloc<double>((size_t)A.nblk * 32 * kTopLd, P));
-  chk(c->blk_ctr = dalloc<int>(16, P));
+  chk(c->blk_ctr = dalloc<int>(32, P));
+  c->ws[0].ctr = c->blk_ctr;
+  c->ws[1].ctr = c->blk_ctr + 16;
   chk(c->gpe_off = dalloc_copy(A.gpe_off, P));
   chk(c->gpe_row = dalloc_copy(A.gpe_row, P));
   chk(c->gpe_col = dalloc_copy(A.gpe_col, P));
@@ -1864,7 +1879,7 @@ int upload(rh_ctx *c) {
   }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
   cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 16 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 32 * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->grid_bar, 0, 2 * sizeof(unsigned));
   {  // co-resident CTAs of k_sep_inverse (cooperative launch)
     int per_sm = 0;
@@ -1876,38 +1891,39 @@ int upload(rh_ctx *c) {
   return RH_OK;
 }
 
-int ensure_tsep(rh_ctx *c, int ld) {
+int ensure_tsep(rh_ctx *c, int ld, int k = 0) {
+  auto &w = c->ws[k];
   const size_t need = (size_t)ld * (size_t)std::max(1, c->A.sep_rows);
-  if (need <= c->tsep_elems) return RH_OK;
-  if (c->Tsep) cudaFree(c->Tsep);
-  c->Tsep = nullptr;
-  c->tsep_elems = 0;
-  if (cudaMalloc(&c->Tsep, need * sizeof(double)) != cudaSuccess) {
+  if (need <= w.tsep_elems) return RH_OK;
+  if (w.Tsep) cudaFree(w.Tsep);
+  w.Tsep = nullptr;
+  w.tsep_elems = 0;
+  if (cudaMalloc(&w.Tsep, need * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return fail(c, RH_E_NOMEM, "workspace allocation failed");
   }
-  c->tsep_elems = need;
+  w.tsep_elems = need;
   return RH_OK;
 }
 
-int ensure_ws(rh_ctx *c, int ld) {
+int ensure_ws(rh_ctx *c, int ld, int k = 0) {
+  auto &w = c->ws[k];
   const size_t need = (size_t)ld * (size_t)c->A.n_x;
-  if (int rc = ensure_tsep(c, ld)) return rc;
-  if (need <= c->ws_elems) return RH_OK;
-  if (c->Zb) cudaFree(c->Zb);
-  if (c->Pb) cudaFree(c->Pb);
-  c->Zb = c->Pb = nullptr;
-  c->ws_elems = 0;
-  if (cudaMalloc(&c->Zb, need * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&c->Pb, need * sizeof(double)) != cudaSuccess) {
+  if (int rc = ensure_tsep(c, ld, k)) return rc;
+  if (need <= w.elems) return RH_OK;
+  if (w.Z) cudaFree(w.Z);
+  if (w.P) cudaFree(w.P);
+  w.Z = w.P = nullptr;
+  w.elems = 0;
+  if (cudaMalloc(&w.Z, need * sizeof(double)) != cudaSuccess || cudaMalloc(&w.P, need * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return fail(c, RH_E_NOMEM, "workspace allocation failed");
   }
-  c->ws_elems = need;
+  w.elems = need;
   return RH_OK;
 }
 
-SegParams make_params(rh_ctx *c) {
+SegParams make_params(rh_ctx *c, int k = 0) {
   SegParams h{};
   const Analysis &A = c->A;
   h.n_x = A.n_x;
@@ -1920,8 +1936,8 @@ SegParams make_params(rh_ctx *c) {
   h.bwd = c->dbwd;
   h.vL = c->vL;
   h.vUt = c->vUt;
-  h.Z = c->Zb;
-  h.P = c->Pb;
+  h.Z = c->ws[k].Z;
+  h.P = c->ws[k].P;
   h.gp_rptr = c->gp_rptr;
   h.gp_col = c->gp_col;
   h.gp_val = c->gp_val;
@@ -1949,7 +1965,7 @@ SegParams make_params(rh_ctx *c) {
   h.ns = A.sep_rows;
   h.sep_off = A.seg_row_off[A.nblk];
   h.Sinv = c->Sinv;
-  h.Tsep = c->Tsep;
+  h.Tsep = c->ws[k].Tsep;
   h.blk_gp_ptr = c->blk_gp_ptr;
   h.blk_gp_loc = c->blk_gp_loc;
   if (const char *env = getenv("RH_DEBUG")) h.debug = atoi(env);  // timing experiments only
@@ -1991,7 +2007,7 @@ SegParams make_params(rh_ctx *c) {
   h.p_kind = c->p_kind;
   h.pdiag = c->pdiag;
   h.smem_stride = c->smem_stride;
-  h.blk_ctr = c->blk_ctr;
+  h.blk_ctr = c->ws[k].ctr;
   h.smem_x_off = c->smem_x_off;
   h.smem_meta_off = c->smem_meta_off;
   h.smem_tmeta_off = c->smem_tmeta_off;
@@ -2035,13 +2051,13 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
 // W == nullptr with ident_j0 >= 0 selects the Cartesian block e_{j0..j0+N-1}.
 int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW, long long ldhw,
              int transposed, int N, cudaStream_t st, double *Zo = nullptr, double *Yxo = nullptr,
-             double *Psio = nullptr, long long ldz = 0) {
+             double *Psio = nullptr, long long ldz = 0, int wsi = 0) {
   if (N <= 0) return RH_OK;
   const Analysis &A = c->A;
   const int ld = (N + kBC - 1) / kBC * kBC;
-  int rc = ensure_ws(c, ld);
+  int rc = ensure_ws(c, ld, wsi);
   if (rc) return rc;
-  SegParams h = make_params(c);
+  SegParams h = make_params(c, wsi);
   h.N = N;
   h.ld = ld;
   h.W = W;
@@ -2088,14 +2104,14 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     }
   }
   if (Zo) {
-    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, c->Zb, 1.0, Zo, ldz);
+    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, h.Z, 1.0, Zo, ldz);
     RH_LAUNCHED(c);
   }
   mark(3);
   k_for<<<gF, 256, c->smem_for, st>>>(h);
   RH_LAUNCHED(c);
   if (Yxo) {
-    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, c->Pb, -1.0, Yxo, ldz);
+    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, h.P, -1.0, Yxo, ldz);
     RH_LAUNCHED(c);
   }
   mark(4);
@@ -2112,7 +2128,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_LT);
   RH_LAUNCHED(c);
   if (Psio) {
-    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, c->Pb, 1.0, Psio, ldz);
+    k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, h.P, 1.0, Psio, ldz);
     RH_LAUNCHED(c);
   }
   mark(7);
@@ -2226,7 +2242,7 @@ int rh_get_info(const rh_ctx *c, rh_info *info) {
   info->n_blocks = A.nblk;
   info->sep_rows = A.sep_rows;
   info->seg_levels = std::max(A.fwd.max_levels, A.bwd.max_levels);
-  info->workspace_bytes = (int64_t)c->ws_elems * 2 * (int64_t)sizeof(double);
+  info->workspace_bytes = (int64_t)(c->ws[0].elems + c->ws[1].elems) * 2 * (int64_t)sizeof(double);
   return RH_OK;
 }
 
@@ -2516,12 +2532,29 @@ int rh_hessian_columns(rh_ctx *c, int32_t j0, int32_t j1, int32_t N, double *H, 
   cudaStream_t st = (cudaStream_t)stream;
   const int ncols = j1 - j0;
   const int nb = (ncols + N - 1) / N;
+  // batches alternate between the caller's stream (workspace 0) and an internal
+  // stream (workspace 1): consecutive batches overlap (tails, latency-bound
+  // kernels); the caller's stream joins the internal one at the end
+  const bool two = nb > 1 && !getenv("RH_ONE_STREAM");
+  if (two) {
+    if (!c->st1) RH_CUDA(c, cudaStreamCreateWithFlags(&c->st1, cudaStreamNonBlocking));
+    if (!c->ev_fork) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    if (!c->ev_join) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    RH_CUDA(c, cudaEventRecord(c->ev_fork, st));
+    RH_CUDA(c, cudaStreamWaitEvent(c->st1, c->ev_fork, 0));
+  }
   for (int b = 0; b < nb; ++b) {
     // balanced batches of width <= N (SURVEY.md 8(d) batch plan)
     const int a0 = (int)((long long)ncols * b / nb), a1 = (int)((long long)ncols * (b + 1) / nb);
     double *out = transposed ? H + (long long)a0 * ldh : H + a0;
-    rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, st);
+    const int k = two ? (b & 1) : 0;
+    rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, k ? c->st1 : st, nullptr, nullptr,
+                  nullptr, 0, k);
     if (rc) return rc;
+  }
+  if (two) {
+    RH_CUDA(c, cudaEventRecord(c->ev_join, c->st1));
+    RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_join, 0));
   }
   return RH_OK;
 }
