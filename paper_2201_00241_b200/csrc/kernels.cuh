@@ -99,6 +99,7 @@ struct FactParams {
   double *dinv, *rowmax;             // per permuted row
   int *status;
   double pivtol;
+  long long *dbg;                    // timing experiment (RH_DEBUG & 128): per-block phase stamps, else null
 };
 
 }  // namespace rh

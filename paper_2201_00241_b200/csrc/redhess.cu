@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   int *skk = reinterpret_cast<int *>(sks + nks);
   unsigned short *stg = reinterpret_cast<unsigned short *>(skk + nks);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  long long *prof = (f.dbg && threadIdx.x == 0) ? f.dbg + 8 * s : nullptr;
+  if (prof) prof[0] = clock64();
   // stage the block's F rows: thread per row, 8-byte cp.async copies all in flight
   for (int a = threadIdx.x; a < nr; a += blockDim.x) {
     const int i = f.row_global[r0 + a];
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   for (int t = threadIdx.x; t < ntg; t += blockDim.x) stg[t] = f.tgt16[tb + t];
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if (prof) prof[1] = clock64();
   // forward split of the block: lvl[0..nw] = each warp's piece rows, lvl[nw+1..nw+2] = tops
   const int *lv = f.fwd_lvl_ptr + f.fwd_seg_lvl[s];
   auto eliminate = [&](int q) {
@@ -279,6 +282,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   };
   for (int q = lv[warp]; q < lv[warp + 1]; ++q) eliminate(q);
   __syncthreads();
+  if (prof) prof[2] = clock64();
   // tops (rows q in [tq0, tq1), ascending): T1, warp per tops row, applies the
   // k-steps from piece rows (final now; a piece row is never an ancestor of a
   // tops row, so these steps commute with the tops' own); T2 is right-looking
@@ -333,6 +337,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
       }
     }
     __syncthreads();
+    if (prof) prof[3] = clock64();
     for (int tk = 0; tk < ntq; ++tk) {   // T2
       const int ak = s_topq[tk];
       const int4 rk = s_trow[tk];
@@ -360,6 +365,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     }
   }
   __syncthreads();
+  if (prof) prof[4] = clock64();
   for (int a = threadIdx.x; a < nr; a += blockDim.x) {   // write back: thread per row
     const int i = f.row_global[r0 + a];
     const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off, rb = f.F_rowptr[i];
@@ -2359,8 +2365,23 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   f.rowmax = c->rowmax;
   f.status = c->status;
   f.pivtol = 1e-14;
+  static long long *fdbg = nullptr;
+  const bool fprof = getenv("RH_DEBUG") && (atoi(getenv("RH_DEBUG")) & 128);
+  if (fprof) {
+    if (!fdbg) cudaMalloc(&fdbg, 8 * 4096 * sizeof(long long));
+    f.dbg = fdbg;
+  }
   k_fact_blocks<<<A.nblk, kSegThreads, c->smem_fact_blk, st>>>(f);
   RH_LAUNCHED(c);
+  if (fprof) {  // timing experiment: per-block phase stamps (tools/fact_prof.py)
+    std::vector<long long> hb((size_t)8 * A.nblk);
+    cudaMemcpyAsync(hb.data(), fdbg, hb.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE *fp = fopen("gpurun_out/fact_prof.bin", "wb")) {
+      fwrite(hb.data(), 8, hb.size(), fp);
+      fclose(fp);
+    }
+  }
   if (A.sep_rows > 0) {
     k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, 0, st>>>(f);
     RH_LAUNCHED(c);
