@@ -1105,6 +1105,25 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
   int e = h.fwd.rptr[q];
   const int ex = h.fwd.rext[q];
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  for (; e + 8 <= ex; e += 8) {   // 8 row gathers in flight
+    int d[8];
+    double c[8], x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      d[u] = h.fwd.dep[e + u];
+      c[u] = val[e + u];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = G[(long long)d[u] * h.ld + col];
+    s0 = fma(c[0], x[0], s0);
+    s1 = fma(c[1], x[1], s1);
+    s2 = fma(c[2], x[2], s2);
+    s3 = fma(c[3], x[3], s3);
+    s0 = fma(c[4], x[4], s0);
+    s1 = fma(c[5], x[5], s1);
+    s2 = fma(c[6], x[6], s2);
+    s3 = fma(c[7], x[7], s3);
+  }
   for (; e + 4 <= ex; e += 4) {
     const int d0 = h.fwd.dep[e], d1 = h.fwd.dep[e + 1], d2 = h.fwd.dep[e + 2], d3 = h.fwd.dep[e + 3];
     const double x0 = G[(long long)d0 * h.ld + col], x1 = G[(long long)d1 * h.ld + col];
