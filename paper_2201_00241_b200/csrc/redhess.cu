@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/redhess.h"
@@ -463,7 +464,7 @@ constexpr int GJT = 64;   // output tile
 constexpr size_t gj_smem_bytes() { return sizeof(double) * (GJB * (GJB + 1) + (3 * GJB + GJT) * (GJT + 1)); }
 __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, int ns, const double *rowmax,
                                                      const int *sep_rows, int *status, double pivtol,
-                                                     unsigned *bar, long long *dbg) {
+                                                     unsigned *bar, long long *dbg, double *dbuf) {
   extern __shared__ double gj_sm[];   // dynamic: gj_smem_bytes()
   double(*Ds)[GJB + 1] = reinterpret_cast<double(*)[GJB + 1]>(gj_sm);
   double(*Cs)[GJT + 1] = reinterpret_cast<double(*)[GJT + 1]>(gj_sm + GJB * (GJB + 1));   // C^T: Cs[m][r] = S[i0 + r][K + m]
@@ -517,46 +518,124 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
     }
   };
   long long *prof = (dbg && tid == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) ? dbg + (blockIdx.x ? 512 : 0) : nullptr;
+  // Gauss-Jordan inverse of the 32 x 32 block Dsrc (smem, row stride GJB + 1)
+  // into Ds by warps 0-3: thread = (rows 8w..8w+7, column lane); the pivot row
+  // goes through shared memory, the pivot column by shuffles; static pivots
+  // checked against the separator rows' original max (rows K0 ..)
+  // (NW warps: thread = (rows (32/NW) w .., column lane), named barrier 1)
+  auto invert32 = [&](const double *Dsrc, int lds, int K0, int bb, bool report, auto nwc) {
+    constexpr int NW = decltype(nwc)::value, RPT = GJB / NW;
+    const int j = lane;
+    double v[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = RPT * warp + r;
+      v[r] = (i < bb && j < bb) ? Dsrc[i * lds + j] : (i == j ? 1.0 : 0.0);
+    }
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < GJB; ++k) {
+      const int wk = k / RPT, kk = k % RPT;
+      if (warp == wk) prow[k & 1][j] = v[kk];
+      double f[RPT];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) f[r] = __shfl_sync(0xffffffffu, v[r], k);
+      asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+      const double pk = prow[k & 1][k];
+      const double inv = fast_rcp(pk);
+      const double rk = j == k ? inv : prow[k & 1][j] * inv;
+      if (warp == wk && j == k && k < bb && !(fabs(pk) > pivtol * rowmax[sep_rows[K0 + k]])) bad = true;
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) {
+        const int i = RPT * warp + r;
+        v[r] = i == k ? rk : (j == k ? -f[r] * inv : fma(-f[r], rk, v[r]));
+      }
+    }
+    if (bad && report) atomicMax(status, sep_rows[K0 + j] + 1);
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");   // every warp has read Dsrc before Ds is written
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) Ds[RPT * warp + r][j] = v[r];
+  };
+  using W4 = std::integral_constant<int, 4>;
+  using W8 = std::integral_constant<int, 8>;
+  const bool helper = blockIdx.x == gridDim.x - 1;   // lookahead CTA: the next panel's D^-1
+  const int ntcta = gridDim.x - 1;                   // tile CTAs
   for (int K = 0; K < ns; K += GJB) {
     const int b = min(GJB, ns - K);
     if (prof) prof[(K / GJB) * 4] = clock64();   // timing experiment (RH_DEBUG & 16)
-    if (warp < 4) {
-      // D^-1 -> Ds (every CTA, redundantly) by 4 warps: thread = (rows 8w..8w+7, column lane);
-      // the pivot row goes through shared memory, the pivot column by shuffles
-      const int j = lane;
-      double v[8];
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int i = 8 * warp + r;
-        v[r] = (i < b && j < b) ? __ldcg(Sin + (long long)(K + i) * ns + K + j) : (i == j ? 1.0 : 0.0);
-      }
-      bool bad = false;
-#pragma unroll
-      for (int k = 0; k < GJB; ++k) {
-        const int wk = k >> 3, kk = k & 7;
-        if (warp == wk) prow[k & 1][j] = v[kk];
-        double f[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) f[r] = __shfl_sync(0xffffffffu, v[r], k);
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const double pk = prow[k & 1][k];
-        const double inv = fast_rcp(pk);
-        const double rk = j == k ? inv : prow[k & 1][j] * inv;
-        if (warp == wk && j == k && k < b && !(fabs(pk) > pivtol * rowmax[sep_rows[K + k]])) bad = true;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int i = 8 * warp + r;
-          v[r] = i == k ? rk : (j == k ? -f[r] * inv : fma(-f[r], rk, v[r]));
+    if (helper) {
+      // panel 0: D_0^-1 first; then D'_{K+1} = S[K1,K1] - S[K1,K] D_K^-1 S[K,K1] (S = state after
+      // panel K-1, what the tiles read now), inverted into Ds and published in dbuf for panel K+1
+      if (K == 0) {
+        for (int t = tid; t < GJB * GJB; t += blockDim.x) {
+          const int i = t / GJB, c = t % GJB;
+          Ts[i][c] = (i < b && c < b) ? __ldcg(Sin + (long long)i * ns + c) : 0.0;
         }
+        __syncthreads();
+        invert32(&Ts[0][0], GJT + 1, 0, b, false, W8{});
+        __syncthreads();
       }
-      if (bad && blockIdx.x == 0) atomicMax(status, sep_rows[K + j] + 1);
+      const int K1 = K + GJB, b1 = min(GJB, ns - K1);
+      if (b1 > 0) {
+        {   // Cs = S[K1,K], Rs = S[K,K1], Ts = S[K1,K1]: all 12 loads per thread in flight
+          double vc[4], vr[4], vt[4];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) Ds[8 * warp + r][j] = v[r];
-    } else if (blockIdx.x < ntiles) {
-      const int tile = blockIdx.x;
-      load_tile(Sin, K, b, (tile / nt) * GJT, (tile % nt) * GJT, tid - 128, 128);
+          for (int u = 0; u < 4; ++u) {
+            const int t = tid + u * 256, i = t / GJB, c = t % GJB;
+            vc[u] = (i < b1 && c < b) ? __ldcg(Sin + (long long)(K1 + i) * ns + K + c) : 0.0;
+            vr[u] = (i < b && c < b1) ? __ldcg(Sin + (long long)(K + i) * ns + K1 + c) : 0.0;
+            vt[u] = (i < b1 && c < b1) ? __ldcg(Sin + (long long)(K1 + i) * ns + K1 + c) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int t = tid + u * 256, i = t / GJB, c = t % GJB;
+            Cs[i][c] = vc[u];
+            Rs[i][c] = vr[u];
+            Ts[i][c] = vt[u];
+          }
+        }
+        __syncthreads();
+        for (int t = tid; t < GJB * GJB; t += blockDim.x) {   // R2 = D_K^-1 S[K,K1]
+          const int i = t / GJB, c = t % GJB;
+          double acc = 0.0;
+#pragma unroll 8
+          for (int l = 0; l < GJB; ++l) acc = fma(Ds[i][l], Rs[l][c], acc);
+          R2[i][c] = acc;
+        }
+        __syncthreads();
+        for (int t = tid; t < GJB * GJB; t += blockDim.x) {   // Ts = S[K1,K1] - S[K1,K] R2
+          const int i = t / GJB, c = t % GJB;
+          double acc = Ts[i][c];
+#pragma unroll 8
+          for (int l = 0; l < GJB; ++l) acc = fma(-Cs[i][l], R2[l][c], acc);
+          Ts[i][c] = acc;
+        }
+        __syncthreads();
+        invert32(&Ts[0][0], GJT + 1, K1, b1, true, W8{});
+        __syncthreads();
+        double *db = dbuf + ((K1 / GJB) & 1) * GJB * GJB;
+        for (int t = tid; t < GJB * GJB; t += blockDim.x) __stcg(db + t, Ds[t / GJB][t % GJB]);
+      }
+    } else {
+      if (K == 0) {   // panel 0: D_0^-1 locally (warps 0-3) while warps 4-7 stage the first tile
+        if (warp < 4) {
+          for (int t = tid; t < GJB * GJB; t += 128) {
+            const int i = t / GJB, c = t % GJB;
+            Ds[i][c] = (i < b && c < b) ? __ldcg(Sin + (long long)i * ns + c) : (i == c ? 1.0 : 0.0);
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          invert32(&Ds[0][0], GJB + 1, 0, b, blockIdx.x == 0, W4{});
+        } else if (blockIdx.x < ntiles) {
+          load_tile(Sin, K, b, (blockIdx.x / nt) * GJT, (blockIdx.x % nt) * GJT, tid - 128, 128);
+        }
+      } else {        // the helper's D_K^-1, then the first tile
+        const double *db = dbuf + ((K / GJB) & 1) * GJB * GJB;
+        for (int t = tid; t < GJB * GJB; t += blockDim.x) Ds[t / GJB][t % GJB] = __ldcg(db + t);
+        if (blockIdx.x < ntiles)
+          load_tile(Sin, K, b, (blockIdx.x / nt) * GJT, (blockIdx.x % nt) * GJT, tid, blockDim.x);
+      }
     }
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int tile = helper ? ntiles : (int)blockIdx.x; tile < ntiles; tile += ntcta) {
       const int i0 = (tile / nt) * GJT, j0 = (tile % nt) * GJT;
       if (tile != (int)blockIdx.x) load_tile(Sin, K, b, i0, j0, tid, blockDim.x);
       __syncthreads();   // Ds (first tile), Cs, Rs = P, Ts
@@ -1560,6 +1639,7 @@ struct rh_ctx {
   unsigned short *tgt16;
   int *sb_src, *sb_dense;
   double *Sbuf = nullptr;   // ping-pong partner of Sinv in k_sep_inverse
+  double *gj_dbuf = nullptr;   // [2][32][32] next panel's diagonal inverse (lookahead CTA)
   unsigned *grid_bar = nullptr;
   int coop_blocks = 1;
   double *dinv_rows, *rowmax;
@@ -1884,6 +1964,7 @@ int upload(rh_ctx *c) {
   chk(c->SinvT = dalloc<double>(ns2, P));
   chk(c->Sbuf = dalloc<double>(std::max<size_t>(ns2, 1), P));
   chk(c->grid_bar = dalloc<unsigned>(2, P));
+  chk(c->gj_dbuf = dalloc<double>(2 * 32 * 32, P));
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
   // shared-memory footprints
   c->smem_fact_blk = fact_smem_bytes(A);
@@ -2427,9 +2508,10 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
         if (!buf) cudaMalloc(&buf, 1024 * sizeof(long long));
         gdbg = buf;
       }
-    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar, &gdbg};
+    double *dbuf = c->gj_dbuf;
+    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar, &gdbg, &dbuf};
     const int ntl = ((ns + GJT - 1) / GJT) * ((ns + GJT - 1) / GJT);
-    const int grid = std::max(1, std::min(ntl, c->coop_blocks));
+    const int grid = std::max(1, std::min(ntl, c->coop_blocks - 1)) + 1;   // tile CTAs + the lookahead CTA
     RH_CUDA(c, cudaLaunchCooperativeKernel((const void *)k_sep_inverse, dim3(grid), dim3(256), args, gj_smem_bytes(), st));
     RH_LAUNCHED(c);
     if (gdbg) {
