@@ -2644,19 +2644,19 @@ int rh_hvp_stages(rh_ctx *c, const double *W, int64_t ldw, double *HW, int64_t l
   return hvp_impl(c, W, ldw, -1, HW, ldhw, 0, N, (cudaStream_t)stream, Z, Yx, Psi, ldz);
 }
 
-int rh_hessian_columns(rh_ctx *c, int32_t j0, int32_t j1, int32_t N, double *H, int64_t ldh, int32_t transposed,
-                       void *stream) {
-  int rc = check_ready(c, true);
-  if (rc) return rc;
-  const int np_ = c->A.n_p;
-  if (j0 < 0 || j1 > np_ || j0 > j1 || N <= 0 || !H) return fail(c, RH_E_ARG, "bad column range / N / H");
-  if ((!transposed && ldh < j1 - j0) || (transposed && ldh < np_)) return fail(c, RH_E_ARG, "ldh too small");
-  cudaStream_t st = (cudaStream_t)stream;
+}  // extern "C"
+
+namespace {
+// Batches of Cartesian columns [j0, j1): balanced batches of
+// width <= N alternate between the caller's stream (workspace 0) and an internal
+// stream (workspace 1), so consecutive batches overlap (tails, latency-bound
+// kernels); the caller's stream joins the internal one at the end.  With Hhost
+// (non-transposed H only), every finished column block is copied to the host
+// on its batch's stream while the next batches compute.
+int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, int transposed, cudaStream_t st,
+                    double *Hhost) {
   const int ncols = j1 - j0;
   const int nb = (ncols + N - 1) / N;
-  // batches alternate between the caller's stream (workspace 0) and an internal
-  // stream (workspace 1): consecutive batches overlap (tails, latency-bound
-  // kernels); the caller's stream joins the internal one at the end
   const bool two = nb > 1 && !getenv("RH_ONE_STREAM");
   if (two) {
     if (!c->st1) RH_CUDA(c, cudaStreamCreateWithFlags(&c->st1, cudaStreamNonBlocking));
@@ -2666,19 +2666,34 @@ int rh_hessian_columns(rh_ctx *c, int32_t j0, int32_t j1, int32_t N, double *H, 
     RH_CUDA(c, cudaStreamWaitEvent(c->st1, c->ev_fork, 0));
   }
   for (int b = 0; b < nb; ++b) {
-    // balanced batches of width <= N (SURVEY.md 8(d) batch plan)
     const int a0 = (int)((long long)ncols * b / nb), a1 = (int)((long long)ncols * (b + 1) / nb);
     double *out = transposed ? H + (long long)a0 * ldh : H + a0;
     const int k = two ? (b & 1) : 0;
-    rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, k ? c->st1 : st, nullptr, nullptr,
-                  nullptr, 0, k);
+    cudaStream_t sb = k ? c->st1 : st;
+    int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0, k);
     if (rc) return rc;
+    if (Hhost)
+      RH_CUDA(c, cudaMemcpy2DAsync(Hhost + a0, ldh * sizeof(double), out, ldh * sizeof(double),
+                                   (size_t)(a1 - a0) * sizeof(double), (size_t)c->A.n_p, cudaMemcpyDeviceToHost, sb));
   }
   if (two) {
     RH_CUDA(c, cudaEventRecord(c->ev_join, c->st1));
     RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_join, 0));
   }
   return RH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int rh_hessian_columns(rh_ctx *c, int32_t j0, int32_t j1, int32_t N, double *H, int64_t ldh, int32_t transposed,
+                       void *stream) {
+  int rc = check_ready(c, true);
+  if (rc) return rc;
+  const int np_ = c->A.n_p;
+  if (j0 < 0 || j1 > np_ || j0 > j1 || N <= 0 || !H) return fail(c, RH_E_ARG, "bad column range / N / H");
+  if ((!transposed && ldh < j1 - j0) || (transposed && ldh < np_)) return fail(c, RH_E_ARG, "ldh too small");
+  return hessian_batches(c, j0, j1, N, H, ldh, transposed, (cudaStream_t)stream, nullptr);
 }
 
 int rh_full_hessian(rh_ctx *c, int32_t N, double *H, void *stream) {
@@ -2708,10 +2723,12 @@ int rh_reduced_hessian_host(rh_ctx *c, const double *x, const double *p, int32_t
   RH_CUDA(c, cudaMemcpyAsync(dp, p, np_ * 8, cudaMemcpyHostToDevice, st));
   int rc = rh_set_state(c, dx, dp, st);
   if (!rc) rc = rh_reduced_gradient(c, dg, nullptr, st);
-  if (!rc) rc = rh_full_hessian(c, N, dH, st);
   if (rc) return rc;
+  if (N <= 0) return fail(c, RH_E_ARG, "N must be positive");
   if (grad_p) RH_CUDA(c, cudaMemcpyAsync(grad_p, dg, np_ * 8, cudaMemcpyDeviceToHost, st));
-  RH_CUDA(c, cudaMemcpyAsync(H, dH, np_ * np_ * 8, cudaMemcpyDeviceToHost, st));
+  // column blocks leave for the host as their batches finish (overlapping the later batches)
+  rc = hessian_batches(c, 0, (int)np_, N, dH, (long long)np_, 0, st, H);
+  if (rc) return rc;
   RH_CUDA(c, cudaStreamSynchronize(st));
   return RH_OK;
 }
