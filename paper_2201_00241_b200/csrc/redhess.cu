@@ -1605,6 +1605,8 @@ constexpr int kSmemSM = 228 * 1024;    // shared memory per SM
 
 }  // namespace
 
+constexpr int kNumWs = 3;   // batch workspaces / streams of a full Hessian
+
 struct rh_ctx {
   int device = -1;
   bool host_only = true;
@@ -1651,15 +1653,15 @@ struct rh_ctx {
   double *lam, *muP, *muQ, *dcoef, *X1col;
   double4 *coef;
   // workspace
-  // batch workspaces: [0] on the caller's stream, [1] on an internal stream so
-  // that consecutive batches of a full Hessian overlap (rh_hessian_columns)
+  // batch workspaces: [0] on the caller's stream, [1..] on internal streams so
+  // that consecutive batches of a full Hessian overlap (hessian_batches)
   struct Workspace {
     double *Z = nullptr, *P = nullptr, *Tsep = nullptr;
     size_t elems = 0, tsep_elems = 0;
     int *ctr = nullptr;   // k_blk ticket counters of this workspace
-  } ws[2];
-  cudaStream_t st1 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  } ws[kNumWs];
+  cudaStream_t sti[kNumWs] = {};                        // internal streams of workspaces 1..
+  cudaEvent_t ev_fork = nullptr, ev_join[kNumWs] = {};
   double *e2e_buf = nullptr;     // rh_reduced_hessian_host staging (x, p, grad, H)
   cudaStream_t e2e_st = nullptr;
   int *blk_gp_ptr, *blk_gp_loc;
@@ -1695,12 +1697,16 @@ struct rh_ctx {
     }
     if (e2e_buf) cudaFree(e2e_buf);
     if (e2e_st) cudaStreamDestroy(e2e_st);
-    if (st1) cudaStreamDestroy(st1);
+    for (int k = 0; k < kNumWs; ++k) {
+      if (sti[k]) cudaStreamDestroy(sti[k]);
+      if (ev_join[k]) cudaEventDestroy(ev_join[k]);
+      sti[k] = nullptr;
+      ev_join[k] = nullptr;
+    }
     if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
     e2e_buf = nullptr;
-    e2e_st = st1 = nullptr;
-    ev_fork = ev_join = nullptr;
+    e2e_st = nullptr;
+    ev_fork = nullptr;
   }
 };
 
@@ -1897,9 +1903,8 @@ int upload(rh_ctx *c) {
   chk(c->ub_src_a = dalloc_copy(A.ubwd.src_a, P));
   chk(c->ub_src_b = dalloc_copy(A.ubwd.src_b, P));
   for (double **t : {&c->tL, &c->tUt, &c->tU, &c->tLt}) chk(*t = dalloc<double>((size_t)A.nblk * 32 * kTopLd, P));
-  chk(c->blk_ctr = dalloc<int>(32, P));
-  c->ws[0].ctr = c->blk_ctr;
-  c->ws[1].ctr = c->blk_ctr + 16;
+  chk(c->blk_ctr = dalloc<int>(16 * kNumWs, P));
+  for (int k = 0; k < kNumWs; ++k) c->ws[k].ctr = c->blk_ctr + 16 * k;
   chk(c->gpe_off = dalloc_copy(A.gpe_off, P));
   chk(c->gpe_row = dalloc_copy(A.gpe_row, P));
   chk(c->gpe_col = dalloc_copy(A.gpe_col, P));
@@ -1985,7 +1990,7 @@ int upload(rh_ctx *c) {
   }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
   cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 32 * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 16 * kNumWs * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->grid_bar, 0, 2 * sizeof(unsigned));
   {  // co-resident CTAs of k_sep_inverse (cooperative launch)
     int per_sm = 0;
@@ -2348,7 +2353,9 @@ int rh_get_info(const rh_ctx *c, rh_info *info) {
   info->n_blocks = A.nblk;
   info->sep_rows = A.sep_rows;
   info->seg_levels = std::max(A.fwd.max_levels, A.bwd.max_levels);
-  info->workspace_bytes = (int64_t)(c->ws[0].elems + c->ws[1].elems) * 2 * (int64_t)sizeof(double);
+  int64_t wse = 0;
+  for (const auto &w : c->ws) wse += (int64_t)w.elems;
+  info->workspace_bytes = wse * 2 * (int64_t)sizeof(double);
   return RH_OK;
 }
 
@@ -2648,37 +2655,41 @@ int rh_hvp_stages(rh_ctx *c, const double *W, int64_t ldw, double *HW, int64_t l
 
 namespace {
 // Batches of Cartesian columns [j0, j1): balanced batches of
-// width <= N alternate between the caller's stream (workspace 0) and an internal
-// stream (workspace 1), so consecutive batches overlap (tails, latency-bound
-// kernels); the caller's stream joins the internal one at the end.  With Hhost
+// width <= N go round-robin to the caller's stream (workspace 0) and internal
+// streams (workspaces 1, 2), so consecutive batches overlap (tails,
+// latency-bound kernels); the caller's stream joins them at the end.  With Hhost
 // (non-transposed H only), every finished column block is copied to the host
 // on its batch's stream while the next batches compute.
 int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, int transposed, cudaStream_t st,
                     double *Hhost) {
   const int ncols = j1 - j0;
   const int nb = (ncols + N - 1) / N;
-  const bool two = nb > 1 && !getenv("RH_ONE_STREAM");
-  if (two) {
-    if (!c->st1) RH_CUDA(c, cudaStreamCreateWithFlags(&c->st1, cudaStreamNonBlocking));
+  int nws = kNumWs;
+  if (const char *env = getenv("RH_STREAMS")) nws = std::max(1, std::min(kNumWs, atoi(env)));   // tuning override
+  nws = std::min(nws, nb);
+  if (nws > 1) {
     if (!c->ev_fork) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
-    if (!c->ev_join) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     RH_CUDA(c, cudaEventRecord(c->ev_fork, st));
-    RH_CUDA(c, cudaStreamWaitEvent(c->st1, c->ev_fork, 0));
+    for (int k = 1; k < nws; ++k) {
+      if (!c->sti[k]) RH_CUDA(c, cudaStreamCreateWithFlags(&c->sti[k], cudaStreamNonBlocking));
+      if (!c->ev_join[k]) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));
+      RH_CUDA(c, cudaStreamWaitEvent(c->sti[k], c->ev_fork, 0));
+    }
   }
   for (int b = 0; b < nb; ++b) {
     const int a0 = (int)((long long)ncols * b / nb), a1 = (int)((long long)ncols * (b + 1) / nb);
     double *out = transposed ? H + (long long)a0 * ldh : H + a0;
-    const int k = two ? (b & 1) : 0;
-    cudaStream_t sb = k ? c->st1 : st;
+    const int k = b % nws;
+    cudaStream_t sb = k ? c->sti[k] : st;
     int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0, k);
     if (rc) return rc;
     if (Hhost)
       RH_CUDA(c, cudaMemcpy2DAsync(Hhost + a0, ldh * sizeof(double), out, ldh * sizeof(double),
                                    (size_t)(a1 - a0) * sizeof(double), (size_t)c->A.n_p, cudaMemcpyDeviceToHost, sb));
   }
-  if (two) {
-    RH_CUDA(c, cudaEventRecord(c->ev_join, c->st1));
-    RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+  for (int k = 1; k < nws; ++k) {
+    RH_CUDA(c, cudaEventRecord(c->ev_join[k], c->sti[k]));
+    RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_join[k], 0));
   }
   return RH_OK;
 }
