@@ -186,9 +186,22 @@ int rh_hessian_columns(rh_ctx *ctx, int32_t j0, int32_t j1, int32_t N, double *H
  * component i of the HVP with e_j), ceil(n_p / N) batches (R10). */
 int rh_full_hessian(rh_ctx *ctx, int32_t N, double *H, void *stream);
 
+/* One pass of the whole path on DEVICE buffers: the same results as
+ * rh_set_state(x, p), rh_reduced_gradient(grad_p) and
+ * rh_hessian_columns(j0, j1, N, H, ldh, transposed), in one call.
+ * x [n_x], p [n_p] (read), grad_p [n_p] (written, required), H as for
+ * rh_hessian_columns (nullable when j0 == j1).  The first block sweep of the
+ * first batches (it needs only the block factors) runs on an internal stream
+ * while the separator is refactorized and inverted; `stream` waits for all of
+ * it.  Synchronizes `stream` once (the pivot flag, as rh_set_state).
+ * Errors: as rh_set_state and rh_hessian_columns. */
+int rh_reduced_hessian(rh_ctx *ctx, const double *x, const double *p, int32_t j0, int32_t j1, int32_t N,
+                       double *grad_p, double *H, int64_t ldh, int32_t transposed, void *stream);
+
 /* End-to-end call with HOST buffers: copies x [n_x], p [n_p] to the device,
- * runs rh_set_state, rh_reduced_gradient and rh_full_hessian(N), and copies
- * grad_p [n_p] (nullable) and H [n_p][n_p] back to the host.  Blocking.
+ * runs rh_reduced_hessian over all columns (batches of N), copies every
+ * finished column block of H [n_p][n_p] back to the host while the later
+ * batches compute, and grad_p [n_p] (nullable).  Blocking.
  * Pinned (page-locked) host buffers give the fastest copies. */
 int rh_reduced_hessian_host(rh_ctx *ctx, const double *x, const double *p, int32_t N,
                             double *grad_p, double *H);

@@ -26,7 +26,8 @@ KIND_THETA, KIND_V, KIND_PG = 0, 1, 2
 # every symbol declared in include/redhess.h (checked by tests/test_abi.py)
 EXPORTS = ["rh_create", "rh_destroy", "rh_last_error", "rh_load_grid", "rh_get_info", "rh_orderings",
            "rh_symbolic", "rh_segments", "rh_set_state", "rh_residual", "rh_reduced_gradient", "rh_set_multipliers",
-           "rh_hvp", "rh_hvp_stages", "rh_hessian_columns", "rh_full_hessian", "rh_reduced_hessian_host",
+           "rh_hvp", "rh_hvp_stages", "rh_hessian_columns", "rh_full_hessian", "rh_reduced_hessian",
+           "rh_reduced_hessian_host",
            "rh_launch_count", "rh_set_timing", "rh_stage_times"]
 
 
@@ -77,6 +78,7 @@ def _load():
         "rh_hvp_stages": ([vp, vp, i64, vp, i64, i32, vp, vp, vp, i64, vp], ctypes.c_int),
         "rh_hessian_columns": ([vp, i32, i32, i32, vp, i64, i32, vp], ctypes.c_int),
         "rh_full_hessian": ([vp, i32, vp, vp], ctypes.c_int),
+        "rh_reduced_hessian": ([vp, vp, vp, i32, i32, i32, vp, vp, i64, i32, vp], ctypes.c_int),
         "rh_reduced_hessian_host": ([vp, vp, vp, i32, vp, vp], ctypes.c_int),
         "rh_launch_count": ([vp], i64),
         "rh_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
@@ -268,6 +270,21 @@ class RedHess:
         return H
 
     # ------------------------------------------------------------------ compute (host buffers)
+    def reduced_hessian(self, x, p, N, j0=0, j1=None, grad=None, H=None, transposed=False, stream=None):
+        """rh_reduced_hessian: state + reduced gradient + Hessian columns [j0, j1) in one call (DEVICE)."""
+        import torch
+        j1 = self.n_p if j1 is None else j1
+        _check_dev(x, self.n_x, "x")
+        _check_dev(p, self.n_p, "p")
+        if grad is None:
+            grad = torch.empty(self.n_p, dtype=torch.float64, device="cuda")
+        if H is None:
+            shape = (j1 - j0, self.n_p) if transposed else (self.n_p, j1 - j0)
+            H = torch.empty(shape, dtype=torch.float64, device="cuda")
+        self._rc(lib().rh_reduced_hessian(self._h, _ptr(x), _ptr(p), j0, j1, N, _ptr(grad), _ptr(H), H.stride(0),
+                                          int(bool(transposed)), _stream(stream)))
+        return grad, H
+
     def reduced_hessian_host(self, x, p, N, grad=None, H=None):
         """End to end with HOST buffers (numpy or pinned torch CPU tensors)."""
         if H is None:

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <numeric>
 #include <cstdio>
@@ -1662,6 +1663,7 @@ struct rh_ctx {
   } ws[kNumWs];
   cudaStream_t sti[kNumWs] = {};                        // internal streams of workspaces 1..
   cudaEvent_t ev_fork = nullptr, ev_join[kNumWs] = {};
+  cudaEvent_t ev_sa = nullptr, ev_sb = nullptr;          // state_impl fork / join
   double *e2e_buf = nullptr;     // rh_reduced_hessian_host staging (x, p, grad, H)
   cudaStream_t e2e_st = nullptr;
   int *blk_gp_ptr, *blk_gp_loc;
@@ -1704,6 +1706,9 @@ struct rh_ctx {
       ev_join[k] = nullptr;
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_sa) cudaEventDestroy(ev_sa);
+    if (ev_sb) cudaEventDestroy(ev_sb);
+    ev_sa = ev_sb = nullptr;
     e2e_buf = nullptr;
     e2e_st = nullptr;
     ev_fork = nullptr;
@@ -2160,15 +2165,18 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
 // one Alg. 2 batch: eight stream-ordered kernels, no host
 // synchronization (cf. the two explicit syncs of PAPER.md:798-805).
 // W == nullptr with ident_j0 >= 0 selects the Cartesian block e_{j0..j0+N-1}.
+// phase: 0 = the whole batch, 1 = only the first block sweep (L, which needs
+// nothing of the separator), 2 = the rest (after a phase-1 launch on workspace wsi)
 int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW, long long ldhw,
              int transposed, int N, cudaStream_t st, double *Zo = nullptr, double *Yxo = nullptr,
-             double *Psio = nullptr, long long ldz = 0, int wsi = 0) {
+             double *Psio = nullptr, long long ldz = 0, int wsi = 0, int phase = 0) {
   if (N <= 0) return RH_OK;
   const Analysis &A = c->A;
   const int ld = (N + kBC - 1) / kBC * kBC;
   int rc = ensure_ws(c, ld, wsi);
   if (rc) return rc;
   SegParams h = make_params(c, wsi);
+  const bool timing = c->timing && phase == 0;
   h.N = N;
   h.ld = ld;
   h.W = W;
@@ -2187,14 +2195,17 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   const int nx = A.n_x;
   const long long tot = (long long)nx * N;
   cudaEvent_t ev[9];
-  if (c->timing)
+  if (timing)
     for (auto &e : ev) cudaEventCreate(&e);
   auto mark = [&](int i) {
-    if (c->timing) cudaEventRecord(ev[i], st);
+    if (timing) cudaEventRecord(ev[i], st);
   };
   mark(0);
-  k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_L);
-  RH_LAUNCHED(c);
+  if (phase != 2) {
+    k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_L);
+    RH_LAUNCHED(c);
+  }
+  if (phase == 1) return RH_OK;
   mark(1);
   if (has_sep) {
     k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_LU);
@@ -2246,7 +2257,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   k_muladd<<<gM, kThreads, 0, st>>>(h);
   RH_LAUNCHED(c);
   mark(8);
-  if (c->timing) {
+  if (timing) {
     cudaEventSynchronize(ev[8]);
     float tot_ms = 0.f;
     for (int s = 0; s < 8; ++s) {
@@ -2390,12 +2401,20 @@ int rh_segments(const rh_ctx *c, int32_t *segment_of_row) {
   return RH_OK;
 }
 
-int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
+}  // extern "C"
+
+namespace {
+// rh_set_state's work.  With a side stream, the block-only derived values
+// (unit-sweep records, tops inverses, G_p records) and `early` (e.g. the first
+// block sweeps of Hessian batches) run on `side` as soon as the block factors
+// exist, concurrently with the separator's elimination and inversion on `st`;
+// `st` joins `side` before the pivot flag is read.
+int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cudaStream_t side,
+               const std::function<int(cudaStream_t)> &early) {
   if (!c || !x || !p) return fail(c, RH_E_ARG, "null argument");
   if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
   if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
   RH_CUDA(c, cudaSetDevice(c->device));
-  cudaStream_t st = (cudaStream_t)stream;
   const Analysis &A = c->A;
   const int nx = A.n_x, np_ = A.n_p, nb = A.n_bus, m = A.n_line;
   c->has_state = c->has_mult = false;
@@ -2489,6 +2508,43 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
       fclose(fp);
     }
   }
+  // block-only values (and `early`) on the side stream while the separator is eliminated on st
+  cudaStream_t sb = side ? side : st;
+  if (side) {
+    if (!c->ev_sa) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_sa, cudaEventDisableTiming));
+    if (!c->ev_sb) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_sb, cudaEventDisableTiming));
+    RH_CUDA(c, cudaEventRecord(c->ev_sa, st));
+    RH_CUDA(c, cudaStreamWaitEvent(side, c->ev_sa, 0));
+  }
+  if (!A.gpe_src.empty()) {
+    const int ne = (int)A.gpe_src.size();
+    k_gather_gpe<<<nblk(ne), kThreads, 0, sb>>>(ne, c->gpe_src, c->gpe_row, c->gpe_col, c->gp_val, c->gpe_rec);
+    RH_LAUNCHED(c);
+  }
+  const int ngp = (int)A.gp_col.size();
+  if (ngp > 0) {
+    k_gather_vals<<<nblk(ngp), kThreads, 0, sb>>>(ngp, c->gpc_pos, c->gp_val, c->gpc_val);
+    RH_LAUNCHED(c);
+  }
+  struct GU {
+    int n;
+    const int *src;
+    double2 *dst;
+  } gu[] = {{c->nrec_f, c->uf_src_a, c->uL}, {c->nrec_f, c->uf_src_b, c->uUt}, {c->nrec_b, c->ub_src_a, c->uU}};
+  for (const GU &q : gu) {
+    if (q.n <= 0) continue;
+    k_gather_code<<<nblk(2LL * q.n), kThreads, 0, sb>>>(2 * q.n, q.src, c->F_val, reinterpret_cast<double *>(q.dst));
+    RH_LAUNCHED(c);
+  }
+  if (A.max_tops > 0) {
+    k_tops_inverse<<<A.nblk, kMaxTops * kMaxTops, 0, sb>>>(c->top_ptr, c->top_fpos_ptr, c->top_fpos, c->F_val,
+                                                           c->tL, c->tUt, c->tU, c->tLt);
+    RH_LAUNCHED(c);
+  }
+  if (early) {
+    const int rc = early(sb);
+    if (rc) return rc;
+  }
   if (A.sep_rows > 0) {
     k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, 0, st>>>(f);
     RH_LAUNCHED(c);
@@ -2543,31 +2599,14 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
       RH_LAUNCHED(c);
     }
   }
-  if (!A.gpe_src.empty()) {
-    const int ne = (int)A.gpe_src.size();
-    k_gather_gpe<<<nblk(ne), kThreads, 0, st>>>(ne, c->gpe_src, c->gpe_row, c->gpe_col, c->gp_val, c->gpe_rec);
+  if (c->nrec_b > 0) {   // L^T records: block rows' L entries below them include L_sb (R_B1)
+    k_gather_code<<<nblk(2LL * c->nrec_b), kThreads, 0, st>>>(2 * c->nrec_b, c->ub_src_b, c->F_val,
+                                                               reinterpret_cast<double *>(c->uLt));
     RH_LAUNCHED(c);
   }
-  const int ngp = (int)A.gp_col.size();
-  if (ngp > 0) {
-    k_gather_vals<<<nblk(ngp), kThreads, 0, st>>>(ngp, c->gpc_pos, c->gp_val, c->gpc_val);
-    RH_LAUNCHED(c);
-  }
-  struct GU {
-    int n;
-    const int *src;
-    double2 *dst;
-  } gu[] = {{c->nrec_f, c->uf_src_a, c->uL}, {c->nrec_f, c->uf_src_b, c->uUt},
-            {c->nrec_b, c->ub_src_a, c->uU}, {c->nrec_b, c->ub_src_b, c->uLt}};
-  for (const GU &q : gu) {
-    if (q.n <= 0) continue;
-    k_gather_code<<<nblk(2LL * q.n), kThreads, 0, st>>>(2 * q.n, q.src, c->F_val, reinterpret_cast<double *>(q.dst));
-    RH_LAUNCHED(c);
-  }
-  if (A.max_tops > 0) {
-    k_tops_inverse<<<A.nblk, kMaxTops * kMaxTops, 0, st>>>(c->top_ptr, c->top_fpos_ptr, c->top_fpos, c->F_val,
-                                                           c->tL, c->tUt, c->tU, c->tLt);
-    RH_LAUNCHED(c);
+  if (side) {
+    RH_CUDA(c, cudaEventRecord(c->ev_sb, side));
+    RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_sb, 0));
   }
   int status = 0;
   RH_CUDA(c, cudaMemcpyAsync(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -2579,6 +2618,13 @@ int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
   }
   c->has_state = true;
   return RH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
+  return state_impl(c, x, p, (cudaStream_t)stream, nullptr, nullptr);
 }
 
 int rh_residual(rh_ctx *c, double *g, double *f, void *stream) {
@@ -2660,13 +2706,25 @@ namespace {
 // latency-bound kernels); the caller's stream joins them at the end.  With Hhost
 // (non-transposed H only), every finished column block is copied to the host
 // on its batch's stream while the next batches compute.
-int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, int transposed, cudaStream_t st,
-                    double *Hhost) {
-  const int ncols = j1 - j0;
-  const int nb = (ncols + N - 1) / N;
+int num_ws(int nb) {
   int nws = kNumWs;
   if (const char *env = getenv("RH_STREAMS")) nws = std::max(1, std::min(kNumWs, atoi(env)));   // tuning override
-  nws = std::min(nws, nb);
+  return std::max(1, std::min(nws, nb));
+}
+
+// batch b of ncols columns split into nb balanced batches: [a0, a1)
+inline void batch_range(int ncols, int nb, int b, int &a0, int &a1) {
+  a0 = (int)((long long)ncols * b / nb);
+  a1 = (int)((long long)ncols * (b + 1) / nb);
+}
+
+// `early`: the first `early` batches already ran their first block sweep (phase 1,
+// workspace b) and now run the rest (phase 2)
+int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, int transposed, cudaStream_t st,
+                    double *Hhost, int early = 0) {
+  const int ncols = j1 - j0;
+  const int nb = (ncols + N - 1) / N;
+  const int nws = num_ws(nb);
   if (nws > 1) {
     if (!c->ev_fork) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     RH_CUDA(c, cudaEventRecord(c->ev_fork, st));
@@ -2677,11 +2735,13 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
     }
   }
   for (int b = 0; b < nb; ++b) {
-    const int a0 = (int)((long long)ncols * b / nb), a1 = (int)((long long)ncols * (b + 1) / nb);
+    int a0, a1;
+    batch_range(ncols, nb, b, a0, a1);
     double *out = transposed ? H + (long long)a0 * ldh : H + a0;
     const int k = b % nws;
     cudaStream_t sb = k ? c->sti[k] : st;
-    int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0, k);
+    int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0, k,
+                      b < early ? 2 : 0);
     if (rc) return rc;
     if (Hhost)
       RH_CUDA(c, cudaMemcpy2DAsync(Hhost + a0, ldh * sizeof(double), out, ldh * sizeof(double),
@@ -2713,6 +2773,51 @@ int rh_full_hessian(rh_ctx *c, int32_t N, double *H, void *stream) {
   return rh_hessian_columns(c, 0, c->A.n_p, N, H, c->A.n_p, 0, stream);
 }
 
+}  // extern "C"
+
+namespace {
+// state + reduced gradient + Hessian columns [j0, j1), with the first block
+// sweep of the first batches overlapping the separator's refactorization
+int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, int j1, int N, double *grad_p,
+                         double *H, long long ldh, int transposed, cudaStream_t st, double *Hhost) {
+  if (!c || !x || !p || !grad_p || (j1 > j0 && !H)) return fail(c, RH_E_ARG, "null argument");
+  if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
+  if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
+  const int np_ = c->A.n_p;
+  if (j0 < 0 || j1 > np_ || j0 > j1 || N <= 0) return fail(c, RH_E_ARG, "bad column range / N");
+  if ((!transposed && ldh < j1 - j0) || (transposed && ldh < np_)) return fail(c, RH_E_ARG, "ldh too small");
+  RH_CUDA(c, cudaSetDevice(c->device));
+  const int ncols = j1 - j0, nb = ncols > 0 ? (ncols + N - 1) / N : 0;
+  const int early = nb > 0 ? std::min(nb, num_ws(nb)) : 0;
+  const int ld = (N + kBC - 1) / kBC * kBC;
+  for (int k = 0; k < early; ++k)   // allocate before anything is enqueued
+    if (int rc = ensure_ws(c, ld, k)) return rc;
+  if (!c->sti[1]) RH_CUDA(c, cudaStreamCreateWithFlags(&c->sti[1], cudaStreamNonBlocking));
+  auto first_sweeps = [&](cudaStream_t sb) -> int {
+    for (int b = 0; b < early; ++b) {
+      int a0, a1;
+      batch_range(ncols, nb, b, a0, a1);
+      double *out = transposed ? H + (long long)a0 * ldh : H + a0;
+      if (int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0,
+                            b, 1))
+        return rc;
+    }
+    return RH_OK;
+  };
+  int rc = state_impl(c, x, p, st, c->sti[1], first_sweeps);
+  if (!rc) rc = rh_reduced_gradient(c, grad_p, nullptr, st);
+  if (!rc && nb > 0) rc = hessian_batches(c, j0, j1, N, H, ldh, transposed, st, Hhost, early);
+  return rc;
+}
+}  // namespace
+
+extern "C" {
+
+int rh_reduced_hessian(rh_ctx *c, const double *x, const double *p, int32_t j0, int32_t j1, int32_t N,
+                       double *grad_p, double *H, int64_t ldh, int32_t transposed, void *stream) {
+  return reduced_hessian_impl(c, x, p, j0, j1, N, grad_p, H, ldh, transposed, (cudaStream_t)stream, nullptr);
+}
+
 int rh_reduced_hessian_host(rh_ctx *c, const double *x, const double *p, int32_t N, double *grad_p, double *H) {
   if (!c || !x || !p || !H) return fail(c, RH_E_ARG, "null argument");
   if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
@@ -2732,14 +2837,11 @@ int rh_reduced_hessian_host(rh_ctx *c, const double *x, const double *p, int32_t
   double *dx = c->e2e_buf, *dp = dx + nx, *dg = dp + np_, *dH = dg + np_;
   RH_CUDA(c, cudaMemcpyAsync(dx, x, nx * 8, cudaMemcpyHostToDevice, st));
   RH_CUDA(c, cudaMemcpyAsync(dp, p, np_ * 8, cudaMemcpyHostToDevice, st));
-  int rc = rh_set_state(c, dx, dp, st);
-  if (!rc) rc = rh_reduced_gradient(c, dg, nullptr, st);
+  // state, gradient and Hessian batches (first sweeps overlapping the separator's
+  // refactorization); column blocks leave for the host as their batches finish
+  int rc = reduced_hessian_impl(c, dx, dp, 0, (int)np_, N, dg, dH, (long long)np_, 0, st, H);
   if (rc) return rc;
-  if (N <= 0) return fail(c, RH_E_ARG, "N must be positive");
   if (grad_p) RH_CUDA(c, cudaMemcpyAsync(grad_p, dg, np_ * 8, cudaMemcpyDeviceToHost, st));
-  // column blocks leave for the host as their batches finish (overlapping the later batches)
-  rc = hessian_batches(c, 0, (int)np_, N, dH, (long long)np_, 0, st, H);
-  if (rc) return rc;
   RH_CUDA(c, cudaStreamSynchronize(st));
   return RH_OK;
 }

@@ -209,3 +209,24 @@ def test_singular_pivot_reported():
     with pytest.raises(rh.RHError) as ei:
         ctx.set_state(_dev(x), _dev(p))
     assert ei.value.code in (rh.RH_E_SINGULAR,)
+
+
+def test_fused_reduced_hessian_matches_separate_calls(solved_case):
+    """rh_reduced_hessian (first block sweeps overlapping the separator's
+    refactorization) == rh_set_state + rh_reduced_gradient + rh_hessian_columns,
+    bitwise (same kernels, same per-column arithmetic order)."""
+    name, g, L, x, p, grad, lam, ops = solved_case
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g)
+    xd, pd = _dev(x), _dev(p)
+    N = {"case9": 2, "case118": 40, "case1354pegase": 200, "case2869pegase": 400}[name]
+    gf, Hf = ctx.reduced_hessian(xd, pd, N)
+    ctx.set_state(xd, pd)
+    gs, _ = ctx.reduced_gradient()
+    Hs = ctx.full_hessian(N)
+    assert np.array_equal(_np(gf), _np(gs))
+    assert np.array_equal(_np(Hf), _np(Hs))
+    assert col_rel_err(_np(Hf), red.full_hessian(ops, N)) <= TOL_H
+    j0, j1 = L.n_p // 4, L.n_p // 4 + max(1, L.n_p // 3)
+    _, Ht = ctx.reduced_hessian(xd, pd, N, j0=j0, j1=j1, transposed=True)
+    assert np.array_equal(_np(Ht).T, _np(Hs)[:, j0:j1])
