@@ -327,7 +327,7 @@ def main():
     for _ in range(2):
         e2e_once()
     te = []
-    for _ in range(max(3, args.steps // 2)):
+    for _ in range(max(5, args.steps)):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

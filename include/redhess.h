@@ -193,7 +193,8 @@ int rh_full_hessian(rh_ctx *ctx, int32_t N, double *H, void *stream);
  * rh_hessian_columns (nullable when j0 == j1).  The first block sweep of the
  * first batches (it needs only the block factors) runs on an internal stream
  * while the separator is refactorized and inverted; `stream` waits for all of
- * it.  Synchronizes `stream` once (the pivot flag, as rh_set_state).
+ * it.  Synchronizes `stream` once, at the end, to read the pivot flag: on
+ * RH_E_SINGULAR the outputs are invalid (as rh_set_state).
  * Errors: as rh_set_state and rh_hessian_columns. */
 int rh_reduced_hessian(rh_ctx *ctx, const double *x, const double *p, int32_t j0, int32_t j1, int32_t N,
                        double *grad_p, double *H, int64_t ldh, int32_t transposed, void *stream);

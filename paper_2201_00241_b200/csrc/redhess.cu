@@ -2409,8 +2409,22 @@ namespace {
 // block sweeps of Hessian batches) run on `side` as soon as the block factors
 // exist, concurrently with the separator's elimination and inversion on `st`;
 // `st` joins `side` before the pivot flag is read.
+int check_pivots(rh_ctx *c, cudaStream_t st) {   // reads the refactorization's pivot flag (one sync)
+  int status = 0;
+  RH_CUDA(c, cudaMemcpyAsync(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RH_CUDA(c, cudaStreamSynchronize(st));
+  if (status != 0) {
+    c->has_state = c->has_mult = false;
+    char buf[160];
+    snprintf(buf, sizeof buf, "refactorization: pivot of permuted row %d below 1e-14 * row max", status - 1);
+    return fail(c, RH_E_SINGULAR, buf);
+  }
+  return RH_OK;
+}
+
+// defer_check: do not read the pivot flag (the caller does, after enqueuing more work)
 int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cudaStream_t side,
-               const std::function<int(cudaStream_t)> &early) {
+               const std::function<int(cudaStream_t)> &early, bool defer_check = false) {
   if (!c || !x || !p) return fail(c, RH_E_ARG, "null argument");
   if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
   if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
@@ -2608,16 +2622,8 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     RH_CUDA(c, cudaEventRecord(c->ev_sb, side));
     RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_sb, 0));
   }
-  int status = 0;
-  RH_CUDA(c, cudaMemcpyAsync(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost, st));
-  RH_CUDA(c, cudaStreamSynchronize(st));
-  if (status != 0) {
-    char buf[160];
-    snprintf(buf, sizeof buf, "refactorization: pivot of permuted row %d below 1e-14 * row max", status - 1);
-    return fail(c, RH_E_SINGULAR, buf);
-  }
   c->has_state = true;
-  return RH_OK;
+  return defer_check ? RH_OK : check_pivots(c, st);
 }
 }  // namespace
 
@@ -2706,8 +2712,8 @@ namespace {
 // latency-bound kernels); the caller's stream joins them at the end.  With Hhost
 // (non-transposed H only), every finished column block is copied to the host
 // on its batch's stream while the next batches compute.
-int num_ws(int nb) {
-  int nws = kNumWs;
+int num_ws(int nb, int cap = kNumWs) {
+  int nws = cap;
   if (const char *env = getenv("RH_STREAMS")) nws = std::max(1, std::min(kNumWs, atoi(env)));   // tuning override
   return std::max(1, std::min(nws, nb));
 }
@@ -2724,7 +2730,9 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
                     double *Hhost, int early = 0) {
   const int ncols = j1 - j0;
   const int nb = (ncols + N - 1) / N;
-  const int nws = num_ws(nb);
+  // with host copies, 2 streams: staggered batches let finished column blocks
+  // travel while later batches compute (3 concurrent batches finish together)
+  const int nws = num_ws(nb, Hhost ? 2 : kNumWs);
   if (nws > 1) {
     if (!c->ev_fork) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     RH_CUDA(c, cudaEventRecord(c->ev_fork, st));
@@ -2788,7 +2796,7 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   if ((!transposed && ldh < j1 - j0) || (transposed && ldh < np_)) return fail(c, RH_E_ARG, "ldh too small");
   RH_CUDA(c, cudaSetDevice(c->device));
   const int ncols = j1 - j0, nb = ncols > 0 ? (ncols + N - 1) / N : 0;
-  const int early = nb > 0 ? std::min(nb, num_ws(nb)) : 0;
+  const int early = nb > 0 ? std::min(nb, num_ws(nb, Hhost ? 2 : kNumWs)) : 0;
   const int ld = (N + kBC - 1) / kBC * kBC;
   for (int k = 0; k < early; ++k)   // allocate before anything is enqueued
     if (int rc = ensure_ws(c, ld, k)) return rc;
@@ -2804,9 +2812,11 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
     }
     return RH_OK;
   };
-  int rc = state_impl(c, x, p, st, c->sti[1], first_sweeps);
+  // everything is enqueued before the one host sync (the pivot flag, read last)
+  int rc = state_impl(c, x, p, st, c->sti[1], first_sweeps, true);
   if (!rc) rc = rh_reduced_gradient(c, grad_p, nullptr, st);
   if (!rc && nb > 0) rc = hessian_batches(c, j0, j1, N, H, ldh, transposed, st, Hhost, early);
+  if (!rc) rc = check_pivots(c, st);
   return rc;
 }
 }  // namespace
