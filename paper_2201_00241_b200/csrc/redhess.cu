@@ -214,6 +214,13 @@ __global__ void k_objective(int n_bus, int ref, const int *has_gen, const double
 // without CTA barriers (warp lanes split every row update; __syncwarp orders
 // the rows of one warp).
 constexpr int kMaxTopsFact = 64;   // tops rows of a block (analysis kMaxTops <= this)
+constexpr int kFactLvl = 20;       // forward split bounds of a block (16 warps + 1, tops 2, pad)
+// byte offset of k_fact_blocks' per-row metadata: after F rows + dinv (doubles),
+// k-step records (int4 + int) and target offsets (uint16)
+__host__ __device__ inline size_t fact_meta_offset(int fo_end, int nr, int nks, int ntg) {
+  const size_t d_end = (size_t)((fo_end + nr + 1) & ~1) * 8;
+  return d_end + (size_t)nks * 20 + (size_t)ntg * 2;
+}
 constexpr int kMaxRowsFact = 1024; // rows of a block (Rmax <= this)
 __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   extern __shared__ double sm[];
@@ -229,6 +236,12 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   int4 *sks = reinterpret_cast<int4 *>(SF + d_end);
   int *skk = reinterpret_cast<int *>(sks + nks);
   unsigned short *stg = reinterpret_cast<unsigned short *>(skk + nks);
+  // per-row metadata (off, len, k-steps [begin, end)), (pivot offset in the row, F row), row order, levels
+  int4 *s_rm = reinterpret_cast<int4 *>(reinterpret_cast<char *>(sm) + ((fact_meta_offset(f.fo[fb + nr], nr, nks, ntg) + 15) & ~15));
+  int2 *s_rd = reinterpret_cast<int2 *>(s_rm + nr);
+  const int *lvg = f.fwd_lvl_ptr + f.fwd_seg_lvl[s];
+  int *s_lv = reinterpret_cast<int *>(s_rd + nr);
+  int *s_ord = s_lv + kFactLvl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   long long *prof = (f.dbg && threadIdx.x == 0) ? f.dbg + 8 * s : nullptr;
   if (prof) prof[0] = clock64();
@@ -249,36 +262,56 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     skk[t] = f.ks_k[kb + t];
   }
   for (int t = threadIdx.x; t < ntg; t += blockDim.x) stg[t] = f.tgt16[tb + t];
+  for (int a = threadIdx.x; a < nr; a += blockDim.x) {
+    const int i = f.row_global[r0 + a];
+    const int off = f.fo[fb + a];
+    s_rm[a] = make_int4(off, f.fo[fb + a + 1] - off, f.ks_ptr[r0 + a] - kb, f.ks_ptr[r0 + a + 1] - kb);
+    s_rd[a] = make_int2(f.F_diag[i] - f.F_rowptr[i], i);
+  }
+  if (threadIdx.x < kFactLvl) s_lv[threadIdx.x] = lvg[threadIdx.x] - lvg[0];
+  const int q0b = lvg[0];
+  for (int t = threadIdx.x; t < nr; t += blockDim.x) s_ord[t] = f.fwd_order[q0b + t];
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (prof) prof[1] = clock64();
   // forward split of the block: lvl[0..nw] = each warp's piece rows, lvl[nw+1..nw+2] = tops
-  const int *lv = f.fwd_lvl_ptr + f.fwd_seg_lvl[s];
+  // (block-relative row positions; s_ord maps a position to the block-local row)
+  const int *lv = s_lv;
+  // up-looking elimination of one row: every k-step's record, pivot reciprocal
+  // and target offsets are prefetched one step ahead, so the chain per k-step is
+  // the row's own values (load, scale, update, store)
   auto eliminate = [&](int q) {
-    const int a = f.fwd_order[q];
-    const int i = f.row_global[r0 + a];
-    const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off;
-    double *w = SF + off;
+    const int a = s_ord[q];
+    const int4 rm = s_rm[a];
+    const int2 rd = s_rd[a];
+    double *w = SF + rm.x;
     double amax = 0.0;
-    for (int t = lane; t < len; t += 32) amax = fmax(amax, fabs(w[t]));
+    for (int t = lane; t < rm.y; t += 32) amax = fmax(amax, fabs(w[t]));
     amax = warp_max(amax);
-    const int k1 = f.ks_ptr[r0 + a + 1] - kb;
-    for (int ks = f.ks_ptr[r0 + a] - kb; ks < k1; ++ks) {
-      const int4 m = sks[ks];
-      const double lik = w[m.x] * sdinv[skk[ks]];
+    const int k1 = rm.w;
+    int ks = rm.z;
+    int4 m = ks < k1 ? sks[ks] : make_int4(0, 0, 0, 0);
+    double dk = ks < k1 ? sdinv[skk[ks]] : 0.0;
+    for (; ks < k1; ++ks) {
+      const int4 mn = ks + 1 < k1 ? sks[ks + 1] : m;
+      const double dkn = ks + 1 < k1 ? sdinv[skk[ks + 1]] : 0.0;
+      const int tgl = lane < m.z ? stg[m.w + lane] : 0;
+      const double ukl = lane < m.z ? SF[m.y + 1 + lane] : 0.0;
+      const double lik = w[m.x] * dk;
       __syncwarp();
       if (lane == 0) w[m.x] = lik;
-      const double *uk = SF + m.y + 1;
-      const unsigned short *tg = stg + m.w;
-      for (int t = lane; t < m.z; t += 32) w[tg[t]] -= lik * uk[t];
+      if (lane < m.z) w[tgl] -= lik * ukl;
+      for (int t = lane + 32; t < m.z; t += 32) w[stg[m.w + t]] -= lik * SF[m.y + 1 + t];
       __syncwarp();
+      m = mn;
+      dk = dkn;
     }
-    const double piv = w[f.F_diag[i] - f.F_rowptr[i]];
+    const double piv = w[rd.x];
     if (lane == 0) {
       const double di = 1.0 / piv;
       sdinv[a] = di;
-      f.dinv[i] = di;
-      if (!(fabs(piv) > f.pivtol * amax)) atomicMax(f.status, i + 1);
+      f.dinv[rd.y] = di;
+      if (!(fabs(piv) > f.pivtol * amax)) atomicMax(f.status, rd.y + 1);
     }
     __syncwarp();
   };
@@ -300,7 +333,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     for (int a = threadIdx.x; a < nr; a += blockDim.x) s_tflag[a] = 0;
     __syncthreads();
     for (int t = threadIdx.x; t < ntq; t += blockDim.x) {
-      s_topq[t] = f.fwd_order[tq0 + t];
+      s_topq[t] = s_ord[tq0 + t];
       s_tflag[s_topq[t]] = 1;
     }
     __syncthreads();
@@ -317,14 +350,15 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     };
     for (int t = warp; t < ntq; t += nw) {   // T1
       const int a = s_topq[t];
-      const int off = f.fo[fb + a], len = f.fo[fb + a + 1] - off;
+      const int4 rm = s_rm[a];
+      const int off = rm.x, len = rm.y;
       double *w = SF + off;
       double amax = 0.0;
       for (int u = lane; u < len; u += 32) amax = fmax(amax, fabs(w[u]));
       amax = warp_max(amax);
-      const int k1 = f.ks_ptr[r0 + a + 1] - kb;
+      const int k1 = rm.w;
       int first_top = k1;
-      for (int ks = f.ks_ptr[r0 + a] - kb; ks < k1; ++ks) {
+      for (int ks = rm.z; ks < k1; ++ks) {
         if (is_top(skk[ks])) {
           first_top = min(first_top, ks);
           continue;
@@ -334,8 +368,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
       if (lane == 0) {
         s_cur[t] = first_top;
         s_amax[t] = amax;
-        const int i = f.row_global[r0 + a];
-        s_trow[t] = make_int4(i, off, off + (f.F_diag[i] - f.F_rowptr[i]), k1);
+        s_trow[t] = make_int4(s_rd[a].y, off, off + s_rd[a].x, k1);
       }
     }
     __syncthreads();
@@ -1738,7 +1771,8 @@ int fail(rh_ctx *c, int code, const std::string &msg) {
 inline int nblk(long long n, int t = kThreads) { return (int)((n + t - 1) / t); }
 
 size_t fact_smem_bytes(const Analysis &A) {
-  return (size_t)(A.max_blk_fnnz + A.rmax + 2) * 8 + (size_t)A.max_blk_ks * 20 + (size_t)A.max_blk_tgt * 2 + 64;
+  return (size_t)(A.max_blk_fnnz + A.rmax + 2) * 8 + (size_t)A.max_blk_ks * 20 + (size_t)A.max_blk_tgt * 2 + 64 +
+         16 + (size_t)A.rmax * (16 + 8 + 4) + kFactLvl * 4 + 64;   // per-row metadata
 }
 
 size_t blk_smem_layout(const Analysis &A, int *off7);
