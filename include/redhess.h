@@ -62,7 +62,8 @@ typedef enum rh_status {
   RH_E_SINGULAR = 4,  /* refactorization pivot below threshold (static pivots, R15)  */
   RH_E_CUDA = 5,      /* CUDA runtime error (message in rh_last_error)               */
   RH_E_NOMEM = 6,     /* device allocation failed                                    */
-  RH_E_NODEV = 7      /* compute call on a host-only context (device = -1)           */
+  RH_E_NODEV = 7,     /* compute call on a host-only context (device = -1)           */
+  RH_E_NOCONV = 8     /* Newton projection did not converge within maxit steps       */
 } rh_status;
 
 /* Bus type codes (MATPOWER): PQ = 1, PV = 2, REF = 3. */
@@ -159,6 +160,21 @@ int rh_reduced_gradient(rh_ctx *ctx, double *grad_p, double *lambda_out, void *s
 /* Override the active multipliers with lambda [n_x] (DEVICE).  Subsequent
  * HVPs return S^T grad^2 l(lambda) S W with S = [-J^{-1} G_p; I] (R16). */
 int rh_set_multipliers(rh_ctx *ctx, const double *lambda, void *stream);
+
+/* Newton-Raphson projection x(p) (Sec. 3.2; SURVEY.md 8(f)
+ * NEXT-1): x_{k+1} = x_k - J_k^{-1} g(x_k, p).  x [n_x] DEVICE, in: initial
+ * guess x_0, out: the solution; p [n_p] DEVICE.  Each step runs the state,
+ * assembly and refactorization of rh_set_state at x_k and one device solve
+ * J_k dx = g_k (block L sweep, separator S^-1, block U sweep on one column).
+ * Stops `extra` steps after the first step with max|dx| <= tol (the oracle's
+ * rule: quadratic convergence puts those steps on the rounding floor).  On
+ * return the state (g, factors) is set at the final x, so rh_residual,
+ * rh_reduced_gradient and the Hessian calls follow directly (multipliers are
+ * invalidated).  iters (host, nullable): steps taken; resid (host, nullable):
+ * max|g| at the final x.  Synchronizes `stream` once per step.
+ * Errors: RH_E_SINGULAR (as rh_set_state), RH_E_NOCONV after maxit steps. */
+int rh_newton(rh_ctx *ctx, double *x, const double *p, double tol, int32_t extra, int32_t maxit,
+              int32_t *iters, double *resid, void *stream);
 
 /* Batched reduced Hessian-vector products, Alg. 2:
  * W [n_p][ldw] (DEVICE, read), HW [n_p][ldhw] (DEVICE, written), N directions,

@@ -18,14 +18,15 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libredhess.so")
 
-RH_OK, RH_E_ARG, RH_E_GRID, RH_E_ORDER, RH_E_SINGULAR, RH_E_CUDA, RH_E_NOMEM, RH_E_NODEV = range(8)
+RH_OK, RH_E_ARG, RH_E_GRID, RH_E_ORDER, RH_E_SINGULAR, RH_E_CUDA, RH_E_NOMEM, RH_E_NODEV, RH_E_NOCONV = range(9)
 STATUS_NAMES = {0: "RH_OK", 1: "RH_E_ARG", 2: "RH_E_GRID", 3: "RH_E_ORDER", 4: "RH_E_SINGULAR",
-                5: "RH_E_CUDA", 6: "RH_E_NOMEM", 7: "RH_E_NODEV"}
+                5: "RH_E_CUDA", 6: "RH_E_NOMEM", 7: "RH_E_NODEV", 8: "RH_E_NOCONV"}
 KIND_THETA, KIND_V, KIND_PG = 0, 1, 2
 
 # every symbol declared in include/redhess.h (checked by tests/test_abi.py)
 EXPORTS = ["rh_create", "rh_destroy", "rh_last_error", "rh_load_grid", "rh_get_info", "rh_orderings",
            "rh_symbolic", "rh_segments", "rh_set_state", "rh_residual", "rh_reduced_gradient", "rh_set_multipliers",
+           "rh_newton",
            "rh_hvp", "rh_hvp_stages", "rh_hessian_columns", "rh_full_hessian", "rh_reduced_hessian",
            "rh_reduced_hessian_host",
            "rh_launch_count", "rh_set_timing", "rh_stage_times"]
@@ -74,6 +75,7 @@ def _load():
         "rh_residual": ([vp, vp, vp, vp], ctypes.c_int),
         "rh_reduced_gradient": ([vp, vp, vp, vp], ctypes.c_int),
         "rh_set_multipliers": ([vp, vp, vp], ctypes.c_int),
+        "rh_newton": ([vp, vp, vp, dbl, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(dbl), vp], ctypes.c_int),
         "rh_hvp": ([vp, vp, i64, vp, i64, i32, vp], ctypes.c_int),
         "rh_hvp_stages": ([vp, vp, i64, vp, i64, i32, vp, vp, vp, i64, vp], ctypes.c_int),
         "rh_hessian_columns": ([vp, i32, i32, i32, vp, i64, i32, vp], ctypes.c_int),
@@ -270,6 +272,16 @@ class RedHess:
         return H
 
     # ------------------------------------------------------------------ compute (host buffers)
+    def newton(self, x, p, tol=1e-11, extra=2, maxit=40, stream=None):
+        """rh_newton: Newton-Raphson projection x(p) in place on the DEVICE vector x; returns (steps, max|g|)."""
+        _check_dev(x, self.n_x, "x")
+        _check_dev(p, self.n_p, "p")
+        it = ctypes.c_int32(0)
+        res = ctypes.c_double(0.0)
+        self._rc(lib().rh_newton(self._h, _ptr(x), _ptr(p), float(tol), int(extra), int(maxit), ctypes.byref(it),
+                                 ctypes.byref(res), _stream(stream)))
+        return it.value, res.value
+
     def reduced_hessian(self, x, p, N, j0=0, j1=None, grad=None, H=None, transposed=False, stream=None):
         """rh_reduced_hessian: state + reduced gradient + Hessian columns [j0, j1) in one call (DEVICE)."""
         import torch

@@ -843,7 +843,9 @@ enum : int {
   MODE_U = 2,     // blocks:    U sweep                                        -> Z
   MODE_UT = 3,    // blocks:    U^T sweep on -Y_x                              -> P
   MODE_UTLT = 4,  // separator: -Y_x - U_bs^T P_b, then S^-T                   -> P
-  MODE_LT = 5     // blocks:    L^T sweep                                      -> P = Psi
+  MODE_LT = 5,    // blocks:    L^T sweep                                      -> P = Psi
+  MODE_LX = 6,    // blocks:    L sweep, right-hand side loaded from Z (Newton)   -> Z
+  MODE_LUX = 7    // separator: rhs from Z - L_sb Z_b (Newton), then S^-1        -> Z
 };
 
 __device__ __forceinline__ double rhs_gpw(const SegParams &h, int row, int col) {
@@ -1075,11 +1077,12 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
   __shared__ __align__(8) unsigned long long mbar;
   __shared__ int s_tk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const bool fwd = mode == MODE_L || mode == MODE_UT;
+  const bool fwd = mode == MODE_L || mode == MODE_UT || mode == MODE_LX;
   const DUnit &U = fwd ? h.uf : h.ub;
-  const double2 *vals = mode == MODE_L ? h.uL : mode == MODE_U ? h.uU : mode == MODE_UT ? h.uUt : h.uLt;
+  const bool lsw = mode == MODE_L || mode == MODE_LX;   // L values
+  const double2 *vals = lsw ? h.uL : mode == MODE_U ? h.uU : mode == MODE_UT ? h.uUt : h.uLt;
   const bool dinv = mode == MODE_U || mode == MODE_UT;
-  double *G = mode <= MODE_U ? h.Z : h.P;
+  double *G = (mode <= MODE_U || mode == MODE_LX) ? h.Z : h.P;
   int *ctr = h.blk_ctr + 2 * mode;
   const int nch = h.ld / kBC;
   const int ntiles = h.nblk * nch;
@@ -1114,7 +1117,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     const int ob = U.doff_off[s], nof = U.doff_off[s + 1] - ob;
     const int nxrows = mode == MODE_L ? 0 : nr + nxr;
     if (tid == 0) {
-      const double *dM = mode == MODE_L ? h.tL : mode == MODE_U ? h.tU : mode == MODE_UT ? h.tUt : h.tLt;
+      const double *dM = lsw ? h.tL : mode == MODE_U ? h.tU : mode == MODE_UT ? h.tUt : h.tLt;
       const unsigned tx = 16u * (nu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + 32u * kTopLd * 8 + 128u +
                           (mode == MODE_L ? 16u * (h.gpe_off[s + 1] - h.gpe_off[s]) + 48u : 0u);
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx)
@@ -1210,8 +1213,9 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
   const int qb = h.fwd.lvl_ptr[h.fwd.seg_lvl[seg]], qe = h.fwd.lvl_ptr[h.fwd.seg_lvl[seg + 1] - 1];
   const int q = qb + qoff;
   if (q >= qe) return;
-  double *G = mode == MODE_LU ? h.Z : h.P;
-  const double *val = mode == MODE_LU ? h.vL : h.vUt;
+  const bool lu = mode == MODE_LU || mode == MODE_LUX;
+  double *G = lu ? h.Z : h.P;
+  const double *val = lu ? h.vL : h.vUt;
   const int a = h.fwd.order[q];
   const int row = h.row_global[h.sep_off + a];
   const double v0 = mode == MODE_LU ? rhs_gpw(h, row, col) : G[(long long)(h.sep_off + a) * h.ld + col];
@@ -1555,6 +1559,40 @@ __global__ void k_unpermute(int n_x, int N, int ld, const int *pinv, const doubl
 }
 
 // ============================================================================
+// Newton-Raphson projection x(p):
+// the right-hand side g in Z-row order (column 0 of the one-column block), and
+// the update x <- x - dx with max|dx|
+// ============================================================================
+__global__ void k_newton_rhs(int n_x, const int *__restrict__ zmap, const double *__restrict__ g, double *X) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n_x) X[(long long)zmap[k] * kSegC] = g[k];
+}
+
+__device__ __forceinline__ void atomic_max_nonneg(double *addr, double v) {   // v >= 0: bit order = value order
+  atomicMax(reinterpret_cast<unsigned long long *>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+__global__ void k_newton_update(int n_x, const int *__restrict__ zmap, const double *__restrict__ X, double *x,
+                                double *dmax) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  double m = 0.0;
+  if (k < n_x) {
+    const double dx = X[(long long)zmap[k] * kSegC];
+    x[k] -= dx;
+    m = fabs(dx);
+  }
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(dmax, m);
+}
+
+__global__ void k_absmax(int n, const double *__restrict__ v, double *out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  double m = k < n ? fabs(v[k]) : 0.0;
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out, m);
+}
+
+// ============================================================================
 // first-order adjoint + reduced gradient, single column
 // ============================================================================
 
@@ -1676,6 +1714,7 @@ struct rh_ctx {
   int *sb_src, *sb_dense;
   double *Sbuf = nullptr;   // ping-pong partner of Sinv in k_sep_inverse
   double *gj_dbuf = nullptr;   // [2][32][32] next panel's diagonal inverse (lookahead CTA)
+  double *nwt = nullptr;       // Newton: max|dx|, max|g| (device scalars)
   unsigned *grid_bar = nullptr;
   int coop_blocks = 1;
   double *dinv_rows, *rowmax;
@@ -2009,6 +2048,7 @@ int upload(rh_ctx *c) {
   chk(c->Sbuf = dalloc<double>(std::max<size_t>(ns2, 1), P));
   chk(c->grid_bar = dalloc<unsigned>(2, P));
   chk(c->gj_dbuf = dalloc<double>(2 * 32 * 32, P));
+  chk(c->nwt = dalloc<double>(4, P));
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
   // shared-memory footprints
   c->smem_fact_blk = fact_smem_bytes(A);
@@ -2719,6 +2759,66 @@ int rh_set_multipliers(rh_ctx *c, const double *lambda, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   RH_CUDA(c, cudaMemcpyAsync(c->lam, lambda, sizeof(double) * c->A.n_x, cudaMemcpyDeviceToDevice, st));
   return build_tape(c, st);
+}
+
+int rh_newton(rh_ctx *c, double *x, const double *p, double tol, int32_t extra, int32_t maxit, int32_t *iters,
+              double *resid, void *stream) {
+  if (!c || !x || !p || maxit <= 0 || extra < 0 || !(tol >= 0.0)) return fail(c, RH_E_ARG, "bad argument");
+  if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
+  if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
+  RH_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const Analysis &A = c->A;
+  if (int rc = ensure_tsep(c, kSegC)) return rc;
+  int left = -1, it = 0;
+  bool done = false;
+  for (; it < maxit && !done; ++it) {
+    // state, assembly and refactorization at x_k (g_k in c->g, factors of J_k)
+    if (int rc = state_impl(c, x, p, st, nullptr, nullptr)) return rc;
+    // J_k dx = g_k: block L sweep and separator (S^-1) on the loaded right-hand side, then U
+    k_newton_rhs<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->pinv, c->g, c->X1col);
+    RH_LAUNCHED(c);
+    SegParams h = make_params(c);
+    h.N = 1;
+    h.ld = kSegC;
+    h.Z = c->X1col;
+    const int g1 = std::min(2 * c->nsm, A.nblk);
+    k_blk<<<g1, kBlkThreads, c->smem_blk, st>>>(h, MODE_LX);
+    RH_LAUNCHED(c);
+    if (A.sep_rows > 0) {
+      k_sep_gather<<<dim3(nblk(A.sep_rows, kThreads / 32), 1), kThreads, 0, st>>>(h, MODE_LUX);
+      RH_LAUNCHED(c);
+      k_sep_gemv<<<nblk(A.sep_rows, kThreads / 32), kThreads, 0, st>>>(h, MODE_LU);
+      RH_LAUNCHED(c);
+    }
+    k_blk<<<g1, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
+    RH_LAUNCHED(c);
+    // x_{k+1} = x_k - dx, max|dx|
+    RH_CUDA(c, cudaMemsetAsync(c->nwt, 0, sizeof(double), st));
+    k_newton_update<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->pinv, c->X1col, x, c->nwt);
+    RH_LAUNCHED(c);
+    double dmax = 0.0;
+    RH_CUDA(c, cudaMemcpyAsync(&dmax, c->nwt, sizeof(double), cudaMemcpyDeviceToHost, st));
+    RH_CUDA(c, cudaStreamSynchronize(st));
+    // the oracle's stopping rule: `extra` more steps after max|dx| <= tol
+    if (left < 0 && dmax <= tol) left = extra;
+    if (left >= 0) {
+      if (left == 0) done = true;
+      else --left;
+    }
+  }
+  if (iters) *iters = it;
+  if (!done) return fail(c, RH_E_NOCONV, "Newton did not converge within maxit steps");
+  // leave the state (g, factors) at the final x
+  if (int rc = state_impl(c, x, p, st, nullptr, nullptr)) return rc;
+  if (resid) {
+    RH_CUDA(c, cudaMemsetAsync(c->nwt + 1, 0, sizeof(double), st));
+    k_absmax<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->g, c->nwt + 1);
+    RH_LAUNCHED(c);
+    RH_CUDA(c, cudaMemcpyAsync(resid, c->nwt + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+    RH_CUDA(c, cudaStreamSynchronize(st));
+  }
+  return RH_OK;
 }
 
 int rh_hvp(rh_ctx *c, const double *W, int64_t ldw, double *HW, int64_t ldhw, int32_t N, void *stream) {

@@ -230,3 +230,41 @@ def test_fused_reduced_hessian_matches_separate_calls(solved_case):
     j0, j1 = L.n_p // 4, L.n_p // 4 + max(1, L.n_p // 3)
     _, Ht = ctx.reduced_hessian(xd, pd, N, j0=j0, j1=j1, transposed=True)
     assert np.array_equal(_np(Ht).T, _np(Hs)[:, j0:j1])
+
+
+def test_newton_projection_matches_oracle(solved_case):
+    """rh_newton vs the oracle's Newton from the same x0 and
+    the same stopping rule: same solution, same step count (+-1), and the state
+    it leaves behind gives the oracle's reduced gradient at x(p)."""
+    name, g, L, x, p, grad, lam, ops = solved_case
+    rng = np.random.default_rng(42)
+    x0 = x + 0.01 * rng.standard_normal(x.size)   # perturbed angles and voltages
+    xo = pf.newton(g, p, x0, L)
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g)
+    xd = _dev(x0)
+    steps, res = ctx.newton(xd, _dev(p))
+    xg = _np(xd)
+    assert np.max(np.abs(xg - xo)) <= 1e-10 * max(1.0, np.max(np.abs(xo))), name
+    assert res <= 1e-10
+    gd, _ = ctx.reduced_gradient()
+    go, _ = red.reduced_gradient(g, xo, p, L)
+    assert np.max(np.abs(_np(gd) - go)) <= 1e-9 * np.max(np.abs(go))
+
+
+def test_newton_from_unsolved_point():
+    """From the generator's unsolved point (loads not backed out, g != 0):
+    both Newtons converge to the same x(p) of the grid's own loads."""
+    g2 = gridgen.make_grid("case118", tap_line=True)
+    L = pf.Layout(g2)
+    x0, p = pf.state_vectors(g2, L)
+    xo = pf.newton(g2, p, x0, L)
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g2)
+    xd = _dev(x0)
+    steps, res = ctx.newton(xd, _dev(p))
+    assert np.max(np.abs(_np(xd) - xo)) <= 1e-10 * max(1.0, np.max(np.abs(xo)))
+    assert res <= 1e-10 and steps >= 3
+    with pytest.raises(rh.RHError) as e:   # one step cannot satisfy a zero tolerance with extra steps
+        ctx.newton(_dev(x0), _dev(p), tol=0.0, extra=2, maxit=1)
+    assert e.value.code == rh.RH_E_NOCONV
