@@ -282,6 +282,22 @@ def main():
     ms_hess = tt[1].item() / args.steps
     ms_pre = tt[2].item() / args.steps
 
+    # ---- Newton projection x(p) from a perturbed solution
+    x_pert = x + 1e-3 * torch.from_numpy(np.random.default_rng(7).standard_normal(n_x)).to(dev)
+    xw = torch.empty_like(x)
+    newton_ms, newton_steps = [], 0
+    for rep in range(4):
+        xw.copy_(x_pert)
+        torch.cuda.synchronize()
+        t0n = time.perf_counter()
+        newton_steps, newton_res = ctx.newton(xw, p)
+        torch.cuda.synchronize()
+        if rep:
+            newton_ms.append((time.perf_counter() - t0n) * 1e3)
+    newton_err = float((xw - x).abs().max().item())
+    ctx.set_state(x, p)
+    ctx.reduced_gradient(grad)
+
     # ---- batched HVP throughput (random W, width N, weak scaling: each GPU its own W)
     W = torch.from_numpy(gridgen.random_W(n_p, N, seed=1 + rank)).to(dev)
     HW = torch.empty_like(W)
@@ -411,6 +427,9 @@ def main():
                              ["A_L", "B_LU", "A_U", "FoR", "A_Ut", "B_UtLt", "A_Lt", "MulAdd", "total"], stage)},
                          "path_m2_gbs": path_gbs, "path_m2_frac": (path_gbs / peak) if path_gbs else None,
                          "path_model": "M2 (6 n_x + 5 n_p) * 8 B per HVP (SURVEY.md 8(d))"},
+            "newton": {"ms": float(np.median(newton_ms)), "steps": newton_steps, "resid_inf": newton_res,
+                       "max_abs_x_err": newton_err,
+                       "start": "solved x + 1e-3 N(0,1) (seed 7; from 1e-2 the oracle diverges too on case9241); tol 1e-11, 2 extra steps (oracle rule); host wall clock incl. one max|dx| readback per step"},
             "cpu_baseline": cpu,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         }

@@ -2800,6 +2800,7 @@ int rh_newton(rh_ctx *c, double *x, const double *p, double tol, int32_t extra, 
     double dmax = 0.0;
     RH_CUDA(c, cudaMemcpyAsync(&dmax, c->nwt, sizeof(double), cudaMemcpyDeviceToHost, st));
     RH_CUDA(c, cudaStreamSynchronize(st));
+    if (getenv("RH_DEBUG") && (atoi(getenv("RH_DEBUG")) & 256)) fprintf(stderr, "newton step %d: max|dx| %.3e\n", it, dmax);
     // the oracle's stopping rule: `extra` more steps after max|dx| <= tol
     if (left < 0 && dmax <= tol) left = extra;
     if (left >= 0) {
