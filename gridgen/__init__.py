@@ -318,3 +318,32 @@ def permute_buses(grid: Grid, perm: np.ndarray) -> Grid:
     g.line_t = inv[grid.line_t].astype(np.int32)
     g.gen_bus = inv[grid.gen_bus].astype(np.int32)
     return g
+
+
+def load_scenario(grid: Grid, T: int, amp: float = 0.05, kind: str = "sin", seed: int = 0,
+                  sigma: float = 0.2):
+    """Seeded load time series w_t = (Pd_t, Qd_t), t = 0..T-1, for the tracking
+    workload (loads "updated every minute"; the paper does
+    not give their evolution, DESIGN.md R-T3).  Every load stays within
+    +-amp of its base value: Pd_t[b] = Pd[b] (1 + amp s_t[b]), s_t[b] in [-1, 1].
+
+      kind "sin":  s_t[b] = 0.7 sin(2 pi t / T) + 0.3 sin(2 pi t / T + phi_b)
+      kind "walk": s_t[b] = clip(s_{t-1}[b] + sigma N(0,1), -1, 1), s_{-1} = 0
+    Returns (Pd [T][n_bus], Qd [T][n_bus]) float64."""
+    rng = np.random.default_rng(seed)
+    n = np.asarray(grid.Pd).shape[0]
+    tt = np.arange(T, dtype=np.float64)[:, None]
+    if kind == "sin":
+        phi = rng.uniform(0.0, 2.0 * np.pi, n)[None, :]
+        s = 0.7 * np.sin(2.0 * np.pi * tt / T) + 0.3 * np.sin(2.0 * np.pi * tt / T + phi)
+    elif kind == "walk":
+        s = np.zeros((T, n))
+        cur = np.zeros(n)
+        for k in range(T):
+            cur = np.clip(cur + sigma * rng.standard_normal(n), -1.0, 1.0)
+            s[k] = cur
+    else:
+        raise ValueError("kind must be 'sin' or 'walk'")
+    Pd = np.asarray(grid.Pd, np.float64)[None, :] * (1.0 + amp * s)
+    Qd = np.asarray(grid.Qd, np.float64)[None, :] * (1.0 + amp * s)
+    return Pd, Qd

@@ -19,5 +19,7 @@ Modules:
                 Eq. powerflowvec, Eq. lagrangian)
   reduction  -- reduced gradient, Alg. 1, Alg. 2, full Hessian, dense definition
                 (PAPER.md 3.3, 4.1-4.3, Eq. socadjoint, Eq. hessvecprod)
+  tracking   -- the real-time tracking step: Newton, g_t, H_t, dense Cholesky
+                solve of Eq. qp_rto (PAPER.md 6.3)
 """
-from . import powerflow, reduction  # noqa: F401
+from . import powerflow, reduction, tracking  # noqa: F401

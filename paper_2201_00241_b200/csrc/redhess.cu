@@ -19,6 +19,7 @@
 #include "../../include/redhess.h"
 #include "analysis.hpp"
 #include "kernels.cuh"
+#include "devutil.cuh"
 
 using namespace rh;
 
@@ -26,14 +27,6 @@ using namespace rh;
 // device helpers
 // ============================================================================
 
-__device__ __forceinline__ int ld_acquire(const int *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(int *p, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 __device__ __forceinline__ double warp_max(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -452,37 +445,7 @@ __global__ void k_sep_dense(int nslots, const int *__restrict__ src, const int *
   if (t < nslots) S[dpos[t]] = F[src[t]];
 }
 
-// 1/x to ~1 ulp: hardware approximation + two Newton steps (pivot reciprocals
-// on the Gauss-Jordan critical path; static pivots, R15)
-__device__ __forceinline__ double fast_rcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
-// Grid-wide barrier of a cooperative launch (all CTAs co-resident): arrival
-// counter + generation word; the last arrival resets the counter and bumps the
-// generation.  `gen` is the generation this CTA waits to leave.
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
-    } else {
-      while ((unsigned)ld_acquire(reinterpret_cast<const int *>(&bar[1])) == gen) {
-      }
-    }
-    __threadfence();
-  }
-  ++gen;
-  __syncthreads();
-}
 
 // Blocked Gauss-Jordan inverse of the dense separator block S in ONE
 // persistent cooperative launch (replaces 2 launches per panel).  Per panel K
@@ -963,11 +926,6 @@ __device__ __forceinline__ void unit_pieces(const UStage &t, char *Xb, int warp)
 constexpr int kBlkThreads = UnitSweep::kWarps * 32;
 constexpr int kTopsLvl = UnitSweep::kWarps + 1;   // lvl[kWarps + 1], lvl[kWarps + 2]: tops units
 static_assert(UnitSweep::kMaxTopUnits <= 2 * UnitSweep::kWarps, "two tops units per warp at most");
-__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 __device__ __forceinline__ void unit_tops(const UStage &t, char *Xb, const double *X, int warp, int lane) {
   const int u0 = t.lvl[kTopsLvl], u1 = t.lvl[kTopsLvl + 1];
   if (u0 >= u1) return;
