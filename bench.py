@@ -176,6 +176,78 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- ours
 
+def backout_loads_lib(rh, ctx, grid, x, p):
+    """Make (x, p) a power-flow solution: shift the loads by the library's own
+    residual g(x, p) (g is linear in Pd, Qd, R2) and reload the grid."""
+    ctx.set_state(x, p)
+    g_res, _ = ctx.residual()
+    g_np = g_res.cpu().numpy()
+    xb, xk, _, _ = ctx.orderings()
+    grid.Pd = grid.Pd.copy()
+    grid.Qd = grid.Qd.copy()
+    th_rows = xk == rh.KIND_THETA
+    grid.Pd[xb[th_rows]] -= g_np[th_rows]
+    grid.Qd[xb[~th_rows]] -= g_np[~th_rows]
+    ctx.load_grid(grid)
+
+
+PAPER_TABLE3 = {"case": "case1354pegase", "N": 256, "gpu_s": [0.05, 0.05, 0.10], "cpu_s": [1.41, 0.81, 2.22],
+                "hardware": "V100 / Xeon (PAPER.md Table 3)"}
+
+
+def tracking_bench(rh, gridgen, dev, case, N, minutes, warm=2, T=60):
+    """Real-time tracking (Table 3): one
+    rh_tracking_step per minute of a +-5 % per-bus-phase load series (seed 4),
+    free controls = the generator set points (R-T2), from the optimum of the
+    base loads (loads and linear costs backed out with the library's residual
+    and reduced gradient, R-T5).  Step 1 = loads + Newton x(p_t; w_t) + g_t +
+    H_t columns; Step 2 = dense Cholesky solve + p update (CUDA events on the
+    stream, host syncs inside included)."""
+    import torch
+    grid = gridgen.tracking_grid(case)
+    ctx = rh.RedHess(dev.index)
+    n_x, n_p = ctx.load_grid(grid)
+    x_np, p_np = ctx.state_vectors(grid)
+    x = torch.from_numpy(x_np).to(dev)
+    p = torch.from_numpy(p_np).to(dev)
+    backout_loads_lib(rh, ctx, grid, x, p)
+    _, _, pb, pk = ctx.orderings()
+    n_pv = int(np.sum(pk == rh.KIND_PG))
+    assert np.all(pk[:n_pv] == rh.KIND_PG)
+    ctx.set_state(x, p)
+    grad = torch.empty(n_p, dtype=torch.float64, device=dev)
+    ctx.reduced_gradient(grad)
+    g_np = grad.cpu().numpy()
+    gen_of_bus = {int(b): i for i, b in enumerate(grid.gen_bus)}
+    grid.c1 = np.array(grid.c1, dtype=np.float64)
+    for k in range(n_pv):                       # dF/dPg_k contains c1 with coefficient 1
+        grid.c1[gen_of_bus[int(pb[k])]] -= g_np[k]
+    ctx.load_grid(grid)
+    Pd, Qd = gridgen.load_scenario(grid, T, amp=0.05, kind="sin", seed=4)
+    Pd_d = torch.from_numpy(Pd).to(dev)
+    Qd_d = torch.from_numpy(Qd).to(dev)
+    H = torch.empty((n_pv, n_p), dtype=torch.float64, device=dev)
+    d = torch.empty(n_pv, dtype=torch.float64, device=dev)
+    recs = []
+    for t in range(warm + minutes):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, _, info = ctx.tracking_step(x, p, N, Pd=Pd_d[t % T], Qd=Qd_d[t % T], j0=0, j1=n_pv, grad=grad, H=H,
+                                          d=d)
+        wall = (time.perf_counter() - t0) * 1e3
+        if t >= warm:
+            recs.append((info, wall))
+    med = lambda k: float(np.median([r[0][k] for r in recs]))
+    return {"case": case, "N": N, "n_free": n_pv, "n_p": n_p, "minutes": minutes,
+            "ms_step1": med("ms_step1"), "ms_step2": med("ms_step2"),
+            "ms_total": float(np.median([r[0]["ms_step1"] + r[0]["ms_step2"] for r in recs])),
+            "wall_ms": float(np.median([r[1] for r in recs])),
+            "newton_steps": med("newton_steps"), "max_tau": float(max(r[0]["tau"] for r in recs)),
+            "max_abs_d": float(d.abs().max().item()),
+            "workload": "tracking_grid (smooth voltages), loads + c1 backed out at the base point, "
+                        "+-5 % per-bus-phase sinusoidal loads (seed 4), free = Pg set points"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -204,16 +276,7 @@ def main():
     p = torch.from_numpy(p_np).to(dev)
     # solved operating point: back the loads out with the library's own residual
     # (loads enter the path only through Pd_ref, R17)
-    ctx.set_state(x, p)
-    g_res, _ = ctx.residual()
-    g_np = g_res.cpu().numpy()
-    xb, xk, _, _ = ctx.orderings()
-    grid.Pd = grid.Pd.copy()
-    grid.Qd = grid.Qd.copy()
-    th_rows = xk == rh.KIND_THETA
-    grid.Pd[xb[th_rows]] -= g_np[th_rows]
-    grid.Qd[xb[~th_rows]] -= g_np[~th_rows]
-    ctx.load_grid(grid)
+    backout_loads_lib(rh, ctx, grid, x, p)
     ctx.set_state(x, p)
     g_res, _ = ctx.residual()
     resid_inf = float(g_res.abs().max().item())
@@ -297,6 +360,14 @@ def main():
     newton_err = float((xw - x).abs().max().item())
     ctx.set_state(x, p)
     ctx.reduced_gradient(grad)
+
+    # ---- real-time tracking: the paper's Table 3 case, and this case
+    tracking = None
+    if world == 1:
+        tracking = {"table3": tracking_bench(rh, gridgen, dev, "case1354pegase", 256, 10),
+                    "paper": PAPER_TABLE3}
+        if case != "case1354pegase":
+            tracking[case] = tracking_bench(rh, gridgen, dev, case, N, 5)
 
     # ---- batched HVP throughput (random W, width N, weak scaling: each GPU its own W)
     W = torch.from_numpy(gridgen.random_W(n_p, N, seed=1 + rank)).to(dev)
@@ -430,6 +501,7 @@ def main():
             "newton": {"ms": float(np.median(newton_ms)), "steps": newton_steps, "resid_inf": newton_res,
                        "max_abs_x_err": newton_err,
                        "start": "solved x + 1e-3 N(0,1) (seed 7; from 1e-2 the oracle diverges too on case9241); tol 1e-11, 2 extra steps (oracle rule); host wall clock incl. one max|dx| readback per step"},
+            "tracking": tracking,
             "cpu_baseline": cpu,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         }

@@ -327,7 +327,9 @@ def load_scenario(grid: Grid, T: int, amp: float = 0.05, kind: str = "sin", seed
     not give their evolution, DESIGN.md R-T3).  Every load stays within
     +-amp of its base value: Pd_t[b] = Pd[b] (1 + amp s_t[b]), s_t[b] in [-1, 1].
 
-      kind "sin":  s_t[b] = 0.7 sin(2 pi t / T) + 0.3 sin(2 pi t / T + phi_b)
+      kind "sin":  s_t[b] = sin(2 pi t / T + phi_b), phi_b ~ U(0, 2 pi) (per-bus
+                   phases: the net load change stays small, so the slack bus can
+                   carry it on the synthetic grids)
       kind "walk": s_t[b] = clip(s_{t-1}[b] + sigma N(0,1), -1, 1), s_{-1} = 0
     Returns (Pd [T][n_bus], Qd [T][n_bus]) float64."""
     rng = np.random.default_rng(seed)
@@ -335,7 +337,7 @@ def load_scenario(grid: Grid, T: int, amp: float = 0.05, kind: str = "sin", seed
     tt = np.arange(T, dtype=np.float64)[:, None]
     if kind == "sin":
         phi = rng.uniform(0.0, 2.0 * np.pi, n)[None, :]
-        s = 0.7 * np.sin(2.0 * np.pi * tt / T) + 0.3 * np.sin(2.0 * np.pi * tt / T + phi)
+        s = np.sin(2.0 * np.pi * tt / T + phi)
     elif kind == "walk":
         s = np.zeros((T, n))
         cur = np.zeros(n)
@@ -347,3 +349,22 @@ def load_scenario(grid: Grid, T: int, amp: float = 0.05, kind: str = "sin", seed
     Pd = np.asarray(grid.Pd, np.float64)[None, :] * (1.0 + amp * s)
     Qd = np.asarray(grid.Qd, np.float64)[None, :] * (1.0 + amp * s)
     return Pd, Qd
+
+
+def tracking_grid(name: str = "case118", seed: int | None = None, **kw) -> Grid:
+    """Grid for the tracking workload: make_grid(name) with a
+    smooth voltage profile -- PQ buses at 1.0, PV set points ~ U(1.0, 1.04), REF
+    at 1.02 -- instead of independent U(0.95, 1.05) magnitudes, whose reactive
+    flows put the backed-out operating point next to voltage collapse (DESIGN.md
+    R-T5).  Loads and linear costs are backed out by the caller (the operating
+    point is then a power-flow solution and p is stationary for the base loads)."""
+    g = make_grid(name, seed, **kw)
+    rng = np.random.default_rng((case_seed(name) if name in CASES else SEED_BASE + 999) + 17
+                                if seed is None else seed + 17)
+    bt = np.asarray(g.bus_type)
+    v = np.ones(bt.shape[0])
+    pv = np.flatnonzero(bt == PV)
+    v[pv] = rng.uniform(1.0, 1.04, pv.shape[0])
+    v[bt == REF] = 1.02
+    g.v = v
+    return g

@@ -63,7 +63,8 @@ typedef enum rh_status {
   RH_E_CUDA = 5,      /* CUDA runtime error (message in rh_last_error)               */
   RH_E_NOMEM = 6,     /* device allocation failed                                    */
   RH_E_NODEV = 7,     /* compute call on a host-only context (device = -1)           */
-  RH_E_NOCONV = 8     /* Newton projection did not converge within maxit steps       */
+  RH_E_NOCONV = 8,    /* Newton projection did not converge within maxit steps       */
+  RH_E_NOTPD = 9      /* tracking Step 2: not positive definite after 64 shifts      */
 } rh_status;
 
 /* Bus type codes (MATPOWER): PQ = 1, PV = 2, REF = 3. */
@@ -222,6 +223,43 @@ int rh_reduced_hessian(rh_ctx *ctx, const double *x, const double *p, int32_t j0
  * Pinned (page-locked) host buffers give the fastest copies. */
 int rh_reduced_hessian_host(rh_ctx *ctx, const double *x, const double *p, int32_t N,
                             double *grad_p, double *H);
+
+/* ---- Real-time tracking (section 6.3) ---- */
+
+/* Replace the loads w = (Pd, Qd): DEVICE arrays [n_bus]
+ * in the grid's bus order (either may be NULL = keep).  Invalidates the state:
+ * call rh_set_state / rh_newton next.  Errors: RH_E_ORDER (no grid). */
+int rh_set_loads(rh_ctx *ctx, const double *Pd, const double *Qd, void *stream);
+
+/* Step 2 of the tracking algorithm, Eq. qp_rto: solve
+ * (Hs + tau I) d = -g, Hs = (H + H^T)/2 (DESIGN.md R-T1), by a dense Cholesky
+ * factorization on the device (blocked, fp64 tensor cores; dense.cu).
+ * tau = 0 first; while a pivot is <= 0, tau = 1e-6, 2e-6, 4e-6, ... up to 64
+ * attempts (R-T4).  DEVICE arrays: H [n][ldh] row-major (either triangle
+ * order: only Hs is used), g [n], d [n] out (nullable), p [n] in/out
+ * (nullable): on success p += alpha d.  tau / attempts: HOST out (nullable).
+ * Needs no grid.  Blocking (one host sync per attempt).
+ * Errors: RH_E_ARG (n < 0, ldh < n, NULL H/g), RH_E_NOTPD (64 attempts failed;
+ * d and p untouched). */
+int rh_dense_spd_solve(rh_ctx *ctx, int32_t n, const double *H, int64_t ldh, const double *g, double *d,
+                       double *p, double alpha, double *tau, int32_t *attempts, void *stream);
+
+/* One tracking update on the free controls [j0, j1) of p
+ * (R-T2: [0, n_p) is the literal step; d is 0 outside the range):
+ *   loads <- (Pd, Qd) (device [n_bus], NULL = keep);
+ *   x <- x(p; w) by rh_newton from x (tol 1e-11, 2 extra steps, maxit 40);
+ *   Step 1: grad_p [n_p] and the columns j0..j1-1 of H_t, TRANSPOSED into
+ *           H [j1-j0][ldh >= n_p] (row k = column j0 + k), batches of N (Alg. 2);
+ *   Step 2: H_ff d = -g_f by rh_dense_spd_solve on the [j0, j1) block,
+ *           d [j1-j0] out, p[j0 + k] += alpha d[k].
+ * x, p, grad_p, H, d: DEVICE.  info (HOST, nullable) [7]: Newton steps,
+ * max|g(x, p)| after Newton, F(p_t; w_t), tau, Cholesky attempts,
+ * Step 1 ms, Step 2 ms (CUDA events on `stream`).  The context's state is left
+ * at (x(p_t; w_t), p_t).  Blocking.
+ * Errors: as rh_newton, rh_reduced_hessian and rh_dense_spd_solve. */
+int rh_tracking_step(rh_ctx *ctx, double *x, double *p, const double *Pd, const double *Qd, int32_t j0,
+                     int32_t j1, int32_t N, double alpha, double *grad_p, double *H, int64_t ldh, double *d,
+                     double *info, void *stream);
 
 /* Number of CUDA kernels this library launched on ctx since creation
  * (bench accounting of "gpu_launches"). */

@@ -39,6 +39,23 @@ def with_loads(grid, Pd, Qd):
     return g
 
 
+def backout_costs(grid, x, p, j0, j1, L=None):
+    """Copy of grid whose linear costs c1 make p stationary on the free
+    generator set points [j0, j1) (DESIGN.md R-T5): c1_gen -= grad_p F.  Exact,
+    because dF/dPg_i contains c1_i with coefficient 1 and nothing else depends
+    on it (R4)."""
+    L = L or pf.Layout(grid)
+    grad, _ = red.reduced_gradient(grid, x, p, L)
+    g2 = grid.copy()
+    c1 = np.array(grid.c1, dtype=np.float64)
+    for k in range(j0, j1):
+        if L.p_kind[k] != 2:
+            raise ValueError("cost back-out needs Pg controls only")
+        c1[L.gen_of_bus[L.p_bus[k]]] -= grad[k]
+    g2.c1 = c1
+    return g2
+
+
 def spd_solve(H, g, tau0=TAU0, max_tries=MAX_TRIES):
     """Step 2 (Eq. qp_rto): d with (Hs + tau I) d = -g, Hs = (H + H^T)/2 (R-T1),
     by Cholesky Hs + tau I = L L^T, L y = -g, L^T d = y.  tau = 0 first, then

@@ -18,9 +18,10 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libredhess.so")
 
-RH_OK, RH_E_ARG, RH_E_GRID, RH_E_ORDER, RH_E_SINGULAR, RH_E_CUDA, RH_E_NOMEM, RH_E_NODEV, RH_E_NOCONV = range(9)
+(RH_OK, RH_E_ARG, RH_E_GRID, RH_E_ORDER, RH_E_SINGULAR, RH_E_CUDA, RH_E_NOMEM, RH_E_NODEV, RH_E_NOCONV,
+ RH_E_NOTPD) = range(10)
 STATUS_NAMES = {0: "RH_OK", 1: "RH_E_ARG", 2: "RH_E_GRID", 3: "RH_E_ORDER", 4: "RH_E_SINGULAR",
-                5: "RH_E_CUDA", 6: "RH_E_NOMEM", 7: "RH_E_NODEV", 8: "RH_E_NOCONV"}
+                5: "RH_E_CUDA", 6: "RH_E_NOMEM", 7: "RH_E_NODEV", 8: "RH_E_NOCONV", 9: "RH_E_NOTPD"}
 KIND_THETA, KIND_V, KIND_PG = 0, 1, 2
 
 # every symbol declared in include/redhess.h (checked by tests/test_abi.py)
@@ -28,7 +29,7 @@ EXPORTS = ["rh_create", "rh_destroy", "rh_last_error", "rh_load_grid", "rh_get_i
            "rh_symbolic", "rh_segments", "rh_set_state", "rh_residual", "rh_reduced_gradient", "rh_set_multipliers",
            "rh_newton",
            "rh_hvp", "rh_hvp_stages", "rh_hessian_columns", "rh_full_hessian", "rh_reduced_hessian",
-           "rh_reduced_hessian_host",
+           "rh_reduced_hessian_host", "rh_set_loads", "rh_dense_spd_solve", "rh_tracking_step",
            "rh_launch_count", "rh_set_timing", "rh_stage_times"]
 
 
@@ -82,6 +83,10 @@ def _load():
         "rh_full_hessian": ([vp, i32, vp, vp], ctypes.c_int),
         "rh_reduced_hessian": ([vp, vp, vp, i32, i32, i32, vp, vp, i64, i32, vp], ctypes.c_int),
         "rh_reduced_hessian_host": ([vp, vp, vp, i32, vp, vp], ctypes.c_int),
+        "rh_set_loads": ([vp, vp, vp, vp], ctypes.c_int),
+        "rh_dense_spd_solve": ([vp, i32, vp, i64, vp, vp, vp, dbl, ctypes.POINTER(dbl), ctypes.POINTER(i32), vp],
+                               ctypes.c_int),
+        "rh_tracking_step": ([vp, vp, vp, vp, vp, i32, i32, i32, dbl, vp, vp, i64, vp, vp, vp], ctypes.c_int),
         "rh_launch_count": ([vp], i64),
         "rh_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
         "rh_stage_times": ([vp, vp], ctypes.c_int),
@@ -177,6 +182,7 @@ class RedHess:
         nx, npp = ctypes.c_int32(), ctypes.c_int32()
         self._rc(lib().rh_load_grid(self._h, ctypes.byref(g), ctypes.byref(nx), ctypes.byref(npp)))
         self.n_x, self.n_p = nx.value, npp.value
+        self.n_bus = int(g.n_bus)
         return self.n_x, self.n_p
 
     def get_info(self):
@@ -305,6 +311,60 @@ class RedHess:
             grad = np.empty(self.n_p)
         self._rc(lib().rh_reduced_hessian_host(self._h, _ptr(x), _ptr(p), N, _ptr(grad), _ptr(H)))
         return grad, H
+
+    # ------------------------------------------------------------------ real-time tracking (PAPER.md 6.3)
+    def set_loads(self, Pd=None, Qd=None, stream=None):
+        """rh_set_loads: DEVICE loads [n_bus] (None = keep); invalidates the state."""
+        if Pd is not None:
+            _check_dev(Pd, self.n_bus, "Pd")
+        if Qd is not None:
+            _check_dev(Qd, self.n_bus, "Qd")
+        self._rc(lib().rh_set_loads(self._h, _ptr(Pd) if Pd is not None else None,
+                                    _ptr(Qd) if Qd is not None else None, _stream(stream)))
+
+    def dense_spd_solve(self, H, g, d=None, p=None, alpha=1.0, stream=None):
+        """rh_dense_spd_solve: d with ((H + H^T)/2 + tau I) d = -g (Eq. qp_rto), DEVICE tensors;
+        p += alpha d when p is given.  Returns (d, tau, attempts)."""
+        import torch
+        n = g.shape[0]
+        _check_dev(g, n, "g")
+        if H.dim() != 2 or H.shape[0] < n or H.shape[1] < n or H.stride(1) != 1 or H.dtype != torch.float64:
+            raise ValueError("H must be a row-major float64 [>= n][>= n] device matrix")
+        if d is None:
+            d = torch.empty(n, dtype=torch.float64, device=g.device)
+        if p is not None:
+            _check_dev(p, n, "p")
+        tau = ctypes.c_double(0.0)
+        att = ctypes.c_int32(0)
+        self._rc(lib().rh_dense_spd_solve(self._h, n, _ptr(H), H.stride(0), _ptr(g), _ptr(d),
+                                          _ptr(p) if p is not None else None, float(alpha), ctypes.byref(tau),
+                                          ctypes.byref(att), _stream(stream)))
+        return d, tau.value, att.value
+
+    def tracking_step(self, x, p, N, Pd=None, Qd=None, j0=0, j1=None, alpha=1.0, grad=None, H=None, d=None,
+                      stream=None):
+        """rh_tracking_step: x <- x(p; w), g_t, columns [j0, j1) of H_t
+        (transposed), d = -H_ff^-1 g_f, p[j0:j1] += alpha d.  DEVICE x, p (updated in place).
+        Returns (grad, H, d, info) with info = dict(newton_steps, resid, F, tau, attempts, ms_step1, ms_step2)."""
+        import torch
+        j1 = self.n_p if j1 is None else j1
+        _check_dev(x, self.n_x, "x")
+        _check_dev(p, self.n_p, "p")
+        for name, v in (("Pd", Pd), ("Qd", Qd)):
+            if v is not None:
+                _check_dev(v, self.n_bus, name)
+        if grad is None:
+            grad = torch.empty(self.n_p, dtype=torch.float64, device="cuda")
+        if H is None:
+            H = torch.empty((j1 - j0, self.n_p), dtype=torch.float64, device="cuda")
+        if d is None:
+            d = torch.empty(j1 - j0, dtype=torch.float64, device="cuda")
+        info = np.zeros(7)
+        self._rc(lib().rh_tracking_step(self._h, _ptr(x), _ptr(p), _ptr(Pd) if Pd is not None else None,
+                                        _ptr(Qd) if Qd is not None else None, j0, j1, N, float(alpha), _ptr(grad),
+                                        _ptr(H), H.stride(0), _ptr(d), _ptr(info), _stream(stream)))
+        keys = ("newton_steps", "resid", "F", "tau", "attempts", "ms_step1", "ms_step2")
+        return grad, H, d, dict(zip(keys, info.tolist()))
 
     # ------------------------------------------------------------------ accounting
     def launch_count(self):

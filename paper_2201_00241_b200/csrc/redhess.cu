@@ -20,6 +20,7 @@
 #include "analysis.hpp"
 #include "kernels.cuh"
 #include "devutil.cuh"
+#include "dense.hpp"
 
 using namespace rh;
 
@@ -1717,8 +1718,13 @@ struct rh_ctx {
   double *pdiag;   // [n_p] 2 c2 of a Pg parameter's generator, else 0 (grid data)
   int *gpe_off, *gpe_row, *gpe_col, *gpe_src, *gpe_split;
   double2 *gpe_rec;
+  DenseWs dws;                 // tracking Step 2 (dense.cu)
+  cudaEvent_t ev_trk[3] = {nullptr, nullptr, nullptr};
 
   void free_all() {
+    dense_ws_free(dws);
+    for (auto &e : ev_trk)
+      if (e) cudaEventDestroy(e), e = nullptr;
     for (void *q : pool) cudaFree(q);
     pool.clear();
     for (auto &w : ws) {
@@ -2719,13 +2725,17 @@ int rh_set_multipliers(rh_ctx *c, const double *lambda, void *stream) {
   return build_tape(c, st);
 }
 
-int rh_newton(rh_ctx *c, double *x, const double *p, double tol, int32_t extra, int32_t maxit, int32_t *iters,
-              double *resid, void *stream) {
+}  // extern "C"
+
+namespace {
+// Newton projection; final_state: leave state + factors at the final x (else the
+// caller recomputes them, e.g. the tracking step's fused Hessian call)
+int newton_impl(rh_ctx *c, double *x, const double *p, double tol, int extra, int maxit, int *iters, double *resid,
+                cudaStream_t st, bool final_state) {
   if (!c || !x || !p || maxit <= 0 || extra < 0 || !(tol >= 0.0)) return fail(c, RH_E_ARG, "bad argument");
   if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
   if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
   RH_CUDA(c, cudaSetDevice(c->device));
-  cudaStream_t st = (cudaStream_t)stream;
   const Analysis &A = c->A;
   if (int rc = ensure_tsep(c, kSegC)) return rc;
   int left = -1, it = 0;
@@ -2768,6 +2778,7 @@ int rh_newton(rh_ctx *c, double *x, const double *p, double tol, int32_t extra, 
   }
   if (iters) *iters = it;
   if (!done) return fail(c, RH_E_NOCONV, "Newton did not converge within maxit steps");
+  if (!final_state) return RH_OK;
   // leave the state (g, factors) at the final x
   if (int rc = state_impl(c, x, p, st, nullptr, nullptr)) return rc;
   if (resid) {
@@ -2778,6 +2789,17 @@ int rh_newton(rh_ctx *c, double *x, const double *p, double tol, int32_t extra, 
     RH_CUDA(c, cudaStreamSynchronize(st));
   }
   return RH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int rh_newton(rh_ctx *c, double *x, const double *p, double tol, int32_t extra, int32_t maxit, int32_t *iters,
+              double *resid, void *stream) {
+  int it = 0;
+  int rc = newton_impl(c, x, p, tol, extra, maxit, &it, resid, (cudaStream_t)stream, true);
+  if (iters) *iters = it;
+  return rc;
 }
 
 int rh_hvp(rh_ctx *c, const double *W, int64_t ldw, double *HW, int64_t ldhw, int32_t N, void *stream) {
@@ -2950,6 +2972,118 @@ int rh_reduced_hessian_host(rh_ctx *c, const double *x, const double *p, int32_t
 }
 
 int64_t rh_launch_count(const rh_ctx *c) { return c ? c->launches : 0; }
+
+}  // extern "C"
+
+namespace {
+constexpr int kMaxShifts = 64;
+
+// tracking Step 2 (dense.cu): tau = 0, then 1e-6 doubling (R-T4); one sync per attempt
+int dense_solve_impl(rh_ctx *c, int n, const double *H, long long ldh, const double *g, double *d, double *p,
+                     double alpha, double *tau_out, int *attempts_out, cudaStream_t st) {
+  double tau = 0.0;
+  int att = 0;
+  if (n > 0) {
+    cudaError_t e = dense_ws_ensure(c->dws, n, c->device);
+    if (e != cudaSuccess) return fail(c, RH_E_CUDA, std::string("dense workspace: ") + cudaGetErrorString(e));
+    bool ok = false;
+    for (att = 1; att <= kMaxShifts; ++att) {
+      int nl = 0;
+      e = dense_spd_attempt(c->dws, n, H, ldh, g, tau, p, alpha, st, &nl);
+      c->launches += nl;
+      if (e != cudaSuccess) return fail(c, RH_E_CUDA, std::string("dense Cholesky: ") + cudaGetErrorString(e));
+      int fl = 0;
+      RH_CUDA(c, cudaMemcpyAsync(&fl, c->dws.fail, sizeof(int), cudaMemcpyDeviceToHost, st));
+      RH_CUDA(c, cudaStreamSynchronize(st));
+      if (fl == 0) {
+        ok = true;
+        break;
+      }
+      tau = (tau == 0.0) ? 1e-6 : 2.0 * tau;
+    }
+    if (!ok) return fail(c, RH_E_NOTPD, "dense Cholesky: not positive definite after 64 diagonal shifts");
+    if (d) RH_CUDA(c, cudaMemcpyAsync(d, c->dws.dbuf, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  }
+  if (tau_out) *tau_out = tau;
+  if (attempts_out) *attempts_out = att;
+  return RH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int rh_set_loads(rh_ctx *c, const double *Pd, const double *Qd, void *stream) {
+  if (!c) return RH_E_ARG;
+  if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
+  if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
+  RH_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = sizeof(double) * c->A.n_bus;
+  if (Pd) RH_CUDA(c, cudaMemcpyAsync(c->Pd, Pd, bytes, cudaMemcpyDeviceToDevice, st));
+  if (Qd) RH_CUDA(c, cudaMemcpyAsync(c->Qd, Qd, bytes, cudaMemcpyDeviceToDevice, st));
+  c->has_state = c->has_mult = false;
+  return RH_OK;
+}
+
+int rh_dense_spd_solve(rh_ctx *c, int32_t n, const double *H, int64_t ldh, const double *g, double *d, double *p,
+                       double alpha, double *tau, int32_t *attempts, void *stream) {
+  if (!c) return RH_E_ARG;
+  if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
+  if (n < 0 || ldh < n || (n > 0 && (!H || !g))) return fail(c, RH_E_ARG, "bad n / ldh / H / g");
+  RH_CUDA(c, cudaSetDevice(c->device));
+  int att = 0;
+  const int rc = dense_solve_impl(c, n, H, ldh, g, d, p, alpha, tau, &att, (cudaStream_t)stream);
+  if (attempts) *attempts = att;
+  return rc;
+}
+
+int rh_tracking_step(rh_ctx *c, double *x, double *p, const double *Pd, const double *Qd, int32_t j0, int32_t j1,
+                     int32_t N, double alpha, double *grad_p, double *H, int64_t ldh, double *d, double *info,
+                     void *stream) {
+  if (!c || !x || !p || !grad_p || !H) return fail(c, RH_E_ARG, "null argument");
+  if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
+  if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
+  const int np_ = c->A.n_p;
+  if (j0 < 0 || j1 > np_ || j0 >= j1 || N <= 0 || ldh < np_) return fail(c, RH_E_ARG, "bad j0/j1/N/ldh");
+  RH_CUDA(c, cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (auto &e : c->ev_trk)
+    if (!e) RH_CUDA(c, cudaEventCreate(&e));
+  RH_CUDA(c, cudaEventRecord(c->ev_trk[0], st));
+  if (Pd || Qd)
+    if (int rc = rh_set_loads(c, Pd, Qd, stream)) return rc;
+  int it = 0;
+  // x(p_t; w_t); the fused call below recomputes state and factors at the final x
+  if (int rc = newton_impl(c, x, p, 1e-11, 2, 40, &it, nullptr, st, false)) return rc;
+  // Step 1: g_t and the free columns of H_t (Alg. 2), transposed
+  if (int rc = reduced_hessian_impl(c, x, p, j0, j1, N, grad_p, H, ldh, 1, st, nullptr)) return rc;
+  RH_CUDA(c, cudaEventRecord(c->ev_trk[1], st));
+  double hv[2] = {0.0, 0.0};   // max|g|, F
+  RH_CUDA(c, cudaMemsetAsync(c->nwt + 1, 0, sizeof(double), st));
+  k_absmax<<<nblk(c->A.n_x), kThreads, 0, st>>>(c->A.n_x, c->g, c->nwt + 1);
+  RH_LAUNCHED(c);
+  RH_CUDA(c, cudaMemcpyAsync(&hv[0], c->nwt + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+  RH_CUDA(c, cudaMemcpyAsync(&hv[1], c->scal + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
+  // Step 2 on the [j0, j1) block: M[k][a] = H_t[j0 + a][j0 + k] (symmetrized inside)
+  double tau = 0.0;
+  int att = 0;
+  if (int rc = dense_solve_impl(c, j1 - j0, H + j0, ldh, grad_p + j0, d, p + j0, alpha, &tau, &att, st)) return rc;
+  RH_CUDA(c, cudaEventRecord(c->ev_trk[2], st));
+  RH_CUDA(c, cudaEventSynchronize(c->ev_trk[2]));
+  if (info) {
+    float m1 = 0.f, m2 = 0.f;
+    cudaEventElapsedTime(&m1, c->ev_trk[0], c->ev_trk[1]);
+    cudaEventElapsedTime(&m2, c->ev_trk[1], c->ev_trk[2]);
+    info[0] = it;
+    info[1] = hv[0];
+    info[2] = hv[1];
+    info[3] = tau;
+    info[4] = att;
+    info[5] = m1;
+    info[6] = m2;
+  }
+  return RH_OK;
+}
 
 int rh_set_timing(rh_ctx *c, int enable) {
   if (!c) return RH_E_ARG;

@@ -153,3 +153,30 @@ def test_tracking_trace_follows_the_optimum(case118):
         dev0, dev1 = np.max(np.abs(p - ps)), np.max(np.abs(p_next - ps))
         assert dev1 < 0.1 * dev0 and dev1 < 50.0 * dev0 * dev0, (t, dev0, dev1)   # Newton: quadratic
         p = p_next
+
+
+def test_backout_costs_makes_p_stationary():
+    g = pf.backout_loads(gridgen.tracking_grid("case118"))
+    L = pf.Layout(g)
+    n_pv = int(np.sum(L.p_kind == 2))
+    x, p = pf.state_vectors(g, L)
+    g0, _ = red.reduced_gradient(g, x, p, L)
+    g2 = trk.backout_costs(g, x, p, 0, n_pv, L)
+    grad, _ = red.reduced_gradient(g2, x, p, L)
+    assert np.max(np.abs(grad[:n_pv])) <= 1e-12 * np.max(np.abs(g0[:n_pv]))
+    np.testing.assert_array_equal(grad[n_pv:], g0[n_pv:])     # the v controls do not see c1
+    # the Newton step from a stationary point with unchanged loads is zero
+    _, _, info = trk.tracking_step(g2, p, x, g2.Pd, g2.Qd, 0, n_pv, N=64, L=L)
+    assert np.max(np.abs(info["d"])) <= 1e-10
+
+
+def test_tracking_grid_is_well_conditioned_for_load_changes():
+    # +-5 % per-bus-phase loads keep the power flow solvable from the base state
+    # on the PEGASE1354-shaped tracking grid (the paper's Table 3 case)
+    g = pf.backout_loads(gridgen.tracking_grid("case1354pegase"))
+    L = pf.Layout(g)
+    x, p = pf.state_vectors(g, L)
+    Pd, Qd = gridgen.load_scenario(g, 60, amp=0.05, kind="sin", seed=4)
+    for t in (0, 15, 30):
+        xt = pf.newton(trk.with_loads(g, Pd[t], Qd[t]), p, x, L)
+        assert np.max(np.abs(pf.residual(trk.with_loads(g, Pd[t], Qd[t]), xt, p, L))) < 1e-10
