@@ -345,30 +345,6 @@ def main():
     ms_hess = tt[1].item() / args.steps
     ms_pre = tt[2].item() / args.steps
 
-    # ---- Newton projection x(p) (SURVEY.md 8(f) NEXT-1) from a perturbed solution
-    x_pert = x + 1e-3 * torch.from_numpy(np.random.default_rng(7).standard_normal(n_x)).to(dev)
-    xw = torch.empty_like(x)
-    newton_ms, newton_steps = [], 0
-    for rep in range(4):
-        xw.copy_(x_pert)
-        torch.cuda.synchronize()
-        t0n = time.perf_counter()
-        newton_steps, newton_res = ctx.newton(xw, p)
-        torch.cuda.synchronize()
-        if rep:
-            newton_ms.append((time.perf_counter() - t0n) * 1e3)
-    newton_err = float((xw - x).abs().max().item())
-    ctx.set_state(x, p)
-    ctx.reduced_gradient(grad)
-
-    # ---- real-time tracking (SURVEY.md 8(f) NEXT-2): the paper's Table 3 case, and this case
-    tracking = None
-    if world == 1:
-        tracking = {"table3": tracking_bench(rh, gridgen, dev, "case1354pegase", 256, 10),
-                    "paper": PAPER_TABLE3}
-        if case != "case1354pegase":
-            tracking[case] = tracking_bench(rh, gridgen, dev, case, N, 5)
-
     # ---- batched HVP throughput (random W, width N, weak scaling: each GPU its own W)
     W = torch.from_numpy(gridgen.random_W(n_p, N, seed=1 + rank)).to(dev)
     HW = torch.empty_like(W)
@@ -461,6 +437,30 @@ def main():
             traffic = prof[key].get("dram_bytes_per_launch")
     except Exception:
         pass
+
+    # ---- Newton projection x(p) (SURVEY.md 8(f) NEXT-1) from a perturbed solution
+    x_pert = x + 1e-3 * torch.from_numpy(np.random.default_rng(7).standard_normal(n_x)).to(dev)
+    xw = torch.empty_like(x)
+    newton_ms, newton_steps = [], 0
+    for rep in range(4):
+        xw.copy_(x_pert)
+        torch.cuda.synchronize()
+        t0n = time.perf_counter()
+        newton_steps, newton_res = ctx.newton(xw, p)
+        torch.cuda.synchronize()
+        if rep:
+            newton_ms.append((time.perf_counter() - t0n) * 1e3)
+    newton_err = float((xw - x).abs().max().item())
+    ctx.set_state(x, p)
+    ctx.reduced_gradient(grad)
+
+    # ---- real-time tracking (SURVEY.md 8(f) NEXT-2): the paper's Table 3 case, and this case
+    tracking = None
+    if world == 1:
+        tracking = {"table3": tracking_bench(rh, gridgen, dev, "case1354pegase", 256, 10),
+                    "paper": PAPER_TABLE3}
+        if case != "case1354pegase":
+            tracking[case] = tracking_bench(rh, gridgen, dev, case, N, 5)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
