@@ -1719,10 +1719,14 @@ struct rh_ctx {
   int *gpe_off, *gpe_row, *gpe_col, *gpe_src, *gpe_split;
   double2 *gpe_rec;
   DenseWs dws;                 // tracking Step 2 (dense.cu)
+  cudaStream_t cp_st = nullptr;   // host copies of finished column blocks (rh_reduced_hessian_host)
+  cudaEvent_t ev_cp = nullptr;
   cudaEvent_t ev_trk[3] = {nullptr, nullptr, nullptr};
 
   void free_all() {
     dense_ws_free(dws);
+    if (cp_st) cudaStreamDestroy(cp_st), cp_st = nullptr;
+    if (ev_cp) cudaEventDestroy(ev_cp), ev_cp = nullptr;
     for (auto &e : ev_trk)
       if (e) cudaEventDestroy(e), e = nullptr;
     for (void *q : pool) cudaFree(q);
@@ -2845,9 +2849,15 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
                     double *Hhost, int early = 0) {
   const int ncols = j1 - j0;
   const int nb = (ncols + N - 1) / N;
-  // with host copies, 2 streams: staggered batches let finished column blocks
-  // travel while later batches compute (3 concurrent batches finish together)
+  // with host copies, 2 compute streams: staggered batches finish one after the
+  // other, and each finished column block travels on a copy stream while later
+  // batches compute (no compute stream waits behind a copy); 3 concurrent
+  // batches would finish together and leave the copies to the tail
   const int nws = num_ws(nb, Hhost ? 2 : kNumWs);
+  if (Hhost) {
+    if (!c->cp_st) RH_CUDA(c, cudaStreamCreateWithFlags(&c->cp_st, cudaStreamNonBlocking));
+    if (!c->ev_cp) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_cp, cudaEventDisableTiming));
+  }
   if (nws > 1) {
     if (!c->ev_fork) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     RH_CUDA(c, cudaEventRecord(c->ev_fork, st));
@@ -2866,13 +2876,21 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
     int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0, k,
                       b < early ? 2 : 0);
     if (rc) return rc;
-    if (Hhost)
+    if (Hhost) {
+      RH_CUDA(c, cudaEventRecord(c->ev_cp, sb));
+      RH_CUDA(c, cudaStreamWaitEvent(c->cp_st, c->ev_cp, 0));
       RH_CUDA(c, cudaMemcpy2DAsync(Hhost + a0, ldh * sizeof(double), out, ldh * sizeof(double),
-                                   (size_t)(a1 - a0) * sizeof(double), (size_t)c->A.n_p, cudaMemcpyDeviceToHost, sb));
+                                   (size_t)(a1 - a0) * sizeof(double), (size_t)c->A.n_p, cudaMemcpyDeviceToHost,
+                                   c->cp_st));
+    }
   }
   for (int k = 1; k < nws; ++k) {
     RH_CUDA(c, cudaEventRecord(c->ev_join[k], c->sti[k]));
     RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_join[k], 0));
+  }
+  if (Hhost) {
+    RH_CUDA(c, cudaEventRecord(c->ev_cp, c->cp_st));
+    RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_cp, 0));
   }
   return RH_OK;
 }

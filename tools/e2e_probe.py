@@ -36,12 +36,12 @@ x = torch.from_numpy(x_np).cuda(); p = torch.from_numpy(p_np).cuda()
 backout_loads_lib(rh, ctx, grid, x, p)
 x_h = torch.from_numpy(x_np).pin_memory(); p_h = torch.from_numpy(p_np).pin_memory()
 H_h = torch.empty((n, n), dtype=torch.float64).pin_memory(); g_h = torch.empty(n, dtype=torch.float64).pin_memory()
-for _ in range(3):
-    ctx.reduced_hessian_host(x_h.numpy(), p_h.numpy(), 1024, grad=g_h.numpy(), H=H_h.numpy())
-ts = []
-for _ in range(20):
-    t0 = time.perf_counter()
-    ctx.reduced_hessian_host(x_h.numpy(), p_h.numpy(), 1024, grad=g_h.numpy(), H=H_h.numpy())
-    ts.append((time.perf_counter() - t0) * 1e3)
-print("e2e ms: median %.3f min %.3f max %.3f" % (np.median(ts), np.min(ts), np.max(ts)))
-print("all:", " ".join("%.2f" % t for t in ts))
+for NB in [int(a) for a in (sys.argv[1:] or ["1024"])]:
+    for _ in range(3):
+        ctx.reduced_hessian_host(x_h.numpy(), p_h.numpy(), NB, grad=g_h.numpy(), H=H_h.numpy())
+    ts = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        ctx.reduced_hessian_host(x_h.numpy(), p_h.numpy(), NB, grad=g_h.numpy(), H=H_h.numpy())
+        ts.append((time.perf_counter() - t0) * 1e3)
+    print("N=%d e2e ms: median %.3f min %.3f max %.3f" % (NB, np.median(ts), np.min(ts), np.max(ts)))
