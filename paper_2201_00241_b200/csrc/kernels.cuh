@@ -49,6 +49,10 @@ struct SegParams {
   int smem_stride;                   // bytes per buffer (two buffers: current tile, prefetched tile)
   int smem_x_off, smem_meta_off, smem_tmeta_off, smem_rec_off, smem_doff_off, smem_lvl_off;  // bytes (tmeta: tops M + rows)
   int *blk_ctr;                      // [2 per mode] tile ticket counter, CTAs done (self-resetting)
+  // 2D TMA tensor maps (CUtensorMap, device memory) of Z and P for this ld: pairs
+  // [box 32 x 64 rows, box 32 x 8 rows]; null = per-row copies (k_blk)
+  const void *tmZ, *tmP;
+  int kblk_group;                    // k_blk: column chunks per ticket (one block's structure staged once)
   const int *seg_row_off, *row_global;
   DSeg fwd, bwd;
   const double *vL, *vUt;             // separator rows' L / U^T values (fwd entry order)

@@ -3,6 +3,7 @@
 // file; the host only runs the one-time symbolic analysis (analysis.cpp).
 //
 // Citations are PAPER.md line numbers (arXiv 2201.00241) or DESIGN.md readings.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1024,6 +1025,22 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned by
                "r"(bytes)
                : "memory");
 }
+// 2D TMA box copies of block rows of Z / P (tensor map in global memory): rows
+// [r0, r0 + box) x columns [c0, c0 + 32) <-> a dense [box][32] tile in shared memory
+__device__ __forceinline__ void tma2d_g2s(void *dst, const void *map, int c0, int r0, unsigned long long *mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(r0), "r"(smem_u32(mbar))
+      : "memory");
+}
+__device__ __forceinline__ void tma2d_s2g(const void *map, int c0, int r0, const void *src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(r0), "r"(smem_u32(src))
+               : "memory");
+}
+constexpr int kTmaBig = 64, kTmaSmall = 8;   // box heights (rows) of the two maps of a pair
+constexpr int kTmapBytes = 128;               // sizeof(CUtensorMap)
 
 // Block sweeps (see above): 2 CTAs of 8 warps per SM, each sweeping one
 // (block, 32-column) tile at a time taken from a global ticket counter
@@ -1044,7 +1061,10 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
   double *G = (mode <= MODE_U || mode == MODE_LX) ? h.Z : h.P;
   int *ctr = h.blk_ctr + 2 * mode;
   const int nch = h.ld / kBC;
-  const int ntiles = h.nblk * nch;
+  // a ticket = one block x up to kblk_group consecutive column chunks: the block's
+  // schedule is staged once and reused (it is ~40 % of a tile's L2 -> SM bytes)
+  const int cg = max(1, min(h.kblk_group, nch)), ngrp = (nch + cg - 1) / cg;
+  const int ntiles = h.nblk * ngrp;
   double *X = reinterpret_cast<double *>(smraw + h.smem_x_off);
   UStage st;
   st.meta = reinterpret_cast<const int4 *>(smraw + h.smem_meta_off);
@@ -1065,37 +1085,60 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     __syncthreads();
     const int tk = s_tk;
     if (tk >= ntiles) break;
-    // timing experiment (RH_DEBUG & 8, MODE_U): per ticket [8 warps' pieces | units << 48, wait, tops, t0, t1]
-    long long *prof = ((h.debug & 8) && h.dbg && mode == MODE_U && tk < 8192) ? h.dbg + (long long)tk * 12 : nullptr;
+    const int s = U.blk_order[tk / ngrp], cbeg = (tk % ngrp) * cg, cend = min(nch, cbeg + cg);
+    for (int ci = cbeg; ci < cend; ++ci) {
+    const bool first = ci == cbeg;
+    if (!first) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the previous chunk's stores have read X
+      __syncthreads();
+    }
+    const int col0 = ci * kBC, tile = (tk / ngrp) * nch + ci;
+    // timing experiment (RH_DEBUG & 8, MODE_U): per tile [8 warps' pieces | units << 48, wait, tops, t0, t1]
+    long long *prof = ((h.debug & 8) && h.dbg && mode == MODE_U && tile < 8192) ? h.dbg + (long long)tile * 12 : nullptr;
     const long long c_a = prof ? clock64() : 0;
-    const int s = U.blk_order[tk / nch], col0 = (tk % nch) * kBC;
     const int r0 = h.seg_row_off[s], nr = h.seg_row_off[s + 1] - r0;
     const int x0 = U.ext_off[s], nxr = mode == MODE_L ? 0 : U.ext_off[s + 1] - x0;
     const int ub = U.unit_off[s], nu = U.unit_off[s + 1] - ub;
     const int rb = U.rec_off[s], nrec = U.rec_off[s + 1] - rb;
     const int ob = U.doff_off[s], nof = U.doff_off[s + 1] - ob;
     const int nxrows = mode == MODE_L ? 0 : nr + nxr;
+    // block rows by 2D TMA boxes (64, then 8 rows), the rest (< 8 block rows, staged
+    // separator rows) by 16-byte cp.async
+    const char *tm = reinterpret_cast<const char *>(G == h.Z ? h.tmZ : h.tmP);
+    const int nbig = tm ? nr / kTmaBig : 0, nsmall = tm ? (nr - nbig * kTmaBig) / kTmaSmall : 0;
+    const int rows_tma = mode == MODE_L ? 0 : nbig * kTmaBig + nsmall * kTmaSmall;
     if (tid == 0) {
       const double *dM = lsw ? h.tL : mode == MODE_U ? h.tU : mode == MODE_UT ? h.tUt : h.tLt;
-      const unsigned tx = 16u * (nu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + 32u * kTopLd * 8 + 128u +
-                          (mode == MODE_L ? 16u * (h.gpe_off[s + 1] - h.gpe_off[s]) + 48u : 0u);
+      const unsigned tx = (first ? 16u * (nu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + 32u * kTopLd * 8 + 128u +
+                                       (mode == MODE_L ? 16u * (h.gpe_off[s + 1] - h.gpe_off[s]) + 48u : 0u)
+                                 : 0u) +
+                          (unsigned)rows_tma * kRowB;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx)
                    : "memory");
+      if (first) {
       bulk_g2s(smraw + h.smem_meta_off, U.meta + ub, 16u * nu, &mbar);
       bulk_g2s(smraw + h.smem_tmeta_off, dM + (size_t)s * 32 * kTopLd, 32u * kTopLd * 8, &mbar);
       bulk_g2s(smraw + h.smem_tmeta_off + 32 * kTopLd * 8, U.top_rows + s * 32, 128u, &mbar);
       bulk_g2s(smraw + h.smem_rec_off, vals + rb, 16u * nrec, &mbar);
       if (nof) bulk_g2s(smraw + h.smem_doff_off, U.doff + ob, 4u * nof, &mbar);
       bulk_g2s(smraw + h.smem_lvl_off, U.lvl + s * UnitSweep::kLvl, 4u * UnitSweep::kLvl, &mbar);
-      if (mode == MODE_L) {   // G_p entry records + warp ranges, behind the block's rows
+      if (mode == MODE_L) {   // G_p entry records + warp ranges, behind the block's rows (kept across chunks)
         const int g0 = h.gpe_off[s], ng = h.gpe_off[s + 1] - g0;
         if (ng) bulk_g2s(X + nr * kBC, h.gpe_rec + g0, 16u * ng, &mbar);
         bulk_g2s(reinterpret_cast<double2 *>(X + nr * kBC) + ng, h.gpe_split + s * 12, 48u, &mbar);
       }
+      }
+      if (rows_tma) {
+        for (int i = 0; i < nbig; ++i) tma2d_g2s(X + i * kTmaBig * kBC, tm, col0, r0 + i * kTmaBig, &mbar);
+        for (int i = 0; i < nsmall; ++i) {
+          const int a = nbig * kTmaBig + i * kTmaSmall;
+          tma2d_g2s(X + a * kBC, tm + kTmapBytes, col0, r0 + a, &mbar);
+        }
+      }
     }
     {  // X rows: 16-byte cp.async (LSU path; 256 B TMA bulk copies are rate-bound on the TMA unit)
       const int c = tid & 15;
-      for (int a = tid >> 4; a < nxrows; a += blockDim.x >> 4) {
+      for (int a = rows_tma + (tid >> 4); a < nxrows; a += blockDim.x >> 4) {
         const long long grow = a < nr ? r0 + a : U.ext_rows[x0 + a - nr];
         cp_async16(X + a * kBC + 2 * c, G + grow * h.ld + col0 + 2 * c);
       }
@@ -1141,8 +1184,21 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // sweep writes -> bulk store reads
     __syncthreads();
-    for (int a = tid; a < nr; a += blockDim.x) bulk_s2g(G + (long long)(r0 + a) * h.ld + col0, X + a * kBC, kRowB);
+    {
+      const int nbs = tm ? nr / kTmaBig : 0, nss = tm ? (nr - nbs * kTmaBig) / kTmaSmall : 0;
+      const int rows_st = nbs * kTmaBig + nss * kTmaSmall;
+      if (tid == 0) {
+        for (int i = 0; i < nbs; ++i) tma2d_s2g(tm, col0, r0 + i * kTmaBig, X + i * kTmaBig * kBC);
+        for (int i = 0; i < nss; ++i) {
+          const int a = nbs * kTmaBig + i * kTmaSmall;
+          tma2d_s2g(tm + kTmapBytes, col0, r0 + a, X + a * kBC);
+        }
+      }
+      for (int a = rows_st + tid; a < nr; a += blockDim.x)
+        bulk_s2g(G + (long long)(r0 + a) * h.ld + col0, X + a * kBC, kRowB);
+    }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }   // column chunks of the ticket
   }
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   // the last CTA out resets the ticket counter for the next launch
@@ -1720,11 +1776,19 @@ struct rh_ctx {
   double2 *gpe_rec;
   DenseWs dws;                 // tracking Step 2 (dense.cu)
   cudaStream_t cp_st = nullptr;   // host copies of finished column blocks (rh_reduced_hessian_host)
+  struct TMapEntry {
+    const double *base;
+    int ld;
+    void *dev;   // [2] CUtensorMap in device memory: boxes of 64 and 8 rows
+  };
+  std::vector<TMapEntry> tmaps;   // k_blk 2D TMA maps per (buffer, ld)
   cudaEvent_t ev_cp = nullptr;
   cudaEvent_t ev_trk[3] = {nullptr, nullptr, nullptr};
 
   void free_all() {
     dense_ws_free(dws);
+    for (auto &e : tmaps) cudaFree(e.dev);
+    tmaps.clear();
     if (cp_st) cudaStreamDestroy(cp_st), cp_st = nullptr;
     if (ev_cp) cudaEventDestroy(ev_cp), ev_cp = nullptr;
     for (auto &e : ev_trk)
@@ -2081,6 +2145,50 @@ int ensure_ws(rh_ctx *c, int ld, int k = 0) {
   return RH_OK;
 }
 
+// 2D tensor maps of a [n_x][ld] fp64 buffer for k_blk's block-row boxes
+// (cuTensorMapEncodeTiled through the runtime's driver entry point, no -lcuda);
+// cached per (buffer, ld).  Returns nullptr if unavailable (k_blk then copies rows).
+const void *tmap_pair(rh_ctx *c, const double *G, int ld) {
+  for (auto &e : c->tmaps)
+    if (e.base == G && e.ld == ld) return e.dev;
+  using Encode = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<Encode>(fn);
+    cudaGetLastError();
+  }
+  if (!encode || getenv("RH_NO_TMA2D")) return nullptr;
+  static_assert(sizeof(CUtensorMap) == kTmapBytes, "tensor map size");
+  CUtensorMap m[2];
+  const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)c->A.n_x};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t estr[2] = {1, 1};
+  const cuuint32_t rows[2] = {(cuuint32_t)kTmaBig, (cuuint32_t)kTmaSmall};
+  for (int i = 0; i < 2; ++i) {
+    const cuuint32_t box[2] = {(cuuint32_t)kBC, rows[i]};
+    if (encode(&m[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(G), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return nullptr;
+  }
+  void *dev = nullptr;
+  if (cudaMalloc(&dev, sizeof m) != cudaSuccess || cudaMemcpy(dev, m, sizeof m, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaGetLastError();
+    if (dev) cudaFree(dev);
+    return nullptr;
+  }
+  c->tmaps.push_back({G, ld, dev});
+  return dev;
+}
+
 SegParams make_params(rh_ctx *c, int k = 0) {
   SegParams h{};
   const Analysis &A = c->A;
@@ -2096,6 +2204,8 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.vUt = c->vUt;
   h.Z = c->ws[k].Z;
   h.P = c->ws[k].P;
+  h.kblk_group = 2;
+  if (const char *env = getenv("RH_KBLK_GROUP")) h.kblk_group = std::max(1, atoi(env));   // tuning override
   h.gp_rptr = c->gp_rptr;
   h.gp_col = c->gp_col;
   h.gp_val = c->gp_val;
@@ -2221,6 +2331,8 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   const bool timing = c->timing && phase == 0;
   h.N = N;
   h.ld = ld;
+  h.tmZ = tmap_pair(c, h.Z, ld);
+  h.tmP = tmap_pair(c, h.P, ld);
   h.W = W;
   h.ldw = ldw;
   h.ident_j0 = ident_j0;
