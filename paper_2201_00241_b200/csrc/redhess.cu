@@ -92,6 +92,9 @@ __global__ void k_assemble(AsmParams a) {
   if (b >= a.n_bus) return;
   const double vb = a.v[b];
   const int s0 = a.bl_ptr[b], s1 = a.bl_ptr[b + 1];
+  const bool isref = b == a.ref;
+  // one pass over the bus's lines: injections P, Q and the off-diagonal
+  // derivatives (which do not depend on P, Q); same per-slot order as before
   double P = 0.0, Q = 0.0;
   for (int s = s0; s < s1; ++s) {
     const int l = a.bl_line[s], o = a.bl_other[s];
@@ -101,69 +104,68 @@ __global__ void k_assemble(AsmParams a) {
     const double B = from ? a.B_ft[l] : a.B_tf[l];
     const double c = cs.x, sn = from ? cs.y : -cs.y;   // cos/sin(th_b - th_o)
     const double vo = a.v[o];
-    P += vo * (G * c + B * sn);
-    Q += vo * (G * sn - B * c);
+    const double gsbc = G * sn - B * c, gcbs = G * c + B * sn;
+    P += vo * gcbs;
+    Q += vo * gsbc;
+    if (isref) {   // grad P_ref over (theta_o, v_o) of the neighbours (theta_ref constant)
+      a.refg_th[o] += vb * vo * gsbc;
+      a.refg_v[o] += vb * gcbs;
+      continue;
+    }
+    const double dPth = vb * vo * gsbc, dPv = vb * gcbs;
+    const double dQth = -vb * vo * gcbs, dQv = vb * gsbc;
+    const int4 sp = *reinterpret_cast<const int4 *>(a.slot_pos + 4 * s);
+    if (sp.x >= 0) a.F_val[sp.x] += dPth;
+    if (sp.y >= 0) a.F_val[sp.y] += dPv;
+    if (sp.z >= 0) a.F_val[sp.z] += dQth;
+    if (sp.w >= 0) a.F_val[sp.w] += dQv;
+    const int2 gs = *reinterpret_cast<const int2 *>(a.gp_slot_pos + 2 * s);
+    if (gs.x >= 0) a.gp_val[gs.x] += dPv;
+    if (gs.y >= 0) a.gp_val[gs.y] += dQv;
   }
   const double Gbb = a.G_ii[b], Bbb = a.B_ii[b];
   P = vb * P + vb * vb * Gbb;
   Q = vb * Q - vb * vb * Bbb;
   a.P[b] = P;
   a.Q[b] = Q;
-  const int t = a.bus_type[b];
-  if (b == a.ref) {
-    // grad P_ref over (theta_o, v_o) of the neighbours and v_ref (theta_ref constant)
-    for (int s = s0; s < s1; ++s) {
-      const int l = a.bl_line[s], o = a.bl_other[s];
-      const double2 cs = a.cs[l];
-      const bool from = a.bl_end[s] == 0;
-      const double G = from ? a.G_ft[l] : a.G_tf[l];
-      const double B = from ? a.B_ft[l] : a.B_tf[l];
-      const double c = cs.x, sn = from ? cs.y : -cs.y;
-      a.refg_th[o] += vb * a.v[o] * (G * sn - B * c);
-      a.refg_v[o] += vb * (G * c + B * sn);
-    }
-    a.refg_v[b] += P / vb + Gbb * vb;
+  if (isref) {
+    a.refg_v[b] += P / vb + Gbb * vb;   // and v_ref
     return;
   }
+  const int t = a.bus_type[b];
   const int rP = a.th_x[b];
   const int rQ = a.v_x[b];
   a.g[rP] = P + a.Pd[b] - (t == RH_PV ? a.pgb[b] : 0.0);
   if (rQ >= 0) a.g[rQ] = Q + a.Qd[b];
   // diagonal block
-  const int *dp = a.diag_pos + 4 * b;
-  a.F_val[dp[0]] += -Q - Bbb * vb * vb;            // dP_b/dth_b
+  const int4 dp = *reinterpret_cast<const int4 *>(a.diag_pos + 4 * b);
+  a.F_val[dp.x] += -Q - Bbb * vb * vb;            // dP_b/dth_b
   if (rQ >= 0) {
-    a.F_val[dp[1]] += P / vb + Gbb * vb;            // dP_b/dv_b
-    a.F_val[dp[2]] += P - Gbb * vb * vb;            // dQ_b/dth_b
-    a.F_val[dp[3]] += Q / vb - Bbb * vb;            // dQ_b/dv_b
+    a.F_val[dp.y] += P / vb + Gbb * vb;            // dP_b/dv_b
+    a.F_val[dp.z] += P - Gbb * vb * vb;            // dQ_b/dth_b
+    a.F_val[dp.w] += Q / vb - Bbb * vb;            // dQ_b/dv_b
   } else {
     a.gp_val[a.gp_self_pos[b]] += P / vb + Gbb * vb; // dP_b/dv_b, v_b in p (PV)
     a.gp_val[a.gp_pg_pos[b]] = -1.0;                  // dP_b/dPg_b
-  }
-  for (int s = s0; s < s1; ++s) {
-    const int l = a.bl_line[s], o = a.bl_other[s];
-    const double2 cs = a.cs[l];
-    const bool from = a.bl_end[s] == 0;
-    const double G = from ? a.G_ft[l] : a.G_tf[l];
-    const double B = from ? a.B_ft[l] : a.B_tf[l];
-    const double c = cs.x, sn = from ? cs.y : -cs.y;
-    const double vo = a.v[o];
-    const double gsbc = G * sn - B * c, gcbs = G * c + B * sn;
-    const double dPth = vb * vo * gsbc, dPv = vb * gcbs;
-    const double dQth = -vb * vo * gcbs, dQv = vb * gsbc;
-    const int *sp = a.slot_pos + 4 * s;
-    if (sp[0] >= 0) a.F_val[sp[0]] += dPth;
-    if (sp[1] >= 0) a.F_val[sp[1]] += dPv;
-    if (sp[2] >= 0) a.F_val[sp[2]] += dQth;
-    if (sp[3] >= 0) a.F_val[sp[3]] += dQv;
-    const int *gs = a.gp_slot_pos + 2 * s;
-    if (gs[0] >= 0) a.gp_val[gs[0]] += dPv;
-    if (gs[1] >= 0) a.gp_val[gs[1]] += dQv;
   }
 }
 
 // f (R4) and the REF multiplier seed mu_ref = f'(Pg_ref) (R22).  One block.
 // scal[0] = P_ref, scal[1] = Pg_ref, scal[2] = mu_ref, scal[3] = f
+__global__ void k_state_init(int nx, int np_, const double *__restrict__ x, const double *__restrict__ p, double *cx,
+                             double *cp, long long nF, double *F_val, long long nG, double *gp_val, int nb,
+                             double *refg_th, double *refg_v, int *status) {
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x, step = (long long)gridDim.x * blockDim.x;
+  for (long long i = t0; i < nx; i += step) cx[i] = x[i];
+  for (long long i = t0; i < np_; i += step) cp[i] = p[i];
+  for (long long i = t0; i < nF; i += step) F_val[i] = 0.0;
+  for (long long i = t0; i < nG; i += step) gp_val[i] = 0.0;
+  for (long long i = t0; i < nb; i += step) {
+    refg_th[i] = 0.0;
+    refg_v[i] = 0.0;
+  }
+  if (t0 == 0) *status = 0;
+}
 __global__ void k_objective(int n_bus, int ref, const int *has_gen, const double *c2b, const double *c1b,
                             const double *c0b, const double *pgb, const double *P, const double *Pd,
                             double *scal) {
@@ -2563,6 +2565,39 @@ namespace {
 // block sweeps of Hessian batches) run on `side` as soon as the block factors
 // exist, concurrently with the separator's elimination and inversion on `st`;
 // `st` joins `side` before the pivot flag is read.
+// timing experiment (RH_DEBUG & 1024): events on the caller's stream at stage
+// boundaries of the fused call, printed by dbg_report
+struct DbgMark {
+  const char *label;
+  cudaEvent_t ev;
+};
+std::vector<DbgMark> g_marks;
+bool dbg_on() {
+  static int v = -1;
+  if (v < 0) v = getenv("RH_DEBUG") && (atoi(getenv("RH_DEBUG")) & 1024) ? 1 : 0;
+  return v == 1;
+}
+void dbg_mark(cudaStream_t st, const char *label) {
+  if (!dbg_on()) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  g_marks.push_back({label, e});
+}
+void dbg_report(cudaStream_t st) {
+  if (!dbg_on() || g_marks.empty()) return;
+  cudaStreamSynchronize(st);
+  float prev = 0.f;
+  for (auto &m : g_marks) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, g_marks[0].ev, m.ev);
+    fprintf(stderr, "  %-28s %8.3f ms  (+%.3f)\n", m.label, t, t - prev);
+    prev = t;
+  }
+  for (auto &m : g_marks) cudaEventDestroy(m.ev);
+  g_marks.clear();
+}
+
 int check_pivots(rh_ctx *c, cudaStream_t st) {   // reads the refactorization's pivot flag (one sync)
   int status = 0;
   RH_CUDA(c, cudaMemcpyAsync(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -2586,13 +2621,13 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   const Analysis &A = c->A;
   const int nx = A.n_x, np_ = A.n_p, nb = A.n_bus, m = A.n_line;
   c->has_state = c->has_mult = false;
-  RH_CUDA(c, cudaMemcpyAsync(c->x, x, sizeof(double) * nx, cudaMemcpyDeviceToDevice, st));
-  RH_CUDA(c, cudaMemcpyAsync(c->p, p, sizeof(double) * np_, cudaMemcpyDeviceToDevice, st));
-  RH_CUDA(c, cudaMemsetAsync(c->F_val, 0, sizeof(double) * A.F_col.size(), st));
-  RH_CUDA(c, cudaMemsetAsync(c->gp_val, 0, sizeof(double) * A.gp_col.size(), st));
-  RH_CUDA(c, cudaMemsetAsync(c->refg_th, 0, sizeof(double) * nb, st));
-  RH_CUDA(c, cudaMemsetAsync(c->refg_v, 0, sizeof(double) * nb, st));
-  RH_CUDA(c, cudaMemsetAsync(c->status, 0, sizeof(int), st));
+  dbg_mark(st, "state start");
+  // x, p into the context; zero the assembled values, the REF gradient, the pivot flag (one launch)
+  k_state_init<<<2 * c->nsm, kThreads, 0, st>>>(nx, np_, x, p, c->x, c->p, (long long)A.F_col.size(), c->F_val,
+                                                (long long)A.gp_col.size(), c->gp_val, nb, c->refg_th, c->refg_v,
+                                                c->status);
+  RH_LAUNCHED(c);
+  dbg_mark(st, "copies + memsets");
   k_bus_state<<<nblk(nx + np_ + 1), kThreads, 0, st>>>(nx, np_, c->x_bus, c->x_kind, c->p_bus, c->p_kind, c->x,
                                                       c->p, c->th, c->v, c->pgb, A.ref, A.theta_ref);
   RH_LAUNCHED(c);
@@ -2632,11 +2667,10 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   a.gp_val = c->gp_val;
   a.refg_th = c->refg_th;
   a.refg_v = c->refg_v;
+  dbg_mark(st, "bus state + line trig");
   k_assemble<<<nblk(nb, 128), 128, 0, st>>>(a);
   RH_LAUNCHED(c);
-  k_objective<<<1, 1024, 0, st>>>(nb, A.ref, c->has_gen, c->c2b, c->c1b, c->c0b, c->pgb, c->P, c->Pd,
-                                  c->scal);
-  RH_LAUNCHED(c);
+  dbg_mark(st, "k_assemble");
   // numeric refactorization: blocks, separator rows (block updates), separator
   FactParams f{};
   f.nblk = A.nblk;
@@ -2665,8 +2699,10 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     if (!fdbg) cudaMalloc(&fdbg, 8 * 4096 * sizeof(long long));
     f.dbg = fdbg;
   }
+  dbg_mark(st, "assembled");
   k_fact_blocks<<<A.nblk, kSegThreads, c->smem_fact_blk, st>>>(f);
   RH_LAUNCHED(c);
+  dbg_mark(st, "k_fact_blocks");
   if (fprof) {  // timing experiment: per-block phase stamps (tools/fact_prof.py)
     std::vector<long long> hb((size_t)8 * A.nblk);
     cudaMemcpyAsync(hb.data(), fdbg, hb.size() * 8, cudaMemcpyDeviceToHost, st);
@@ -2684,6 +2720,9 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     RH_CUDA(c, cudaEventRecord(c->ev_sa, st));
     RH_CUDA(c, cudaStreamWaitEvent(side, c->ev_sa, 0));
   }
+  // the objective and its REF terms (needed by the gradient, not by the factorization)
+  k_objective<<<1, 1024, 0, sb>>>(nb, A.ref, c->has_gen, c->c2b, c->c1b, c->c0b, c->pgb, c->P, c->Pd, c->scal);
+  RH_LAUNCHED(c);
   if (!A.gpe_src.empty()) {
     const int ne = (int)A.gpe_src.size();
     k_gather_gpe<<<nblk(ne), kThreads, 0, sb>>>(ne, c->gpe_src, c->gpe_row, c->gpe_col, c->gp_val, c->gpe_rec);
@@ -2714,6 +2753,7 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     if (rc) return rc;
   }
   if (A.sep_rows > 0) {
+    dbg_mark(st, "side stream forked");
     k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, 0, st>>>(f);
     RH_LAUNCHED(c);
     // dense Schur complement of the separator, inverted by blocked Gauss-Jordan
@@ -2754,6 +2794,7 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
         fclose(fp);
       }
     }
+    dbg_mark(st, "k_sep_inverse");
     k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
     RH_LAUNCHED(c);
   }
@@ -3059,8 +3100,12 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   };
   // everything is enqueued before the one host sync (the pivot flag, read last)
   int rc = state_impl(c, x, p, st, c->sti[1], first_sweeps, true);
+  dbg_mark(st, "state done (joined side)");
   if (!rc) rc = rh_reduced_gradient(c, grad_p, nullptr, st);
+  dbg_mark(st, "gradient + tape");
   if (!rc && nb > 0) rc = hessian_batches(c, j0, j1, N, H, ldh, transposed, st, Hhost, early);
+  dbg_mark(st, "batches joined");
+  dbg_report(st);
   if (!rc) rc = check_pivots(c, st);
   return rc;
 }

@@ -87,7 +87,7 @@ def test_hvp_stages_random_W(solved_case):
     name, g, L, x, p, grad, lam, ops = solved_case
     ctx, *_ = setup(g)
     ctx.reduced_gradient()
-    for N in (1, 3, 37):
+    for N in (1, 3, 37, 70):
         W = gridgen.random_W(L.n_p, N, seed=N)
         trace = {}
         HWo = red.hvp_batch(ops, W, trace)
