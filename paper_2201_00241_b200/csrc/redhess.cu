@@ -1778,6 +1778,13 @@ struct rh_ctx {
   double2 *gpe_rec;
   DenseWs dws;                 // tracking Step 2 (dense.cu)
   cudaStream_t cp_st = nullptr;   // host copies of finished column blocks (rh_reduced_hessian_host)
+  // the fused call's gradient runs on its own stream with its own separator
+  // workspace and ticket counters; batches wait for the tape before k_for
+  cudaStream_t grad_st = nullptr;
+  cudaEvent_t ev_state = nullptr, ev_tape = nullptr;
+  double *grad_tsep = nullptr;
+  int *grad_ctr = nullptr;
+  cudaEvent_t tape_wait = nullptr;   // set while a fused call enqueues its batches
   struct TMapEntry {
     const double *base;
     int ld;
@@ -1792,6 +1799,12 @@ struct rh_ctx {
     for (auto &e : tmaps) cudaFree(e.dev);
     tmaps.clear();
     if (cp_st) cudaStreamDestroy(cp_st), cp_st = nullptr;
+    if (grad_st) cudaStreamDestroy(grad_st), grad_st = nullptr;
+    if (ev_state) cudaEventDestroy(ev_state), ev_state = nullptr;
+    if (ev_tape) cudaEventDestroy(ev_tape), ev_tape = nullptr;
+    if (grad_tsep) cudaFree(grad_tsep), grad_tsep = nullptr;
+    if (grad_ctr) cudaFree(grad_ctr), grad_ctr = nullptr;
+    tape_wait = nullptr;
     if (ev_cp) cudaEventDestroy(ev_cp), ev_cp = nullptr;
     for (auto &e : ev_trk)
       if (e) cudaEventDestroy(e), e = nullptr;
@@ -2386,6 +2399,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
     RH_LAUNCHED(c);
   }
   mark(3);
+  if (c->tape_wait) RH_CUDA(c, cudaStreamWaitEvent(st, c->tape_wait, 0));   // FoR needs the gradient's tape
   k_for<<<gF, 256, c->smem_for, st>>>(h);
   RH_LAUNCHED(c);
   if (Yxo) {
@@ -2837,11 +2851,16 @@ int rh_residual(rh_ctx *c, double *g, double *f, void *stream) {
   return RH_OK;
 }
 
-int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *stream) {
+}  // extern "C"
+
+namespace {
+// first-order adjoint + reduced gradient + FoR tape on `st`; own_ws: use the
+// gradient's private separator workspace and ticket counters (concurrent with
+// Hessian batches in the fused call)
+int gradient_impl(rh_ctx *c, double *grad_p, double *lambda_out, cudaStream_t st, bool own_ws) {
   int rc = check_ready(c, false);
   if (rc) return rc;
   if (!grad_p) return fail(c, RH_E_ARG, "grad_p is null");
-  cudaStream_t st = (cudaStream_t)stream;
   const Analysis &A = c->A;
   k_grad_rhs<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->x_bus, c->x_kind, c->pinv, c->refg_th, c->refg_v,
                                                 c->scal, c->X1col);
@@ -2853,6 +2872,17 @@ int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *str
   h.N = 1;
   h.ld = kSegC;   // column 0 carries the right-hand side, columns 1..31 stay zero
   h.P = c->X1col;
+  if (own_ws) {
+    if (!c->grad_tsep) {
+      if (cudaMalloc(&c->grad_tsep, sizeof(double) * kSegC * std::max(1, A.sep_rows)) != cudaSuccess ||
+          cudaMalloc(&c->grad_ctr, 16 * sizeof(int)) != cudaSuccess || cudaMemset(c->grad_ctr, 0, 16 * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, RH_E_NOMEM, "gradient workspace allocation failed");
+      }
+    }
+    h.Tsep = c->grad_tsep;
+    h.blk_ctr = c->grad_ctr;
+  }
   const int g1 = std::min(2 * c->nsm, A.nblk);
   k_blk<<<g1, kBlkThreads, c->smem_blk, st>>>(h, MODE_UT);
   RH_LAUNCHED(c);
@@ -2871,6 +2901,13 @@ int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *str
   if (lambda_out)
     RH_CUDA(c, cudaMemcpyAsync(lambda_out, c->lam, sizeof(double) * A.n_x, cudaMemcpyDeviceToDevice, st));
   return build_tape(c, st);
+}
+}  // namespace
+
+extern "C" {
+
+int rh_reduced_gradient(rh_ctx *c, double *grad_p, double *lambda_out, void *stream) {
+  return gradient_impl(c, grad_p, lambda_out, (cudaStream_t)stream, false);
 }
 
 int rh_set_multipliers(rh_ctx *c, const double *lambda, void *stream) {
@@ -3101,10 +3138,24 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   // everything is enqueued before the one host sync (the pivot flag, read last)
   int rc = state_impl(c, x, p, st, c->sti[1], first_sweeps, true);
   dbg_mark(st, "state done (joined side)");
-  if (!rc) rc = rh_reduced_gradient(c, grad_p, nullptr, st);
-  dbg_mark(st, "gradient + tape");
-  if (!rc && nb > 0) rc = hessian_batches(c, j0, j1, N, H, ldh, transposed, st, Hhost, early);
-  dbg_mark(st, "batches joined");
+  // the gradient (and the tape) on its own stream; the batches' separator and U
+  // sweeps run meanwhile, each batch waits for the tape right before k_for
+  if (!rc) {
+    if (!c->grad_st) RH_CUDA(c, cudaStreamCreateWithFlags(&c->grad_st, cudaStreamNonBlocking));
+    if (!c->ev_state) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_state, cudaEventDisableTiming));
+    if (!c->ev_tape) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_tape, cudaEventDisableTiming));
+    RH_CUDA(c, cudaEventRecord(c->ev_state, st));
+    RH_CUDA(c, cudaStreamWaitEvent(c->grad_st, c->ev_state, 0));
+    rc = gradient_impl(c, grad_p, nullptr, c->grad_st, true);
+    if (!rc) RH_CUDA(c, cudaEventRecord(c->ev_tape, c->grad_st));
+  }
+  if (!rc && nb > 0) {
+    c->tape_wait = c->ev_tape;
+    rc = hessian_batches(c, j0, j1, N, H, ldh, transposed, st, Hhost, early);
+    c->tape_wait = nullptr;
+  }
+  if (!rc) RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_tape, 0));
+  dbg_mark(st, "gradient + batches joined");
   dbg_report(st);
   if (!rc) rc = check_pivots(c, st);
   return rc;
