@@ -1785,6 +1785,8 @@ struct rh_ctx {
   double *grad_tsep = nullptr;
   int *grad_ctr = nullptr;
   cudaEvent_t tape_wait = nullptr;   // set while a fused call enqueues its batches
+  // side stream of the fused call: block-only derived values done; each early L sweep done
+  cudaEvent_t ev_derived = nullptr, ev_early[kNumWs] = {};
   struct TMapEntry {
     const double *base;
     int ld;
@@ -1805,6 +1807,9 @@ struct rh_ctx {
     if (grad_tsep) cudaFree(grad_tsep), grad_tsep = nullptr;
     if (grad_ctr) cudaFree(grad_ctr), grad_ctr = nullptr;
     tape_wait = nullptr;
+    if (ev_derived) cudaEventDestroy(ev_derived), ev_derived = nullptr;
+    for (auto &e : ev_early)
+      if (e) cudaEventDestroy(e), e = nullptr;
     if (ev_cp) cudaEventDestroy(ev_cp), ev_cp = nullptr;
     for (auto &e : ev_trk)
       if (e) cudaEventDestroy(e), e = nullptr;
@@ -2763,6 +2768,8 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     RH_LAUNCHED(c);
   }
   if (early) {
+    if (!c->ev_derived) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_derived, cudaEventDisableTiming));
+    RH_CUDA(c, cudaEventRecord(c->ev_derived, sb));   // what st needs from the side stream
     const int rc = early(sb);
     if (rc) return rc;
   }
@@ -2827,7 +2834,9 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
                                                                reinterpret_cast<double *>(c->uLt));
     RH_LAUNCHED(c);
   }
-  if (side) {
+  if (side && early) {   // the early sweeps are joined batch by batch (hessian_batches)
+    RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_derived, 0));
+  } else if (side) {
     RH_CUDA(c, cudaEventRecord(c->ev_sb, side));
     RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_sb, 0));
   }
@@ -3063,6 +3072,7 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
     double *out = transposed ? H + (long long)a0 * ldh : H + a0;
     const int k = b % nws;
     cudaStream_t sb = k ? c->sti[k] : st;
+    if (b < early) RH_CUDA(c, cudaStreamWaitEvent(sb, c->ev_early[b], 0));   // its L sweep (side stream)
     int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0, k,
                       b < early ? 2 : 0);
     if (rc) return rc;
@@ -3132,6 +3142,8 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
       if (int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0,
                             b, 1))
         return rc;
+      if (!c->ev_early[b]) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_early[b], cudaEventDisableTiming));
+      RH_CUDA(c, cudaEventRecord(c->ev_early[b], sb));
     }
     return RH_OK;
   };
