@@ -9,7 +9,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv 
 timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.txt 2>&1
 timeout 900 python bench.py "$@" > $OUT/bench.json 2> $OUT/bench.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $OUT/launches.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 450 --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline "$@" > $OUT/ncu_launch_bench.log 2>&1
 python tools/launch_summary.py $OUT/launches.csv > $OUT/launch_summary.txt 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_blk|k_for|k_sep_gemm|k_sep_gather|k_muladd" -s 10 -c 8 \
