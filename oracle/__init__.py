@@ -19,7 +19,9 @@ Modules:
                 Eq. powerflowvec, Eq. lagrangian)
   reduction  -- reduced gradient, Alg. 1, Alg. 2, full Hessian, dense definition
                 (PAPER.md 3.3, 4.1-4.3, Eq. socadjoint, Eq. hessvecprod)
+  coloring   -- Jacobians by column coloring + forward mode (PAPER.md 4,
+                PAPER.md:440-468, 694-713)
   tracking   -- the real-time tracking step: Newton, g_t, H_t, dense Cholesky
                 solve of Eq. qp_rto (PAPER.md 6.3)
 """
-from . import powerflow, reduction, tracking  # noqa: F401
+from . import coloring, powerflow, reduction, tracking  # noqa: F401
