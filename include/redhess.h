@@ -261,6 +261,27 @@ int rh_tracking_step(rh_ctx *ctx, double *x, double *p, const double *Pd, const 
                      int32_t j1, int32_t N, double alpha, double *grad_p, double *H, int64_t ldh, double *d,
                      double *info, void *stream);
 
+/* ---- Jacobians by column coloring + forward mode (
+ *      SURVEY.md 8(f) NEXT-4) ---- */
+
+/* Jacobian modes for rh_set_state / rh_newton / rh_reduced_hessian:
+ * RH_JAC_ANALYTIC (default) assembles J and G_p from the closed-form partials;
+ * RH_JAC_COLORED evaluates them the paper's way: the columns of [J | G_p] are
+ * colored (greedy, column order, DESIGN.md R-C1..R-C3), one forward-mode tangent
+ * per color is propagated through the residual, and J, G_p are decompressed from
+ * the compressed product.  Same values up to rounding.  Invalidates the state. */
+enum { RH_JAC_ANALYTIC = 0, RH_JAC_COLORED = 1 };
+int rh_set_jacobian_mode(rh_ctx *ctx, int32_t mode);
+
+/* The column coloring (host outputs): colors [n_x + n_p] (x columns, then p
+ * columns; nullable), ncolors (nullable).  Needs a loaded grid. */
+int rh_coloring(const rh_ctx *ctx, int32_t *colors, int32_t *ncolors);
+
+/* Compressed Jacobian at the current state: JS [n_x][ncolors] (DEVICE,
+ * row-major, rows in the natural x order = residual rows, R5) = [J | G_p] S,
+ * S[j][color(j)] = 1, by forward-mode tangents.  Needs rh_set_state. */
+int rh_compressed_jacobian(rh_ctx *ctx, double *JS, void *stream);
+
 /* Number of CUDA kernels this library launched on ctx since creation
  * (bench accounting of "gpu_launches"). */
 int64_t rh_launch_count(const rh_ctx *ctx);

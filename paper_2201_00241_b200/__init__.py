@@ -23,6 +23,7 @@ LIB_PATH = os.path.join(HERE, "libredhess.so")
 STATUS_NAMES = {0: "RH_OK", 1: "RH_E_ARG", 2: "RH_E_GRID", 3: "RH_E_ORDER", 4: "RH_E_SINGULAR",
                 5: "RH_E_CUDA", 6: "RH_E_NOMEM", 7: "RH_E_NODEV", 8: "RH_E_NOCONV", 9: "RH_E_NOTPD"}
 KIND_THETA, KIND_V, KIND_PG = 0, 1, 2
+JAC_ANALYTIC, JAC_COLORED = 0, 1
 
 # every symbol declared in include/redhess.h (checked by tests/test_abi.py)
 EXPORTS = ["rh_create", "rh_destroy", "rh_last_error", "rh_load_grid", "rh_get_info", "rh_orderings",
@@ -30,6 +31,7 @@ EXPORTS = ["rh_create", "rh_destroy", "rh_last_error", "rh_load_grid", "rh_get_i
            "rh_newton",
            "rh_hvp", "rh_hvp_stages", "rh_hessian_columns", "rh_full_hessian", "rh_reduced_hessian",
            "rh_reduced_hessian_host", "rh_set_loads", "rh_dense_spd_solve", "rh_tracking_step",
+           "rh_set_jacobian_mode", "rh_coloring", "rh_compressed_jacobian",
            "rh_launch_count", "rh_set_timing", "rh_stage_times"]
 
 
@@ -87,6 +89,9 @@ def _load():
         "rh_dense_spd_solve": ([vp, i32, vp, i64, vp, vp, vp, dbl, ctypes.POINTER(dbl), ctypes.POINTER(i32), vp],
                                ctypes.c_int),
         "rh_tracking_step": ([vp, vp, vp, vp, vp, i32, i32, i32, dbl, vp, vp, i64, vp, vp, vp], ctypes.c_int),
+        "rh_set_jacobian_mode": ([vp, i32], ctypes.c_int),
+        "rh_coloring": ([vp, vp, ctypes.POINTER(i32)], ctypes.c_int),
+        "rh_compressed_jacobian": ([vp, vp, vp], ctypes.c_int),
         "rh_launch_count": ([vp], i64),
         "rh_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
         "rh_stage_times": ([vp, vp], ctypes.c_int),
@@ -365,6 +370,26 @@ class RedHess:
                                         _ptr(H), H.stride(0), _ptr(d), _ptr(info), _stream(stream)))
         keys = ("newton_steps", "resid", "F", "tau", "attempts", "ms_step1", "ms_step2")
         return grad, H, d, dict(zip(keys, info.tolist()))
+
+    # ------------------------------------------------------------------ colored Jacobians (PAPER.md 4)
+    def set_jacobian_mode(self, mode):
+        """rh_set_jacobian_mode: JAC_ANALYTIC or JAC_COLORED (coloring + forward mode)."""
+        self._rc(lib().rh_set_jacobian_mode(self._h, int(mode)))
+
+    def coloring(self):
+        """rh_coloring: (colors [n_x + n_p] int32, ncolors)."""
+        nc = ctypes.c_int32(0)
+        colors = np.zeros(self.n_x + self.n_p, np.int32)
+        self._rc(lib().rh_coloring(self._h, _ptr(colors), ctypes.byref(nc)))
+        return colors, nc.value
+
+    def compressed_jacobian(self, stream=None):
+        """rh_compressed_jacobian: JS [n_x][ncolors] (DEVICE) at the current state."""
+        import torch
+        _, nc = self.coloring()
+        JS = torch.empty((self.n_x, max(1, nc)), dtype=torch.float64, device="cuda")
+        self._rc(lib().rh_compressed_jacobian(self._h, _ptr(JS), _stream(stream)))
+        return JS
 
     # ------------------------------------------------------------------ accounting
     def launch_count(self):

@@ -1298,6 +1298,90 @@ std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
       }
   }
 
+  // ---------------- column coloring of [J | G_p] (NEXT-4) ----------------
+  // Columns: x entries, then p entries (R-C1).  Structural rows (natural residual
+  // rows) of a theta_o / v_o column: the P / Q rows of o and its neighbours; of a
+  // Pg_o column: P_o (R-C2).  Greedy: each column takes the smallest color unused
+  // by its conflicting predecessors.
+  {
+    const int np_ = A.n_p, ncol = nx + np_;
+    std::vector<std::vector<int32_t>> nbr(n);
+    for (int b = 0; b < n; ++b) {
+      for (int s = A.bl_ptr[b]; s < A.bl_ptr[b + 1]; ++s) nbr[b].push_back(A.bl_other[s]);
+      nbr[b].push_back(b);
+      sort_unique(nbr[b]);
+    }
+    std::vector<std::vector<int32_t>> crow(ncol);
+    auto bus_rows = [&](int o, std::vector<int32_t> &out) {
+      out.clear();
+      for (int c : nbr[o]) {
+        if (A.th_x[c] >= 0) out.push_back(A.th_x[c]);
+        if (A.v_x[c] >= 0) out.push_back(A.v_x[c]);
+      }
+    };
+    for (int j = 0; j < nx; ++j) bus_rows(A.x_bus[j], crow[j]);
+    for (int k = 0; k < np_; ++k) {
+      if (A.p_kind[k] == RH_KIND_PG) crow[nx + k] = {A.th_x[A.p_bus[k]]};
+      else bus_rows(A.p_bus[k], crow[nx + k]);
+    }
+    std::vector<std::vector<int32_t>> row_cols(nx);
+    std::vector<int32_t> stamp(ncol + 1, -1);
+    A.colors.assign(ncol, -1);
+    A.ncolors = 0;
+    for (int j = 0; j < ncol; ++j) {
+      for (int r : crow[j])
+        for (int k : row_cols[r]) stamp[A.colors[k]] = j;
+      int c = 0;
+      while (stamp[c] == j) ++c;
+      A.colors[j] = c;
+      A.ncolors = std::max(A.ncolors, c + 1);
+      for (int r : crow[j]) row_cols[r].push_back(j);
+    }
+    A.col_th.assign(n, -1);
+    A.col_v.assign(n, -1);
+    A.col_pg.assign(n, -1);
+    for (int b = 0; b < n; ++b) {
+      if (A.th_x[b] >= 0) A.col_th[b] = A.colors[A.th_x[b]];
+      if (A.v_x[b] >= 0) A.col_v[b] = A.colors[A.v_x[b]];
+      else if (A.v_p[b] >= 0) A.col_v[b] = A.colors[nx + A.v_p[b]];
+      if (A.pg_p[b] >= 0) A.col_pg[b] = A.colors[nx + A.pg_p[b]];
+    }
+    // decompression entries: F (J) and G_p positions with their row and column color
+    A.jd_pos.clear(); A.jd_row.clear(); A.jd_col.clear();
+    A.gd_pos.clear(); A.gd_row.clear(); A.gd_col.clear();
+    auto addj = [&](int pos, int row, int color) {
+      if (pos < 0) return;
+      A.jd_pos.push_back(pos); A.jd_row.push_back(row); A.jd_col.push_back(color);
+    };
+    auto addg = [&](int pos, int row, int color) {
+      if (pos < 0) return;
+      A.gd_pos.push_back(pos); A.gd_row.push_back(row); A.gd_col.push_back(color);
+    };
+    for (int b = 0; b < n; ++b) {
+      if (b == A.ref) continue;
+      const int rP = A.th_x[b], rQ = A.v_x[b];
+      addj(A.diag_pos[4 * b + 0], rP, A.col_th[b]);
+      if (rQ >= 0) {
+        addj(A.diag_pos[4 * b + 1], rP, A.col_v[b]);
+        addj(A.diag_pos[4 * b + 2], rQ, A.col_th[b]);
+        addj(A.diag_pos[4 * b + 3], rQ, A.col_v[b]);
+      }
+      addg(A.gp_self_pos[b], rP, A.col_v[b]);
+      addg(A.gp_pg_pos[b], rP, A.col_pg[b]);
+      for (int s = A.bl_ptr[b]; s < A.bl_ptr[b + 1]; ++s) {
+        const int o = A.bl_other[s];
+        addj(A.slot_pos[4 * s + 0], rP, A.col_th[o]);
+        addj(A.slot_pos[4 * s + 1], rP, A.col_v[o]);
+        if (rQ >= 0) {
+          addj(A.slot_pos[4 * s + 2], rQ, A.col_th[o]);
+          addj(A.slot_pos[4 * s + 3], rQ, A.col_v[o]);
+        }
+        addg(A.gp_slot_pos[2 * s + 0], rP, A.col_v[o]);
+        if (rQ >= 0) addg(A.gp_slot_pos[2 * s + 1], rQ, A.col_v[o]);
+      }
+    }
+  }
+
   // ---------------- FoR sources / destinations ----------------
   A.dth_src.assign(n, -1);
   A.dv_src.assign(n, -1);

@@ -149,6 +149,13 @@ struct Analysis {
   std::vector<int32_t> gp_self_pos;         // per bus: position of (P_b, v_p[b]) if b PV else -1
   std::vector<int32_t> gp_pg_pos;           // per bus: position of (P_b, Pg_b) if b PV else -1
   std::vector<int32_t> gp_slot_pos;         // [2 n_line * 2]: (P_b, v_o), (Q_b, v_o)
+  // column coloring of [J | G_p] (NEXT-4, DESIGN.md R-C1..R-C3): colors of the
+  // n_x + n_p columns, per-bus seed colors, decompression entries (F / G_p
+  // position, natural residual row, color)
+  std::vector<int32_t> colors;
+  int ncolors = 0;
+  std::vector<int32_t> col_th, col_v, col_pg;
+  std::vector<int32_t> jd_pos, jd_row, jd_col, gd_pos, gd_row, gd_col;
   // G_p CSC (by p column): positions into gp value array and permuted rows
   std::vector<int32_t> gpc_ptr, gpc_pos, gpc_row;
 

@@ -152,6 +152,62 @@ __global__ void k_assemble(AsmParams a) {
 
 // f (R4) and the REF multiplier seed mu_ref = f'(Pg_ref) (R22).  One block.
 // scal[0] = P_ref, scal[1] = Pg_ref, scal[2] = mu_ref, scal[3] = f
+// NEXT-4: forward-mode tangents of the residual, one
+// direction per column color.  Thread (bus b, color c): the seed of a bus
+// variable is 1 iff its column has color c; the dual-number derivative of
+// P_b = v_b sum_o v_o (G cos th_bo + B sin th_bo) + v_b^2 G_bb and of Q_b
+// (R1) along that seed, minus the Pg seed for g[P_b] (R2), lands in
+// JS[row][c] with rows in the natural x order.
+__global__ void k_jvp_colored(int n_bus, int ref, int C, const int *__restrict__ bl_ptr,
+                              const int *__restrict__ bl_line, const int *__restrict__ bl_other,
+                              const int *__restrict__ bl_end, const double2 *__restrict__ cs,
+                              const double *__restrict__ G_ft, const double *__restrict__ B_ft,
+                              const double *__restrict__ G_tf, const double *__restrict__ B_tf,
+                              const double *__restrict__ G_ii, const double *__restrict__ B_ii,
+                              const double *__restrict__ v, const int *__restrict__ th_x, const int *__restrict__ v_x,
+                              const int *__restrict__ col_th, const int *__restrict__ col_v,
+                              const int *__restrict__ col_pg, double *JS) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)n_bus * C) return;
+  const int b = (int)(t / C), c = (int)(t % C);
+  if (b == ref) return;
+  const double vb = v[b];
+  const double sth_b = col_th[b] == c ? 1.0 : 0.0, sv_b = col_v[b] == c ? 1.0 : 0.0;
+  double dP = 0.0, dQ = 0.0;
+  for (int s = bl_ptr[b]; s < bl_ptr[b + 1]; ++s) {
+    const int l = bl_line[s], o = bl_other[s];
+    const double2 q = cs[l];
+    const bool from = bl_end[s] == 0;
+    const double G = from ? G_ft[l] : G_tf[l];
+    const double B = from ? B_ft[l] : B_tf[l];
+    const double co = q.x, sn = from ? q.y : -q.y;   // cos/sin(th_b - th_o)
+    const double vo = v[o];
+    const double sth_o = col_th[o] == c ? 1.0 : 0.0, sv_o = col_v[o] == c ? 1.0 : 0.0;
+    const double gcbs = G * co + B * sn, gsbc = G * sn - B * co;
+    const double dvv = sv_b * vo + vb * sv_o, vv = vb * vo, dth = sth_b - sth_o;
+    dP += dvv * gcbs - vv * gsbc * dth;   // d[v_b v_o (G c + B s)]
+    dQ += dvv * gsbc + vv * gcbs * dth;   // d[v_b v_o (G s - B c)]
+  }
+  dP += 2.0 * vb * G_ii[b] * sv_b;
+  dQ -= 2.0 * vb * B_ii[b] * sv_b;
+  if (col_pg[b] == c) dP -= 1.0;
+  JS[(long long)th_x[b] * C + c] = dP;
+  if (v_x[b] >= 0) JS[(long long)v_x[b] * C + c] = dQ;
+}
+
+// decompression: entry (pos, row, color) of J / G_p reads JS[row][color]
+__global__ void k_decompress(int nj, const int *__restrict__ jpos, const int *__restrict__ jrow,
+                             const int *__restrict__ jcol, double *F_val, int ng, const int *__restrict__ gpos,
+                             const int *__restrict__ grow, const int *__restrict__ gcol, double *gp_val, int C,
+                             const double *__restrict__ JS) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < nj) F_val[jpos[t]] = JS[(long long)jrow[t] * C + jcol[t]];
+  else if (t - nj < ng) {
+    const int u = t - nj;
+    gp_val[gpos[u]] = JS[(long long)grow[u] * C + gcol[u]];
+  }
+}
+
 __global__ void k_state_init(int nx, int np_, const double *__restrict__ x, const double *__restrict__ p, double *cx,
                              double *cp, long long nF, double *F_val, long long nG, double *gp_val, int nb,
                              double *refg_th, double *refg_v, int *status) {
@@ -1715,6 +1771,10 @@ struct rh_ctx {
   double *F_val;
   int *status;
   int *diag_pos, *slot_pos, *gp_rptr, *gp_col, *gp_self_pos, *gp_pg_pos, *gp_slot_pos;
+  // NEXT-4: Jacobians by column coloring + forward mode (rh_set_jacobian_mode)
+  int *col_th, *col_v, *col_pg, *jd_pos, *jd_row, *jd_col, *gd_pos, *gd_row, *gd_col;
+  double *JS = nullptr;   // [n_x][ncolors] compressed [J | G_p] S
+  int jac_mode = 0;       // 0 analytic assembly, 1 colored forward mode
   double *gp_val;
   int *gpc_ptr, *gpc_pos, *gpc_row;
   double *gpc_val;
@@ -1929,6 +1989,10 @@ int upload(rh_ctx *c) {
   UP(F_rowptr, A.F_rowptr); UP(F_diag, A.F_diag);
   UP(diag_pos, A.diag_pos); UP(slot_pos, A.slot_pos); UP(gp_rptr, A.gp_rptr); UP(gp_col, A.gp_col);
   UP(gp_self_pos, A.gp_self_pos); UP(gp_pg_pos, A.gp_pg_pos); UP(gp_slot_pos, A.gp_slot_pos);
+  UP(col_th, A.col_th); UP(col_v, A.col_v); UP(col_pg, A.col_pg);
+  UP(jd_pos, A.jd_pos); UP(jd_row, A.jd_row); UP(jd_col, A.jd_col);
+  UP(gd_pos, A.gd_pos); UP(gd_row, A.gd_row); UP(gd_col, A.gd_col);
+  chk(c->JS = dalloc<double>((size_t)A.n_x * std::max(1, A.ncolors), P));
   UP(gpc_ptr, A.gpc_ptr); UP(gpc_pos, A.gpc_pos); UP(gpc_row, zr(A.gpc_row));
   UP(dth_src, zr(A.dth_src)); UP(dv_src, zr(A.dv_src)); UP(yth_dst, zr(A.yth_dst)); UP(yv_dst, zr(A.yv_dst));
   UP(pg_p, A.pg_p); UP(near_ref, A.near_ref);
@@ -2617,6 +2681,25 @@ void dbg_report(cudaStream_t st) {
   g_marks.clear();
 }
 
+// NEXT-4: JS = [J | G_p] S by forward-mode tangents (needs line trig and bus
+// state of the current point); decompress = overwrite J's and G_p's values
+int colored_jacobian(rh_ctx *c, cudaStream_t st, bool decompress) {
+  const Analysis &A = c->A;
+  const int C = std::max(1, A.ncolors);
+  const long long nt = (long long)A.n_bus * C;
+  k_jvp_colored<<<(unsigned)((nt + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+      A.n_bus, A.ref, C, c->bl_ptr, c->bl_line, c->bl_other, c->bl_end, c->cs, c->G_ft, c->B_ft, c->G_tf, c->B_tf,
+      c->G_ii, c->B_ii, c->v, c->th_x, c->v_x, c->col_th, c->col_v, c->col_pg, c->JS);
+  RH_LAUNCHED(c);
+  if (decompress) {
+    const int nj = (int)A.jd_pos.size(), ng = (int)A.gd_pos.size();
+    k_decompress<<<nblk(nj + ng), kThreads, 0, st>>>(nj, c->jd_pos, c->jd_row, c->jd_col, c->F_val, ng, c->gd_pos,
+                                                     c->gd_row, c->gd_col, c->gp_val, C, c->JS);
+    RH_LAUNCHED(c);
+  }
+  return RH_OK;
+}
+
 int check_pivots(rh_ctx *c, cudaStream_t st) {   // reads the refactorization's pivot flag (one sync)
   int status = 0;
   RH_CUDA(c, cudaMemcpyAsync(&status, c->status, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -2690,6 +2773,8 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   k_assemble<<<nblk(nb, 128), 128, 0, st>>>(a);
   RH_LAUNCHED(c);
   dbg_mark(st, "k_assemble");
+  if (c->jac_mode == 1)
+    if (int rc = colored_jacobian(c, st, true)) return rc;
   // numeric refactorization: blocks, separator rows (block updates), separator
   FactParams f{};
   f.nblk = A.nblk;
@@ -3320,6 +3405,33 @@ int rh_tracking_step(rh_ctx *c, double *x, double *p, const double *Pd, const do
     info[5] = m1;
     info[6] = m2;
   }
+  return RH_OK;
+}
+
+int rh_set_jacobian_mode(rh_ctx *c, int32_t mode) {
+  if (!c) return RH_E_ARG;
+  if (mode != RH_JAC_ANALYTIC && mode != RH_JAC_COLORED) return fail(c, RH_E_ARG, "unknown Jacobian mode");
+  c->jac_mode = mode;
+  c->has_state = c->has_mult = false;
+  return RH_OK;
+}
+
+int rh_coloring(const rh_ctx *c, int32_t *colors, int32_t *ncolors) {
+  if (!c) return RH_E_ARG;
+  if (!c->loaded) return RH_E_ORDER;
+  if (colors) std::copy(c->A.colors.begin(), c->A.colors.end(), colors);
+  if (ncolors) *ncolors = c->A.ncolors;
+  return RH_OK;
+}
+
+int rh_compressed_jacobian(rh_ctx *c, double *JS, void *stream) {
+  int rc = check_ready(c, false);
+  if (rc) return rc;
+  if (!JS) return fail(c, RH_E_ARG, "JS is null");
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((rc = colored_jacobian(c, st, false))) return rc;
+  RH_CUDA(c, cudaMemcpyAsync(JS, c->JS, sizeof(double) * c->A.n_x * std::max(1, c->A.ncolors),
+                             cudaMemcpyDeviceToDevice, st));
   return RH_OK;
 }
 

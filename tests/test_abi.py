@@ -144,3 +144,18 @@ def test_host_only_context_refuses_compute():
     with pytest.raises(rh.RHError) as ei:
         c.reduced_hessian_host(x, p, 5)
     assert ei.value.code == rh.RH_E_NODEV
+
+
+@pytest.mark.parametrize("name", ["case9", "case118", "case1354pegase", "case9241pegase"])
+def test_coloring_matches_oracle(name):
+    # NEXT-4: the host analysis colors [J | G_p] exactly as oracle/coloring.py (R-C1, R-C2)
+    from oracle import coloring as col
+    from oracle import powerflow as pf
+    g = gridgen.make_grid(name)
+    ctx = rh.RedHess(-1)
+    ctx.load_grid(g)
+    colors, nc = ctx.coloring()
+    L = pf.Layout(g)
+    co = col.greedy_coloring(col.column_rows(g, L), L.n_x)
+    assert nc == int(co.max()) + 1
+    assert np.array_equal(colors, co.astype(np.int32))
