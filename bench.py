@@ -248,6 +248,14 @@ def tracking_bench(rh, gridgen, dev, case, N, minutes, warm=2, T=60):
                         "+-5 % per-bus-phase sinusoidal loads (seed 4), free = Pg set points"}
 
 
+def lib_cj(ctx, JS):
+    """rh_compressed_jacobian into a preallocated device buffer."""
+    import paper_2201_00241_b200 as rh
+    rc = rh.lib().rh_compressed_jacobian(ctx._h, JS.data_ptr(), rh._stream(None))
+    if rc:
+        raise rh.RHError(rc, rh.lib().rh_last_error(ctx._h).decode())
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -454,6 +462,40 @@ def main():
     ctx.set_state(x, p)
     ctx.reduced_gradient(grad)
 
+    # ---- NEXT-4: Jacobians by coloring + forward mode (PAPER.md 4) vs analytic assembly
+    colors, ncolors = ctx.coloring()
+    JSb = torch.empty((n_x, max(1, ncolors)), dtype=torch.float64, device=dev)
+    ej0, ej1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    jv, st_ms = [], {}
+    for _ in range(3):
+        lib_cj(ctx, JSb)
+    for _ in range(10):
+        torch.cuda.synchronize()
+        ej0.record(stream)
+        lib_cj(ctx, JSb)
+        ej1.record(stream)
+        torch.cuda.synchronize()
+        jv.append(ej0.elapsed_time(ej1))
+    for mode in (rh.JAC_ANALYTIC, rh.JAC_COLORED):
+        ctx.set_jacobian_mode(mode)
+        ts = []
+        for rep in range(6):
+            torch.cuda.synchronize()
+            ej0.record(stream)
+            ctx.reduced_hessian(x, p, N, j0, j1, grad, H=Hloc, transposed=True)
+            ej1.record(stream)
+            torch.cuda.synchronize()
+            if rep:
+                ts.append(ej0.elapsed_time(ej1))
+        st_ms[mode] = float(np.median(ts))
+    ctx.set_jacobian_mode(rh.JAC_ANALYTIC)
+    ctx.set_state(x, p)
+    ctx.reduced_gradient(grad)
+    jac_colored = {"ncolors": ncolors, "columns": n_x + n_p, "compressed_jacobian_ms": float(np.median(jv)),
+                   "step_ms_analytic": st_ms[rh.JAC_ANALYTIC], "step_ms_colored": st_ms[rh.JAC_COLORED],
+                   "note": "k_jvp_colored (one forward-mode tangent per color) timed alone; steps = the fused "
+                           "state + gradient + Hessian call (L2 not flushed) in each Jacobian mode"}
+
     # ---- real-time tracking: the paper's Table 3 case, and this case
     tracking = None
     if world == 1:
@@ -502,6 +544,7 @@ def main():
                        "max_abs_x_err": newton_err,
                        "start": "solved x + 1e-3 N(0,1) (seed 7; from 1e-2 the oracle diverges too on case9241); tol 1e-11, 2 extra steps (oracle rule); host wall clock incl. one max|dx| readback per step"},
             "tracking": tracking,
+            "jacobian_colored": jac_colored,
             "cpu_baseline": cpu,
             "clocks": {k: clk[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
         }
