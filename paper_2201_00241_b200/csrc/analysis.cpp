@@ -1298,6 +1298,33 @@ std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
       }
   }
 
+  // ---------------- incidence owners; slot uniqueness (two-kernel assembly) ----------------
+  {
+    A.bl_bus.assign(2 * m, -1);
+    for (int b = 0; b < n; ++b)
+      for (int s = A.bl_ptr[b]; s < A.bl_ptr[b + 1]; ++s) A.bl_bus[s] = b;
+    std::vector<int32_t> seen;
+    for (int v : A.slot_pos)
+      if (v >= 0) seen.push_back(v);
+    const size_t nf = seen.size();
+    sort_unique(seen);
+    bool uniq = seen.size() == nf;
+    seen.clear();
+    for (int v : A.gp_slot_pos)
+      if (v >= 0) seen.push_back(v);
+    const size_t ng = seen.size();
+    sort_unique(seen);
+    uniq = uniq && seen.size() == ng;
+    seen.clear();
+    if (A.ref >= 0) {
+      for (int s = A.bl_ptr[A.ref]; s < A.bl_ptr[A.ref + 1]; ++s) seen.push_back(A.bl_other[s]);
+      const size_t nr = seen.size();
+      sort_unique(seen);
+      uniq = uniq && seen.size() == nr;
+    }
+    A.asm_unique = uniq;
+  }
+
   // ---------------- column coloring of [J | G_p] (NEXT-4) ----------------
   // Columns: x entries, then p entries (R-C1).  Structural rows (natural residual
   // rows) of a theta_o / v_o column: the P / Q rows of o and its neighbours; of a

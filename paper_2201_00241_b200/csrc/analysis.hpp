@@ -129,6 +129,8 @@ struct Analysis {
 
   // bus -> incident line CSR (slots); end = 0 if bus is the line's from-end
   std::vector<int32_t> bl_ptr, bl_line, bl_other, bl_end;
+  std::vector<int32_t> bl_bus;   // [2 n_line] owner bus of each incidence
+  bool asm_unique = false;       // no two incidences share a J / G_p / REF-gradient slot (no parallel lines)
 
   // ---------------- ordering + symbolic ----------------
   std::vector<int32_t> perm, pinv;          // perm[new] = old x index

@@ -82,11 +82,83 @@ struct AsmParams {
   const int *diag_pos, *slot_pos;
   const int *gp_self_pos, *gp_pg_pos, *gp_slot_pos;
   double *P, *Q, *g, *F_val, *gp_val, *refg_th, *refg_v;
+  const int *bl_bus;    // two-kernel path: owner bus of each incidence
+  double *tP, *tQ;      // two-kernel path: per-incidence injection terms
+  int n_inc;
 };
 
 // Bus-centric assembly (race-free: bus b owns rows P_b, Q_b).  Eq. powerflow
 // with the Ybus diagonal (R1); g per Eq. powerflowvec
 // (R2); J / G_p entries per SURVEY.md Appendix A.
+// Two-kernel assembly (grids without parallel lines, A.asm_unique): every J /
+// G_p line slot and REF-gradient entry has one incidence, so the line kernel
+// stores it directly, and the bus kernel sums its incidences' injection terms in
+// the same order as k_assemble (equal to rounding: k_assemble contracts each term
+// into its running sum with an FMA), with much shorter dependent chains.
+__global__ void k_asm_lines(AsmParams a) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.n_inc) return;
+  const int b = a.bl_bus[s], l = a.bl_line[s], o = a.bl_other[s];
+  const double vb = a.v[b], vo = a.v[o];
+  const double2 cs = a.cs[l];
+  const bool from = a.bl_end[s] == 0;
+  const double G = from ? a.G_ft[l] : a.G_tf[l];
+  const double B = from ? a.B_ft[l] : a.B_tf[l];
+  const double c = cs.x, sn = from ? cs.y : -cs.y;   // cos/sin(th_b - th_o)
+  const double gsbc = G * sn - B * c, gcbs = G * c + B * sn;
+  a.tP[s] = vo * gcbs;
+  a.tQ[s] = vo * gsbc;
+  if (b == a.ref) {
+    a.refg_th[o] = vb * vo * gsbc;
+    a.refg_v[o] = vb * gcbs;
+    return;
+  }
+  const double dPth = vb * vo * gsbc, dPv = vb * gcbs;
+  const double dQth = -vb * vo * gcbs, dQv = vb * gsbc;
+  const int4 sp = *reinterpret_cast<const int4 *>(a.slot_pos + 4 * s);
+  if (sp.x >= 0) a.F_val[sp.x] = dPth;
+  if (sp.y >= 0) a.F_val[sp.y] = dPv;
+  if (sp.z >= 0) a.F_val[sp.z] = dQth;
+  if (sp.w >= 0) a.F_val[sp.w] = dQv;
+  const int2 gs = *reinterpret_cast<const int2 *>(a.gp_slot_pos + 2 * s);
+  if (gs.x >= 0) a.gp_val[gs.x] = dPv;
+  if (gs.y >= 0) a.gp_val[gs.y] = dQv;
+}
+__global__ void k_asm_buses(AsmParams a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.n_bus) return;
+  const double vb = a.v[b];
+  double P = 0.0, Q = 0.0;
+  for (int s = a.bl_ptr[b]; s < a.bl_ptr[b + 1]; ++s) {
+    P += a.tP[s];
+    Q += a.tQ[s];
+  }
+  const double Gbb = a.G_ii[b], Bbb = a.B_ii[b];
+  P = vb * P + vb * vb * Gbb;
+  Q = vb * Q - vb * vb * Bbb;
+  a.P[b] = P;
+  a.Q[b] = Q;
+  if (b == a.ref) {
+    a.refg_v[b] += P / vb + Gbb * vb;
+    return;
+  }
+  const int t = a.bus_type[b];
+  const int rP = a.th_x[b];
+  const int rQ = a.v_x[b];
+  a.g[rP] = P + a.Pd[b] - (t == RH_PV ? a.pgb[b] : 0.0);
+  if (rQ >= 0) a.g[rQ] = Q + a.Qd[b];
+  const int4 dp = *reinterpret_cast<const int4 *>(a.diag_pos + 4 * b);
+  a.F_val[dp.x] += -Q - Bbb * vb * vb;
+  if (rQ >= 0) {
+    a.F_val[dp.y] += P / vb + Gbb * vb;
+    a.F_val[dp.z] += P - Gbb * vb * vb;
+    a.F_val[dp.w] += Q / vb - Bbb * vb;
+  } else {
+    a.gp_val[a.gp_self_pos[b]] += P / vb + Gbb * vb;
+    a.gp_val[a.gp_pg_pos[b]] = -1.0;
+  }
+}
+
 __global__ void k_assemble(AsmParams a) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= a.n_bus) return;
@@ -1774,6 +1846,8 @@ struct rh_ctx {
   // NEXT-4: Jacobians by column coloring + forward mode (rh_set_jacobian_mode)
   int *col_th, *col_v, *col_pg, *jd_pos, *jd_row, *jd_col, *gd_pos, *gd_row, *gd_col;
   double *JS = nullptr;   // [n_x][ncolors] compressed [J | G_p] S
+  int *bl_bus = nullptr;
+  double *asm_tP = nullptr, *asm_tQ = nullptr;
   int jac_mode = 0;       // 0 analytic assembly, 1 colored forward mode
   double *gp_val;
   int *gpc_ptr, *gpc_pos, *gpc_row;
@@ -1993,6 +2067,9 @@ int upload(rh_ctx *c) {
   UP(jd_pos, A.jd_pos); UP(jd_row, A.jd_row); UP(jd_col, A.jd_col);
   UP(gd_pos, A.gd_pos); UP(gd_row, A.gd_row); UP(gd_col, A.gd_col);
   chk(c->JS = dalloc<double>((size_t)A.n_x * std::max(1, A.ncolors), P));
+  UP(bl_bus, A.bl_bus);
+  chk(c->asm_tP = dalloc<double>((size_t)std::max(1, 2 * A.n_line), P));
+  chk(c->asm_tQ = dalloc<double>((size_t)std::max(1, 2 * A.n_line), P));
   UP(gpc_ptr, A.gpc_ptr); UP(gpc_pos, A.gpc_pos); UP(gpc_row, zr(A.gpc_row));
   UP(dth_src, zr(A.dth_src)); UP(dv_src, zr(A.dv_src)); UP(yth_dst, zr(A.yth_dst)); UP(yv_dst, zr(A.yv_dst));
   UP(pg_p, A.pg_p); UP(near_ref, A.near_ref);
@@ -2769,9 +2846,20 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   a.gp_val = c->gp_val;
   a.refg_th = c->refg_th;
   a.refg_v = c->refg_v;
+  a.bl_bus = c->bl_bus;
+  a.tP = c->asm_tP;
+  a.tQ = c->asm_tQ;
+  a.n_inc = 2 * m;
   dbg_mark(st, "bus state + line trig");
-  k_assemble<<<nblk(nb, 128), 128, 0, st>>>(a);
-  RH_LAUNCHED(c);
+  if (A.asm_unique && !getenv("RH_ASM_SERIAL")) {
+    k_asm_lines<<<nblk(2 * m), kThreads, 0, st>>>(a);
+    RH_LAUNCHED(c);
+    k_asm_buses<<<nblk(nb), kThreads, 0, st>>>(a);
+    RH_LAUNCHED(c);
+  } else {
+    k_assemble<<<nblk(nb, 128), 128, 0, st>>>(a);
+    RH_LAUNCHED(c);
+  }
   dbg_mark(st, "k_assemble");
   if (c->jac_mode == 1)
     if (int rc = colored_jacobian(c, st, true)) return rc;

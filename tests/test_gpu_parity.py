@@ -268,3 +268,24 @@ def test_newton_from_unsolved_point():
     with pytest.raises(rh.RHError) as e:   # one step cannot satisfy a zero tolerance with extra steps
         ctx.newton(_dev(x0), _dev(p), tol=0.0, extra=2, maxit=1)
     assert e.value.code == rh.RH_E_NOCONV
+
+
+def test_two_kernel_assembly_matches_serial(monkeypatch):
+    """The line + bus assembly kernels (grids without parallel lines) agree with the
+    bus-serial k_assemble to rounding: same per-bus summation order, but the serial
+    kernel contracts v_o (G c + B s) into its running sum with an FMA."""
+    g = pf.backout_loads(gridgen.make_grid("case1354pegase"))
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g)
+    x, p = ctx.state_vectors(g)
+    out = []
+    for serial in (False, True):
+        if serial:
+            monkeypatch.setenv("RH_ASM_SERIAL", "1")
+        gd, H = ctx.reduced_hessian(_dev(x), _dev(p), 256)
+        res, f = ctx.residual()
+        out.append((_np(gd), _np(H), _np(res)))
+    (g0, H0, r0), (g1, H1, r1) = out
+    assert np.max(np.abs(g0 - g1)) <= 1e-12 * np.max(np.abs(g1))
+    assert np.max(np.abs(r0 - r1)) <= 1e-12 * np.max(np.abs(g.Pd)) + 1e-13
+    assert col_rel_err(H0, H1) <= 1e-10      # rounding amplified by the solves (R21)
