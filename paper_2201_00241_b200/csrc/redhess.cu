@@ -40,37 +40,8 @@ __device__ __forceinline__ double warp_max(double v) {
 // J and G_p assembly (Appendix A identities), grad P_ref
 // ============================================================================
 
-// x, p -> bus-level theta, v, Pg (R5 orderings)
-__global__ void k_bus_state(int n_x, int n_p, const int *x_bus, const int *x_kind, const int *p_bus,
-                            const int *p_kind, const double *x, const double *p, double *th, double *v,
-                            double *pgb, int ref, double theta_ref) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n_x) {
-    const int b = x_bus[k];
-    if (x_kind[k] == RH_KIND_THETA)
-      th[b] = x[k];
-    else
-      v[b] = x[k];
-  } else if (k < n_x + n_p) {
-    const int q = k - n_x;
-    const int b = p_bus[q];
-    if (p_kind[q] == RH_KIND_PG)
-      pgb[b] = p[q];
-    else
-      v[b] = p[q];
-  } else if (k == n_x + n_p) {
-    th[ref] = theta_ref;
-  }
-}
-
-// per line: c = cos(th_f - th_t), s = sin(th_f - th_t) (trig once per line)
-__global__ void k_line_trig(int m, const int *lf, const int *lt, const double *th, double2 *cs) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= m) return;
-  double s, c;
-  sincos(th[lf[l]] - th[lt[l]], &s, &c);
-  cs[l] = make_double2(c, s);
-}
+// (k_state_prep: x, p -> bus-level theta, v, Pg (R5 orderings); per
+// line c = cos(th_f - th_t), s = sin(th_f - th_t), trig once per line)
 
 struct AsmParams {
   int n_bus, ref;
@@ -280,20 +251,49 @@ __global__ void k_decompress(int nj, const int *__restrict__ jpos, const int *__
   }
 }
 
-__global__ void k_state_init(int nx, int np_, const double *__restrict__ x, const double *__restrict__ p, double *cx,
+// The state's independent prologue in ONE launch (grid-stride segments): x, p
+// into the context; zero the assembled values, the REF gradient and the pivot
+// flag; bus state (theta, v, Pg per bus) and line trig (cos, sin of
+// theta_f - theta_t), both read from the caller's x, p directly.
+__global__ void k_state_prep(int nx, int np_, const double *__restrict__ x, const double *__restrict__ p, double *cx,
                              double *cp, long long nF, double *F_val, long long nG, double *gp_val, int nb,
-                             double *refg_th, double *refg_v, int *status) {
+                             double *refg_th, double *refg_v, int *status, const int *__restrict__ x_bus,
+                             const int *__restrict__ x_kind, const int *__restrict__ p_bus,
+                             const int *__restrict__ p_kind, double *th, double *v, double *pgb, int ref,
+                             double theta_ref, int m, const int *__restrict__ lf, const int *__restrict__ lt,
+                             const int *__restrict__ th_x, double2 *cs) {
   const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x, step = (long long)gridDim.x * blockDim.x;
-  for (long long i = t0; i < nx; i += step) cx[i] = x[i];
-  for (long long i = t0; i < np_; i += step) cp[i] = p[i];
+  for (long long i = t0; i < nx; i += step) {
+    const double xv = x[i];
+    cx[i] = xv;
+    if (x_kind[i] == RH_KIND_THETA) th[x_bus[i]] = xv;
+    else v[x_bus[i]] = xv;
+  }
+  for (long long i = t0; i < np_; i += step) {
+    const double pv = p[i];
+    cp[i] = pv;
+    if (p_kind[i] == RH_KIND_PG) pgb[p_bus[i]] = pv;
+    else v[p_bus[i]] = pv;
+  }
+  for (long long l = t0; l < m; l += step) {
+    const int f = lf[l], t = lt[l];
+    const double tf = f == ref ? theta_ref : x[th_x[f]], tt = t == ref ? theta_ref : x[th_x[t]];
+    double s, c;
+    sincos(tf - tt, &s, &c);
+    cs[l] = make_double2(c, s);
+  }
   for (long long i = t0; i < nF; i += step) F_val[i] = 0.0;
   for (long long i = t0; i < nG; i += step) gp_val[i] = 0.0;
   for (long long i = t0; i < nb; i += step) {
     refg_th[i] = 0.0;
     refg_v[i] = 0.0;
   }
-  if (t0 == 0) *status = 0;
+  if (t0 == 0) {
+    *status = 0;
+    th[ref] = theta_ref;
+  }
 }
+
 __global__ void k_objective(int n_bus, int ref, const int *has_gen, const double *c2b, const double *c1b,
                             const double *c0b, const double *pgb, const double *P, const double *Pd,
                             double *scal) {
@@ -2801,16 +2801,11 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   const int nx = A.n_x, np_ = A.n_p, nb = A.n_bus, m = A.n_line;
   c->has_state = c->has_mult = false;
   dbg_mark(st, "state start");
-  // x, p into the context; zero the assembled values, the REF gradient, the pivot flag (one launch)
-  k_state_init<<<2 * c->nsm, kThreads, 0, st>>>(nx, np_, x, p, c->x, c->p, (long long)A.F_col.size(), c->F_val,
+  // x, p into the context, zeroed accumulators, bus state and line trig (one launch)
+  k_state_prep<<<2 * c->nsm, kThreads, 0, st>>>(nx, np_, x, p, c->x, c->p, (long long)A.F_col.size(), c->F_val,
                                                 (long long)A.gp_col.size(), c->gp_val, nb, c->refg_th, c->refg_v,
-                                                c->status);
-  RH_LAUNCHED(c);
-  dbg_mark(st, "copies + memsets");
-  k_bus_state<<<nblk(nx + np_ + 1), kThreads, 0, st>>>(nx, np_, c->x_bus, c->x_kind, c->p_bus, c->p_kind, c->x,
-                                                      c->p, c->th, c->v, c->pgb, A.ref, A.theta_ref);
-  RH_LAUNCHED(c);
-  k_line_trig<<<nblk(m), kThreads, 0, st>>>(m, c->lf, c->lt, c->th, c->cs);
+                                                c->status, c->x_bus, c->x_kind, c->p_bus, c->p_kind, c->th, c->v,
+                                                c->pgb, A.ref, A.theta_ref, m, c->lf, c->lt, c->th_x, c->cs);
   RH_LAUNCHED(c);
   AsmParams a{};
   a.n_bus = nb;
