@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     }
     const double piv = w[rd.x];
     if (lane == 0) {
-      const double di = 1.0 / piv;
+      const double di = fast_rcp(piv);
       sdinv[a] = di;
       f.dinv[rd.y] = di;
       if (!(fabs(piv) > f.pivtol * amax)) atomicMax(f.status, rd.y + 1);
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
       const int4 rk = s_trow[tk];
       const int ik = rk.x;
       const double piv = SF[rk.z];
-      const double dk = 1.0 / piv;
+      const double dk = fast_rcp(piv);
       if (tk % nw == warp && lane == 0) {
         sdinv[ak] = dk;
         f.dinv[ik] = dk;
