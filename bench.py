@@ -267,8 +267,15 @@ def main():
 
     rank, world, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # one rank per GPU; BENCH_DIST_BACKEND=gloo (ranks sharing a GPU) is a
+        # plumbing check of the sharded path on a 1-GPU box, not a measurement
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        dev_idx = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev_idx)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
