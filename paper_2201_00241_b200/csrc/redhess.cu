@@ -3016,7 +3016,12 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
 extern "C" {
 
 int rh_set_state(rh_ctx *c, const double *x, const double *p, void *stream) {
-  return state_impl(c, x, p, (cudaStream_t)stream, nullptr, nullptr);
+  // block-only derived values on a side stream, concurrent with the separator's elimination
+  if (c && !c->host_only && c->loaded && !c->sti[1]) {
+    RH_CUDA(c, cudaSetDevice(c->device));
+    RH_CUDA(c, cudaStreamCreateWithFlags(&c->sti[1], cudaStreamNonBlocking));
+  }
+  return state_impl(c, x, p, (cudaStream_t)stream, c ? c->sti[1] : nullptr, nullptr);
 }
 
 int rh_residual(rh_ctx *c, double *g, double *f, void *stream) {
@@ -3111,9 +3116,11 @@ int newton_impl(rh_ctx *c, double *x, const double *p, double tol, int extra, in
   if (int rc = ensure_tsep(c, kSegC)) return rc;
   int left = -1, it = 0;
   bool done = false;
+  // block-only derived values on a side stream, concurrent with the separator's elimination
+  if (!c->sti[1]) RH_CUDA(c, cudaStreamCreateWithFlags(&c->sti[1], cudaStreamNonBlocking));
   for (; it < maxit && !done; ++it) {
     // state, assembly and refactorization at x_k (g_k in c->g, factors of J_k)
-    if (int rc = state_impl(c, x, p, st, nullptr, nullptr)) return rc;
+    if (int rc = state_impl(c, x, p, st, c->sti[1], nullptr)) return rc;
     // J_k dx = g_k: block L sweep and separator (S^-1) on the loaded right-hand side, then U
     k_newton_rhs<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->pinv, c->g, c->X1col);
     RH_LAUNCHED(c);
@@ -3151,7 +3158,7 @@ int newton_impl(rh_ctx *c, double *x, const double *p, double tol, int extra, in
   if (!done) return fail(c, RH_E_NOCONV, "Newton did not converge within maxit steps");
   if (!final_state) return RH_OK;
   // leave the state (g, factors) at the final x
-  if (int rc = state_impl(c, x, p, st, nullptr, nullptr)) return rc;
+  if (int rc = state_impl(c, x, p, st, c->sti[1], nullptr)) return rc;
   if (resid) {
     RH_CUDA(c, cudaMemsetAsync(c->nwt + 1, 0, sizeof(double), st));
     k_absmax<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->g, c->nwt + 1);
