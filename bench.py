@@ -97,7 +97,8 @@ def run_reference(args):
     import gridgen
     case = args.case
     N = args.N or gridgen.CONFIG_N.get(case, 256)
-    grid = gridgen.make_grid(case)
+    from oracle import powerflow as pf
+    grid = pf.backout_loads(gridgen.make_grid(case))   # the same solved operating point as our arm
     cols = min(128, args.cpu_cols)
     vals = []
     for i in range(args.warmup + args.steps):
