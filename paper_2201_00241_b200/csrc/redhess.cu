@@ -2636,15 +2636,17 @@ int rh_load_grid(rh_ctx *c, const rh_grid *g, int32_t *n_x, int32_t *n_p) {
   }
   c->loaded = c->has_state = c->has_mult = false;
   // block size: the largest whose shared-memory stages fit
-  // Prefer the largest block size that fits AND leaves at least two blocks (a
-  // single block serializes the whole refactorization and every sweep in one
-  // CTA: case118 0.46 -> 0.31 ms); otherwise the first that fits.
+  // Prefer the largest block size that fits AND leaves at least kMinBlocks
+  // blocks (few blocks serialize the refactorization and the sweeps on few
+  // CTAs: case118 0.46 -> 0.32 ms, case1354 0.42-0.51 -> 0.41 ms; case2869 and
+  // case9241 keep 256); otherwise the fitting size with the most blocks.
+  constexpr int kMinBlocks = 16;
   std::string msg;
   bool fits = false;
-  std::vector<int> cands = {256, 128, 512, 64};
+  std::vector<int> cands = {256, 128, 64, 512};
   const bool forced = getenv("RH_RMAX") != nullptr;
   if (forced) cands.insert(cands.begin(), atoi(getenv("RH_RMAX")));  // tuning override
-  int fallback = -1;
+  int fallback = -1, fallback_blocks = 0;
   for (int rmax : cands) {
     msg = analyze(*g, c->A, rmax);
     if (!msg.empty()) return fail(c, RH_E_GRID, msg);
@@ -2654,8 +2656,11 @@ int rh_load_grid(rh_ctx *c, const rh_grid *g, int32_t *n_x, int32_t *n_p) {
            (size_t)8 * A.sep_rows * sizeof(double) <= lim &&
            fact_smem_bytes(A) <= lim && blk_smem_fits(A, kSmemSM) && A.max_seg_rows <= kMaxRowsFact &&
            A.ufwd.max_tunits <= UnitSweep::kMaxTopUnits && A.ubwd.max_tunits <= UnitSweep::kMaxTopUnits;
-    if (fits && fallback < 0) fallback = rmax;
-    if (fits && (forced || A.nblk >= 2)) break;
+    if (fits && A.nblk > fallback_blocks) {
+      fallback = rmax;
+      fallback_blocks = A.nblk;
+    }
+    if (fits && (forced || A.nblk >= kMinBlocks)) break;
     fits = false;
   }
   if (!fits && fallback >= 0) {
