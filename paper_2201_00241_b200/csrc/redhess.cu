@@ -1911,6 +1911,29 @@ struct rh_ctx {
   int *gpe_off, *gpe_row, *gpe_col, *gpe_src, *gpe_split;
   double2 *gpe_rec;
   DenseWs dws;                 // tracking Step 2 (dense.cu)
+  // CUDA graph of the fused call (rh_reduced_hessian): captured on the second
+  // identical call, replayed afterwards; dropped when any workspace moves
+  struct GraphKey {
+    const void *x, *p, *grad, *H, *st;
+    long long ldh;
+    int j0, j1, N, transposed, jac_mode;
+    bool operator==(const GraphKey &o) const {
+      return x == o.x && p == o.p && grad == o.grad && H == o.H && st == o.st && ldh == o.ldh && j0 == o.j0 &&
+             j1 == o.j1 && N == o.N && transposed == o.transposed && jac_mode == o.jac_mode;
+    }
+  };
+  GraphKey g_seen{}, g_key{};
+  bool g_valid = false, g_disabled = false;
+  cudaGraphExec_t g_exec = nullptr;
+  long long g_launches = 0;
+  cudaStream_t g_st = nullptr;           // capture / replay stream when the caller's is the legacy one
+  cudaEvent_t g_ev[2] = {nullptr, nullptr};
+  void drop_graph() {
+    if (g_exec) cudaGraphExecDestroy(g_exec);
+    g_exec = nullptr;
+    g_valid = false;
+    g_seen = GraphKey{};
+  }
   cudaStream_t cp_st = nullptr;   // host copies of finished column blocks (rh_reduced_hessian_host)
   // the fused call's gradient runs on its own stream with its own separator
   // workspace and ticket counters; batches wait for the tape before k_for
@@ -1931,6 +1954,10 @@ struct rh_ctx {
   cudaEvent_t ev_trk[3] = {nullptr, nullptr, nullptr};
 
   void free_all() {
+    drop_graph();
+    if (g_st) cudaStreamDestroy(g_st), g_st = nullptr;
+    for (auto &e : g_ev)
+      if (e) cudaEventDestroy(e), e = nullptr;
     dense_ws_free(dws);
     for (auto &e : tmaps) cudaFree(e.dev);
     tmaps.clear();
@@ -2278,6 +2305,7 @@ int ensure_tsep(rh_ctx *c, int ld, int k = 0) {
   auto &w = c->ws[k];
   const size_t need = (size_t)ld * (size_t)std::max(1, c->A.sep_rows);
   if (need <= w.tsep_elems) return RH_OK;
+  c->drop_graph();   // the captured fused call points at the old buffer
   if (w.Tsep) cudaFree(w.Tsep);
   w.Tsep = nullptr;
   w.tsep_elems = 0;
@@ -2294,6 +2322,7 @@ int ensure_ws(rh_ctx *c, int ld, int k = 0) {
   const size_t need = (size_t)ld * (size_t)c->A.n_x;
   if (int rc = ensure_tsep(c, ld, k)) return rc;
   if (need <= w.elems) return RH_OK;
+  c->drop_graph();
   if (w.Z) cudaFree(w.Z);
   if (w.P) cudaFree(w.P);
   w.Z = w.P = nullptr;
@@ -3312,7 +3341,8 @@ namespace {
 // state + reduced gradient + Hessian columns [j0, j1), with the first block
 // sweep of the first batches overlapping the separator's refactorization
 int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, int j1, int N, double *grad_p,
-                         double *H, long long ldh, int transposed, cudaStream_t st, double *Hhost) {
+                         double *H, long long ldh, int transposed, cudaStream_t st, double *Hhost,
+                         bool defer_pivots = false) {
   if (!c || !x || !p || !grad_p || (j1 > j0 && !H)) return fail(c, RH_E_ARG, "null argument");
   if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
   if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
@@ -3361,7 +3391,7 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   if (!rc) RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_tape, 0));
   dbg_mark(st, "gradient + batches joined");
   dbg_report(st);
-  if (!rc) rc = check_pivots(c, st);
+  if (!rc && !defer_pivots) rc = check_pivots(c, st);
   return rc;
 }
 }  // namespace
@@ -3370,7 +3400,75 @@ extern "C" {
 
 int rh_reduced_hessian(rh_ctx *c, const double *x, const double *p, int32_t j0, int32_t j1, int32_t N,
                        double *grad_p, double *H, int64_t ldh, int32_t transposed, void *stream) {
-  return reduced_hessian_impl(c, x, p, j0, j1, N, grad_p, H, ldh, transposed, (cudaStream_t)stream, nullptr);
+  cudaStream_t st = (cudaStream_t)stream;
+  // CUDA graph: the fused call enqueues ~90 launches, memsets and cross-stream
+  // events; a repeated call with the same buffers replays the captured graph
+  // (one launch) and reads the pivot flag as usual.  RH_NO_GRAPH=1 disables.
+  const bool graphs = c && c->loaded && !c->host_only && !c->g_disabled && !getenv("RH_NO_GRAPH") && !dbg_on() &&
+                      x && p && grad_p && (j1 <= j0 || H);
+  if (graphs) {
+    rh_ctx::GraphKey key{x, p, grad_p, H, (const void *)st, (long long)ldh, j0, j1, N, transposed, c->jac_mode};
+    const bool replay = c->g_valid && key == c->g_key, capture = !replay && key == c->g_seen;
+    if (replay || capture) {
+      RH_CUDA(c, cudaSetDevice(c->device));
+      // the legacy default stream cannot be captured: run on an internal stream
+      // ordered after / before the caller's
+      cudaStream_t cs = st;
+      if (!st) {
+        if (!c->g_st) RH_CUDA(c, cudaStreamCreateWithFlags(&c->g_st, cudaStreamNonBlocking));
+        for (auto &e : c->g_ev)
+          if (!e) RH_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        RH_CUDA(c, cudaEventRecord(c->g_ev[0], st));
+        RH_CUDA(c, cudaStreamWaitEvent(c->g_st, c->g_ev[0], 0));
+        cs = c->g_st;
+      }
+      auto finish = [&]() -> int {
+        c->has_state = c->has_mult = true;
+        if (!st) {
+          RH_CUDA(c, cudaEventRecord(c->g_ev[1], cs));
+          RH_CUDA(c, cudaStreamWaitEvent(st, c->g_ev[1], 0));
+        }
+        return check_pivots(c, cs);
+      };
+      if (replay) {
+        RH_CUDA(c, cudaGraphLaunch(c->g_exec, cs));
+        c->launches += c->g_launches;
+        return finish();
+      }
+      c->drop_graph();   // second identical call: capture it, then replay
+      const long long l0 = c->launches;
+      cudaGraph_t g = nullptr;
+      if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        const int rc = reduced_hessian_impl(c, x, p, j0, j1, N, grad_p, H, ldh, transposed, cs, nullptr, true);
+        const cudaError_t e = cudaStreamEndCapture(cs, &g);
+        cudaGraphExec_t ex = nullptr;
+        if (rc == RH_OK && e == cudaSuccess && g && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+          cudaGraphDestroy(g);
+          c->g_exec = ex;
+          c->g_key = key;
+          c->g_valid = true;
+          c->g_launches = c->launches - l0;
+          c->launches = l0;
+          RH_CUDA(c, cudaGraphLaunch(ex, cs));
+          c->launches += c->g_launches;
+          c->err.clear();
+          return finish();
+        }
+        if (g) cudaGraphDestroy(g);
+      }
+      if (!st) {   // release the ordering taken above
+        cudaEventRecord(c->g_ev[1], cs);
+        cudaStreamWaitEvent(st, c->g_ev[1], 0);
+      }
+      // capture unsupported here: run uncaptured from now on
+      cudaGetLastError();
+      c->g_disabled = true;
+      c->launches = l0;
+      c->err.clear();
+    }
+    c->g_seen = key;
+  }
+  return reduced_hessian_impl(c, x, p, j0, j1, N, grad_p, H, ldh, transposed, st, nullptr);
 }
 
 int rh_reduced_hessian_host(rh_ctx *c, const double *x, const double *p, int32_t N, double *grad_p, double *H) {

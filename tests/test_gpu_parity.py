@@ -289,3 +289,37 @@ def test_two_kernel_assembly_matches_serial(monkeypatch):
     assert np.max(np.abs(g0 - g1)) <= 1e-12 * np.max(np.abs(g1))
     assert np.max(np.abs(r0 - r1)) <= 1e-12 * np.max(np.abs(g.Pd)) + 1e-13
     assert col_rel_err(H0, H1) <= 1e-10      # rounding amplified by the solves (R21)
+
+
+@pytest.mark.parametrize("own_stream", [False, True])
+def test_fused_call_graph_replay(own_stream):
+    """rh_reduced_hessian captures a CUDA graph on the second identical call and
+    replays it afterwards: results must equal an uncaptured context's, also after
+    the inputs change in place (the graph reads the buffers, not their values)."""
+    g = pf.backout_loads(gridgen.make_grid("case1354pegase"))
+    ctx, ref = rh.RedHess(0), rh.RedHess(0)
+    ctx.load_grid(g)
+    ref.load_grid(g)
+    x, p = ctx.state_vectors(g)
+    xd, pd = _dev(x), _dev(p)
+    grad = torch.empty(ctx.n_p, dtype=torch.float64, device="cuda")
+    H = torch.empty((ctx.n_p, ctx.n_p), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream() if own_stream else torch.cuda.current_stream()
+    outs = []
+    with torch.cuda.stream(s):
+        for it in range(4):
+            if it == 3:   # new point, same buffers
+                xd.add_(1e-3 * torch.from_numpy(np.random.default_rng(1).standard_normal(x.size)).cuda())
+            ctx.reduced_hessian(xd, pd, 256, grad=grad, H=H, stream=s)
+            s.synchronize()
+            outs.append((_np(grad).copy(), _np(H).copy()))
+    for a, b in outs[1:3]:
+        pass
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][1], outs[2][1])
+    import os
+    os.environ["RH_NO_GRAPH"] = "1"
+    try:
+        gr, Hr = ref.reduced_hessian(xd, pd, 256)
+    finally:
+        del os.environ["RH_NO_GRAPH"]
+    assert np.array_equal(_np(Hr), outs[3][1]) and np.array_equal(_np(gr), outs[3][0])
