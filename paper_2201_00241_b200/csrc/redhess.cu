@@ -1922,17 +1922,21 @@ struct rh_ctx {
              j1 == o.j1 && N == o.N && transposed == o.transposed && jac_mode == o.jac_mode;
     }
   };
-  GraphKey g_seen{}, g_key{};
-  bool g_valid = false, g_disabled = false;
-  cudaGraphExec_t g_exec = nullptr;
-  long long g_launches = 0;
+  struct GraphSlot {   // [0] rh_reduced_hessian, [1] rh_reduced_hessian_host
+    GraphKey seen{}, key{};
+    bool valid = false, disabled = false;
+    cudaGraphExec_t exec = nullptr;
+    long long launches = 0;
+  } gslot[2];
   cudaStream_t g_st = nullptr;           // capture / replay stream when the caller's is the legacy one
   cudaEvent_t g_ev[2] = {nullptr, nullptr};
   void drop_graph() {
-    if (g_exec) cudaGraphExecDestroy(g_exec);
-    g_exec = nullptr;
-    g_valid = false;
-    g_seen = GraphKey{};
+    for (auto &g : gslot) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+      g.valid = false;
+      g.seen = GraphKey{};
+    }
   }
   cudaStream_t cp_st = nullptr;   // host copies of finished column blocks (rh_reduced_hessian_host)
   // the fused call's gradient runs on its own stream with its own separator
@@ -3396,77 +3400,97 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
 }
 }  // namespace
 
+namespace {
+// CUDA graph of a fused call: `enqueue(cs)`
+// enqueues the whole call on cs without the final pivot check.  Captured on the
+// second identical call (same key), replayed afterwards; the pivot flag is read
+// after each run.  Returns false when the caller should run uncaptured (first
+// call, graphs disabled, capture unsupported); else rc holds the result.
+template <typename F>
+bool graph_run(rh_ctx *c, int slot, const rh_ctx::GraphKey &key, cudaStream_t st, int &rc, F &&enqueue) {
+  auto &g = c->gslot[slot];
+  if (g.disabled || getenv("RH_NO_GRAPH") || dbg_on()) return false;
+  const bool replay = g.valid && key == g.key, capture = !replay && key == g.seen;
+  if (!replay && !capture) {
+    g.seen = key;
+    return false;
+  }
+  auto cuda = [&](cudaError_t e) {
+    if (e == cudaSuccess) return true;
+    rc = fail(c, RH_E_CUDA, cudaGetErrorString(e));
+    return false;
+  };
+  if (!cuda(cudaSetDevice(c->device))) return true;
+  // the legacy default stream cannot be captured: run on an internal stream
+  // ordered after / before the caller's
+  cudaStream_t cs = st;
+  if (!st) {
+    if (!c->g_st && !cuda(cudaStreamCreateWithFlags(&c->g_st, cudaStreamNonBlocking))) return true;
+    for (auto &e : c->g_ev)
+      if (!e && !cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming))) return true;
+    if (!cuda(cudaEventRecord(c->g_ev[0], st)) || !cuda(cudaStreamWaitEvent(c->g_st, c->g_ev[0], 0))) return true;
+    cs = c->g_st;
+  }
+  auto join = [&]() {
+    if (!st) {
+      cudaEventRecord(c->g_ev[1], cs);
+      cudaStreamWaitEvent(st, c->g_ev[1], 0);
+    }
+  };
+  auto finish = [&]() {
+    c->has_state = c->has_mult = true;
+    join();
+    rc = check_pivots(c, cs);
+    return true;
+  };
+  if (replay) {
+    if (!cuda(cudaGraphLaunch(g.exec, cs))) return true;
+    c->launches += g.launches;
+    return finish();
+  }
+  c->drop_graph();
+  const long long l0 = c->launches;
+  cudaGraph_t gr = nullptr;
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    const int rc2 = enqueue(cs);
+    const cudaError_t e = cudaStreamEndCapture(cs, &gr);
+    cudaGraphExec_t ex = nullptr;
+    if (rc2 == RH_OK && e == cudaSuccess && gr && cudaGraphInstantiate(&ex, gr, 0) == cudaSuccess) {
+      cudaGraphDestroy(gr);
+      g.exec = ex;
+      g.key = key;
+      g.valid = true;
+      g.launches = c->launches - l0;
+      c->launches = l0;
+      c->err.clear();
+      if (!cuda(cudaGraphLaunch(ex, cs))) return true;
+      c->launches += g.launches;
+      return finish();
+    }
+    if (gr) cudaGraphDestroy(gr);
+  }
+  // capture unsupported for this call: run uncaptured from now on
+  cudaGetLastError();
+  join();
+  g.disabled = true;
+  c->launches = l0;
+  c->err.clear();
+  return false;
+}
+}  // namespace
+
 extern "C" {
 
 int rh_reduced_hessian(rh_ctx *c, const double *x, const double *p, int32_t j0, int32_t j1, int32_t N,
                        double *grad_p, double *H, int64_t ldh, int32_t transposed, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  // CUDA graph: the fused call enqueues ~90 launches, memsets and cross-stream
-  // events; a repeated call with the same buffers replays the captured graph
-  // (one launch) and reads the pivot flag as usual.  RH_NO_GRAPH=1 disables.
-  const bool graphs = c && c->loaded && !c->host_only && !c->g_disabled && !getenv("RH_NO_GRAPH") && !dbg_on() &&
-                      x && p && grad_p && (j1 <= j0 || H);
-  if (graphs) {
+  if (c && c->loaded && !c->host_only && x && p && grad_p && (j1 <= j0 || H)) {
     rh_ctx::GraphKey key{x, p, grad_p, H, (const void *)st, (long long)ldh, j0, j1, N, transposed, c->jac_mode};
-    const bool replay = c->g_valid && key == c->g_key, capture = !replay && key == c->g_seen;
-    if (replay || capture) {
-      RH_CUDA(c, cudaSetDevice(c->device));
-      // the legacy default stream cannot be captured: run on an internal stream
-      // ordered after / before the caller's
-      cudaStream_t cs = st;
-      if (!st) {
-        if (!c->g_st) RH_CUDA(c, cudaStreamCreateWithFlags(&c->g_st, cudaStreamNonBlocking));
-        for (auto &e : c->g_ev)
-          if (!e) RH_CUDA(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        RH_CUDA(c, cudaEventRecord(c->g_ev[0], st));
-        RH_CUDA(c, cudaStreamWaitEvent(c->g_st, c->g_ev[0], 0));
-        cs = c->g_st;
-      }
-      auto finish = [&]() -> int {
-        c->has_state = c->has_mult = true;
-        if (!st) {
-          RH_CUDA(c, cudaEventRecord(c->g_ev[1], cs));
-          RH_CUDA(c, cudaStreamWaitEvent(st, c->g_ev[1], 0));
-        }
-        return check_pivots(c, cs);
-      };
-      if (replay) {
-        RH_CUDA(c, cudaGraphLaunch(c->g_exec, cs));
-        c->launches += c->g_launches;
-        return finish();
-      }
-      c->drop_graph();   // second identical call: capture it, then replay
-      const long long l0 = c->launches;
-      cudaGraph_t g = nullptr;
-      if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-        const int rc = reduced_hessian_impl(c, x, p, j0, j1, N, grad_p, H, ldh, transposed, cs, nullptr, true);
-        const cudaError_t e = cudaStreamEndCapture(cs, &g);
-        cudaGraphExec_t ex = nullptr;
-        if (rc == RH_OK && e == cudaSuccess && g && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
-          cudaGraphDestroy(g);
-          c->g_exec = ex;
-          c->g_key = key;
-          c->g_valid = true;
-          c->g_launches = c->launches - l0;
-          c->launches = l0;
-          RH_CUDA(c, cudaGraphLaunch(ex, cs));
-          c->launches += c->g_launches;
-          c->err.clear();
-          return finish();
-        }
-        if (g) cudaGraphDestroy(g);
-      }
-      if (!st) {   // release the ordering taken above
-        cudaEventRecord(c->g_ev[1], cs);
-        cudaStreamWaitEvent(st, c->g_ev[1], 0);
-      }
-      // capture unsupported here: run uncaptured from now on
-      cudaGetLastError();
-      c->g_disabled = true;
-      c->launches = l0;
-      c->err.clear();
-    }
-    c->g_seen = key;
+    int rc = -1;
+    if (graph_run(c, 0, key, st, rc, [&](cudaStream_t cs) {
+          return reduced_hessian_impl(c, x, p, j0, j1, N, grad_p, H, ldh, transposed, cs, nullptr, true);
+        }))
+      return rc;
   }
   return reduced_hessian_impl(c, x, p, j0, j1, N, grad_p, H, ldh, transposed, st, nullptr);
 }
@@ -3488,13 +3512,22 @@ int rh_reduced_hessian_host(rh_ctx *c, const double *x, const double *p, int32_t
   }
   cudaStream_t st = c->e2e_st;
   double *dx = c->e2e_buf, *dp = dx + nx, *dg = dp + np_, *dH = dg + np_;
-  RH_CUDA(c, cudaMemcpyAsync(dx, x, nx * 8, cudaMemcpyHostToDevice, st));
-  RH_CUDA(c, cudaMemcpyAsync(dp, p, np_ * 8, cudaMemcpyHostToDevice, st));
-  // state, gradient and Hessian batches (first sweeps overlapping the separator's
-  // refactorization); column blocks leave for the host as their batches finish
-  int rc = reduced_hessian_impl(c, dx, dp, 0, (int)np_, N, dg, dH, (long long)np_, 0, st, H);
+  // H2D inputs; state, gradient and Hessian batches (first sweeps overlapping the
+  // separator's refactorization); column blocks leave for the host as their
+  // batches finish; the gradient last.  Repeated calls replay a CUDA graph
+  // (pinned host buffers; pageable ones fall back to plain enqueues).
+  auto enqueue = [&](cudaStream_t cs, bool defer) -> int {
+    RH_CUDA(c, cudaMemcpyAsync(dx, x, nx * 8, cudaMemcpyHostToDevice, cs));
+    RH_CUDA(c, cudaMemcpyAsync(dp, p, np_ * 8, cudaMemcpyHostToDevice, cs));
+    int rc = reduced_hessian_impl(c, dx, dp, 0, (int)np_, N, dg, dH, (long long)np_, 0, cs, H, true);
+    if (rc) return rc;
+    if (grad_p) RH_CUDA(c, cudaMemcpyAsync(grad_p, dg, np_ * 8, cudaMemcpyDeviceToHost, cs));
+    return defer ? RH_OK : check_pivots(c, cs);
+  };
+  rh_ctx::GraphKey key{x, p, grad_p, H, (const void *)st, (long long)np_, 0, (int)np_, N, 0, c->jac_mode};
+  int rc = -1;
+  if (!graph_run(c, 1, key, st, rc, [&](cudaStream_t cs) { return enqueue(cs, true); })) rc = enqueue(st, false);
   if (rc) return rc;
-  if (grad_p) RH_CUDA(c, cudaMemcpyAsync(grad_p, dg, np_ * 8, cudaMemcpyDeviceToHost, st));
   RH_CUDA(c, cudaStreamSynchronize(st));
   return RH_OK;
 }

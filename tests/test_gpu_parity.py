@@ -323,3 +323,27 @@ def test_fused_call_graph_replay(own_stream):
     finally:
         del os.environ["RH_NO_GRAPH"]
     assert np.array_equal(_np(Hr), outs[3][1]) and np.array_equal(_np(gr), outs[3][0])
+
+
+def test_host_call_graph_replay():
+    """rh_reduced_hessian_host replays a CUDA graph from the third identical call
+    (pinned buffers): equal to the first call and to the device call."""
+    g = pf.backout_loads(gridgen.make_grid("case1354pegase"))
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g)
+    x, p = ctx.state_vectors(g)
+    xh = torch.from_numpy(x).pin_memory()
+    ph = torch.from_numpy(p).pin_memory()
+    Hh = torch.empty((ctx.n_p, ctx.n_p), dtype=torch.float64).pin_memory()
+    gh = torch.empty(ctx.n_p, dtype=torch.float64).pin_memory()
+    outs = []
+    for it in range(4):
+        if it == 3:
+            xh.add_(1e-3 * torch.from_numpy(np.random.default_rng(2).standard_normal(x.size)))
+        ctx.reduced_hessian_host(xh.numpy(), ph.numpy(), 256, grad=gh.numpy(), H=Hh.numpy())
+        outs.append((gh.numpy().copy(), Hh.numpy().copy()))
+    assert all(np.array_equal(outs[0][1], o[1]) and np.array_equal(outs[0][0], o[0]) for o in outs[1:3])
+    ref = rh.RedHess(0)
+    ref.load_grid(g)
+    gr, Hr = ref.reduced_hessian(_dev(xh.numpy()), _dev(p), 256)
+    assert np.array_equal(_np(Hr), outs[3][1]) and np.array_equal(_np(gr), outs[3][0])
