@@ -1922,12 +1922,12 @@ struct rh_ctx {
              j1 == o.j1 && N == o.N && transposed == o.transposed && jac_mode == o.jac_mode;
     }
   };
-  struct GraphSlot {   // [0] rh_reduced_hessian, [1] rh_reduced_hessian_host
+  struct GraphSlot {   // [0] rh_reduced_hessian, [1] rh_reduced_hessian_host, [2] a Newton step
     GraphKey seen{}, key{};
     bool valid = false, disabled = false;
     cudaGraphExec_t exec = nullptr;
     long long launches = 0;
-  } gslot[2];
+  } gslot[3];
   cudaStream_t g_st = nullptr;           // capture / replay stream when the caller's is the legacy one
   cudaEvent_t g_ev[2] = {nullptr, nullptr};
   void drop_graph() {
@@ -2840,6 +2840,87 @@ int check_pivots(rh_ctx *c, cudaStream_t st) {   // reads the refactorization's 
   return RH_OK;
 }
 
+// CUDA graph of a fused call (DESIGN.md "Whole-step scheduling"): `enqueue(cs)`
+// enqueues the whole call on cs without the final pivot check.  Captured on the
+// second identical call (same key), replayed afterwards; the pivot flag is read
+// after each run.  Returns false when the caller should run uncaptured (first
+// call, graphs disabled, capture unsupported); else rc holds the result.
+template <typename F>
+bool graph_run(rh_ctx *c, int slot, const rh_ctx::GraphKey &key, cudaStream_t st, int &rc, F &&enqueue,
+               bool mult = true) {
+  auto &g = c->gslot[slot];
+  if (g.disabled || getenv("RH_NO_GRAPH") || dbg_on()) return false;
+  const bool replay = g.valid && key == g.key, capture = !replay && key == g.seen;
+  if (!replay && !capture) {
+    g.seen = key;
+    return false;
+  }
+  auto cuda = [&](cudaError_t e) {
+    if (e == cudaSuccess) return true;
+    rc = fail(c, RH_E_CUDA, cudaGetErrorString(e));
+    return false;
+  };
+  if (!cuda(cudaSetDevice(c->device))) return true;
+  // the legacy default stream cannot be captured: run on an internal stream
+  // ordered after / before the caller's
+  cudaStream_t cs = st;
+  if (!st) {
+    if (!c->g_st && !cuda(cudaStreamCreateWithFlags(&c->g_st, cudaStreamNonBlocking))) return true;
+    for (auto &e : c->g_ev)
+      if (!e && !cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming))) return true;
+    if (!cuda(cudaEventRecord(c->g_ev[0], st)) || !cuda(cudaStreamWaitEvent(c->g_st, c->g_ev[0], 0))) return true;
+    cs = c->g_st;
+  }
+  auto join = [&]() {
+    if (!st) {
+      cudaEventRecord(c->g_ev[1], cs);
+      cudaStreamWaitEvent(st, c->g_ev[1], 0);
+    }
+  };
+  auto finish = [&]() {
+    c->has_state = true;
+    if (mult) c->has_mult = true;
+    join();
+    rc = check_pivots(c, cs);
+    return true;
+  };
+  if (replay) {
+    if (!cuda(cudaGraphLaunch(g.exec, cs))) return true;
+    c->launches += g.launches;
+    return finish();
+  }
+  if (g.exec) cudaGraphExecDestroy(g.exec);   // this slot only: the others stay valid
+  g.exec = nullptr;
+  g.valid = false;
+  const long long l0 = c->launches;
+  cudaGraph_t gr = nullptr;
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+    const int rc2 = enqueue(cs);
+    const cudaError_t e = cudaStreamEndCapture(cs, &gr);
+    cudaGraphExec_t ex = nullptr;
+    if (rc2 == RH_OK && e == cudaSuccess && gr && cudaGraphInstantiate(&ex, gr, 0) == cudaSuccess) {
+      cudaGraphDestroy(gr);
+      g.exec = ex;
+      g.key = key;
+      g.valid = true;
+      g.launches = c->launches - l0;
+      c->launches = l0;
+      c->err.clear();
+      if (!cuda(cudaGraphLaunch(ex, cs))) return true;
+      c->launches += g.launches;
+      return finish();
+    }
+    if (gr) cudaGraphDestroy(gr);
+  }
+  // capture unsupported for this call: run uncaptured from now on
+  cudaGetLastError();
+  join();
+  g.disabled = true;
+  c->launches = l0;
+  c->err.clear();
+  return false;
+}
+
 // defer_check: do not read the pivot flag (the caller does, after enqueuing more work)
 int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cudaStream_t side,
                const std::function<int(cudaStream_t)> &early, bool defer_check = false) {
@@ -3168,31 +3249,42 @@ int newton_impl(rh_ctx *c, double *x, const double *p, double tol, int extra, in
   bool done = false;
   // block-only derived values on a side stream, concurrent with the separator's elimination
   if (!c->sti[1]) RH_CUDA(c, cudaStreamCreateWithFlags(&c->sti[1], cudaStreamNonBlocking));
-  for (; it < maxit && !done; ++it) {
-    // state, assembly and refactorization at x_k (g_k in c->g, factors of J_k)
-    if (int rc = state_impl(c, x, p, st, c->sti[1], nullptr)) return rc;
-    // J_k dx = g_k: block L sweep and separator (S^-1) on the loaded right-hand side, then U
-    k_newton_rhs<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->pinv, c->g, c->X1col);
+  // one Newton step, enqueued without host syncs: state, assembly and
+  // refactorization at x_k (g_k in c->g, factors of J_k); J_k dx = g_k by the
+  // block L sweep, the separator (S^-1), the U sweep; x_{k+1} = x_k - dx
+  // and max|dx|.  Replayed as a CUDA graph from the third step.
+  auto step = [&](cudaStream_t cs) -> int {
+    if (int rc = state_impl(c, x, p, cs, c->sti[1], nullptr, true)) return rc;
+    k_newton_rhs<<<nblk(A.n_x), kThreads, 0, cs>>>(A.n_x, c->pinv, c->g, c->X1col);
     RH_LAUNCHED(c);
     SegParams h = make_params(c);
     h.N = 1;
     h.ld = kSegC;
     h.Z = c->X1col;
     const int g1 = std::min(2 * c->nsm, A.nblk);
-    k_blk<<<g1, kBlkThreads, c->smem_blk, st>>>(h, MODE_LX);
+    k_blk<<<g1, kBlkThreads, c->smem_blk, cs>>>(h, MODE_LX);
     RH_LAUNCHED(c);
     if (A.sep_rows > 0) {
-      k_sep_gather<<<dim3(nblk(A.sep_rows, kThreads / 32), 1), kThreads, 0, st>>>(h, MODE_LUX);
+      k_sep_gather<<<dim3(nblk(A.sep_rows, kThreads / 32), 1), kThreads, 0, cs>>>(h, MODE_LUX);
       RH_LAUNCHED(c);
-      k_sep_gemv<<<nblk(A.sep_rows, kThreads / 32), kThreads, 0, st>>>(h, MODE_LU);
+      k_sep_gemv<<<nblk(A.sep_rows, kThreads / 32), kThreads, 0, cs>>>(h, MODE_LU);
       RH_LAUNCHED(c);
     }
-    k_blk<<<g1, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
+    k_blk<<<g1, kBlkThreads, c->smem_blk, cs>>>(h, MODE_U);
     RH_LAUNCHED(c);
-    // x_{k+1} = x_k - dx, max|dx|
-    RH_CUDA(c, cudaMemsetAsync(c->nwt, 0, sizeof(double), st));
-    k_newton_update<<<nblk(A.n_x), kThreads, 0, st>>>(A.n_x, c->pinv, c->X1col, x, c->nwt);
+    RH_CUDA(c, cudaMemsetAsync(c->nwt, 0, sizeof(double), cs));
+    k_newton_update<<<nblk(A.n_x), kThreads, 0, cs>>>(A.n_x, c->pinv, c->X1col, x, c->nwt);
     RH_LAUNCHED(c);
+    return RH_OK;
+  };
+  const rh_ctx::GraphKey key{x, p, nullptr, nullptr, (const void *)st, 0, -2, 0, 0, 0, c->jac_mode};
+  for (; it < maxit && !done; ++it) {
+    int rc = -1;
+    if (!graph_run(c, 2, key, st, rc, step, false)) {
+      rc = step(st);
+      if (!rc) rc = check_pivots(c, st);
+    }
+    if (rc) return rc;
     double dmax = 0.0;
     RH_CUDA(c, cudaMemcpyAsync(&dmax, c->nwt, sizeof(double), cudaMemcpyDeviceToHost, st));
     RH_CUDA(c, cudaStreamSynchronize(st));
@@ -3397,85 +3489,6 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   dbg_report(st);
   if (!rc && !defer_pivots) rc = check_pivots(c, st);
   return rc;
-}
-}  // namespace
-
-namespace {
-// CUDA graph of a fused call (DESIGN.md "Whole-step scheduling"): `enqueue(cs)`
-// enqueues the whole call on cs without the final pivot check.  Captured on the
-// second identical call (same key), replayed afterwards; the pivot flag is read
-// after each run.  Returns false when the caller should run uncaptured (first
-// call, graphs disabled, capture unsupported); else rc holds the result.
-template <typename F>
-bool graph_run(rh_ctx *c, int slot, const rh_ctx::GraphKey &key, cudaStream_t st, int &rc, F &&enqueue) {
-  auto &g = c->gslot[slot];
-  if (g.disabled || getenv("RH_NO_GRAPH") || dbg_on()) return false;
-  const bool replay = g.valid && key == g.key, capture = !replay && key == g.seen;
-  if (!replay && !capture) {
-    g.seen = key;
-    return false;
-  }
-  auto cuda = [&](cudaError_t e) {
-    if (e == cudaSuccess) return true;
-    rc = fail(c, RH_E_CUDA, cudaGetErrorString(e));
-    return false;
-  };
-  if (!cuda(cudaSetDevice(c->device))) return true;
-  // the legacy default stream cannot be captured: run on an internal stream
-  // ordered after / before the caller's
-  cudaStream_t cs = st;
-  if (!st) {
-    if (!c->g_st && !cuda(cudaStreamCreateWithFlags(&c->g_st, cudaStreamNonBlocking))) return true;
-    for (auto &e : c->g_ev)
-      if (!e && !cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming))) return true;
-    if (!cuda(cudaEventRecord(c->g_ev[0], st)) || !cuda(cudaStreamWaitEvent(c->g_st, c->g_ev[0], 0))) return true;
-    cs = c->g_st;
-  }
-  auto join = [&]() {
-    if (!st) {
-      cudaEventRecord(c->g_ev[1], cs);
-      cudaStreamWaitEvent(st, c->g_ev[1], 0);
-    }
-  };
-  auto finish = [&]() {
-    c->has_state = c->has_mult = true;
-    join();
-    rc = check_pivots(c, cs);
-    return true;
-  };
-  if (replay) {
-    if (!cuda(cudaGraphLaunch(g.exec, cs))) return true;
-    c->launches += g.launches;
-    return finish();
-  }
-  c->drop_graph();
-  const long long l0 = c->launches;
-  cudaGraph_t gr = nullptr;
-  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-    const int rc2 = enqueue(cs);
-    const cudaError_t e = cudaStreamEndCapture(cs, &gr);
-    cudaGraphExec_t ex = nullptr;
-    if (rc2 == RH_OK && e == cudaSuccess && gr && cudaGraphInstantiate(&ex, gr, 0) == cudaSuccess) {
-      cudaGraphDestroy(gr);
-      g.exec = ex;
-      g.key = key;
-      g.valid = true;
-      g.launches = c->launches - l0;
-      c->launches = l0;
-      c->err.clear();
-      if (!cuda(cudaGraphLaunch(ex, cs))) return true;
-      c->launches += g.launches;
-      return finish();
-    }
-    if (gr) cudaGraphDestroy(gr);
-  }
-  // capture unsupported for this call: run uncaptured from now on
-  cudaGetLastError();
-  join();
-  g.disabled = true;
-  c->launches = l0;
-  c->err.clear();
-  return false;
 }
 }  // namespace
 
