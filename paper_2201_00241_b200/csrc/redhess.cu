@@ -724,20 +724,34 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
           }
         }
         __syncthreads();
-        for (int t = tid; t < GJB * GJB; t += blockDim.x) {   // R2 = D_K^-1 S[K,K1]
-          const int i = t / GJB, c = t % GJB;
-          double acc = 0.0;
+        {   // R2 = D_K^-1 S[K,K1]: thread = column c, rows i0 + 8u (four chains in flight)
+          const int c = tid % GJB, i0 = tid / GJB;
+          double acc[GJB * GJB / 256];
+#pragma unroll
+          for (int u = 0; u < GJB * GJB / 256; ++u) acc[u] = 0.0;
 #pragma unroll 8
-          for (int l = 0; l < GJB; ++l) acc = fma(Ds[i][l], Rs[l][c], acc);
-          R2[i][c] = acc;
+          for (int l = 0; l < GJB; ++l) {
+            const double r = Rs[l][c];
+#pragma unroll
+            for (int u = 0; u < GJB * GJB / 256; ++u) acc[u] = fma(Ds[i0 + 8 * u][l], r, acc[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < GJB * GJB / 256; ++u) R2[i0 + 8 * u][c] = acc[u];
         }
         __syncthreads();
-        for (int t = tid; t < GJB * GJB; t += blockDim.x) {   // Ts = S[K1,K1] - S[K1,K] R2
-          const int i = t / GJB, c = t % GJB;
-          double acc = Ts[i][c];
+        {   // Ts = S[K1,K1] - S[K1,K] R2
+          const int c = tid % GJB, i0 = tid / GJB;
+          double acc[GJB * GJB / 256];
+#pragma unroll
+          for (int u = 0; u < GJB * GJB / 256; ++u) acc[u] = Ts[i0 + 8 * u][c];
 #pragma unroll 8
-          for (int l = 0; l < GJB; ++l) acc = fma(-Cs[i][l], R2[l][c], acc);
-          Ts[i][c] = acc;
+          for (int l = 0; l < GJB; ++l) {
+            const double r = R2[l][c];
+#pragma unroll
+            for (int u = 0; u < GJB * GJB / 256; ++u) acc[u] = fma(-Cs[i0 + 8 * u][l], r, acc[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < GJB * GJB / 256; ++u) Ts[i0 + 8 * u][c] = acc[u];
         }
         __syncthreads();
         invert32(&Ts[0][0], GJT + 1, K1, b1, true, W8{});
