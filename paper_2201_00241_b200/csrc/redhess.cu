@@ -771,11 +771,18 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
         } else if (blockIdx.x < ntiles) {
           load_tile(Sin, K, b, (blockIdx.x / nt) * GJT, (blockIdx.x % nt) * GJT, tid - 128, 128);
         }
-      } else {        // the helper's D_K^-1, then the first tile
+      } else {        // the helper's D_K^-1 (loads in flight while the first tile's are issued)
         const double *db = dbuf + ((K / GJB) & 1) * GJB * GJB;
-        for (int t = tid; t < GJB * GJB; t += blockDim.x) Ds[t / GJB][t % GJB] = __ldcg(db + t);
+        double dv[GJB * GJB / 256];
+#pragma unroll
+        for (int u = 0; u < GJB * GJB / 256; ++u) dv[u] = __ldcg(db + tid + 256 * u);
         if (blockIdx.x < ntiles)
           load_tile(Sin, K, b, (blockIdx.x / nt) * GJT, (blockIdx.x % nt) * GJT, tid, blockDim.x);
+#pragma unroll
+        for (int u = 0; u < GJB * GJB / 256; ++u) {
+          const int t = tid + 256 * u;
+          Ds[t / GJB][t % GJB] = dv[u];
+        }
       }
     }
     for (int tile = helper ? ntiles : (int)blockIdx.x; tile < ntiles; tile += ntcta) {
