@@ -972,10 +972,11 @@ __device__ __forceinline__ double rhs_gpw(const SegParams &h, int row, int col) 
 
 // ----------------------------------------------------------------------------
 // Block sweeps by bus units.
-// Persistent: one CTA per SM walks a contiguous range of (block, 32-column
-// chunk) tiles, balanced by the host's per-block cost.  The next tile's rows
-// stream into the second X buffer (cp.async) while the current tile is swept,
-// so the HBM traffic overlaps the shared-memory-bound sweep.  Lanes own
+// Persistent: two CTAs per SM take tickets from a global counter, heaviest
+// blocks first; a ticket is one block x two 32-column chunks, the block's unit
+// schedule staged once (TMA bulk copies) and the chunks' block rows moved by 2D
+// TMA boxes.  While one CTA waits on its copies the other's sweep uses the SM
+// (DESIGN.md "Block sweeps").  Lanes own
 // columns; a warp walks its pieces' units without synchronization; a unit is
 // the 1 or 2 rows of one bus, so every dependency value read from shared
 // memory feeds both rows (half the shared-memory wavefronts per FMA of a
