@@ -189,3 +189,20 @@ def test_tracking_step_full_size_case9241():
     assert eH <= 1e-9
     assert ed <= 1e-8
     assert info["tau"] == info_o["tau"] == 0.0
+
+
+def test_tracking_step_voltage_block_and_single_control():
+    # free range not starting at 0 (the voltage set points [n_pv, n_p)) and a single
+    # free control: the [j0, j1) block of the transposed columns, p untouched outside
+    g, L, c, x, p = _tracking_case("case118", dict(tap_line=True))
+    n_pv = int(np.sum(L.p_kind == 2))
+    Pd, Qd = gridgen.load_scenario(g, 60, amp=0.05, kind="sin", seed=5)
+    for j0, j1 in ((n_pv, L.n_p), (3, 4)):
+        p_o, x_o, info_o = trk.tracking_step(g, p, x, Pd[2], Qd[2], j0, j1, N=64, L=L)
+        xd, pd = _dev(x), _dev(p)
+        grad, H, d, info = c.tracking_step(xd, pd, 64, Pd=_dev(Pd[2]), Qd=_dev(Qd[2]), j0=j0, j1=j1)
+        assert (info["tau"], info["attempts"]) == (info_o["tau"], info_o["attempts"])
+        assert _rel(_np(d), info_o["d"]) <= 1e-8
+        pn = _np(pd)
+        assert np.all(pn[:j0] == p[:j0]) and np.all(pn[j1:] == p[j1:])
+        assert float(np.max(np.abs(pn - p_o))) <= 1e-8 * max(1.0, float(np.max(np.abs(info_o["d"]))))
