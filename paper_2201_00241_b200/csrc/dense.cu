@@ -181,6 +181,7 @@ __device__ __forceinline__ void diag_factor(const CholArgs &a, int kt, double (*
 #pragma unroll
     for (int m = c + 1; m < 32; ++m)
       if (m <= lane) q[m] = fma(-l, col[m], q[m]);
+    __syncwarp();   // every lane has read col before the next step overwrites it
   }
 #pragma unroll
   for (int m = 0; m < 32; ++m) s[lane][m] = (m <= lane) ? q[m] : 0.0;
