@@ -2335,7 +2335,7 @@ int ensure_tsep(rh_ctx *c, int ld, int k = 0) {
   if (w.Tsep) cudaFree(w.Tsep);
   w.Tsep = nullptr;
   w.tsep_elems = 0;
-  if (cudaMalloc(&w.Tsep, need * sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&w.Tsep, need * sizeof(double)) != cudaSuccess || cudaMemset(w.Tsep, 0, need * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return fail(c, RH_E_NOMEM, "workspace allocation failed");
   }
@@ -2353,7 +2353,8 @@ int ensure_ws(rh_ctx *c, int ld, int k = 0) {
   if (w.P) cudaFree(w.P);
   w.Z = w.P = nullptr;
   w.elems = 0;
-  if (cudaMalloc(&w.Z, need * sizeof(double)) != cudaSuccess || cudaMalloc(&w.P, need * sizeof(double)) != cudaSuccess) {
+  if (cudaMalloc(&w.Z, need * sizeof(double)) != cudaSuccess || cudaMalloc(&w.P, need * sizeof(double)) != cudaSuccess ||
+      cudaMemset(w.Z, 0, need * sizeof(double)) != cudaSuccess || cudaMemset(w.P, 0, need * sizeof(double)) != cudaSuccess) {
     cudaGetLastError();
     return fail(c, RH_E_NOMEM, "workspace allocation failed");
   }
