@@ -202,13 +202,11 @@ __device__ __forceinline__ void diag_factor(const CholArgs &a, int kt, double (*
 
 __global__ void __launch_bounds__(kCholWarps * 32, 1) k_chol(CholArgs a) {
   extern __shared__ double csm[];
-  __shared__ unsigned s_gen;
+
   __shared__ double s_dv[32], s_col[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, gid = lane >> 2, tig = lane & 3;
   double(*s)[kSLd] = reinterpret_cast<double(*)[kSLd]>(csm + warp * 32 * kSLd);
-  if (threadIdx.x == 0) s_gen = (unsigned)ld_acquire(reinterpret_cast<const int *>(&a.bar[1]));
-  __syncthreads();
-  unsigned gen = s_gen;
+  unsigned gen = 0;   // barrier phase (a.bar[0] zeroed by the host before the launch)
   const int nt = a.nt;
   const long long W = (long long)gridDim.x * kCholWarps, gw = (long long)blockIdx.x * kCholWarps + warp;
   const long long nfill = (long long)nt * (nt + 1) / 2;
@@ -217,7 +215,7 @@ __global__ void __launch_bounds__(kCholWarps * 32, 1) k_chol(CholArgs a) {
     tri_decode(u, i, j);
     fill_tile(a, i, j, s, lane);
   }
-  grid_barrier(a.bar, gen);
+  grid_barrier_count(a.bar, gen);
   for (int k = -1; k <= nt - 2; ++k) {
     const int c1 = k + 1, m = nt - c1;
     if (a.dbg && blockIdx.x == 0 && threadIdx.x == 0 && k + 1 < 256) a.dbg[(k + 1) * 4 + 0] = gtimer();
@@ -301,7 +299,7 @@ __global__ void __launch_bounds__(kCholWarps * 32, 1) k_chol(CholArgs a) {
       }
       __syncwarp();
     }
-    grid_barrier(a.bar, gen);
+    grid_barrier_count(a.bar, gen);
   }
 }
 
@@ -415,6 +413,7 @@ cudaError_t dense_spd_attempt(DenseWs &w, int n, const double *H, long long ldh,
   if (nt > w.cap) return cudaErrorInvalidValue;
   if (++w.epoch <= 0) w.epoch = 1;   // flags compare against the epoch: never reset
   cudaError_t e = cudaMemsetAsync(w.fail, 0, 2 * sizeof(int), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
   CholArgs a;
   a.H = H;

@@ -46,6 +46,25 @@ __device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
   __syncthreads();
 }
 
+// Grid-wide barrier on a monotonic arrival counter (zeroed by the host before
+// the launch): barrier number `phase` (1, 2, ...) completes when the counter
+// reaches phase * gridDim.x.  One atomic per CTA and no reset on the critical
+// path (the generation barrier above needs a second fence + atomic from the
+// last arrival).
+__device__ __forceinline__ void grid_barrier_count(unsigned *cnt, unsigned &phase) {
+  __syncthreads();
+  ++phase;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt, 1u);
+    const unsigned target = phase * gridDim.x;
+    while ((int)((unsigned)ld_acquire(reinterpret_cast<const int *>(cnt)) - target) < 0) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // D(8x8) += A(8x4) B(4x8) on the fp64 tensor cores: a = A[gid][tig], b = B[tig][gid],
 // (c0, c1) = D[gid][2 tig], D[gid][2 tig + 1] (gid = lane / 4, tig = lane % 4)
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {

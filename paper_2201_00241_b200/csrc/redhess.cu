@@ -600,12 +600,9 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
   double(*Rs)[GJT + 1] = Cs + GJB;                                                     // P, then R
   double(*Ts)[GJT + 1] = Rs + GJB;
   double(*R2)[GJT + 1] = Ts + GJT;   // R = D^-1 P
-  __shared__ unsigned s_gen;
   const int tid = threadIdx.x;
   const int nt = (ns + GJT - 1) / GJT, ntiles = nt * nt;
-  if (tid == 0) s_gen = (unsigned)ld_acquire(reinterpret_cast<const int *>(&bar[1]));
-  __syncthreads();
-  unsigned gen = s_gen;
+  unsigned gen = 0;   // barrier phase (bar[0] zeroed by the host before the launch)
   double *Sin = Sa, *Sout = Sb;
   __shared__ double prow[2][GJB];
   const int warp = tid >> 5, lane = tid & 31;
@@ -846,7 +843,7 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
       __syncthreads();
     }
     if (prof) prof[(K / GJB) * 4 + 2] = clock64();
-    grid_barrier(bar, gen);
+    grid_barrier_count(bar, gen);
     if (prof) prof[(K / GJB) * 4 + 3] = clock64();
     double *t = Sin;
     Sin = Sout;
@@ -3126,6 +3123,7 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar, &gdbg, &dbuf};
     const int ntl = ((ns + GJT - 1) / GJT) * ((ns + GJT - 1) / GJT);
     const int grid = std::max(1, std::min(ntl, c->coop_blocks - 1)) + 1;   // tile CTAs + the lookahead CTA
+    RH_CUDA(c, cudaMemsetAsync(c->grid_bar, 0, sizeof(unsigned), st));
     RH_CUDA(c, cudaLaunchCooperativeKernel((const void *)k_sep_inverse, dim3(grid), dim3(256), args, gj_smem_bytes(), st));
     RH_LAUNCHED(c);
     if (gdbg) {
