@@ -25,32 +25,11 @@ __device__ __forceinline__ double fast_rcp(double x) {
   return fma(r, e, r);
 }
 
-// Grid-wide barrier of a cooperative launch (all CTAs co-resident): arrival
-// counter + generation word; the last arrival resets the counter and bumps the
-// generation.  `gen` is the generation this CTA waits to leave.
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned &gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(&bar[1], 1u);
-    } else {
-      while ((unsigned)ld_acquire(reinterpret_cast<const int *>(&bar[1])) == gen) {
-      }
-    }
-    __threadfence();
-  }
-  ++gen;
-  __syncthreads();
-}
 
-// Grid-wide barrier on a monotonic arrival counter (zeroed by the host before
-// the launch): barrier number `phase` (1, 2, ...) completes when the counter
-// reaches phase * gridDim.x.  One atomic per CTA and no reset on the critical
-// path (the generation barrier above needs a second fence + atomic from the
-// last arrival).
+// Grid-wide barrier of a cooperative launch (all CTAs co-resident) on a
+// monotonic arrival counter zeroed by the host before the launch: barrier
+// number `phase` (1, 2, ...) completes when the counter reaches
+// phase * gridDim.x.  One atomic per CTA, no reset on the critical path.
 __device__ __forceinline__ void grid_barrier_count(unsigned *cnt, unsigned &phase) {
   __syncthreads();
   ++phase;
