@@ -347,3 +347,27 @@ def test_host_call_graph_replay():
     ref.load_grid(g)
     gr, Hr = ref.reduced_hessian(_dev(xh.numpy()), _dev(p), 256)
     assert np.array_equal(_np(Hr), outs[3][1]) and np.array_equal(_np(gr), outs[3][0])
+
+
+def test_empty_and_degenerate_ranges():
+    """Empty inputs: an HVP with N = 0, an empty column range, the fused call with
+    j0 == j1 (state + gradient only), a 0 x 0 dense solve; and N > n_p (one batch
+    wider than the Hessian) against the default batching, bitwise."""
+    g = pf.backout_loads(gridgen.make_grid("case118", tap_line=True))
+    ctx, x, p = setup(g)
+    ctx.reduced_gradient()
+    W0 = torch.empty((ctx.n_p, 0), dtype=torch.float64, device="cuda")
+    assert ctx.hvp(W0).shape == (ctx.n_p, 0)
+    H0 = torch.empty((ctx.n_p, 1), dtype=torch.float64, device="cuda")
+    ctx.hessian_columns(5, 5, 16, H=H0)                      # nothing to do, no error
+    gd, _ = ctx.reduced_hessian(_dev(x), _dev(p), 16, j0=7, j1=7, H=H0)
+    L = pf.Layout(g)
+    grad_o, _ = red.reduced_gradient(g, x, p, L)
+    assert np.max(np.abs(_np(gd) - grad_o)) <= 1e-10 * np.max(np.abs(grad_o))
+    d, tau, att = ctx.dense_spd_solve(torch.empty((0, 0), dtype=torch.float64, device="cuda"),
+                                      torch.empty(0, dtype=torch.float64, device="cuda"))
+    assert d.numel() == 0 and att == 0
+    ctx.set_state(_dev(x), _dev(p))
+    ctx.reduced_gradient()
+    Hwide = _np(ctx.full_hessian(4 * ctx.n_p))
+    assert np.array_equal(Hwide, _np(ctx.full_hessian(64)))
