@@ -3375,7 +3375,14 @@ int num_ws(int nb, int cap = kNumWs) {
 }
 
 // batch b of ncols columns split into nb balanced batches: [a0, a1)
-inline void batch_range(int ncols, int nb, int b, int &a0, int &a1) {
+// front = full batches of N first, the remainder last (host copies: the last
+// batch's copy is the tail nothing overlaps, so it should be the smallest)
+inline void batch_range(int ncols, int nb, int b, int &a0, int &a1, int N = 0, bool front = false) {
+  if (front) {
+    a0 = std::min(ncols, b * N);
+    a1 = std::min(ncols, (b + 1) * N);
+    return;
+  }
   a0 = (int)((long long)ncols * b / nb);
   a1 = (int)((long long)ncols * (b + 1) / nb);
 }
@@ -3406,7 +3413,7 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
   }
   for (int b = 0; b < nb; ++b) {
     int a0, a1;
-    batch_range(ncols, nb, b, a0, a1);
+    batch_range(ncols, nb, b, a0, a1, N, Hhost != nullptr);
     double *out = transposed ? H + (long long)a0 * ldh : H + a0;
     const int k = b % nws;
     cudaStream_t sb = k ? c->sti[k] : st;
@@ -3476,7 +3483,7 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   auto first_sweeps = [&](cudaStream_t sb) -> int {
     for (int b = 0; b < early; ++b) {
       int a0, a1;
-      batch_range(ncols, nb, b, a0, a1);
+      batch_range(ncols, nb, b, a0, a1, N, Hhost != nullptr);
       double *out = transposed ? H + (long long)a0 * ldh : H + a0;
       if (int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0,
                             b, 1))
