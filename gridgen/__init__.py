@@ -6,7 +6,7 @@ residual, no Jacobian, no Hessian.  It only draws a topology, line impedances,
 a bus-type partition, bus-level state (theta, v, Pg), loads, costs and seed
 blocks W -- the recipe of SURVEY.md section 8(d) -- and converts branch
 impedances to Ybus entries with the standard MATPOWER branch model
-("build_admittance"; pinned by tests/test_gridgen.py against
+(SPEC.md:61-68, "build_admittance"; pinned by tests/test_oracle.py::test_spec_admittance_values against
 SPEC.md:67-68's worked values 1/(j0.1) = -j10 and -1/(0.01+j0.1)).
 
 Shapes follow PAPER.md:846-853 (Table 1): for each case the generator
