@@ -313,7 +313,7 @@ def main():
         # overlap the separator's refactorization), then the all-gather
         if timed:
             ev[0].record(stream)
-        ctx.reduced_hessian(x, p, N, j0=j0, j1=j1, grad=grad, H=Hloc, transposed=True)
+        ctx.reduced_hessian(x, p, N, j0=j0, j1=j1, grad=grad, H=Hloc[:j1 - j0], transposed=True)
         if timed:
             ev[2].record(stream)
         if world > 1:
@@ -494,7 +494,7 @@ def main():
         for rep in range(6):
             torch.cuda.synchronize()
             ej0.record(stream)
-            ctx.reduced_hessian(x, p, N, j0, j1, grad, H=Hloc, transposed=True)
+            ctx.reduced_hessian(x, p, N, j0, j1, grad, H=Hloc[:j1 - j0], transposed=True)
             ej1.record(stream)
             torch.cuda.synchronize()
             if rep:

@@ -227,13 +227,21 @@ def _dc_angles(n_bus, f, t, x, ref, rng, max_diff=0.25):
 
 
 def make_grid(name: str = "case118", seed: int | None = None, *, lossless: bool = False,
-              tap_line: bool = False, theta_ref: float = 0.0, shape=None) -> Grid:
+              tap_line: bool = False, theta_ref: float = 0.0, shape=None, parallel_lines: int = 0,
+              phase_shift: float = 0.0) -> Grid:
     """Draw a synthetic grid shaped like `name` (Table 1).
 
     lossless=True zeroes every conductance (G_ft = G_tf = G_ii = 0, no phase
     shift) -- the closed-form test case of SURVEY.md 8(c).
     tap_line=True gives one line an off-nominal tap (1.05) so that
     Y_ft != Y_tf and Y_ff != Y_tt.
+    parallel_lines=k appends k extra lines between the end buses of existing
+    lines (every other one reversed, f <-> t), each with its own impedance:
+    their Ybus entries add (include/redhess.h, rh_grid; R1).
+    phase_shift=phi gives one line (index 1) a phase-shifting transformer of
+    angle phi rad, so that Y_ft and Y_tf differ by more than a conjugate tap.
+    shape=(n_v, n_e, n_pv) overrides the case's counts; n_pv = n_v - 1 gives a
+    grid without PQ buses (n_pq = 0, R24).
     """
     if shape is None:
         n_v, n_e, n_pv = CASES[name]
@@ -250,6 +258,12 @@ def make_grid(name: str = "case118", seed: int | None = None, *, lossless: bool 
         picks = rng.choice(n_v, size=n_pv + 1, replace=False)
         bus_type[picks[0]] = REF
         bus_type[picks[1:]] = PV
+    if parallel_lines:
+        prng = np.random.default_rng(seed + 7)
+        dup = prng.choice(f.shape[0], size=parallel_lines, replace=False)
+        rev = (np.arange(parallel_lines) % 2) == 1
+        f, t = (np.concatenate([f, np.where(rev, t[dup], f[dup])]).astype(np.int32),
+                np.concatenate([t, np.where(rev, f[dup], t[dup])]).astype(np.int32))
     n_line = f.shape[0]
     r = rng.uniform(0.002, 0.05, n_line)
     x = r * rng.uniform(3.0, 10.0, n_line)
@@ -258,6 +272,8 @@ def make_grid(name: str = "case118", seed: int | None = None, *, lossless: bool 
     if tap_line:
         tap[0] = 1.05
     shift = np.zeros(n_line)
+    if phase_shift and not lossless:
+        shift[1 % n_line] = phase_shift
     bsh = np.where(rng.random(n_v) < 0.05, rng.uniform(0.0, 0.02, n_v), 0.0)
     gsh = np.zeros(n_v)
     if lossless:

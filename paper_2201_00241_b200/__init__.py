@@ -133,12 +133,46 @@ def _stream(stream):
     return stream.cuda_stream
 
 
-def _check_dev(t, n=None, name="array"):
+def _check_dev(t, n=None, name="array", device=None):
+    """A contiguous float64 CUDA tensor with exactly n elements (n=None: any size)."""
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
-    if n is not None and t.numel() < n:
+    if device is not None and device >= 0 and t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the context is on cuda:{device}")
+    if n is not None and t.numel() != n:
         raise ValueError(f"{name} has {t.numel()} elements, need {n}")
+
+
+def _check_dev_mat(t, rows, cols, name="array", device=None):
+    """A row-major float64 CUDA matrix of shape [rows][cols] with unit column
+    stride and row stride >= cols (the library's [row][ld] layout)."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
+        raise TypeError(f"{name} must be a float64 CUDA tensor")
+    if device is not None and device >= 0 and t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the context is on cuda:{device}")
+    if t.dim() != 2 or tuple(t.shape) != (rows, cols):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, need ({rows}, {cols})")
+    if cols > 0 and rows > 0 and (t.stride(1) != 1 or t.stride(0) < cols):
+        raise ValueError(f"{name} must be row-major with unit column stride (strides {t.stride()})")
+
+
+def _check_host(a, shape, name="array", writable=False):
+    """A C-contiguous float64 HOST array (numpy, or a CPU torch tensor) of exactly `shape`."""
+    if isinstance(a, np.ndarray):
+        ok = a.dtype == np.float64 and a.flags.c_contiguous and (a.flags.writeable or not writable)
+        shp = a.shape
+    else:
+        import torch
+        if not isinstance(a, torch.Tensor) or a.is_cuda:
+            raise TypeError(f"{name} must be a host (numpy or CPU torch) float64 array")
+        ok = a.dtype == torch.float64 and a.is_contiguous()
+        shp = tuple(a.shape)
+    if not ok:
+        raise TypeError(f"{name} must be a C-contiguous{' writable' if writable else ''} float64 host array")
+    if tuple(shp) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(shp)}, need {tuple(shape)}")
 
 
 class RedHess:
@@ -225,14 +259,16 @@ class RedHess:
 
     # ------------------------------------------------------------------ compute (device)
     def set_state(self, x, p, stream=None):
-        _check_dev(x, self.n_x, "x")
-        _check_dev(p, self.n_p, "p")
+        _check_dev(x, self.n_x, "x", self.device)
+        _check_dev(p, self.n_p, "p", self.device)
         self._rc(lib().rh_set_state(self._h, _ptr(x), _ptr(p), _stream(stream)))
 
     def residual(self, g=None, f=None, stream=None):
         import torch
         g = torch.empty(self.n_x, dtype=torch.float64, device="cuda") if g is None else g
         f = torch.empty(1, dtype=torch.float64, device="cuda") if f is None else f
+        _check_dev(g, self.n_x, "g", self.device)
+        _check_dev(f, 1, "f", self.device)
         self._rc(lib().rh_residual(self._h, _ptr(g), _ptr(f), _stream(stream)))
         return g, f
 
@@ -240,37 +276,58 @@ class RedHess:
         import torch
         grad = torch.empty(self.n_p, dtype=torch.float64, device="cuda") if grad is None else grad
         lam = torch.empty(self.n_x, dtype=torch.float64, device="cuda") if lam is None else lam
+        _check_dev(grad, self.n_p, "grad", self.device)
+        _check_dev(lam, self.n_x, "lambda", self.device)
         self._rc(lib().rh_reduced_gradient(self._h, _ptr(grad), _ptr(lam), _stream(stream)))
         return grad, lam
 
     def set_multipliers(self, lam, stream=None):
-        _check_dev(lam, self.n_x, "lambda")
+        _check_dev(lam, self.n_x, "lambda", self.device)
         self._rc(lib().rh_set_multipliers(self._h, _ptr(lam), _stream(stream)))
 
     def hvp(self, W, HW=None, stream=None):
         """W: [n_p][N] float64 CUDA tensor (batch index fastest) -> HW [n_p][N]."""
         import torch
-        _check_dev(W, name="W")
+        if not isinstance(W, torch.Tensor) or W.dim() != 2:
+            raise TypeError("W must be a 2-D float64 CUDA tensor [n_p][N]")
         N = W.shape[1]
+        _check_dev_mat(W, self.n_p, N, "W", self.device)
         HW = torch.empty((self.n_p, N), dtype=torch.float64, device=W.device) if HW is None else HW
+        _check_dev_mat(HW, self.n_p, N, "HW", self.device)
         self._rc(lib().rh_hvp(self._h, _ptr(W), W.stride(0), _ptr(HW), HW.stride(0), N, _stream(stream)))
         return HW
 
     def hvp_stages(self, W, stream=None):
         import torch
-        _check_dev(W, name="W")
+        if not isinstance(W, torch.Tensor) or W.dim() != 2:
+            raise TypeError("W must be a 2-D float64 CUDA tensor [n_p][N]")
         N = W.shape[1]
+        _check_dev_mat(W, self.n_p, N, "W", self.device)
         HW = torch.empty((self.n_p, N), dtype=torch.float64, device=W.device)
         Z, Yx, Psi = (torch.empty((self.n_x, N), dtype=torch.float64, device=W.device) for _ in range(3))
         self._rc(lib().rh_hvp_stages(self._h, _ptr(W), W.stride(0), _ptr(HW), HW.stride(0), N, _ptr(Z), _ptr(Yx),
                                     _ptr(Psi), Z.stride(0), _stream(stream)))
         return HW, Z, Yx, Psi
 
-    def hessian_columns(self, j0, j1, N, H=None, transposed=False, stream=None):
+    def _check_range(self, j0, j1):
+        if not (0 <= j0 <= j1 <= self.n_p):
+            raise ValueError(f"column range [{j0}, {j1}) is not inside [0, {self.n_p})")
+
+    def _cols_out(self, H, j0, j1, transposed):
         import torch
+        shape = (j1 - j0, self.n_p) if transposed else (self.n_p, j1 - j0)
         if H is None:
-            shape = (j1 - j0, self.n_p) if transposed else (self.n_p, j1 - j0)
-            H = torch.empty(shape, dtype=torch.float64, device="cuda")
+            return torch.empty(shape, dtype=torch.float64, device="cuda")
+        if j1 == j0:     # nothing is written; any float64 CUDA matrix will do
+            if not isinstance(H, torch.Tensor) or not H.is_cuda or H.dtype != torch.float64 or H.dim() != 2:
+                raise TypeError("H must be a float64 CUDA matrix")
+            return H
+        _check_dev_mat(H, shape[0], shape[1], "H", self.device)
+        return H
+
+    def hessian_columns(self, j0, j1, N, H=None, transposed=False, stream=None):
+        self._check_range(j0, j1)
+        H = self._cols_out(H, j0, j1, transposed)
         self._rc(lib().rh_hessian_columns(self._h, j0, j1, N, _ptr(H), H.stride(0), int(bool(transposed)),
                                          _stream(stream)))
         return H
@@ -278,15 +335,17 @@ class RedHess:
     def full_hessian(self, N, H=None, stream=None):
         import torch
         H = torch.empty((self.n_p, self.n_p), dtype=torch.float64, device="cuda") if H is None else H
-        _check_dev(H, self.n_p * self.n_p, "H")
+        _check_dev(H, self.n_p * self.n_p, "H", self.device)
+        if H.dim() != 2 or tuple(H.shape) != (self.n_p, self.n_p):
+            raise ValueError(f"H has shape {tuple(H.shape)}, need ({self.n_p}, {self.n_p})")
         self._rc(lib().rh_full_hessian(self._h, N, _ptr(H), _stream(stream)))
         return H
 
     # ------------------------------------------------------------------ compute (host buffers)
     def newton(self, x, p, tol=1e-11, extra=2, maxit=40, stream=None):
         """rh_newton: Newton-Raphson projection x(p) in place on the DEVICE vector x; returns (steps, max|g|)."""
-        _check_dev(x, self.n_x, "x")
-        _check_dev(p, self.n_p, "p")
+        _check_dev(x, self.n_x, "x", self.device)
+        _check_dev(p, self.n_p, "p", self.device)
         it = ctypes.c_int32(0)
         res = ctypes.c_double(0.0)
         self._rc(lib().rh_newton(self._h, _ptr(x), _ptr(p), float(tol), int(extra), int(maxit), ctypes.byref(it),
@@ -297,13 +356,13 @@ class RedHess:
         """rh_reduced_hessian: state + reduced gradient + Hessian columns [j0, j1) in one call (DEVICE)."""
         import torch
         j1 = self.n_p if j1 is None else j1
-        _check_dev(x, self.n_x, "x")
-        _check_dev(p, self.n_p, "p")
+        self._check_range(j0, j1)
+        _check_dev(x, self.n_x, "x", self.device)
+        _check_dev(p, self.n_p, "p", self.device)
         if grad is None:
             grad = torch.empty(self.n_p, dtype=torch.float64, device="cuda")
-        if H is None:
-            shape = (j1 - j0, self.n_p) if transposed else (self.n_p, j1 - j0)
-            H = torch.empty(shape, dtype=torch.float64, device="cuda")
+        _check_dev(grad, self.n_p, "grad", self.device)
+        H = self._cols_out(H, j0, j1, transposed)
         self._rc(lib().rh_reduced_hessian(self._h, _ptr(x), _ptr(p), j0, j1, N, _ptr(grad), _ptr(H), H.stride(0),
                                           int(bool(transposed)), _stream(stream)))
         return grad, H
@@ -314,6 +373,10 @@ class RedHess:
             H = np.empty((self.n_p, self.n_p))
         if grad is None:
             grad = np.empty(self.n_p)
+        _check_host(x, (self.n_x,), "x")
+        _check_host(p, (self.n_p,), "p")
+        _check_host(grad, (self.n_p,), "grad", writable=True)
+        _check_host(H, (self.n_p, self.n_p), "H", writable=True)
         self._rc(lib().rh_reduced_hessian_host(self._h, _ptr(x), _ptr(p), N, _ptr(grad), _ptr(H)))
         return grad, H
 
@@ -321,9 +384,9 @@ class RedHess:
     def set_loads(self, Pd=None, Qd=None, stream=None):
         """rh_set_loads: DEVICE loads [n_bus] (None = keep); invalidates the state."""
         if Pd is not None:
-            _check_dev(Pd, self.n_bus, "Pd")
+            _check_dev(Pd, self.n_bus, "Pd", self.device)
         if Qd is not None:
-            _check_dev(Qd, self.n_bus, "Qd")
+            _check_dev(Qd, self.n_bus, "Qd", self.device)
         self._rc(lib().rh_set_loads(self._h, _ptr(Pd) if Pd is not None else None,
                                     _ptr(Qd) if Qd is not None else None, _stream(stream)))
 
@@ -332,13 +395,15 @@ class RedHess:
         p += alpha d when p is given.  Returns (d, tau, attempts)."""
         import torch
         n = g.shape[0]
-        _check_dev(g, n, "g")
-        if H.dim() != 2 or H.shape[0] < n or H.shape[1] < n or H.stride(1) != 1 or H.dtype != torch.float64:
-            raise ValueError("H must be a row-major float64 [>= n][>= n] device matrix")
+        _check_dev(g, n, "g", self.device)
+        if (not isinstance(H, torch.Tensor) or not H.is_cuda or H.dim() != 2 or H.shape[0] < n or H.shape[1] < n
+                or (n > 0 and H.stride(1) != 1) or H.dtype != torch.float64):
+            raise ValueError("H must be a row-major float64 [>= n][>= n] CUDA matrix")
         if d is None:
             d = torch.empty(n, dtype=torch.float64, device=g.device)
+        _check_dev(d, n, "d", self.device)
         if p is not None:
-            _check_dev(p, n, "p")
+            _check_dev(p, n, "p", self.device)
         tau = ctypes.c_double(0.0)
         att = ctypes.c_int32(0)
         self._rc(lib().rh_dense_spd_solve(self._h, n, _ptr(H), H.stride(0), _ptr(g), _ptr(d),
@@ -353,17 +418,19 @@ class RedHess:
         Returns (grad, H, d, info) with info = dict(newton_steps, resid, F, tau, attempts, ms_step1, ms_step2)."""
         import torch
         j1 = self.n_p if j1 is None else j1
-        _check_dev(x, self.n_x, "x")
-        _check_dev(p, self.n_p, "p")
+        _check_dev(x, self.n_x, "x", self.device)
+        _check_dev(p, self.n_p, "p", self.device)
         for name, v in (("Pd", Pd), ("Qd", Qd)):
             if v is not None:
-                _check_dev(v, self.n_bus, name)
+                _check_dev(v, self.n_bus, name, self.device)
+        self._check_range(j0, j1)
         if grad is None:
             grad = torch.empty(self.n_p, dtype=torch.float64, device="cuda")
-        if H is None:
-            H = torch.empty((j1 - j0, self.n_p), dtype=torch.float64, device="cuda")
+        _check_dev(grad, self.n_p, "grad", self.device)
+        H = self._cols_out(H, j0, j1, True)
         if d is None:
             d = torch.empty(j1 - j0, dtype=torch.float64, device="cuda")
+        _check_dev(d, j1 - j0, "d", self.device)
         info = np.zeros(7)
         self._rc(lib().rh_tracking_step(self._h, _ptr(x), _ptr(p), _ptr(Pd) if Pd is not None else None,
                                         _ptr(Qd) if Qd is not None else None, j0, j1, N, float(alpha), _ptr(grad),

@@ -2899,7 +2899,7 @@ bool graph_run(rh_ctx *c, int slot, const rh_ctx::GraphKey &key, cudaStream_t st
   };
   auto finish = [&]() {
     c->has_state = true;
-    if (mult) c->has_mult = true;
+    c->has_mult = mult;   // a state-only replay (Newton) leaves no valid multipliers
     join();
     rc = check_pivots(c, cs);
     return true;
@@ -3476,7 +3476,11 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   RH_CUDA(c, cudaSetDevice(c->device));
   const int ncols = j1 - j0, nb = ncols > 0 ? (ncols + N - 1) / N : 0;
   const int early = nb > 0 ? std::min(nb, num_ws(nb, Hhost ? 2 : kNumWs)) : 0;
-  const int ld = (N + kBC - 1) / kBC * kBC;
+  // the widest batch actually run (front-loaded batches of N for host copies,
+  // else ceil(ncols / nb)), not the caller's N: a shard or N > n_p must not
+  // allocate workspaces no batch uses
+  const int wmax = nb > 0 ? (Hhost ? std::min(N, ncols) : (ncols + nb - 1) / nb) : 0;
+  const int ld = (wmax + kBC - 1) / kBC * kBC;
   for (int k = 0; k < early; ++k)   // allocate before anything is enqueued
     if (int rc = ensure_ws(c, ld, k)) return rc;
   if (!c->sti[1]) RH_CUDA(c, cudaStreamCreateWithFlags(&c->sti[1], cudaStreamNonBlocking));

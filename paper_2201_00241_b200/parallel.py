@@ -34,7 +34,14 @@ def gather_columns(H_local, n_p: int, group=None, out=None):
     c = H_local.shape[0]
     if out is None:
         out = torch.empty((world * c, n_p), dtype=H_local.dtype, device=H_local.device)
-    dist.all_gather_into_tensor(out, H_local, group=group)
+    if H_local.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo (ranks sharing one GPU in the tests) gathers host tensors: stage
+        # through host memory; NCCL gathers device memory directly
+        tmp = torch.empty((world * c, n_p), dtype=H_local.dtype)
+        dist.all_gather_into_tensor(tmp, H_local.cpu(), group=group)
+        out.copy_(tmp)
+    else:
+        dist.all_gather_into_tensor(out, H_local, group=group)
     return out, out[:n_p]
 
 
@@ -57,8 +64,21 @@ class ShardedHessian:
     def local_columns(self, N: int):
         """This rank's columns (transposed slab); no communication."""
         if self.j1 > self.j0:
-            self.ctx.hessian_columns(self.j0, self.j1, N, H=self.H_local, transposed=True)
+            self.ctx.hessian_columns(self.j0, self.j1, N, H=self.H_local[:self.j1 - self.j0], transposed=True)
         return self.H_local
+
+    def reduced(self, x, p, N: int, grad=None):
+        """State + reduced gradient + this rank's columns in one library call
+        (rh_reduced_hessian, transposed slab), then the one all-gather.
+        Returns (grad, H^T) with H^T [n_p][n_p] (row j = column j of H)."""
+        rows = self.j1 - self.j0
+        grad, _ = self.ctx.reduced_hessian(x, p, N, j0=self.j0, j1=self.j1, grad=grad,
+                                           H=self.H_local[:rows] if rows else self.H_local,
+                                           transposed=True)
+        if self.world == 1:
+            return grad, self.H_local[:self.ctx.n_p]
+        _, HT = gather_columns(self.H_local, self.ctx.n_p, self.group, out=self.H_all)
+        return grad, HT
 
     def full(self, N: int):
         """Every rank's columns, gathered: returns H^T ([n_p][n_p], row j = column j of H)."""

@@ -159,3 +159,22 @@ def test_coloring_matches_oracle(name):
     co = col.greedy_coloring(col.column_rows(g, L), L.n_x)
     assert nc == int(co.max()) + 1
     assert np.array_equal(colors, co.astype(np.int32))
+
+
+def test_host_buffers_validated_before_the_call():
+    """reduced_hessian_host checks dtype, contiguity and shape of every
+    host buffer before libredhess sees it (a float32 / short / strided array
+    would be read or written past its end by the C call)."""
+    c = rh.RedHess(-1)
+    c.load_grid(gridgen.make_grid("case9"))
+    x = np.zeros(c.n_x)
+    p = np.ones(c.n_p)
+    bad = [dict(x=x.astype(np.float32)), dict(x=x[:-1]), dict(p=np.ones(2 * c.n_p)[::2]),
+           dict(H=np.empty((c.n_p, c.n_p - 1))), dict(grad=np.empty(c.n_p + 1)),
+           dict(H=np.empty((c.n_p, c.n_p), dtype=np.float32))]
+    for kw in bad:
+        args = dict(x=x, p=p)
+        args.update(kw)
+        xx, pp = args.pop("x"), args.pop("p")
+        with pytest.raises((TypeError, ValueError)):
+            c.reduced_hessian_host(xx, pp, 5, **args)

@@ -433,3 +433,52 @@ def test_unsolved_point_hessian_is_shifted_problem():
     H1 = red.reduced_hessian(g1)
     assert np.max(np.abs(H0 - H1)) <= 1e-13 * np.max(np.abs(H0))
     assert math.isfinite(float(np.max(H0)))
+
+
+# ---------------------------------------------------------------- input classes the ABI accepts
+# (include/redhess.h rh_grid: parallel lines add, phase shifters, n_pq = 0; R1, R24)
+
+VARIANTS = {
+    "parallel+shift": dict(name="case9", kw=dict(parallel_lines=3, phase_shift=0.08, tap_line=True)),
+    "parallel118": dict(name="case118", kw=dict(parallel_lines=6, phase_shift=-0.05)),
+    "no_pq": dict(name="allpv", kw=dict(shape=(12, 17, 11))),
+}
+
+
+def variant_grid(key):
+    v = VARIANTS[key]
+    return solved(v["name"], **v["kw"])
+
+
+def test_variant_grids_have_their_feature():
+    g = variant_grid("parallel+shift")
+    pairs = [tuple(sorted(e)) for e in zip(g.line_f.tolist(), g.line_t.tolist())]
+    assert len(set(pairs)) == len(pairs) - 3                       # three doubled corridors
+    # phase shifter: Y_tf != Y_ft (a tap alone keeps G_ft = G_tf, B_ft = B_tf)
+    assert abs(g.G_ft[1] - g.G_tf[1]) > 1e-3
+    L = pf.Layout(variant_grid("no_pq"))
+    assert L.n_x == 11 and L.n_p == 23
+
+
+@pytest.mark.parametrize("key", sorted(VARIANTS))
+def test_variant_residual_zero_and_jacobian_complex_step(key):
+    g = variant_grid(key)
+    L = pf.Layout(g)
+    x, p = pf.state_vectors(g, L)
+    assert np.max(np.abs(pf.residual(g, x, p, L))) <= 1e-12
+    J, Gp = pf.jacobians(g, x, p, L)
+    Jcs = pins.cs_columns(lambda xc: pf.residual(g, xc, p.astype(np.complex128), L), x)
+    Gcs = pins.cs_columns(lambda pc: pf.residual(g, x.astype(np.complex128), pc, L), p)
+    assert np.max(np.abs(J.toarray() - Jcs)) <= 1e-13 * np.max(np.abs(Jcs))
+    assert np.max(np.abs(Gp.toarray() - Gcs)) <= 1e-13 * max(1.0, np.max(np.abs(Gcs)))
+
+
+@pytest.mark.parametrize("key", sorted(VARIANTS))
+def test_variant_hessian_complex_step(key):
+    """H by Alg. 2 vs complex-step of the reduced gradient through complex Newton
+    (SURVEY.md 8(c) pin (1)) on grids with parallel lines, a phase shifter and no
+    PQ bus: the oracle is pinned on every input class the GPU tests feed it."""
+    g = variant_grid(key)
+    H = red.reduced_hessian(g, N=16)
+    Hcs, _ = pins.cs_reduced_hessian(g)
+    assert np.max(np.abs(H - Hcs)) <= 1e-12 * np.max(np.abs(Hcs))

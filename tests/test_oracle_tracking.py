@@ -180,3 +180,29 @@ def test_tracking_grid_is_well_conditioned_for_load_changes():
     for t in (0, 15, 30):
         xt = pf.newton(trk.with_loads(g, Pd[t], Qd[t]), p, x, L)
         assert np.max(np.abs(pf.residual(trk.with_loads(g, Pd[t], Qd[t]), xt, p, L))) < 1e-10
+
+
+def test_run_tracking_constant_loads_is_newton_on_F(case118):
+    """run_tracking over a CONSTANT load series is Newton's method on F over the
+    free set points (PAPER.md:962-975 with w_t = w): the trace's |g_t| contracts
+    quadratically to the rounding floor, every step is PD (tau = 0), |d_t|
+    contracts with it, and p_t is the iterate (p_0 first)."""
+    L = pf.Layout(case118)
+    x, p = pf.state_vectors(case118, L)
+    n_pv = int(np.sum(L.p_kind == 2))
+    T = 6
+    Pd = np.repeat(np.asarray(case118.Pd, float)[None, :], T, 0)
+    Qd = np.repeat(np.asarray(case118.Qd, float)[None, :], T, 0)
+    tr = trk.run_tracking(case118, p, x, Pd, Qd, 0, n_pv, N=64, L=L)
+    assert [e["t"] for e in tr] == list(range(T))
+    assert np.array_equal(tr[0]["p"], p)
+    gn = [e["grad_inf"] for e in tr]
+    assert gn[-1] < 1e-9 * gn[0]
+    for a, b in zip(gn[:-1], gn[1:]):
+        if 1e-6 < a < 1.0:
+            assert b <= 10.0 * a * a, (a, b)
+    assert all(e["tau"] == 0.0 for e in tr)
+    dn = [e["d_inf"] for e in tr]
+    assert dn[-1] < 1e-6 * dn[0]
+    # only the free range moves
+    assert np.array_equal(tr[-1]["p"][n_pv:], p[n_pv:])

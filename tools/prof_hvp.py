@@ -1,4 +1,8 @@
-"""Run a few HVP batches on one case (for ncu).  python tools/prof_hvp.py [case] [N] [reps]"""
+"""Run a few HVP batches on one case (for ncu).  python tools/prof_hvp.py [case] [N] [reps]
+
+The LAST batch runs between cudaProfilerStart/Stop, so
+`ncu --profile-from-start off ...` captures exactly one complete Alg. 2 batch
+(every kernel of it: k_blk x4, k_sep_gather x2, k_sep_gemm x2, k_for, k_muladd)."""
 import os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -16,7 +20,11 @@ ctx.set_state(torch.from_numpy(x).cuda(), torch.from_numpy(p).cuda())
 ctx.reduced_gradient()
 W = torch.randn(ctx.n_p, N, dtype=torch.float64, device="cuda")
 HW = torch.empty_like(W)
-for _ in range(reps):
+for _ in range(max(0, reps - 1)):
     ctx.hvp(W, HW)
 torch.cuda.synchronize()
+torch.cuda.profiler.start()
+ctx.hvp(W, HW)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print("ok", ctx.get_info())
