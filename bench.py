@@ -58,63 +58,161 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------- oracle (CPU)
+# The CPU oracle as it stands (oracle/, never tuned for this), timed on the
+# host cores.  Two modes (SURVEY.md 8(d) "How the oracle is timed alongside"):
+#   * single core: setup (state + gradient, assembly + SuperLU factorization),
+#     Alg. 2 on Cartesian batches with a per-stage breakdown (the Fig. 6 analog,
+#     PAPER.md:920-936), and Alg. 1 one column at a time ("N=1 corresponds to
+#     the CPU implementation");
+#   * all cores: a process pool over contiguous column ranges, every worker
+#     single-threaded with its own setup and factorization; one pool pass is a
+#     REAL full Hessian (no extrapolation).
 
-def oracle_time(grid, n_cols, N):
-    """Time the CPU oracle (as it stands) on a bounded sample: setup (J, G_p,
-    Lagrangian Hessian, SuperLU factorization, lambda, grad) plus n_cols Cartesian
-    HVP columns by Alg. 2 in batches of N.  Returns (HVP/s extrapolated to the
-    full Hessian, seconds spent, cores used, details)."""
-    from threadpoolctl import threadpool_limits
+_POOL = {}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _oracle_setup(grid, timers=None):
     from oracle import powerflow as pf
     from oracle import reduction as red
-    with threadpool_limits(1):
+    t0 = time.perf_counter()
+    L = pf.Layout(grid)
+    x, p = pf.state_vectors(grid, L)
+    grad, lam = red.reduced_gradient(grid, x, p, L)            # lambda + grad_p F
+    t1 = time.perf_counter()
+    ops = red.operators(grid, x, p, lam, L)                    # J, G_p, Lagrangian Hessian, SuperLU
+    t2 = time.perf_counter()
+    if timers is not None:
+        timers["state_gradient"] = timers.get("state_gradient", 0.0) + (t1 - t0)
+        timers["assembly_factorization"] = timers.get("assembly_factorization", 0.0) + (t2 - t1)
+    return L, ops
+
+
+def _oracle_columns(ops, n_p, j0, j1, N, timers=None):
+    from oracle import reduction as red
+    acc = 0.0
+    for a in range(j0, j1, N):
+        b = min(j1, a + N)
+        W = np.zeros((n_p, b - a))
+        W[np.arange(a, b), np.arange(b - a)] = 1.0
+        acc += float(red.hvp_batch(ops, W, timers=timers).sum())
+    return acc
+
+
+def _pool_init(case):
+    from threadpoolctl import threadpool_limits
+    import gridgen
+    from oracle import powerflow as pf
+    _POOL["limits"] = threadpool_limits(1)
+    _POOL["grid"] = pf.backout_loads(gridgen.make_grid(case))
+
+
+def _pool_task(args):
+    j0, j1, N = args
+    t0 = time.perf_counter()
+    L, ops = _oracle_setup(_POOL["grid"])
+    t1 = time.perf_counter()
+    chk = _oracle_columns(ops, L.n_p, j0, j1, N)
+    return t1 - t0, time.perf_counter() - t1, chk
+
+
+class OraclePool:
+    """All-cores oracle: `workers` single-threaded processes, each with its own
+    grid copy (built once, outside any timing), setup and factorization."""
+
+    def __init__(self, case, n_p, workers):
+        import multiprocessing as mpx
+        self.n_p, self.workers = n_p, max(1, min(workers, n_p))
+        self.pool = mpx.get_context("spawn").Pool(self.workers, initializer=_pool_init, initargs=(case,))
+
+    def full_hessian(self, N):
+        """One real full Hessian: setup on every worker + its contiguous column range.
+        Returns (wall seconds, max worker setup seconds, checksum)."""
+        c = -(-self.n_p // self.workers)
+        tasks = [(j0, min(self.n_p, j0 + c), min(N, c)) for j0 in range(0, self.n_p, c)]
         t0 = time.perf_counter()
-        L = pf.Layout(grid)
-        x, p = pf.state_vectors(grid, L)
-        grad, lam = red.reduced_gradient(grid, x, p, L)
-        ops = red.operators(grid, x, p, lam, L)
+        res = self.pool.map(_pool_task, tasks, chunksize=1)
+        wall = time.perf_counter() - t0
+        return wall, max(r[0] for r in res), sum(r[2] for r in res)
+
+    def close(self):
+        self.pool.terminate()
+        self.pool.join()
+
+
+def oracle_single_core(grid, n_cols, N, alg1_cols=8):
+    """Single-threaded oracle on a bounded sample: setup + n_cols Cartesian
+    columns by Alg. 2 (batches of N, per-stage timers) + alg1_cols columns by
+    Alg. 1.  Returns a dict; full-Hessian figures are EXTRAPOLATED and say so."""
+    from threadpoolctl import threadpool_limits
+    from oracle import reduction as red
+    with threadpool_limits(1):
+        st = {}
+        t0 = time.perf_counter()
+        L, ops = _oracle_setup(grid, st)
         t_setup = time.perf_counter() - t0
         n_cols = min(n_cols, L.n_p)
         t1 = time.perf_counter()
-        done = 0
-        while done < n_cols:
-            w = min(N, n_cols - done)
-            W = np.zeros((L.n_p, w))
-            W[np.arange(done, done + w), np.arange(w)] = 1.0
-            red.hvp_batch(ops, W)
-            done += w
+        _oracle_columns(ops, L.n_p, 0, n_cols, N, st)
         t_cols = time.perf_counter() - t1
+        k = min(alg1_cols, L.n_p)
+        t2 = time.perf_counter()
+        for j in range(k):
+            e = np.zeros(L.n_p)
+            e[j] = 1.0
+            red.hvp_sequential(ops, e)
+        t_alg1 = (time.perf_counter() - t2) / k
     per_col = t_cols / n_cols
     t_full = t_setup + per_col * L.n_p
-    return L.n_p / t_full, t_setup + t_cols, 1, dict(setup_s=t_setup, per_col_s=per_col,
-                                                       full_hessian_s_extrapolated=t_full, cols=n_cols)
+    return {"cores": 1, "setup_s": t_setup, "alg2_per_column_s": per_col, "alg2_columns": n_cols, "N": N,
+            "alg1_per_column_s": t_alg1, "alg1_columns": k,
+            "stages_s": {kk: float(v) for kk, v in st.items()},
+            "full_hessian_s_extrapolated": t_full, "hvps_per_s_extrapolated": L.n_p / t_full,
+            "alg1_full_hessian_s_extrapolated": t_setup + t_alg1 * L.n_p,
+            "spent_s": t_setup + t_cols + t_alg1 * k}
 
 
 def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores.  One step =
+    one REAL full Hessian (setup on every worker + all n_p Cartesian columns)
+    through the all-cores process pool; ms_per_step is the time it ran."""
     rank, world, _ = dist_env()
     if world > 1 and rank != 0:
         return 0
     import gridgen
+    from oracle import powerflow as pf
     case = args.case
     N = args.N or gridgen.CONFIG_N.get(case, 256)
-    from oracle import powerflow as pf
     grid = pf.backout_loads(gridgen.make_grid(case))   # the same solved operating point as our arm
-    cols = min(128, args.cpu_cols)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        v, spent, cores, det = oracle_time(grid, cols, N)
-        if i >= args.warmup:
-            vals.append((v, spent, det))
-    v = float(np.median([a[0] for a in vals]))
-    t_full = float(np.median([a[2]["full_hessian_s_extrapolated"] for a in vals]))
+    from oracle import powerflow as pf2
+    n_p = pf2.Layout(grid).n_p
+    cores = host_cores()
+    pool = OraclePool(case, n_p, cores)
+    try:
+        walls = []
+        for i in range(args.warmup + args.steps):
+            wall, t_setup, _ = pool.full_hessian(N)
+            if i >= args.warmup:
+                walls.append(wall)
+    finally:
+        pool.close()
+    t = float(np.median(walls))
+    v = n_p / t
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": workload_name(case, N), "case": case, "N": N},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"per step: oracle setup + {cols} Cartesian columns (Alg. 2, batch {N}), "
-                                   f"extrapolated to all n_p columns; single-threaded BLAS/SuperLU"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": pool.workers, "host_cores": cores, "kind": "oracle",
+                         "sample": f"per step: one full grad^2 F of {case} (all {n_p} Cartesian columns, Alg. 2) "
+                                   f"by {pool.workers} single-threaded oracle processes over contiguous column "
+                                   f"ranges, each with its own setup + SuperLU factorization; not extrapolated"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -419,40 +517,73 @@ def main():
     e2e_val = n_p / t_e2e.item()
 
     # ---- roofline of the dominant kernel: k_blk, the bus-unit block sweeps
-    # (4 of the 8 kernels of an Alg. 2 batch).  Algorithmic HBM bytes of one
-    # k_blk launch: read + write of every block row of Z (or P) for the batch,
-    # 2 * (n_x - ns) * N * 8 B.  Per-stage device times
-    # come from CUDA events the library records around each kernel of a batch.
+    # (4 of the 8 kernels of an Alg. 2 batch, ~55 % of its time).  Algorithmic
+    # bytes = SURVEY.md 8(d)'s M2 share of the two solve stages, per HVP
+    #   [SpMul + L + U]  reads w (n_p), writes z (n_x)
+    #   [U^T + L^T]      reads y_x (n_x), writes psi (n_x)
+    # = (3 n_x + n_p) * 8 B, credited in full to the 4 k_blk launches of a
+    # batch (the separator kernels get none): per launch (3 n_x + n_p) 8 N / 4.
+    # Per-stage device times: CUDA events the library records around each
+    # kernel of a batch, on the stream the kernels run on (rh_set_timing).
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
     ctx.set_timing(True)
     stage = np.zeros(9)
-    for _ in range(5):
+    reps_t = 5
+    for _ in range(reps_t):
         ctx.hvp(W, HW)
         stage += ctx.stage_times()
     ctx.set_timing(False)
-    stage /= 5
+    stage /= reps_t
+    names = ["A_L", "B_LU", "A_U", "FoR", "A_Ut", "B_UtLt", "A_Lt", "MulAdd"]
     seg_ms = stage[[0, 2, 4, 6]]                      # A_L, A_U, A_Ut, A_Lt
     ns = info["sep_rows"]
-    seg_bytes = 2.0 * (n_x - ns) * N * 8
-    achieved = seg_bytes / (seg_ms.mean() * 1e-3) / 1e9 if seg_ms.mean() > 0 else None
-    m2_bytes_per_hvp = (6 * n_x + 5 * n_p) * 8            # SURVEY.md 8(d) model M2, whole path
+    m2_hvp = (6 * n_x + 5 * n_p) * 8                  # SURVEY.md 8(d) model M2, whole path
+    solve_m2_hvp = (3 * n_x + n_p) * 8                # its solve-stage share
+    kblk_bytes = solve_m2_hvp * N / 4.0
+    launch_ms = float(seg_ms.mean())
+    achieved = kblk_bytes / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else None
+    batch_ms = float(stage[:8].sum())                 # the 8 stages back to back (events per kernel)
+    path_gbs = m2_hvp * N / (batch_ms * 1e-3) / 1e9 if batch_ms > 0 else None
     cols_local = j1 - j0
-    ms_batches = ms_hess - ms_pre                  # batches' share of the fused call (estimate)
-    path_gbs = m2_bytes_per_hvp * cols_local / (ms_batches * 1e-3) / 1e9 if ms_batches > 0 else None
-    traffic = None
+    step_gbs = m2_hvp * cols_local / (ms_step * 1e-3) / 1e9 if ms_step > 0 else None
+    # secondary, per-launch read + write of the block rows each k_blk launch moves
+    # (A_L reads W and G_p only and writes Z's block rows; the others read and write them)
+    rw_bytes = np.array([(n_x - ns) * N * 8 + n_p * N * 8] + [2.0 * (n_x - ns) * N * 8] * 3)
+    rw_gbs = float(np.mean(rw_bytes / (seg_ms * 1e-3) / 1e9)) if np.all(seg_ms > 0) else None
+    traffic, ncu_share = None, None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        key = f"{case}:N={N}"
-        if key in prof and prof[key].get("kernel", "").startswith("k_blk"):
-            traffic = prof[key].get("dram_bytes_per_launch")
+        rec = prof.get(f"{case}:N={N}", {})
+        traffic = rec.get("k_blk_dram_bytes_per_launch", rec.get("dram_bytes_per_launch"))
+        ncu_share = rec.get("k_blk_time_share")
     except Exception:
         pass
+    roofline = {
+        "bound": "hbm", "kernel": "k_blk (bus-unit block triangular sweeps, 4 of 8 kernels per Alg. 2 batch)",
+        "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+        "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+        "algorithmic_bytes_per_launch": kblk_bytes,
+        "model": "SURVEY.md 8(d) M2 solve-stage share: (3 n_x + n_p) * 8 B per HVP over the 4 k_blk launches "
+                 "of a batch, / mean k_blk launch time (CUDA events, random W, N columns)",
+        "launch_ms": launch_ms, "stage_ms": {k: float(v) for k, v in zip(names, stage[:8])},
+        "batch_ms": batch_ms, "k_blk_share_of_batch": float(seg_ms.sum() / batch_ms) if batch_ms > 0 else None,
+        "k_blk_share_of_batch_ncu": ncu_share,
+        "path_m2_gbs": path_gbs, "path_m2_frac": (path_gbs / peak) if path_gbs else None,
+        "path_model": "M2 (6 n_x + 5 n_p) * 8 B per HVP (SURVEY.md 8(d)) / stage-timed batch (sum of the 8 "
+                      "kernels' event times)",
+        "step_m2_gbs": step_gbs, "step_m2_frac": (step_gbs / peak) if step_gbs else None,
+        "step_model": "M2 bytes of all this rank's columns / ms_per_step (state + refactorization + gradient "
+                      "included in the time, not in the bytes)",
+        "kblk_rw_gbs": rw_gbs, "kblk_rw_frac": (rw_gbs / peak) if rw_gbs else None,
+        "kblk_rw_model": "block rows each launch moves: A_L (n_x - n_sep) N 8 + n_p N 8 (W), "
+                         "A_U / A_Ut / A_Lt 2 (n_x - n_sep) N 8",
+    }
 
     # ---- Newton projection x(p) from a perturbed solution
     x_pert = x + 1e-3 * torch.from_numpy(np.random.default_rng(7).standard_normal(n_x)).to(dev)
@@ -521,11 +652,20 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, spent, cores, det = oracle_time(grid, args.cpu_cols, N)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"oracle setup + {det['cols']} Cartesian columns of {case} (Alg. 2, batch {N}), "
-                         f"extrapolated to all {n_p} columns ({spent:.1f} s CPU); single-threaded BLAS/SuperLU",
-               "full_hessian_s": det["full_hessian_s_extrapolated"]}
+        sc = oracle_single_core(grid, args.cpu_cols, N)
+        cores = host_cores()
+        pool = OraclePool(case, n_p, cores)
+        try:
+            pool.full_hessian(N)                       # warm the workers (imports, first factorization)
+            wall, t_setup_w, _ = pool.full_hessian(N)
+        finally:
+            pool.close()
+        cpu = {"value": n_p / wall, "unit": UNIT, "cores": pool.workers, "host_cores": cores, "kind": "oracle",
+               "sample": f"one real full grad^2 F of {case} ({n_p} Cartesian columns, Alg. 2) by {pool.workers} "
+                         f"single-threaded oracle processes (own setup + SuperLU each), {wall:.2f} s; plus a "
+                         f"single-core sample: setup + {sc['alg2_columns']} columns (Alg. 2, batch {N}) and "
+                         f"{sc['alg1_columns']} columns by Alg. 1",
+               "full_hessian_s": wall, "worker_setup_s": t_setup_w, "single_core": sc}
 
     if rank == 0:
         out = {
@@ -545,16 +685,7 @@ def main():
             "gpu_launches": launches,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": t_e2e.item() * 1e3},
-            "roofline": {"bound": "hbm", "kernel": "k_blk (bus-unit block triangular sweeps, 4 of 8 kernels per batch)",
-                         "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": seg_bytes,
-                         "model": "2 (n_x - n_sep) N 8 B per k_blk launch",
-                         "launch_ms": float(seg_ms.mean()),
-                         "stage_ms": {k: float(v) for k, v in zip(
-                             ["A_L", "B_LU", "A_U", "FoR", "A_Ut", "B_UtLt", "A_Lt", "MulAdd", "total"], stage)},
-                         "path_m2_gbs": path_gbs, "path_m2_frac": (path_gbs / peak) if path_gbs else None,
-                         "path_model": "M2 (6 n_x + 5 n_p) * 8 B per HVP (SURVEY.md 8(d))"},
+            "roofline": roofline,
             "newton": {"ms": float(np.median(newton_ms)) if newton_ms else None, "steps": newton_steps,
                        "resid_inf": newton_res, "error": newton_fail,
                        "max_abs_x_err": newton_err,

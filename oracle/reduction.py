@@ -62,20 +62,45 @@ def operators(grid, x, p, lam, L=None) -> Operators:
     return Operators(J, Gp, Hxx, Hxp, Hpx, Hpp)
 
 
-def hvp_batch(ops: Operators, W, trace: dict | None = None):
-    """Alg. 2, parallel reduction, W of shape [n_p][N]."""
+def hvp_batch(ops: Operators, W, trace: dict | None = None, timers: dict | None = None):
+    """Alg. 2, parallel reduction, W of shape [n_p][N].
+    `timers` (optional, bench.py's per-stage CPU breakdown only) accumulates
+    wall seconds per Alg. 2 stage; it does not change the arithmetic."""
     W = np.asarray(W, dtype=np.float64)
     if W.ndim == 1:
         W = W[:, None]
+    tick = _Ticker(timers)
     B = ops.Gp @ W                                  # SpMul         (PAPER.md:600)
+    tick("SpMul")
     Z = -ops.solve(B)                               # BatchSparseSolve   J Z = -B   (601)
+    tick("SparseSolve")
     Yx = ops.Hxx @ Z + ops.Hxp @ W                  # BatchTensorProjection  (602, Eq. reduction)
     Yp = ops.Hpx @ Z + ops.Hpp @ W
+    tick("TensorProjection")
     Psi = -ops.solve_T(Yx)                          # BatchSparseSolve^T  J^T Psi = -Yx (603)
+    tick("SparseSolveT")
     HW = Yp + ops.Gp.T @ Psi                        # SpMulAdd      (604)
+    tick("SpMulAdd")
     if trace is not None:
         trace.update(B=B, Z=Z, Yx=Yx, Yp=Yp, Psi=Psi)
     return np.asarray(HW)
+
+
+class _Ticker:
+    """Accumulates wall time between calls into a dict (no-op without one)."""
+
+    def __init__(self, timers):
+        import time
+        self.t = timers
+        self.clock = time.perf_counter
+        self.last = self.clock() if timers is not None else 0.0
+
+    def __call__(self, name):
+        if self.t is None:
+            return
+        now = self.clock()
+        self.t[name] = self.t.get(name, 0.0) + (now - self.last)
+        self.last = now
 
 
 def hvp_sequential(ops: Operators, w):

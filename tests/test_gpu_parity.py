@@ -1,9 +1,9 @@
 """GPU parity: the CUDA path (through the C ABI) vs the CPU oracle (-m gpu).
 
-Tolerance (BASELINE.json north_star, R21): per-column max-norm
-relative error <= 1e-9 on Hessian entries (primary); entrywise <= 1e-9 for
-entries >= 1e-4 * max|H| (secondary: both sides carry absolute rounding
-errors ~1e-14 * cond * max|H|, which swamp smaller entries).  Intermediates (g, J-based quantities, Z, Y_x, Psi) use
+Tolerance (BASELINE.json north_star, R21 revised r02): tests/parity.py
+-- per-column max-norm relative error <= 1e-9 (primary); entrywise <= 1e-9 on
+entries >= 1e-4 max|H|, and at SURVEY R21's 1e-6 floor either <= 1e-9 or
+within 4x the oracle's own pivot-order floor.  Intermediates (g, J-based quantities, Z, Y_x, Psi) use
 1e-11 relative to the block's max.  Integer outputs (orderings, sizes) are
 compared exactly.
 """
@@ -13,6 +13,7 @@ import pytest
 import gridgen
 from oracle import powerflow as pf
 from oracle import reduction as red
+from parity import check_hessian
 
 pytestmark = pytest.mark.gpu
 
@@ -33,11 +34,6 @@ def _np(t):
 def col_rel_err(A, B):
     den = np.maximum(np.max(np.abs(B), axis=0), 1e-300)
     return float(np.max(np.max(np.abs(A - B), axis=0) / den))
-
-
-def entry_rel_err(A, B, floor=1e-4):
-    m = np.abs(B) >= floor * np.max(np.abs(B))
-    return float(np.max(np.abs(A - B)[m] / np.abs(B)[m]))
 
 
 def setup(grid):
@@ -107,8 +103,7 @@ def test_full_hessian_parity(solved_case):
     N = {"case9": 5, "case118": 64, "case1354pegase": 256, "case2869pegase": 512}[name]
     H = _np(ctx.full_hessian(N))
     Ho = red.full_hessian(ops, N)
-    assert col_rel_err(H, Ho) <= TOL_H
-    assert entry_rel_err(H, Ho) <= TOL_H
+    check_hessian(H, Ho, f"{name} N={N} (separate calls)", ops, N, red.full_hessian)
     # batch invariance: bitwise identical across N (fixed per-column arithmetic order)
     for N2 in (1, 7, L.n_p):
         assert np.array_equal(_np(ctx.full_hessian(N2)), H), N2

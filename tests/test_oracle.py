@@ -482,3 +482,19 @@ def test_variant_hessian_complex_step(key):
     H = red.reduced_hessian(g, N=16)
     Hcs, _ = pins.cs_reduced_hessian(g)
     assert np.max(np.abs(H - Hcs)) <= 1e-12 * np.max(np.abs(Hcs))
+
+
+def test_oracle_pivot_order_floor():
+    """The oracle's Alg. 2 with two SuperLU column orderings (COLAMD, MMD on
+    A^T + A) agrees per column to rounding: the reference the GPU is held to is
+    stable, and tests/parity.py's 'oracle floor' is a rounding floor, not a
+    second answer."""
+    from parity import col_rel_err, oracle_alt_ordering
+    g = solved("case1354pegase")
+    L = pf.Layout(g)
+    x, p = pf.state_vectors(g, L)
+    _, lam = red.reduced_gradient(g, x, p, L)
+    ops = red.operators(g, x, p, lam, L)
+    H1 = red.full_hessian(ops, 256)
+    H2 = oracle_alt_ordering(ops, 256, red.full_hessian)
+    assert col_rel_err(H2, H1) <= 1e-10
