@@ -25,6 +25,7 @@ struct DSeg {
   const int *__restrict__ dep;       // local row index (local entries) / global permuted row (external)
   const int *__restrict__ ext_off;   // [nseg + 1] blocks: staged separator rows
   const int *__restrict__ ext_rows;
+  const int *__restrict__ dep_seg;   // fwd only: block of each separator row's external dependency
 };
 
 // Bus-unit schedule of one pattern direction (analysis.hpp UnitSweep).
@@ -60,9 +61,16 @@ struct SegParams {
   const double *Sinv, *SinvT;          // dense [ns][ns] inverse of the separator block L_ss U_ss (+ transpose)
   double *Tsep;                        // [ns][ld] separator right-hand sides
   const int *blk_gp_ptr, *blk_gp_loc;  // per block: local rows with G_p entries
-  const double *W;                   // [n_p][ldw]; null with ident_j0 >= 0 (Cartesian block)
+  const double *W;                   // [n_p][ldw]; null for a Cartesian block (icol)
   long long ldw;
-  int ident_j0;
+  // Cartesian batch (full Hessian): column k of the batch is e_{icol[k]} (k < N);
+  // its output goes to position icol[k] - icol_base of the caller's block.
+  // tmask[s * tmask_words + c / 32] bit c % 32: chunk c of block s has a nonzero
+  // right-hand side -G_p W (null: every chunk).  k_batch_plan writes both.
+  const int *icol;
+  int icol_base;
+  const unsigned *tmask;
+  int tmask_words;
   double *HW;
   long long ldhw;
   int transposed;

@@ -940,12 +940,66 @@ __global__ void k_gather_code(int n, const int *__restrict__ src, const double *
 
 __device__ __forceinline__ double load_W(const SegParams &h, int row, int col) {
   if (col >= h.N) return 0.0;
-  if (h.ident_j0 >= 0) return row == h.ident_j0 + col ? 1.0 : 0.0;
+  if (h.icol) return row == __ldg(h.icol + col) ? 1.0 : 0.0;
   return h.W[(long long)row * h.ldw + col];
 }
 
 __device__ __forceinline__ long long hw_index(const SegParams &h, int row, int col) {
-  return h.transposed ? (long long)col * h.ldhw + row : (long long)row * h.ldhw + col;
+  const int c = h.icol ? __ldg(h.icol + col) - h.icol_base : col;
+  return h.transposed ? (long long)c * h.ldhw + row : (long long)row * h.ldhw + c;
+}
+
+// chunk ci (32 columns) of block s has a nonzero right-hand side -G_p W
+__device__ __forceinline__ bool tile_live(const SegParams &h, int s, int ci) {
+  return !h.tmask || ((__ldg(h.tmask + s * h.tmask_words + (ci >> 5)) >> (ci & 31)) & 1u);
+}
+
+// Cartesian batch plan (full Hessian).  For W = I[:, lo:hi],
+// B = G_p W is very sparse: column j touches only the blocks
+// holding rows of G_p's column j (bus j's rows and, for a voltage parameter,
+// its neighbours'), and a block's L sweep (which depends on nothing outside the
+// block) is identically zero for every other column.  The batch's columns are
+// taken in `gorder` order (all p columns sorted by their first touched block,
+// then index), so each block's columns are contiguous and its nonzero L-sweep
+// tiles are one or two 32-column chunks; `mask` records them.  One CTA; the
+// per-column arithmetic does not depend on the order (results are bitwise
+// those of the natural order).
+__global__ void __launch_bounds__(1024) k_batch_plan(int n_p, int lo, int hi, const int *__restrict__ gorder,
+                                                     const int *__restrict__ pcb_ptr, const int *__restrict__ pcb,
+                                                     int nblk, int words, int *cols, unsigned *mask) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < nblk * words; i += blockDim.x) mask[i] = 0u;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n_p; i0 += blockDim.x) {
+    const int i = i0 + tid;
+    const int j = i < n_p ? gorder[i] : -1;
+    const bool in = j >= lo && j < hi;
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    if (in) {
+      const int pos = base + (warp ? wsum[warp - 1] : 0) + __popc(bal & ((1u << lane) - 1u));
+      cols[pos] = j;
+      for (int e = pcb_ptr[j]; e < pcb_ptr[j + 1]; ++e)
+        atomicOr(mask + pcb[e] * words + (pos >> 10), 1u << ((pos >> 5) & 31));
+    }
+    __syncthreads();
+    if (tid == 0) base += wsum[31];
+    __syncthreads();
+  }
 }
 
 constexpr int kSegC = 32;   // columns of the single-RHS (lambda) path
@@ -1235,8 +1289,14 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     const int tk = s_tk;
     if (tk >= ntiles) break;
     const int s = U.blk_order[tk / ngrp], cbeg = (tk % ngrp) * cg, cend = min(nch, cbeg + cg);
+    bool staged = false;
     for (int ci = cbeg; ci < cend; ++ci) {
-    const bool first = ci == cbeg;
+    // Cartesian batch: an L tile whose right-hand side is zero stays zero (not
+    // computed, not stored); the U sweep starts such a tile from zeros
+    const bool live = tile_live(h, s, ci);
+    if (mode == MODE_L && !live) continue;
+    const bool first = !staged;
+    staged = true;
     if (!first) {
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // the previous chunk's stores have read X
       __syncthreads();
@@ -1254,8 +1314,10 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     // block rows by 2D TMA boxes (64, then 8 rows), the rest (< 8 block rows, staged
     // separator rows) by 16-byte cp.async
     const char *tm = reinterpret_cast<const char *>(G == h.Z ? h.tmZ : h.tmP);
-    const int nbig = tm ? nr / kTmaBig : 0, nsmall = tm ? (nr - nbig * kTmaBig) / kTmaSmall : 0;
+    const bool zfill = mode == MODE_U && !live;   // its L result is zero: no block rows to load
+    const int nbig = tm && !zfill ? nr / kTmaBig : 0, nsmall = tm && !zfill ? (nr - nbig * kTmaBig) / kTmaSmall : 0;
     const int rows_tma = mode == MODE_L ? 0 : nbig * kTmaBig + nsmall * kTmaSmall;
+    const int rows_zero = zfill ? nr : 0;
     if (tid == 0) {
       const double *dM = lsw ? h.tL : mode == MODE_U ? h.tU : mode == MODE_UT ? h.tUt : h.tLt;
       const unsigned tx = (first ? 16u * (nu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + 32u * kTopLd * 8 + 128u +
@@ -1287,12 +1349,12 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     }
     {  // X rows: 16-byte cp.async (LSU path; 256 B TMA bulk copies are rate-bound on the TMA unit)
       const int c = tid & 15;
-      for (int a = rows_tma + (tid >> 4); a < nxrows; a += blockDim.x >> 4) {
+      for (int a = rows_tma + rows_zero + (tid >> 4); a < nxrows; a += blockDim.x >> 4) {
         const long long grow = a < nr ? r0 + a : U.ext_rows[x0 + a - nr];
         cp_async16(X + a * kBC + 2 * c, G + grow * h.ld + col0 + 2 * c);
       }
     }
-    if (mode == MODE_L)   // right-hand side -G_p W (SpMul fused): zero, then the G_p rows below
+    if (mode == MODE_L || zfill)   // L: right-hand side -G_p W (SpMul fused): zero, then the G_p rows below
       for (int i = tid; i < nr * (kBC / 2); i += blockDim.x) reinterpret_cast<double2 *>(X)[i] = make_double2(0.0, 0.0);
     asm volatile("cp.async.wait_all;" ::: "memory");
     {  // wait for the copies of this tile
@@ -1378,6 +1440,7 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
   const int q = qb + qoff;
   if (q >= qe) return;
   const bool lu = mode == MODE_LU || mode == MODE_LUX;
+  const bool masked = mode == MODE_LU && h.tmask;   // Cartesian batch: skip block rows of zero L tiles
   double *G = lu ? h.Z : h.P;
   const double *val = lu ? h.vL : h.vUt;
   const int a = h.fwd.order[q];
@@ -1395,7 +1458,8 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
       c[u] = val[e + u];
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = G[(long long)d[u] * h.ld + col];
+    for (int u = 0; u < 8; ++u)
+      x[u] = (!masked || tile_live(h, h.fwd.dep_seg[e + u], blockIdx.y)) ? G[(long long)d[u] * h.ld + col] : 0.0;
     s0 = fma(c[0], x[0], s0);
     s1 = fma(c[1], x[1], s1);
     s2 = fma(c[2], x[2], s2);
@@ -1405,16 +1469,17 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
     s2 = fma(c[6], x[6], s2);
     s3 = fma(c[7], x[7], s3);
   }
+  auto ld_dep = [&](int e1) {
+    return (!masked || tile_live(h, h.fwd.dep_seg[e1], blockIdx.y)) ? G[(long long)h.fwd.dep[e1] * h.ld + col] : 0.0;
+  };
   for (; e + 4 <= ex; e += 4) {
-    const int d0 = h.fwd.dep[e], d1 = h.fwd.dep[e + 1], d2 = h.fwd.dep[e + 2], d3 = h.fwd.dep[e + 3];
-    const double x0 = G[(long long)d0 * h.ld + col], x1 = G[(long long)d1 * h.ld + col];
-    const double x2 = G[(long long)d2 * h.ld + col], x3 = G[(long long)d3 * h.ld + col];
+    const double x0 = ld_dep(e), x1 = ld_dep(e + 1), x2 = ld_dep(e + 2), x3 = ld_dep(e + 3);
     s0 = fma(val[e], x0, s0);
     s1 = fma(val[e + 1], x1, s1);
     s2 = fma(val[e + 2], x2, s2);
     s3 = fma(val[e + 3], x3, s3);
   }
-  for (; e < ex; ++e) s0 = fma(val[e], G[(long long)h.fwd.dep[e] * h.ld + col], s0);
+  for (; e < ex; ++e) s0 = fma(val[e], ld_dep(e), s0);
   h.Tsep[(long long)a * h.ld + col] = v0 - ((s0 + s1) + (s2 + s3));
 }
 
@@ -1901,6 +1966,9 @@ struct rh_ctx {
   struct Workspace {
     double *Z = nullptr, *P = nullptr, *Tsep = nullptr;
     size_t elems = 0, tsep_elems = 0;
+    int *pcols = nullptr;        // Cartesian batch plan: the batch's columns, home-block order
+    unsigned *pmask = nullptr;   // and its nonzero L-tile mask [nblk][words]
+    int plan_ld = 0;
     int *ctr = nullptr;   // k_blk ticket counters of this workspace
   } ws[kNumWs];
   cudaStream_t sti[kNumWs] = {};                        // internal streams of workspaces 1..
@@ -1928,6 +1996,7 @@ struct rh_ctx {
   double4 *fg_scoef, *fg_ometa;
   double *pdiag;   // [n_p] 2 c2 of a Pg parameter's generator, else 0 (grid data)
   int *gpe_off, *gpe_row, *gpe_col, *gpe_src, *gpe_split;
+  int *gorder = nullptr, *pcb_ptr = nullptr, *pcb = nullptr;   // Cartesian batch plans (k_batch_plan)
   double2 *gpe_rec;
   DenseWs dws;                 // tracking Step 2 (dense.cu)
   // CUDA graph of the fused call (rh_reduced_hessian): captured on the second
@@ -2003,6 +2072,8 @@ struct rh_ctx {
       if (w.Z) cudaFree(w.Z);
       if (w.P) cudaFree(w.P);
       if (w.Tsep) cudaFree(w.Tsep);
+      if (w.pcols) cudaFree(w.pcols);
+      if (w.pmask) cudaFree(w.pmask);
       w = Workspace();
     }
     if (e2e_buf) cudaFree(e2e_buf);
@@ -2161,6 +2232,39 @@ int upload(rh_ctx *c) {
     D.dep = d;
   };
   mkseg(c->dfwd, A.fwd);
+  {  // block of every separator external dependency (fwd), for the Cartesian batch mask
+    std::vector<int32_t> ds(std::max<size_t>(1, A.fwd.dep.size()), -1);
+    const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
+    for (int q = qb; q < qe; ++q)
+      for (int e = A.fwd.rptr[q]; e < A.fwd.rext[q]; ++e) ds[e] = A.seg_of[A.fwd.dep[e]];
+    int *d;
+    chk(d = dalloc_copy(ds, P));
+    c->dfwd.dep_seg = d;
+  }
+  {  // Cartesian batch plans: blocks touched by each p column (rows of G_p's column
+     // in a block), and all p columns ordered by their first touched block, then index
+    const int np_ = A.n_p;
+    std::vector<int32_t> ptr(np_ + 1, 0), blk, key(np_), ord(np_);
+    for (int j = 0; j < np_; ++j) {
+      std::vector<int32_t> t;
+      for (int q = A.gpc_ptr[j]; q < A.gpc_ptr[j + 1]; ++q) {
+        const int sg = A.seg_of[A.gpc_row[q]];
+        if (sg < A.nblk) t.push_back(sg);
+      }
+      std::sort(t.begin(), t.end());
+      t.erase(std::unique(t.begin(), t.end()), t.end());
+      key[j] = t.empty() ? A.nblk : t[0];
+      blk.insert(blk.end(), t.begin(), t.end());
+      ptr[j + 1] = (int)blk.size();
+      ord[j] = j;
+    }
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key[a] < key[b]; });
+    if (blk.empty()) blk.push_back(0);
+    if (ord.empty()) ord.push_back(0);
+    chk(c->gorder = dalloc_copy(ord, P));
+    chk(c->pcb_ptr = dalloc_copy(ptr, P));
+    chk(c->pcb = dalloc_copy(blk, P));
+  }
   mkseg(c->dbwd, A.bwd);
   auto mkunit = [&](DUnit &D, const UnitSweep &U, const DSeg &S) {
     D.meta = reinterpret_cast<const int4 *>(dalloc_copy(U.meta, P));
@@ -2359,6 +2463,26 @@ int ensure_ws(rh_ctx *c, int ld, int k = 0) {
   return RH_OK;
 }
 
+// Cartesian batch plan buffers of workspace k for batches of width <= ld
+int ensure_plan(rh_ctx *c, int ld, int k) {
+  auto &w = c->ws[k];
+  if (ld <= w.plan_ld) return RH_OK;
+  c->drop_graph();
+  if (w.pcols) cudaFree(w.pcols);
+  if (w.pmask) cudaFree(w.pmask);
+  w.pcols = nullptr;
+  w.pmask = nullptr;
+  w.plan_ld = 0;
+  const size_t words = (size_t)(ld / 32 + 31) / 32;
+  if (cudaMalloc(&w.pcols, (size_t)ld * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&w.pmask, (size_t)std::max(1, c->A.nblk) * words * sizeof(unsigned)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, RH_E_NOMEM, "plan allocation failed");
+  }
+  w.plan_ld = ld;
+  return RH_OK;
+}
+
 // 2D tensor maps of a [n_x][ld] fp64 buffer for k_blk's block-row boxes
 // (cuTensorMapEncodeTiled through the runtime's driver entry point, no -lcuda);
 // cached per (buffer, ld).  Returns nullptr if unavailable (k_blk then copies rows).
@@ -2533,7 +2657,7 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
 // W == nullptr with ident_j0 >= 0 selects the Cartesian block e_{j0..j0+N-1}.
 // phase: 0 = the whole batch, 1 = only the first block sweep (L, which needs
 // nothing of the separator), 2 = the rest (after a phase-1 launch on workspace wsi)
-int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW, long long ldhw,
+int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW, long long ldhw,
              int transposed, int N, cudaStream_t st, double *Zo = nullptr, double *Yxo = nullptr,
              double *Psio = nullptr, long long ldz = 0, int wsi = 0, int phase = 0) {
   if (N <= 0) return RH_OK;
@@ -2541,6 +2665,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   const int ld = (N + kBC - 1) / kBC * kBC;
   int rc = ensure_ws(c, ld, wsi);
   if (rc) return rc;
+  if (ident_lo >= 0 && (rc = ensure_plan(c, ld, wsi))) return rc;
   SegParams h = make_params(c, wsi);
   const bool timing = c->timing && phase == 0;
   h.N = N;
@@ -2549,7 +2674,18 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_j0, double *HW
   h.tmP = tmap_pair(c, h.P, ld);
   h.W = W;
   h.ldw = ldw;
-  h.ident_j0 = ident_j0;
+  if (ident_lo >= 0) {   // Cartesian batch e_{ident_lo .. ident_lo + N - 1}: columns in home-block order
+    h.icol = c->ws[wsi].pcols;
+    h.icol_base = ident_lo;
+    h.tmask = c->ws[wsi].pmask;
+    h.tmask_words = (ld / 32 + 31) / 32;
+    if (phase != 2) {
+      k_batch_plan<<<1, 1024, 0, st>>>(A.n_p, ident_lo, ident_lo + N, c->gorder, c->pcb_ptr, c->pcb, A.nblk,
+                                       h.tmask_words, c->ws[wsi].pcols, c->ws[wsi].pmask);
+      RH_LAUNCHED(c);
+    }
+    if (getenv("RH_NO_MASK")) h.tmask = nullptr;   // experiment: dense L sweep on the same column order
+  }
   h.HW = HW;
   h.ldhw = ldhw;
   h.transposed = transposed;
