@@ -1237,6 +1237,11 @@ __device__ __forceinline__ void tma2d_g2s(void *dst, const void *map, int c0, in
       "l"(map), "r"(c0), "r"(r0), "r"(smem_u32(mbar))
       : "memory");
 }
+// L2 prefetch of a box (no shared memory, no barrier): the next chunk's block rows
+__device__ __forceinline__ void tma2d_prefetch_l2(const void *map, int c0, int r0) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(r0)
+               : "memory");
+}
 __device__ __forceinline__ void tma2d_s2g(const void *map, int c0, int r0, const void *src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
                "r"(r0), "r"(smem_u32(src))
@@ -1346,6 +1351,12 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
           tma2d_g2s(X + a * kBC, tm + kTmapBytes, col0, r0 + a, &mbar);
         }
       }
+      // the next chunk of this ticket: its block rows into L2 while this chunk sweeps
+      if (tm && mode != MODE_L && ci + 1 < cend && !(h.debug & 4096) && !(mode == MODE_U && !tile_live(h, s, ci + 1))) {
+        const int nb2 = nr / kTmaBig, ns2 = (nr - nb2 * kTmaBig) / kTmaSmall;
+        for (int i = 0; i < nb2; ++i) tma2d_prefetch_l2(tm, col0 + kBC, r0 + i * kTmaBig);
+        for (int i = 0; i < ns2; ++i) tma2d_prefetch_l2(tm + kTmapBytes, col0 + kBC, r0 + nb2 * kTmaBig + i * kTmaSmall);
+      }
     }
     {  // X rows: 16-byte cp.async (LSU path; 256 B TMA bulk copies are rate-bound on the TMA unit)
       const int c = tid & 15;
@@ -1386,7 +1397,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
         prof[warp] = (clock64() - c_c) | ((long long)(st.lvl[warp + 1] - st.lvl[warp]) << 48);
         if (warp == 0) {
           prof[8] = c_b - c_a;
-          prof[9] = c_c - c_b;
+          prof[9] = (c_c - c_b) | ((long long)first << 48);
           prof[10] = c_a;
         }
       }
@@ -2657,6 +2668,7 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
 // W == nullptr with ident_j0 >= 0 selects the Cartesian block e_{j0..j0+N-1}.
 // phase: 0 = the whole batch, 1 = only the first block sweep (L, which needs
 // nothing of the separator), 2 = the rest (after a phase-1 launch on workspace wsi)
+void dbg_mark(cudaStream_t st, const char *label);
 int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW, long long ldhw,
              int transposed, int N, cudaStream_t st, double *Zo = nullptr, double *Yxo = nullptr,
              double *Psio = nullptr, long long ldz = 0, int wsi = 0, int phase = 0) {
@@ -2701,8 +2713,16 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   cudaEvent_t ev[9];
   if (timing)
     for (auto &e : ev) cudaEventCreate(&e);
+  static const char *kMarkNames[kNumWs][9] = {
+      {"w0 start", "w0 A_L done", "w0 B_LU done", "w0 A_U done", "w0 FoR done", "w0 A_Ut done", "w0 B_UtLt done",
+       "w0 A_Lt done", "w0 MulAdd done"},
+      {"w1 start", "w1 A_L done", "w1 B_LU done", "w1 A_U done", "w1 FoR done", "w1 A_Ut done", "w1 B_UtLt done",
+       "w1 A_Lt done", "w1 MulAdd done"},
+      {"w2 start", "w2 A_L done", "w2 B_LU done", "w2 A_U done", "w2 FoR done", "w2 A_Ut done", "w2 B_UtLt done",
+       "w2 A_Lt done", "w2 MulAdd done"}};
   auto mark = [&](int i) {
     if (timing) cudaEventRecord(ev[i], st);
+    if (wsi < kNumWs && (phase != 1 || i <= 1) && (phase != 2 || i >= 1)) dbg_mark(st, kMarkNames[wsi][i]);
   };
   mark(0);
   if (phase != 2) {
@@ -2953,12 +2973,19 @@ void dbg_mark(cudaStream_t st, const char *label) {
 void dbg_report(cudaStream_t st) {
   if (!dbg_on() || g_marks.empty()) return;
   cudaStreamSynchronize(st);
-  float prev = 0.f;
+  cudaDeviceSynchronize();
+  std::vector<std::pair<float, const char *>> tl;
   for (auto &m : g_marks) {
     float t = 0.f;
     cudaEventElapsedTime(&t, g_marks[0].ev, m.ev);
-    fprintf(stderr, "  %-28s %8.3f ms  (+%.3f)\n", m.label, t, t - prev);
-    prev = t;
+    tl.push_back({t, m.label});
+  }
+  std::stable_sort(tl.begin(), tl.end(), [](const std::pair<float, const char *> &a,
+                                            const std::pair<float, const char *> &b) { return a.first < b.first; });
+  float prev = 0.f;
+  for (auto &m : tl) {
+    fprintf(stderr, "  %-28s %8.3f ms  (+%.3f)\n", m.second, m.first, m.first - prev);
+    prev = m.first;
   }
   for (auto &m : g_marks) cudaEventDestroy(m.ev);
   g_marks.clear();
@@ -3639,7 +3666,11 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   // the gradient (and the tape) on its own stream; the batches' separator and U
   // sweeps run meanwhile, each batch waits for the tape right before k_for
   if (!rc) {
-    if (!c->grad_st) RH_CUDA(c, cudaStreamCreateWithFlags(&c->grad_st, cudaStreamNonBlocking));
+    if (!c->grad_st) {   // high priority: its small latency-bound kernels go first when SMs free up
+      int lo = 0, hi = 0;
+      RH_CUDA(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      RH_CUDA(c, cudaStreamCreateWithPriority(&c->grad_st, cudaStreamNonBlocking, getenv("RH_NO_PRIO") ? lo : hi));
+    }
     if (!c->ev_state) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_state, cudaEventDisableTiming));
     if (!c->ev_tape) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_tape, cudaEventDisableTiming));
     RH_CUDA(c, cudaEventRecord(c->ev_state, st));

@@ -31,11 +31,11 @@ def ev_time(fn, reps=10):
     return float(np.median(ts)), float(min(ts))
 
 
-def run(name, N):
+def run(name, N, modes=("mask", "nomask")):
     g = pf.backout_loads(gridgen.make_grid(name))
     out = {}
     Href = None
-    for mode in ("mask", "nomask"):
+    for mode in modes:
         if mode == "nomask":
             os.environ["RH_NO_MASK"] = "1"
         else:
@@ -69,6 +69,14 @@ def run(name, N):
 
 
 if __name__ == "__main__":
-    cases = sys.argv[1:] or ["case118", "case1354pegase", "case2869pegase", "case9241pegase"]
+    args = sys.argv[1:]
+    modes = ("mask", "nomask")
+    if args and args[0] == "--mask-only":
+        modes = ("mask",)
+        args = args[1:]
+    cases = args or ["case118", "case1354pegase", "case2869pegase", "case9241pegase"]
+    tag = os.environ.get("PROBE_TAG", "")
     for c in cases:
-        run(c, gridgen.CONFIG_N.get(c, 256))
+        if tag:
+            print("variant", tag, end=": ")
+        run(c, gridgen.CONFIG_N.get(c, 256), modes)
