@@ -516,6 +516,29 @@ def main():
         dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
     e2e_val = n_p / t_e2e.item()
 
+    # ---- multi-GPU projection on this GPU: one rank's contiguous column shard of a
+    # G-GPU run, timed alone (the replicated state + gradient
+    # included; the all-gather, tens of microseconds over NVLink, is not)
+    shards = {}
+    if world == 1:
+        ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for G in (2, 4, 8):
+            c = -(-n_p // G)
+            Hs = torch.empty((c, n_p), dtype=torch.float64, device=dev)
+            ts = []
+            for rep in range(8):
+                if flush is not None:
+                    flush.fill_(1.0)
+                torch.cuda.synchronize()
+                ev_a.record(stream)
+                ctx.reduced_hessian(x, p, N, j0=0, j1=c, grad=grad, H=Hs, transposed=True)
+                ev_b.record(stream)
+                torch.cuda.synchronize()
+                if rep >= 3:
+                    ts.append(ev_a.elapsed_time(ev_b))
+            shards[str(G)] = {"columns": c, "ms": float(np.median(ts)),
+                              "projected_hvps_per_s": n_p / (float(np.median(ts)) * 1e-3)}
+
     # ---- roofline of the dominant kernel: k_blk, the bus-unit block sweeps
     # (4 of the 8 kernels of an Alg. 2 batch, ~55 % of its time).  Algorithmic
     # bytes = SURVEY.md 8(d)'s M2 share of the two solve stages, per HVP
@@ -532,57 +555,95 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
-    ctx.set_timing(True)
-    stage = np.zeros(9)
-    reps_t = 5
-    for _ in range(reps_t):
-        ctx.hvp(W, HW)
-        stage += ctx.stage_times()
-    ctx.set_timing(False)
-    stage /= reps_t
     names = ["A_L", "B_LU", "A_U", "FoR", "A_Ut", "B_UtLt", "A_Lt", "MulAdd"]
-    seg_ms = stage[[0, 2, 4, 6]]                      # A_L, A_U, A_Ut, A_Lt
     ns = info["sep_rows"]
     m2_hvp = (6 * n_x + 5 * n_p) * 8                  # SURVEY.md 8(d) model M2, whole path
     solve_m2_hvp = (3 * n_x + n_p) * 8                # its solve-stage share
+    for_m2_hvp = 2 * (n_x + n_p) * 8                  # its FoR share: reads z, w; writes y_x, y_p
     kblk_bytes = solve_m2_hvp * N / 4.0
-    launch_ms = float(seg_ms.mean())
-    achieved = kblk_bytes / (launch_ms * 1e-3) / 1e9 if launch_ms > 0 else None
-    batch_ms = float(stage[:8].sum())                 # the 8 stages back to back (events per kernel)
-    path_gbs = m2_hvp * N / (batch_ms * 1e-3) / 1e9 if batch_ms > 0 else None
+
+    def stage_roofline(kind):
+        """Per-stage device times of one Alg. 2 batch of width N (CUDA events the library
+        records around each kernel, on the stream they run on): kind 'cartesian' = the
+        full Hessian's first N columns (what the timed step runs), 'random' = W ~ N(0, 1)."""
+        Hc = torch.empty((n_p, min(N, n_p)), dtype=torch.float64, device=dev)
+        ctx.set_timing(True)
+        st_ = np.zeros(9)
+        reps_t = 5
+        for _ in range(reps_t):
+            if flush is not None:
+                flush.fill_(1.0)
+            if kind == "cartesian":
+                ctx.hessian_columns(0, min(N, n_p), N, H=Hc)
+            else:
+                ctx.hvp(W, HW)
+            st_ += ctx.stage_times()
+        ctx.set_timing(False)
+        st_ /= reps_t
+        seg = st_[[0, 2, 4, 6]]                        # A_L, A_U, A_Ut, A_Lt
+        lm = float(seg.mean())
+        ach = kblk_bytes / (lm * 1e-3) / 1e9 if lm > 0 else None
+        bm = float(st_[:8].sum())
+        cols = min(N, n_p)
+        pg = m2_hvp * cols / (bm * 1e-3) / 1e9 if bm > 0 else None
+        fg = for_m2_hvp * cols / (st_[3] * 1e-3) / 1e9 if st_[3] > 0 else None
+        return {"kind": kind, "achieved": ach, "frac": (ach / peak) if ach else None, "launch_ms": lm,
+                "stage_ms": {k: float(v) for k, v in zip(names, st_[:8])}, "batch_ms": bm,
+                "k_blk_share_of_batch": float(seg.sum() / bm) if bm > 0 else None,
+                "path_m2_gbs": pg, "path_m2_frac": (pg / peak) if pg else None,
+                "for_m2_gbs": fg, "for_m2_frac": (fg / peak) if fg else None, "columns": cols,
+                "launch_ms_each": [float(v) for v in seg]}
+
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    rl_cart = stage_roofline("cartesian")
+    rl_rand = stage_roofline("random")
     cols_local = j1 - j0
     step_gbs = m2_hvp * cols_local / (ms_step * 1e-3) / 1e9 if ms_step > 0 else None
+    seg_ms = np.array(rl_rand["launch_ms_each"])
     # secondary, per-launch read + write of the block rows each k_blk launch moves
     # (A_L reads W and G_p only and writes Z's block rows; the others read and write them)
     rw_bytes = np.array([(n_x - ns) * N * 8 + n_p * N * 8] + [2.0 * (n_x - ns) * N * 8] * 3)
     rw_gbs = float(np.mean(rw_bytes / (seg_ms * 1e-3) / 1e9)) if np.all(seg_ms > 0) else None
-    traffic, ncu_share = None, None
+    traffic, ncu_share, ncu_rec = None, None, {}
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-        rec = prof.get(f"{case}:N={N}", {})
-        traffic = rec.get("k_blk_dram_bytes_per_launch", rec.get("dram_bytes_per_launch"))
-        ncu_share = rec.get("k_blk_time_share")
+        ncu_rec = prof.get(f"{case}:N={N}:cartesian", {})
+        traffic = ncu_rec.get("k_blk_dram_bytes_per_launch")
+        ncu_share = ncu_rec.get("k_blk_time_share")
     except Exception:
         pass
+    achieved = rl_cart["achieved"]
     roofline = {
         "bound": "hbm", "kernel": "k_blk (bus-unit block triangular sweeps, 4 of 8 kernels per Alg. 2 batch)",
         "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
         "algorithmic_bytes_per_launch": kblk_bytes,
         "model": "SURVEY.md 8(d) M2 solve-stage share: (3 n_x + n_p) * 8 B per HVP over the 4 k_blk launches "
-                 "of a batch, / mean k_blk launch time (CUDA events, random W, N columns)",
-        "launch_ms": launch_ms, "stage_ms": {k: float(v) for k, v in zip(names, stage[:8])},
-        "batch_ms": batch_ms, "k_blk_share_of_batch": float(seg_ms.sum() / batch_ms) if batch_ms > 0 else None,
-        "k_blk_share_of_batch_ncu": ncu_share,
-        "path_m2_gbs": path_gbs, "path_m2_frac": (path_gbs / peak) if path_gbs else None,
-        "path_model": "M2 (6 n_x + 5 n_p) * 8 B per HVP (SURVEY.md 8(d)) / stage-timed batch (sum of the 8 "
+                 "of a batch, / mean k_blk launch time of a Cartesian batch (the full Hessian's first N columns, "
+                 "the batches the timed step runs; CUDA events, L2 flushed)",
+        "launch_ms": rl_cart["launch_ms"], "stage_ms": rl_cart["stage_ms"], "batch_ms": rl_cart["batch_ms"],
+        "k_blk_share_of_batch": rl_cart["k_blk_share_of_batch"], "k_blk_share_of_batch_ncu": ncu_share,
+        "traffic_over_algorithmic": (traffic / kblk_bytes) if traffic else None,
+        "path_m2_gbs": rl_cart["path_m2_gbs"], "path_m2_frac": rl_cart["path_m2_frac"],
+        "path_model": "M2 (6 n_x + 5 n_p) * 8 B per HVP (SURVEY.md 8(d)) / stage-timed batch (sum of its "
                       "kernels' event times)",
+        "for_m2_frac": rl_cart["for_m2_frac"],
+        "for_model": "k_for's M2 share 2 (n_x + n_p) * 8 B per HVP / its event time",
         "step_m2_gbs": step_gbs, "step_m2_frac": (step_gbs / peak) if step_gbs else None,
         "step_model": "M2 bytes of all this rank's columns / ms_per_step (state + refactorization + gradient "
                       "included in the time, not in the bytes)",
+        "random_W": {k: v for k, v in rl_rand.items() if k != "launch_ms_each"},
         "kblk_rw_gbs": rw_gbs, "kblk_rw_frac": (rw_gbs / peak) if rw_gbs else None,
-        "kblk_rw_model": "block rows each launch moves: A_L (n_x - n_sep) N 8 + n_p N 8 (W), "
+        "kblk_rw_model": "random W: block rows each launch moves: A_L (n_x - n_sep) N 8 + n_p N 8 (W), "
                          "A_U / A_Ut / A_Lt 2 (n_x - n_sep) N 8",
+        "ncu": {k: ncu_rec.get(k) for k in ("round", "batch_us_serialized", "k_blk_dram_over_m2", "stages")}
+        if ncu_rec else None,
     }
 
     # ---- Newton projection x(p) (SURVEY.md 8(f) NEXT-1) from a perturbed solution
@@ -690,6 +751,10 @@ def main():
                        "resid_inf": newton_res, "error": newton_fail,
                        "max_abs_x_err": newton_err,
                        "start": "solved x + 1e-3 N(0,1) (seed 7; from 1e-2 the oracle diverges too on case9241); tol 1e-11, 2 extra steps (oracle rule); host wall clock incl. one max|dx| readback per step"},
+            "shard_projection": {"per_rank": shards,
+                                 "note": "one rank's shard [0, ceil(n_p/G)) of the G-GPU column split, fused call "
+                                         "(state + refactorization + gradient replicated), timed alone on this GPU; "
+                                         "no all-gather"} if shards else None,
             "tracking": tracking,
             "jacobian_colored": jac_colored,
             "cpu_baseline": cpu,

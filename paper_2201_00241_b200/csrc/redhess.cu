@@ -1710,20 +1710,18 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     }
     __syncthreads();
   }
-  for (int i = warp; i < nout; i += nw) {   // warp per output bus, lane per column, all from shared memory
-    const int4 d = s_dst[i];
-    const double4 mt = s_meta[i];
-    const double dth_b = fsm[i * 64 + lane], dv_b = fsm[i * 64 + 32 + lane];
-    double yth = 0.0, yv = mt.x * dv_b;
-    for (int q = d.z; q < d.z + d.w; ++q) {
-      // canonical slot coefficients (k_for_tape): D = dth_b - dth_o,
-      // yth += K D + c2 dv_b + c3 dv_o,  yv += c2 D + m dv_o
-      const double4 k = s_coef[q];
-      const int o = s_oe[q] >> 1;
-      const double D = dth_b - fsm[o * 64 + lane], dv_o = fsm[o * 64 + 32 + lane];
-      yth = fma(k.x, D, fma(k.y, dv_b, fma(k.z, dv_o, yth)));
-      yv = fma(k.y, D, fma(k.w, dv_o, yv));
-    }
+  // warp per output bus, lane per column, all from shared memory; two buses at a
+  // time (independent FMA chains, same per-bus order as one at a time)
+  auto slot = [&](int q, double dth_b, double dv_b, double &yth, double &yv) {
+    // canonical slot coefficients (k_for_tape): D = dth_b - dth_o,
+    // yth += K D + c2 dv_b + c3 dv_o,  yv += c2 D + m dv_o
+    const double4 k = s_coef[q];
+    const int o = s_oe[q] >> 1;
+    const double D = dth_b - fsm[o * 64 + lane], dv_o = fsm[o * 64 + 32 + lane];
+    yth = fma(k.x, D, fma(k.y, dv_b, fma(k.z, dv_o, yth)));
+    yv = fma(k.y, D, fma(k.w, dv_o, yv));
+  };
+  auto finish = [&](const int4 d, const double4 mt, double yth, double yv) {
     if (mt.y != 0.0 || mt.z != 0.0) {
       yth += sref[lane] * mt.y;
       yv += sref[lane] * mt.z;
@@ -1734,6 +1732,25 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     } else if (d.y <= -2 && col < h.N) {
       h.HW[hw_index(h, -(d.y + 2), col)] = yv;
     }
+  };
+  for (int i = warp; i < nout; i += 2 * nw) {
+    const int i2 = i + nw;
+    const bool two = i2 < nout;
+    const int4 d = s_dst[i], d2 = two ? s_dst[i2] : make_int4(-1, -1, 0, 0);
+    const double4 mt = s_meta[i], mt2 = two ? s_meta[i2] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const double dth_b = fsm[i * 64 + lane], dv_b = fsm[i * 64 + 32 + lane];
+    const double dth_b2 = two ? fsm[i2 * 64 + lane] : 0.0, dv_b2 = two ? fsm[i2 * 64 + 32 + lane] : 0.0;
+    double yth = 0.0, yv = mt.x * dv_b, yth2 = 0.0, yv2 = mt2.x * dv_b2;
+    const int n1 = d.w, n2 = d2.w, nmin = min(n1, n2);
+    int t = 0;
+    for (; t < nmin; ++t) {
+      slot(d.z + t, dth_b, dv_b, yth, yv);
+      slot(d2.z + t, dth_b2, dv_b2, yth2, yv2);
+    }
+    for (; t < n1; ++t) slot(d.z + t, dth_b, dv_b, yth, yv);
+    for (; t < n2; ++t) slot(d2.z + t, dth_b2, dv_b2, yth2, yv2);
+    finish(d, mt, yth, yv);
+    if (two) finish(d2, mt2, yth2, yv2);
   }
 }
 
@@ -1777,12 +1794,23 @@ __global__ void __launch_bounds__(kThreads, 4) k_muladd(SegParams h) {
     col[u] = (ch0 + u) * 32 + lane;
     acc[u] = col[u] < h.N ? (pg ? c2x2 * load_W(h, cp, col[u]) : h.HW[hw_index(h, cp, col[u])]) : 0.0;
   }
-  for (int q = q0; q < q1; ++q) {
-    const double g = h.gpc_val[q];
-    const double *pr = h.P + (long long)h.gpc_row[q] * h.ld;
+  // four G_p entries at a time: all their Psi loads in flight, then the FMAs in entry order
+  for (int q = q0; q < q1; q += 4) {
+    double g[4], xv[4][FCH];
 #pragma unroll
-    for (int u = 0; u < FCH; ++u)
-      if (col[u] < h.ld) acc[u] = fma(g, pr[col[u]], acc[u]);
+    for (int k = 0; k < 4; ++k) {
+      const bool in = q + k < q1;
+      g[k] = in ? h.gpc_val[q + k] : 0.0;
+      const double *pr = h.P + (long long)(in ? h.gpc_row[q + k] : 0) * h.ld;
+#pragma unroll
+      for (int u = 0; u < FCH; ++u) xv[k][u] = (in && col[u] < h.ld) ? pr[col[u]] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (q + k < q1)
+#pragma unroll
+        for (int u = 0; u < FCH; ++u)
+          if (col[u] < h.ld) acc[u] = fma(g[k], xv[k][u], acc[u]);
   }
 #pragma unroll
   for (int u = 0; u < FCH; ++u)
@@ -2042,6 +2070,8 @@ struct rh_ctx {
   // workspace and ticket counters; batches wait for the tape before k_for
   cudaStream_t grad_st = nullptr;
   cudaEvent_t ev_state = nullptr, ev_tape = nullptr;
+  cudaEvent_t ev_vl = nullptr;   // separator rows' L / U^T values ready (after R_B1)
+  bool early_gathered = false;   // the fused call's early batches also formed their separator rhs
   double *grad_tsep = nullptr;
   int *grad_ctr = nullptr;
   cudaEvent_t tape_wait = nullptr;   // set while a fused call enqueues its batches
@@ -2068,6 +2098,7 @@ struct rh_ctx {
     if (grad_st) cudaStreamDestroy(grad_st), grad_st = nullptr;
     if (ev_state) cudaEventDestroy(ev_state), ev_state = nullptr;
     if (ev_tape) cudaEventDestroy(ev_tape), ev_tape = nullptr;
+    if (ev_vl) cudaEventDestroy(ev_vl), ev_vl = nullptr;
     if (grad_tsep) cudaFree(grad_tsep), grad_tsep = nullptr;
     if (grad_ctr) cudaFree(grad_ctr), grad_ctr = nullptr;
     tape_wait = nullptr;
@@ -2667,7 +2698,9 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
 // synchronization (cf. the two explicit syncs of PAPER.md:798-805).
 // W == nullptr with ident_j0 >= 0 selects the Cartesian block e_{j0..j0+N-1}.
 // phase: 0 = the whole batch, 1 = only the first block sweep (L, which needs
-// nothing of the separator), 2 = the rest (after a phase-1 launch on workspace wsi)
+// nothing of the separator), 2 = the rest (after a phase-1 launch on workspace wsi),
+// 3 = only the separator right-hand sides (needs the separator rows' L values, not
+// S^-1; after phase 1), 4 = the rest after phases 1 and 3
 void dbg_mark(cudaStream_t st, const char *label);
 int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW, long long ldhw,
              int transposed, int N, cudaStream_t st, double *Zo = nullptr, double *Yxo = nullptr,
@@ -2691,7 +2724,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
     h.icol_base = ident_lo;
     h.tmask = c->ws[wsi].pmask;
     h.tmask_words = (ld / 32 + 31) / 32;
-    if (phase != 2) {
+    if (phase == 0 || phase == 1) {
       k_batch_plan<<<1, 1024, 0, st>>>(A.n_p, ident_lo, ident_lo + N, c->gorder, c->pcb_ptr, c->pcb, A.nblk,
                                        h.tmask_words, c->ws[wsi].pcols, c->ws[wsi].pmask);
       RH_LAUNCHED(c);
@@ -2722,21 +2755,25 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
        "w2 A_Lt done", "w2 MulAdd done"}};
   auto mark = [&](int i) {
     if (timing) cudaEventRecord(ev[i], st);
-    if (wsi < kNumWs && (phase != 1 || i <= 1) && (phase != 2 || i >= 1)) dbg_mark(st, kMarkNames[wsi][i]);
+    if (wsi < kNumWs && (phase != 1 || i <= 1) && (phase < 2 || i >= 1)) dbg_mark(st, kMarkNames[wsi][i]);
   };
-  mark(0);
-  if (phase != 2) {
+  if (phase <= 1) {
+    mark(0);
     k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_L);
     RH_LAUNCHED(c);
   }
   if (phase == 1) return RH_OK;
-  mark(1);
+  if (phase != 3) mark(1);
   if (has_sep) {
-    k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_LU);
-    RH_LAUNCHED(c);
+    if (phase != 4) {
+      k_sep_gather<<<gSg, kThreads, 0, st>>>(h, MODE_LU);
+      RH_LAUNCHED(c);
+    }
+    if (phase == 3) return RH_OK;
     k_sep_gemm<<<gSm, GTHREADS, gemm_smem_bytes(), st>>>(h, MODE_LU);
     RH_LAUNCHED(c);
   }
+  if (phase == 3) return RH_OK;
   mark(2);
   k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
   RH_LAUNCHED(c);
@@ -3106,7 +3143,7 @@ bool graph_run(rh_ctx *c, int slot, const rh_ctx::GraphKey &key, cudaStream_t st
 
 // defer_check: do not read the pivot flag (the caller does, after enqueuing more work)
 int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cudaStream_t side,
-               const std::function<int(cudaStream_t)> &early, bool defer_check = false) {
+               const std::function<int(cudaStream_t, int)> &early, bool defer_check = false) {
   if (!c || !x || !p) return fail(c, RH_E_ARG, "null argument");
   if (c->host_only) return fail(c, RH_E_NODEV, "host-only context (device = -1)");
   if (!c->loaded) return fail(c, RH_E_ORDER, "no grid loaded");
@@ -3252,13 +3289,30 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   if (early) {
     if (!c->ev_derived) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_derived, cudaEventDisableTiming));
     RH_CUDA(c, cudaEventRecord(c->ev_derived, sb));   // what st needs from the side stream
-    const int rc = early(sb);
+    const int rc = early(sb, 1);
     if (rc) return rc;
   }
   if (A.sep_rows > 0) {
     dbg_mark(st, "side stream forked");
     k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, 0, st>>>(f);
     RH_LAUNCHED(c);
+    {  // separator rows' entries of the forward pattern (k_sep_gather): L and U^T values
+       // (final after R_B1; the Gauss-Jordan inverse below does not touch F)
+      const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
+      const int e0 = A.fwd.rptr[qb], ne = A.fwd.rptr[qe] - e0;
+      if (ne > 0) {
+        k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_a + e0, c->F_val, c->vL + e0);
+        RH_LAUNCHED(c);
+        k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_b + e0, c->F_val, c->vUt + e0);
+        RH_LAUNCHED(c);
+      }
+    }
+    if (early && side) {   // the early batches' separator right-hand sides need these values, not S^-1
+      if (!c->ev_vl) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_vl, cudaEventDisableTiming));
+      RH_CUDA(c, cudaEventRecord(c->ev_vl, st));
+      RH_CUDA(c, cudaStreamWaitEvent(sb, c->ev_vl, 0));
+      if (int rc = early(sb, 2)) return rc;
+    }
     // dense Schur complement of the separator, inverted by blocked Gauss-Jordan
     const int ns = A.sep_rows;
     RH_CUDA(c, cudaMemsetAsync(c->Sinv, 0, sizeof(double) * (size_t)ns * ns, st));
@@ -3301,16 +3355,6 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     dbg_mark(st, "k_sep_inverse");
     k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
     RH_LAUNCHED(c);
-  }
-  {  // separator rows' entries of the forward pattern (k_sep_gather): L and U^T values
-    const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
-    const int e0 = A.fwd.rptr[qb], ne = A.fwd.rptr[qe] - e0;
-    if (ne > 0) {
-      k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_a + e0, c->F_val, c->vL + e0);
-      RH_LAUNCHED(c);
-      k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_b + e0, c->F_val, c->vUt + e0);
-      RH_LAUNCHED(c);
-    }
   }
   if (c->nrec_b > 0) {   // L^T records: block rows' L entries below them include L_sb (R_B1)
     k_gather_code<<<nblk(2LL * c->nrec_b), kThreads, 0, st>>>(2 * c->nrec_b, c->ub_src_b, c->F_val,
@@ -3582,7 +3626,7 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
     cudaStream_t sb = k ? c->sti[k] : st;
     if (b < early) RH_CUDA(c, cudaStreamWaitEvent(sb, c->ev_early[b], 0));   // its L sweep (side stream)
     int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0, k,
-                      b < early ? 2 : 0);
+                      b < early ? (c->early_gathered ? 4 : 2) : 0);
     if (rc) return rc;
     if (Hhost) {
       RH_CUDA(c, cudaEventRecord(c->ev_cp, sb));
@@ -3647,17 +3691,23 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   for (int k = 0; k < early; ++k)   // allocate before anything is enqueued
     if (int rc = ensure_ws(c, ld, k)) return rc;
   if (!c->sti[1]) RH_CUDA(c, cudaStreamCreateWithFlags(&c->sti[1], cudaStreamNonBlocking));
-  auto first_sweeps = [&](cudaStream_t sb) -> int {
+  // stage 1 (as soon as the block factors exist): plan + L sweep of the first
+  // batches; stage 2 (as soon as the separator rows' L values exist, while S^-1 is
+  // still being computed): their separator right-hand sides
+  c->early_gathered = false;
+  auto first_sweeps = [&](cudaStream_t sb, int stage) -> int {
+    if (stage == 2 && getenv("RH_NO_EARLY_GATHER")) return RH_OK;
     for (int b = 0; b < early; ++b) {
       int a0, a1;
       batch_range(ncols, nb, b, a0, a1, N, Hhost != nullptr);
       double *out = transposed ? H + (long long)a0 * ldh : H + a0;
       if (int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0,
-                            b, 1))
+                            b, stage == 1 ? 1 : 3))
         return rc;
       if (!c->ev_early[b]) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_early[b], cudaEventDisableTiming));
       RH_CUDA(c, cudaEventRecord(c->ev_early[b], sb));
     }
+    if (stage == 2) c->early_gathered = true;
     return RH_OK;
   };
   // everything is enqueued before the one host sync (the pivot flag, read last)
