@@ -75,6 +75,7 @@ struct SegParams {
   long long ldhw;
   int transposed;
   double *Z, *P;                     // [n_x][ld] work blocks (Z, then -Y_x -> Psi)
+  double *Yp;                        // [n_p][ld] Y_p of the voltage parameters (k_for -> k_muladd)
   const int *gp_rptr, *gp_col;       // G_p CSR over permuted rows
   const double *gp_val;
   const int *gpc_ptr, *gpc_row;      // G_p CSC (p columns), rows permuted

@@ -1497,80 +1497,88 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
 // C[m][n] = sum_k M[m][k] T[k][n] written to the separator slab of Z / P
 // (rows sep_off + m, contiguous in segment order): the one dense contraction
 // of the path, on the fp64 tensor cores (DMMA, mma.sync m8n8k4).  64 x 64
-// output tile per CTA, 8 warps of 32 x 16 (4 x 2 mma tiles), k in tiles of 16
-// staged in shared memory (double-buffered, next tile prefetched into
-// registers).  Fixed k order: deterministic.
-constexpr int GBM = 64, GBN = 64, GBK = 16, GGRP = 2, GTHREADS = 256 * GGRP;
-// in-CTA split-K: GGRP groups of 8 warps take alternate k tiles (more DMMA
-// chains in flight per SM); the partial tiles are added in fixed group order
-constexpr size_t gemm_smem_bytes() {
-  return sizeof(double) * GGRP * 2 * (GBM * (GBK + 1) + GBK * (GBN + 1));
+// output tile per CTA, 8 warps of 32 x 16 (4 x 2 mma tiles) per group, k in
+// tiles of 16 through a GSTAGES-deep cp.async pipeline.  Both operand tiles
+// are k-major with rows padded to 72 doubles, so every fragment load (lane
+// (g, t) reads row t, column g) hits 16 distinct banks per half-warp: no bank
+// conflicts.  The k-major A tile is a row range of the transposed operator
+// (S^-T for S^-1 and vice versa).  In-CTA split-K: GGRP groups of 8 warps take
+// alternate k tiles; the partial tiles are added in fixed group order
+// (deterministic).
+constexpr int GBM = 64, GBN = 64, GBK = 16, GGRP = 2, GTHREADS = 256 * GGRP, GSTAGES = 3, GLD = 72;
+constexpr int GTILE = GBK * GLD;   // doubles per operand tile per stage
+constexpr size_t gemm_smem_bytes() { return sizeof(double) * GGRP * GSTAGES * 2 * GTILE; }
+__device__ __forceinline__ void cp_async8z(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async16z(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
 __global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
   extern __shared__ __align__(16) double gsm[];
   const int grp = threadIdx.x >> 8;
-  typedef double ATile[GBM][GBK + 1];
-  typedef double BTile[GBK][GBN + 1];
-  ATile *As = reinterpret_cast<ATile *>(gsm + grp * 2 * (GBM * (GBK + 1) + GBK * (GBN + 1)));
-  BTile *Bs = reinterpret_cast<BTile *>(reinterpret_cast<double *>(As) + 2 * GBM * (GBK + 1));
+  double *As = gsm + grp * GSTAGES * 2 * GTILE;   // [stage][k][m]
+  double *Bs = As + GSTAGES * GTILE;              // [stage][k][n]
   const int ns = h.ns, ld = h.ld;
-  const double *M = mode == MODE_LU ? h.Sinv : h.SinvT;
+  const double *MT = mode == MODE_LU ? h.SinvT : h.Sinv;   // A[m][k] = MT[k][m]
   double *G = mode == MODE_LU ? h.Z : h.P;
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
   const int tid = threadIdx.x & 255, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 2, wn = warp & 3;   // warp tile rows wm*32.., cols wn*16..
   const int gid = lane >> 2, tig = lane & 3;
+  const int nkt = (ns + GBK - 1) / GBK;
+  const int myt = nkt > grp ? (nkt - grp + GGRP - 1) / GGRP : 0;   // k tiles grp, grp + GGRP, ...
+  auto issue = [&](int t) {
+    const int st = t % GSTAGES, k0 = (grp + t * GGRP) * GBK;
+    double *a = As + st * GTILE, *b = Bs + st * GTILE;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {   // A: 16 k x 64 m doubles, 8-byte copies (ns is odd)
+      const int idx = tid + r * 256, kk = idx >> 6, mm = idx & 63;
+      const int gk = k0 + kk, gm = m0 + mm;
+      const bool v = gk < ns && gm < ns;
+      cp_async8z(a + kk * GLD + mm, MT + (v ? (long long)gk * ns + gm : 0), v);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {   // B: 16 k x 64 n doubles, 16-byte copies (ld is a multiple of 32)
+      const int idx = tid + r * 256, kk = idx >> 5, nn = (idx & 31) * 2;
+      const int gk = k0 + kk, gn = n0 + nn;
+      const bool v = gk < ns && gn < ld;
+      cp_async16z(b + kk * GLD + nn, h.Tsep + (v ? (long long)gk * ld + gn : 0), v);
+    }
+  };
   double acc[4][2][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  double ra[4], rb[4];
-  auto load = [&](int k0) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int idx = tid + r * 256;            // 1024 = 64 (m) x 16 (k), k fastest
-      const int mm = idx / GBK, kk = idx % GBK;
-      ra[r] = (m0 + mm < ns && k0 + kk < ns) ? __ldg(M + (long long)(m0 + mm) * ns + k0 + kk) : 0.0;
-      const int kb = idx / GBN, nn = idx % GBN;  // 1024 = 16 (k) x 64 (n), n fastest
-      rb[r] = (k0 + kb < ns && n0 + nn < ld) ? h.Tsep[(long long)(k0 + kb) * ld + n0 + nn] : 0.0;
-    }
-  };
-  auto store = [&](int buf) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int idx = tid + r * 256;
-      As[buf][idx / GBK][idx % GBK] = ra[r];
-      Bs[buf][idx / GBN][idx % GBN] = rb[r];
-    }
-  };
   auto gsync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + grp) : "memory"); };
-  const int kstep = GBK * GGRP;
-  int buf = 0;
-  if (grp * GBK < ns) {
-    load(grp * GBK);
-    store(0);
+#pragma unroll
+  for (int t = 0; t < GSTAGES - 1; ++t) {
+    if (t < myt) issue(t);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  gsync();
-  for (int k0 = grp * GBK; k0 < ns; k0 += kstep, buf ^= 1) {
-    if (k0 + kstep < ns) load(k0 + kstep);
-    double a[GBK / 4][4], bv[GBK / 4][2];   // all fragments of the k tile, then 32 DMMA
+  for (int t = 0; t < myt; ++t) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(GSTAGES - 2) : "memory");
+    gsync();   // tile t landed for every thread; everyone is done with tile t - 1
+    if (t + GSTAGES - 1 < myt) issue(t + GSTAGES - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const double *a = As + (t % GSTAGES) * GTILE, *b = Bs + (t % GSTAGES) * GTILE;
 #pragma unroll
     for (int q = 0; q < GBK / 4; ++q) {
+      double af[4], bf[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[q][i] = As[buf][wm * 32 + i * 8 + gid][4 * q + tig];
+      for (int i = 0; i < 4; ++i) af[i] = a[(4 * q + tig) * GLD + wm * 32 + i * 8 + gid];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bv[q][j] = Bs[buf][4 * q + tig][wn * 16 + j * 8 + gid];
-    }
-#pragma unroll
-    for (int q = 0; q < GBK / 4; ++q)
+      for (int j = 0; j < 2; ++j) bf[j] = b[(4 * q + tig) * GLD + wn * 16 + j * 8 + gid];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[q][i], bv[q][j]);
-    if (k0 + kstep < ns) store(buf ^ 1);
-    gsync();
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   // fixed-order reduction: group 1 parks its partial tile, group 0 adds and stores
   __syncthreads();
   double(*Red)[GBN + 2] = reinterpret_cast<double(*)[GBN + 2]>(gsm);
@@ -1654,6 +1662,10 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
   int *s_oe = reinterpret_cast<int *>(s_dst + h.fg_maxout);
   int2 *s_fill = reinterpret_cast<int2 *>(s_oe + h.fg_maxslots);   // [2 maxloc]
   __shared__ int s_nfill;
+  // timing experiment (RH_DEBUG & 8192): per CTA [start, staged+filled, copies landed, end]
+  long long *prof = ((h.debug & 8192) && h.dbg && g * gridDim.y + blockIdx.y < 16384)
+                        ? h.dbg + 4LL * (g * gridDim.y + blockIdx.y) : nullptr;
+  if (prof && tid == 0) prof[0] = clock64();
   if (tid == 0) {
     s_nfill = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
@@ -1689,6 +1701,7 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     for (int u = 0; u < 4; ++u)
       if (f + u < s_nfill) fsm[s_fill[f + u].x + lane] = v[u];
   }
+  if (prof && tid == 0) prof[1] = clock64();
   {
     unsigned done = 0;
     while (!done)
@@ -1698,6 +1711,7 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
                    : "memory");
   }
   __syncthreads();
+  if (prof && tid == 0) prof[2] = clock64();
   const int r0 = h.fg_ref[g], r1 = h.fg_ref[g + 1];
   if (r0 < r1) {   // REF objective rank-1 term f''(Pg_ref) (grad P_ref . delta) (R22), once per tile
     if (warp == 0) {
@@ -1729,8 +1743,8 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     if (d.x >= 0) h.P[(long long)d.x * h.ld + col] = -yth;
     if (d.y >= 0) {
       h.P[(long long)d.y * h.ld + col] = -yv;
-    } else if (d.y <= -2 && col < h.N) {
-      h.HW[hw_index(h, -(d.y + 2), col)] = yv;
+    } else if (d.y <= -2) {
+      h.Yp[(long long)(-(d.y + 2)) * h.ld + col] = yv;
     }
   };
   for (int i = warp; i < nout; i += 2 * nw) {
@@ -1751,6 +1765,10 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     for (; t < n2; ++t) slot(d2.z + t, dth_b2, dv_b2, yth2, yv2);
     finish(d, mt, yth, yv);
     if (two) finish(d2, mt2, yth2, yv2);
+  }
+  if (prof) {
+    __syncthreads();
+    if (tid == 0) prof[3] = clock64();
   }
 }
 
@@ -1774,47 +1792,48 @@ __global__ void k_for_tape(int nslots, int nout, const int2 *slots, const int *o
   }
 }
 
-constexpr int FCH = 2;   // column chunks of 32 per warp in k_muladd
-
-// SpMulAdd HW = Y_p + G_p^T Psi: one warp per p row, lanes over
-// columns, FCH chunks per warp
-__global__ void __launch_bounds__(kThreads, 4) k_muladd(SegParams h) {
-  const int lane = threadIdx.x & 31;
-  const int cp = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
-  if (cp >= h.n_p) return;
-  const int q0 = h.gpc_ptr[cp], q1 = h.gpc_ptr[cp + 1];
-  const int ch0 = blockIdx.y * FCH;
-  double acc[FCH];
-  int col[FCH];
+// SpMulAdd HW = Y_p + G_p^T Psi: a CTA = 32 p rows x 32 columns,
+// warp per p row (4 each), lane per column, the G_p entries' Psi loads four at a
+// time in flight; the tile then leaves through shared memory so that the
+// transposed layout (H^T rows, the multi-GPU slabs) is written 256 B per warp
+// store instead of one 8-byte sector per lane.
+__global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
+  __shared__ double T[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cp0 = blockIdx.x * 32, col = blockIdx.y * 32 + lane;
+#pragma unroll 1
+  for (int r = warp; r < 32; r += kThreads / 32) {
+    const int cp = cp0 + r;
+    double acc = 0.0;
+    if (cp < h.n_p) {
+      // Y_p: a Pg row is the cost diagonal 2 c2 w (from W); a v row was written by k_for
+      const double c2x2 = h.pdiag[cp];
+      const bool pg = c2x2 != 0.0 || h.p_kind[cp] == RH_KIND_PG;
+      acc = pg ? c2x2 * load_W(h, cp, col) : h.Yp[(long long)cp * h.ld + col];
+      const int q0 = h.gpc_ptr[cp], q1 = h.gpc_ptr[cp + 1];
+      for (int q = q0; q < q1; q += 4) {   // four G_p entries' Psi loads in flight, FMAs in entry order
+        double g[4], xv[4];
 #pragma unroll
-  // Y_p: a Pg row is the cost diagonal 2 c2 w (from W); a v row was written by k_for
-  const double c2x2 = h.pdiag[cp];
-  const bool pg = c2x2 != 0.0 || h.p_kind[cp] == RH_KIND_PG;
-  for (int u = 0; u < FCH; ++u) {
-    col[u] = (ch0 + u) * 32 + lane;
-    acc[u] = col[u] < h.N ? (pg ? c2x2 * load_W(h, cp, col[u]) : h.HW[hw_index(h, cp, col[u])]) : 0.0;
-  }
-  // four G_p entries at a time: all their Psi loads in flight, then the FMAs in entry order
-  for (int q = q0; q < q1; q += 4) {
-    double g[4], xv[4][FCH];
+        for (int k = 0; k < 4; ++k) {
+          const bool in = q + k < q1;
+          g[k] = in ? h.gpc_val[q + k] : 0.0;
+          xv[k] = in ? h.P[(long long)h.gpc_row[q + k] * h.ld + col] : 0.0;
+        }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool in = q + k < q1;
-      g[k] = in ? h.gpc_val[q + k] : 0.0;
-      const double *pr = h.P + (long long)(in ? h.gpc_row[q + k] : 0) * h.ld;
-#pragma unroll
-      for (int u = 0; u < FCH; ++u) xv[k][u] = (in && col[u] < h.ld) ? pr[col[u]] : 0.0;
+        for (int k = 0; k < 4; ++k)
+          if (q + k < q1) acc = fma(g[k], xv[k], acc);
+      }
+      if (!h.transposed && col < h.N) h.HW[hw_index(h, cp, col)] = acc;
     }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (q + k < q1)
-#pragma unroll
-        for (int u = 0; u < FCH; ++u)
-          if (col[u] < h.ld) acc[u] = fma(g[k], xv[k][u], acc[u]);
+    T[r][lane] = acc;
   }
-#pragma unroll
-  for (int u = 0; u < FCH; ++u)
-    if (col[u] < h.N) h.HW[hw_index(h, cp, col[u])] = acc[u];
+  if (!h.transposed) return;
+  __syncthreads();
+#pragma unroll 1
+  for (int c = warp; c < 32; c += kThreads / 32) {   // H^T row of column c, p rows cp0 .. cp0 + 31
+    const int cc = blockIdx.y * 32 + c;
+    if (cc < h.N && cp0 + lane < h.n_p) h.HW[hw_index(h, cp0 + lane, cc)] = T[lane][c];
+  }
 }
 
 // natural-order copy of an internal block: out[k][col] = sgn * X[zmap[k]][col]
@@ -2005,6 +2024,8 @@ struct rh_ctx {
   struct Workspace {
     double *Z = nullptr, *P = nullptr, *Tsep = nullptr;
     size_t elems = 0, tsep_elems = 0;
+    double *Yp = nullptr;        // [n_p][ld] Y_p of the voltage parameters
+    size_t yp_elems = 0;
     int *pcols = nullptr;        // Cartesian batch plan: the batch's columns, home-block order
     unsigned *pmask = nullptr;   // and its nonzero L-tile mask [nblk][words]
     int plan_ld = 0;
@@ -2116,6 +2137,7 @@ struct rh_ctx {
       if (w.Tsep) cudaFree(w.Tsep);
       if (w.pcols) cudaFree(w.pcols);
       if (w.pmask) cudaFree(w.pmask);
+      if (w.Yp) cudaFree(w.Yp);
       w = Workspace();
     }
     if (e2e_buf) cudaFree(e2e_buf);
@@ -2490,6 +2512,18 @@ int ensure_ws(rh_ctx *c, int ld, int k = 0) {
   auto &w = c->ws[k];
   const size_t need = (size_t)ld * (size_t)c->A.n_x;
   if (int rc = ensure_tsep(c, ld, k)) return rc;
+  const size_t nyp = (size_t)ld * (size_t)std::max(1, c->A.n_p);
+  if (nyp > w.yp_elems) {
+    c->drop_graph();
+    if (w.Yp) cudaFree(w.Yp);
+    w.Yp = nullptr;
+    w.yp_elems = 0;
+    if (cudaMalloc(&w.Yp, nyp * sizeof(double)) != cudaSuccess || cudaMemset(w.Yp, 0, nyp * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, RH_E_NOMEM, "workspace allocation failed");
+    }
+    w.yp_elems = nyp;
+  }
   if (need <= w.elems) return RH_OK;
   c->drop_graph();
   if (w.Z) cudaFree(w.Z);
@@ -2584,6 +2618,7 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.vUt = c->vUt;
   h.Z = c->ws[k].Z;
   h.P = c->ws[k].P;
+  h.Yp = c->ws[k].Yp;
   h.kblk_group = 2;
   if (const char *env = getenv("RH_KBLK_GROUP")) h.kblk_group = std::max(1, atoi(env));   // tuning override
   h.gp_rptr = c->gp_rptr;
@@ -2617,7 +2652,7 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.blk_gp_ptr = c->blk_gp_ptr;
   h.blk_gp_loc = c->blk_gp_loc;
   if (const char *env = getenv("RH_DEBUG")) h.debug = atoi(env);  // timing experiments only
-  if (h.debug & 8) {
+  if (h.debug & (8 | 8192)) {
     static long long *dbg = nullptr;
     if (!dbg) cudaMalloc(&dbg, sizeof(long long) * 26 * 65536);
     h.dbg = dbg;
@@ -2739,8 +2774,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   const int gA = (int)std::min<long long>(((h.debug & 64) ? 1LL : 2LL) * c->nsm, (long long)nb * (ld / kBC));   // debug 64: 1 CTA/SM (experiment)
   const dim3 gSg(nblk(A.sep_rows, kThreads / 32), ld / 32),
       gSm((ld + GBN - 1) / GBN, (A.sep_rows + GBM - 1) / GBM);
-  const int nch32 = ld / 32, fch = (nch32 + FCH - 1) / FCH;
-  const dim3 gF((int)A.fg.grp_nout.size(), ld / 32), gM(nblk(A.n_p, kThreads / 32), fch);
+  const dim3 gF((int)A.fg.grp_nout.size(), ld / 32), gM((A.n_p + 31) / 32, ld / 32);
   const int nx = A.n_x;
   const long long tot = (long long)nx * N;
   cudaEvent_t ev[9];
@@ -2794,6 +2828,15 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   if (c->tape_wait) RH_CUDA(c, cudaStreamWaitEvent(st, c->tape_wait, 0));   // FoR needs the gradient's tape
   k_for<<<gF, 256, c->smem_for, st>>>(h);
   RH_LAUNCHED(c);
+  if ((h.debug & 8192) && h.dbg) {  // timing experiment: per-CTA phase cycles of k_for (tools/kfor_prof.py)
+    std::vector<long long> hb((size_t)4 * std::min<long long>(16384, (long long)gF.x * gF.y));
+    cudaMemcpyAsync(hb.data(), h.dbg, hb.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (FILE *fp = fopen("gpurun_out/kfor_prof.bin", "wb")) {
+      fwrite(hb.data(), 8, hb.size(), fp);
+      fclose(fp);
+    }
+  }
   if (Yxo) {
     k_unpermute<<<nblk(tot), kThreads, 0, st>>>(nx, N, ld, c->pinv, h.P, -1.0, Yxo, ldz);
     RH_LAUNCHED(c);

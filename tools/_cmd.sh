@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_inputs.py -x -q -p no:cacheprovider > gpurun_out/r02h_pytest.txt 2>&1; tail -3 gpurun_out/r02h_pytest.txt
-bash tools/ab_step.sh r02h "base:" "base2:"
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_inputs.py -x -q -p no:cacheprovider > gpurun_out/r02l_pytest.txt 2>&1; tail -3 gpurun_out/r02l_pytest.txt
+bash tools/ab_step.sh r02l "base:"
