@@ -1649,57 +1649,64 @@ __device__ __forceinline__ double delta_src(const SegParams &h, int src, int col
 // parameters from W), so each line end's gather reads shared memory instead
 // of L2; warp per output bus, lane per column.
 __global__ void __launch_bounds__(256) k_for(SegParams h) {
-  extern __shared__ __align__(128) double fsm[];   // [maxloc][2][32] delta rows, then the tile's tape
+  extern __shared__ __align__(128) double fsm[];   // [maxrows][32] delta rows, then the tile's tape
   __shared__ __align__(8) unsigned long long mbar;
   __shared__ double sref[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int g = blockIdx.x, col0 = blockIdx.y * 32, col = col0 + lane;
-  const int l0 = h.fg_off[g], nl = h.fg_off[g + 1] - l0, nout = h.fg_nout[g], ob = h.fg_obase[g];
+  const int l0 = h.fg_off[g], nout = h.fg_nout[g], ob = h.fg_obase[g];
   const int sb = h.fg_sbase[g], nsl = h.fg_sbase[g + 1] - sb;
-  double4 *s_coef = reinterpret_cast<double4 *>(fsm + (size_t)h.fg_maxloc * 64);
+  const int zlo = h.fg_zlo[g], zn = h.fg_zn[g];
+  const int c0 = h.fg_cp_off[g], ncp = h.fg_cp_off[g + 1] - c0;
+  const int f0 = h.fg_fill_off[g], nfill = h.fg_fill_off[g + 1] - f0;
+  double4 *s_coef = reinterpret_cast<double4 *>(fsm + (size_t)h.fg_maxrows * 32);
   double4 *s_meta = s_coef + h.fg_maxslots;
   int4 *s_dst = reinterpret_cast<int4 *>(s_meta + h.fg_maxout);
   int *s_oe = reinterpret_cast<int *>(s_dst + h.fg_maxout);
-  int2 *s_fill = reinterpret_cast<int2 *>(s_oe + h.fg_maxslots);   // [2 maxloc]
-  __shared__ int s_nfill;
   // timing experiment (RH_DEBUG & 8192): per CTA [start, staged+filled, copies landed, end]
   long long *prof = ((h.debug & 8192) && h.dbg && g * gridDim.y + blockIdx.y < 16384)
                         ? h.dbg + 4LL * (g * gridDim.y + blockIdx.y) : nullptr;
   if (prof && tid == 0) prof[0] = clock64();
+  const char *tm = reinterpret_cast<const char *>(h.tmZ);
+  const int nbig = tm ? zn / kTmaBig : 0, nsmall = tm ? (zn - nbig * kTmaBig) / kTmaSmall : 0;
+  const int rows_tma = nbig * kTmaBig + nsmall * kTmaSmall;
   if (tid == 0) {
-    s_nfill = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const unsigned tx = 256u * h.fg_zrows[g] + 36u * nsl + 48u * nout;
+    const unsigned tx = 256u * (zn + ncp) + 36u * nsl + 48u * nout;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx) : "memory");
     bulk_g2s(s_coef, h.fg_scoef + sb, 32u * nsl, &mbar);
     bulk_g2s(s_oe, h.fg_soe + sb, 4u * nsl, &mbar);
     bulk_g2s(s_meta, h.fg_ometa + ob, 32u * nout, &mbar);
     bulk_g2s(s_dst, h.fg_odst + ob, 16u * nout, &mbar);
+    // the outputs' Z row range by 2D TMA boxes (64, then 8 rows)
+    for (int i = 0; i < nbig; ++i) tma2d_g2s(fsm + i * kTmaBig * 32, tm, col0, zlo + i * kTmaBig, &mbar);
+    for (int i = 0; i < nsmall; ++i) {
+      const int r = nbig * kTmaBig + i * kTmaSmall;
+      tma2d_g2s(fsm + r * 32, tm + kTmapBytes, col0, zlo + r, &mbar);
+    }
   }
-  __syncthreads();
-  // thread per local: bulk copies of its Z rows; rows without a Z source go to
-  // a list (zero, or a v parameter from W) that the warps then fill, lane =
-  // column, 4 rows in flight per warp
-  for (int l = tid; l < nl; l += blockDim.x) {
-    const int4 e = h.fg_loc[l0 + l];
-    if (e.x >= 0) bulk_g2s(fsm + l * 64, h.Z + (long long)e.x * h.ld + col0, 256, &mbar);
-    else s_fill[atomicAdd(&s_nfill, 1)] = make_int2(l * 64, -1);
-    if (e.y >= 0) bulk_g2s(fsm + l * 64 + 32, h.Z + (long long)e.y * h.ld + col0, 256, &mbar);
-    else s_fill[atomicAdd(&s_nfill, 1)] = make_int2(l * 64 + 32, e.y == -1 ? -1 : -(e.y + 2));
+  __syncthreads();   // mbarrier initialised and armed
+  // the rest of the range and the other Z sources: per-row bulk copies
+  for (int r = rows_tma + tid; r < zn; r += blockDim.x)
+    bulk_g2s(fsm + r * 32, h.Z + (long long)(zlo + r) * h.ld + col0, 256, &mbar);
+  for (int i = tid; i < ncp; i += blockDim.x) {
+    const int2 e = h.fg_cp[c0 + i];
+    bulk_g2s(fsm + e.x * 32, h.Z + (long long)e.y * h.ld + col0, 256, &mbar);
   }
-  __syncthreads();
-  for (int f = 4 * warp; f < s_nfill; f += 4 * nw) {
+  // rows without a Z source: zero, or a v parameter from W; lane = column, 4 rows in flight per warp
+  for (int f = 4 * warp; f < nfill; f += 4 * nw) {
     double v[4];
+    int2 q[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int2 q = f + u < s_nfill ? s_fill[f + u] : make_int2(-1, -1);
-      v[u] = q.y >= 0 ? load_W(h, q.y, col) : 0.0;
+      q[u] = f + u < nfill ? h.fg_fill[f0 + f + u] : make_int2(-1, -1);
+      v[u] = q[u].y >= 0 ? load_W(h, q[u].y, col) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (f + u < s_nfill) fsm[s_fill[f + u].x + lane] = v[u];
+      if (f + u < nfill) fsm[q[u].x * 32 + lane] = v[u];
   }
   if (prof && tid == 0) prof[1] = clock64();
   {
@@ -1717,8 +1724,8 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     if (warp == 0) {
       double sr = 0.0;
       for (int q = r0; q < r1; ++q) {
-        const int l = h.fg_ref_loc[q], b = h.fg_loc[l0 + l].z;
-        sr += h.refg_th[b] * fsm[l * 64 + lane] + h.refg_v[b] * fsm[l * 64 + 32 + lane];
+        const int4 e = h.fg_loc[l0 + h.fg_ref_loc[q]];
+        sr += h.refg_th[e.z] * fsm[(e.w & 0xffff) * 32 + lane] + h.refg_v[e.z] * fsm[(e.w >> 16) * 32 + lane];
       }
       sref[lane] = sr * h.f2ref;
     }
@@ -1730,8 +1737,8 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     // canonical slot coefficients (k_for_tape): D = dth_b - dth_o,
     // yth += K D + c2 dv_b + c3 dv_o,  yv += c2 D + m dv_o
     const double4 k = s_coef[q];
-    const int o = s_oe[q] >> 1;
-    const double D = dth_b - fsm[o * 64 + lane], dv_o = fsm[o * 64 + 32 + lane];
+    const int o = s_oe[q];
+    const double D = dth_b - fsm[(o & 0xffff) * 32 + lane], dv_o = fsm[(o >> 16) * 32 + lane];
     yth = fma(k.x, D, fma(k.y, dv_b, fma(k.z, dv_o, yth)));
     yv = fma(k.y, D, fma(k.w, dv_o, yv));
   };
@@ -1752,17 +1759,18 @@ __global__ void __launch_bounds__(256) k_for(SegParams h) {
     const bool two = i2 < nout;
     const int4 d = s_dst[i], d2 = two ? s_dst[i2] : make_int4(-1, -1, 0, 0);
     const double4 mt = s_meta[i], mt2 = two ? s_meta[i2] : make_double4(0.0, 0.0, 0.0, 0.0);
-    const double dth_b = fsm[i * 64 + lane], dv_b = fsm[i * 64 + 32 + lane];
-    const double dth_b2 = two ? fsm[i2 * 64 + lane] : 0.0, dv_b2 = two ? fsm[i2 * 64 + 32 + lane] : 0.0;
+    const int o1 = d.w, o2 = d2.w;   // own staging rows
+    const double dth_b = fsm[(o1 & 0xffff) * 32 + lane], dv_b = fsm[(o1 >> 16) * 32 + lane];
+    const double dth_b2 = two ? fsm[(o2 & 0xffff) * 32 + lane] : 0.0, dv_b2 = two ? fsm[(o2 >> 16) * 32 + lane] : 0.0;
     double yth = 0.0, yv = mt.x * dv_b, yth2 = 0.0, yv2 = mt2.x * dv_b2;
-    const int n1 = d.w, n2 = d2.w, nmin = min(n1, n2);
+    const int q1 = d.z & 0xffff, q2 = d2.z & 0xffff, n1 = d.z >> 16, n2 = d2.z >> 16, nmin = min(n1, n2);
     int t = 0;
     for (; t < nmin; ++t) {
-      slot(d.z + t, dth_b, dv_b, yth, yv);
-      slot(d2.z + t, dth_b2, dv_b2, yth2, yv2);
+      slot(q1 + t, dth_b, dv_b, yth, yv);
+      slot(q2 + t, dth_b2, dv_b2, yth2, yv2);
     }
-    for (; t < n1; ++t) slot(d.z + t, dth_b, dv_b, yth, yv);
-    for (; t < n2; ++t) slot(d2.z + t, dth_b2, dv_b2, yth2, yv2);
+    for (; t < n1; ++t) slot(q1 + t, dth_b, dv_b, yth, yv);
+    for (; t < n2; ++t) slot(q2 + t, dth_b2, dv_b2, yth2, yv2);
     finish(d, mt, yth, yv);
     if (two) finish(d2, mt2, yth2, yv2);
   }
@@ -2050,7 +2058,10 @@ struct rh_ctx {
   int smem_stride = 0;
   int *blk_ctr = nullptr;
   size_t smem_blk = 0, smem_for = 0;
-  int *fg_off, *fg_nout, *fg_obase, *fg_zrows, *fg_sbase, *fg_ref, *fg_ref_loc, *fg_soe, *fg_out_bus;
+  int *fg_off, *fg_nout, *fg_obase, *fg_sbase, *fg_ref, *fg_ref_loc, *fg_soe, *fg_out_bus;
+  int *fg_zlo, *fg_zn, *fg_cp_off, *fg_fill_off;
+  int2 *fg_cp, *fg_fill;
+  int fg_maxrows = 1;
   int4 *fg_loc, *fg_odst;
   int2 *fg_slots;
   double4 *fg_scoef, *fg_ometa;
@@ -2358,7 +2369,64 @@ int upload(rh_ctx *c) {
       if (dst[i] >= 0) dst[i] = zrow[dst[i]];
       if (dst[i + 1] >= 0) dst[i + 1] = zrow[dst[i + 1]];
     }
-    for (size_t q = 0; q < soe.size(); ++q) soe[q] = F.slots[2 * q + 1];
+    // staging rows of every group: the outputs' Z row range [zlo, zlo + zn) first
+    // (rows of halo buses inside it are shared), then per-row copies and fills
+    const int ng = (int)F.grp_nout.size();
+    std::vector<int32_t> zlo(ng, 0), zn(ng, 0), cpo(1, 0), fio(1, 0), cp, fi;
+    int maxrows = 1;
+    for (int gi = 0; gi < ng; ++gi) {
+      const int lb = F.grp_off[gi], nl = F.grp_off[gi + 1] - lb, no = F.grp_nout[gi];
+      int lo = INT32_MAX, hi = -1;
+      for (int i = 0; i < no; ++i)
+        for (int k = 0; k < 2; ++k) {
+          const int z = loc[4 * (lb + i) + k];
+          if (z >= 0) lo = std::min(lo, z), hi = std::max(hi, z);
+        }
+      int n_a = hi >= lo ? hi - lo + 1 : 0;
+      if (n_a > 3 * no + 16 || getenv("RH_FOR_NO_RANGE")) n_a = 0;   // too sparse: per-row copies only
+      zlo[gi] = n_a ? lo : 0;
+      zn[gi] = n_a;
+      int next = n_a;
+      for (int l = 0; l < nl; ++l) {
+        int rows[2];
+        for (int k = 0; k < 2; ++k) {
+          const int src = loc[4 * (lb + l) + k];
+          if (src >= 0 && n_a && src >= lo && src < lo + n_a) {
+            rows[k] = src - lo;
+          } else if (src >= 0) {
+            rows[k] = next++;
+            cp.push_back(rows[k]);
+            cp.push_back(src);
+          } else {
+            rows[k] = next++;
+            fi.push_back(rows[k]);
+            fi.push_back(src == -1 ? -1 : -(src + 2));
+          }
+        }
+        loc[4 * (lb + l) + 3] = rows[0] | (rows[1] << 16);
+      }
+      cpo.push_back((int)cp.size() / 2);
+      fio.push_back((int)fi.size() / 2);
+      maxrows = std::max(maxrows, next);
+      for (int q = F.grp_sbase[gi]; q < F.grp_sbase[gi + 1]; ++q)
+        soe[q] = loc[4 * (lb + (F.slots[2 * q + 1] >> 1)) + 3];
+      for (int i = 0; i < no; ++i) {   // per output: (theta row, v row, first slot | slots << 16, own staging rows)
+        const int o = F.grp_obase[gi] + i;
+        dst[4 * o + 2] = dst[4 * o + 2] | (dst[4 * o + 3] << 16);
+        dst[4 * o + 3] = loc[4 * (lb + i) + 3];
+      }
+    }
+    if (cp.empty()) cp.assign(2, 0);
+    if (fi.empty()) fi.assign(2, 0);
+    chk(c->fg_zlo = dalloc_copy(zlo, P));
+    chk(c->fg_zn = dalloc_copy(zn, P));
+    chk(c->fg_cp_off = dalloc_copy(cpo, P));
+    chk(c->fg_fill_off = dalloc_copy(fio, P));
+    c->fg_cp = reinterpret_cast<int2 *>(dalloc_copy(cp, P));
+    c->fg_fill = reinterpret_cast<int2 *>(dalloc_copy(fi, P));
+    chk(c->fg_cp);
+    chk(c->fg_fill);
+    c->fg_maxrows = maxrows;
     c->fg_loc = reinterpret_cast<int4 *>(dalloc_copy(loc, P));
     c->fg_odst = reinterpret_cast<int4 *>(dalloc_copy(dst, P));
     c->fg_slots = reinterpret_cast<int2 *>(dalloc_copy(F.slots, P));
@@ -2370,7 +2438,6 @@ int upload(rh_ctx *c) {
     chk(c->fg_off = dalloc_copy(F.grp_off, P));
     chk(c->fg_nout = dalloc_copy(F.grp_nout, P));
     chk(c->fg_obase = dalloc_copy(F.grp_obase, P));
-    chk(c->fg_zrows = dalloc_copy(F.grp_zrows, P));
     chk(c->fg_sbase = dalloc_copy(F.grp_sbase, P));
     chk(c->fg_ref = dalloc_copy(F.grp_ref, P));
     chk(c->fg_ref_loc = dalloc_copy(F.ref_loc, P));
@@ -2380,8 +2447,7 @@ int upload(rh_ctx *c) {
       if (A.p_kind[q] == RH_KIND_PG) pdiag[q] = 2.0 * A.c2b[A.p_bus[q]];
     chk(c->pdiag = dalloc_copy(pdiag, P));
     chk(c->fg_ometa = dalloc<double4>(F.out_bus.size(), P));
-    c->smem_for = (size_t)F.max_loc * 64 * sizeof(double) + (size_t)F.max_slots * 36 + (size_t)F.max_nout * 48 +
-                  (size_t)F.max_loc * 16;
+    c->smem_for = (size_t)c->fg_maxrows * 32 * sizeof(double) + (size_t)F.max_slots * 36 + (size_t)F.max_nout * 48;
   }
   mkunit(c->duf, A.ufwd, c->dfwd);
   mkunit(c->dub, A.ubwd, c->dbwd);
@@ -2673,12 +2739,17 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.gpe_rec = c->gpe_rec;
   h.maxrx = c->maxrx;
   h.fg_off = c->fg_off;
-  h.fg_maxloc = A.fg.max_loc;
+  h.fg_maxrows = c->fg_maxrows;
+  h.fg_zlo = c->fg_zlo;
+  h.fg_zn = c->fg_zn;
+  h.fg_cp_off = c->fg_cp_off;
+  h.fg_fill_off = c->fg_fill_off;
+  h.fg_cp = c->fg_cp;
+  h.fg_fill = c->fg_fill;
   h.fg_maxout = A.fg.max_nout;
   h.fg_maxslots = A.fg.max_slots;
   h.fg_nout = c->fg_nout;
   h.fg_obase = c->fg_obase;
-  h.fg_zrows = c->fg_zrows;
   h.fg_sbase = c->fg_sbase;
   h.fg_ref = c->fg_ref;
   h.fg_ref_loc = c->fg_ref_loc;
