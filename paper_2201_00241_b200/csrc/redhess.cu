@@ -1648,7 +1648,8 @@ __device__ __forceinline__ double delta_src(const SegParams &h, int src, int col
 // staged once in shared memory (Z rows by TMA bulk copies on an mbarrier, v
 // parameters from W), so each line end's gather reads shared memory instead
 // of L2; warp per output bus, lane per column.
-__global__ void __launch_bounds__(256) k_for(SegParams h) {
+constexpr int kForThreads = 512;   // 16 warps: two CTAs per SM (shared memory), 32 warps to hide latency
+__global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
   extern __shared__ __align__(128) double fsm[];   // [maxrows][32] delta rows, then the tile's tape
   __shared__ __align__(8) unsigned long long mbar;
   __shared__ double sref[32];
@@ -2897,7 +2898,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   }
   mark(3);
   if (c->tape_wait) RH_CUDA(c, cudaStreamWaitEvent(st, c->tape_wait, 0));   // FoR needs the gradient's tape
-  k_for<<<gF, 256, c->smem_for, st>>>(h);
+  k_for<<<gF, kForThreads, c->smem_for, st>>>(h);
   RH_LAUNCHED(c);
   if ((h.debug & 8192) && h.dbg) {  // timing experiment: per-CTA phase cycles of k_for (tools/kfor_prof.py)
     std::vector<long long> hb((size_t)4 * std::min<long long>(16384, (long long)gF.x * gF.y));
