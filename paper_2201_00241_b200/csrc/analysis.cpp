@@ -692,8 +692,14 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
             pad4(r);
           }
         } else {
-          for (int pass = 0; pass < 2; ++pass) {   // separator: external entries first, then local
-            for (int k : deps) {
+          // separator: external entries first (grouped by block, then row: a Cartesian
+          // batch's gather skips whole blocks), then local
+          std::vector<int32_t> ord(deps.begin(), deps.end());
+          std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+            return A.seg_of[a] != A.seg_of[b] ? A.seg_of[a] < A.seg_of[b] : a < b;
+          });
+          for (int pass = 0; pass < 2; ++pass) {
+            for (int k : ord) {
               const bool local = A.seg_of[k] == s;
               if (local != (pass == 1)) continue;
               S.dep.push_back(local ? A.loc_of[k] : k);

@@ -25,7 +25,10 @@ struct DSeg {
   const int *__restrict__ dep;       // local row index (local entries) / global permuted row (external)
   const int *__restrict__ ext_off;   // [nseg + 1] blocks: staged separator rows
   const int *__restrict__ ext_rows;
-  const int *__restrict__ dep_seg;   // fwd only: block of each separator row's external dependency
+  // fwd only: per separator row q (index q - first separator q), its external entries
+  // in runs of one block each: runs [grp_ptr[i], grp_ptr[i + 1]), run g = block grp_blk[g]
+  // over entries [.., grp_end[g])
+  const int *__restrict__ grp_ptr, *__restrict__ grp_blk, *__restrict__ grp_end;
 };
 
 // Bus-unit schedule of one pattern direction (analysis.hpp UnitSweep).

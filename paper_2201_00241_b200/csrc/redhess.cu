@@ -1460,6 +1460,28 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
   int e = h.fwd.rptr[q];
   const int ex = h.fwd.rext[q];
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (masked) {
+    // Cartesian batch: only the block runs whose tile of this chunk is live (the
+    // others are identically zero); four chains over the live entries in order
+    for (int g = h.fwd.grp_ptr[qoff], g1 = h.fwd.grp_ptr[qoff + 1]; g < g1; ++g) {
+      const int ee = h.fwd.grp_end[g];
+      if (!tile_live(h, h.fwd.grp_blk[g], blockIdx.y)) {
+        e = ee;
+        continue;
+      }
+      for (; e + 4 <= ee; e += 4) {
+        const double x0 = G[(long long)h.fwd.dep[e] * h.ld + col], x1 = G[(long long)h.fwd.dep[e + 1] * h.ld + col];
+        const double x2 = G[(long long)h.fwd.dep[e + 2] * h.ld + col], x3 = G[(long long)h.fwd.dep[e + 3] * h.ld + col];
+        s0 = fma(val[e], x0, s0);
+        s1 = fma(val[e + 1], x1, s1);
+        s2 = fma(val[e + 2], x2, s2);
+        s3 = fma(val[e + 3], x3, s3);
+      }
+      for (; e < ee; ++e) s0 = fma(val[e], G[(long long)h.fwd.dep[e] * h.ld + col], s0);
+    }
+    h.Tsep[(long long)a * h.ld + col] = v0 - ((s0 + s1) + (s2 + s3));
+    return;
+  }
   for (; e + 8 <= ex; e += 8) {   // 8 row gathers in flight
     int d[8];
     double c[8], x[8];
@@ -1470,7 +1492,7 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u)
-      x[u] = (!masked || tile_live(h, h.fwd.dep_seg[e + u], blockIdx.y)) ? G[(long long)d[u] * h.ld + col] : 0.0;
+      x[u] = G[(long long)d[u] * h.ld + col];
     s0 = fma(c[0], x[0], s0);
     s1 = fma(c[1], x[1], s1);
     s2 = fma(c[2], x[2], s2);
@@ -1480,9 +1502,7 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
     s2 = fma(c[6], x[6], s2);
     s3 = fma(c[7], x[7], s3);
   }
-  auto ld_dep = [&](int e1) {
-    return (!masked || tile_live(h, h.fwd.dep_seg[e1], blockIdx.y)) ? G[(long long)h.fwd.dep[e1] * h.ld + col] : 0.0;
-  };
+  auto ld_dep = [&](int e1) { return G[(long long)h.fwd.dep[e1] * h.ld + col]; };
   for (; e + 4 <= ex; e += 4) {
     const double x0 = ld_dep(e), x1 = ld_dep(e + 1), x2 = ld_dep(e + 2), x3 = ld_dep(e + 3);
     s0 = fma(val[e], x0, s0);
@@ -2308,14 +2328,31 @@ int upload(rh_ctx *c) {
     D.dep = d;
   };
   mkseg(c->dfwd, A.fwd);
-  {  // block of every separator external dependency (fwd), for the Cartesian batch mask
+  {  // runs of one block in the separator rows' external dependencies (fwd), for the Cartesian batch mask
     std::vector<int32_t> ds(std::max<size_t>(1, A.fwd.dep.size()), -1);
     const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
     for (int q = qb; q < qe; ++q)
       for (int e = A.fwd.rptr[q]; e < A.fwd.rext[q]; ++e) ds[e] = A.seg_of[A.fwd.dep[e]];
-    int *d;
-    chk(d = dalloc_copy(ds, P));
-    c->dfwd.dep_seg = d;
+    // runs of one block in every separator row's external entries
+    std::vector<int32_t> gp(1, 0), gb, ge;
+    for (int q = qb; q < qe; ++q) {
+      for (int e = A.fwd.rptr[q]; e < A.fwd.rext[q]; ++e)
+        if (e == A.fwd.rptr[q] || ds[e] != ds[e - 1]) {
+          gb.push_back(ds[e]);
+          ge.push_back(e + 1);
+        } else {
+          ge.back() = e + 1;
+        }
+      gp.push_back((int)gb.size());
+    }
+    if (gb.empty()) gb.push_back(0), ge.push_back(0);
+    int *g1, *g2, *g3;
+    chk(g1 = dalloc_copy(gp, P));
+    chk(g2 = dalloc_copy(gb, P));
+    chk(g3 = dalloc_copy(ge, P));
+    c->dfwd.grp_ptr = g1;
+    c->dfwd.grp_blk = g2;
+    c->dfwd.grp_end = g3;
   }
   {  // Cartesian batch plans: blocks touched by each p column (rows of G_p's column
      // in a block), and all p columns ordered by their first touched block, then index
