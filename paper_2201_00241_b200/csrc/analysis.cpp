@@ -88,9 +88,15 @@ std::vector<int32_t> minimum_degree(std::vector<std::vector<int32_t>> adj) {
 // always land in the same piece (or both in the tops), so the bus-unit sweeps
 // can process them together.  A unit's parent is the unit holding the
 // elimination-tree parent of its highest row.
+//
+// Unit sweeps (dual = true): the cut goes on while the largest piece exceeds
+// `cut` x (remaining pieces' cost / nw), and the pieces are packed onto the
+// warps twice, once per pattern direction with that direction's unit cost (a
+// fixed per-unit latency plus one per dependency unit): warp_rows for the
+// forward sweeps (L, U^T), warp_rows_b for the backward ones (U, L^T).
 BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<int32_t> &unit_lo,
                        const std::vector<std::vector<int32_t>> &Ls, const std::vector<std::vector<int32_t>> &Lrow,
-                       int nw, int max_tops) {
+                       int nw, int max_tops, bool dual = false, double cut = 1.25) {
   const int n = (int)rows.size();   // ascending permuted rows
   std::vector<int> uofr(n), ubeg;   // unit of each local row, first local row of each unit
   for (int i = 0; i < n; ++i) {
@@ -131,35 +137,78 @@ BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<int32
   const double target = total / nw;
   std::vector<char> is_top(nu, 0);
   int ntop = 0, ntop_units = 0;
+  double rem = total;
   while (true) {
     int best = -1;
     for (int k = 0; k < (int)pieces.size(); ++k)
       if (best < 0 || sc[pieces[k]] > sc[pieces[best]]) best = k;
-    if (best < 0 || sc[pieces[best]] <= 1.25 * target || kids[pieces[best]].empty()) break;
+    if (best < 0 || kids[pieces[best]].empty()) break;
+    if (sc[pieces[best]] <= (dual ? cut * rem / nw : cut * target)) break;
     const int p = pieces[best];
     if (ntop + usize[p] > max_tops || ntop_units >= UnitSweep::kMaxTopUnits) break;
     pieces.erase(pieces.begin() + best);
     is_top[p] = 1;
     ntop += usize[p];
     ++ntop_units;
+    rem -= cost[p];
     for (int k : kids[p]) pieces.push_back(k);
   }
   std::sort(pieces.begin(), pieces.end(), [&](int x, int y) { return sc[x] > sc[y]; });
-  std::vector<double> load(nw, 0.0);
-  BlockSplit B;
-  B.warp_rows.assign(nw, {});
-  for (int p : pieces) {
-    const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    load[w] += sc[p];
-    std::vector<int> st{p};
-    while (!st.empty()) {
-      const int x = st.back();
-      st.pop_back();
-      for (int i = ubeg[x]; i < ubeg[x + 1]; ++i) B.warp_rows[w].push_back(rows[i]);
-      for (int k : kids[x]) st.push_back(k);
-    }
+  if (getenv("RH_DEBUG_SCHED") && nw == UnitSweep::kWarps) {
+    static double s_big = 0, s_tgt = 0;
+    static int nblk_seen = 0;
+    double rp = 0;
+    for (int p : pieces) rp += sc[p];
+    s_big += pieces.empty() ? 0 : sc[pieces[0]];
+    s_tgt += rp / nw;
+    if (++nblk_seen % 10 == 0)
+      fprintf(stderr, "split: %d blocks: sum largest piece %.0f, sum remaining/nw %.0f; this block: %zu pieces, tops %d units %d rows\n",
+              nblk_seen, s_big, s_tgt, pieces.size(), ntop_units, ntop);
   }
-  for (auto &v : B.warp_rows) std::sort(v.begin(), v.end());  // ascending = forward topological
+  BlockSplit B;
+  // LPT of the pieces onto the warps by subtree cost w (per unit)
+  auto pack = [&](const std::vector<double> &w, std::vector<std::vector<int32_t>> &out) {
+    std::vector<double> sw(nu);
+    for (int u = 0; u < nu; ++u) {
+      sw[u] = w[u];
+      for (int k : kids[u]) sw[u] += sw[k];
+    }
+    std::vector<int> pc(pieces);
+    std::stable_sort(pc.begin(), pc.end(), [&](int x, int y) { return sw[x] > sw[y]; });
+    std::vector<double> load(nw, 0.0);
+    out.assign(nw, {});
+    for (int p : pc) {
+      const int wi = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[wi] += sw[p];
+      std::vector<int> st{p};
+      while (!st.empty()) {
+        const int x = st.back();
+        st.pop_back();
+        for (int i = ubeg[x]; i < ubeg[x + 1]; ++i) out[wi].push_back(rows[i]);
+        for (int k : kids[x]) st.push_back(k);
+      }
+    }
+    for (auto &v : out) std::sort(v.begin(), v.end());  // ascending = forward topological
+  };
+  if (!dual) {
+    pack(cost, B.warp_rows);
+  } else {
+    // direction costs: a fixed per-unit latency + its dependency units (fwd: L row, bwd: U row)
+    constexpr double kUnitLat = 6.0;
+    std::vector<double> cf(nu), cb(nu);
+    std::vector<int32_t> du;
+    for (int u = 0; u < nu; ++u)
+      for (int dir = 0; dir < 2; ++dir) {
+        du.clear();
+        for (int i = ubeg[u]; i < ubeg[u + 1]; ++i)
+          for (int k : dir == 0 ? Lrow[rows[i]] : Ls[rows[i]])
+            if (unit_lo[k] != unit_lo[rows[ubeg[u]]]) du.push_back(unit_lo[k]);
+        sort_unique(du);
+        (dir == 0 ? cf : cb)[u] = kUnitLat + (double)du.size();
+      }
+    pack(cf, B.warp_rows);
+    pack(cb, B.warp_rows_b);
+  }
   for (int u = 0; u < nu; ++u)
     if (is_top[u])
       for (int i = ubeg[u]; i < ubeg[u + 1]; ++i) B.tops.push_back(rows[i]);
@@ -217,7 +266,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
     };
     for (int w = 0; w < UnitSweep::kWarps; ++w) {
       lvl.push_back((int)units.size());
-      add_units(B.warp_rows[w]);
+      add_units(fwd ? B.warp_rows[w] : B.warp_rows_b[w]);
     }
     lvl.push_back((int)units.size());
     const int tu0 = (int)units.size();
@@ -255,10 +304,15 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
     // emit one dependency list; returns the int4 meta; `hdr`: piece unit header
     // records.  Every dependency is a pair of tile rows (o0, o1) (byte offsets;
     // a one-value dependency repeats its row with a zero second coefficient);
-    // lists are padded to chunks of 4 with zero dependencies on the unit's row.
+    // lists hold exactly the unit's dependencies, each starting at an even pair.
     auto emit = [&](const std::vector<int> &u, const std::vector<std::pair<int, int>> &du, bool hdr,
                     std::vector<int> *pos_rows, std::vector<int32_t> *pos_out) {
       const bool two = u.size() == 2;
+      // the list starts at an even dependency (offset pairs are read as int4 per two dependencies)
+      if (((int)U.doff.size() - off0) % 4) {
+        U.doff.push_back(0);
+        U.doff.push_back(0);
+      }
       const int cbeg = (int)U.src_a.size() / 2 - rec0, obeg = (int)U.doff.size() - off0;
       auto rec = [&](int a0, int a1, int b0, int b1) {
         U.src_a.push_back(a0);
@@ -273,16 +327,9 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         rec(fwd ? -1 : inv(f), (!fwd && two) ? inv(sr) : -1, fwd ? inv(f) : -1, (fwd && two) ? inv(sr) : -1);
         if (two) rec(coef(false, sr, f), -1, coef(true, sr, f), -1);
       }
-      const int nd = (int)du.size(), nchunk = std::max(1, (nd + 3) / 4);   // >= 1 chunk (straight-line chunk 0)
+      const int nd = (int)du.size();   // exact count: no padding (r02: lists were padded to 4)
       const int rowb = UnitSweep::kCols * 8;
-      for (int di = 0; di < 4 * nchunk; ++di) {
-        if (di >= nd) {   // padding: zero coefficients on the unit's own (finite) row
-          U.doff.push_back(A.loc_of[u[0]] * rowb);
-          U.doff.push_back(A.loc_of[u[0]] * rowb);
-          rec(-1, -1, -1, -1);
-          if (two) rec(-1, -1, -1, -1);
-          continue;
-        }
+      for (int di = 0; di < nd; ++di) {
         const int k0 = du[di].first, nv = du[di].second, k1 = nv == 2 ? k0 + 1 : -1;
         U.doff.push_back(tile_row(k0) * rowb);
         U.doff.push_back(tile_row(nv == 2 ? k1 : k0) * rowb);   // one-value dependency: its row again, zero coefficient
@@ -299,7 +346,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         }
       }
       return std::array<int, 4>{A.loc_of[u[0]] | ((two ? A.loc_of[u[1]] : 0) << 16), cbeg, obeg,
-                                nchunk | ((two ? 1 : 0) << 16)};
+                                nd | ((two ? 1 : 0) << 16)};
     };
     for (int ui = 0; ui < (int)units.size(); ++ui) {
       const auto &u = units[ui];
@@ -312,6 +359,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
       for (int a = 0; a < UnitSweep::kTopRows; ++a)
         U.top_rows.push_back(T.empty() ? 0 : A.loc_of[T[a < (int)T.size() ? a : 0]]);
     }
+    while (((int)U.doff.size() - off0) % 4) U.doff.push_back(0);   // 16-byte bulk copies
     U.unit_off.push_back((int)(U.meta.size() / 4));
     U.tmeta_off.push_back((int)(U.tmeta.size() / 4));
     U.rec_off.push_back((int)U.src_a.size() / 2);
@@ -335,7 +383,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         int r = 0;
         for (int u = lv[w]; u < lv[w + 1]; ++u) {
           const int *m = U.meta.data() + 4 * (ub + u);
-          r += (m[3] & 0xffff) * 4 * ((m[3] >> 16) ? 2 : 1);
+          r += (m[3] & 0xffff) * ((m[3] >> 16) ? 2 : 1);
         }
         mu = std::max(mu, lv[w + 1] - lv[w]);
         mr = std::max(mr, r);
@@ -345,6 +393,24 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
               fwd ? "fwd" : "bwd", s, U.unit_off[s + 1] - ub, mu, mr, sr / UnitSweep::kWarps,
               lv[UnitSweep::kWarps + 2] - lv[UnitSweep::kWarps + 1]);
     }
+    {  // warp balance of the pieces phase, unit cost = 6 + dependencies (latency-bound units)
+      double smax = 0, smean = 0;
+      for (int s = 0; s < nb; ++s) {
+        const int *lv = U.lvl.data() + s * UnitSweep::kLvl;
+        const int ub = U.unit_off[s];
+        double mx = 0, sm = 0;
+        for (int w = 0; w < UnitSweep::kWarps; ++w) {
+          double c = 0;
+          for (int u = lv[w]; u < lv[w + 1]; ++u) c += 6 + (U.meta[4 * (ub + u) + 3] & 0xffff);
+          mx = std::max(mx, c);
+          sm += c;
+        }
+        smax += mx;
+        smean += sm / UnitSweep::kWarps;
+      }
+      fprintf(stderr, "  %s pieces balance: sum over blocks of max-warp cost %.0f, of mean-warp cost %.0f (ratio %.3f)\n",
+              fwd ? "fwd" : "bwd", smax, smean, smax / smean);
+    }
     fprintf(stderr, "units %s: blocks %d max rows %d units %d tops-units %d rec %d doff %d; records %zu, cost sum %lld\n",
             fwd ? "fwd" : "bwd", nb, U.max_rows, U.max_units, U.max_tunits, U.max_rec, U.max_doff,
             U.src_a.size() / 2, tot);
@@ -352,9 +418,9 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
     long long wf_piece = 0, wf_tops = 0, deps = 0, real = 0;
     for (size_t u = 0; u < U.meta.size() / 4; ++u) {
       const int *m = U.meta.data() + 4 * u;
-      const int nchk = m[3] & 0xffff, two = m[3] >> 16;
-      wf_piece += nchk * (16 + (two ? 8 : 4) + 2) + (two ? 2 : 1) + 4 * (two ? 2 : 1) + 1;
-      deps += 4 * nchk;
+      const int nd = m[3] & 0xffff, two = m[3] >> 16;
+      wf_piece += nd * 4 + nd * (two ? 2 : 1) + (nd + 1) / 2 + (two ? 2 : 1) + 4 * (two ? 2 : 1) + 1;
+      deps += nd;
     }
     wf_tops = 16 * 2 * 8 * 4;   // DMMA: 16 output tiles x 8 k-steps x (A + B fragments)
     for (size_t i = 0; i < U.doff.size(); i += 2) real += U.doff[i] != U.doff[i + 1] || true;
@@ -729,9 +795,11 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
     A.split[s] = split_block(rows, A.unit_lo, Ls, Lrow, kSchedWarps, tops_cap);
   }
   A.usplit.assign(nb, BlockSplit());
+  double ucut = 1.0;
+  if (const char *env = getenv("RH_CUT")) ucut = atof(env);   // tuning override
   for (int s = 0; s < nb; ++s) {
     std::vector<int32_t> rows(A.row_global.begin() + A.seg_row_off[s], A.row_global.begin() + A.seg_row_off[s + 1]);
-    A.usplit[s] = split_block(rows, A.unit_lo, Ls, Lrow, UnitSweep::kWarps, tops_cap);
+    A.usplit[s] = split_block(rows, A.unit_lo, Ls, Lrow, UnitSweep::kWarps, tops_cap, true, ucut);
   }
   A.top_fwd_base.clear();
   A.top_bwd_base.clear();

@@ -50,7 +50,8 @@ struct SegSweep {
 };
 
 struct BlockSplit {
-  std::vector<std::vector<int32_t>> warp_rows;  // per warp: piece rows (global, ascending)
+  std::vector<std::vector<int32_t>> warp_rows;  // per warp: piece rows (global, ascending); unit sweeps: forward
+  std::vector<std::vector<int32_t>> warp_rows_b;  // unit sweeps: the backward sweeps' packing of the same pieces
   std::vector<int32_t> tops;                    // top rows (global, ascending)
 };
 
@@ -71,10 +72,11 @@ struct UnitSweep {
   std::vector<int32_t> lvl;          // [nblk * kLvl], block-relative unit indices
   // per unit (int4): row_f | row_s << 16 (tile rows, sweep order), first record
   // (double2, block-relative), first dependency offset pair (int, block-
-  // relative, multiple of 8), nchunks | two_rows << 16.  A dependency is a
+  // relative, multiple of 4), ndeps | two_rows << 16.  A dependency is a
   // pair of tile-row byte offsets (o0, o1) and one (one-row unit) or two
   // (two-row unit) double2 coefficient records (c_f0, c_f1), (c_s0, c_s1);
-  // lists are padded to chunks of 4 dependencies.
+  // no padding (r02: lists padded to chunks of 4 read 2.5x the real
+  // dependencies in the forward sweeps).
   std::vector<int32_t> meta;
   std::vector<int32_t> tmeta;        // (unused: the tops' dense product runs on DMMA, see top_rows)
   std::vector<int32_t> tmeta_off;    // [nblk + 1] into tmeta (units)

@@ -1073,17 +1073,58 @@ __device__ __forceinline__ void dep_chunk(const double2 *__restrict__ rc, const 
   }
 }
 
-// sf = sum c_f x, ss = sum c_s x over a dependency list of `nch` >= 1 chunks
-// of 4 dependencies (tile-row byte offsets o0, o1; records (c_f0, c_f1) [,
-// (c_s0, c_s1)]).  Chunk 0 straight-line, the rest rolled: most units have one.
-// Branch-free, two-deep FMA chains, fixed order (deterministic).
+// one or two dependencies (the tail of a list): dependency 0 -> chains (f0, f1),
+// dependency 1 -> chains (f2, f3), the chunk's assignment
+template <bool TWO, bool PAIR>
+__device__ __forceinline__ void dep_tail(const double2 *__restrict__ rc, const int2 *__restrict__ of, const char *Xb,
+                                         double &f0, double &f1, double &f2, double &f3, double &s0, double &s1,
+                                         double &s2, double &s3) {
+  const int2 a = of[0];
+  const double x00 = lds(Xb + a.x), x01 = lds(Xb + a.y);
+  double x10 = 0.0, x11 = 0.0;
+  if (PAIR) {
+    const int2 b = of[1];
+    x10 = lds(Xb + b.x);
+    x11 = lds(Xb + b.y);
+  }
+  if (TWO) {
+    const double2 p0 = rc[0], q0 = rc[1];
+    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1); s0 = fma(q0.x, x00, s0); s1 = fma(q0.y, x01, s1);
+    if (PAIR) {
+      const double2 p1 = rc[2], q1 = rc[3];
+      f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3); s2 = fma(q1.x, x10, s2); s3 = fma(q1.y, x11, s3);
+    }
+  } else {
+    const double2 p0 = rc[0];
+    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1);
+    if (PAIR) {
+      const double2 p1 = rc[1];
+      f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3);
+    }
+  }
+}
+
+// sf = sum c_f x, ss = sum c_s x over a dependency list of exactly `nd`
+// dependencies (tile-row byte offsets o0, o1; records (c_f0, c_f1) [, (c_s0,
+// c_s1)]): chunks of 4, then a pair and / or a single.  The list starts at an
+// even dependency (int4 offset loads).  Branch-free inside a chunk, two-deep
+// FMA chains, fixed order (deterministic; the chain of every dependency is the
+// one the padded chunks of r02 gave it, so the sums are bitwise unchanged).
 template <bool TWO>
-__device__ __forceinline__ void dep_sums(const double2 *__restrict__ rc, const int4 *__restrict__ of, int nch,
+__device__ __forceinline__ void dep_sums(const double2 *__restrict__ rc, const int4 *__restrict__ of, int nd,
                                          const char *Xb, double &sf, double &ss) {
   double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  dep_chunk<TWO>(rc, of, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
+  int c = 0;
 #pragma unroll 1
-  for (int c = 1; c < nch; ++c) dep_chunk<TWO>(rc + c * (TWO ? 8 : 4), of + 2 * c, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
+  for (; c + 4 <= nd; c += 4) dep_chunk<TWO>(rc + c * (TWO ? 2 : 1), of + c / 2, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
+  const int2 *of2 = reinterpret_cast<const int2 *>(of) + c;
+  rc += c * (TWO ? 2 : 1);
+  if (nd - c >= 2) {
+    dep_tail<TWO, true>(rc, of2, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
+    if (nd - c == 3) dep_tail<TWO, false>(rc + (TWO ? 4 : 2), of2 + 2, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
+  } else if (nd - c == 1) {
+    dep_tail<TWO, false>(rc, of2, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
+  }
   sf = (f0 + f1) + (f2 + f3);
   ss = (s0 + s1) + (s2 + s3);
 }
@@ -1092,14 +1133,14 @@ __device__ __forceinline__ void dep_sums(const double2 *__restrict__ rc, const i
 template <bool DINV>
 __device__ __forceinline__ void unit_solve(const UStage &t, const int4 m, char *Xb) {
   const int rf = (m.x & 0xffff) * kRowB, rs = (m.x >> 16) * kRowB;
-  const int nch = m.w & 0xffff;
+  const int nd = m.w & 0xffff;
   const double2 *rc = t.rec + m.y;
   const int4 *of = t.doff + (m.z >> 2);
   double sf, ss;
   const double2 hd = rc[0];
   if (m.w >> 16) {
     const double csf = rc[1].x;
-    dep_sums<true>(rc + 2, of, nch, Xb, sf, ss);
+    dep_sums<true>(rc + 2, of, nd, Xb, sf, ss);
     double xf = lds(Xb + rf) - sf;
     if (DINV) xf *= hd.x;
     double xs = fma(-csf, xf, lds(Xb + rs) - ss);
@@ -1107,7 +1148,7 @@ __device__ __forceinline__ void unit_solve(const UStage &t, const int4 m, char *
     *reinterpret_cast<double *>(Xb + rf) = xf;
     *reinterpret_cast<double *>(Xb + rs) = xs;
   } else {
-    dep_sums<false>(rc + 1, of, nch, Xb, sf, ss);
+    dep_sums<false>(rc + 1, of, nd, Xb, sf, ss);
     double xf = lds(Xb + rf) - sf;
     if (DINV) xf *= hd.x;
     *reinterpret_cast<double *>(Xb + rf) = xf;
@@ -1462,22 +1503,35 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   if (masked) {
     // Cartesian batch: only the block runs whose tile of this chunk is live (the
-    // others are identically zero); four chains over the live entries in order
+    // others are identically zero).  Every live entry goes to the chain the
+    // unmasked loops below give it ((e - e0) mod 4, the last (ex - e0) mod 4
+    // entries to chain 0), in the same order, so both paths are bitwise equal.
+    const int e0 = e, tail = ex - ((ex - e0) & 3);
     for (int g = h.fwd.grp_ptr[qoff], g1 = h.fwd.grp_ptr[qoff + 1]; g < g1; ++g) {
       const int ee = h.fwd.grp_end[g];
       if (!tile_live(h, h.fwd.grp_blk[g], blockIdx.y)) {
         e = ee;
         continue;
       }
-      for (; e + 4 <= ee; e += 4) {
-        const double x0 = G[(long long)h.fwd.dep[e] * h.ld + col], x1 = G[(long long)h.fwd.dep[e + 1] * h.ld + col];
-        const double x2 = G[(long long)h.fwd.dep[e + 2] * h.ld + col], x3 = G[(long long)h.fwd.dep[e + 3] * h.ld + col];
-        s0 = fma(val[e], x0, s0);
-        s1 = fma(val[e + 1], x1, s1);
-        s2 = fma(val[e + 2], x2, s2);
-        s3 = fma(val[e + 3], x3, s3);
+      for (; e < ee; e += 4) {   // (ends past ee: the next run restarts at ee)
+        double x[4], c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e + u < ee) {
+            c[u] = val[e + u];
+            x[u] = G[(long long)h.fwd.dep[e + u] * h.ld + col];
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e + u < ee) {
+            const int k = e + u >= tail ? 0 : ((e + u - e0) & 3);
+            if (k == 0) s0 = fma(c[u], x[u], s0);
+            else if (k == 1) s1 = fma(c[u], x[u], s1);
+            else if (k == 2) s2 = fma(c[u], x[u], s2);
+            else s3 = fma(c[u], x[u], s3);
+          }
       }
-      for (; e < ee; ++e) s0 = fma(val[e], G[(long long)h.fwd.dep[e] * h.ld + col], s0);
+      e = ee;
     }
     h.Tsep[(long long)a * h.ld + col] = v0 - ((s0 + s1) + (s2 + s3));
     return;
