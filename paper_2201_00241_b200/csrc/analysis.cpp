@@ -304,7 +304,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
     // emit one dependency list; returns the int4 meta; `hdr`: piece unit header
     // records.  Every dependency is a pair of tile rows (o0, o1) (byte offsets;
     // a one-value dependency repeats its row with a zero second coefficient);
-    // lists hold exactly the unit's dependencies, each starting at an even pair.
+    // lists hold the unit's dependencies padded to an even count (slots of two).
     auto emit = [&](const std::vector<int> &u, const std::vector<std::pair<int, int>> &du, bool hdr,
                     std::vector<int> *pos_rows, std::vector<int32_t> *pos_out) {
       const bool two = u.size() == 2;
@@ -327,9 +327,17 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         rec(fwd ? -1 : inv(f), (!fwd && two) ? inv(sr) : -1, fwd ? inv(f) : -1, (fwd && two) ? inv(sr) : -1);
         if (two) rec(coef(false, sr, f), -1, coef(true, sr, f), -1);
       }
-      const int nd = (int)du.size();   // exact count: no padding (r02: lists were padded to 4)
+      const int nd = (int)du.size();   // no padding to 4 (r02: lists were padded to chunks of 4)
+      const int ndp = nd + (nd & 1);    // even: dep_slots takes two dependencies per slot
       const int rowb = UnitSweep::kCols * 8;
-      for (int di = 0; di < nd; ++di) {
+      for (int di = 0; di < ndp; ++di) {
+        if (di >= nd) {   // padding: zero coefficients on the unit's own (finite) row
+          U.doff.push_back(A.loc_of[u[0]] * rowb);
+          U.doff.push_back(A.loc_of[u[0]] * rowb);
+          rec(-1, -1, -1, -1);
+          if (two) rec(-1, -1, -1, -1);
+          continue;
+        }
         const int k0 = du[di].first, nv = du[di].second, k1 = nv == 2 ? k0 + 1 : -1;
         U.doff.push_back(tile_row(k0) * rowb);
         U.doff.push_back(tile_row(nv == 2 ? k1 : k0) * rowb);   // one-value dependency: its row again, zero coefficient
@@ -345,8 +353,11 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
             for (int v = 0; v < nv; ++v) (*pos_out)[ti(u[ri]) * nt + ti(k0 + v)] = (int)(at + 2 * ri + v);
         }
       }
-      return std::array<int, 4>{A.loc_of[u[0]] | ((two ? A.loc_of[u[1]] : 0) << 16), cbeg, obeg,
-                                nd | ((two ? 1 : 0) << 16)};
+      // (x, y) tile byte offsets of the rows; z record byte offset; w offsets' byte
+      // offset | ndeps << 16 | two << 30
+      if (obeg * 4 >= (1 << 16) || ndp >= (1 << 14)) U.overflow = true;
+      return std::array<int, 4>{A.loc_of[u[0]] * rowb, two ? A.loc_of[u[1]] * rowb : 0, cbeg * 16,
+                                obeg * 4 | ndp << 16 | (two ? 1 << 30 : 0)};
     };
     for (int ui = 0; ui < (int)units.size(); ++ui) {
       const auto &u = units[ui];
@@ -383,7 +394,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         int r = 0;
         for (int u = lv[w]; u < lv[w + 1]; ++u) {
           const int *m = U.meta.data() + 4 * (ub + u);
-          r += (m[3] & 0xffff) * ((m[3] >> 16) ? 2 : 1);
+          r += ((m[3] >> 16) & 0x3fff) * ((m[3] >> 30) & 1 ? 2 : 1);
         }
         mu = std::max(mu, lv[w + 1] - lv[w]);
         mr = std::max(mr, r);
@@ -401,7 +412,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         double mx = 0, sm = 0;
         for (int w = 0; w < UnitSweep::kWarps; ++w) {
           double c = 0;
-          for (int u = lv[w]; u < lv[w + 1]; ++u) c += 6 + (U.meta[4 * (ub + u) + 3] & 0xffff);
+          for (int u = lv[w]; u < lv[w + 1]; ++u) c += 6 + ((U.meta[4 * (ub + u) + 3] >> 16) & 0x3fff);
           mx = std::max(mx, c);
           sm += c;
         }
@@ -418,7 +429,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
     long long wf_piece = 0, wf_tops = 0, deps = 0, real = 0;
     for (size_t u = 0; u < U.meta.size() / 4; ++u) {
       const int *m = U.meta.data() + 4 * u;
-      const int nd = m[3] & 0xffff, two = m[3] >> 16;
+      const int nd = (m[3] >> 16) & 0x3fff, two = (m[3] >> 30) & 1;
       wf_piece += nd * 4 + nd * (two ? 2 : 1) + (nd + 1) / 2 + (two ? 2 : 1) + 4 * (two ? 2 : 1) + 1;
       deps += nd;
     }
@@ -1499,6 +1510,7 @@ std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
   for (int s = A.bl_ptr[A.ref]; s < A.bl_ptr[A.ref + 1]; ++s) A.near_ref.push_back(A.bl_other[s]);
   sort_unique(A.near_ref);
   build_segments(A, Ls, Lrow, fpos, rmax);
+  if (A.ufwd.overflow || A.ubwd.overflow) return "block sweep schedule exceeds its 16-bit offset encoding";
   build_for_groups(A);
   return "";
 }

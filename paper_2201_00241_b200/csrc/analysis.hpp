@@ -70,13 +70,15 @@ struct UnitSweep {
   static constexpr int kMaxTopUnits = 16;   // one tops unit per warp
   std::vector<int32_t> unit_off;     // [nblk + 1] units of each block
   std::vector<int32_t> lvl;          // [nblk * kLvl], block-relative unit indices
-  // per unit (int4): row_f | row_s << 16 (tile rows, sweep order), first record
-  // (double2, block-relative), first dependency offset pair (int, block-
-  // relative, multiple of 4), ndeps | two_rows << 16.  A dependency is a
+  // per unit (int4): tile byte offsets of row_f and row_s (sweep order), byte
+  // offset of the first record (block-relative), byte offset of the first
+  // dependency offset pair (block-relative, multiple of 16) | ndeps << 16 |
+  // two_rows << 30.  A dependency is a
   // pair of tile-row byte offsets (o0, o1) and one (one-row unit) or two
   // (two-row unit) double2 coefficient records (c_f0, c_f1), (c_s0, c_s1);
-  // no padding (r02: lists padded to chunks of 4 read 2.5x the real
-  // dependencies in the forward sweeps).
+  // lists are padded to an even count (r02: to chunks of 4, which read 2.5x
+  // the real dependencies in the forward sweeps).
+  bool overflow = false;              // a field of the meta encoding overflowed (grid rejected)
   std::vector<int32_t> meta;
   std::vector<int32_t> tmeta;        // (unused: the tops' dense product runs on DMMA, see top_rows)
   std::vector<int32_t> tmeta_off;    // [nblk + 1] into tmeta (units)

@@ -1041,89 +1041,67 @@ struct UStage {
   const int4 *meta;
   const double *topM;    // [32][kTopLd] dense tops inverse of this sweep
   const int *toprow;     // [32] tile rows of the tops
-  const double2 *rec;
-  const int4 *doff;
   const int *lvl;
+  // 32-bit shared-window addresses of the hot loop (no generic -> shared
+  // conversions per access): X + lane * 8, unit records, dependency offsets
+  unsigned xs, rec, doff;
 };
 
-__device__ __forceinline__ double lds(const char *p) { return *reinterpret_cast<const double *>(p); }
-
-// sf = sum c_f x, ss = sum c_s x over a dependency list of `nch` chunks of 4
-// dependencies (tile-row byte offsets o0, o1; records (c_f0, c_f1) [, (c_s0,
-// c_s1)]).  Branch-free, two-deep FMA chains, fixed order (deterministic).
-template <bool TWO>
-__device__ __forceinline__ void dep_chunk(const double2 *__restrict__ rc, const int4 *__restrict__ of, const char *Xb,
-                                          double &f0, double &f1, double &f2, double &f3, double &s0, double &s1,
-                                          double &s2, double &s3) {
-  const int4 a = of[0], b = of[1];
-  const double x00 = lds(Xb + a.x), x01 = lds(Xb + a.y), x10 = lds(Xb + a.z), x11 = lds(Xb + a.w);
-  const double x20 = lds(Xb + b.x), x21 = lds(Xb + b.y), x30 = lds(Xb + b.z), x31 = lds(Xb + b.w);
-  if (TWO) {
-    const double2 p0 = rc[0], q0 = rc[1], p1 = rc[2], q1 = rc[3], p2 = rc[4], q2 = rc[5], p3 = rc[6], q3 = rc[7];
-    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1); s0 = fma(q0.x, x00, s0); s1 = fma(q0.y, x01, s1);
-    f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3); s2 = fma(q1.x, x10, s2); s3 = fma(q1.y, x11, s3);
-    f0 = fma(p2.x, x20, f0); f1 = fma(p2.y, x21, f1); s0 = fma(q2.x, x20, s0); s1 = fma(q2.y, x21, s1);
-    f2 = fma(p3.x, x30, f2); f3 = fma(p3.y, x31, f3); s2 = fma(q3.x, x30, s2); s3 = fma(q3.y, x31, s3);
-  } else {
-    const double2 p0 = rc[0], p1 = rc[1], p2 = rc[2], p3 = rc[3];
-    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1);
-    f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3);
-    f0 = fma(p2.x, x20, f0); f1 = fma(p2.y, x21, f1);
-    f2 = fma(p3.x, x30, f2); f3 = fma(p3.y, x31, f3);
-  }
+// shared-memory accesses of the unit sweeps by 32-bit shared addresses.  All
+// are volatile asm: they keep program order among themselves, which orders a
+// unit's result stores before the loads of later units that read them.
+__device__ __forceinline__ double ldsd(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double2 ldsd2(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int4 ldsi4(unsigned a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void stsd(unsigned a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
-// one or two dependencies (the tail of a list): dependency 0 -> chains (f0, f1),
-// dependency 1 -> chains (f2, f3), the chunk's assignment
-template <bool TWO, bool PAIR>
-__device__ __forceinline__ void dep_tail(const double2 *__restrict__ rc, const int2 *__restrict__ of, const char *Xb,
-                                         double &f0, double &f1, double &f2, double &f3, double &s0, double &s1,
-                                         double &s2, double &s3) {
-  const int2 a = of[0];
-  const double x00 = lds(Xb + a.x), x01 = lds(Xb + a.y);
-  double x10 = 0.0, x11 = 0.0;
-  if (PAIR) {
-    const int2 b = of[1];
-    x10 = lds(Xb + b.x);
-    x11 = lds(Xb + b.y);
-  }
-  if (TWO) {
-    const double2 p0 = rc[0], q0 = rc[1];
-    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1); s0 = fma(q0.x, x00, s0); s1 = fma(q0.y, x01, s1);
-    if (PAIR) {
-      const double2 p1 = rc[2], q1 = rc[3];
-      f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3); s2 = fma(q1.x, x10, s2); s3 = fma(q1.y, x11, s3);
-    }
-  } else {
-    const double2 p0 = rc[0];
-    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1);
-    if (PAIR) {
-      const double2 p1 = rc[1];
-      f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3);
-    }
-  }
-}
+// Unit meta (int4, UnitSweep): x = first row's tile byte offset, y = second
+// row's, z = first record's byte offset, w = dependency offsets' byte offset |
+// ndeps << 16 | two rows << 30 | paired with next << 31.  Dependencies come in
+// slots of two (lists padded to an even count): slot = one int4 of tile-row
+// byte offsets (o0, o1 of dependency 2k, then of 2k + 1) and two (one-row unit)
+// or four (two-row unit) double2 coefficient records.
+__device__ __forceinline__ int unit_ns(const int4 m) { return ((m.w >> 16) & 0x3fff) >> 1; }
+__device__ __forceinline__ bool unit_two(const int4 m) { return (m.w >> 30) & 1; }
 
-// sf = sum c_f x, ss = sum c_s x over a dependency list of exactly `nd`
-// dependencies (tile-row byte offsets o0, o1; records (c_f0, c_f1) [, (c_s0,
-// c_s1)]): chunks of 4, then a pair and / or a single.  The list starts at an
-// even dependency (int4 offset loads).  Branch-free inside a chunk, two-deep
-// FMA chains, fixed order (deterministic; the chain of every dependency is the
-// one the padded chunks of r02 gave it, so the sums are bitwise unchanged).
+// sf = sum c_f x, ss = sum c_s x over ns >= 1 slots.  Chains: dependency 2k ->
+// (f0, f1), 2k + 1 -> (f2, f3) (and s); slot 0 starts them (products, no zero
+// fill), fixed order (deterministic).
 template <bool TWO>
-__device__ __forceinline__ void dep_sums(const double2 *__restrict__ rc, const int4 *__restrict__ of, int nd,
-                                         const char *Xb, double &sf, double &ss) {
-  double f0 = 0.0, f1 = 0.0, f2 = 0.0, f3 = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-  int c = 0;
+__device__ __forceinline__ void dep_slots(const UStage &t, unsigned rc, unsigned of, int ns, double &sf, double &ss) {
+  double f0, f1, f2, f3, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  {
+    const int4 o = ldsi4(of);
+    const double2 p0 = ldsd2(rc), q0 = TWO ? ldsd2(rc + 16) : p0;
+    const double2 p1 = ldsd2(rc + (TWO ? 32 : 16)), q1 = TWO ? ldsd2(rc + 48) : p1;
+    const double x00 = ldsd(t.xs + o.x), x01 = ldsd(t.xs + o.y), x10 = ldsd(t.xs + o.z), x11 = ldsd(t.xs + o.w);
+    f0 = p0.x * x00; f1 = p0.y * x01; f2 = p1.x * x10; f3 = p1.y * x11;
+    if (TWO) { s0 = q0.x * x00; s1 = q0.y * x01; s2 = q1.x * x10; s3 = q1.y * x11; }
+  }
 #pragma unroll 1
-  for (; c + 4 <= nd; c += 4) dep_chunk<TWO>(rc + c * (TWO ? 2 : 1), of + c / 2, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
-  const int2 *of2 = reinterpret_cast<const int2 *>(of) + c;
-  rc += c * (TWO ? 2 : 1);
-  if (nd - c >= 2) {
-    dep_tail<TWO, true>(rc, of2, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
-    if (nd - c == 3) dep_tail<TWO, false>(rc + (TWO ? 4 : 2), of2 + 2, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
-  } else if (nd - c == 1) {
-    dep_tail<TWO, false>(rc, of2, Xb, f0, f1, f2, f3, s0, s1, s2, s3);
+  for (int k = 1; k < ns; ++k) {
+    rc += TWO ? 64 : 32;
+    of += 16;
+    const int4 o = ldsi4(of);
+    const double2 p0 = ldsd2(rc), q0 = TWO ? ldsd2(rc + 16) : p0;
+    const double2 p1 = ldsd2(rc + (TWO ? 32 : 16)), q1 = TWO ? ldsd2(rc + 48) : p1;
+    const double x00 = ldsd(t.xs + o.x), x01 = ldsd(t.xs + o.y), x10 = ldsd(t.xs + o.z), x11 = ldsd(t.xs + o.w);
+    f0 = fma(p0.x, x00, f0); f1 = fma(p0.y, x01, f1); f2 = fma(p1.x, x10, f2); f3 = fma(p1.y, x11, f3);
+    if (TWO) { s0 = fma(q0.x, x00, s0); s1 = fma(q0.y, x01, s1); s2 = fma(q1.x, x10, s2); s3 = fma(q1.y, x11, s3); }
   }
   sf = (f0 + f1) + (f2 + f3);
   ss = (s0 + s1) + (s2 + s3);
@@ -1131,38 +1109,37 @@ __device__ __forceinline__ void dep_sums(const double2 *__restrict__ rc, const i
 
 // one piece unit: x_f = (x_f - sum) d_f ; x_s = (x_s - sum - c_sf x_f) d_s
 template <bool DINV>
-__device__ __forceinline__ void unit_solve(const UStage &t, const int4 m, char *Xb) {
-  const int rf = (m.x & 0xffff) * kRowB, rs = (m.x >> 16) * kRowB;
-  const int nd = m.w & 0xffff;
-  const double2 *rc = t.rec + m.y;
-  const int4 *of = t.doff + (m.z >> 2);
-  double sf, ss;
-  const double2 hd = rc[0];
-  if (m.w >> 16) {
-    const double csf = rc[1].x;
-    dep_sums<true>(rc + 2, of, nd, Xb, sf, ss);
-    double xf = lds(Xb + rf) - sf;
+__device__ __forceinline__ void unit_solve(const UStage &t, const int4 m) {
+  const unsigned rc = t.rec + m.z, of = t.doff + (m.w & 0xffff);
+  const int ns = unit_ns(m);
+  const double2 hd = ldsd2(rc);
+  if (unit_two(m)) {
+    const double csf = ldsd(rc + 16);
+    double sf = 0.0, ss = 0.0;
+    if (ns) dep_slots<true>(t, rc + 32, of, ns, sf, ss);
+    double xf = ldsd(t.xs + m.x) - sf;
     if (DINV) xf *= hd.x;
-    double xs = fma(-csf, xf, lds(Xb + rs) - ss);
+    double xs = fma(-csf, xf, ldsd(t.xs + m.y) - ss);
     if (DINV) xs *= hd.y;
-    *reinterpret_cast<double *>(Xb + rf) = xf;
-    *reinterpret_cast<double *>(Xb + rs) = xs;
+    stsd(t.xs + m.x, xf);
+    stsd(t.xs + m.y, xs);
   } else {
-    dep_sums<false>(rc + 1, of, nd, Xb, sf, ss);
-    double xf = lds(Xb + rf) - sf;
+    double sf = 0.0, ss;
+    if (ns) dep_slots<false>(t, rc + 16, of, ns, sf, ss);
+    double xf = ldsd(t.xs + m.x) - sf;
     if (DINV) xf *= hd.x;
-    *reinterpret_cast<double *>(Xb + rf) = xf;
+    stsd(t.xs + m.x, xf);
   }
 }
 
 template <bool DINV>
-__device__ __forceinline__ void unit_pieces(const UStage &t, char *Xb, int warp) {
+__device__ __forceinline__ void unit_pieces(const UStage &t, int warp) {
   const int q0 = t.lvl[warp], q1 = t.lvl[warp + 1];
   int4 m = q0 < q1 ? t.meta[q0] : make_int4(0, 0, 0, 0);
 #pragma unroll 1
   for (int u = q0; u < q1; ++u) {
     const int4 mn = u + 1 < q1 ? t.meta[u + 1] : m;
-    unit_solve<DINV>(t, m, Xb);
+    unit_solve<DINV>(t, m);
     m = mn;
   }
 }
@@ -1172,7 +1149,7 @@ __device__ __forceinline__ void unit_pieces(const UStage &t, char *Xb, int warp)
 constexpr int kBlkThreads = UnitSweep::kWarps * 32;
 constexpr int kTopsLvl = UnitSweep::kWarps + 1;   // lvl[kWarps + 1], lvl[kWarps + 2]: tops units
 static_assert(UnitSweep::kMaxTopUnits <= 2 * UnitSweep::kWarps, "two tops units per warp at most");
-__device__ __forceinline__ void unit_tops(const UStage &t, char *Xb, const double *X, int warp, int lane) {
+__device__ __forceinline__ void unit_tops(const UStage &t, const double *X, int warp, int lane) {
   const int u0 = t.lvl[kTopsLvl], u1 = t.lvl[kTopsLvl + 1];
   if (u0 >= u1) return;
 #pragma unroll
@@ -1180,15 +1157,17 @@ __device__ __forceinline__ void unit_tops(const UStage &t, char *Xb, const doubl
     const int u = u0 + warp + k * UnitSweep::kWarps;
     if (u < u1) {
       const int4 m = t.meta[u];
-      const int rf = (m.x & 0xffff) * kRowB, rs = (m.x >> 16) * kRowB;
+      const unsigned rc = t.rec + m.z, of = t.doff + (m.w & 0xffff);
+      const int ns = unit_ns(m);
+      if (!ns) continue;
       double sf, ss;
-      if (m.w >> 16) {
-        dep_sums<true>(t.rec + m.y, t.doff + (m.z >> 2), m.w & 0xffff, Xb, sf, ss);
-        *reinterpret_cast<double *>(Xb + rf) = lds(Xb + rf) - sf;
-        *reinterpret_cast<double *>(Xb + rs) = lds(Xb + rs) - ss;
+      if (unit_two(m)) {
+        dep_slots<true>(t, rc, of, ns, sf, ss);
+        stsd(t.xs + m.x, ldsd(t.xs + m.x) - sf);
+        stsd(t.xs + m.y, ldsd(t.xs + m.y) - ss);
       } else {
-        dep_sums<false>(t.rec + m.y, t.doff + (m.z >> 2), m.w & 0xffff, Xb, sf, ss);
-        *reinterpret_cast<double *>(Xb + rf) = lds(Xb + rf) - sf;
+        dep_slots<false>(t, rc, of, ns, sf, ss);
+        stsd(t.xs + m.x, ldsd(t.xs + m.x) - sf);
       }
     }
   }
@@ -1319,15 +1298,15 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
   st.meta = reinterpret_cast<const int4 *>(smraw + h.smem_meta_off);
   st.topM = reinterpret_cast<const double *>(smraw + h.smem_tmeta_off);
   st.toprow = reinterpret_cast<const int *>(smraw + h.smem_tmeta_off + 32 * kTopLd * 8);
-  st.rec = reinterpret_cast<const double2 *>(smraw + h.smem_rec_off);
-  st.doff = reinterpret_cast<const int4 *>(smraw + h.smem_doff_off);
   st.lvl = reinterpret_cast<const int *>(smraw + h.smem_lvl_off);
+  st.xs = smem_u32(X) + lane * 8;
+  st.rec = smem_u32(smraw + h.smem_rec_off);
+  st.doff = smem_u32(smraw + h.smem_doff_off);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   unsigned parity = 0;
-  char *Xb = reinterpret_cast<char *>(X) + lane * 8;
   for (;;) {
     if (tid == 0) s_tk = atomicAdd(ctr, 1);
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // my previous stores have read X
@@ -1427,13 +1406,13 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     }
     const long long c_b = prof ? clock64() : 0;
     if (fwd) {
-      if (dinv) unit_pieces<true>(st, Xb, warp); else unit_pieces<false>(st, Xb, warp);
+      if (dinv) unit_pieces<true>(st, warp); else unit_pieces<false>(st, warp);
       __syncthreads();
-      unit_tops(st, Xb, X, warp, lane);
+      unit_tops(st, X, warp, lane);
     } else {
-      unit_tops(st, Xb, X, warp, lane);
+      unit_tops(st, X, warp, lane);
       const long long c_c = prof ? clock64() : 0;
-      if (dinv) unit_pieces<true>(st, Xb, warp); else unit_pieces<false>(st, Xb, warp);
+      if (dinv) unit_pieces<true>(st, warp); else unit_pieces<false>(st, warp);
       if (prof && lane == 0) {
         prof[warp] = (clock64() - c_c) | ((long long)(st.lvl[warp + 1] - st.lvl[warp]) << 48);
         if (warp == 0) {
