@@ -1107,26 +1107,30 @@ __device__ __forceinline__ void dep_slots(const UStage &t, unsigned rc, unsigned
   ss = (s0 + s1) + (s2 + s3);
 }
 
-// one piece unit: x_f = (x_f - sum) d_f ; x_s = (x_s - sum - c_sf x_f) d_s
+// one piece unit: x_f = (x_f - sum) d_f ; x_s = (x_s - sum - c_sf x_f) d_s.
+// A unit's own rows are written by nothing but the unit itself, so their
+// right-hand sides are read first (they leave the dependency chain).
 template <bool DINV>
 __device__ __forceinline__ void unit_solve(const UStage &t, const int4 m) {
   const unsigned rc = t.rec + m.z, of = t.doff + (m.w & 0xffff);
   const int ns = unit_ns(m);
   const double2 hd = ldsd2(rc);
   if (unit_two(m)) {
+    const double bf = ldsd(t.xs + m.x), bs = ldsd(t.xs + m.y);
     const double csf = ldsd(rc + 16);
     double sf = 0.0, ss = 0.0;
     if (ns) dep_slots<true>(t, rc + 32, of, ns, sf, ss);
-    double xf = ldsd(t.xs + m.x) - sf;
+    double xf = bf - sf;
     if (DINV) xf *= hd.x;
-    double xs = fma(-csf, xf, ldsd(t.xs + m.y) - ss);
+    double xs = fma(-csf, xf, bs - ss);
     if (DINV) xs *= hd.y;
     stsd(t.xs + m.x, xf);
     stsd(t.xs + m.y, xs);
   } else {
+    const double bf = ldsd(t.xs + m.x);
     double sf = 0.0, ss;
     if (ns) dep_slots<false>(t, rc + 16, of, ns, sf, ss);
-    double xf = ldsd(t.xs + m.x) - sf;
+    double xf = bf - sf;
     if (DINV) xf *= hd.x;
     stsd(t.xs + m.x, xf);
   }
@@ -1152,6 +1156,16 @@ static_assert(UnitSweep::kMaxTopUnits <= 2 * UnitSweep::kWarps, "two tops units 
 __device__ __forceinline__ void unit_tops(const UStage &t, const double *X, int warp, int lane) {
   const int u0 = t.lvl[kTopsLvl], u1 = t.lvl[kTopsLvl + 1];
   if (u0 >= u1) return;
+  // the product's A fragments and B row offsets do not depend on X: loaded
+  // before the gather, so the DMMA chain below waits on X loads only
+  const int gid = lane >> 2, tig = lane & 3, mt = warp >> 1, nb = (warp & 1) * 2;
+  double a[UnitSweep::kTopRows / 4];
+  int br[UnitSweep::kTopRows / 4];
+#pragma unroll
+  for (int k = 0; k < UnitSweep::kTopRows / 4; ++k) {
+    a[k] = t.topM[(mt * 8 + gid) * kTopLd + k * 4 + tig];
+    br[k] = t.toprow[k * 4 + tig] * kBC + nb * 8 + gid;
+  }
 #pragma unroll
   for (int k = 0; k < 2; ++k) {   // gather: t_T = X_T - (dependencies outside the tops)
     const int u = u0 + warp + k * UnitSweep::kWarps;
@@ -1174,14 +1188,17 @@ __device__ __forceinline__ void unit_tops(const UStage &t, const double *X, int 
   __syncthreads();
   // X_T = M t_T: 32 x 32 (tops rows x tile columns) on the fp64 tensor cores;
   // warp = one 8-row tile x two 8-column tiles, k in steps of 4 (8 DMMA each)
-  const int gid = lane >> 2, tig = lane & 3, mt = warp >> 1, nb = (warp & 1) * 2;
+  double b[UnitSweep::kTopRows / 4][2];
+#pragma unroll
+  for (int k = 0; k < UnitSweep::kTopRows / 4; ++k) {
+    b[k][0] = X[br[k]];
+    b[k][1] = X[br[k] + 8];
+  }
   double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int k = 0; k < UnitSweep::kTopRows / 4; ++k) {
-    const double a = t.topM[(mt * 8 + gid) * kTopLd + k * 4 + tig];
-    const int br = t.toprow[k * 4 + tig] * kBC;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) dmma_8x8x4(c[j][0], c[j][1], a, X[br + (nb + j) * 8 + gid]);
+    for (int j = 0; j < 2; ++j) dmma_8x8x4(c[j][0], c[j][1], a[k], b[k][j]);
   }
   __syncthreads();
   const int nt = t.lvl[kTopsLvl + 2];   // tops rows
