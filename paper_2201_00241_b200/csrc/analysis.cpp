@@ -1511,6 +1511,98 @@ std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
   sort_unique(A.near_ref);
   build_segments(A, Ls, Lrow, fpos, rmax);
   if (A.ufwd.overflow || A.ubwd.overflow) return "block sweep schedule exceeds its 16-bit offset encoding";
+  {  // separator runs per block (U^T sweep epilogue partials; analysis.hpp sr_*)
+    const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
+    struct Run { int g, e0, e1; };
+    std::vector<std::vector<Run>> per(A.nblk);
+    int g = 0;
+    for (int q = qb; q < qe; ++q) {
+      int e = A.fwd.rptr[q];
+      while (e < A.fwd.rext[q]) {
+        int f = e;
+        const int b = A.seg_of[A.fwd.dep[e]];
+        while (f < A.fwd.rext[q] && A.seg_of[A.fwd.dep[f]] == b) ++f;
+        per[b].push_back({g++, e, f});
+        e = f;
+      }
+    }
+    A.sr_nruns = g;
+    A.sr_off.assign(A.nblk + 1, 0);
+    A.sr_init.clear();
+    A.sr_ent_slot.clear();
+    A.sr_ent_src.clear();
+    A.sr_ent_trow.clear();
+    constexpr int kHdr = 3;   // header slots: 12 ints, warp w's runs are run slots [wr[w], wr[w + 1])
+    for (int b = 0; b < A.nblk; ++b) {
+      const int base = A.sr_off[b], nr = (int)per[b].size();
+      // runs onto the k_blk warps by LPT on their entry counts (+ a per-run latency)
+      std::vector<int> ord(nr), wof(nr);
+      std::iota(ord.begin(), ord.end(), 0);
+      std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
+        return per[b][x].e1 - per[b][x].e0 > per[b][y].e1 - per[b][y].e0;
+      });
+      std::vector<long long> load(UnitSweep::kWarps, 0);
+      for (int i : ord) {
+        const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+        load[w] += 4 + per[b][i].e1 - per[b][i].e0;
+        wof[i] = w;
+      }
+      std::vector<Run> runs;
+      std::vector<int> wr(kHdr * 4, 0);
+      for (int w = 0; w < UnitSweep::kWarps; ++w) {
+        wr[w] = (int)runs.size();
+        for (int i = 0; i < nr; ++i)
+          if (wof[i] == w) runs.push_back(per[b][i]);
+      }
+      wr[UnitSweep::kWarps] = (int)runs.size();
+      if (nr) A.sr_init.insert(A.sr_init.end(), wr.begin(), wr.end());
+      int k = base + (nr ? kHdr : 0) + nr;   // first entry slot
+      for (const Run &r : runs) {
+        A.sr_init.insert(A.sr_init.end(), {r.g, k - base, r.e1 - r.e0, 0});
+        for (int e = r.e0; e < r.e1; ++e, ++k) {
+          A.sr_ent_slot.push_back(k);
+          A.sr_ent_src.push_back(e);
+          A.sr_ent_trow.push_back(A.loc_of[A.fwd.dep[e]] * UnitSweep::kCols * 8);
+        }
+      }
+      A.sr_init.resize(4 * (size_t)k, 0);
+      A.sr_off[b + 1] = k;
+    }
+  }
+  if (getenv("RH_DEBUG_SCHED")) {   // separator gather statistics
+    const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
+    long long ext = 0, loc = 0, runs = 0;
+    std::set<int> rows;
+    for (int q = qb; q < qe; ++q) {
+      for (int e = A.fwd.rptr[q]; e < A.fwd.rext[q]; ++e) {
+        rows.insert(A.fwd.dep[e]);
+        if (e == A.fwd.rptr[q] || A.seg_of[A.fwd.dep[e]] != A.seg_of[A.fwd.dep[e - 1]]) ++runs;
+      }
+      ext += A.fwd.rext[q] - A.fwd.rptr[q];
+      loc += A.fwd.rptr[q + 1] - A.fwd.rext[q];
+    }
+    {
+      std::vector<long long> pb(A.nblk, 0), rb(A.nblk, 0);
+      long long mxrun = 0, n32 = 0;
+      for (int q = qb; q < qe; ++q) {
+        int e = A.fwd.rptr[q];
+        while (e < A.fwd.rext[q]) {
+          int f = e;
+          const int b = A.seg_of[A.fwd.dep[e]];
+          while (f < A.fwd.rext[q] && A.seg_of[A.fwd.dep[f]] == b) ++f;
+          pb[b] += f - e;
+          rb[b]++;
+          mxrun = std::max<long long>(mxrun, f - e);
+          if (f - e > 32) n32 += f - e - 32;
+          e = f;
+        }
+      }
+      fprintf(stderr, "separator runs: max entries per block %lld, max runs per block %lld, max run %lld, entries beyond 32 %lld\n",
+              *std::max_element(pb.begin(), pb.end()), *std::max_element(rb.begin(), rb.end()), mxrun, n32);
+    }
+    fprintf(stderr, "separator: rows %d, external entries %lld (distinct block rows %zu, runs %lld), local entries %lld, S slots %zu\n",
+            qe - qb, ext, rows.size(), runs, loc, A.sb_src.size());
+  }
   build_for_groups(A);
   return "";
 }

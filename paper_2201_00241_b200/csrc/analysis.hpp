@@ -217,6 +217,16 @@ struct Analysis {
   // separator block S (Schur complement after R_B1), densified for its inversion
   std::vector<int32_t> sb_src;              // [nslots] F positions of separator-column entries of separator rows
   std::vector<int32_t> sb_dense;            // [nslots] row-major position in the dense ns x ns block
+  // U^T sweep epilogue partials (k_blk MODE_UT): the separator rows' external entries
+  // in runs of one block (runs numbered in separator-row order, as k_sep_gather reads
+  // them); per block a record region of 16-byte slots [3 header slots: warp w's runs
+  // are run slots [wr[w], wr[w + 1]) (LPT on entries) | run table | entries], staged
+  // behind the block rows: run slot (g, first entry slot, entries, 0), entry slot
+  // (U^T value, tile byte offset of the block row) filled per state
+  std::vector<int32_t> sr_off;              // [nblk + 1] record slots
+  std::vector<int32_t> sr_init;             // [4 * slots] run slots' ints, entry slots 0
+  std::vector<int32_t> sr_ent_slot, sr_ent_src, sr_ent_trow;   // per entry: slot, fwd entry e, tile byte offset
+  int sr_nruns = 0;
 };
 
 // Returns "" on success, else an error message (grid rejected).

@@ -62,7 +62,12 @@ struct SegParams {
   const double *vL, *vUt;             // separator rows' L / U^T values (fwd entry order)
   int ns, sep_off;                     // separator rows, first separator slot in row_global
   const double *Sinv, *SinvT;          // dense [ns][ns] inverse of the separator block L_ss U_ss (+ transpose)
-  double *Tsep;                        // [ns][ld] separator right-hand sides
+  double *Tsep;                        // [ns][ld] separator right-hand sides, then the run partials:
+  // U^T sweep epilogue (k_blk MODE_UT): Part[g] = sum over run g's entries (one block's
+  // rows) of U^T value x P row, [nruns][ld] behind Tsep; k_sep_gather (UTLT) sums the runs
+  int nruns;
+  const int *sr_off;                   // per block: its record slots (analysis.hpp sr_*)
+  const double2 *sr_rec;               // [run table (g, first entry slot, entries) | entries (value, tile offset)]
   const int *blk_gp_ptr, *blk_gp_loc;  // per block: local rows with G_p entries
   const double *W;                   // [n_p][ldw]; null for a Cartesian block (icol)
   long long ldw;

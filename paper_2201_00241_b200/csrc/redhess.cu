@@ -915,6 +915,13 @@ __global__ void k_gather_gpe(int n, const int *__restrict__ src, const int *__re
 }
 
 // copy factor values into the sweep value arrays (entry order of the sweeps)
+// entry slots of the per-block separator run records: (U^T value, tile byte offset)
+__global__ void k_sr_fill(int n, const int *__restrict__ slot, const int *__restrict__ src,
+                          const int *__restrict__ trow, const double *__restrict__ vUt, double2 *rec) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) rec[slot[k]] = make_double2(vUt[src[k]], __longlong_as_double((long long)trow[k]));
+}
+
 __global__ void k_gather_vals(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < n) dst[e] = src[e] >= 0 ? F[src[e]] : 0.0;   // src < 0: padding entry
@@ -1063,6 +1070,11 @@ __device__ __forceinline__ double2 ldsd2(unsigned a) {
 __device__ __forceinline__ int4 ldsi4(unsigned a) {
   int4 v;
   asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int ldsi(unsigned a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ void stsd(unsigned a, double v) {
@@ -1353,6 +1365,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     const int rb = U.rec_off[s], nrec = U.rec_off[s + 1] - rb;
     const int ob = U.doff_off[s], nof = U.doff_off[s + 1] - ob;
     const int nxrows = mode == MODE_L ? 0 : nr + nxr;
+    const int nsr = mode == MODE_UT && h.nruns > 0 ? h.sr_off[s + 1] - h.sr_off[s] : 0;   // run record slots
     // block rows by 2D TMA boxes (64, then 8 rows), the rest (< 8 block rows, staged
     // separator rows) by 16-byte cp.async
     const char *tm = reinterpret_cast<const char *>(G == h.Z ? h.tmZ : h.tmP);
@@ -1363,7 +1376,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     if (tid == 0) {
       const double *dM = lsw ? h.tL : mode == MODE_U ? h.tU : mode == MODE_UT ? h.tUt : h.tLt;
       const unsigned tx = (first ? 16u * (nu + nrec) + 4u * nof + 4u * UnitSweep::kLvl + 32u * kTopLd * 8 + 128u +
-                                       (mode == MODE_L ? 16u * (h.gpe_off[s + 1] - h.gpe_off[s]) + 48u : 0u)
+                                       (mode == MODE_L ? 16u * (h.gpe_off[s + 1] - h.gpe_off[s]) + 48u : 0u) +
+                                       16u * nsr
                                  : 0u) +
                           (unsigned)rows_tma * kRowB;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx)
@@ -1375,6 +1389,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
       bulk_g2s(smraw + h.smem_rec_off, vals + rb, 16u * nrec, &mbar);
       if (nof) bulk_g2s(smraw + h.smem_doff_off, U.doff + ob, 4u * nof, &mbar);
       bulk_g2s(smraw + h.smem_lvl_off, U.lvl + s * UnitSweep::kLvl, 4u * UnitSweep::kLvl, &mbar);
+      if (nsr)   // U^T: the block's separator run records behind its rows (kept across chunks)
+        bulk_g2s(X + nr * kBC, h.sr_rec + h.sr_off[s], 16u * nsr, &mbar);
       if (mode == MODE_L) {   // G_p entry records + warp ranges, behind the block's rows (kept across chunks)
         const int g0 = h.gpe_off[s], ng = h.gpe_off[s + 1] - g0;
         if (ng) bulk_g2s(X + nr * kBC, h.gpe_rec + g0, 16u * ng, &mbar);
@@ -1456,6 +1472,39 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
       for (int a = rows_st + tid; a < nr; a += blockDim.x)
         bulk_s2g(G + (long long)(r0 + a) * h.ld + col0, X + a * kBC, kRowB);
     }
+    if (nsr) {
+      // separator right-hand-side partials of this block's runs (k_sep_gather UTLT
+      // sums them; X is read while the bulk stores above read it too): Part[g] = sum
+      // of U^T value x P row over run g's entries, in order (entry k -> chain k & 1),
+      // from the run records staged behind the rows
+      double *part = h.Tsep + (long long)h.ns * h.ld;
+      const unsigned rr = smem_u32(X + nr * kBC);
+      const int rw0 = ldsi(rr + 4 * warp), rw1 = ldsi(rr + 4 * warp + 4);   // this warp's runs (LPT)
+      for (int r = rw0; r < rw1; ++r) {
+        const int4 rt = ldsi4(rr + 16 * (3 + r));
+        double a0 = 0.0, a1 = 0.0;
+        int k = 0;
+        for (; k + 4 <= rt.z; k += 4) {   // four entries' loads in flight
+          const unsigned ea = rr + 16 * (rt.y + k);
+          const double2 n0 = ldsd2(ea), n1 = ldsd2(ea + 16), n2 = ldsd2(ea + 32), n3 = ldsd2(ea + 48);
+          const double x0 = ldsd(st.xs + (int)__double_as_longlong(n0.y));
+          const double x1 = ldsd(st.xs + (int)__double_as_longlong(n1.y));
+          const double x2 = ldsd(st.xs + (int)__double_as_longlong(n2.y));
+          const double x3 = ldsd(st.xs + (int)__double_as_longlong(n3.y));
+          a0 = fma(n0.x, x0, a0);
+          a1 = fma(n1.x, x1, a1);
+          a0 = fma(n2.x, x2, a0);
+          a1 = fma(n3.x, x3, a1);
+        }
+        for (; k < rt.z; ++k) {
+          const double2 en = ldsd2(rr + 16 * (rt.y + k));
+          const double x = ldsd(st.xs + (int)__double_as_longlong(en.y));
+          if (k & 1) a1 = fma(en.x, x, a1);
+          else a0 = fma(en.x, x, a0);
+        }
+        part[(long long)rt.x * h.ld + col0 + lane] = a0 + a1;
+      }
+    }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }   // column chunks of the ticket
   }
@@ -1497,6 +1546,23 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
   int e = h.fwd.rptr[q];
   const int ex = h.fwd.rext[q];
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (mode == MODE_UTLT) {
+    // the U^T sweep left one partial per run (k_blk MODE_UT epilogue): sum them in run order
+    const double *part = h.Tsep + (long long)h.ns * h.ld + col;
+    const int g0 = h.fwd.grp_ptr[qoff], g1 = h.fwd.grp_ptr[qoff + 1];
+    int g = g0;
+    for (; g + 4 <= g1; g += 4) {
+      const double x0 = part[(long long)g * h.ld], x1 = part[(long long)(g + 1) * h.ld];
+      const double x2 = part[(long long)(g + 2) * h.ld], x3 = part[(long long)(g + 3) * h.ld];
+      s0 += x0;
+      s1 += x1;
+      s2 += x2;
+      s3 += x3;
+    }
+    for (; g < g1; ++g) s0 += part[(long long)g * h.ld];
+    h.Tsep[(long long)a * h.ld + col] = v0 - ((s0 + s1) + (s2 + s3));
+    return;
+  }
   if (masked) {
     // Cartesian batch: only the block runs whose tile of this chunk is live (the
     // others are identically zero).  Every live entry goes to the chain the
@@ -2176,6 +2242,9 @@ struct rh_ctx {
   cudaEvent_t ev_vl = nullptr;   // separator rows' L / U^T values ready (after R_B1)
   bool early_gathered = false;   // the fused call's early batches also formed their separator rhs
   double *grad_tsep = nullptr;
+  int nruns = 0, n_sr_ent = 0;                 // separator external-entry runs (one block each), entries
+  int *sr_off = nullptr, *sr_ent_slot = nullptr, *sr_ent_src = nullptr, *sr_ent_trow = nullptr;
+  double2 *sr_rec = nullptr;                   // per-block record regions (run slots static, entries per state)
   int *grad_ctr = nullptr;
   cudaEvent_t tape_wait = nullptr;   // set while a fused call enqueues its batches
   // side stream of the fused call: block-only derived values done; each early L sweep done
@@ -2281,6 +2350,7 @@ int blk_max_rows(const Analysis &A) {   // tile rows, incl. the L sweep's G_p en
   for (int s = 0; s < A.nblk; ++s) {
     const int nr = A.seg_row_off[s + 1] - A.seg_row_off[s], ne = A.gpe_off[s + 1] - A.gpe_off[s];
     m = std::max(m, nr + (16 * ne + 48 + kRowB - 1) / kRowB);
+    m = std::max(m, nr + (16 * (A.sr_off[s + 1] - A.sr_off[s]) + kRowB - 1) / kRowB);   // U^T: separator run records
   }
   return m;
 }
@@ -2394,6 +2464,19 @@ int upload(rh_ctx *c) {
           ge.back() = e + 1;
         }
       gp.push_back((int)gb.size());
+    }
+    {  // U^T sweep epilogue partials: per-block record regions (analysis.hpp sr_*)
+      c->nruns = A.sr_nruns;
+      c->n_sr_ent = (int)A.sr_ent_src.size();
+      std::vector<int32_t> init(A.sr_init);
+      if (init.empty()) init.assign(4, 0);
+      chk(c->sr_off = dalloc_copy(A.sr_off, P));
+      chk(c->sr_rec = reinterpret_cast<double2 *>(dalloc_copy(init, P)));
+      if (c->n_sr_ent) {
+        chk(c->sr_ent_slot = dalloc_copy(A.sr_ent_slot, P));
+        chk(c->sr_ent_src = dalloc_copy(A.sr_ent_src, P));
+        chk(c->sr_ent_trow = dalloc_copy(A.sr_ent_trow, P));
+      }
     }
     if (gb.empty()) gb.push_back(0), ge.push_back(0);
     int *g1, *g2, *g3;
@@ -2648,7 +2731,7 @@ int upload(rh_ctx *c) {
 
 int ensure_tsep(rh_ctx *c, int ld, int k = 0) {
   auto &w = c->ws[k];
-  const size_t need = (size_t)ld * (size_t)std::max(1, c->A.sep_rows);
+  const size_t need = (size_t)ld * (size_t)(std::max(1, c->A.sep_rows) + c->nruns);   // Tsep + run partials
   if (need <= w.tsep_elems) return RH_OK;
   c->drop_graph();   // the captured fused call points at the old buffer
   if (w.Tsep) cudaFree(w.Tsep);
@@ -2803,6 +2886,9 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.sep_off = A.seg_row_off[A.nblk];
   h.Sinv = c->Sinv;
   h.Tsep = c->ws[k].Tsep;
+  h.nruns = c->nruns;
+  h.sr_off = c->sr_off;
+  h.sr_rec = c->sr_rec;
   h.blk_gp_ptr = c->blk_gp_ptr;
   h.blk_gp_loc = c->blk_gp_loc;
   if (const char *env = getenv("RH_DEBUG")) h.debug = atoi(env);  // timing experiments only
@@ -3507,6 +3593,11 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
         RH_LAUNCHED(c);
         k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_b + e0, c->F_val, c->vUt + e0);
         RH_LAUNCHED(c);
+        if (c->n_sr_ent) {   // U^T values into the per-block run record regions (k_blk MODE_UT epilogue)
+          k_sr_fill<<<nblk(c->n_sr_ent), kThreads, 0, st>>>(c->n_sr_ent, c->sr_ent_slot, c->sr_ent_src,
+                                                              c->sr_ent_trow, c->vUt, c->sr_rec);
+          RH_LAUNCHED(c);
+        }
       }
     }
     if (early && side) {   // the early batches' separator right-hand sides need these values, not S^-1
@@ -3617,7 +3708,7 @@ int gradient_impl(rh_ctx *c, double *grad_p, double *lambda_out, cudaStream_t st
   h.P = c->X1col;
   if (own_ws) {
     if (!c->grad_tsep) {
-      if (cudaMalloc(&c->grad_tsep, sizeof(double) * kSegC * std::max(1, A.sep_rows)) != cudaSuccess ||
+      if (cudaMalloc(&c->grad_tsep, sizeof(double) * kSegC * (std::max(1, A.sep_rows) + c->nruns)) != cudaSuccess ||
           cudaMalloc(&c->grad_ctr, 16 * sizeof(int)) != cudaSuccess || cudaMemset(c->grad_ctr, 0, 16 * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         return fail(c, RH_E_NOMEM, "gradient workspace allocation failed");
