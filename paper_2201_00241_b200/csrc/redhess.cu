@@ -3875,16 +3875,26 @@ int num_ws(int nb, int cap = kNumWs) {
 }
 
 // batch b of ncols columns split into nb balanced batches: [a0, a1)
-// front = full batches of N first, the remainder last (host copies: the last
-// batch's copy is the tail nothing overlaps, so it should be the smallest)
-inline void batch_range(int ncols, int nb, int b, int &a0, int &a1, int N = 0, bool front = false) {
-  if (front) {
-    a0 = std::min(ncols, b * N);
-    a1 = std::min(ncols, (b + 1) * N);
-    return;
-  }
+inline void batch_range(int ncols, int nb, int b, int &a0, int &a1) {
   a0 = (int)((long long)ncols * b / nb);
   a1 = (int)((long long)ncols * (b + 1) / nb);
+}
+
+// batch bounds of a host-copy call: full batches of N first, then the remainder
+// split into pieces of <= tail columns (the last batch's copy is the tail that
+// nothing overlaps, so it should be small)
+std::vector<int> host_cuts(int ncols, int N) {
+  std::vector<int> cuts(1, 0);
+  if (ncols <= 0) return cuts;
+  int tail = std::max(32, N / 2), first = N;   // (e2e probe, case9241: 1 stream, tail N/2: 2.58 -> 2.35 ms)
+  if (const char *env = getenv("RH_E2E_TAIL")) tail = std::max(32, atoi(env));     // tuning override
+  if (const char *env = getenv("RH_E2E_FIRST")) first = std::max(32, atoi(env));   // tuning override
+  int a = 0;
+  if (ncols > first && first < N) cuts.push_back(a = first);   // an early first block for the copy stream
+  while (ncols - a > N) cuts.push_back(a += N);
+  const int r = ncols - a, np = (r + tail - 1) / tail;
+  for (int q = 1; q <= np; ++q) cuts.push_back(a + (int)((long long)r * q / np));
+  return cuts;
 }
 
 // `early`: the first `early` batches already ran their first block sweep (phase 1,
@@ -3892,12 +3902,20 @@ inline void batch_range(int ncols, int nb, int b, int &a0, int &a1, int N = 0, b
 int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, int transposed, cudaStream_t st,
                     double *Hhost, int early = 0) {
   const int ncols = j1 - j0;
-  const int nb = (ncols + N - 1) / N;
-  // with host copies, 2 compute streams: staggered batches finish one after the
-  // other, and each finished column block travels on a copy stream while later
-  // batches compute (no compute stream waits behind a copy); 3 concurrent
-  // batches would finish together and leave the copies to the tail
-  const int nws = num_ws(nb, Hhost ? 2 : kNumWs);
+  int nb = (ncols + N - 1) / N;
+  std::vector<int> cuts;   // batch bounds (host copies only)
+  if (Hhost) {
+    cuts = host_cuts(ncols, N);
+    nb = (int)cuts.size() - 1;
+  }
+  // with host copies, one compute stream: batches finish one after the other,
+  // and each finished column block travels on a copy stream while later batches
+  // compute (the D2H of H, 1.2 ms on case9241, is the e2e bound: it should start
+  // as early as possible); concurrent batches would finish together and leave
+  // the copies to the tail
+  int host_streams = 1;   // host copies: batches one after another, each copied while the next computes
+  if (const char *env = getenv("RH_E2E_STREAMS")) host_streams = std::max(1, atoi(env));   // tuning override
+  const int nws = num_ws(nb, Hhost ? host_streams : kNumWs);
   if (Hhost) {
     if (!c->cp_st) RH_CUDA(c, cudaStreamCreateWithFlags(&c->cp_st, cudaStreamNonBlocking));
     if (!c->ev_cp) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_cp, cudaEventDisableTiming));
@@ -3913,7 +3931,12 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
   }
   for (int b = 0; b < nb; ++b) {
     int a0, a1;
-    batch_range(ncols, nb, b, a0, a1, N, Hhost != nullptr);
+    if (Hhost) {
+      a0 = cuts[b];
+      a1 = cuts[b + 1];
+    } else {
+      batch_range(ncols, nb, b, a0, a1);
+    }
     double *out = transposed ? H + (long long)a0 * ldh : H + a0;
     const int k = b % nws;
     cudaStream_t sb = k ? c->sti[k] : st;
@@ -3974,12 +3997,20 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   if (j0 < 0 || j1 > np_ || j0 > j1 || N <= 0) return fail(c, RH_E_ARG, "bad column range / N");
   if ((!transposed && ldh < j1 - j0) || (transposed && ldh < np_)) return fail(c, RH_E_ARG, "ldh too small");
   RH_CUDA(c, cudaSetDevice(c->device));
-  const int ncols = j1 - j0, nb = ncols > 0 ? (ncols + N - 1) / N : 0;
-  const int early = nb > 0 ? std::min(nb, num_ws(nb, Hhost ? 2 : kNumWs)) : 0;
+  const int ncols = j1 - j0;
+  const std::vector<int> cuts = Hhost ? host_cuts(ncols, N) : std::vector<int>();
+  const int nb = Hhost ? (int)cuts.size() - 1 : ncols > 0 ? (ncols + N - 1) / N : 0;
+  int host_streams = 1;   // as hessian_batches
+  if (const char *env = getenv("RH_E2E_STREAMS")) host_streams = std::max(1, atoi(env));   // tuning override
+  const int early = nb > 0 ? std::min(nb, num_ws(nb, Hhost ? host_streams : kNumWs)) : 0;
   // the widest batch actually run (front-loaded batches of N for host copies,
   // else ceil(ncols / nb)), not the caller's N: a shard or N > n_p must not
   // allocate workspaces no batch uses
-  const int wmax = nb > 0 ? (Hhost ? std::min(N, ncols) : (ncols + nb - 1) / nb) : 0;
+  int wmax = 0;
+  if (Hhost)
+    for (int b = 0; b < nb; ++b) wmax = std::max(wmax, cuts[b + 1] - cuts[b]);
+  else if (nb > 0)
+    wmax = (ncols + nb - 1) / nb;
   const int ld = (wmax + kBC - 1) / kBC * kBC;
   for (int k = 0; k < early; ++k)   // allocate before anything is enqueued
     if (int rc = ensure_ws(c, ld, k)) return rc;
@@ -3992,7 +4023,12 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
     if (stage == 2 && getenv("RH_NO_EARLY_GATHER")) return RH_OK;
     for (int b = 0; b < early; ++b) {
       int a0, a1;
-      batch_range(ncols, nb, b, a0, a1, N, Hhost != nullptr);
+      if (Hhost) {
+        a0 = cuts[b];
+        a1 = cuts[b + 1];
+      } else {
+        batch_range(ncols, nb, b, a0, a1);
+      }
       double *out = transposed ? H + (long long)a0 * ldh : H + a0;
       if (int rc = hvp_impl(c, nullptr, 0, j0 + a0, out, ldh, transposed, a1 - a0, sb, nullptr, nullptr, nullptr, 0,
                             b, stage == 1 ? 1 : 3))
