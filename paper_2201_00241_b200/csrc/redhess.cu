@@ -1943,40 +1943,76 @@ __global__ void k_for_tape(int nslots, int nout, const int2 *slots, const int *o
 // transposed layout (H^T rows, the multi-GPU slabs) is written 256 B per warp
 // store instead of one 8-byte sector per lane.
 __global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
+  // HW = Y_p + G_p^T Psi (SpMulAdd).  Warp w takes four
+  // consecutive p rows (cp0 + 4w ..), whose G_p column entries are contiguous
+  // in the CSC arrays: the lanes load them together (one round trip for rows and
+  // values), then the Psi row loads of up to 8 entries are in flight at once and
+  // each entry's FMA goes to its p row in entry order (the order of a one-row
+  // loop: same sums).  Lane = batch column.
   __shared__ double T[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int cp0 = blockIdx.x * 32, col = blockIdx.y * 32 + lane;
-#pragma unroll 1
-  for (int r = warp; r < 32; r += kThreads / 32) {
-    const int cp = cp0 + r;
-    double acc = 0.0;
-    if (cp < h.n_p) {
-      // Y_p: a Pg row is the cost diagonal 2 c2 w (from W); a v row was written by k_for
-      const double c2x2 = h.pdiag[cp];
-      const bool pg = c2x2 != 0.0 || h.p_kind[cp] == RH_KIND_PG;
-      acc = pg ? c2x2 * load_W(h, cp, col) : h.Yp[(long long)cp * h.ld + col];
-      const int q0 = h.gpc_ptr[cp], q1 = h.gpc_ptr[cp + 1];
-      for (int q = q0; q < q1; q += 4) {   // four G_p entries' Psi loads in flight, FMAs in entry order
-        double g[4], xv[4];
+  // blockIdx.x = column chunk (fastest: the CTAs of one p group read whole Psi
+  // rows together), blockIdx.y = p group
+  const int cp0 = blockIdx.y * 32, col = blockIdx.x * 32 + lane;
+  const int rb = cp0 + 4 * warp;   // this warp's first p row
+  int ptr = 0;
+  double c2x2 = 0.0;
+  int kind = 0;
+  if (lane < 5) ptr = h.gpc_ptr[min(rb + lane, h.n_p)];
+  if (lane < 4 && rb + lane < h.n_p) {
+    c2x2 = h.pdiag[rb + lane];
+    kind = h.p_kind[rb + lane];
+  }
+  const int b0 = __shfl_sync(0xffffffffu, ptr, 0), b1 = __shfl_sync(0xffffffffu, ptr, 1);
+  const int b2 = __shfl_sync(0xffffffffu, ptr, 2), b3 = __shfl_sync(0xffffffffu, ptr, 3);
+  const int b4 = __shfl_sync(0xffffffffu, ptr, 4);
+  double acc[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const bool in = q + k < q1;
-          g[k] = in ? h.gpc_val[q + k] : 0.0;
-          xv[k] = in ? h.P[(long long)h.gpc_row[q + k] * h.ld + col] : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (q + k < q1) acc = fma(g[k], xv[k], acc);
-      }
-      if (!h.transposed && col < h.N) h.HW[hw_index(h, cp, col)] = acc;
+  for (int j = 0; j < 4; ++j) {   // Y_p: a Pg row is the cost diagonal 2 c2 w (from W); a v row was written by k_for
+    const double cj = __shfl_sync(0xffffffffu, c2x2, j);
+    const int kj = __shfl_sync(0xffffffffu, kind, j);
+    const int cp = rb + j;
+    acc[j] = cp < h.n_p ? ((cj != 0.0 || kj == RH_KIND_PG) ? cj * load_W(h, cp, col) : h.Yp[(long long)cp * h.ld + col])
+                        : 0.0;
+  }
+  for (int base = b0; base < b4; base += 32) {
+    const int n = min(32, b4 - base);
+    int er = 0;
+    double ev = 0.0;
+    if (lane < n) {
+      er = h.gpc_row[base + lane];
+      ev = h.gpc_val[base + lane];
     }
-    T[r][lane] = acc;
+    for (int k0 = 0; k0 < n; k0 += 8) {
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int row = __shfl_sync(0xffffffffu, er, (k0 + k) & 31);
+        x[k] = k0 + k < n ? h.P[(long long)row * h.ld + col] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double v = __shfl_sync(0xffffffffu, ev, (k0 + k) & 31);
+        if (k0 + k >= n) break;
+        const int e = base + k0 + k;   // entry -> its p row (warp-uniform)
+        if (e < b1) acc[0] = fma(v, x[k], acc[0]);
+        else if (e < b2) acc[1] = fma(v, x[k], acc[1]);
+        else if (e < b3) acc[2] = fma(v, x[k], acc[2]);
+        else acc[3] = fma(v, x[k], acc[3]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int cp = rb + j;
+    if (!h.transposed && cp < h.n_p && col < h.N) h.HW[hw_index(h, cp, col)] = acc[j];
+    T[4 * warp + j][lane] = acc[j];
   }
   if (!h.transposed) return;
   __syncthreads();
 #pragma unroll 1
   for (int c = warp; c < 32; c += kThreads / 32) {   // H^T row of column c, p rows cp0 .. cp0 + 31
-    const int cc = blockIdx.y * 32 + c;
+    const int cc = blockIdx.x * 32 + c;
     if (cc < h.N && cp0 + lane < h.n_p) h.HW[hw_index(h, cp0 + lane, cc)] = T[lane][c];
   }
 }
@@ -3019,7 +3055,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   const int gA = (int)std::min<long long>(((h.debug & 64) ? 1LL : 2LL) * c->nsm, (long long)nb * (ld / kBC));   // debug 64: 1 CTA/SM (experiment)
   const dim3 gSg(nblk(A.sep_rows, kThreads / 32), ld / 32),
       gSm((ld + GBN - 1) / GBN, (A.sep_rows + GBM - 1) / GBM);
-  const dim3 gF((int)A.fg.grp_nout.size(), ld / 32), gM((A.n_p + 31) / 32, ld / 32);
+  const dim3 gF((int)A.fg.grp_nout.size(), ld / 32), gM(ld / 32, (A.n_p + 31) / 32);   // k_muladd: column chunks fastest
   const int nx = A.n_x;
   const long long tot = (long long)nx * N;
   cudaEvent_t ev[9];
