@@ -127,6 +127,7 @@ struct FactParams {
   double *dinv, *rowmax;             // per permuted row
   int *status;
   double pivtol;
+  int sep_maxlen;                    // R_B1: longest separator row of F (shared-memory staging)
   long long *dbg;                    // timing experiment (RH_DEBUG & 128): per-block phase stamps, else null
 };
 

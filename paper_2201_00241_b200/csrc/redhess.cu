@@ -536,29 +536,61 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
 // R_B1: one warp per separator row: the updates from block columns (rows of
 // blocks are final).  Afterwards the separator x separator entries hold the
 // Schur complement.
+// R_B1: a warp per separator row, the row staged in shared memory (max row
+// length f.sep_maxlen), its k-steps against the block columns in order; each
+// step's U row values and target offsets (<= 32 of them: one per lane) are
+// loaded one step ahead, so only the shared-memory multiplier stays on the
+// chain (r02: the row lived in global memory, one L2 round trip per step).
 __global__ void __launch_bounds__(kThreads) k_fact_sep_rows(FactParams f) {
-  const int lane = threadIdx.x & 31;
+  extern __shared__ double fsr[];   // [kThreads / 32][sep_maxlen]
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= f.ns) return;
   const int q = f.seg_row_off[f.nblk] + a;
   const int i = f.row_global[q];
-  const int rb = f.F_rowptr[i], re = f.F_rowptr[i + 1];
-  double *w = f.F_val + rb;
+  const int rb = f.F_rowptr[i], re = f.F_rowptr[i + 1], len = re - rb;
+  double *ws = fsr + (size_t)wl * f.sep_maxlen;
   double amax = 0.0;
-  for (int e = rb + lane; e < re; e += 32) amax = fmax(amax, fabs(f.F_val[e]));
+  for (int e = lane; e < len; e += 32) {
+    const double v = f.F_val[rb + e];
+    ws[e] = v;
+    amax = fmax(amax, fabs(v));
+  }
   amax = warp_max(amax);
   if (lane == 0) f.rowmax[i] = amax;
+  __syncwarp();
   const int4 *gks = reinterpret_cast<const int4 *>(f.ks4);
-  for (int ks = f.ks_ptr[q]; ks < f.ks_ptr[q + 1]; ++ks) {
-    const int4 m = gks[ks];
-    const double lik = w[m.x] * f.dinv[f.ks_k[ks]];
+  const int k0 = f.ks_ptr[q], k1 = f.ks_ptr[q + 1];
+  // step ks's (meta, 1 / pivot, first 32 U values and target offsets) in registers
+  int4 m = make_int4(0, 0, 0, 0);
+  double dk = 0.0, u0 = 0.0;
+  int t0 = 0;
+  auto fetch = [&](int ks, int4 &mm, double &dd, double &uu, int &tt) {
+    mm = gks[ks];
+    dd = f.dinv[f.ks_k[ks]];
+    if (lane < mm.z) {
+      uu = f.F_val[mm.y + 1 + lane];
+      tt = f.tgt16[mm.w + lane];
+    }
+  };
+  if (k0 < k1) fetch(k0, m, dk, u0, t0);
+  for (int ks = k0; ks < k1; ++ks) {
+    int4 mn = m;
+    double dn = 0.0, un = 0.0;
+    int tn = 0;
+    if (ks + 1 < k1) fetch(ks + 1, mn, dn, un, tn);
+    const double lik = ws[m.x] * dk;
     __syncwarp();
-    if (lane == 0) w[m.x] = lik;
-    const double *uk = f.F_val + m.y + 1;
-    const unsigned short *tg = f.tgt16 + m.w;
-    for (int t = lane; t < m.z; t += 32) w[tg[t]] -= lik * uk[t];
+    if (lane == 0) ws[m.x] = lik;
+    if (lane < m.z) ws[t0] -= lik * u0;
+    for (int t = 32 + lane; t < m.z; t += 32) ws[f.tgt16[m.w + t]] -= lik * f.F_val[m.y + 1 + t];
     __syncwarp();
+    m = mn;
+    dk = dn;
+    u0 = un;
+    t0 = tn;
   }
+  for (int e = lane; e < len; e += 32) f.F_val[rb + e] = ws[e];
 }
 
 // ----------------------------------------------------------------------------
@@ -2278,6 +2310,7 @@ struct rh_ctx {
   cudaEvent_t ev_vl = nullptr;   // separator rows' L / U^T values ready (after R_B1)
   bool early_gathered = false;   // the fused call's early batches also formed their separator rhs
   double *grad_tsep = nullptr;
+  int sep_maxlen = 1;                          // longest separator row of F (k_fact_sep_rows staging)
   int nruns = 0, n_sr_ent = 0;                 // separator external-entry runs (one block each), entries
   int *sr_off = nullptr, *sr_ent_slot = nullptr, *sr_ent_src = nullptr, *sr_ent_trow = nullptr;
   double2 *sr_rec = nullptr;                   // per-block record regions (run slots static, entries per state)
@@ -2755,6 +2788,17 @@ int upload(rh_ctx *c) {
   cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
   if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 16 * kNumWs * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->grid_bar, 0, 2 * sizeof(unsigned));
+  {  // R_B1 stages each separator row in shared memory (k_fact_sep_rows)
+    int ml = 1;
+    for (int q = A.seg_row_off[A.nblk]; q < A.seg_row_off[A.nblk + 1]; ++q) {
+      const int r = A.row_global[q];
+      ml = std::max(ml, A.F_rowptr[r + 1] - A.F_rowptr[r]);
+    }
+    c->sep_maxlen = ml;
+    const size_t sm = sizeof(double) * (kThreads / 32) * ml;
+    if (sm > 48 * 1024 && e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_fact_sep_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  }
   {  // co-resident CTAs of k_sep_inverse (cooperative launch)
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sep_inverse, 256, gj_smem_bytes());
@@ -3618,7 +3662,8 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   }
   if (A.sep_rows > 0) {
     dbg_mark(st, "side stream forked");
-    k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, 0, st>>>(f);
+    f.sep_maxlen = c->sep_maxlen;
+    k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, sizeof(double) * (kThreads / 32) * f.sep_maxlen, st>>>(f);
     RH_LAUNCHED(c);
     {  // separator rows' entries of the forward pattern (k_sep_gather): L and U^T values
        // (final after R_B1; the Gauss-Jordan inverse below does not touch F)
