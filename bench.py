@@ -565,8 +565,9 @@ def main():
     def stage_roofline(kind):
         """Per-stage device times of one Alg. 2 batch of width N (CUDA events the library
         records around each kernel, on the stream they run on): kind 'cartesian' = the
-        full Hessian's first N columns (what the timed step runs), 'random' = W ~ N(0, 1)."""
-        Hc = torch.empty((n_p, min(N, n_p)), dtype=torch.float64, device=dev)
+        full Hessian's first N columns written as a transposed slab (what the timed step
+        runs), 'random' = W ~ N(0, 1)."""
+        Hc = torch.empty((min(N, n_p), n_p), dtype=torch.float64, device=dev)   # transposed slab, as the step
         ctx.set_timing(True)
         st_ = np.zeros(9)
         reps_t = 5
@@ -574,7 +575,7 @@ def main():
             if flush is not None:
                 flush.fill_(1.0)
             if kind == "cartesian":
-                ctx.hessian_columns(0, min(N, n_p), N, H=Hc)
+                ctx.hessian_columns(0, min(N, n_p), N, H=Hc, transposed=True)
             else:
                 ctx.hvp(W, HW)
             st_ += ctx.stage_times()

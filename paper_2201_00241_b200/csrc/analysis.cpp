@@ -982,6 +982,52 @@ void build_segments(Analysis &A, const std::vector<std::vector<int32_t>> &Ls,
 
 }  // namespace
 
+// epilogue partial runs (Analysis::RunRecs): per block, its runs packed onto
+// the k_blk warps by LPT on their entry counts (+ a per-run latency)
+struct PRun {
+  int g;
+  std::vector<std::pair<int, int>> ent;   // (coefficient source, tile byte offset)
+};
+void build_run_recs(Analysis::RunRecs &R, const std::vector<std::vector<PRun>> &per, int nruns) {
+  constexpr int kHdr = 3;   // header slots: 12 ints, warp w's runs are run slots [wr[w], wr[w + 1])
+  const int nb = (int)per.size();
+  R = Analysis::RunRecs();
+  R.nruns = nruns;
+  R.off.assign(nb + 1, 0);
+  for (int b = 0; b < nb; ++b) {
+    const int base = R.off[b], nr = (int)per[b].size();
+    std::vector<int> ord(nr), wof(nr);
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return per[b][x].ent.size() > per[b][y].ent.size(); });
+    std::vector<long long> load(UnitSweep::kWarps, 0);
+    for (int i : ord) {
+      const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      load[w] += 4 + (long long)per[b][i].ent.size();
+      wof[i] = w;
+    }
+    std::vector<const PRun *> runs;
+    std::vector<int> wr(kHdr * 4, 0);
+    for (int w = 0; w < UnitSweep::kWarps; ++w) {
+      wr[w] = (int)runs.size();
+      for (int i = 0; i < nr; ++i)
+        if (wof[i] == w) runs.push_back(&per[b][i]);
+    }
+    wr[UnitSweep::kWarps] = (int)runs.size();
+    if (nr) R.init.insert(R.init.end(), wr.begin(), wr.end());
+    int k = base + (nr ? kHdr : 0) + nr;   // first entry slot
+    for (const PRun *r : runs) {
+      R.init.insert(R.init.end(), {r->g, k - base, (int)r->ent.size(), 0});
+      for (const auto &en : r->ent) {
+        R.ent_slot.push_back(k++);
+        R.ent_src.push_back(en.first);
+        R.ent_trow.push_back(en.second);
+      }
+    }
+    R.init.resize(4 * (size_t)k, 0);
+    R.off[b + 1] = k;
+  }
+}
+
 std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
   std::ostringstream err;
   const int n = g.n_bus, m = g.n_line, ng = g.n_gen;
@@ -1511,63 +1557,46 @@ std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
   sort_unique(A.near_ref);
   build_segments(A, Ls, Lrow, fpos, rmax);
   if (A.ufwd.overflow || A.ubwd.overflow) return "block sweep schedule exceeds its 16-bit offset encoding";
-  {  // separator runs per block (U^T sweep epilogue partials; analysis.hpp sr_*)
+  {  // epilogue partial runs of the U^T and L^T sweeps (analysis.hpp RunRecs)
+    const int rowb = UnitSweep::kCols * 8;
+    // separator rows' external entries, runs of one block in separator-row order
+    std::vector<std::vector<PRun>> per(A.nblk);
     const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
-    struct Run { int g, e0, e1; };
-    std::vector<std::vector<Run>> per(A.nblk);
     int g = 0;
     for (int q = qb; q < qe; ++q) {
       int e = A.fwd.rptr[q];
       while (e < A.fwd.rext[q]) {
-        int f = e;
         const int b = A.seg_of[A.fwd.dep[e]];
-        while (f < A.fwd.rext[q] && A.seg_of[A.fwd.dep[f]] == b) ++f;
-        per[b].push_back({g++, e, f});
-        e = f;
+        PRun r{g++, {}};
+        for (; e < A.fwd.rext[q] && A.seg_of[A.fwd.dep[e]] == b; ++e) r.ent.push_back({e, A.loc_of[A.fwd.dep[e]] * rowb});
+        per[b].push_back(std::move(r));
       }
     }
-    A.sr_nruns = g;
-    A.sr_off.assign(A.nblk + 1, 0);
-    A.sr_init.clear();
-    A.sr_ent_slot.clear();
-    A.sr_ent_src.clear();
-    A.sr_ent_trow.clear();
-    constexpr int kHdr = 3;   // header slots: 12 ints, warp w's runs are run slots [wr[w], wr[w + 1])
-    for (int b = 0; b < A.nblk; ++b) {
-      const int base = A.sr_off[b], nr = (int)per[b].size();
-      // runs onto the k_blk warps by LPT on their entry counts (+ a per-run latency)
-      std::vector<int> ord(nr), wof(nr);
-      std::iota(ord.begin(), ord.end(), 0);
-      std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) {
-        return per[b][x].e1 - per[b][x].e0 > per[b][y].e1 - per[b][y].e0;
-      });
-      std::vector<long long> load(UnitSweep::kWarps, 0);
-      for (int i : ord) {
-        const int w = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-        load[w] += 4 + per[b][i].e1 - per[b][i].e0;
-        wof[i] = w;
+    build_run_recs(A.sr, per, g);
+    // G_p columns' block entries, runs of one block per column (blocks ascending)
+    per.assign(A.nblk, {});
+    A.ma_run_ptr.assign(1, 0);
+    A.ma_sep_ptr.assign(1, 0);
+    A.ma_sep_q.clear();
+    g = 0;
+    for (int j = 0; j < A.n_p; ++j) {
+      std::vector<std::pair<int, int>> bq;   // (block, q) of the column's block entries, CSC order within a block
+      for (int q = A.gpc_ptr[j]; q < A.gpc_ptr[j + 1]; ++q) {
+        const int sg = A.seg_of[A.gpc_row[q]];
+        if (sg == A.nblk) A.ma_sep_q.push_back(q);
+        else bq.push_back({sg, q});
       }
-      std::vector<Run> runs;
-      std::vector<int> wr(kHdr * 4, 0);
-      for (int w = 0; w < UnitSweep::kWarps; ++w) {
-        wr[w] = (int)runs.size();
-        for (int i = 0; i < nr; ++i)
-          if (wof[i] == w) runs.push_back(per[b][i]);
+      std::stable_sort(bq.begin(), bq.end(), [](const std::pair<int, int> &x, const std::pair<int, int> &y) { return x.first < y.first; });
+      for (size_t i = 0; i < bq.size();) {
+        const int b = bq[i].first;
+        PRun r{g++, {}};
+        for (; i < bq.size() && bq[i].first == b; ++i) r.ent.push_back({bq[i].second, A.loc_of[A.gpc_row[bq[i].second]] * rowb});
+        per[b].push_back(std::move(r));
       }
-      wr[UnitSweep::kWarps] = (int)runs.size();
-      if (nr) A.sr_init.insert(A.sr_init.end(), wr.begin(), wr.end());
-      int k = base + (nr ? kHdr : 0) + nr;   // first entry slot
-      for (const Run &r : runs) {
-        A.sr_init.insert(A.sr_init.end(), {r.g, k - base, r.e1 - r.e0, 0});
-        for (int e = r.e0; e < r.e1; ++e, ++k) {
-          A.sr_ent_slot.push_back(k);
-          A.sr_ent_src.push_back(e);
-          A.sr_ent_trow.push_back(A.loc_of[A.fwd.dep[e]] * UnitSweep::kCols * 8);
-        }
-      }
-      A.sr_init.resize(4 * (size_t)k, 0);
-      A.sr_off[b + 1] = k;
+      A.ma_run_ptr.push_back(g);
+      A.ma_sep_ptr.push_back((int)A.ma_sep_q.size());
     }
+    build_run_recs(A.ma, per, g);
   }
   if (getenv("RH_DEBUG_SCHED")) {   // separator gather statistics
     const int qb = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk]], qe = A.fwd.lvl_ptr[A.fwd.seg_lvl[A.nblk + 1] - 1];
@@ -1597,7 +1626,23 @@ std::string analyze(const ::rh_grid &g, Analysis &A, int rmax) {
           e = f;
         }
       }
-      fprintf(stderr, "separator runs: max entries per block %lld, max runs per block %lld, max run %lld, entries beyond 32 %lld\n",
+      {
+      long long runs = 0, single = 0, sepent = 0, ent = 0;
+      for (int j = 0; j < A.n_p; ++j) {
+        std::set<int> sg;
+        for (int q = A.gpc_ptr[j]; q < A.gpc_ptr[j + 1]; ++q) {
+          const int sgm = A.seg_of[A.gpc_row[q]];
+          sg.insert(sgm);
+          ++ent;
+          if (sgm == A.nblk) ++sepent;
+        }
+        runs += (long long)sg.size() - (sg.count(A.nblk) ? 1 : 0);
+        single += sg.size() == 1 && !sg.count(A.nblk);
+      }
+      fprintf(stderr, "G_p columns: %d, entries %lld (separator %lld), block runs %lld, single-block columns %lld\n", A.n_p, ent,
+              sepent, runs, single);
+    }
+    fprintf(stderr, "separator runs: max entries per block %lld, max runs per block %lld, max run %lld, entries beyond 32 %lld\n",
               *std::max_element(pb.begin(), pb.end()), *std::max_element(rb.begin(), rb.end()), mxrun, n32);
     }
     fprintf(stderr, "separator: rows %d, external entries %lld (distinct block rows %zu, runs %lld), local entries %lld, S slots %zu\n",

@@ -217,16 +217,30 @@ struct Analysis {
   // separator block S (Schur complement after R_B1), densified for its inversion
   std::vector<int32_t> sb_src;              // [nslots] F positions of separator-column entries of separator rows
   std::vector<int32_t> sb_dense;            // [nslots] row-major position in the dense ns x ns block
-  // U^T sweep epilogue partials (k_blk MODE_UT): the separator rows' external entries
-  // in runs of one block (runs numbered in separator-row order, as k_sep_gather reads
-  // them); per block a record region of 16-byte slots [3 header slots: warp w's runs
-  // are run slots [wr[w], wr[w + 1]) (LPT on entries) | run table | entries], staged
-  // behind the block rows: run slot (g, first entry slot, entries, 0), entry slot
-  // (U^T value, tile byte offset of the block row) filled per state
-  std::vector<int32_t> sr_off;              // [nblk + 1] record slots
-  std::vector<int32_t> sr_init;             // [4 * slots] run slots' ints, entry slots 0
-  std::vector<int32_t> sr_ent_slot, sr_ent_src, sr_ent_trow;   // per entry: slot, fwd entry e, tile byte offset
-  int sr_nruns = 0;
+  // Epilogue partials of the block sweeps (k_blk): runs = (output row, block)
+  // pairs, each a list of entries (coefficient, block row); per block a record
+  // region of 16-byte slots [3 header slots: warp w's runs are run slots
+  // [wr[w], wr[w + 1]) (LPT on entries) | run table (g, first entry slot,
+  // entries, 0) | entries (coefficient, tile byte offset of the block row)],
+  // staged behind the tile's rows; entry coefficients are filled per state.
+  struct RunRecs {
+    int nruns = 0;
+    std::vector<int32_t> off;                         // [nblk + 1] record slots
+    std::vector<int32_t> init;                        // [4 * slots] run slots' ints, entry slots 0
+    std::vector<int32_t> ent_slot, ent_src, ent_trow; // per entry: slot, coefficient source, tile byte offset
+  };
+  // U^T sweep (MODE_UT): the separator rows' external entries in runs of one
+  // block (runs numbered in separator-row order, as k_sep_gather reads them);
+  // coefficient source = fwd entry e (U^T value)
+  RunRecs sr;
+  // L^T sweep (MODE_LT): G_p^T Psi of SpMulAdd, G_p column entries in runs of
+  // one block (runs numbered by p column, blocks ascending); coefficient source
+  // = CSC position q (G_p value).  Separator entries of each column are added
+  // by k_muladd from Psi itself.
+  RunRecs ma;
+  std::vector<int32_t> ma_run_ptr;   // [n_p + 1] runs of each p column
+  std::vector<int32_t> ma_sep_ptr;   // [n_p + 1] into ma_sep_q
+  std::vector<int32_t> ma_sep_q;     // CSC positions of separator-row entries
 };
 
 // Returns "" on success, else an error message (grid rejected).

@@ -68,6 +68,12 @@ struct SegParams {
   int nruns;
   const int *sr_off;                   // per block: its record slots (analysis.hpp sr_*)
   const double2 *sr_rec;               // [run table (g, first entry slot, entries) | entries (value, tile offset)]
+  // L^T sweep epilogue (k_blk MODE_LT): Mp[g] = sum over G_p run g's entries (one
+  // p column's rows in one block) of G_p value x Psi row; k_muladd adds the runs
+  const int *ma_off;
+  const double2 *ma_rec;
+  double *Mp;                          // [ma runs][ld], null: no partials (gradient sweeps)
+  const int *ma_run_ptr, *ma_sep_ptr, *ma_sep_q;   // per p column: its runs; its separator entries (CSC q)
   const int *blk_gp_ptr, *blk_gp_loc;  // per block: local rows with G_p entries
   const double *W;                   // [n_p][ldw]; null for a Cartesian block (icol)
   long long ldw;

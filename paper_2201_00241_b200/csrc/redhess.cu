@@ -533,10 +533,9 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
   }
 }
 
-// R_B1: one warp per separator row: the updates from block columns (rows of
-// blocks are final).  Afterwards the separator x separator entries hold the
-// Schur complement.
-// R_B1: a warp per separator row, the row staged in shared memory (max row
+// R_B1: the separator rows' updates from block columns (rows of blocks are
+// final); afterwards the separator x separator entries hold the Schur
+// complement.  A warp per separator row, the row staged in shared memory (max row
 // length f.sep_maxlen), its k-steps against the block columns in order; each
 // step's U row values and target offsets (<= 32 of them: one per lane) are
 // loaded one step ahead, so only the shared-memory multiplier stays on the
@@ -947,11 +946,11 @@ __global__ void k_gather_gpe(int n, const int *__restrict__ src, const int *__re
 }
 
 // copy factor values into the sweep value arrays (entry order of the sweeps)
-// entry slots of the per-block separator run records: (U^T value, tile byte offset)
+// entry slots of the per-block epilogue run records: (coefficient, tile byte offset)
 __global__ void k_sr_fill(int n, const int *__restrict__ slot, const int *__restrict__ src,
-                          const int *__restrict__ trow, const double *__restrict__ vUt, double2 *rec) {
+                          const int *__restrict__ trow, const double *__restrict__ val, double2 *rec) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) rec[slot[k]] = make_double2(vUt[src[k]], __longlong_as_double((long long)trow[k]));
+  if (k < n) rec[slot[k]] = make_double2(val[src[k]], __longlong_as_double((long long)trow[k]));
 }
 
 __global__ void k_gather_vals(int n, const int *__restrict__ src, const double *__restrict__ F, double *dst) {
@@ -1397,7 +1396,12 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     const int rb = U.rec_off[s], nrec = U.rec_off[s + 1] - rb;
     const int ob = U.doff_off[s], nof = U.doff_off[s + 1] - ob;
     const int nxrows = mode == MODE_L ? 0 : nr + nxr;
-    const int nsr = mode == MODE_UT && h.nruns > 0 ? h.sr_off[s + 1] - h.sr_off[s] : 0;   // run record slots
+    // epilogue partial runs (analysis.hpp RunRecs): U^T -> separator right-hand
+    // sides, L^T -> G_p^T Psi; their records staged behind the tile's rows
+    const bool ep_ut = mode == MODE_UT && h.nruns > 0, ep_lt = mode == MODE_LT && h.Mp;
+    const int *roff = ep_lt ? h.ma_off : h.sr_off;
+    const int nsr = ep_ut || ep_lt ? roff[s + 1] - roff[s] : 0;   // run record slots
+    const int rrow = ep_lt ? nr + nxr : nr;                        // their first tile row
     // block rows by 2D TMA boxes (64, then 8 rows), the rest (< 8 block rows, staged
     // separator rows) by 16-byte cp.async
     const char *tm = reinterpret_cast<const char *>(G == h.Z ? h.tmZ : h.tmP);
@@ -1421,8 +1425,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
       bulk_g2s(smraw + h.smem_rec_off, vals + rb, 16u * nrec, &mbar);
       if (nof) bulk_g2s(smraw + h.smem_doff_off, U.doff + ob, 4u * nof, &mbar);
       bulk_g2s(smraw + h.smem_lvl_off, U.lvl + s * UnitSweep::kLvl, 4u * UnitSweep::kLvl, &mbar);
-      if (nsr)   // U^T: the block's separator run records behind its rows (kept across chunks)
-        bulk_g2s(X + nr * kBC, h.sr_rec + h.sr_off[s], 16u * nsr, &mbar);
+      if (nsr)   // the block's run records behind its rows (kept across chunks)
+        bulk_g2s(X + rrow * kBC, (ep_lt ? h.ma_rec : h.sr_rec) + roff[s], 16u * nsr, &mbar);
       if (mode == MODE_L) {   // G_p entry records + warp ranges, behind the block's rows (kept across chunks)
         const int g0 = h.gpe_off[s], ng = h.gpe_off[s + 1] - g0;
         if (ng) bulk_g2s(X + nr * kBC, h.gpe_rec + g0, 16u * ng, &mbar);
@@ -1505,12 +1509,12 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
         bulk_s2g(G + (long long)(r0 + a) * h.ld + col0, X + a * kBC, kRowB);
     }
     if (nsr) {
-      // separator right-hand-side partials of this block's runs (k_sep_gather UTLT
-      // sums them; X is read while the bulk stores above read it too): Part[g] = sum
-      // of U^T value x P row over run g's entries, in order (entry k -> chain k & 1),
-      // from the run records staged behind the rows
-      double *part = h.Tsep + (long long)h.ns * h.ld;
-      const unsigned rr = smem_u32(X + nr * kBC);
+      // partials of this block's runs (U^T: separator right-hand sides, k_sep_gather
+      // UTLT sums them; L^T: G_p^T Psi, k_muladd sums them; X is read while the bulk
+      // stores above read it too): Part[g] = sum of coefficient x tile row over run
+      // g's entries, in order (entry k -> chain k & 1), from the staged run records
+      double *part = ep_lt ? h.Mp : h.Tsep + (long long)h.ns * h.ld;
+      const unsigned rr = smem_u32(X + rrow * kBC);
       const int rw0 = ldsi(rr + 4 * warp), rw1 = ldsi(rr + 4 * warp + 4);   // this warp's runs (LPT)
       for (int r = rw0; r < rw1; ++r) {
         const int4 rt = ldsi4(rr + 16 * (3 + r));
@@ -1976,28 +1980,30 @@ __global__ void k_for_tape(int nslots, int nout, const int2 *slots, const int *o
 // store instead of one 8-byte sector per lane.
 __global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
   // HW = Y_p + G_p^T Psi (SpMulAdd).  Warp w takes four
-  // consecutive p rows (cp0 + 4w ..), whose G_p column entries are contiguous
-  // in the CSC arrays: the lanes load them together (one round trip for rows and
-  // values), then the Psi row loads of up to 8 entries are in flight at once and
-  // each entry's FMA goes to its p row in entry order (the order of a one-row
-  // loop: same sums).  Lane = batch column.
+  // consecutive p rows (cp0 + 4w ..).  G_p^T Psi: the L^T sweep left one partial
+  // row per (p column, block) run (Mp, k_blk MODE_LT epilogue; runs numbered by
+  // p column, so the four rows' runs are contiguous): the partials are added in
+  // run order, then the entries on separator rows (Psi rows, CSC order).
+  // Without partials (h.Mp null) every G_p entry is taken from Psi (CSC order).
+  // Lane = batch column; up to 8 row loads in flight.
   __shared__ double T[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // blockIdx.x = column chunk (fastest: the CTAs of one p group read whole Psi
+  // blockIdx.x = column chunk (fastest: the CTAs of one p group read whole
   // rows together), blockIdx.y = p group
   const int cp0 = blockIdx.y * 32, col = blockIdx.x * 32 + lane;
   const int rb = cp0 + 4 * warp;   // this warp's first p row
-  int ptr = 0;
+  const int *rptr = h.Mp ? h.ma_run_ptr : h.gpc_ptr;   // runs (partials) or all CSC entries
+  int ptr = 0, sptr = 0;
   double c2x2 = 0.0;
   int kind = 0;
-  if (lane < 5) ptr = h.gpc_ptr[min(rb + lane, h.n_p)];
+  if (lane < 5) {
+    ptr = rptr[min(rb + lane, h.n_p)];
+    if (h.Mp) sptr = h.ma_sep_ptr[min(rb + lane, h.n_p)];
+  }
   if (lane < 4 && rb + lane < h.n_p) {
     c2x2 = h.pdiag[rb + lane];
     kind = h.p_kind[rb + lane];
   }
-  const int b0 = __shfl_sync(0xffffffffu, ptr, 0), b1 = __shfl_sync(0xffffffffu, ptr, 1);
-  const int b2 = __shfl_sync(0xffffffffu, ptr, 2), b3 = __shfl_sync(0xffffffffu, ptr, 3);
-  const int b4 = __shfl_sync(0xffffffffu, ptr, 4);
   double acc[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {   // Y_p: a Pg row is the cost diagonal 2 c2 w (from W); a v row was written by k_for
@@ -2007,30 +2013,52 @@ __global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
     acc[j] = cp < h.n_p ? ((cj != 0.0 || kj == RH_KIND_PG) ? cj * load_W(h, cp, col) : h.Yp[(long long)cp * h.ld + col])
                         : 0.0;
   }
-  for (int base = b0; base < b4; base += 32) {
-    const int n = min(32, b4 - base);
-    int er = 0;
-    double ev = 0.0;
-    if (lane < n) {
-      er = h.gpc_row[base + lane];
-      ev = h.gpc_val[base + lane];
-    }
-    for (int k0 = 0; k0 < n; k0 += 8) {
-      double x[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int row = __shfl_sync(0xffffffffu, er, (k0 + k) & 31);
-        x[k] = k0 + k < n ? h.P[(long long)row * h.ld + col] : 0.0;
+  // pass 0: runs (partials) or all entries; pass 1 (partials only): separator entries
+  for (int pass = 0; pass < (h.Mp ? 2 : 1); ++pass) {
+    const int pv = pass ? sptr : ptr;
+    const int b0 = __shfl_sync(0xffffffffu, pv, 0), b1 = __shfl_sync(0xffffffffu, pv, 1);
+    const int b2 = __shfl_sync(0xffffffffu, pv, 2), b3 = __shfl_sync(0xffffffffu, pv, 3);
+    const int b4 = __shfl_sync(0xffffffffu, pv, 4);
+    const bool partials = h.Mp && !pass;
+    for (int base = b0; base < b4; base += 32) {
+      const int n = min(32, b4 - base);
+      long long er = 0;   // row offset (elements) of each lane's item
+      double ev = 1.0;
+      if (lane < n) {
+        if (partials) {
+          er = (long long)(base + lane) * h.ld;
+        } else {
+          const int q = pass ? h.ma_sep_q[base + lane] : base + lane;
+          er = (long long)h.gpc_row[q] * h.ld;
+          ev = h.gpc_val[q];
+        }
       }
+      const double *src = partials ? h.Mp : h.P;
+      for (int k0 = 0; k0 < n; k0 += 8) {
+        double x[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double v = __shfl_sync(0xffffffffu, ev, (k0 + k) & 31);
-        if (k0 + k >= n) break;
-        const int e = base + k0 + k;   // entry -> its p row (warp-uniform)
-        if (e < b1) acc[0] = fma(v, x[k], acc[0]);
-        else if (e < b2) acc[1] = fma(v, x[k], acc[1]);
-        else if (e < b3) acc[2] = fma(v, x[k], acc[2]);
-        else acc[3] = fma(v, x[k], acc[3]);
+        for (int k = 0; k < 8; ++k) {
+          const long long ro = __shfl_sync(0xffffffffu, er, (k0 + k) & 31);
+          x[k] = k0 + k < n ? src[ro + col] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const double v = __shfl_sync(0xffffffffu, ev, (k0 + k) & 31);
+          if (k0 + k >= n) break;
+          const int e = base + k0 + k;   // item -> its p row (warp-uniform)
+          const double t = partials ? x[k] : v * x[k];
+          if (partials) {
+            if (e < b1) acc[0] += t;
+            else if (e < b2) acc[1] += t;
+            else if (e < b3) acc[2] += t;
+            else acc[3] += t;
+          } else {
+            if (e < b1) acc[0] = fma(v, x[k], acc[0]);
+            else if (e < b2) acc[1] = fma(v, x[k], acc[1]);
+            else if (e < b3) acc[2] = fma(v, x[k], acc[2]);
+            else acc[3] = fma(v, x[k], acc[3]);
+          }
+        }
       }
     }
   }
@@ -2239,6 +2267,8 @@ struct rh_ctx {
     size_t elems = 0, tsep_elems = 0;
     double *Yp = nullptr;        // [n_p][ld] Y_p of the voltage parameters
     size_t yp_elems = 0;
+    double *Mp = nullptr;        // [ma runs][ld] L^T sweep partials of G_p^T Psi (k_muladd adds them)
+    size_t mp_elems = 0;
     int *pcols = nullptr;        // Cartesian batch plan: the batch's columns, home-block order
     unsigned *pmask = nullptr;   // and its nonzero L-tile mask [nblk][words]
     int plan_ld = 0;
@@ -2311,9 +2341,14 @@ struct rh_ctx {
   bool early_gathered = false;   // the fused call's early batches also formed their separator rhs
   double *grad_tsep = nullptr;
   int sep_maxlen = 1;                          // longest separator row of F (k_fact_sep_rows staging)
-  int nruns = 0, n_sr_ent = 0;                 // separator external-entry runs (one block each), entries
-  int *sr_off = nullptr, *sr_ent_slot = nullptr, *sr_ent_src = nullptr, *sr_ent_trow = nullptr;
-  double2 *sr_rec = nullptr;                   // per-block record regions (run slots static, entries per state)
+  // epilogue partial runs of k_blk (analysis.hpp RunRecs): U^T -> separator
+  // right-hand sides (sr), L^T -> G_p^T Psi of SpMulAdd (ma)
+  struct DRunRecs {
+    int nruns = 0, n_ent = 0;
+    int *off = nullptr, *slot = nullptr, *src = nullptr, *trow = nullptr;
+    double2 *rec = nullptr;   // per-block record regions (run slots static, entries per state)
+  } dsr, dma;
+  int *ma_run_ptr = nullptr, *ma_sep_ptr = nullptr, *ma_sep_q = nullptr;
   int *grad_ctr = nullptr;
   cudaEvent_t tape_wait = nullptr;   // set while a fused call enqueues its batches
   // side stream of the fused call: block-only derived values done; each early L sweep done
@@ -2358,8 +2393,12 @@ struct rh_ctx {
       if (w.pcols) cudaFree(w.pcols);
       if (w.pmask) cudaFree(w.pmask);
       if (w.Yp) cudaFree(w.Yp);
+      if (w.Mp) cudaFree(w.Mp);
       w = Workspace();
     }
+    dsr = DRunRecs();   // device arrays were in the pool
+    dma = DRunRecs();
+    ma_run_ptr = ma_sep_ptr = ma_sep_q = nullptr;
     if (e2e_buf) cudaFree(e2e_buf);
     if (e2e_st) cudaStreamDestroy(e2e_st);
     for (int k = 0; k < kNumWs; ++k) {
@@ -2419,7 +2458,9 @@ int blk_max_rows(const Analysis &A) {   // tile rows, incl. the L sweep's G_p en
   for (int s = 0; s < A.nblk; ++s) {
     const int nr = A.seg_row_off[s + 1] - A.seg_row_off[s], ne = A.gpe_off[s + 1] - A.gpe_off[s];
     m = std::max(m, nr + (16 * ne + 48 + kRowB - 1) / kRowB);
-    m = std::max(m, nr + (16 * (A.sr_off[s + 1] - A.sr_off[s]) + kRowB - 1) / kRowB);   // U^T: separator run records
+    m = std::max(m, nr + (16 * (A.sr.off[s + 1] - A.sr.off[s]) + kRowB - 1) / kRowB);   // U^T: separator run records
+    m = std::max(m, nr + (A.bwd.ext_off[s + 1] - A.bwd.ext_off[s]) +                     // L^T: staged separator rows,
+                        (16 * (A.ma.off[s + 1] - A.ma.off[s]) + kRowB - 1) / kRowB);      // then G_p run records
   }
   return m;
 }
@@ -2534,18 +2575,28 @@ int upload(rh_ctx *c) {
         }
       gp.push_back((int)gb.size());
     }
-    {  // U^T sweep epilogue partials: per-block record regions (analysis.hpp sr_*)
-      c->nruns = A.sr_nruns;
-      c->n_sr_ent = (int)A.sr_ent_src.size();
-      std::vector<int32_t> init(A.sr_init);
+    // k_blk epilogue partials: per-block record regions (analysis.hpp RunRecs)
+    auto up_runs = [&](const Analysis::RunRecs &R, rh_ctx::DRunRecs &D) {
+      D.nruns = R.nruns;
+      D.n_ent = (int)R.ent_src.size();
+      std::vector<int32_t> init(R.init);
       if (init.empty()) init.assign(4, 0);
-      chk(c->sr_off = dalloc_copy(A.sr_off, P));
-      chk(c->sr_rec = reinterpret_cast<double2 *>(dalloc_copy(init, P)));
-      if (c->n_sr_ent) {
-        chk(c->sr_ent_slot = dalloc_copy(A.sr_ent_slot, P));
-        chk(c->sr_ent_src = dalloc_copy(A.sr_ent_src, P));
-        chk(c->sr_ent_trow = dalloc_copy(A.sr_ent_trow, P));
+      chk(D.off = dalloc_copy(R.off, P));
+      chk(D.rec = reinterpret_cast<double2 *>(dalloc_copy(init, P)));
+      if (D.n_ent) {
+        chk(D.slot = dalloc_copy(R.ent_slot, P));
+        chk(D.src = dalloc_copy(R.ent_src, P));
+        chk(D.trow = dalloc_copy(R.ent_trow, P));
       }
+    };
+    up_runs(A.sr, c->dsr);
+    up_runs(A.ma, c->dma);
+    {
+      std::vector<int32_t> sq(A.ma_sep_q);
+      if (sq.empty()) sq.push_back(0);
+      chk(c->ma_run_ptr = dalloc_copy(A.ma_run_ptr, P));
+      chk(c->ma_sep_ptr = dalloc_copy(A.ma_sep_ptr, P));
+      chk(c->ma_sep_q = dalloc_copy(sq, P));
     }
     if (gb.empty()) gb.push_back(0), ge.push_back(0);
     int *g1, *g2, *g3;
@@ -2811,7 +2862,7 @@ int upload(rh_ctx *c) {
 
 int ensure_tsep(rh_ctx *c, int ld, int k = 0) {
   auto &w = c->ws[k];
-  const size_t need = (size_t)ld * (size_t)(std::max(1, c->A.sep_rows) + c->nruns);   // Tsep + run partials
+  const size_t need = (size_t)ld * (size_t)(std::max(1, c->A.sep_rows) + c->dsr.nruns);   // Tsep + run partials
   if (need <= w.tsep_elems) return RH_OK;
   c->drop_graph();   // the captured fused call points at the old buffer
   if (w.Tsep) cudaFree(w.Tsep);
@@ -2840,6 +2891,18 @@ int ensure_ws(rh_ctx *c, int ld, int k = 0) {
       return fail(c, RH_E_NOMEM, "workspace allocation failed");
     }
     w.yp_elems = nyp;
+  }
+  const size_t nmp = (size_t)ld * (size_t)std::max(1, c->dma.nruns);
+  if (nmp > w.mp_elems) {
+    c->drop_graph();
+    if (w.Mp) cudaFree(w.Mp);
+    w.Mp = nullptr;
+    w.mp_elems = 0;
+    if (cudaMalloc(&w.Mp, nmp * sizeof(double)) != cudaSuccess || cudaMemset(w.Mp, 0, nmp * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, RH_E_NOMEM, "workspace allocation failed");
+    }
+    w.mp_elems = nmp;
   }
   if (need <= w.elems) return RH_OK;
   c->drop_graph();
@@ -2966,9 +3029,15 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.sep_off = A.seg_row_off[A.nblk];
   h.Sinv = c->Sinv;
   h.Tsep = c->ws[k].Tsep;
-  h.nruns = c->nruns;
-  h.sr_off = c->sr_off;
-  h.sr_rec = c->sr_rec;
+  h.nruns = c->dsr.nruns;
+  h.sr_off = c->dsr.off;
+  h.sr_rec = c->dsr.rec;
+  h.ma_off = c->dma.off;
+  h.ma_rec = c->dma.rec;
+  h.Mp = c->dma.nruns > 0 ? c->ws[k].Mp : nullptr;
+  h.ma_run_ptr = c->ma_run_ptr;
+  h.ma_sep_ptr = c->ma_sep_ptr;
+  h.ma_sep_q = c->ma_sep_q;
   h.blk_gp_ptr = c->blk_gp_ptr;
   h.blk_gp_loc = c->blk_gp_loc;
   if (const char *env = getenv("RH_DEBUG")) h.debug = atoi(env);  // timing experiments only
@@ -3638,6 +3707,11 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   if (ngp > 0) {
     k_gather_vals<<<nblk(ngp), kThreads, 0, sb>>>(ngp, c->gpc_pos, c->gp_val, c->gpc_val);
     RH_LAUNCHED(c);
+    if (c->dma.n_ent) {   // G_p values into the per-block run record regions (k_blk MODE_LT epilogue)
+      k_sr_fill<<<nblk(c->dma.n_ent), kThreads, 0, sb>>>(c->dma.n_ent, c->dma.slot, c->dma.src, c->dma.trow,
+                                                          c->gpc_val, c->dma.rec);
+      RH_LAUNCHED(c);
+    }
   }
   struct GU {
     int n;
@@ -3674,9 +3748,9 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
         RH_LAUNCHED(c);
         k_gather_vals<<<nblk(ne), kThreads, 0, st>>>(ne, c->fwd_src_b + e0, c->F_val, c->vUt + e0);
         RH_LAUNCHED(c);
-        if (c->n_sr_ent) {   // U^T values into the per-block run record regions (k_blk MODE_UT epilogue)
-          k_sr_fill<<<nblk(c->n_sr_ent), kThreads, 0, st>>>(c->n_sr_ent, c->sr_ent_slot, c->sr_ent_src,
-                                                              c->sr_ent_trow, c->vUt, c->sr_rec);
+        if (c->dsr.n_ent) {   // U^T values into the per-block run record regions (k_blk MODE_UT epilogue)
+          k_sr_fill<<<nblk(c->dsr.n_ent), kThreads, 0, st>>>(c->dsr.n_ent, c->dsr.slot, c->dsr.src, c->dsr.trow,
+                                                              c->vUt, c->dsr.rec);
           RH_LAUNCHED(c);
         }
       }
@@ -3787,9 +3861,10 @@ int gradient_impl(rh_ctx *c, double *grad_p, double *lambda_out, cudaStream_t st
   h.N = 1;
   h.ld = kSegC;   // column 0 carries the right-hand side, columns 1..31 stay zero
   h.P = c->X1col;
+  h.Mp = nullptr;   // no SpMulAdd partials (k_grad_out forms G_p^T lambda itself)
   if (own_ws) {
     if (!c->grad_tsep) {
-      if (cudaMalloc(&c->grad_tsep, sizeof(double) * kSegC * (std::max(1, A.sep_rows) + c->nruns)) != cudaSuccess ||
+      if (cudaMalloc(&c->grad_tsep, sizeof(double) * kSegC * (std::max(1, A.sep_rows) + c->dsr.nruns)) != cudaSuccess ||
           cudaMalloc(&c->grad_ctr, 16 * sizeof(int)) != cudaSuccess || cudaMemset(c->grad_ctr, 0, 16 * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         return fail(c, RH_E_NOMEM, "gradient workspace allocation failed");

@@ -58,7 +58,8 @@ def run(name, N, modes=("mask", "nomask")):
         ctx.set_state(xd, pd)
         ctx.reduced_gradient()
         ctx.set_timing(True)
-        ctx.hessian_columns(0, min(N, ctx.n_p), N)
+        HcT = torch.empty((min(N, ctx.n_p), ctx.n_p), dtype=torch.float64, device="cuda")
+        ctx.hessian_columns(0, min(N, ctx.n_p), N, H=HcT, transposed=True)   # the step's layout
         out[mode + "_cart_stages"] = [round(float(v), 4) for v in ctx.stage_times()[:9]]
         W = torch.randn(ctx.n_p, N, dtype=torch.float64, device="cuda")
         ctx.hvp(W)
@@ -79,4 +80,4 @@ if __name__ == "__main__":
     for c in cases:
         if tag:
             print("variant", tag, end=": ")
-        run(c, gridgen.CONFIG_N.get(c, 256), modes)
+        run(c, int(os.environ.get("PROBE_N", 0)) or gridgen.CONFIG_N.get(c, 256), modes)
