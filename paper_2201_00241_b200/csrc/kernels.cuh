@@ -65,6 +65,7 @@ struct SegParams {
   double *Tsep;                        // [ns][ld] separator right-hand sides, then the run partials:
   // U^T sweep epilogue (k_blk MODE_UT): Part[g] = sum over run g's entries (one block's
   // rows) of U^T value x P row, [nruns][ld] behind Tsep; k_sep_gather (UTLT) sums the runs
+  unsigned char *nzf;                  // Cartesian LU: [chunk][ns] separator rows of T that are nonzero (k_sep_spmm)
   int nruns;
   const int *sr_off;                   // per block: its record slots (analysis.hpp sr_*)
   const double2 *sr_rec;               // [run table (g, first entry slot, entries) | entries (value, tile offset)]

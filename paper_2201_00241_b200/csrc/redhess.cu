@@ -1604,6 +1604,7 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
     // others are identically zero).  Every live entry goes to the chain the
     // unmasked loops below give it ((e - e0) mod 4, the last (ex - e0) mod 4
     // entries to chain 0), in the same order, so both paths are bitwise equal.
+    // The row's nonzero flag for this chunk goes to nzf (k_sep_spmm).
     const int e0 = e, tail = ex - ((ex - e0) & 3);
     for (int g = h.fwd.grp_ptr[qoff], g1 = h.fwd.grp_ptr[qoff + 1]; g < g1; ++g) {
       const int ee = h.fwd.grp_end[g];
@@ -1631,7 +1632,10 @@ __global__ void __launch_bounds__(kThreads) k_sep_gather(SegParams h, int mode) 
       }
       e = ee;
     }
-    h.Tsep[(long long)a * h.ld + col] = v0 - ((s0 + s1) + (s2 + s3));
+    const double t = v0 - ((s0 + s1) + (s2 + s3));
+    h.Tsep[(long long)a * h.ld + col] = t;
+    const unsigned nz = __ballot_sync(0xffffffffu, t != 0.0);
+    if (lane == 0) h.nzf[(long long)blockIdx.y * ((h.ns + 15) & ~15) + a] = nz != 0u;   // rows of 16-byte words
     return;
   }
   for (; e + 8 <= ex; e += 8) {   // 8 row gathers in flight
@@ -1789,6 +1793,82 @@ __global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
 
 // Single right-hand side (the first-order adjoint): separator rows of P =
 // S^-T t, warp per row, lanes over k (coalesced rows of S^-T), fixed order.
+// Cartesian batches, separator rows of the L solve: T = (rhs - L_sb Z_b) has
+// few nonzero rows per 32-column chunk (the separator rows that depend on the
+// chunk's home blocks, ~10 % of them), so Z_sep = S^-1 T is formed over those
+// rows only: the chunk's nonzero-row list (nzf, from k_sep_gather) is
+// compacted, the rows of T and of S^-T (= S^-1 columns) are staged in shared
+// memory SPK at a time, and each lane (= column) accumulates in increasing k.
+// A row of the list that is zero in some column adds an exact zero there, so
+// every column's sum is its own nonzero terms in increasing k: the result does
+// not depend on the other columns of the chunk (bitwise N- and shard-invariant).
+constexpr int SPK = 48, SPM = 64;   // staged k rows, output rows per CTA
+__global__ void __launch_bounds__(256) k_sep_spmm(SegParams h) {
+  extern __shared__ __align__(16) double spm[];
+  double(*Ts)[32] = reinterpret_cast<double(*)[32]>(spm);               // [SPK][32]
+  double(*As)[SPM] = reinterpret_cast<double(*)[SPM]>(spm + SPK * 32);  // [SPK][SPM]: S^-1[m0 + m][k]
+  int *klist = reinterpret_cast<int *>(spm + SPK * 32 + SPK * SPM);     // [ns]
+  __shared__ int s_nk;
+  const int ns = h.ns, ld = h.ld, c = blockIdx.x, m0 = blockIdx.y * SPM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp == 0) {   // compact the chunk's nonzero rows, increasing k: 16 flags per 16-byte load
+    const int nsf = (ns + 15) & ~15, nw16 = nsf >> 4;   // flag row stride (bytes), 16-byte words
+    const uint4 *fw = reinterpret_cast<const uint4 *>(h.nzf + (long long)c * nsf);
+    int n = 0;
+    for (int i = 0; 32 * i < nw16; ++i) {   // 512 rows per pass (one pass up to ns = 512)
+      const uint4 wi = lane + 32 * i < nw16 ? fw[lane + 32 * i] : make_uint4(0, 0, 0, 0);
+      const unsigned v[4] = {wi.x, wi.y, wi.z, wi.w};
+      const int r0 = 16 * (lane + 32 * i);   // flags past ns (row padding) are stale: masked
+      unsigned fl = 0u;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (r0 + j < ns && ((v[j >> 2] >> (8 * (j & 3))) & 0xffu) != 0u) fl |= 1u << j;
+      const int cnt = __popc(fl);
+      int pre = cnt;   // inclusive scan over the lanes
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += t;
+      }
+      int at = n + pre - cnt;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (fl & (1u << j)) klist[at++] = r0 + j;
+      n += __shfl_sync(0xffffffffu, pre, 31);
+    }
+    if (lane == 0) s_nk = n;
+  }
+  __syncthreads();
+  const int nk = s_nk;
+  double acc[SPM / 8];
+#pragma unroll
+  for (int i = 0; i < SPM / 8; ++i) acc[i] = 0.0;
+  for (int k0 = 0; k0 < nk; k0 += SPK) {
+    const int kn = min(SPK, nk - k0);
+    for (int t = tid; t < kn * 32; t += 256) {
+      const int kk = t >> 5, cc = t & 31;
+      Ts[kk][cc] = h.Tsep[(long long)klist[k0 + kk] * ld + c * 32 + cc];
+    }
+    for (int t = tid; t < kn * SPM; t += 256) {
+      const int kk = t / SPM, mm = t % SPM;
+      As[kk][mm] = m0 + mm < ns ? h.SinvT[(long long)klist[k0 + kk] * ns + m0 + mm] : 0.0;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < kn; ++kk) {
+      const double tv = Ts[kk][lane];
+#pragma unroll
+      for (int i = 0; i < SPM / 8; ++i) acc[i] = fma(As[kk][warp + 8 * i], tv, acc[i]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < SPM / 8; ++i) {
+    const int m = m0 + warp + 8 * i;
+    if (m < ns) h.Z[(long long)(h.sep_off + m) * ld + c * 32 + lane] = acc[i];
+  }
+}
+inline size_t spmm_smem_bytes(int ns) { return sizeof(double) * (SPK * 32 + SPK * SPM) + sizeof(int) * (size_t)ns; }
+
 __global__ void __launch_bounds__(kThreads) k_sep_gemv(SegParams h, int mode) {
   const int lane = threadIdx.x & 31;
   const int m = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
@@ -2862,7 +2942,9 @@ int upload(rh_ctx *c) {
 
 int ensure_tsep(rh_ctx *c, int ld, int k = 0) {
   auto &w = c->ws[k];
-  const size_t need = (size_t)ld * (size_t)(std::max(1, c->A.sep_rows) + c->dsr.nruns);   // Tsep + run partials
+  // Tsep + run partials + the Cartesian nonzero-row flags ([ld / 32][ns] bytes)
+  const size_t need = (size_t)ld * (size_t)(std::max(1, c->A.sep_rows) + c->dsr.nruns) +
+                      ((size_t)(ld / 32) * ((std::max(1, c->A.sep_rows) + 15) & ~15) + 7) / 8;
   if (need <= w.tsep_elems) return RH_OK;
   c->drop_graph();   // the captured fused call points at the old buffer
   if (w.Tsep) cudaFree(w.Tsep);
@@ -3144,6 +3226,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   const bool timing = c->timing && phase == 0;
   h.N = N;
   h.ld = ld;
+  h.nzf = reinterpret_cast<unsigned char *>(h.Tsep + (long long)ld * (std::max(1, A.sep_rows) + c->dsr.nruns));
   h.tmZ = tmap_pair(c, h.Z, ld);
   h.tmP = tmap_pair(c, h.P, ld);
   h.W = W;
@@ -3198,7 +3281,11 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
       RH_LAUNCHED(c);
     }
     if (phase == 3) return RH_OK;
-    k_sep_gemm<<<gSm, GTHREADS, gemm_smem_bytes(), st>>>(h, MODE_LU);
+    if (h.tmask && !getenv("RH_NO_SPMM")) {   // Cartesian batch: S^-1 over T's nonzero rows only
+      k_sep_spmm<<<dim3(ld / 32, (A.sep_rows + SPM - 1) / SPM), 256, spmm_smem_bytes(A.sep_rows), st>>>(h);
+    } else {
+      k_sep_gemm<<<gSm, GTHREADS, gemm_smem_bytes(), st>>>(h, MODE_LU);
+    }
     RH_LAUNCHED(c);
   }
   if (phase == 3) return RH_OK;
