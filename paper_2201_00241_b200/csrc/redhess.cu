@@ -1845,13 +1845,29 @@ __global__ void __launch_bounds__(256) k_sep_spmm(SegParams h) {
   for (int i = 0; i < SPM / 8; ++i) acc[i] = 0.0;
   for (int k0 = 0; k0 < nk; k0 += SPK) {
     const int kn = min(SPK, nk - k0);
-    for (int t = tid; t < kn * 32; t += 256) {
-      const int kk = t >> 5, cc = t & 31;
-      Ts[kk][cc] = h.Tsep[(long long)klist[k0 + kk] * ld + c * 32 + cc];
-    }
-    for (int t = tid; t < kn * SPM; t += 256) {
-      const int kk = t / SPM, mm = t % SPM;
-      As[kk][mm] = m0 + mm < ns ? h.SinvT[(long long)klist[k0 + kk] * ns + m0 + mm] : 0.0;
+    {   // every thread's staging loads in flight at once (18 per thread at most)
+      constexpr int NT = SPK * 32 / 256, NA = SPK * SPM / 256;
+      double vt[NT], va[NA];
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const int t = tid + 256 * i, kk = t >> 5, cc = t & 31;
+        vt[i] = kk < kn ? h.Tsep[(long long)klist[k0 + kk] * ld + c * 32 + cc] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const int t = tid + 256 * i, kk = t / SPM, mm = t % SPM;
+        va[i] = kk < kn && m0 + mm < ns ? h.SinvT[(long long)klist[k0 + kk] * ns + m0 + mm] : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const int t = tid + 256 * i;
+        Ts[t >> 5][t & 31] = vt[i];
+      }
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const int t = tid + 256 * i;
+        As[t / SPM][t % SPM] = va[i];
+      }
     }
     __syncthreads();
     for (int kk = 0; kk < kn; ++kk) {
