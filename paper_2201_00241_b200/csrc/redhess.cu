@@ -4142,10 +4142,17 @@ inline void batch_range(int ncols, int nb, int b, int &a0, int &a1) {
 // batch bounds of a host-copy call: full batches of N first, then the remainder
 // split into pieces of <= tail columns (the last batch's copy is the tail that
 // nothing overlaps, so it should be small)
-std::vector<int> host_cuts(int ncols, int N) {
+// Host copies of H are the e2e bound when H is large (case9241: 66.8 MB = 1.2 ms
+// of D2H against a 1.6 ms step): then batches run one after another on one
+// stream, each copied while the next computes, and the remainder is split so the
+// last copy is small (e2e probe: 2.58 -> 2.35 ms).  Smaller H (case2869: 8.3 MB,
+// 0.15 ms) is compute-bound: two concurrent streams, remainder in one batch.
+bool host_copy_bound(int n_p) { return (double)n_p * n_p * 8.0 >= 32.0 * (1 << 20); }
+
+std::vector<int> host_cuts(int ncols, int N, bool copy_bound) {
   std::vector<int> cuts(1, 0);
   if (ncols <= 0) return cuts;
-  int tail = std::max(32, N / 2), first = N;   // (e2e probe, case9241: 1 stream, tail N/2: 2.58 -> 2.35 ms)
+  int tail = copy_bound ? std::max(32, N / 2) : N, first = N;
   if (const char *env = getenv("RH_E2E_TAIL")) tail = std::max(32, atoi(env));     // tuning override
   if (const char *env = getenv("RH_E2E_FIRST")) first = std::max(32, atoi(env));   // tuning override
   int a = 0;
@@ -4164,15 +4171,13 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
   int nb = (ncols + N - 1) / N;
   std::vector<int> cuts;   // batch bounds (host copies only)
   if (Hhost) {
-    cuts = host_cuts(ncols, N);
+    cuts = host_cuts(ncols, N, host_copy_bound(c->A.n_p));
     nb = (int)cuts.size() - 1;
   }
-  // with host copies, one compute stream: batches finish one after the other,
-  // and each finished column block travels on a copy stream while later batches
-  // compute (the D2H of H, 1.2 ms on case9241, is the e2e bound: it should start
-  // as early as possible); concurrent batches would finish together and leave
-  // the copies to the tail
-  int host_streams = 1;   // host copies: batches one after another, each copied while the next computes
+  // with host copies each finished column block travels on a copy stream while
+  // later batches compute; copy-bound calls (host_copy_bound) run their batches
+  // one after the other so the copies start as early as possible
+  int host_streams = host_copy_bound(c->A.n_p) ? 1 : 2;   // host copies (host_copy_bound)
   if (const char *env = getenv("RH_E2E_STREAMS")) host_streams = std::max(1, atoi(env));   // tuning override
   const int nws = num_ws(nb, Hhost ? host_streams : kNumWs);
   if (Hhost) {
@@ -4257,9 +4262,9 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
   if ((!transposed && ldh < j1 - j0) || (transposed && ldh < np_)) return fail(c, RH_E_ARG, "ldh too small");
   RH_CUDA(c, cudaSetDevice(c->device));
   const int ncols = j1 - j0;
-  const std::vector<int> cuts = Hhost ? host_cuts(ncols, N) : std::vector<int>();
+  const std::vector<int> cuts = Hhost ? host_cuts(ncols, N, host_copy_bound(c->A.n_p)) : std::vector<int>();
   const int nb = Hhost ? (int)cuts.size() - 1 : ncols > 0 ? (ncols + N - 1) / N : 0;
-  int host_streams = 1;   // as hessian_batches
+  int host_streams = host_copy_bound(c->A.n_p) ? 1 : 2;   // as hessian_batches
   if (const char *env = getenv("RH_E2E_STREAMS")) host_streams = std::max(1, atoi(env));   // tuning override
   const int early = nb > 0 ? std::min(nb, num_ws(nb, Hhost ? host_streams : kNumWs)) : 0;
   // the widest batch actually run (front-loaded batches of N for host copies,
