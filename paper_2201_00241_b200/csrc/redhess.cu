@@ -1932,9 +1932,10 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
   double4 *s_meta = s_coef + h.fg_maxslots;
   int4 *s_dst = reinterpret_cast<int4 *>(s_meta + h.fg_maxout);
   int *s_oe = reinterpret_cast<int *>(s_dst + h.fg_maxout);
-  // timing experiment (RH_DEBUG & 8192): per CTA [start, staged+filled, copies landed, end]
+  // timing experiment (RH_DEBUG & 8192): per CTA [start, armed, row copies issued, filled,
+  // copies landed, end]
   long long *prof = ((h.debug & 8192) && h.dbg && g * gridDim.y + blockIdx.y < 16384)
-                        ? h.dbg + 4LL * (g * gridDim.y + blockIdx.y) : nullptr;
+                        ? h.dbg + 6LL * (g * gridDim.y + blockIdx.y) : nullptr;
   if (prof && tid == 0) prof[0] = clock64();
   const char *tm = reinterpret_cast<const char *>(h.tmZ);
   const int nbig = tm ? zn / kTmaBig : 0, nsmall = tm ? (zn - nbig * kTmaBig) / kTmaSmall : 0;
@@ -1957,6 +1958,7 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
     }
   }
   __syncthreads();   // mbarrier initialised and armed
+  if (prof && tid == 0) prof[1] = clock64();
   // the rest of the range and the other Z sources: per-row bulk copies
   for (int r = rows_tma + tid; r < zn; r += blockDim.x)
     bulk_g2s(fsm + r * 32, h.Z + (long long)(zlo + r) * h.ld + col0, 256, &mbar);
@@ -1964,6 +1966,7 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
     const int2 e = h.fg_cp[c0 + i];
     bulk_g2s(fsm + e.x * 32, h.Z + (long long)e.y * h.ld + col0, 256, &mbar);
   }
+  if (prof && tid == 0) prof[2] = clock64();
   // rows without a Z source: zero, or a v parameter from W; lane = column, 4 rows in flight per warp
   for (int f = 4 * warp; f < nfill; f += 4 * nw) {
     double v[4];
@@ -1977,7 +1980,7 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
     for (int u = 0; u < 4; ++u)
       if (f + u < nfill) fsm[q[u].x * 32 + lane] = v[u];
   }
-  if (prof && tid == 0) prof[1] = clock64();
+  if (prof && tid == 0) prof[3] = clock64();
   {
     unsigned done = 0;
     while (!done)
@@ -1987,7 +1990,7 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
                    : "memory");
   }
   __syncthreads();
-  if (prof && tid == 0) prof[2] = clock64();
+  if (prof && tid == 0) prof[4] = clock64();
   const int r0 = h.fg_ref[g], r1 = h.fg_ref[g + 1];
   if (r0 < r1) {   // REF objective rank-1 term f''(Pg_ref) (grad P_ref . delta) (R22), once per tile
     if (warp == 0) {
@@ -2045,7 +2048,7 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
   }
   if (prof) {
     __syncthreads();
-    if (tid == 0) prof[3] = clock64();
+    if (tid == 0) prof[5] = clock64();
   }
 }
 
@@ -3326,7 +3329,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   k_for<<<gF, kForThreads, c->smem_for, st>>>(h);
   RH_LAUNCHED(c);
   if ((h.debug & 8192) && h.dbg) {  // timing experiment: per-CTA phase cycles of k_for (tools/kfor_prof.py)
-    std::vector<long long> hb((size_t)4 * std::min<long long>(16384, (long long)gF.x * gF.y));
+    std::vector<long long> hb((size_t)6 * std::min<long long>(16384, (long long)gF.x * gF.y));
     cudaMemcpyAsync(hb.data(), h.dbg, hb.size() * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     if (FILE *fp = fopen("gpurun_out/kfor_prof.bin", "wb")) {
