@@ -1797,8 +1797,9 @@ __global__ void __launch_bounds__(GTHREADS) k_sep_gemm(SegParams h, int mode) {
 // few nonzero rows per 32-column chunk (the separator rows that depend on the
 // chunk's home blocks, ~10 % of them), so Z_sep = S^-1 T is formed over those
 // rows only: the chunk's nonzero-row list (nzf, from k_sep_gather) is
-// compacted, the rows of T and of S^-T (= S^-1 columns) are staged in shared
-// memory SPK at a time, and each lane (= column) accumulates in increasing k.
+// compacted, the rows of T and the matching columns of S^-1 (S^-1 itself, so
+// this does not wait for its transpose) are staged in shared memory SPK at a
+// time, and each lane (= column) accumulates in increasing k.
 // A row of the list that is zero in some column adds an exact zero there, so
 // every column's sum is its own nonzero terms in increasing k: the result does
 // not depend on the other columns of the chunk (bitwise N- and shard-invariant).
@@ -1856,7 +1857,7 @@ __global__ void __launch_bounds__(256) k_sep_spmm(SegParams h) {
 #pragma unroll
       for (int i = 0; i < NA; ++i) {
         const int t = tid + 256 * i, kk = t / SPM, mm = t % SPM;
-        va[i] = kk < kn && m0 + mm < ns ? h.SinvT[(long long)klist[k0 + kk] * ns + m0 + mm] : 0.0;
+        va[i] = kk < kn && m0 + mm < ns ? h.Sinv[(long long)(m0 + mm) * ns + klist[k0 + kk]] : 0.0;
       }
 #pragma unroll
       for (int i = 0; i < NT; ++i) {
@@ -2437,6 +2438,9 @@ struct rh_ctx {
   cudaStream_t grad_st = nullptr;
   cudaEvent_t ev_state = nullptr, ev_tape = nullptr;
   cudaEvent_t ev_vl = nullptr;   // separator rows' L / U^T values ready (after R_B1)
+  cudaEvent_t ev_ult = nullptr;   // fused call: L^T records (side stream)
+  cudaEvent_t ev_tr = nullptr;   // S^-T ready (k_transpose; the gradient stream in the fused call)
+  bool tr_pending = false;       // fused call: S^-T not yet launched (reduced_hessian_impl does it)
   bool early_gathered = false;   // the fused call's early batches also formed their separator rhs
   double *grad_tsep = nullptr;
   int sep_maxlen = 1;                          // longest separator row of F (k_fact_sep_rows staging)
@@ -2474,6 +2478,8 @@ struct rh_ctx {
     if (ev_state) cudaEventDestroy(ev_state), ev_state = nullptr;
     if (ev_tape) cudaEventDestroy(ev_tape), ev_tape = nullptr;
     if (ev_vl) cudaEventDestroy(ev_vl), ev_vl = nullptr;
+    if (ev_ult) cudaEventDestroy(ev_ult), ev_ult = nullptr;
+    if (ev_tr) cudaEventDestroy(ev_tr), ev_tr = nullptr;
     if (grad_tsep) cudaFree(grad_tsep), grad_tsep = nullptr;
     if (grad_ctr) cudaFree(grad_ctr), grad_ctr = nullptr;
     tape_wait = nullptr;
@@ -3303,6 +3309,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
     if (h.tmask && !getenv("RH_NO_SPMM")) {   // Cartesian batch: S^-1 over T's nonzero rows only
       k_sep_spmm<<<dim3(ld / 32, (A.sep_rows + SPM - 1) / SPM), 256, spmm_smem_bytes(A.sep_rows), st>>>(h);
     } else {
+      if (c->ev_tr) RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_tr, 0));   // reads S^-T
       k_sep_gemm<<<gSm, GTHREADS, gemm_smem_bytes(), st>>>(h, MODE_LU);
     }
     RH_LAUNCHED(c);
@@ -3865,6 +3872,13 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
       if (!c->ev_vl) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_vl, cudaEventDisableTiming));
       RH_CUDA(c, cudaEventRecord(c->ev_vl, st));
       RH_CUDA(c, cudaStreamWaitEvent(sb, c->ev_vl, 0));
+      if (c->nrec_b > 0) {   // L^T records need R_B1's values, not S^-1: off the critical path too
+        k_gather_code<<<nblk(2LL * c->nrec_b), kThreads, 0, sb>>>(2 * c->nrec_b, c->ub_src_b, c->F_val,
+                                                                   reinterpret_cast<double *>(c->uLt));
+        RH_LAUNCHED(c);
+      }
+      if (!c->ev_ult) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_ult, cudaEventDisableTiming));
+      RH_CUDA(c, cudaEventRecord(c->ev_ult, sb));
       if (int rc = early(sb, 2)) return rc;
     }
     // dense Schur complement of the separator, inverted by blocked Gauss-Jordan
@@ -3907,14 +3921,24 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
       }
     }
     dbg_mark(st, "k_sep_inverse");
-    k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
-    RH_LAUNCHED(c);
+    // S^-T (the dense L-side product of random-W batches, the gradient's transposed
+    // GEMV): in the fused call on the gradient stream, so the Cartesian batches
+    // (their L-side product reads S^-1) do not wait for it; users wait on ev_tr
+    if (!c->ev_tr) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_tr, cudaEventDisableTiming));
+    if (early && side) {
+      c->tr_pending = true;   // the fused call runs it first on the gradient stream
+    } else {
+      k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
+      RH_LAUNCHED(c);
+      RH_CUDA(c, cudaEventRecord(c->ev_tr, st));
+    }
   }
-  if (c->nrec_b > 0) {   // L^T records: block rows' L entries below them include L_sb (R_B1)
+  if (c->nrec_b > 0 && !(early && side && A.sep_rows > 0)) {   // L^T records: block rows' L entries include L_sb (R_B1)
     k_gather_code<<<nblk(2LL * c->nrec_b), kThreads, 0, st>>>(2 * c->nrec_b, c->ub_src_b, c->F_val,
                                                                reinterpret_cast<double *>(c->uLt));
     RH_LAUNCHED(c);
   }
+  if (early && side && A.sep_rows > 0) RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_ult, 0));   // (done during the inverse)
   if (side && early) {   // the early sweeps are joined batch by batch (hessian_batches)
     RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_derived, 0));
   } else if (side) {
@@ -4196,14 +4220,17 @@ int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, 
       RH_CUDA(c, cudaStreamWaitEvent(c->sti[k], c->ev_fork, 0));
     }
   }
-  for (int b = 0; b < nb; ++b) {
-    int a0, a1;
+  auto range = [&](int b, int &a0, int &a1) {
     if (Hhost) {
       a0 = cuts[b];
       a1 = cuts[b + 1];
     } else {
       batch_range(ncols, nb, b, a0, a1);
     }
+  };
+  for (int b = 0; b < nb; ++b) {
+    int a0, a1;
+    range(b, a0, a1);
     double *out = transposed ? H + (long long)a0 * ldh : H + a0;
     const int k = b % nws;
     cudaStream_t sb = k ? c->sti[k] : st;
@@ -4321,6 +4348,13 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
     if (!c->ev_tape) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_tape, cudaEventDisableTiming));
     RH_CUDA(c, cudaEventRecord(c->ev_state, st));
     RH_CUDA(c, cudaStreamWaitEvent(c->grad_st, c->ev_state, 0));
+    if (c->tr_pending) {   // S^-T off the batches' critical path: the gradient's GEMV reads it
+      const int ns = c->A.sep_rows;
+      k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, c->grad_st>>>(c->Sinv, c->SinvT, ns);
+      RH_LAUNCHED(c);
+      RH_CUDA(c, cudaEventRecord(c->ev_tr, c->grad_st));
+      c->tr_pending = false;
+    }
     rc = gradient_impl(c, grad_p, nullptr, c->grad_st, true);
     if (!rc) RH_CUDA(c, cudaEventRecord(c->ev_tape, c->grad_st));
   }
