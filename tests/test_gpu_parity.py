@@ -113,6 +113,29 @@ def test_full_hessian_parity(solved_case):
     assert np.array_equal(Ht.T, H[:, j0:j1])
 
 
+def test_cartesian_separator_paths(solved_case, monkeypatch):
+    """The Cartesian batches' L-side separator product over T's nonzero rows only
+    (k_sep_spmm, the default) and the dense S^-1 GEMM (RH_NO_SPMM), and the masked
+    vs dense L sweep (RH_NO_MASK): each matches the oracle at the parity bar, and
+    the mask on/off is bitwise ("Cartesian batches")."""
+    name, g, L, x, p, grad, lam, ops = solved_case
+    ctx, *_ = setup(g)
+    ctx.reduced_gradient()
+    N = {"case9": 5, "case118": 64, "case1354pegase": 256, "case2869pegase": 512}[name]
+    H = _np(ctx.full_hessian(N))
+    Ho = red.full_hessian(ops, N)
+    monkeypatch.setenv("RH_NO_SPMM", "1")
+    Hg = _np(ctx.full_hessian(N))
+    assert col_rel_err(Hg, Ho) <= TOL_H
+    assert col_rel_err(Hg, H) <= 1e-12     # two summation orders of the same product
+    monkeypatch.delenv("RH_NO_SPMM")
+    monkeypatch.setenv("RH_NO_MASK", "1")   # dense L sweep + dense separator GEMM
+    Hd = _np(ctx.full_hessian(N))
+    assert np.array_equal(Hd, Hg)
+    monkeypatch.delenv("RH_NO_MASK")
+    assert np.array_equal(_np(ctx.full_hessian(N)), H)
+
+
 def test_set_multipliers_any_lambda(solved_case):
     name, g, L, x, p, *_ = solved_case
     if name not in ("case9", "case118"):
