@@ -640,15 +640,23 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
   // stage C^T, P and T (T := 0 on the panel columns) of one output tile; `t0`,
   // `nthr`: the participating threads.  Batches of 16 loads in flight per thread.
   auto load_tile = [&](const double *Sin, int K, int b, int i0, int j0, int t0, int nthr) {
-    constexpr int NB = 16;
+    // one pass issues a thread's C, P and T loads together (all in flight: one L2
+    // round trip per pass; 256 threads: one pass)
+    constexpr int NB = 8;
     for (int base = t0; base < GJT * GJB; base += NB * nthr) {
-      double va[NB], vb[NB];
+      double va[NB], vb[NB], vt[2 * NB];
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
         const int t = base + q * nthr;
         const int r = t / GJB, m = t % GJB, m2 = t / GJT, c = t % GJT;
         va[q] = (t < GJT * GJB && i0 + r < ns && m < b) ? __ldcg(Sin + (long long)(i0 + r) * ns + K + m) : 0.0;
         vb[q] = (t < GJT * GJB && m2 < b && j0 + c < ns) ? __ldcg(Sin + (long long)(K + m2) * ns + j0 + c) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 2 * NB; ++q) {   // T: twice the elements, the same passes
+        const int t = 2 * (base - t0) + t0 + q * nthr, r = t / GJT, c = t % GJT;
+        const bool inJ = j0 + c >= K && j0 + c < K + b;
+        vt[q] = (t < GJT * GJT && i0 + r < ns && j0 + c < ns && !inJ) ? __ldcg(Sin + (long long)(i0 + r) * ns + j0 + c) : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
@@ -658,18 +666,9 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
           Rs[t / GJT][t % GJT] = vb[q];
         }
       }
-    }
-    for (int base = t0; base < GJT * GJT; base += NB * nthr) {
-      double vt[NB];
 #pragma unroll
-      for (int q = 0; q < NB; ++q) {
-        const int t = base + q * nthr, r = t / GJT, c = t % GJT;
-        const bool inJ = j0 + c >= K && j0 + c < K + b;
-        vt[q] = (t < GJT * GJT && i0 + r < ns && j0 + c < ns && !inJ) ? __ldcg(Sin + (long long)(i0 + r) * ns + j0 + c) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < NB; ++q) {
-        const int t = base + q * nthr;
+      for (int q = 0; q < 2 * NB; ++q) {
+        const int t = 2 * (base - t0) + t0 + q * nthr;
         if (t < GJT * GJT) Ts[t / GJT][t % GJT] = vt[q];
       }
     }
