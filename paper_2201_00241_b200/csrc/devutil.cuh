@@ -44,6 +44,21 @@ __device__ __forceinline__ void grid_barrier_count(unsigned *cnt, unsigned &phas
   __syncthreads();
 }
 
+// The same on a subset of the grid: the first `n` CTAs (phase * n arrivals).
+__device__ __forceinline__ void grid_barrier_n(unsigned *cnt, unsigned &phase, int n) {
+  __syncthreads();
+  ++phase;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(cnt, 1u);
+    const unsigned target = phase * (unsigned)n;
+    while ((int)((unsigned)ld_acquire(reinterpret_cast<const int *>(cnt)) - target) < 0) {
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // D(8x8) += A(8x4) B(4x8) on the fp64 tensor cores: a = A[gid][tig], b = B[tig][gid],
 // (c0, c1) = D[gid][2 tig], D[gid][2 tig + 1] (gid = lane / 4, tig = lane % 4)
 __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {

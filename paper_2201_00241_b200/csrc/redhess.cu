@@ -624,7 +624,7 @@ constexpr int GJT = 64;   // output tile
 constexpr size_t gj_smem_bytes() { return sizeof(double) * (GJB * (GJB + 1) + (3 * GJB + GJT) * (GJT + 1)); }
 __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, int ns, const double *rowmax,
                                                      const int *sep_rows, int *status, double pivtol,
-                                                     unsigned *bar, long long *dbg, double *dbuf) {
+                                                     unsigned *bar, long long *dbg, double *dbuf, int gj_warps) {
   extern __shared__ double gj_sm[];   // dynamic: gj_smem_bytes()
   double(*Ds)[GJB + 1] = reinterpret_cast<double(*)[GJB + 1]>(gj_sm);
   double(*Cs)[GJT + 1] = reinterpret_cast<double(*)[GJT + 1]>(gj_sm + GJB * (GJB + 1));   // C^T: Cs[m][r] = S[i0 + r][K + m]
@@ -712,6 +712,7 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
 #pragma unroll
     for (int r = 0; r < RPT; ++r) Ds[RPT * warp + r][j] = v[r];
   };
+  using W2 = std::integral_constant<int, 2>;
   using W4 = std::integral_constant<int, 4>;
   using W8 = std::integral_constant<int, 8>;
   const bool helper = blockIdx.x == gridDim.x - 1;   // lookahead CTA: the next panel's D^-1
@@ -721,7 +722,17 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
     if (prof) prof[(K / GJB) * 4] = clock64();   // timing experiment (RH_DEBUG & 16)
     if (helper) {
       // panel 0: D_0^-1 first; then D'_{K+1} = S[K1,K1] - S[K1,K] D_K^-1 S[K,K1] (S = state after
-      // panel K-1, what the tiles read now), inverted into Ds and published in dbuf for panel K+1
+      // panel K-1, what the tiles read now), inverted into Ds and published in dbuf for panel K+1.
+      // The lookahead CTA is not part of the tiles' barrier: it waits for the tiles' panel
+      // K-1 (the arrival counter) and publishes D_{K+1}^-1 with a flag (bar[1]), so the
+      // tiles of panel K+1 start as soon as both their panel K and D_{K+1}^-1 are done.
+      if (K > 0 && tid == 0) {
+        const unsigned target = (unsigned)(K / GJB) * ntcta;
+        while ((int)((unsigned)ld_acquire(reinterpret_cast<const int *>(bar)) - target) < 0) {
+        }
+        __threadfence();
+      }
+      __syncthreads();
       if (K == 0) {
         for (int t = tid; t < GJB * GJB; t += blockDim.x) {
           const int i = t / GJB, c = t % GJB;
@@ -751,40 +762,64 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
           }
         }
         __syncthreads();
-        {   // R2 = D_K^-1 S[K,K1]: thread = column c, rows i0 + 8u (four chains in flight)
+        // the two 32 x 32 x 32 products: thread = column c, rows i0 + 8u; each of its
+        // four outputs in four partial chains over l mod 4 (16 FMA chains of 8 in
+        // flight), added in a fixed order
+        constexpr int NU = GJB * GJB / 256;
+        {   // R2 = D_K^-1 S[K,K1]
           const int c = tid % GJB, i0 = tid / GJB;
-          double acc[GJB * GJB / 256];
+          double acc[NU][4];
 #pragma unroll
-          for (int u = 0; u < GJB * GJB / 256; ++u) acc[u] = 0.0;
-#pragma unroll 8
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+#pragma unroll
           for (int l = 0; l < GJB; ++l) {
             const double r = Rs[l][c];
 #pragma unroll
-            for (int u = 0; u < GJB * GJB / 256; ++u) acc[u] = fma(Ds[i0 + 8 * u][l], r, acc[u]);
+            for (int u = 0; u < NU; ++u) acc[u][l & 3] = fma(Ds[i0 + 8 * u][l], r, acc[u][l & 3]);
           }
 #pragma unroll
-          for (int u = 0; u < GJB * GJB / 256; ++u) R2[i0 + 8 * u][c] = acc[u];
+          for (int u = 0; u < NU; ++u) R2[i0 + 8 * u][c] = (acc[u][0] + acc[u][1]) + (acc[u][2] + acc[u][3]);
         }
         __syncthreads();
         {   // Ts = S[K1,K1] - S[K1,K] R2
           const int c = tid % GJB, i0 = tid / GJB;
-          double acc[GJB * GJB / 256];
+          double acc[NU][4];
 #pragma unroll
-          for (int u = 0; u < GJB * GJB / 256; ++u) acc[u] = Ts[i0 + 8 * u][c];
-#pragma unroll 8
+          for (int u = 0; u < NU; ++u)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+#pragma unroll
           for (int l = 0; l < GJB; ++l) {
             const double r = R2[l][c];
 #pragma unroll
-            for (int u = 0; u < GJB * GJB / 256; ++u) acc[u] = fma(-Cs[i0 + 8 * u][l], r, acc[u]);
+            for (int u = 0; u < NU; ++u) acc[u][l & 3] = fma(Cs[i0 + 8 * u][l], r, acc[u][l & 3]);
           }
 #pragma unroll
-          for (int u = 0; u < GJB * GJB / 256; ++u) Ts[i0 + 8 * u][c] = acc[u];
+          for (int u = 0; u < NU; ++u)
+            Ts[i0 + 8 * u][c] -= (acc[u][0] + acc[u][1]) + (acc[u][2] + acc[u][3]);
         }
         __syncthreads();
-        invert32(&Ts[0][0], GJT + 1, K1, b1, true, W8{});
+        if (prof) prof[(K / GJB) * 4 + 1] = clock64();
+        {   // experiment (RH_GJW): warps of the lookahead's inverse
+          const int gw = gj_warps;
+          if (gw == 2) {
+            if (warp < 2) invert32(&Ts[0][0], GJT + 1, K1, b1, true, W2{});
+          } else if (gw == 4) {
+            if (warp < 4) invert32(&Ts[0][0], GJT + 1, K1, b1, true, W4{});
+          } else {
+            invert32(&Ts[0][0], GJT + 1, K1, b1, true, W8{});
+          }
+        }
         __syncthreads();
         double *db = dbuf + ((K1 / GJB) & 1) * GJB * GJB;
         for (int t = tid; t < GJB * GJB; t += blockDim.x) __stcg(db + t, Ds[t / GJB][t % GJB]);
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence();
+          st_release(reinterpret_cast<int *>(bar + 1), K1 / GJB);   // D_{K+1}^-1 published
+        }
       }
     } else {
       if (K == 0) {   // panel 0: D_0^-1 locally (warps 0-3) while warps 4-7 stage the first tile
@@ -799,6 +834,10 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
           load_tile(Sin, K, b, (blockIdx.x / nt) * GJT, (blockIdx.x % nt) * GJT, tid - 128, 128);
         }
       } else {        // the helper's D_K^-1 (loads in flight while the first tile's are issued)
+        if (tid == 0)
+          while (ld_acquire(reinterpret_cast<const int *>(bar + 1)) < K / GJB) {
+          }
+        __syncthreads();
         const double *db = dbuf + ((K / GJB) & 1) * GJB * GJB;
         double dv[GJB * GJB / 256];
 #pragma unroll
@@ -873,7 +912,7 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
       __syncthreads();
     }
     if (prof) prof[(K / GJB) * 4 + 2] = clock64();
-    grid_barrier_count(bar, gen);
+    if (!helper) grid_barrier_n(bar, gen, ntcta);   // the tile CTAs only (see the lookahead CTA)
     if (prof) prof[(K / GJB) * 4 + 3] = clock64();
     double *t = Sin;
     Sin = Sout;
@@ -3904,10 +3943,12 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
         gdbg = buf;
       }
     double *dbuf = c->gj_dbuf;
-    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar, &gdbg, &dbuf};
+    int gj_warps = 8;
+    if (const char *env = getenv("RH_GJW")) gj_warps = atoi(env);   // experiment
+    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar, &gdbg, &dbuf, &gj_warps};
     const int ntl = ((ns + GJT - 1) / GJT) * ((ns + GJT - 1) / GJT);
     const int grid = std::max(1, std::min(ntl, c->coop_blocks - 1)) + 1;   // tile CTAs + the lookahead CTA
-    RH_CUDA(c, cudaMemsetAsync(c->grid_bar, 0, sizeof(unsigned), st));
+    RH_CUDA(c, cudaMemsetAsync(c->grid_bar, 0, 2 * sizeof(unsigned), st));   // tiles' arrivals, D^-1 flag
     RH_CUDA(c, cudaLaunchCooperativeKernel((const void *)k_sep_inverse, dim3(grid), dim3(256), args, gj_smem_bytes(), st));
     RH_LAUNCHED(c);
     if (gdbg) {
