@@ -305,9 +305,24 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
     // records.  Every dependency is a pair of tile rows (o0, o1) (byte offsets;
     // a one-value dependency repeats its row with a zero second coefficient);
     // lists hold the unit's dependencies padded to an even count (slots of two).
-    auto emit = [&](const std::vector<int> &u, const std::vector<std::pair<int, int>> &du, bool hdr,
-                    std::vector<int> *pos_rows, std::vector<int32_t> *pos_out) {
+    auto emit = [&](const std::vector<int> &u, std::vector<std::pair<int, int>> du, bool hdr,
+                    std::vector<int> *pos_rows, std::vector<int32_t> *pos_out, const std::vector<int> *prev) {
       const bool two = u.size() == 2;
+      // forwarding: a dependency on the unit solved just before (same warp) is read
+      // from that unit's results in registers; its coefficients go to the header
+      int fw_k0 = -1, fw_nv = 0;
+      bool fw_swap = false;
+      if (prev && hdr) {
+        const int plo = A.unit_lo[(*prev)[0]];
+        for (size_t i = 0; i < du.size(); ++i)
+          if (du[i].first == plo && A.seg_of[plo] == s) {
+            fw_k0 = plo;
+            fw_nv = du[i].second;
+            fw_swap = (*prev)[0] != plo;   // the previous unit's first row is the pair's second
+            du.erase(du.begin() + i);
+            break;
+          }
+      }
       // the list starts at an even dependency (offset pairs are read as int4 per two dependencies)
       if (((int)U.doff.size() - off0) % 4) {
         U.doff.push_back(0);
@@ -326,6 +341,12 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         const int f = u[0], sr = two ? u[1] : -1;
         rec(fwd ? -1 : inv(f), (!fwd && two) ? inv(sr) : -1, fwd ? inv(f) : -1, (fwd && two) ? inv(sr) : -1);
         if (two) rec(coef(false, sr, f), -1, coef(true, sr, f), -1);
+        if (fw_k0 >= 0) {   // the forwarded dependency's coefficient records (as a list entry's)
+          const int k0 = fw_k0, k1 = fw_nv == 2 ? fw_k0 + 1 : -1;
+          auto cf = [&](bool b, int i, int k) { return k < 0 ? -1 : coef(b, i, k); };
+          rec(cf(false, u[0], k0), cf(false, u[0], k1), cf(true, u[0], k0), cf(true, u[0], k1));
+          if (two) rec(cf(false, u[1], k0), cf(false, u[1], k1), cf(true, u[1], k0), cf(true, u[1], k1));
+        }
       }
       const int nd = (int)du.size();   // no padding to 4 (r02: lists were padded to chunks of 4)
       const int ndp = nd + (nd & 1);    // even: dep_slots takes two dependencies per slot
@@ -355,14 +376,19 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
       }
       // (x, y) tile byte offsets of the rows; z record byte offset; w offsets' byte
       // offset | ndeps << 16 | two << 30
-      if (obeg * 4 >= (1 << 16) || ndp >= (1 << 14)) U.overflow = true;
+      if (obeg * 4 >= (1 << 16) || ndp >= (1 << 13)) U.overflow = true;
       return std::array<int, 4>{A.loc_of[u[0]] * rowb, two ? A.loc_of[u[1]] * rowb : 0, cbeg * 16,
-                                obeg * 4 | ndp << 16 | (two ? 1 << 30 : 0)};
+                                obeg * 4 | ndp << 16 | (fw_swap ? 1 << 29 : 0) | (two ? 1 << 30 : 0) |
+                                    (fw_k0 >= 0 ? (int)(1u << 31) : 0)};
     };
+    const bool fwd_prev = !getenv("RH_NO_FORWARD");
     for (int ui = 0; ui < (int)units.size(); ++ui) {
       const auto &u = units[ui];
       const bool is_top = ui >= tu0;
-      const auto m = emit(u, dep_units(u, false, is_top), !is_top, nullptr, nullptr);
+      bool first_of_warp = false;   // the warp's first unit has no predecessor in registers
+      for (int w = 0; w <= UnitSweep::kWarps; ++w) first_of_warp |= lvl[w] == ui;
+      const std::vector<int> *prev = fwd_prev && !is_top && !first_of_warp ? &units[ui - 1] : nullptr;
+      const auto m = emit(u, dep_units(u, false, is_top), !is_top, nullptr, nullptr, prev);
       U.meta.insert(U.meta.end(), m.begin(), m.end());
     }
     {  // tops (dense product on the fp64 tensor cores): tile rows of the block's tops, ascending
@@ -394,7 +420,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         int r = 0;
         for (int u = lv[w]; u < lv[w + 1]; ++u) {
           const int *m = U.meta.data() + 4 * (ub + u);
-          r += ((m[3] >> 16) & 0x3fff) * ((m[3] >> 30) & 1 ? 2 : 1);
+          r += ((m[3] >> 16) & 0x1fff) * ((m[3] >> 30) & 1 ? 2 : 1);
         }
         mu = std::max(mu, lv[w + 1] - lv[w]);
         mr = std::max(mr, r);
@@ -412,7 +438,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         double mx = 0, sm = 0;
         for (int w = 0; w < UnitSweep::kWarps; ++w) {
           double c = 0;
-          for (int u = lv[w]; u < lv[w + 1]; ++u) c += 6 + ((U.meta[4 * (ub + u) + 3] >> 16) & 0x3fff);
+          for (int u = lv[w]; u < lv[w + 1]; ++u) c += 6 + ((U.meta[4 * (ub + u) + 3] >> 16) & 0x1fff);
           mx = std::max(mx, c);
           sm += c;
         }
@@ -429,7 +455,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
     long long wf_piece = 0, wf_tops = 0, deps = 0, real = 0;
     for (size_t u = 0; u < U.meta.size() / 4; ++u) {
       const int *m = U.meta.data() + 4 * u;
-      const int nd = (m[3] >> 16) & 0x3fff, two = (m[3] >> 30) & 1;
+      const int nd = (m[3] >> 16) & 0x1fff, two = (m[3] >> 30) & 1;
       wf_piece += nd * 4 + nd * (two ? 2 : 1) + (nd + 1) / 2 + (two ? 2 : 1) + 4 * (two ? 2 : 1) + 1;
       deps += nd;
     }

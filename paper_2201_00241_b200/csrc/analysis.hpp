@@ -72,8 +72,11 @@ struct UnitSweep {
   std::vector<int32_t> lvl;          // [nblk * kLvl], block-relative unit indices
   // per unit (int4): tile byte offsets of row_f and row_s (sweep order), byte
   // offset of the first record (block-relative), byte offset of the first
-  // dependency offset pair (block-relative, multiple of 16) | ndeps << 16 |
-  // two_rows << 30.  A dependency is a
+  // dependency offset pair (block-relative, multiple of 16) | ndeps << 16
+  // (13 bits) | swapped << 29 | two_rows << 30 | forwarded << 31: a forwarded
+  // unit's dependency on the unit solved just before it (same warp) is taken
+  // from that unit's results in registers, its coefficient records follow the
+  // header (swapped: the previous unit's first row is the pair's second).  A dependency is a
   // pair of tile-row byte offsets (o0, o1) and one (one-row unit) or two
   // (two-row unit) double2 coefficient records (c_f0, c_f1), (c_s0, c_s1);
   // lists are padded to an even count (r02: to chunks of 4, which read 2.5x

@@ -1156,7 +1156,7 @@ __device__ __forceinline__ void stsd(unsigned a, double v) {
 // slots of two (lists padded to an even count): slot = one int4 of tile-row
 // byte offsets (o0, o1 of dependency 2k, then of 2k + 1) and two (one-row unit)
 // or four (two-row unit) double2 coefficient records.
-__device__ __forceinline__ int unit_ns(const int4 m) { return ((m.w >> 16) & 0x3fff) >> 1; }
+__device__ __forceinline__ int unit_ns(const int4 m) { return ((m.w >> 16) & 0x1fff) >> 1; }
 __device__ __forceinline__ bool unit_two(const int4 m) { return (m.w >> 30) & 1; }
 
 // sf = sum c_f x, ss = sum c_s x over ns >= 1 slots.  Chains: dependency 2k ->
@@ -1190,30 +1190,46 @@ __device__ __forceinline__ void dep_slots(const UStage &t, unsigned rc, unsigned
 
 // one piece unit: x_f = (x_f - sum) d_f ; x_s = (x_s - sum - c_sf x_f) d_s.
 // A unit's own rows are written by nothing but the unit itself, so their
-// right-hand sides are read first (they leave the dependency chain).
+// right-hand sides are read first (they leave the dependency chain).  A
+// forwarded dependency (meta bit 31) on the unit solved just before is taken
+// from that unit's results (pf, ps) in registers, its records after the header;
+// it is added after the list's sums.  Returns this unit's (x_f, x_s).
 template <bool DINV>
-__device__ __forceinline__ void unit_solve(const UStage &t, const int4 m) {
+__device__ __forceinline__ double2 unit_solve(const UStage &t, const int4 m, double pf, double ps) {
   const unsigned rc = t.rec + m.z, of = t.doff + (m.w & 0xffff);
   const int ns = unit_ns(m);
+  const bool fw = m.w < 0;
+  const double x0 = (m.w >> 29) & 1 ? ps : pf, x1 = (m.w >> 29) & 1 ? pf : ps;   // the forwarded pair
   const double2 hd = ldsd2(rc);
   if (unit_two(m)) {
     const double bf = ldsd(t.xs + m.x), bs = ldsd(t.xs + m.y);
     const double csf = ldsd(rc + 16);
     double sf = 0.0, ss = 0.0;
-    if (ns) dep_slots<true>(t, rc + 32, of, ns, sf, ss);
+    if (ns) dep_slots<true>(t, rc + (fw ? 64 : 32), of, ns, sf, ss);
+    if (fw) {
+      const double2 p = ldsd2(rc + 32), q = ldsd2(rc + 48);
+      sf = fma(p.x, x0, fma(p.y, x1, sf));
+      ss = fma(q.x, x0, fma(q.y, x1, ss));
+    }
     double xf = bf - sf;
     if (DINV) xf *= hd.x;
     double xs = fma(-csf, xf, bs - ss);
     if (DINV) xs *= hd.y;
     stsd(t.xs + m.x, xf);
     stsd(t.xs + m.y, xs);
+    return make_double2(xf, xs);
   } else {
     const double bf = ldsd(t.xs + m.x);
     double sf = 0.0, ss;
-    if (ns) dep_slots<false>(t, rc + 16, of, ns, sf, ss);
+    if (ns) dep_slots<false>(t, rc + (fw ? 32 : 16), of, ns, sf, ss);
+    if (fw) {
+      const double2 p = ldsd2(rc + 16);
+      sf = fma(p.x, x0, fma(p.y, x1, sf));
+    }
     double xf = bf - sf;
     if (DINV) xf *= hd.x;
     stsd(t.xs + m.x, xf);
+    return make_double2(xf, xf);
   }
 }
 
@@ -1221,10 +1237,11 @@ template <bool DINV>
 __device__ __forceinline__ void unit_pieces(const UStage &t, int warp) {
   const int q0 = t.lvl[warp], q1 = t.lvl[warp + 1];
   int4 m = q0 < q1 ? t.meta[q0] : make_int4(0, 0, 0, 0);
+  double2 x = make_double2(0.0, 0.0);   // the previous unit's results (forwarding)
 #pragma unroll 1
   for (int u = q0; u < q1; ++u) {
     const int4 mn = u + 1 < q1 ? t.meta[u + 1] : m;
-    unit_solve<DINV>(t, m);
+    x = unit_solve<DINV>(t, m, x.x, x.y);
     m = mn;
   }
 }
