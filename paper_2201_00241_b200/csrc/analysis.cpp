@@ -167,7 +167,7 @@ BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<int32
   }
   BlockSplit B;
   // LPT of the pieces onto the warps by subtree cost w (per unit)
-  auto pack = [&](const std::vector<double> &w, std::vector<std::vector<int32_t>> &out) {
+  auto pack = [&](const std::vector<double> &w, std::vector<std::vector<int32_t>> &out, bool post = false) {
     std::vector<double> sw(nu);
     for (int u = 0; u < nu; ++u) {
       sw[u] = w[u];
@@ -180,6 +180,20 @@ BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<int32
     for (int p : pc) {
       const int wi = (int)(std::min_element(load.begin(), load.end()) - load.begin());
       load[wi] += sw[p];
+      if (post) {   // depth-first postorder: every parent right after its last child
+        std::vector<std::pair<int, int>> st{{p, 0}};
+        while (!st.empty()) {
+          auto &[x, ci] = st.back();
+          if (ci < (int)kids[x].size()) {
+            const int k = kids[x][ci++];
+            st.push_back({k, 0});
+          } else {
+            for (int i = ubeg[x]; i < ubeg[x + 1]; ++i) out[wi].push_back(rows[i]);
+            st.pop_back();
+          }
+        }
+        continue;
+      }
       std::vector<int> st{p};
       while (!st.empty()) {
         const int x = st.back();
@@ -188,7 +202,8 @@ BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<int32
         for (int k : kids[x]) st.push_back(k);
       }
     }
-    for (auto &v : out) std::sort(v.begin(), v.end());  // ascending = forward topological
+    if (!post)
+      for (auto &v : out) std::sort(v.begin(), v.end());  // ascending = forward topological
   };
   if (!dual) {
     pack(cost, B.warp_rows);
@@ -206,8 +221,13 @@ BlockSplit split_block(const std::vector<int32_t> &rows, const std::vector<int32
         sort_unique(du);
         (dir == 0 ? cf : cb)[u] = kUnitLat + (double)du.size();
       }
-    pack(cf, B.warp_rows);
-    pack(cb, B.warp_rows_b);
+    // unit sweeps: pieces in depth-first postorder (forward sweeps: a parent right
+    // after its last child; the backward sweeps walk it reversed: a parent right
+    // before one of its children), so most units forward a dependency from the
+    // unit solved just before (build_units)
+    const bool post = !getenv("RH_NO_POSTORDER");
+    pack(cf, B.warp_rows, post);
+    pack(cb, B.warp_rows_b, post);
   }
   for (int u = 0; u < nu; ++u)
     if (is_top[u])
@@ -349,7 +369,7 @@ void build_units(Analysis &A, bool fwd, const std::vector<std::vector<int32_t>> 
         }
       }
       const int nd = (int)du.size();   // no padding to 4 (r02: lists were padded to chunks of 4)
-      const int ndp = nd + (nd & 1);    // even: dep_slots takes two dependencies per slot
+      const int ndp = nd;               // slots of two, an odd last one alone (dep_slots)
       const int rowb = UnitSweep::kCols * 8;
       for (int di = 0; di < ndp; ++di) {
         if (di >= nd) {   // padding: zero coefficients on the unit's own (finite) row

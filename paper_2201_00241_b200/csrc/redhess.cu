@@ -1156,12 +1156,25 @@ __device__ __forceinline__ void stsd(unsigned a, double v) {
 // slots of two (lists padded to an even count): slot = one int4 of tile-row
 // byte offsets (o0, o1 of dependency 2k, then of 2k + 1) and two (one-row unit)
 // or four (two-row unit) double2 coefficient records.
-__device__ __forceinline__ int unit_ns(const int4 m) { return ((m.w >> 16) & 0x1fff) >> 1; }
+__device__ __forceinline__ int unit_nd(const int4 m) { return (m.w >> 16) & 0x1fff; }
+__device__ __forceinline__ int unit_ns(const int4 m) { return unit_nd(m) >> 1; }
 __device__ __forceinline__ bool unit_two(const int4 m) { return (m.w >> 30) & 1; }
 
 // sf = sum c_f x, ss = sum c_s x over ns >= 1 slots.  Chains: dependency 2k ->
 // (f0, f1), 2k + 1 -> (f2, f3) (and s); slot 0 starts them (products, no zero
 // fill), fixed order (deterministic).
+template <bool TWO>
+__device__ __forceinline__ void dep_one(const UStage &t, unsigned rc, unsigned of, double &sf, double &ss) {
+  int2 o;
+  asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(o.x), "=r"(o.y) : "r"(of));
+  const double2 p0 = ldsd2(rc), q0 = TWO ? ldsd2(rc + 16) : p0;
+  const double x00 = ldsd(t.xs + o.x), x01 = ldsd(t.xs + o.y);
+  sf = fma(p0.x, x00, fma(p0.y, x01, sf));
+  if (TWO) ss = fma(q0.x, x00, fma(q0.y, x01, ss));
+}
+// a list of nd >= 1 dependencies: slots of two, then an odd last one alone
+template <bool TWO>
+__device__ __forceinline__ void dep_list(const UStage &t, unsigned rc, unsigned of, int nd, double &sf, double &ss);
 template <bool TWO>
 __device__ __forceinline__ void dep_slots(const UStage &t, unsigned rc, unsigned of, int ns, double &sf, double &ss) {
   double f0, f1, f2, f3, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -1187,6 +1200,14 @@ __device__ __forceinline__ void dep_slots(const UStage &t, unsigned rc, unsigned
   sf = (f0 + f1) + (f2 + f3);
   ss = (s0 + s1) + (s2 + s3);
 }
+template <bool TWO>
+__device__ __forceinline__ void dep_list(const UStage &t, unsigned rc, unsigned of, int nd, double &sf, double &ss) {
+  const int ns = nd >> 1;
+  sf = 0.0;
+  ss = 0.0;
+  if (ns) dep_slots<TWO>(t, rc, of, ns, sf, ss);
+  if (nd & 1) dep_one<TWO>(t, rc + ns * (TWO ? 64 : 32), of + ns * 16, sf, ss);
+}
 
 // one piece unit: x_f = (x_f - sum) d_f ; x_s = (x_s - sum - c_sf x_f) d_s.
 // A unit's own rows are written by nothing but the unit itself, so their
@@ -1197,7 +1218,7 @@ __device__ __forceinline__ void dep_slots(const UStage &t, unsigned rc, unsigned
 template <bool DINV>
 __device__ __forceinline__ double2 unit_solve(const UStage &t, const int4 m, double pf, double ps) {
   const unsigned rc = t.rec + m.z, of = t.doff + (m.w & 0xffff);
-  const int ns = unit_ns(m);
+  const int nd = unit_nd(m);
   const bool fw = m.w < 0;
   const double x0 = (m.w >> 29) & 1 ? ps : pf, x1 = (m.w >> 29) & 1 ? pf : ps;   // the forwarded pair
   const double2 hd = ldsd2(rc);
@@ -1205,7 +1226,7 @@ __device__ __forceinline__ double2 unit_solve(const UStage &t, const int4 m, dou
     const double bf = ldsd(t.xs + m.x), bs = ldsd(t.xs + m.y);
     const double csf = ldsd(rc + 16);
     double sf = 0.0, ss = 0.0;
-    if (ns) dep_slots<true>(t, rc + (fw ? 64 : 32), of, ns, sf, ss);
+    if (nd) dep_list<true>(t, rc + (fw ? 64 : 32), of, nd, sf, ss);
     if (fw) {
       const double2 p = ldsd2(rc + 32), q = ldsd2(rc + 48);
       sf = fma(p.x, x0, fma(p.y, x1, sf));
@@ -1221,7 +1242,7 @@ __device__ __forceinline__ double2 unit_solve(const UStage &t, const int4 m, dou
   } else {
     const double bf = ldsd(t.xs + m.x);
     double sf = 0.0, ss;
-    if (ns) dep_slots<false>(t, rc + (fw ? 32 : 16), of, ns, sf, ss);
+    if (nd) dep_list<false>(t, rc + (fw ? 32 : 16), of, nd, sf, ss);
     if (fw) {
       const double2 p = ldsd2(rc + 16);
       sf = fma(p.x, x0, fma(p.y, x1, sf));
@@ -1270,15 +1291,15 @@ __device__ __forceinline__ void unit_tops(const UStage &t, const double *X, int 
     if (u < u1) {
       const int4 m = t.meta[u];
       const unsigned rc = t.rec + m.z, of = t.doff + (m.w & 0xffff);
-      const int ns = unit_ns(m);
-      if (!ns) continue;
+      const int nd = unit_nd(m);
+      if (!nd) continue;
       double sf, ss;
       if (unit_two(m)) {
-        dep_slots<true>(t, rc, of, ns, sf, ss);
+        dep_list<true>(t, rc, of, nd, sf, ss);
         stsd(t.xs + m.x, ldsd(t.xs + m.x) - sf);
         stsd(t.xs + m.y, ldsd(t.xs + m.y) - ss);
       } else {
-        dep_slots<false>(t, rc, of, ns, sf, ss);
+        dep_list<false>(t, rc, of, nd, sf, ss);
         stsd(t.xs + m.x, ldsd(t.xs + m.x) - sf);
       }
     }
