@@ -2515,7 +2515,6 @@ struct rh_ctx {
   cudaEvent_t ev_state = nullptr, ev_tape = nullptr;
   cudaEvent_t ev_vl = nullptr;   // separator rows' L / U^T values ready (after R_B1)
   cudaEvent_t ev_ult = nullptr;   // fused call: L^T records (side stream)
-  cudaEvent_t ev_tr = nullptr;   // S^-T ready (k_transpose; the gradient stream in the fused call)
   bool tr_pending = false;       // fused call: S^-T not yet launched (reduced_hessian_impl does it)
   bool early_gathered = false;   // the fused call's early batches also formed their separator rhs
   double *grad_tsep = nullptr;
@@ -2555,7 +2554,6 @@ struct rh_ctx {
     if (ev_tape) cudaEventDestroy(ev_tape), ev_tape = nullptr;
     if (ev_vl) cudaEventDestroy(ev_vl), ev_vl = nullptr;
     if (ev_ult) cudaEventDestroy(ev_ult), ev_ult = nullptr;
-    if (ev_tr) cudaEventDestroy(ev_tr), ev_tr = nullptr;
     if (grad_tsep) cudaFree(grad_tsep), grad_tsep = nullptr;
     if (grad_ctr) cudaFree(grad_ctr), grad_ctr = nullptr;
     tape_wait = nullptr;
@@ -3385,7 +3383,8 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
     if (h.tmask && !getenv("RH_NO_SPMM")) {   // Cartesian batch: S^-1 over T's nonzero rows only
       k_sep_spmm<<<dim3(ld / 32, (A.sep_rows + SPM - 1) / SPM), 256, spmm_smem_bytes(A.sep_rows), st>>>(h);
     } else {
-      if (c->ev_tr) RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_tr, 0));   // reads S^-T
+      // reads S^-T: formed on the state's stream (rh_set_state) or, in the fused
+      // call, on the gradient stream that the call joins before it returns
       k_sep_gemm<<<gSm, GTHREADS, gemm_smem_bytes(), st>>>(h, MODE_LU);
     }
     RH_LAUNCHED(c);
@@ -4000,15 +3999,14 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     }
     dbg_mark(st, "k_sep_inverse");
     // S^-T (the dense L-side product of random-W batches, the gradient's transposed
-    // GEMV): in the fused call on the gradient stream, so the Cartesian batches
-    // (their L-side product reads S^-1) do not wait for it; users wait on ev_tr
-    if (!c->ev_tr) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_tr, cudaEventDisableTiming));
+    // GEMV): in the fused call on the gradient stream (which the call joins before
+    // it returns), so the Cartesian batches (their L-side product reads S^-1) do
+    // not wait for it
     if (early && side) {
       c->tr_pending = true;   // the fused call runs it first on the gradient stream
     } else {
       k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, st>>>(c->Sinv, c->SinvT, ns);
       RH_LAUNCHED(c);
-      RH_CUDA(c, cudaEventRecord(c->ev_tr, st));
     }
   }
   if (c->nrec_b > 0 && !(early && side && A.sep_rows > 0)) {   // L^T records: block rows' L entries include L_sb (R_B1)
@@ -4430,7 +4428,6 @@ int reduced_hessian_impl(rh_ctx *c, const double *x, const double *p, int j0, in
       const int ns = c->A.sep_rows;
       k_transpose<<<dim3((ns + 31) / 32, (ns + 31) / 32), dim3(32, 8), 0, c->grad_st>>>(c->Sinv, c->SinvT, ns);
       RH_LAUNCHED(c);
-      RH_CUDA(c, cudaEventRecord(c->ev_tr, c->grad_st));
       c->tr_pending = false;
     }
     rc = gradient_impl(c, grad_p, nullptr, c->grad_st, true);

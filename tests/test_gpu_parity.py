@@ -341,6 +341,14 @@ def test_fused_call_graph_replay(own_stream):
     finally:
         del os.environ["RH_NO_GRAPH"]
     assert np.array_equal(_np(Hr), outs[3][1]) and np.array_equal(_np(gr), outs[3][0])
+    # after graph replays, separate calls on the same state (the bench's order): a
+    # random-W batch (dense separator GEMM on S^-T, formed on the fused call's
+    # gradient stream) equals the uncaptured context's
+    W = _dev(np.random.default_rng(3).standard_normal((ctx.n_p, 64)))
+    with torch.cuda.stream(s):
+        HW = ctx.hvp(W, stream=s)
+        s.synchronize()
+    assert np.array_equal(_np(HW), _np(ref.hvp(W)))
 
 
 def test_host_call_graph_replay():
