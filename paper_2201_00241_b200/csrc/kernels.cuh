@@ -108,13 +108,13 @@ struct SegParams {
   // outputs' range, 2D TMA boxes), then one row per remaining Z source (per-row
   // bulk copies, fg_cp: staging row, Z row) and per W / zero source (fg_fill:
   // staging row, p row or -1).  A local's (theta, v) staging rows are packed
-  // theta | v << 16 (fg_loc .w for every local, fg_soe for the other end of a slot).
+  // theta | v << 16 in fg_loc .w; fg_soe holds the other end's rows of a slot as byte offsets.
   const int *fg_off, *fg_nout, *fg_obase, *fg_sbase, *fg_ref, *fg_ref_loc;
   const int *fg_zlo, *fg_zn, *fg_cp_off, *fg_fill_off;
   const int2 *fg_cp, *fg_fill;
   int fg_maxrows, fg_maxout, fg_maxslots;
   const int4 *fg_loc, *fg_odst;        // per local: sources, bus, packed staging rows; per output: theta row, v row, first slot, slots
-  const int *fg_soe;                   // per slot: packed staging rows of the other end
+  const int2 *fg_soe;                  // per slot: byte offsets (theta, v) of the other end's staging rows
   const double4 *fg_scoef, *fg_ometa;  // per state and lambda (k_for_tape): slot coefficients; dcoef, grad P_ref
   const int *p_kind;                   // Pg diagonal of Y_p in k_muladd
   const double *pdiag;                 // [n_p] 2 c2 (Pg parameters) else 0

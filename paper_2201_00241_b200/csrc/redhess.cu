@@ -2008,7 +2008,8 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
   double4 *s_coef = reinterpret_cast<double4 *>(fsm + (size_t)h.fg_maxrows * 32);
   double4 *s_meta = s_coef + h.fg_maxslots;
   int4 *s_dst = reinterpret_cast<int4 *>(s_meta + h.fg_maxout);
-  int *s_oe = reinterpret_cast<int *>(s_dst + h.fg_maxout);
+  // per slot: byte offsets (theta, v) of the other end's staging rows
+  const int2 *s_oe = reinterpret_cast<const int2 *>(s_dst + h.fg_maxout);
   // timing experiment (RH_DEBUG & 8192): per CTA [start, armed, row copies issued, filled,
   // copies landed, end]
   long long *prof = ((h.debug & 8192) && h.dbg && g * gridDim.y + blockIdx.y < 16384)
@@ -2021,10 +2022,10 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    const unsigned tx = 256u * (zn + ncp) + 36u * nsl + 48u * nout;
+    const unsigned tx = 256u * (zn + ncp) + 40u * nsl + 48u * nout;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&mbar)), "r"(tx) : "memory");
     bulk_g2s(s_coef, h.fg_scoef + sb, 32u * nsl, &mbar);
-    bulk_g2s(s_oe, h.fg_soe + sb, 4u * nsl, &mbar);
+    bulk_g2s(const_cast<int2 *>(s_oe), h.fg_soe + sb, 8u * nsl, &mbar);
     bulk_g2s(s_meta, h.fg_ometa + ob, 32u * nout, &mbar);
     bulk_g2s(s_dst, h.fg_odst + ob, 16u * nout, &mbar);
     // the outputs' Z row range by 2D TMA boxes (64, then 8 rows)
@@ -2082,12 +2083,14 @@ __global__ void __launch_bounds__(kForThreads, 2) k_for(SegParams h) {
   }
   // warp per output bus, lane per column, all from shared memory; two buses at a
   // time (independent FMA chains, same per-bus order as one at a time)
+  const char *fl = reinterpret_cast<const char *>(fsm + lane);   // this lane's column of staging row 0
   auto slot = [&](int q, double dth_b, double dv_b, double &yth, double &yv) {
     // canonical slot coefficients (k_for_tape): D = dth_b - dth_o,
     // yth += K D + c2 dv_b + c3 dv_o,  yv += c2 D + m dv_o
     const double4 k = s_coef[q];
-    const int o = s_oe[q];
-    const double D = dth_b - fsm[(o & 0xffff) * 32 + lane], dv_o = fsm[(o >> 16) * 32 + lane];
+    const int2 o = s_oe[q];
+    const double D = dth_b - *reinterpret_cast<const double *>(fl + o.x);
+    const double dv_o = *reinterpret_cast<const double *>(fl + o.y);
     yth = fma(k.x, D, fma(k.y, dv_b, fma(k.z, dv_o, yth)));
     yv = fma(k.y, D, fma(k.w, dv_o, yv));
   };
@@ -2469,7 +2472,8 @@ struct rh_ctx {
   int smem_stride = 0;
   int *blk_ctr = nullptr;
   size_t smem_blk = 0, smem_for = 0;
-  int *fg_off, *fg_nout, *fg_obase, *fg_sbase, *fg_ref, *fg_ref_loc, *fg_soe, *fg_out_bus;
+  int *fg_off, *fg_nout, *fg_obase, *fg_sbase, *fg_ref, *fg_ref_loc, *fg_out_bus;
+  int2 *fg_soe;
   int *fg_zlo, *fg_zn, *fg_cp_off, *fg_fill_off;
   int2 *fg_cp, *fg_fill;
   int fg_maxrows = 1;
@@ -2830,7 +2834,7 @@ int upload(rh_ctx *c) {
   };
   {  // staged tensor projection tiles; delta sources and outputs -> Z rows
     const ForGroups &F = A.fg;
-    std::vector<int32_t> loc = F.loc, dst = F.out_dst, soe(F.slots.size() / 2);
+    std::vector<int32_t> loc = F.loc, dst = F.out_dst, soe(F.slots.size());
     for (size_t i = 0; i < loc.size(); i += 4) {
       if (loc[i] >= 0) loc[i] = zrow[loc[i]];
       if (loc[i + 1] >= 0) loc[i + 1] = zrow[loc[i + 1]];
@@ -2878,8 +2882,11 @@ int upload(rh_ctx *c) {
       cpo.push_back((int)cp.size() / 2);
       fio.push_back((int)fi.size() / 2);
       maxrows = std::max(maxrows, next);
-      for (int q = F.grp_sbase[gi]; q < F.grp_sbase[gi + 1]; ++q)
-        soe[q] = loc[4 * (lb + (F.slots[2 * q + 1] >> 1)) + 3];
+      for (int q = F.grp_sbase[gi]; q < F.grp_sbase[gi + 1]; ++q) {   // byte offsets of the other end's rows
+        const int r = loc[4 * (lb + (F.slots[2 * q + 1] >> 1)) + 3];
+        soe[2 * q] = (r & 0xffff) * 256;
+        soe[2 * q + 1] = (r >> 16) * 256;
+      }
       for (int i = 0; i < no; ++i) {   // per output: (theta row, v row, first slot | slots << 16, own staging rows)
         const int o = F.grp_obase[gi] + i;
         dst[4 * o + 2] = dst[4 * o + 2] | (dst[4 * o + 3] << 16);
@@ -2903,7 +2910,7 @@ int upload(rh_ctx *c) {
     chk(c->fg_loc);
     chk(c->fg_odst);
     chk(c->fg_slots);
-    chk(c->fg_soe = dalloc_copy(soe, P));
+    chk(c->fg_soe = reinterpret_cast<int2 *>(dalloc_copy(soe, P)));
     chk(c->fg_out_bus = dalloc_copy(F.out_bus, P));
     chk(c->fg_off = dalloc_copy(F.grp_off, P));
     chk(c->fg_nout = dalloc_copy(F.grp_nout, P));
@@ -2911,13 +2918,13 @@ int upload(rh_ctx *c) {
     chk(c->fg_sbase = dalloc_copy(F.grp_sbase, P));
     chk(c->fg_ref = dalloc_copy(F.grp_ref, P));
     chk(c->fg_ref_loc = dalloc_copy(F.ref_loc, P));
-    chk(c->fg_scoef = dalloc<double4>(soe.size(), P));
+    chk(c->fg_scoef = dalloc<double4>(soe.size() / 2, P));
     std::vector<double> pdiag(A.n_p, 0.0);
     for (int q = 0; q < A.n_p; ++q)
       if (A.p_kind[q] == RH_KIND_PG) pdiag[q] = 2.0 * A.c2b[A.p_bus[q]];
     chk(c->pdiag = dalloc_copy(pdiag, P));
     chk(c->fg_ometa = dalloc<double4>(F.out_bus.size(), P));
-    c->smem_for = (size_t)c->fg_maxrows * 32 * sizeof(double) + (size_t)F.max_slots * 36 + (size_t)F.max_nout * 48;
+    c->smem_for = (size_t)c->fg_maxrows * 32 * sizeof(double) + (size_t)F.max_slots * 40 + (size_t)F.max_nout * 48;
   }
   mkunit(c->duf, A.ufwd, c->dfwd);
   mkunit(c->dub, A.ubwd, c->dbwd);
