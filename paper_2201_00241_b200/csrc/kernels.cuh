@@ -57,6 +57,13 @@ struct SegParams {
   // [box 32 x 64 rows, box 32 x 8 rows]; null = per-row copies (k_blk)
   const void *tmZ, *tmP;
   int kblk_group;                    // k_blk: column chunks per ticket (one block's structure staged once)
+  // split U sweep of Cartesian batches: k_blk MODE_U with
+  // spike = 1 sweeps the live tiles with the staged separator rows taken as zero (Z^0,
+  // dead tiles skipped), spike = 2 computes the blocks' spikes (block rows zero,
+  // staged separator rows = identity columns) into Msp; k_spike then forms
+  // Z_b = Z_b^0 + Msp_b z_ext
+  int spike;
+  const double *Msp;                 // [n_x][kSpLd] per block row: -(U_bb^-1 U_bs) over the block's staged separator rows
   const int *seg_row_off, *row_global;
   DSeg fwd, bwd;
   const double *vL, *vUt;             // separator rows' L / U^T values (fwd entry order)

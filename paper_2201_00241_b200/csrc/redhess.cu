@@ -1454,8 +1454,9 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     for (int ci = cbeg; ci < cend; ++ci) {
     // Cartesian batch: an L tile whose right-hand side is zero stays zero (not
     // computed, not stored); the U sweep starts such a tile from zeros
-    const bool live = tile_live(h, s, ci);
-    if (mode == MODE_L && !live) continue;
+    const bool live = h.spike != 2 && tile_live(h, s, ci);
+    if ((mode == MODE_L || h.spike == 1) && !live) continue;   // (U0: a dead tile's Z^0 is zero, never stored)
+    if (h.spike == 2 && ci * kBC >= U.ext_off[s + 1] - U.ext_off[s]) continue;   // spike columns beyond the block's
     const bool first = !staged;
     staged = true;
     if (!first) {
@@ -1481,7 +1482,7 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     // block rows by 2D TMA boxes (64, then 8 rows), the rest (< 8 block rows, staged
     // separator rows) by 16-byte cp.async
     const char *tm = reinterpret_cast<const char *>(G == h.Z ? h.tmZ : h.tmP);
-    const bool zfill = mode == MODE_U && !live;   // its L result is zero: no block rows to load
+    const bool zfill = mode == MODE_U && !live;   // its L result is zero (or a spike tile): no block rows to load
     const int nbig = tm && !zfill ? nr / kTmaBig : 0, nsmall = tm && !zfill ? (nr - nbig * kTmaBig) / kTmaSmall : 0;
     const int rows_tma = mode == MODE_L ? 0 : nbig * kTmaBig + nsmall * kTmaSmall;
     const int rows_zero = zfill ? nr : 0;
@@ -1526,6 +1527,12 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     {  // X rows: 16-byte cp.async (LSU path; 256 B TMA bulk copies are rate-bound on the TMA unit)
       const int c = tid & 15;
       for (int a = rows_tma + rows_zero + (tid >> 4); a < nxrows; a += blockDim.x >> 4) {
+        if (a >= nr && h.spike) {   // staged separator rows: zero (U0) or identity columns (spikes)
+          const int k = a - nr - col0;
+          reinterpret_cast<double2 *>(X + a * kBC)[c] =
+              make_double2(h.spike == 2 && k == 2 * c ? 1.0 : 0.0, h.spike == 2 && k == 2 * c + 1 ? 1.0 : 0.0);
+          continue;
+        }
         const long long grow = a < nr ? r0 + a : U.ext_rows[x0 + a - nr];
         cp_async16(X + a * kBC + 2 * c, G + grow * h.ld + col0 + 2 * c);
       }
@@ -1571,18 +1578,20 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // sweep writes -> bulk store reads
     __syncthreads();
-    {
-      const int nbs = tm ? nr / kTmaBig : 0, nss = tm ? (nr - nbs * kTmaBig) / kTmaSmall : 0;
+    {  // (U0: Z^0 goes to P, Z keeps the L sweep's result for the separator gather)
+      const char *ts = h.spike == 1 ? reinterpret_cast<const char *>(h.tmP) : tm;
+      double *Gs = h.spike == 1 ? h.P : G;
+      const int nbs = ts ? nr / kTmaBig : 0, nss = ts ? (nr - nbs * kTmaBig) / kTmaSmall : 0;
       const int rows_st = nbs * kTmaBig + nss * kTmaSmall;
       if (tid == 0) {
-        for (int i = 0; i < nbs; ++i) tma2d_s2g(tm, col0, r0 + i * kTmaBig, X + i * kTmaBig * kBC);
+        for (int i = 0; i < nbs; ++i) tma2d_s2g(ts, col0, r0 + i * kTmaBig, X + i * kTmaBig * kBC);
         for (int i = 0; i < nss; ++i) {
           const int a = nbs * kTmaBig + i * kTmaSmall;
-          tma2d_s2g(tm + kTmapBytes, col0, r0 + a, X + a * kBC);
+          tma2d_s2g(ts + kTmapBytes, col0, r0 + a, X + a * kBC);
         }
       }
       for (int a = rows_st + tid; a < nr; a += blockDim.x)
-        bulk_s2g(G + (long long)(r0 + a) * h.ld + col0, X + a * kBC, kRowB);
+        bulk_s2g(Gs + (long long)(r0 + a) * h.ld + col0, X + a * kBC, kRowB);
     }
     if (nsr) {
       // partials of this block's runs (U^T: separator right-hand sides, k_sep_gather
@@ -1629,6 +1638,59 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
       ctr[1] = 0;
       __threadfence();
     }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// Split U sweep of Cartesian batches (SURVEY.md
+// 8(a)-6).  A block's U rows depend on the separator only through its staged
+// separator rows z_ext (U_bs), so by linearity
+//   z_b = U_bb^-1 (y_b - U_bs z_ext) = Z_b^0 + Msp_b z_ext,
+//   Z_b^0 = U_bb^-1 y_b (k_blk MODE_U, spike = 1: needs no S^-1, runs while the
+//   separator is inverted; zero for the dead tiles of a Cartesian batch),
+//   Msp_b = -U_bb^-1 U_bs (k_blk MODE_U, spike = 2, once per state: the block's
+//   sweep of identity columns on its staged separator rows).
+// k_spike forms z_b for every (block, 32-column) tile once z_ext is known: a
+// dense [rows x K] x [K x 32] product on the fp64 tensor cores (DMMA m8n8k4,
+// K = the block's staged separator rows rounded up to 4), accumulated onto
+// Z_b^0 (live tiles) and stored.  Per column the arithmetic does not depend on
+// the batch (bitwise N- and mask-invariant).
+// ----------------------------------------------------------------------------
+constexpr int kSpLd = 64;       // Msp row stride: at most 64 staged separator rows per block
+constexpr int kSpThreads = 256;
+__global__ void __launch_bounds__(kSpThreads) k_spike(SegParams h) {
+  __shared__ __align__(16) double zs[kSpLd][36];   // z_ext rows x 32 columns (stride 36: conflict-free B fragments)
+  const int s = blockIdx.x, ci = blockIdx.y, col0 = ci * kBC;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const DUnit &U = h.ub;
+  const int r0 = h.seg_row_off[s], nr = h.seg_row_off[s + 1] - r0;
+  const int x0 = U.ext_off[s], nxr = U.ext_off[s + 1] - x0, K = (nxr + 3) & ~3;
+  const bool live = tile_live(h, s, ci);
+  for (int k = warp; k < K; k += kSpThreads / 32)
+    zs[k][lane] = k < nxr ? h.Z[(long long)U.ext_rows[x0 + k] * h.ld + col0 + lane] : 0.0;
+  __syncthreads();
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int mt = warp; mt * 8 < nr; mt += kSpThreads / 32) {
+    const int r = mt * 8 + gid;
+    const bool in = r < nr;
+    double *zr = h.Z + (long long)(r0 + r) * h.ld + col0 + 2 * tig;
+    const double *z0 = h.P + (long long)(r0 + r) * h.ld + col0 + 2 * tig;   // Z^0 (k_blk U0)
+    double c[4][2];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const double2 v = in && live ? *reinterpret_cast<const double2 *>(z0 + 8 * n) : make_double2(0.0, 0.0);
+      c[n][0] = v.x;
+      c[n][1] = v.y;
+    }
+    const double *ar = h.Msp + (long long)(r0 + (in ? r : 0)) * kSpLd + tig;
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const double a = in ? __ldg(ar + k0) : 0.0;
+#pragma unroll
+      for (int n = 0; n < 4; ++n) dmma_8x8x4(c[n][0], c[n][1], a, zs[k0 + tig][8 * n + gid]);
+    }
+    if (in)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) *reinterpret_cast<double2 *>(zr + 8 * n) = make_double2(c[n][0], c[n][1]);
   }
 }
 
@@ -2535,6 +2597,11 @@ struct rh_ctx {
   cudaEvent_t tape_wait = nullptr;   // set while a fused call enqueues its batches
   // side stream of the fused call: block-only derived values done; each early L sweep done
   cudaEvent_t ev_derived = nullptr, ev_early[kNumWs] = {};
+  // split U sweep of Cartesian batches (k_spike): per-block spikes, recomputed per state
+  double *Msp = nullptr;
+  bool spike_ok = false, spike_pending = false;
+  cudaEvent_t ev_spike = nullptr;
+  cudaStream_t spk_st = nullptr;
   struct TMapEntry {
     const double *base;
     int ld;
@@ -2562,6 +2629,8 @@ struct rh_ctx {
     if (grad_ctr) cudaFree(grad_ctr), grad_ctr = nullptr;
     tape_wait = nullptr;
     if (ev_derived) cudaEventDestroy(ev_derived), ev_derived = nullptr;
+    if (ev_spike) cudaEventDestroy(ev_spike), ev_spike = nullptr;
+    if (spk_st) cudaStreamDestroy(spk_st), spk_st = nullptr;
     for (auto &e : ev_early)
       if (e) cudaEventDestroy(e), e = nullptr;
     if (ev_cp) cudaEventDestroy(ev_cp), ev_cp = nullptr;
@@ -3003,6 +3072,12 @@ int upload(rh_ctx *c) {
   chk(c->grid_bar = dalloc<unsigned>(2, P));
   chk(c->gj_dbuf = dalloc<double>(2 * 32 * 32, P));
   chk(c->nwt = dalloc<double>(4, P));
+  {  // split U sweep (k_spike): every block's staged separator rows fit the spike stride
+    int mx = 0;
+    for (int s = 0; s < A.nblk; ++s) mx = std::max(mx, A.bwd.ext_off[s + 1] - A.bwd.ext_off[s]);
+    c->spike_ok = A.sep_rows > 0 && A.nblk > 0 && mx <= kSpLd && !getenv("RH_NO_SPIKE");
+    if (c->spike_ok) chk(c->Msp = dalloc<double>((size_t)nx * kSpLd, P));
+  }
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
   // shared-memory footprints
   c->smem_fact_blk = fact_smem_bytes(A);
@@ -3189,6 +3264,8 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.Yp = c->ws[k].Yp;
   h.kblk_group = 2;
   if (const char *env = getenv("RH_KBLK_GROUP")) h.kblk_group = std::max(1, atoi(env));   // tuning override
+  h.spike = 0;
+  h.Msp = c->Msp;
   h.gp_rptr = c->gp_rptr;
   h.gp_col = c->gp_col;
   h.gp_val = c->gp_val;
@@ -3319,6 +3396,26 @@ int build_tape(rh_ctx *c, cudaStream_t st) {
 // 3 = only the separator right-hand sides (needs the separator rows' L values, not
 // S^-1; after phase 1), 4 = the rest after phases 1 and 3
 void dbg_mark(cudaStream_t st, const char *label);
+// The blocks' spikes Msp_b = -U_bb^-1 U_bs of the split U sweep (k_spike), once
+// per state before the first Cartesian batch: k_blk MODE_U (spike = 2) on
+// identity columns of each block's staged separator rows (one or two 32-column
+// chunks per block), written in Z's row order with row stride kSpLd.
+int ensure_spikes(rh_ctx *c, cudaStream_t st) {
+  if (!c->spike_ok || !c->spike_pending) return RH_OK;
+  SegParams h = make_params(c, 0);
+  h.N = kSpLd;
+  h.ld = kSpLd;
+  h.Z = const_cast<double *>(c->Msp);
+  h.tmZ = tmap_pair(c, c->Msp, kSpLd);
+  h.tmP = nullptr;
+  h.spike = 2;
+  const int g = (int)std::min<long long>(2LL * c->nsm, (long long)c->A.nblk * (kSpLd / kBC));
+  k_blk<<<g, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
+  RH_LAUNCHED(c);
+  c->spike_pending = false;
+  return RH_OK;
+}
+
 int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW, long long ldhw,
              int transposed, int N, cudaStream_t st, double *Zo = nullptr, double *Yxo = nullptr,
              double *Psio = nullptr, long long ldz = 0, int wsi = 0, int phase = 0) {
@@ -3374,10 +3471,20 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
     if (timing) cudaEventRecord(ev[i], st);
     if (wsi < kNumWs && (phase != 1 || i <= 1) && (phase < 2 || i >= 1)) dbg_mark(st, kMarkNames[wsi][i]);
   };
+  // Cartesian batches: split U sweep (k_spike) - Z^0 (into P) right after the L
+  // sweep (it needs neither R_B1 nor S^-1: in the fused call it runs while the
+  // separator is factored and inverted), the spikes' product once z_ext is known
+  const bool split = h.icol && c->spike_ok && has_sep;
   if (phase <= 1) {
     mark(0);
     k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_L);
     RH_LAUNCHED(c);
+    if (split) {
+      SegParams hu = h;
+      hu.spike = 1;
+      k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(hu, MODE_U);
+      RH_LAUNCHED(c);
+    }
   }
   if (phase == 1) return RH_OK;
   if (phase != 3) mark(1);
@@ -3398,9 +3505,12 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   }
   if (phase == 3) return RH_OK;
   mark(2);
-  k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
+  if (split)
+    k_spike<<<dim3(nb, ld / kBC), kSpThreads, 0, st>>>(h);
+  else
+    k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
   RH_LAUNCHED(c);
-  if ((h.debug & 8) && h.dbg) {  // timing experiment: per-tile cycles of this launch (tools/kblk_prof.py)
+  if ((h.debug & 8) && h.dbg && !split) {  // timing experiment: per-tile cycles of this launch (tools/kblk_prof.py)
     std::vector<long long> hb((size_t)12 * std::min(8192, nb * (ld / kBC)));
     cudaMemcpyAsync(hb.data(), h.dbg, hb.size() * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
@@ -3783,6 +3893,7 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   const Analysis &A = c->A;
   const int nx = A.n_x, np_ = A.n_p, nb = A.n_bus, m = A.n_line;
   c->has_state = c->has_mult = false;
+  c->spike_pending = true;
   dbg_mark(st, "state start");
   // x, p into the context, zeroed accumulators, bus state and line trig (one launch)
   k_state_prep<<<2 * c->nsm, kThreads, 0, st>>>(nx, np_, x, p, c->x, c->p, (long long)A.F_col.size(), c->F_val,
@@ -3926,6 +4037,13 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   if (early) {
     if (!c->ev_derived) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_derived, cudaEventDisableTiming));
     RH_CUDA(c, cudaEventRecord(c->ev_derived, sb));   // what st needs from the side stream
+    if (side && c->spike_ok && A.sep_rows > 0) {   // the split U sweep's spikes on a stream of their own
+      if (!c->spk_st) RH_CUDA(c, cudaStreamCreateWithFlags(&c->spk_st, cudaStreamNonBlocking));
+      if (!c->ev_spike) RH_CUDA(c, cudaEventCreateWithFlags(&c->ev_spike, cudaEventDisableTiming));
+      RH_CUDA(c, cudaStreamWaitEvent(c->spk_st, c->ev_derived, 0));
+      if (int rc = ensure_spikes(c, c->spk_st)) return rc;
+      RH_CUDA(c, cudaEventRecord(c->ev_spike, c->spk_st));
+    }
     const int rc = early(sb, 1);
     if (rc) return rc;
   }
@@ -4024,6 +4142,7 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   if (early && side && A.sep_rows > 0) RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_ult, 0));   // (done during the inverse)
   if (side && early) {   // the early sweeps are joined batch by batch (hessian_batches)
     RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_derived, 0));
+    if (c->spike_ok && !c->spike_pending) RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_spike, 0));
   } else if (side) {
     RH_CUDA(c, cudaEventRecord(c->ev_sb, side));
     RH_CUDA(c, cudaStreamWaitEvent(st, c->ev_sb, 0));
@@ -4278,6 +4397,7 @@ std::vector<int> host_cuts(int ncols, int N, bool copy_bound) {
 int hessian_batches(rh_ctx *c, int j0, int j1, int N, double *H, long long ldh, int transposed, cudaStream_t st,
                     double *Hhost, int early = 0) {
   const int ncols = j1 - j0;
+  if (int rc = ensure_spikes(c, st)) return rc;   // (before the batches fork to other streams)
   int nb = (ncols + N - 1) / N;
   std::vector<int> cuts;   // batch bounds (host copies only)
   if (Hhost) {
