@@ -63,6 +63,7 @@ struct SegParams {
   // staged separator rows = identity columns) into Msp; k_spike then forms
   // Z_b = Z_b^0 + Msp_b z_ext
   int spike;
+  const int *tlist;                  // Cartesian batch: live tiles (count, then block << 16 | chunk)
   const double *Msp;                 // [n_x][kSpLd] per block row: -(U_bb^-1 U_bs) over the block's staged separator rows
   const int *seg_row_off, *row_global;
   DSeg fwd, bwd;

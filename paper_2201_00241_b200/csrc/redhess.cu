@@ -1042,7 +1042,8 @@ __device__ __forceinline__ bool tile_live(const SegParams &h, int s, int ci) {
 // those of the natural order).
 __global__ void __launch_bounds__(1024) k_batch_plan(int n_p, int lo, int hi, const int *__restrict__ gorder,
                                                      const int *__restrict__ pcb_ptr, const int *__restrict__ pcb,
-                                                     int nblk, int words, int *cols, unsigned *mask) {
+                                                     int nblk, int words, int *cols, unsigned *mask, int nch,
+                                                     int *tlist) {
   __shared__ int wsum[32];
   __shared__ int base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1076,6 +1077,33 @@ __global__ void __launch_bounds__(1024) k_batch_plan(int n_p, int lo, int hi, co
     if (tid == 0) base += wsum[31];
     __syncthreads();
   }
+  // the live tiles as a list (count, then block << 16 | chunk): the sparse L and
+  // U0 sweeps take tickets over these only
+  __threadfence_block();
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < nblk * nch; i0 += blockDim.x) {
+    const int i = i0 + tid, sb = i / max(nch, 1), ci = i - sb * nch;
+    const bool in = i < nblk * nch && ((__ldcg(mask + sb * words + (ci >> 5)) >> (ci & 31)) & 1u);
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      int v = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+      }
+      wsum[lane] = v;
+    }
+    __syncthreads();
+    if (in) tlist[1 + base + (warp ? wsum[warp - 1] : 0) + __popc(bal & ((1u << lane) - 1u))] = sb << 16 | ci;
+    __syncthreads();
+    if (tid == 0) base += wsum[31];
+    __syncthreads();
+  }
+  if (tid == 0) tlist[0] = base;
 }
 
 constexpr int kSegC = 32;   // columns of the single-RHS (lambda) path
@@ -1428,7 +1456,9 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
   // a ticket = one block x up to kblk_group consecutive column chunks: the block's
   // schedule is staged once and reused (it is ~40 % of a tile's L2 -> SM bytes)
   const int cg = max(1, min(h.kblk_group, nch)), ngrp = (nch + cg - 1) / cg;
-  const int ntiles = h.nblk * ngrp;
+  // sparse sweeps of a Cartesian batch (L, U0): tickets over the live tiles only
+  const int *tl = h.tlist && h.tmask && (mode == MODE_L || h.spike == 1) ? h.tlist : nullptr;
+  const int ntiles = tl ? __ldg(tl) : h.nblk * ngrp;
   double *X = reinterpret_cast<double *>(smraw + h.smem_x_off);
   UStage st;
   st.meta = reinterpret_cast<const int4 *>(smraw + h.smem_meta_off);
@@ -1449,7 +1479,9 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
     __syncthreads();
     const int tk = s_tk;
     if (tk >= ntiles) break;
-    const int s = U.blk_order[tk / ngrp], cbeg = (tk % ngrp) * cg, cend = min(nch, cbeg + cg);
+    const int te = tl ? __ldg(tl + 1 + tk) : 0;
+    const int s = tl ? te >> 16 : U.blk_order[tk / ngrp], cbeg = tl ? te & 0xffff : (tk % ngrp) * cg;
+    const int cend = tl ? cbeg + 1 : min(nch, cbeg + cg);
     bool staged = false;
     for (int ci = cbeg; ci < cend; ++ci) {
     // Cartesian batch: an L tile whose right-hand side is zero stays zero (not
@@ -2512,6 +2544,7 @@ struct rh_ctx {
     size_t mp_elems = 0;
     int *pcols = nullptr;        // Cartesian batch plan: the batch's columns, home-block order
     unsigned *pmask = nullptr;   // and its nonzero L-tile mask [nblk][words]
+    int *plist = nullptr;        // and its live tiles: count, then block << 16 | chunk
     int plan_ld = 0;
     int *ctr = nullptr;   // k_blk ticket counters of this workspace
   } ws[kNumWs];
@@ -2644,6 +2677,7 @@ struct rh_ctx {
       if (w.Tsep) cudaFree(w.Tsep);
       if (w.pcols) cudaFree(w.pcols);
       if (w.pmask) cudaFree(w.pmask);
+      if (w.plist) cudaFree(w.plist);
       if (w.Yp) cudaFree(w.Yp);
       if (w.Mp) cudaFree(w.Mp);
       w = Workspace();
@@ -3189,12 +3223,15 @@ int ensure_plan(rh_ctx *c, int ld, int k) {
   c->drop_graph();
   if (w.pcols) cudaFree(w.pcols);
   if (w.pmask) cudaFree(w.pmask);
+  if (w.plist) cudaFree(w.plist);
   w.pcols = nullptr;
   w.pmask = nullptr;
+  w.plist = nullptr;
   w.plan_ld = 0;
   const size_t words = (size_t)(ld / 32 + 31) / 32;
   if (cudaMalloc(&w.pcols, (size_t)ld * sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&w.pmask, (size_t)std::max(1, c->A.nblk) * words * sizeof(unsigned)) != cudaSuccess) {
+      cudaMalloc(&w.pmask, (size_t)std::max(1, c->A.nblk) * words * sizeof(unsigned)) != cudaSuccess ||
+      cudaMalloc(&w.plist, ((size_t)std::max(1, c->A.nblk) * (ld / 32) + 1) * sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     return fail(c, RH_E_NOMEM, "plan allocation failed");
   }
@@ -3438,10 +3475,12 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
     h.icol = c->ws[wsi].pcols;
     h.icol_base = ident_lo;
     h.tmask = c->ws[wsi].pmask;
+    h.tlist = c->ws[wsi].plist;
     h.tmask_words = (ld / 32 + 31) / 32;
     if (phase == 0 || phase == 1) {
       k_batch_plan<<<1, 1024, 0, st>>>(A.n_p, ident_lo, ident_lo + N, c->gorder, c->pcb_ptr, c->pcb, A.nblk,
-                                       h.tmask_words, c->ws[wsi].pcols, c->ws[wsi].pmask);
+                                       h.tmask_words, c->ws[wsi].pcols, c->ws[wsi].pmask, ld / kBC,
+                                       c->ws[wsi].plist);
       RH_LAUNCHED(c);
     }
     if (getenv("RH_NO_MASK")) h.tmask = nullptr;   // experiment: dense L sweep on the same column order
