@@ -539,13 +539,15 @@ def main():
             shards[str(G)] = {"columns": c, "ms": float(np.median(ts)),
                               "projected_hvps_per_s": n_p / (float(np.median(ts)) * 1e-3)}
 
-    # ---- roofline of the dominant kernel: k_blk, the bus-unit block sweeps
-    # (4 of the 8 kernels of an Alg. 2 batch, ~55 % of its time).  Algorithmic
-    # bytes = SURVEY.md 8(d)'s M2 share of the two solve stages, per HVP
+    # ---- roofline of the dominant kernels: the block triangular solves (k_blk,
+    # the bus-unit block sweeps, and on Cartesian batches k_spike, the U sweep's
+    # spike product; ~55 % of an Alg. 2 batch).  Algorithmic bytes = SURVEY.md
+    # 8(d)'s M2 share of the two solve stages, per HVP
     #   [SpMul + L + U]  reads w (n_p), writes z (n_x)
     #   [U^T + L^T]      reads y_x (n_x), writes psi (n_x)
-    # = (3 n_x + n_p) * 8 B, credited in full to the 4 k_blk launches of a
-    # batch (the separator kernels get none): per launch (3 n_x + n_p) 8 N / 4.
+    # = (3 n_x + n_p) * 8 B, credited in full to the 4 block-solve stages of a
+    # batch (L [+ U0], U [k_spike on Cartesian batches], U^T, L^T; the separator
+    # kernels get none): per stage (3 n_x + n_p) 8 N / 4.
     # Per-stage device times: CUDA events the library records around each
     # kernel of a batch, on the stream the kernels run on (rh_set_timing).
     peaks = {}
@@ -615,19 +617,20 @@ def main():
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
         ncu_rec = prof.get(f"{case}:N={N}:cartesian", {})
-        traffic = ncu_rec.get("k_blk_dram_bytes_per_launch")
-        ncu_share = ncu_rec.get("k_blk_time_share")
+        traffic = ncu_rec.get("solve_dram_bytes_per_stage", ncu_rec.get("k_blk_dram_bytes_per_launch"))
+        ncu_share = ncu_rec.get("solve_time_share", ncu_rec.get("k_blk_time_share"))
     except Exception:
         pass
     achieved = rl_cart["achieved"]
     roofline = {
-        "bound": "hbm", "kernel": "k_blk (bus-unit block triangular sweeps, 4 of 8 kernels per Alg. 2 batch)",
+        "bound": "hbm", "kernel": "block triangular solves: k_blk (bus-unit sweeps L, U0, U^T, L^T) + k_spike "
+                                  "(the U sweep's spike product on Cartesian batches)",
         "achieved": achieved, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
         "algorithmic_bytes_per_launch": kblk_bytes,
-        "model": "SURVEY.md 8(d) M2 solve-stage share: (3 n_x + n_p) * 8 B per HVP over the 4 k_blk launches "
-                 "of a batch, / mean k_blk launch time of a Cartesian batch (the full Hessian's first N columns, "
-                 "the batches the timed step runs; CUDA events, L2 flushed)",
+        "model": "SURVEY.md 8(d) M2 solve-stage share: (3 n_x + n_p) * 8 B per HVP over the 4 block-solve "
+                 "stages of a batch (L + U0, U = k_spike, U^T, L^T), / their mean event time in a Cartesian batch "
+                 "(the full Hessian's first N columns, the batches the timed step runs; CUDA events, L2 flushed)",
         "launch_ms": rl_cart["launch_ms"], "stage_ms": rl_cart["stage_ms"], "batch_ms": rl_cart["batch_ms"],
         "k_blk_share_of_batch": rl_cart["k_blk_share_of_batch"], "k_blk_share_of_batch_ncu": ncu_share,
         "traffic_over_algorithmic": (traffic / kblk_bytes) if traffic else None,
@@ -643,7 +646,8 @@ def main():
         "kblk_rw_gbs": rw_gbs, "kblk_rw_frac": (rw_gbs / peak) if rw_gbs else None,
         "kblk_rw_model": "random W: block rows each launch moves: A_L (n_x - n_sep) N 8 + n_p N 8 (W), "
                          "A_U / A_Ut / A_Lt 2 (n_x - n_sep) N 8",
-        "ncu": {k: ncu_rec.get(k) for k in ("round", "batch_us_serialized", "k_blk_dram_over_m2", "stages")}
+        "ncu": {k: ncu_rec.get(k) for k in ("round", "batch_us_serialized", "k_blk_dram_over_m2", "solve_dram_over_m2",
+                                            "solve_kernels", "stages")}
         if ncu_rec else None,
     }
 

@@ -9,7 +9,8 @@ M2 share (bytes per HVP x N):
   [FoR]             (k_for)              reads z, w; writes y_x, y_p  2 (n_x + n_p)
   [U^T + L^T]       (A_Ut, B_UtLt, A_Lt) reads y_x, writes psi        2 n_x
   [SpMulAdd]        (k_muladd)           reads psi, y_p; writes Hw    n_x + 2 n_p
-The k_blk record (mean DRAM bytes per launch, its share of the batch time) is
+The k_blk record (mean DRAM bytes per launch, its share of the batch time) and the
+block-solve record (k_blk + k_spike DRAM bytes per solve stage, 4 per batch) are
 what bench.py reports as roofline.traffic."""
 import csv, io, json, os, subprocess, sys
 
@@ -48,22 +49,22 @@ def main():
     tot_us = sum(k["us"] for k in ks)
     w = 8.0 * N
     m2 = {"SpMul+L+U": (npp + nx) * w, "FoR": 2 * (nx + npp) * w, "UT+LT": 2 * nx * w, "SpMulAdd": (nx + 2 * npp) * w}
-    # stage grouping by launch order: k_blk launches are A_L, A_U, A_Ut, A_Lt
+    # stage grouping by launch order: everything before k_for is SpMul + L + U (on a
+    # Cartesian batch: plan, L, U0, separator gather + product, k_spike), k_for is
+    # FoR, then U^T + L^T until k_muladd
     stages = {"SpMul+L+U": [], "FoR": [], "UT+LT": [], "SpMulAdd": []}
-    nblk = 0
+    seen_for = False
     for k in ks:
         n = k["kernel"]
-        if n == "k_blk":
-            nblk += 1
-            stages["SpMul+L+U" if nblk <= 2 else "UT+LT"].append(k)
-        elif n in ("k_sep_gather", "k_sep_gemm"):
-            stages["SpMul+L+U" if nblk <= 1 else "UT+LT"].append(k)
-        elif n == "k_for":
+        if n == "k_for":
+            seen_for = True
             stages["FoR"].append(k)
         elif n == "k_muladd":
             stages["SpMulAdd"].append(k)
-        elif n == "k_batch_plan":
-            stages["SpMul+L+U"].append(k)
+        else:
+            stages["UT+LT" if seen_for else "SpMul+L+U"].append(k)
+    # the block-solve kernels (k_blk launches and k_spike): 4 solve stages per batch
+    solve = [k for k in ks if k["kernel"] in ("k_blk", "k_spike")]
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     st = {}
@@ -79,10 +80,14 @@ def main():
         "k_blk_dram_bytes_per_launch": sum(k["read"] + k["write"] for k in blk) / max(1, len(blk)),
         "k_blk_time_share": sum(k["us"] for k in blk) / tot_us if tot_us else None,
         "k_blk_m2_bytes_per_launch": (3 * nx + npp) * w / 4.0,
+        "solve_kernels": [k["kernel"] for k in solve],
+        "solve_dram_bytes_per_stage": sum(k["read"] + k["write"] for k in solve) / 4.0,
+        "solve_time_share": sum(k["us"] for k in solve) / tot_us if tot_us else None,
         "stages": st,
         "source": f"ncu --set full --clock-control none --profile-from-start off, tools/prof_hvp.py {case} {N} 3 {kind}",
     }
     rec["k_blk_dram_over_m2"] = rec["k_blk_dram_bytes_per_launch"] / rec["k_blk_m2_bytes_per_launch"]
+    rec["solve_dram_over_m2"] = rec["solve_dram_bytes_per_stage"] / rec["k_blk_m2_bytes_per_launch"]
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     db = json.load(open(path)) if os.path.exists(path) else {}
     db = {k: v for k, v in db.items() if isinstance(v, dict) and "kind" in v}   # drop the r01 format
