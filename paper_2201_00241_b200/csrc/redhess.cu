@@ -1688,41 +1688,80 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
 // Z_b^0 (live tiles) and stored.  Per column the arithmetic does not depend on
 // the batch (bitwise N- and mask-invariant).
 // ----------------------------------------------------------------------------
-constexpr int kSpLd = 64;       // Msp row stride: at most 64 staged separator rows per block
+constexpr int kSpLd = 64;       // Msp row stride (the spike sweep's output): <= 64 staged separator rows
+constexpr int kSpQ = 9;         // k_spike: K <= 4 kSpQ = 36 staged separator rows per block
+constexpr int kSpMt = 32;       // m-tiles (8 rows) per block: blocks of <= 256 rows
 constexpr int kSpThreads = 256;
-__global__ void __launch_bounds__(kSpThreads) k_spike(SegParams h) {
-  __shared__ __align__(16) double zs[kSpLd][36];   // z_ext rows x 32 columns (stride 36: conflict-free B fragments)
+// Msp in DMMA A-fragment order (once per state, after the spike sweep): for block
+// s, m-tile mt and k-step q the 32 values a warp's lanes (gid, tig) hold,
+// Msp[r0 + 8 mt + gid][4 q + tig], contiguous: one coalesced 256 B load each.
+__global__ void k_spike_frag(SegParams h, double *Mf) {
+  const int s = blockIdx.x, mt = blockIdx.y, lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int r0 = h.seg_row_off[s], nr = h.seg_row_off[s + 1] - r0, r = 8 * mt + (lane >> 2);
+  if (q < kSpQ)
+    Mf[(((long long)s * kSpMt + mt) * kSpQ + q) * 32 + lane] =
+        r < nr ? h.Msp[(long long)(r0 + r) * kSpLd + 4 * q + (lane & 3)] : 0.0;
+}
+// z_b = Z_b^0 + Msp_b z_ext for one (block, 32-column) tile: z_ext staged in
+// shared memory, A fragments by coalesced loads, one m-tile per warp at a time.
+__global__ void __launch_bounds__(kSpThreads) k_spike(SegParams h, const double *__restrict__ Mf) {
+  __shared__ __align__(16) double zs[4 * kSpQ][36];   // z_ext rows x 32 columns (stride 36: conflict-free B fragments)
   const int s = blockIdx.x, ci = blockIdx.y, col0 = ci * kBC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const DUnit &U = h.ub;
   const int r0 = h.seg_row_off[s], nr = h.seg_row_off[s + 1] - r0;
   const int x0 = U.ext_off[s], nxr = U.ext_off[s + 1] - x0, K = (nxr + 3) & ~3;
   const bool live = tile_live(h, s, ci);
-  for (int k = warp; k < K; k += kSpThreads / 32)
-    zs[k][lane] = k < nxr ? h.Z[(long long)U.ext_rows[x0 + k] * h.ld + col0 + lane] : 0.0;
+  {  // stage z_ext: every load in flight, then the stores
+    double v[(4 * kSpQ + kSpThreads / 32 - 1) / (kSpThreads / 32)];
+#pragma unroll
+    for (int u = 0; u < (int)(sizeof(v) / sizeof(double)); ++u) {
+      const int k = warp + u * (kSpThreads / 32);
+      v[u] = k < nxr ? h.Z[(long long)U.ext_rows[x0 + k] * h.ld + col0 + lane] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < (int)(sizeof(v) / sizeof(double)); ++u) {
+      const int k = warp + u * (kSpThreads / 32);
+      if (k < 4 * kSpQ) zs[k][lane] = v[u];
+    }
+  }
   __syncthreads();
   const int gid = lane >> 2, tig = lane & 3;
-  for (int mt = warp; mt * 8 < nr; mt += kSpThreads / 32) {
-    const int r = mt * 8 + gid;
-    const bool in = r < nr;
-    double *zr = h.Z + (long long)(r0 + r) * h.ld + col0 + 2 * tig;
-    const double *z0 = h.P + (long long)(r0 + r) * h.ld + col0 + 2 * tig;   // Z^0 (k_blk U0)
-    double c[4][2];
+  const double *mf = Mf + (long long)s * kSpMt * kSpQ * 32 + lane;
+  constexpr int NW = kSpThreads / 32;
+  for (int m0 = warp; m0 * 8 < nr; m0 += 2 * NW) {   // two m-tiles (m0, m0 + NW) per pass: each B fragment feeds both
+    const bool two = (m0 + NW) * 8 < nr;
+    double c[2][4][2];
+    long long ro[2];
+    bool in[2];
 #pragma unroll
-    for (int n = 0; n < 4; ++n) {
-      const double2 v = in && live ? *reinterpret_cast<const double2 *>(z0 + 8 * n) : make_double2(0.0, 0.0);
-      c[n][0] = v.x;
-      c[n][1] = v.y;
+    for (int t = 0; t < 2; ++t) {
+      const int r = (m0 + t * NW) * 8 + gid;
+      in[t] = (t == 0 || two) && r < nr;
+      ro[t] = (long long)(r0 + r) * h.ld + col0 + 2 * tig;
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {   // Z^0 (k_blk U0, in P) of a live tile, else zero
+        const double2 v = in[t] && live ? *reinterpret_cast<const double2 *>(h.P + ro[t] + 8 * n) : make_double2(0.0, 0.0);
+        c[t][n][0] = v.x;
+        c[t][n][1] = v.y;
+      }
     }
-    const double *ar = h.Msp + (long long)(r0 + (in ? r : 0)) * kSpLd + tig;
-    for (int k0 = 0; k0 < K; k0 += 4) {
-      const double a = in ? __ldg(ar + k0) : 0.0;
+    for (int q = 0; 4 * q < K; ++q) {
+      const double a0 = __ldg(mf + (m0 * kSpQ + q) * 32);   // coalesced: the fragment-order spikes
+      const double a1 = two ? __ldg(mf + ((m0 + NW) * kSpQ + q) * 32) : 0.0;
 #pragma unroll
-      for (int n = 0; n < 4; ++n) dmma_8x8x4(c[n][0], c[n][1], a, zs[k0 + tig][8 * n + gid]);
+      for (int n = 0; n < 4; ++n) {
+        const double bq = zs[4 * q + tig][8 * n + gid];
+        dmma_8x8x4(c[0][n][0], c[0][n][1], a0, bq);
+        dmma_8x8x4(c[1][n][0], c[1][n][1], a1, bq);
+      }
     }
-    if (in)
 #pragma unroll
-      for (int n = 0; n < 4; ++n) *reinterpret_cast<double2 *>(zr + 8 * n) = make_double2(c[n][0], c[n][1]);
+    for (int t = 0; t < 2; ++t)
+      if (in[t])
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+          *reinterpret_cast<double2 *>(h.Z + ro[t] + 8 * n) = make_double2(c[t][n][0], c[t][n][1]);
   }
 }
 
@@ -2631,7 +2670,7 @@ struct rh_ctx {
   // side stream of the fused call: block-only derived values done; each early L sweep done
   cudaEvent_t ev_derived = nullptr, ev_early[kNumWs] = {};
   // split U sweep of Cartesian batches (k_spike): per-block spikes, recomputed per state
-  double *Msp = nullptr;
+  double *Msp = nullptr, *Mfrag = nullptr;   // spikes: sweep output [n_x][kSpLd], A-fragment order
   bool spike_ok = false, spike_pending = false;
   cudaEvent_t ev_spike = nullptr;
   cudaStream_t spk_st = nullptr;
@@ -3109,8 +3148,12 @@ int upload(rh_ctx *c) {
   {  // split U sweep (k_spike): every block's staged separator rows fit the spike stride
     int mx = 0;
     for (int s = 0; s < A.nblk; ++s) mx = std::max(mx, A.bwd.ext_off[s + 1] - A.bwd.ext_off[s]);
-    c->spike_ok = A.sep_rows > 0 && A.nblk > 0 && mx <= kSpLd && !getenv("RH_NO_SPIKE");
-    if (c->spike_ok) chk(c->Msp = dalloc<double>((size_t)nx * kSpLd, P));
+    c->spike_ok = A.sep_rows > 0 && A.nblk > 0 && mx <= 4 * kSpQ && A.max_seg_rows <= 8 * kSpMt &&
+                  !getenv("RH_NO_SPIKE");
+    if (c->spike_ok) {
+      chk(c->Msp = dalloc<double>((size_t)nx * kSpLd, P));
+      chk(c->Mfrag = dalloc<double>((size_t)A.nblk * kSpMt * kSpQ * 32, P));
+    }
   }
   if (!ok) return fail(c, RH_E_NOMEM, "device allocation failed while loading the grid");
   // shared-memory footprints
@@ -3449,6 +3492,8 @@ int ensure_spikes(rh_ctx *c, cudaStream_t st) {
   const int g = (int)std::min<long long>(2LL * c->nsm, (long long)c->A.nblk * (kSpLd / kBC));
   k_blk<<<g, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
   RH_LAUNCHED(c);
+  k_spike_frag<<<dim3(c->A.nblk, kSpMt), kSpQ * 32, 0, st>>>(h, c->Mfrag);
+  RH_LAUNCHED(c);
   c->spike_pending = false;
   return RH_OK;
 }
@@ -3545,7 +3590,7 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
   if (phase == 3) return RH_OK;
   mark(2);
   if (split)
-    k_spike<<<dim3(nb, ld / kBC), kSpThreads, 0, st>>>(h);
+    k_spike<<<dim3(nb, ld / kBC), kSpThreads, 0, st>>>(h, c->Mfrag);
   else
     k_blk<<<gA, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
   RH_LAUNCHED(c);
