@@ -63,6 +63,9 @@ struct SegParams {
   // staged separator rows = identity columns) into Msp; k_spike then forms
   // Z_b = Z_b^0 + Msp_b z_ext
   int spike;
+  const int *ma_gptr;                // k_muladd: per group of 4 p rows, its items (static)
+  const int2 *ma_items;              // (target j << 30 | kind << 28 | row, CSC position)
+  int ma_ngrp;
   const int *tlist;                  // Cartesian batch: live tiles (count, then block << 16 | chunk)
   const double *Msp;                 // [n_x][kSpLd] per block row: -(U_bb^-1 U_bs) over the block's staged separator rows
   const int *seg_row_off, *row_global;

@@ -2304,73 +2304,42 @@ __global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
   // rows together), blockIdx.y = p group
   const int cp0 = blockIdx.y * 32, col = blockIdx.x * 32 + lane;
   const int rb = cp0 + 4 * warp;   // this warp's first p row
-  const int *rptr = h.Mp ? h.ma_run_ptr : h.gpc_ptr;   // runs (partials) or all CSC entries
-  int ptr = 0, sptr = 0;
-  double c2x2 = 0.0;
-  int kind = 0;
-  if (lane < 5) {
-    ptr = rptr[min(rb + lane, h.n_p)];
-    if (h.Mp) sptr = h.ma_sep_ptr[min(rb + lane, h.n_p)];
-  }
-  if (lane < 4 && rb + lane < h.n_p) {
-    c2x2 = h.pdiag[rb + lane];
-    kind = h.p_kind[rb + lane];
-  }
-  double acc[4];
+  // the group's items (static, upload): target row j, source (Y_p row, the Pg
+  // diagonal 2 c2 w, an L^T partial row, a Psi row with its G_p value), in the
+  // order each row adds them; one coalesced record load, then up to 8 row loads
+  // in flight (r02: the CSC / run pointer chains were 3-4 dependent round trips)
+  const int g = rb >> 2;
+  const int i0 = g < h.ma_ngrp ? h.ma_gptr[g] : 0, i1 = g < h.ma_ngrp ? h.ma_gptr[g + 1] : 0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int base = i0; base < i1; base += 32) {
+    const int n = min(32, i1 - base);
+    int code = 0;
+    double coef = 1.0;
+    if (lane < n) {
+      const int2 it = h.ma_items[base + lane];
+      code = it.x;
+      const int kind = (code >> 28) & 3;
+      coef = kind == 3 ? h.gpc_val[it.y] : kind == 1 ? h.pdiag[code & 0x0fffffff] : 1.0;
+    }
+    for (int k0 = 0; k0 < n; k0 += 8) {
+      double x[8];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {   // Y_p: a Pg row is the cost diagonal 2 c2 w (from W); a v row was written by k_for
-    const double cj = __shfl_sync(0xffffffffu, c2x2, j);
-    const int kj = __shfl_sync(0xffffffffu, kind, j);
-    const int cp = rb + j;
-    acc[j] = cp < h.n_p ? ((cj != 0.0 || kj == RH_KIND_PG) ? cj * load_W(h, cp, col) : h.Yp[(long long)cp * h.ld + col])
-                        : 0.0;
-  }
-  // pass 0: runs (partials) or all entries; pass 1 (partials only): separator entries
-  for (int pass = 0; pass < (h.Mp ? 2 : 1); ++pass) {
-    const int pv = pass ? sptr : ptr;
-    const int b0 = __shfl_sync(0xffffffffu, pv, 0), b1 = __shfl_sync(0xffffffffu, pv, 1);
-    const int b2 = __shfl_sync(0xffffffffu, pv, 2), b3 = __shfl_sync(0xffffffffu, pv, 3);
-    const int b4 = __shfl_sync(0xffffffffu, pv, 4);
-    const bool partials = h.Mp && !pass;
-    for (int base = b0; base < b4; base += 32) {
-      const int n = min(32, b4 - base);
-      long long er = 0;   // row offset (elements) of each lane's item
-      double ev = 1.0;
-      if (lane < n) {
-        if (partials) {
-          er = (long long)(base + lane) * h.ld;
-        } else {
-          const int q = pass ? h.ma_sep_q[base + lane] : base + lane;
-          er = (long long)h.gpc_row[q] * h.ld;
-          ev = h.gpc_val[q];
-        }
+      for (int k = 0; k < 8; ++k) {
+        const int cd = __shfl_sync(0xffffffffu, code, (k0 + k) & 31);
+        const int kind = (cd >> 28) & 3, row = cd & 0x0fffffff;
+        const double *src = kind == 0 ? h.Yp : kind == 2 ? h.Mp : h.P;
+        x[k] = k0 + k >= n ? 0.0 : kind == 1 ? load_W(h, row, col) : src[(long long)row * h.ld + col];
       }
-      const double *src = partials ? h.Mp : h.P;
-      for (int k0 = 0; k0 < n; k0 += 8) {
-        double x[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const long long ro = __shfl_sync(0xffffffffu, er, (k0 + k) & 31);
-          x[k] = k0 + k < n ? src[ro + col] : 0.0;
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const double v = __shfl_sync(0xffffffffu, ev, (k0 + k) & 31);
-          if (k0 + k >= n) break;
-          const int e = base + k0 + k;   // item -> its p row (warp-uniform)
-          const double t = partials ? x[k] : v * x[k];
-          if (partials) {
-            if (e < b1) acc[0] += t;
-            else if (e < b2) acc[1] += t;
-            else if (e < b3) acc[2] += t;
-            else acc[3] += t;
-          } else {
-            if (e < b1) acc[0] = fma(v, x[k], acc[0]);
-            else if (e < b2) acc[1] = fma(v, x[k], acc[1]);
-            else if (e < b3) acc[2] = fma(v, x[k], acc[2]);
-            else acc[3] = fma(v, x[k], acc[3]);
-          }
-        }
+      for (int k = 0; k < 8; ++k) {
+        const int cd = __shfl_sync(0xffffffffu, code, (k0 + k) & 31);
+        const double v = __shfl_sync(0xffffffffu, coef, (k0 + k) & 31);
+        if (k0 + k >= n) break;
+        const int j = (unsigned)cd >> 30;
+        if (j == 0) acc[0] = fma(v, x[k], acc[0]);
+        else if (j == 1) acc[1] = fma(v, x[k], acc[1]);
+        else if (j == 2) acc[2] = fma(v, x[k], acc[2]);
+        else acc[3] = fma(v, x[k], acc[3]);
       }
     }
   }
@@ -2665,6 +2634,9 @@ struct rh_ctx {
     double2 *rec = nullptr;   // per-block record regions (run slots static, entries per state)
   } dsr, dma;
   int *ma_run_ptr = nullptr, *ma_sep_ptr = nullptr, *ma_sep_q = nullptr;
+  int *ma_gptr = nullptr;        // k_muladd: items of each group of 4 p rows
+  int2 *ma_items = nullptr;
+  int ma_ngrp = 0;
   int *grad_ctr = nullptr;
   cudaEvent_t tape_wait = nullptr;   // set while a fused call enqueues its batches
   // side stream of the fused call: block-only derived values done; each early L sweep done
@@ -2724,6 +2696,9 @@ struct rh_ctx {
     dsr = DRunRecs();   // device arrays were in the pool
     dma = DRunRecs();
     ma_run_ptr = ma_sep_ptr = ma_sep_q = nullptr;
+    ma_gptr = nullptr;
+    ma_items = nullptr;
+    ma_ngrp = 0;
     if (e2e_buf) cudaFree(e2e_buf);
     if (e2e_st) cudaStreamDestroy(e2e_st);
     for (int k = 0; k < kNumWs; ++k) {
@@ -2922,6 +2897,34 @@ int upload(rh_ctx *c) {
       chk(c->ma_run_ptr = dalloc_copy(A.ma_run_ptr, P));
       chk(c->ma_sep_ptr = dalloc_copy(A.ma_sep_ptr, P));
       chk(c->ma_sep_q = dalloc_copy(sq, P));
+      // k_muladd items per group of 4 p rows: (target j << 30 | kind << 28 | row, CSC position);
+      // kind 0 Y_p row, 1 Pg diagonal (2 c2 w), 2 L^T partial row (run), 3 Psi row x G_p value
+      const std::vector<int32_t> zgr = zr(A.gpc_row);
+      const bool part = A.ma.nruns > 0;
+      std::vector<int32_t> items, gptr(1, 0);
+      const int ng = (A.n_p + 3) / 4;
+      for (int gi = 0; gi < ng; ++gi) {
+        for (int j = 0; j < 4 && 4 * gi + j < A.n_p; ++j) {
+          const int cp = 4 * gi + j;
+          auto push = [&](int kind, int row, int q) {
+            items.push_back((int32_t)((unsigned)j << 30 | (unsigned)kind << 28 | (unsigned)row));
+            items.push_back(q);
+          };
+          push(A.p_kind[cp] == RH_KIND_PG ? 1 : 0, cp, 0);
+          if (part) {
+            for (int r = A.ma_run_ptr[cp]; r < A.ma_run_ptr[cp + 1]; ++r) push(2, r, 0);
+            for (int e = A.ma_sep_ptr[cp]; e < A.ma_sep_ptr[cp + 1]; ++e) push(3, zgr[A.ma_sep_q[e]], A.ma_sep_q[e]);
+          } else {
+            for (int q = A.gpc_ptr[cp]; q < A.gpc_ptr[cp + 1]; ++q) push(3, zgr[q], q);
+          }
+        }
+        gptr.push_back((int)items.size() / 2);
+      }
+      if (items.empty()) items.assign(2, 0);
+      c->ma_ngrp = ng;
+      chk(c->ma_gptr = dalloc_copy(gptr, P));
+      c->ma_items = reinterpret_cast<int2 *>(dalloc_copy(items, P));
+      chk(c->ma_items);
     }
     if (gb.empty()) gb.push_back(0), ge.push_back(0);
     int *g1, *g2, *g3;
@@ -3383,6 +3386,9 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.ma_run_ptr = c->ma_run_ptr;
   h.ma_sep_ptr = c->ma_sep_ptr;
   h.ma_sep_q = c->ma_sep_q;
+  h.ma_gptr = c->ma_gptr;
+  h.ma_items = c->ma_items;
+  h.ma_ngrp = c->ma_ngrp;
   h.blk_gp_ptr = c->blk_gp_ptr;
   h.blk_gp_loc = c->blk_gp_loc;
   if (const char *env = getenv("RH_DEBUG")) h.debug = atoi(env);  // timing experiments only
