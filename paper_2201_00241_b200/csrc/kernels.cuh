@@ -45,6 +45,7 @@ struct SegParams {
   int n_x, n_p, n_bus, N, ld;
   int nblk;                          // segment nblk = separator
   DUnit uf, ub;                      // bus-unit block sweeps: fwd (L, U^T), bwd (U, L^T)
+  DUnit ubp;                         // bwd pruned to the rows G_p^T Psi needs (L^T of Cartesian batches)
   const double2 *uL, *uUt, *uU, *uLt;  // their record values (per state)
   const double *tL, *tUt, *tU, *tLt;   // [nblk][32][36] dense tops inverses per sweep (k_tops_inverse)
   const int *gpe_off, *gpe_split;      // L sweep: per block G_p entry records and 8 warp ranges

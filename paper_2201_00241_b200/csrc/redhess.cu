@@ -1446,7 +1446,8 @@ __global__ void __launch_bounds__(kBlkThreads, 2) k_blk(SegParams h, int mode) {
   __shared__ int s_tk;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool fwd = mode == MODE_L || mode == MODE_UT || mode == MODE_LX;
-  const DUnit &U = fwd ? h.uf : h.ub;
+  // L^T sweep of a Cartesian batch: the schedule pruned to the Psi rows G_p^T Psi reads
+  const DUnit &U = fwd ? h.uf : mode == MODE_LT && h.icol ? h.ubp : h.ub;
   const bool lsw = mode == MODE_L || mode == MODE_LX;   // L values
   const double2 *vals = lsw ? h.uL : mode == MODE_U ? h.uU : mode == MODE_UT ? h.uUt : h.uLt;
   const bool dinv = mode == MODE_U || mode == MODE_UT;
@@ -2565,7 +2566,7 @@ struct rh_ctx {
   int *fact_seg_lvl, *fact_lvl_ptr, *fact_order;
   int *top_ptr, *top_fpos_ptr, *top_fpos, *top_fwd_base, *top_bwd_base;
   // bus-unit block sweeps
-  DUnit duf{}, dub{};
+  DUnit duf{}, dub{}, dubp{};   // dubp: dub pruned for the L^T sweep of Cartesian batches
   double2 *uL = nullptr, *uUt = nullptr, *uU = nullptr, *uLt = nullptr;
   int nrec_f = 0, nrec_b = 0;
   int *uf_src_a, *uf_src_b, *ub_src_a, *ub_src_b;
@@ -3073,6 +3074,42 @@ int upload(rh_ctx *c) {
   }
   mkunit(c->duf, A.ufwd, c->dfwd);
   mkunit(c->dub, A.ubwd, c->dbwd);
+  {  // L^T sweep of Cartesian batches (the full Hessian): only Psi rows in the support
+     // of G_p and the rows they depend on are ever read (HW = Y_p + G_p^T Psi); the
+     // closure runs upward through the L pattern (psi_i needs psi_j for L[j][i] != 0),
+     // the other units are dropped from the bwd schedule (dubp; needed rows bitwise
+     // unchanged, the dropped rows are never read)
+    std::vector<char> need(A.n_x, 0);
+    for (int q = 0; q < A.n_x; ++q) {
+      bool n = A.gp_rptr[q + 1] > A.gp_rptr[q];
+      for (int e = A.F_rowptr[q]; e < A.F_diag[q] && !n; ++e) n = need[A.F_col[e]] != 0;
+      need[q] = n;
+    }
+    const UnitSweep &U = A.ubwd;
+    std::vector<int32_t> meta, uoff(1, 0), lvl(U.lvl);
+    for (int sb = 0; sb < A.nblk; ++sb) {
+      const int ub = U.unit_off[sb], nu = U.unit_off[sb + 1] - ub, r0 = A.seg_row_off[sb];
+      const int *lv = U.lvl.data() + (size_t)sb * UnitSweep::kLvl;
+      std::vector<int> keep_before(nu + 1, 0);
+      for (int u = 0; u < nu; ++u) {
+        const int *m = U.meta.data() + 4 * (size_t)(ub + u);
+        const bool tops = u >= lv[UnitSweep::kWarps + 1] && u < lv[UnitSweep::kWarps + 2];
+        const bool two = (m[3] >> 30) & 1;
+        const bool k = tops || need[A.row_global[r0 + m[0] / kRowB]] || (two && need[A.row_global[r0 + m[1] / kRowB]]);
+        keep_before[u + 1] = keep_before[u] + (k ? 1 : 0);
+        if (k) meta.insert(meta.end(), m, m + 4);
+      }
+      uoff.push_back(uoff.back() + keep_before[nu]);
+      for (int w = 0; w <= UnitSweep::kWarps + 2; ++w) lvl[(size_t)sb * UnitSweep::kLvl + w] = keep_before[lv[w]];
+    }
+    if (meta.empty()) meta.assign(4, 0);
+    c->dubp = c->dub;
+    c->dubp.meta = reinterpret_cast<const int4 *>(dalloc_copy(meta, P));
+    chk(c->dubp.meta);
+    chk(c->dubp.unit_off = dalloc_copy(uoff, P));
+    chk(c->dubp.lvl = dalloc_copy(lvl, P));
+    if (getenv("RH_NO_LT_PRUNE")) c->dubp = c->dub;
+  }
   c->nrec_f = (int)A.ufwd.src_a.size() / 2;
   c->nrec_b = (int)A.ubwd.src_a.size() / 2;
   chk(c->uf_src_a = dalloc_copy(A.ufwd.src_a, P));
@@ -3400,6 +3437,7 @@ SegParams make_params(rh_ctx *c, int k = 0) {
   h.SinvT = c->SinvT;
   h.uf = c->duf;
   h.ub = c->dub;
+  h.ubp = c->dubp;
   h.uL = c->uL;
   h.uUt = c->uUt;
   h.uU = c->uU;
