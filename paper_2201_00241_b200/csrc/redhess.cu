@@ -3188,8 +3188,10 @@ int upload(rh_ctx *c) {
   {  // split U sweep (k_spike): every block's staged separator rows fit the spike stride
     int mx = 0;
     for (int s = 0; s < A.nblk; ++s) mx = std::max(mx, A.bwd.ext_off[s + 1] - A.bwd.ext_off[s]);
+    // (small grids are launch-latency-bound: the split adds three launches per state and
+    // batch and measured slower on case1354 (0.28 -> 0.31 ms), neutral on case2869)
     c->spike_ok = A.sep_rows > 0 && A.nblk > 0 && mx <= 4 * kSpQ && A.max_seg_rows <= 8 * kSpMt &&
-                  !getenv("RH_NO_SPIKE");
+                  (A.n_x >= 8192 || getenv("RH_SPIKE")) && !getenv("RH_NO_SPIKE");
     if (c->spike_ok) {
       chk(c->Msp = dalloc<double>((size_t)nx * kSpLd, P));
       chk(c->Mfrag = dalloc<double>((size_t)A.nblk * kSpMt * kSpQ * 32, P));

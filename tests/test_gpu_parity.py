@@ -136,6 +136,41 @@ def test_cartesian_separator_paths(solved_case, monkeypatch):
     assert np.array_equal(_np(ctx.full_hessian(N)), H)
 
 
+def test_split_u_sweep_forced(solved_case, monkeypatch):
+    """The split U sweep of Cartesian batches (Z^0 swept
+    without the separator, spikes per block, k_spike's DMMA product) and the pruned
+    L^T sweep, forced on the small configs (RH_SPIKE=1; by default only grids with
+    n_x >= 8192 take it): the oracle's Hessian at the parity bar, the unsplit path
+    within rounding, bitwise N invariance, mask on/off bitwise (both with the dense
+    separator product), and the fused call bitwise equal to the separate calls."""
+    name, g, L, x, p, grad, lam, ops = solved_case
+    N = {"case9": 5, "case118": 64, "case1354pegase": 256, "case2869pegase": 512}[name]
+    ctx0, *_ = setup(g)
+    ctx0.reduced_gradient()
+    H0 = _np(ctx0.full_hessian(N))              # default path (unsplit on these grids)
+    monkeypatch.setenv("RH_SPIKE", "1")
+    ctx, *_ = setup(g)                          # the split is chosen when the grid is loaded
+    ctx.reduced_gradient()
+    H = _np(ctx.full_hessian(N))
+    Ho = red.full_hessian(ops, N)
+    check_hessian(H, Ho, f"{name} N={N} (split U sweep)", ops, N, red.full_hessian)
+    assert col_rel_err(H, H0) <= 1e-11        # the same solve, two summation orders
+    for N2 in (7, L.n_p):
+        assert np.array_equal(_np(ctx.full_hessian(N2)), H), N2
+    monkeypatch.setenv("RH_NO_SPMM", "1")       # the dense separator product, as without the mask
+    Hg = _np(ctx.full_hessian(N))
+    monkeypatch.setenv("RH_NO_MASK", "1")       # every tile live: Z^0 swept everywhere
+    assert np.array_equal(_np(ctx.full_hessian(N)), Hg)
+    monkeypatch.delenv("RH_NO_MASK")
+    monkeypatch.delenv("RH_NO_SPMM")
+    xd, pd = _dev(x), _dev(p)
+    gf = torch.empty(L.n_p, dtype=torch.float64, device="cuda")
+    Hf = torch.empty((L.n_p, L.n_p), dtype=torch.float64, device="cuda")
+    for _ in range(3):                          # uncaptured, captured, replayed
+        ctx.reduced_hessian(xd, pd, N, grad=gf, H=Hf)
+        assert np.array_equal(_np(Hf), H)
+
+
 def test_set_multipliers_any_lambda(solved_case):
     name, g, L, x, p, *_ = solved_case
     if name not in ("case9", "case118"):
