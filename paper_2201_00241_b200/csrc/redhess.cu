@@ -2555,6 +2555,7 @@ struct rh_ctx {
     unsigned *pmask = nullptr;   // and its nonzero L-tile mask [nblk][words]
     int *plist = nullptr;        // and its live tiles: count, then block << 16 | chunk
     int plan_ld = 0;
+    int plan_lo = -1, plan_hi = -1;   // the Cartesian batch the plan buffers hold (static per range: reused)
     int *ctr = nullptr;   // k_blk ticket counters of this workspace
   } ws[kNumWs];
   cudaStream_t sti[kNumWs] = {};                        // internal streams of workspaces 1..
@@ -3117,7 +3118,7 @@ int upload(rh_ctx *c) {
   chk(c->ub_src_a = dalloc_copy(A.ubwd.src_a, P));
   chk(c->ub_src_b = dalloc_copy(A.ubwd.src_b, P));
   for (double **t : {&c->tL, &c->tUt, &c->tU, &c->tLt}) chk(*t = dalloc<double>((size_t)A.nblk * 32 * kTopLd, P));
-  chk(c->blk_ctr = dalloc<int>(16 * kNumWs, P));
+  chk(c->blk_ctr = dalloc<int>(16 * (kNumWs + 1), P));   // + the spike sweep's own tickets
   for (int k = 0; k < kNumWs; ++k) c->ws[k].ctr = c->blk_ctr + 16 * k;
   chk(c->gpe_off = dalloc_copy(A.gpe_off, P));
   chk(c->gpe_row = dalloc_copy(A.gpe_row, P));
@@ -3217,7 +3218,7 @@ int upload(rh_ctx *c) {
   }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device);
   cudaError_t e = cudaMemset(c->X1col, 0, (size_t)nx * kSegC * sizeof(double));
-  if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 16 * kNumWs * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(c->blk_ctr, 0, 16 * (kNumWs + 1) * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(c->grid_bar, 0, 2 * sizeof(unsigned));
   {  // R_B1 stages each separator row in shared memory (k_fact_sep_rows)
     int ml = 1;
@@ -3321,6 +3322,7 @@ int ensure_plan(rh_ctx *c, int ld, int k) {
     return fail(c, RH_E_NOMEM, "plan allocation failed");
   }
   w.plan_ld = ld;
+  w.plan_lo = w.plan_hi = -1;
   return RH_OK;
 }
 
@@ -3535,6 +3537,9 @@ int ensure_spikes(rh_ctx *c, cudaStream_t st) {
   h.tmZ = tmap_pair(c, c->Msp, kSpLd);
   h.tmP = nullptr;
   h.spike = 2;
+  // its own ticket counters: in the fused call it runs on its own stream, concurrently
+  // with the early batches' L and Z^0 sweeps (which use the workspaces' counters)
+  h.blk_ctr = c->blk_ctr + 16 * kNumWs;
   const int g = (int)std::min<long long>(2LL * c->nsm, (long long)c->A.nblk * (kSpLd / kBC));
   k_blk<<<g, kBlkThreads, c->smem_blk, st>>>(h, MODE_U);
   RH_LAUNCHED(c);
@@ -3568,7 +3573,17 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
     h.tmask = c->ws[wsi].pmask;
     h.tlist = c->ws[wsi].plist;
     h.tmask_words = (ld / 32 + 31) / 32;
-    if (phase == 0 || phase == 1) {
+    auto &wp = c->ws[wsi];
+    if ((phase == 0 || phase == 1) && !(wp.plan_lo == ident_lo && wp.plan_hi == ident_lo + N)) {
+      // the plan of a column range is static (gorder and the G_p blocks): built once per
+      // (workspace, range) and reused by later calls and graph replays of the same range
+      // (a captured graph that skipped the plan relies on these buffers: rebuilding them
+      // outside a capture drops the graphs)
+      cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cst);
+      if (cst == cudaStreamCaptureStatusNone && wp.plan_lo >= 0) c->drop_graph();
+      wp.plan_lo = ident_lo;
+      wp.plan_hi = ident_lo + N;
       k_batch_plan<<<1, 1024, 0, st>>>(A.n_p, ident_lo, ident_lo + N, c->gorder, c->pcb_ptr, c->pcb, A.nblk,
                                        h.tmask_words, c->ws[wsi].pcols, c->ws[wsi].pmask, ld / kBC,
                                        c->ws[wsi].plist);

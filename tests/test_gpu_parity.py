@@ -171,6 +171,28 @@ def test_split_u_sweep_forced(solved_case, monkeypatch):
         assert np.array_equal(_np(Hf), H)
 
 
+def test_plan_cache_other_ranges(solved_case):
+    """Cartesian batch plans are cached per (workspace, column range) and skipped by
+    later calls and graph replays of the same range: a call on other ranges in
+    between (rebuilding the plans) must not leave a replayed graph with stale plans."""
+    name, g, L, x, p, *_ = solved_case
+    N = {"case9": 5, "case118": 64, "case1354pegase": 256, "case2869pegase": 512}[name]
+    ctx, *_ = setup(g)
+    ctx.reduced_gradient()
+    H = _np(ctx.full_hessian(N))
+    xd, pd = _dev(x), _dev(p)
+    gf = torch.empty(L.n_p, dtype=torch.float64, device="cuda")
+    Hf = torch.empty((L.n_p, L.n_p), dtype=torch.float64, device="cuda")
+    for _ in range(3):                           # uncaptured, captured, replayed
+        ctx.reduced_hessian(xd, pd, N, grad=gf, H=Hf)
+        assert np.array_equal(_np(Hf), H)
+    j0, j1 = L.n_p // 5, L.n_p // 5 + min(37, L.n_p - L.n_p // 5)
+    assert np.array_equal(_np(ctx.hessian_columns(j0, j1, max(1, N // 3))), H[:, j0:j1])
+    for _ in range(3):
+        ctx.reduced_hessian(xd, pd, N, grad=gf, H=Hf)
+        assert np.array_equal(_np(Hf), H)
+
+
 def test_set_multipliers_any_lambda(solved_case):
     name, g, L, x, p, *_ = solved_case
     if name not in ("case9", "case118"):
