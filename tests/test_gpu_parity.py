@@ -233,6 +233,28 @@ def test_lossless_closed_form_gpu(name):
     assert np.max(np.abs(H - Hc)) <= 1e-9 * np.max(np.abs(Hc))
 
 
+def test_case9241_repeated_fused_calls():
+    """Uncaptured fused calls back to back (each with its own output buffers, so no
+    graph): the per-state spike sweep on its own stream, the early L / Z^0 sweeps on the
+    side stream and the cached batch plans must give bitwise the same Hessian every
+    time (r02: a ticket counter shared by the spike sweep and workspace 0's Z^0 sweep
+    raced once the cached plans removed the plan kernel's latency)."""
+    g = pf.backout_loads(gridgen.make_grid("case9241pegase"))
+    ctx = rh.RedHess(0)
+    ctx.load_grid(g)
+    x, p = ctx.state_vectors(g)
+    xd, pd = _dev(x), _dev(p)
+    outs = []
+    for _ in range(4):
+        gf, Hf = ctx.reduced_hessian(xd, pd, 1024)
+        outs.append((_np(gf), _np(Hf)))
+    for gf, Hf in outs[1:]:
+        assert np.array_equal(Hf, outs[0][1]) and np.array_equal(gf, outs[0][0])
+    ctx.set_state(xd, pd)
+    ctx.reduced_gradient()
+    assert np.array_equal(_np(ctx.full_hessian(1024)), outs[0][1])
+
+
 def test_case9241_sampled_columns_vs_oracle():
     """Full size of the north-star config, in the launch configuration the bench
     uses (N = 1024): sampled columns checked against the oracle one by one."""
