@@ -3574,16 +3574,15 @@ int hvp_impl(rh_ctx *c, const double *W, long long ldw, int ident_lo, double *HW
     h.tlist = c->ws[wsi].plist;
     h.tmask_words = (ld / 32 + 31) / 32;
     auto &wp = c->ws[wsi];
-    if ((phase == 0 || phase == 1) && !(wp.plan_lo == ident_lo && wp.plan_hi == ident_lo + N)) {
-      // the plan of a column range is static (gorder and the G_p blocks): built once per
-      // (workspace, range) and reused by later calls and graph replays of the same range
-      // (a captured graph that skipped the plan relies on these buffers: rebuilding them
-      // outside a capture drops the graphs)
-      cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
-      cudaStreamIsCapturing(st, &cst);
-      if (cst == cudaStreamCaptureStatusNone && wp.plan_lo >= 0) c->drop_graph();
-      wp.plan_lo = ident_lo;
-      wp.plan_hi = ident_lo + N;
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cst);
+    const bool capturing = cst != cudaStreamCaptureStatusNone;
+    if ((phase == 0 || phase == 1) && (capturing || !(wp.plan_lo == ident_lo && wp.plan_hi == ident_lo + N))) {
+      // the plan of a column range is static (gorder and the G_p blocks): an eager call
+      // reuses the workspace's plan of the same range; a captured graph always carries
+      // its own plans (graph launches invalidate the cache: graph_run)
+      wp.plan_lo = capturing ? -1 : ident_lo;
+      wp.plan_hi = capturing ? -1 : ident_lo + N;
       k_batch_plan<<<1, 1024, 0, st>>>(A.n_p, ident_lo, ident_lo + N, c->gorder, c->pcb_ptr, c->pcb, A.nblk,
                                        h.tmask_words, c->ws[wsi].pcols, c->ws[wsi].pmask, ld / kBC,
                                        c->ws[wsi].plist);
@@ -3991,6 +3990,7 @@ bool graph_run(rh_ctx *c, int slot, const rh_ctx::GraphKey &key, cudaStream_t st
     rc = check_pivots(c, cs);
     return true;
   };
+  for (auto &w : c->ws) w.plan_lo = w.plan_hi = -1;   // graphs rebuild their batches' plans
   if (replay) {
     if (!cuda(cudaGraphLaunch(g.exec, cs))) return true;
     c->launches += g.launches;
