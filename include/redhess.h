@@ -286,6 +286,16 @@ int rh_compressed_jacobian(rh_ctx *ctx, double *JS, void *stream);
  * (bench accounting of "gpu_launches"). */
 int64_t rh_launch_count(const rh_ctx *ctx);
 
+/* Smallest static-pivot ratio |u_kk| / max_j |J_kj| (J's row k before
+ * elimination) over every pivot of the most recent refactorization (block
+ * rows, their tops, and the separator's Gauss-Jordan pivots; R15).
+ * The factorization uses static diagonal pivots and reports RH_E_SINGULAR only
+ * below 1e-14; ratios far below ~1e-8 flag an operating point where static
+ * pivoting loses digits (the caller may then re-solve in the oracle or move
+ * the state).  Host double *min_ratio.  One device read (synchronous).
+ * Errors: RH_E_ORDER before a state, RH_E_NODEV on a host-only context. */
+int rh_pivot_ratio(const rh_ctx *ctx, double *min_ratio);
+
 /* Device-time breakdown of the most recent HVP batch when stage timing is
  * enabled (rh_set_timing(ctx, 1); adds one host sync per batch): ms_out[9]
  * receives the eight kernels of one Alg. 2 batch {blocks L (+SpMul),

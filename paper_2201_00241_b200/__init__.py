@@ -32,7 +32,7 @@ EXPORTS = ["rh_create", "rh_destroy", "rh_last_error", "rh_load_grid", "rh_get_i
            "rh_hvp", "rh_hvp_stages", "rh_hessian_columns", "rh_full_hessian", "rh_reduced_hessian",
            "rh_reduced_hessian_host", "rh_set_loads", "rh_dense_spd_solve", "rh_tracking_step",
            "rh_set_jacobian_mode", "rh_coloring", "rh_compressed_jacobian",
-           "rh_launch_count", "rh_set_timing", "rh_stage_times"]
+           "rh_launch_count", "rh_set_timing", "rh_stage_times", "rh_pivot_ratio"]
 
 
 class RHError(RuntimeError):
@@ -95,6 +95,7 @@ def _load():
         "rh_launch_count": ([vp], i64),
         "rh_set_timing": ([vp, ctypes.c_int], ctypes.c_int),
         "rh_stage_times": ([vp, vp], ctypes.c_int),
+        "rh_pivot_ratio": ([vp, vp], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -464,6 +465,12 @@ class RedHess:
 
     def set_timing(self, enable=True):
         self._rc(lib().rh_set_timing(self._h, int(bool(enable))))
+
+    def pivot_ratio(self):
+        """rh_pivot_ratio: smallest |u_kk| / max|J row k| of the last refactorization (R15)."""
+        out = np.zeros(1, np.float64)
+        self._rc(lib().rh_pivot_ratio(self._h, _ptr(out)))
+        return float(out[0])
 
     def stage_times(self):
         out = np.zeros(9, np.float32)

@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
       sdinv[a] = di;
       f.dinv[rd.y] = di;
       if (!(fabs(piv) > f.pivtol * amax)) atomicMax(f.status, rd.y + 1);
+      f.rowmax[rd.y] = amax;   // (rh_pivot_ratio: |u_kk| = 1 / |dinv| against it)
     }
     __syncwarp();
   };
@@ -508,6 +509,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
         sdinv[ak] = dk;
         f.dinv[ik] = dk;
         if (!(fabs(piv) > f.pivtol * s_amax[tk])) atomicMax(f.status, ik + 1);
+        f.rowmax[ik] = s_amax[tk];
       }
       for (int t = tk + 1 + ((warp - (tk + 1) % nw + nw) % nw); t < ntq; t += nw) {
         // t == tk + 1 + warp (mod nw): rows i > k spread over the warps
@@ -624,7 +626,8 @@ constexpr int GJT = 64;   // output tile
 constexpr size_t gj_smem_bytes() { return sizeof(double) * (GJB * (GJB + 1) + (3 * GJB + GJT) * (GJT + 1)); }
 __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, int ns, const double *rowmax,
                                                      const int *sep_rows, int *status, double pivtol,
-                                                     unsigned *bar, long long *dbg, double *dbuf, int gj_warps) {
+                                                     unsigned *bar, long long *dbg, double *dbuf, int gj_warps,
+                                                     double *seppiv) {
   extern __shared__ double gj_sm[];   // dynamic: gj_smem_bytes()
   double(*Ds)[GJB + 1] = reinterpret_cast<double(*)[GJB + 1]>(gj_sm);
   double(*Cs)[GJT + 1] = reinterpret_cast<double(*)[GJT + 1]>(gj_sm + GJB * (GJB + 1));   // C^T: Cs[m][r] = S[i0 + r][K + m]
@@ -701,6 +704,7 @@ __global__ void __launch_bounds__(256, 1) k_sep_inverse(double *Sa, double *Sb, 
       const double inv = fast_rcp(pk);
       const double rk = j == k ? inv : prow[k & 1][j] * inv;
       if (warp == wk && j == k && k < bb && !(fabs(pk) > pivtol * rowmax[sep_rows[K0 + k]])) bad = true;
+      if (report && warp == wk && j == k && k < bb) seppiv[K0 + k] = pk;   // (rh_pivot_ratio)
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         const int i = RPT * warp + r;
@@ -2529,7 +2533,8 @@ struct rh_ctx {
   unsigned short *tgt16;
   int *sb_src, *sb_dense;
   double *Sbuf = nullptr;   // ping-pong partner of Sinv in k_sep_inverse
-  double *gj_dbuf = nullptr;   // [2][32][32] next panel's diagonal inverse (lookahead CTA)
+  double *gj_dbuf = nullptr;
+  double *sep_piv = nullptr;   // the separator's Gauss-Jordan pivots (rh_pivot_ratio)   // [2][32][32] next panel's diagonal inverse (lookahead CTA)
   double *nwt = nullptr;       // Newton: max|dx|, max|g| (device scalars)
   unsigned *grid_bar = nullptr;
   int coop_blocks = 1;
@@ -3185,6 +3190,7 @@ int upload(rh_ctx *c) {
   chk(c->Sbuf = dalloc<double>(std::max<size_t>(ns2, 1), P));
   chk(c->grid_bar = dalloc<unsigned>(2, P));
   chk(c->gj_dbuf = dalloc<double>(2 * 32 * 32, P));
+  chk(c->sep_piv = dalloc<double>(std::max(1, A.sep_rows), P));
   chk(c->nwt = dalloc<double>(4, P));
   {  // split U sweep (k_spike): every block's staged separator rows fit the spike stride
     int mx = 0;
@@ -4256,7 +4262,8 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     double *dbuf = c->gj_dbuf;
     int gj_warps = 8;
     if (const char *env = getenv("RH_GJW")) gj_warps = atoi(env);   // experiment
-    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar, &gdbg, &dbuf, &gj_warps};
+    double *seppiv = c->sep_piv;
+    void *args[] = {&Sa, &Sb, &nsv, &rowmax, &sep_rows, &status, &pivtol, &bar, &gdbg, &dbuf, &gj_warps, &seppiv};
     const int ntl = ((ns + GJT - 1) / GJT) * ((ns + GJT - 1) / GJT);
     const int grid = std::max(1, std::min(ntl, c->coop_blocks - 1)) + 1;   // tile CTAs + the lookahead CTA
     RH_CUDA(c, cudaMemsetAsync(c->grid_bar, 0, 2 * sizeof(unsigned), st));   // tiles' arrivals, D^-1 flag
@@ -4919,6 +4926,29 @@ int rh_compressed_jacobian(rh_ctx *c, double *JS, void *stream) {
 int rh_set_timing(rh_ctx *c, int enable) {
   if (!c) return RH_E_ARG;
   c->timing = enable != 0;
+  return RH_OK;
+}
+
+int rh_pivot_ratio(const rh_ctx *c, double *min_ratio) {
+  if (!c || !min_ratio) return RH_E_ARG;
+  if (c->host_only) return RH_E_NODEV;
+  if (!c->has_state) return RH_E_ORDER;
+  const Analysis &A = c->A;
+  const int nx = A.n_x, ns = A.sep_rows;
+  std::vector<double> dinv(nx), rmax(nx), sp(std::max(1, ns));
+  if (cudaSetDevice(c->device) != cudaSuccess ||
+      cudaMemcpy(dinv.data(), c->dinv_rows, nx * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(rmax.data(), c->rowmax, nx * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess ||
+      cudaMemcpy(sp.data(), c->sep_piv, sp.size() * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return RH_E_CUDA;
+  double r = INFINITY;
+  for (int q = 0; q < nx; ++q) {   // segment position -> permuted row
+    const int i = A.row_global[q];
+    const bool sep = q >= A.seg_row_off[A.nblk];
+    const double piv = sep ? std::fabs(sp[q - A.seg_row_off[A.nblk]]) : 1.0 / std::fabs(dinv[i]);
+    if (rmax[i] > 0.0) r = std::min(r, piv / rmax[i]);
+  }
+  *min_ratio = r;
   return RH_OK;
 }
 

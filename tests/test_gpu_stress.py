@@ -55,8 +55,9 @@ def test_ill_conditioned_state(name, N):
     H = Hd.cpu().numpy()
     err = col_rel_err(H, Ho)
     gerr = float(np.max(np.abs(gd.cpu().numpy() - grad)) / np.max(np.abs(grad)))
+    ratio = ctx.pivot_ratio()                                  # the static pivots' margin (R15)
     rec = {"label": f"stress {name} N={N}", "col_maxnorm": err, "oracle_floor_col": floor,
-           "max_abs_H": float(np.max(np.abs(Ho))), "grad_rel": gerr}
+           "max_abs_H": float(np.max(np.abs(Ho))), "grad_rel": gerr, "pivot_ratio": ratio}
     print("\nparity", json.dumps(rec))
     log = os.environ.get("RH_PARITY_LOG")
     if log:
@@ -64,3 +65,35 @@ def test_ill_conditioned_state(name, N):
             fh.write(json.dumps(rec) + "\n")
     assert gerr <= 1e-9, rec
     assert err <= max(1e-9, 10.0 * floor), rec
+    assert 1e-14 < ratio <= 1.0, rec
+
+
+def test_pivot_ratio_solved_vs_stressed():
+    """rh_pivot_ratio: the smallest static-pivot margin |u_kk| / max|J row k| of the
+    last refactorization equals the smallest |u_kk| / row max of the oracle's
+    static-pivot LU of the same permuted J (within rounding), and is reset by
+    every state."""
+    import scipy.sparse as sp
+    for stressed in (False, True):
+        g = stressed_grid("case118") if stressed else pf.backout_loads(gridgen.make_grid("case118"))
+        ctx = rh.RedHess(0)
+        ctx.load_grid(g)
+        xs, ps = ctx.state_vectors(g)
+        ctx.set_state(torch.from_numpy(xs).cuda(), torch.from_numpy(ps).cuda())
+        r = ctx.pivot_ratio()
+        # reference: dense Doolittle without pivoting on the library's permuted J
+        L = pf.Layout(g)
+        x, p = pf.state_vectors(g, L)
+        J, _ = pf.jacobians(g, x, p, L)
+        perm = ctx.symbolic()["perm"]
+        A = J.toarray()[np.ix_(perm, perm)]
+        rowmax = np.max(np.abs(A), axis=1)
+        U = A.copy()
+        n = U.shape[0]
+        piv = np.empty(n)
+        for k in range(n):
+            piv[k] = U[k, k]
+            U[k + 1:, k:] -= np.outer(U[k + 1:, k] / U[k, k], U[k, k:])
+        ref = float(np.min(np.abs(piv) / rowmax))
+        assert abs(r - ref) <= 1e-6 * ref, (stressed, r, ref)
+
