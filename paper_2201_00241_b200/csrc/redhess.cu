@@ -2315,7 +2315,12 @@ __global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
   // in flight (r02: the CSC / run pointer chains were 3-4 dependent round trips)
   const int g = rb >> 2;
   const int i0 = g < h.ma_ngrp ? h.ma_gptr[g] : 0, i1 = g < h.ma_ngrp ? h.ma_gptr[g + 1] : 0;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  // this warp's 4 rows accumulate in T[4 warp + j][lane] (shared memory, conflict-free):
+  // one load-FMA-store per item and no per-item branch on its target row; every row
+  // adds its items in list order (the same order as with register accumulators)
+  double *tw = &T[4 * warp][lane];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) tw[33 * j] = 0.0;
   for (int base = i0; base < i1; base += 32) {
     const int n = min(32, i1 - base);
     int code = 0;
@@ -2340,19 +2345,17 @@ __global__ void __launch_bounds__(kThreads) k_muladd(SegParams h) {
         const int cd = __shfl_sync(0xffffffffu, code, (k0 + k) & 31);
         const double v = __shfl_sync(0xffffffffu, coef, (k0 + k) & 31);
         if (k0 + k >= n) break;
-        const int j = (unsigned)cd >> 30;
-        if (j == 0) acc[0] = fma(v, x[k], acc[0]);
-        else if (j == 1) acc[1] = fma(v, x[k], acc[1]);
-        else if (j == 2) acc[2] = fma(v, x[k], acc[2]);
-        else acc[3] = fma(v, x[k], acc[3]);
+        double *t = tw + 33 * ((unsigned)cd >> 30);
+        *t = fma(v, x[k], *t);
       }
     }
   }
+  if (!h.transposed) {
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int cp = rb + j;
-    if (!h.transposed && cp < h.n_p && col < h.N) h.HW[hw_index(h, cp, col)] = acc[j];
-    T[4 * warp + j][lane] = acc[j];
+    for (int j = 0; j < 4; ++j) {
+      const int cp = rb + j;
+      if (cp < h.n_p && col < h.N) h.HW[hw_index(h, cp, col)] = tw[33 * j];
+    }
   }
   if (!h.transposed) return;
   __syncthreads();
