@@ -562,34 +562,49 @@ __global__ void __launch_bounds__(kThreads) k_fact_sep_rows(FactParams f) {
   __syncwarp();
   const int4 *gks = reinterpret_cast<const int4 *>(f.ks4);
   const int k0 = f.ks_ptr[q], k1 = f.ks_ptr[q + 1];
-  // step ks's (meta, 1 / pivot, first 32 U values and target offsets) in registers
-  int4 m = make_int4(0, 0, 0, 0);
-  double dk = 0.0, u0 = 0.0;
-  int t0 = 0;
-  auto fetch = [&](int ks, int4 &mm, double &dd, double &uu, int &tt) {
-    mm = gks[ks];
-    dd = f.dinv[f.ks_k[ks]];
-    if (lane < mm.z) {
-      uu = f.F_val[mm.y + 1 + lane];
-      tt = f.tgt16[mm.w + lane];
+  // r02: the k-steps of a chunk of 32 are loaded lane-parallel up front (meta and
+  // 1 / pivot: lane s holds step s), and each step's first 32 U values and target
+  // offsets are prefetched kPfD steps ahead in a register ring; with one step of
+  // prefetch every step waited for a fresh L2 round trip (the row's steps are a
+  // serial chain: 59 on case9241's longest separator row)
+  constexpr int kPfD = 8;
+  for (int c0 = k0; c0 < k1; c0 += 32) {
+    const int nc = min(32, k1 - c0);
+    const int4 mv = lane < nc ? gks[c0 + lane] : make_int4(0, 0, 0, 0);
+    const double dv = lane < nc ? f.dinv[f.ks_k[c0 + lane]] : 0.0;
+    double ur[kPfD];
+    int tr[kPfD];
+    auto pf = [&](int st, double &uu, int &tt) {   // U values / targets of chunk step st
+      const int mz = __shfl_sync(0xffffffffu, mv.z, st), my = __shfl_sync(0xffffffffu, mv.y, st);
+      const int mw = __shfl_sync(0xffffffffu, mv.w, st);
+      uu = 0.0;
+      tt = 0;
+      if (st < nc && lane < mz) {
+        uu = f.F_val[my + 1 + lane];
+        tt = f.tgt16[mw + lane];
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < kPfD; ++j) pf(j, ur[j], tr[j]);
+    for (int s0 = 0; s0 < nc; s0 += kPfD) {
+#pragma unroll
+      for (int j = 0; j < kPfD; ++j) {
+        const int st = s0 + j;
+        if (st >= nc) break;
+        const int mx = __shfl_sync(0xffffffffu, mv.x, st), my = __shfl_sync(0xffffffffu, mv.y, st);
+        const int mz = __shfl_sync(0xffffffffu, mv.z, st), mw = __shfl_sync(0xffffffffu, mv.w, st);
+        const double dk = __shfl_sync(0xffffffffu, dv, st);
+        const double u0 = ur[j];
+        const int t0 = tr[j];
+        pf(st + kPfD, ur[j], tr[j]);   // refill this slot for step st + kPfD
+        const double lik = ws[mx] * dk;
+        __syncwarp();
+        if (lane == 0) ws[mx] = lik;
+        if (lane < mz) ws[t0] -= lik * u0;
+        for (int t = 32 + lane; t < mz; t += 32) ws[f.tgt16[mw + t]] -= lik * f.F_val[my + 1 + t];
+        __syncwarp();
+      }
     }
-  };
-  if (k0 < k1) fetch(k0, m, dk, u0, t0);
-  for (int ks = k0; ks < k1; ++ks) {
-    int4 mn = m;
-    double dn = 0.0, un = 0.0;
-    int tn = 0;
-    if (ks + 1 < k1) fetch(ks + 1, mn, dn, un, tn);
-    const double lik = ws[m.x] * dk;
-    __syncwarp();
-    if (lane == 0) ws[m.x] = lik;
-    if (lane < m.z) ws[t0] -= lik * u0;
-    for (int t = 32 + lane; t < m.z; t += 32) ws[f.tgt16[m.w + t]] -= lik * f.F_val[m.y + 1 + t];
-    __syncwarp();
-    m = mn;
-    dk = dn;
-    u0 = un;
-    t0 = tn;
   }
   for (int e = lane; e < len; e += 32) f.F_val[rb + e] = ws[e];
 }
