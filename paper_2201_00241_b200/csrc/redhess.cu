@@ -30,6 +30,15 @@ using namespace rh;
 // ============================================================================
 
 
+__device__ __forceinline__ int ld_acquire_cta_shared(const int *p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_shared(int *p, int v) {
+  asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ double warp_max(double v) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
@@ -455,12 +464,14 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     __shared__ double s_amax[kMaxTopsFact];
     __shared__ int s_topq[kMaxTopsFact];    // block-local row of every tops row
     __shared__ int4 s_trow[kMaxTopsFact];   // per tops row: F row (global), smem row offset, pivot offset, k-steps end
-    __shared__ unsigned char s_tflag[kMaxRowsFact];   // tops membership by block-local row
+    __shared__ unsigned char s_tflag[kMaxRowsFact];   // tops index + 1 by block-local row (0: not a tops row)
+    __shared__ int s_tdone[kMaxTopsFact];              // T2: tops row final (dataflow flag)
     for (int a = threadIdx.x; a < nr; a += blockDim.x) s_tflag[a] = 0;
     __syncthreads();
     for (int t = threadIdx.x; t < ntq; t += blockDim.x) {
       s_topq[t] = s_ord[tq0 + t];
-      s_tflag[s_topq[t]] = 1;
+      s_tflag[s_topq[t]] = (unsigned char)(t + 1);
+      s_tdone[t] = 0;
     }
     __syncthreads();
     auto is_top = [&](int kloc) { return s_tflag[kloc] != 0; };
@@ -499,31 +510,31 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     }
     __syncthreads();
     if (prof) prof[3] = clock64();
-    for (int tk = 0; tk < ntq; ++tk) {   // T2
-      const int ak = s_topq[tk];
-      const int4 rk = s_trow[tk];
-      const int ik = rk.x;
-      const double piv = SF[rk.z];
-      const double dk = fast_rcp(piv);
-      if (tk % nw == warp && lane == 0) {
-        sdinv[ak] = dk;
-        f.dinv[ik] = dk;
-        if (!(fabs(piv) > f.pivtol * s_amax[tk])) atomicMax(f.status, ik + 1);
-        f.rowmax[ik] = s_amax[tk];
-      }
-      for (int t = tk + 1 + ((warp - (tk + 1) % nw + nw) % nw); t < ntq; t += nw) {
-        // t == tk + 1 + warp (mod nw): rows i > k spread over the warps
-        const int4 rt = s_trow[t];
-        const int k1 = rt.w;
-        int ks = s_cur[t];
-        if (ks < k1 && skk[ks] == ak) {
-          kstep(SF + rt.y, ks, dk);
-          for (++ks; ks < k1 && !is_top(skk[ks]); ++ks) {
-          }
-          if (lane == 0) s_cur[t] = ks;
+    // T2, up-looking with dataflow flags (r02; right-looking with one CTA barrier per
+    // tops row before): warp w takes tops rows t = w, w + nw, ...; row t applies its
+    // k-steps on tops rows k in increasing k, each once row k is final, then forms
+    // its pivot.  Every row receives the same updates in the same order as before.
+    for (int t = warp; t < ntq; t += nw) {
+      const int4 rt = s_trow[t];
+      double *w = SF + rt.y;
+      for (int ks = s_cur[t]; ks < rt.w; ++ks) {
+        const int kt = (int)s_tflag[skk[ks]] - 1;   // tops index of k (-1: a piece row, applied in T1)
+        if (kt < 0) continue;
+        while (ld_acquire_cta_shared(s_tdone + kt) == 0) {
         }
+        kstep(w, ks, sdinv[skk[ks]]);
       }
-      __syncthreads();
+      const double piv = SF[rt.z];
+      const double dk = fast_rcp(piv);
+      if (lane == 0) {
+        sdinv[s_topq[t]] = dk;
+        f.dinv[rt.x] = dk;
+        if (!(fabs(piv) > f.pivtol * s_amax[t])) atomicMax(f.status, rt.x + 1);
+        f.rowmax[rt.x] = s_amax[t];
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) st_release_cta_shared(s_tdone + t, 1);
     }
   }
   __syncthreads();
