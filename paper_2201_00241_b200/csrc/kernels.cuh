@@ -148,6 +148,7 @@ struct FactParams {
   double pivtol;
   int sep_maxlen;                    // R_B1: longest separator row of F (shared-memory staging)
   long long *dbg;                    // timing experiment (RH_DEBUG & 128): per-block phase stamps, else null
+  int df;                            // R_A: one dataflow pass over the block's rows (else pieces + tops phases)
 };
 
 }  // namespace rh

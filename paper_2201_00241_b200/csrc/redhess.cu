@@ -450,6 +450,50 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
     }
     __syncwarp();
   };
+  if (f.df) {
+    // r02 (late): every row of the block in one dataflow pass - warp w takes rows
+    // w, w + nw, ... in elimination order (pieces and tops alike) and applies its
+    // k-steps in increasing k, each once row k is final (per-row done flags in shared
+    // memory, acquire/release at CTA scope).  The static subtree-to-warp schedule left
+    // the warps unbalanced (max 106k vs mean 71k cycles) and needed the two tops phases.
+    __shared__ int s_rdone[kMaxRowsFact];
+    for (int a = threadIdx.x; a < nr; a += blockDim.x) s_rdone[a] = 0;
+    __syncthreads();
+    for (int a = warp; a < nr; a += nw) {
+      const int4 rm = s_rm[a];
+      const int2 rd = s_rd[a];
+      double *w = SF + rm.x;
+      double amax = 0.0;
+      for (int t = lane; t < rm.y; t += 32) amax = fmax(amax, fabs(w[t]));
+      amax = warp_max(amax);
+      for (int ks = rm.z; ks < rm.w; ++ks) {
+        const int4 m = sks[ks];
+        const int kl = skk[ks];
+        const int tgl = lane < m.z ? stg[m.w + lane] : 0;
+        while (ld_acquire_cta_shared(s_rdone + kl) == 0) {
+        }
+        const double dk = sdinv[kl];
+        const double ukl = lane < m.z ? SF[m.y + 1 + lane] : 0.0;
+        const double lik = w[m.x] * dk;
+        __syncwarp();
+        if (lane == 0) w[m.x] = lik;
+        if (lane < m.z) w[tgl] -= lik * ukl;
+        for (int t = lane + 32; t < m.z; t += 32) w[stg[m.w + t]] -= lik * SF[m.y + 1 + t];
+        __syncwarp();
+      }
+      const double piv = w[rd.x];
+      if (lane == 0) {
+        const double di = fast_rcp(piv);
+        sdinv[a] = di;
+        f.dinv[rd.y] = di;
+        if (!(fabs(piv) > f.pivtol * amax)) atomicMax(f.status, rd.y + 1);
+        f.rowmax[rd.y] = amax;
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) st_release_cta_shared(s_rdone + a, 1);
+    }
+  } else {
   for (int q = lv[warp]; q < lv[warp + 1]; ++q) eliminate(q);
   __syncthreads();
   if (prof) prof[2] = clock64();
@@ -536,6 +580,7 @@ __global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
       __syncwarp();
       if (lane == 0) st_release_cta_shared(s_tdone + t, 1);
     }
+  }
   }
   __syncthreads();
   if (prof) prof[4] = clock64();
@@ -4158,6 +4203,7 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   f.rowmax = c->rowmax;
   f.status = c->status;
   f.pivtol = 1e-14;
+  f.df = !getenv("RH_FACT_STATIC");   // (RH_FACT_STATIC: the static pieces + tops phases, experiment)
   static long long *fdbg = nullptr;
   const bool fprof = getenv("RH_DEBUG") && (atoi(getenv("RH_DEBUG")) & 128);
   if (fprof) {
