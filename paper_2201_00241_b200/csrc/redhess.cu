@@ -356,7 +356,7 @@ __host__ __device__ inline size_t fact_meta_offset(int fo_end, int nr, int nks, 
   return d_end + (size_t)nks * 20 + (size_t)ntg * 2;
 }
 constexpr int kMaxRowsFact = 1024; // rows of a block (Rmax <= this)
-__global__ void __launch_bounds__(kSegThreads, 1) k_fact_blocks(FactParams f) {
+__global__ void __launch_bounds__(2 * kSegThreads, 1) k_fact_blocks(FactParams f) {
   extern __shared__ double sm[];
   const int s = blockIdx.x;
   const int r0 = f.seg_row_off[s], nr = f.seg_row_off[s + 1] - r0;
@@ -4211,7 +4211,10 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
     f.dbg = fdbg;
   }
   dbg_mark(st, "assembled");
-  k_fact_blocks<<<A.nblk, kSegThreads, c->smem_fact_blk, st>>>(f);
+  // dataflow pass: 32 warps (any count works); the static schedule needs its 16
+  int fthreads = f.df ? 2 * kSegThreads : kSegThreads;
+  if (const char *env = getenv("RH_FACT_THREADS")) fthreads = f.df ? atoi(env) : kSegThreads;   // experiment
+  k_fact_blocks<<<A.nblk, fthreads, c->smem_fact_blk, st>>>(f);
   RH_LAUNCHED(c);
   dbg_mark(st, "k_fact_blocks");
   if (fprof) {  // timing experiment: per-block phase stamps (tools/fact_prof.py)
