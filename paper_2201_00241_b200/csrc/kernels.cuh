@@ -147,6 +147,7 @@ struct FactParams {
   int *status;
   double pivtol;
   int sep_maxlen;                    // R_B1: longest separator row of F (shared-memory staging)
+  int sep_maxu;                      // R_B1: most U entries one separator row's k-steps read
   long long *dbg;                    // timing experiment (RH_DEBUG & 128): per-block phase stamps, else null
   int df;                            // R_A: one dataflow pass over the block's rows (else pieces + tops phases)
 };

@@ -598,15 +598,44 @@ __global__ void __launch_bounds__(2 * kSegThreads, 1) k_fact_blocks(FactParams f
 // step's U row values and target offsets (<= 32 of them: one per lane) are
 // loaded one step ahead, so only the shared-memory multiplier stays on the
 // chain (r02: the row lived in global memory, one L2 round trip per step).
+// per-warp staging of k_fact_sep_rows: the row, its k-steps' U values, their targets (uint16)
+__host__ __device__ inline size_t sep_warp_doubles(int maxlen, int maxu) {
+  return (size_t)maxlen + (size_t)maxu + ((size_t)maxu + 3) / 4;
+}
 __global__ void __launch_bounds__(kThreads) k_fact_sep_rows(FactParams f) {
-  extern __shared__ double fsr[];   // [kThreads / 32][sep_maxlen]
+  extern __shared__ double fsr[];   // per warp: [sep_maxlen] row, [sep_maxu] U values, [sep_maxu] targets
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (a >= f.ns) return;
   const int q = f.seg_row_off[f.nblk] + a;
   const int i = f.row_global[q];
   const int rb = f.F_rowptr[i], re = f.F_rowptr[i + 1], len = re - rb;
-  double *ws = fsr + (size_t)wl * f.sep_maxlen;
+  double *ws = fsr + (size_t)wl * sep_warp_doubles(f.sep_maxlen, f.sep_maxu);
+  double *uv = ws + f.sep_maxlen;
+  unsigned short *tg = reinterpret_cast<unsigned short *>(uv + f.sep_maxu);
+  const int4 *gks = reinterpret_cast<const int4 *>(f.ks4);
+  const int k0 = f.ks_ptr[q], k1 = f.ks_ptr[q + 1];
+  // r02 (late): everything the row's k-steps read is staged before the chain starts -
+  // the row, every step's U values (cp.async, all in flight; a step's values sit at its
+  // target offset, the row's targets being contiguous) and the targets - so the chain of
+  // up to 59 steps runs from shared memory (a register prefetch ring still waited on L2)
+  const int tb = k0 < k1 ? gks[k0].w : 0;
+  for (int c0 = k0; c0 < k1; c0 += 32) {
+    const int nc = min(32, k1 - c0);
+    const int4 mv = lane < nc ? gks[c0 + lane] : make_int4(0, 0, 0, 0);
+    for (int st = 0; st < nc; ++st) {
+      const int my = __shfl_sync(0xffffffffu, mv.y, st), mz = __shfl_sync(0xffffffffu, mv.z, st);
+      const int mw = __shfl_sync(0xffffffffu, mv.w, st);
+      for (int j = lane; j < mz; j += 32) {
+        const unsigned d = (unsigned)__cvta_generic_to_shared(uv + (mw - tb) + j);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(f.F_val + my + 1 + j) : "memory");
+      }
+    }
+  }
+  if (k1 > k0) {
+    const int4 ml = gks[k1 - 1];
+    for (int e = lane; e < ml.w + ml.z - tb; e += 32) tg[e] = f.tgt16[tb + e];
+  }
   double amax = 0.0;
   for (int e = lane; e < len; e += 32) {
     const double v = f.F_val[rb + e];
@@ -615,51 +644,21 @@ __global__ void __launch_bounds__(kThreads) k_fact_sep_rows(FactParams f) {
   }
   amax = warp_max(amax);
   if (lane == 0) f.rowmax[i] = amax;
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncwarp();
-  const int4 *gks = reinterpret_cast<const int4 *>(f.ks4);
-  const int k0 = f.ks_ptr[q], k1 = f.ks_ptr[q + 1];
-  // r02: the k-steps of a chunk of 32 are loaded lane-parallel up front (meta and
-  // 1 / pivot: lane s holds step s), and each step's first 32 U values and target
-  // offsets are prefetched kPfD steps ahead in a register ring; with one step of
-  // prefetch every step waited for a fresh L2 round trip (the row's steps are a
-  // serial chain: 59 on case9241's longest separator row)
-  constexpr int kPfD = 8;
   for (int c0 = k0; c0 < k1; c0 += 32) {
     const int nc = min(32, k1 - c0);
     const int4 mv = lane < nc ? gks[c0 + lane] : make_int4(0, 0, 0, 0);
     const double dv = lane < nc ? f.dinv[f.ks_k[c0 + lane]] : 0.0;
-    double ur[kPfD];
-    int tr[kPfD];
-    auto pf = [&](int st, double &uu, int &tt) {   // U values / targets of chunk step st
-      const int mz = __shfl_sync(0xffffffffu, mv.z, st), my = __shfl_sync(0xffffffffu, mv.y, st);
-      const int mw = __shfl_sync(0xffffffffu, mv.w, st);
-      uu = 0.0;
-      tt = 0;
-      if (st < nc && lane < mz) {
-        uu = f.F_val[my + 1 + lane];
-        tt = f.tgt16[mw + lane];
-      }
-    };
-#pragma unroll
-    for (int j = 0; j < kPfD; ++j) pf(j, ur[j], tr[j]);
-    for (int s0 = 0; s0 < nc; s0 += kPfD) {
-#pragma unroll
-      for (int j = 0; j < kPfD; ++j) {
-        const int st = s0 + j;
-        if (st >= nc) break;
-        const int mx = __shfl_sync(0xffffffffu, mv.x, st), my = __shfl_sync(0xffffffffu, mv.y, st);
-        const int mz = __shfl_sync(0xffffffffu, mv.z, st), mw = __shfl_sync(0xffffffffu, mv.w, st);
-        const double dk = __shfl_sync(0xffffffffu, dv, st);
-        const double u0 = ur[j];
-        const int t0 = tr[j];
-        pf(st + kPfD, ur[j], tr[j]);   // refill this slot for step st + kPfD
-        const double lik = ws[mx] * dk;
-        __syncwarp();
-        if (lane == 0) ws[mx] = lik;
-        if (lane < mz) ws[t0] -= lik * u0;
-        for (int t = 32 + lane; t < mz; t += 32) ws[f.tgt16[mw + t]] -= lik * f.F_val[my + 1 + t];
-        __syncwarp();
-      }
+    for (int st = 0; st < nc; ++st) {
+      const int mx = __shfl_sync(0xffffffffu, mv.x, st), mz = __shfl_sync(0xffffffffu, mv.z, st);
+      const int mo = __shfl_sync(0xffffffffu, mv.w, st) - tb;
+      const double dk = __shfl_sync(0xffffffffu, dv, st);
+      const double lik = ws[mx] * dk;
+      __syncwarp();
+      if (lane == 0) ws[mx] = lik;
+      for (int j = lane; j < mz; j += 32) ws[tg[mo + j]] -= lik * uv[mo + j];
+      __syncwarp();
     }
   }
   for (int e = lane; e < len; e += 32) f.F_val[rb + e] = ws[e];
@@ -2707,6 +2706,7 @@ struct rh_ctx {
   bool early_gathered = false;   // the fused call's early batches also formed their separator rhs
   double *grad_tsep = nullptr;
   int sep_maxlen = 1;                          // longest separator row of F (k_fact_sep_rows staging)
+  int sep_maxu = 1;                            // most U entries of one separator row's k-steps (staged too)
   // epilogue partial runs of k_blk (analysis.hpp RunRecs): U^T -> separator
   // right-hand sides (sr), L^T -> G_p^T Psi of SpMulAdd (ma)
   struct DRunRecs {
@@ -3307,7 +3307,13 @@ int upload(rh_ctx *c) {
       ml = std::max(ml, A.F_rowptr[r + 1] - A.F_rowptr[r]);
     }
     c->sep_maxlen = ml;
-    const size_t sm = sizeof(double) * (kThreads / 32) * ml;
+    int mu = 1;   // the most U entries a separator row's k-steps read (their targets are contiguous)
+    for (int q = A.seg_row_off[A.nblk]; q < A.seg_row_off[A.nblk + 1]; ++q) {
+      const int k0 = A.ks_ptr[q], k1 = A.ks_ptr[q + 1];
+      if (k1 > k0) mu = std::max(mu, A.ks4[4 * (k1 - 1) + 3] + A.ks4[4 * (k1 - 1) + 2] - A.ks4[4 * k0 + 3]);
+    }
+    c->sep_maxu = mu;
+    const size_t sm = sizeof(double) * (kThreads / 32) * sep_warp_doubles(ml, mu);
     if (sm > 48 * 1024 && e == cudaSuccess)
       e = cudaFuncSetAttribute(k_fact_sep_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   }
@@ -4283,7 +4289,9 @@ int state_impl(rh_ctx *c, const double *x, const double *p, cudaStream_t st, cud
   if (A.sep_rows > 0) {
     dbg_mark(st, "side stream forked");
     f.sep_maxlen = c->sep_maxlen;
-    k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads, sizeof(double) * (kThreads / 32) * f.sep_maxlen, st>>>(f);
+    f.sep_maxu = c->sep_maxu;
+    k_fact_sep_rows<<<nblk((long long)A.sep_rows * 32), kThreads,
+                      sizeof(double) * (kThreads / 32) * sep_warp_doubles(f.sep_maxlen, f.sep_maxu), st>>>(f);
     RH_LAUNCHED(c);
     {  // separator rows' entries of the forward pattern (k_sep_gather): L and U^T values
        // (final after R_B1; the Gauss-Jordan inverse below does not touch F)
